@@ -1,0 +1,126 @@
+/*
+ * trajseek.h — C-ABI of libtrajseek.so, the B200 (sm_100a) engine behind the
+ * distance-threshold search path of arXiv 1405.7461 (GPUTrajDistSearch).
+ *
+ * The reference (`trajseek`, pure Python + numpy) has no native boundary;
+ * each entry point below replaces one reference Python function on the hot
+ * path (paths relative to /root/reference/pkg/src/trajseek/):
+ *
+ *   tsk_db_create / tsk_db_free   SegmentStore residency (core.py:121-243);
+ *                                 the device SoA + hoisted per-segment invariants
+ *   tsk_sort_by_start             SegmentStore stable sort (core.py:162-166)
+ *   tsk_index_build / _copy       build_index (index.py:85-146)            [K2]
+ *   tsk_candidate_ranges          candidate_range (index.py:149-173)       [K3]
+ *   tsk_search                    run_search (engine.py:151-204) and
+ *                                 execute_batch (engine.py:97-148)        [K1+K4]
+ *   tsk_pair_intervals            pair_intervals (core.py:464-565)          [K1]
+ *
+ * Conventions: plain pointers and sizes only; host arrays are owned by the
+ * caller (numpy); every function returns TSK_OK or an error code and the
+ * thread-local message is available from tsk_last_error().  A handle is
+ * thread-compatible (one host thread at a time per handle).
+ */
+#ifndef TRAJSEEK_H
+#define TRAJSEEK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSK_ABI_VERSION 1
+
+enum {
+    TSK_OK = 0,
+    TSK_EINVAL = 1,  /* precondition violated → DomainError (core.py:25-26) */
+    TSK_ECUDA = 2,   /* CUDA runtime failure → RuntimeError              */
+    TSK_ENOMEM = 3,  /* allocation failure → MemoryError                 */
+    TSK_ENODEV = 4   /* no CUDA device                                   */
+};
+
+/* tsk_search flags */
+enum {
+    TSK_NOOP = 1u << 0,          /* launch with pair arithmetic elided (engine.py:86-88,207-224) */
+    TSK_ORDER_REFERENCE = 1u << 1,/* items in the reference order: (batch, entry, query)          */
+    TSK_ORDER_QUERY_MAJOR = 1u << 2,/* items ordered (query, entry) as brute_force (oracle.py:26) */
+    TSK_SPANS_GIVEN = 1u << 3,   /* b_first/b_last supplied by the caller (execute_batch)        */
+    TSK_WANT_ORDINALS = 1u << 4, /* also return query/entry ordinals (pair_intervals)            */
+    TSK_QUERIES_RESIDENT = 1u << 5,/* reuse the query set uploaded by the previous call on this db */
+    TSK_RESULTS_ON_DEVICE = 1u << 6 /* leave hit columns in HBM (no D2H): device-throughput runs */
+};
+
+/* Index extent rules (index.py:26) */
+enum { TSK_EXTENT_MEMBER = 0, TSK_EXTENT_GRID = 1 };
+
+/* One segment store in SoA form: 2 int64 id columns + 8 float64 columns,
+ * sorted by non-decreasing ts (SegmentStore, core.py:121-166). */
+typedef struct tsk_columns {
+    int64_t n;
+    const int64_t *traj, *seg;
+    const double *xs, *ys, *zs, *ts, *xe, *ye, *ze, *te;
+} tsk_columns;
+
+typedef struct tsk_db tsk_db;         /* device-resident entry store (+ index) */
+typedef struct tsk_result tsk_result; /* search output (pinned host columns)   */
+
+int tsk_abi_version(void);
+int tsk_device_count(void);
+const char *tsk_last_error(void);
+
+/* Upload a sorted store to `device` and hoist per-segment invariants. */
+int tsk_db_create(int device, const tsk_columns *cols, tsk_db **out);
+void tsk_db_free(tsk_db *db);
+int64_t tsk_db_size(const tsk_db *db);
+
+/* Stable device sort of n start times: perm[i] = input row of sorted row i
+ * (numpy argsort kind="stable", core.py:163). */
+int tsk_sort_by_start(int device, int64_t n, const double *ts, int64_t *perm);
+
+/* [K2] Build the m-bin temporal index on the device (index.py:85-146).
+ * hdr receives {bin_width, t0, t_max}; *n_nonempty the non-empty bin count.
+ * The index stays on the db handle and serves tsk_candidate_ranges/tsk_search. */
+int tsk_index_build(tsk_db *db, int64_t m, int extent_rule, int64_t *n_nonempty, double *hdr);
+/* Copy the non-empty-bin arrays (each n_nonempty long); bin_id = bin number j. */
+int tsk_index_copy(const tsk_db *db, double *ne_start, double *ne_end, int64_t *ne_first,
+                   int64_t *ne_last, int64_t *bin_id);
+
+/* [K3] Candidate ranges of k closed intervals; (-1,-1) where none qualifies. */
+int tsk_candidate_ranges(tsk_db *db, int64_t k, const double *begin, const double *end,
+                         int64_t *first, int64_t *last);
+
+/* [K1+K3+K4] Evaluate a batch plan.  Batch b holds query ordinals
+ * b_lo[b]..b_hi[b] (contiguous, ascending).  Without TSK_SPANS_GIVEN the
+ * candidate span of each batch comes from the db's index (K3, engine.py:177-179);
+ * with it, b_first/b_last supply the spans.  d must be finite and >= 0. */
+int tsk_search(tsk_db *db, const tsk_columns *queries, int64_t nb, const int64_t *b_lo,
+               const int64_t *b_hi, const int64_t *b_first, const int64_t *b_last, double d,
+               uint32_t flags, tsk_result **out);
+
+/* [K1] pair_intervals(rows, cols, d): the rows×cols mesh, row-major hits. */
+int tsk_pair_intervals(int device, const tsk_columns *rows, const tsk_columns *cols, double d,
+                       tsk_result **out);
+
+/* Result accessors.  per_batch (nb × 4 int64): first, last, overlaps, hits
+ * (first = last = -1 for a batch with no candidates).  Column pointers stay
+ * valid until tsk_result_free.  Missing columns come back NULL. */
+int tsk_result_info(const tsk_result *r, int64_t *n_hits, int64_t *nb, double *device_ms);
+/* Device time of the whole call and of the K1 launches (CUDA events), and
+ * the number of kernels this library launched for the call. */
+int tsk_result_timing(const tsk_result *r, double *device_ms, double *k1_ms, int64_t *launches);
+int tsk_result_per_batch(const tsk_result *r, int64_t *per_batch);
+int tsk_result_columns(const tsk_result *r, const int64_t **query_traj, const int64_t **query_seg,
+                       const int64_t **entry_traj, const int64_t **entry_seg,
+                       const double **t_begin, const double **t_end, const int64_t **query_ord,
+                       const int64_t **entry_ord);
+void tsk_result_free(tsk_result *r);
+
+/* Measured FP64 pipe rate of `device` (DADD/DMUL per second, each counted
+ * as one op; DFMA counted as one op too) — the roofline denominator of the
+ * FP64-bound pair kernel. */
+int tsk_probe_fp64(int device, double *dadd_per_s, double *dmul_per_s, double *dfma_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TRAJSEEK_H */

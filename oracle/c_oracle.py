@@ -1,0 +1,103 @@
+"""ctypes loader for the C oracle (oracle/pair_oracle.c) — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's baseline arm use this.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "_build", "liboracle.so")
+_lib = None
+
+_D = ctypes.c_double
+_I64 = ctypes.c_int64
+_PD = ctypes.POINTER(ctypes.c_double)
+_PI64 = ctypes.POINTER(ctypes.c_int64)
+
+
+def build() -> str:
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return _SO
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(
+            os.path.join(_HERE, "pair_oracle.c")
+        ):
+            build()
+        L = ctypes.CDLL(_SO)
+        L.orc_pair.argtypes = [_PD, _PD, _D, _PD, _PD, ctypes.POINTER(ctypes.c_int)]
+        L.orc_pair.restype = ctypes.c_int
+        L.orc_floor_divide.argtypes = [_D, _D]
+        L.orc_floor_divide.restype = _D
+        L.orc_floor_divide_many.argtypes = [_I64, _PD, _D, _PD]
+        L.orc_brute_force.argtypes = [
+            _I64, ctypes.POINTER(_PD), _I64, ctypes.POINTER(_PD), _D, ctypes.c_int,
+            ctypes.POINTER(_PI64), ctypes.POINTER(_PI64), ctypes.POINTER(_PD), ctypes.POINTER(_PD),
+            _PI64, _PI64,
+        ]
+        L.orc_brute_force.restype = _I64
+        L.orc_free.argtypes = [ctypes.c_void_p]
+        _lib = L
+    return _lib
+
+
+_FLOATS = ("xs", "ys", "zs", "ts", "xe", "ye", "ze", "te")
+
+
+def pair(a, b, d):
+    """a, b: 8-tuples (xs ys zs ts xe ye ze te) → (begin, end) or None."""
+    A = (ctypes.c_double * 8)(*a)
+    B = (ctypes.c_double * 8)(*b)
+    bg, en = ctypes.c_double(), ctypes.c_double()
+    tm = ctypes.c_int()
+    if lib().orc_pair(A, B, d, ctypes.byref(bg), ctypes.byref(en), ctypes.byref(tm)):
+        return bg.value, en.value
+    return None
+
+
+def floor_divide(a: np.ndarray, b: float) -> np.ndarray:
+    a = np.ascontiguousarray(a, np.float64)
+    out = np.empty_like(a)
+    lib().orc_floor_divide_many(a.shape[0], a.ctypes.data_as(_PD), b, out.ctypes.data_as(_PD))
+    return out
+
+
+def _colptrs(store):
+    cols = [np.ascontiguousarray(store[k], np.float64) for k in _FLOATS]
+    arr = (_PD * 8)(*[c.ctypes.data_as(_PD) for c in cols])
+    return arr, cols
+
+
+def brute_force(store, queries, d, threads=None):
+    """Query-major brute force over dict stores → result dict like oracle.brute_force."""
+    threads = threads or max(1, os.cpu_count() or 1)
+    ep, keep_e = _colptrs(store)
+    qp, keep_q = _colptrs(queries)
+    qo, eo = _PI64(), _PI64()
+    tb, te = _PD(), _PD()
+    tm, sm = _I64(), _I64()
+    ne = store["ts"].shape[0]
+    nq = queries["ts"].shape[0]
+    n = lib().orc_brute_force(ne, ep, nq, qp, d, threads, ctypes.byref(qo), ctypes.byref(eo),
+                              ctypes.byref(tb), ctypes.byref(te), ctypes.byref(tm), ctypes.byref(sm))
+    q_ord = np.ctypeslib.as_array(qo, (n,)).copy() if n else np.empty(0, np.int64)
+    e_ord = np.ctypeslib.as_array(eo, (n,)).copy() if n else np.empty(0, np.int64)
+    t_b = np.ctypeslib.as_array(tb, (n,)).copy() if n else np.empty(0)
+    t_e = np.ctypeslib.as_array(te, (n,)).copy() if n else np.empty(0)
+    for p in (qo, eo, tb, te):
+        lib().orc_free(ctypes.cast(p, ctypes.c_void_p))
+    del keep_e, keep_q
+    return {
+        "query_traj": queries["traj"][q_ord], "query_seg": queries["seg"][q_ord],
+        "entry_traj": store["traj"][e_ord], "entry_seg": store["seg"][e_ord],
+        "t_begin": t_b, "t_end": t_e,
+    }, int(tm.value), int(sm.value)

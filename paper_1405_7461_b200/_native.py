@@ -1,0 +1,290 @@
+"""ctypes binding of libtrajseek.so (the C-ABI declared in include/trajseek.h).
+
+The product path has no CPU fallback: if the shared library is missing or
+no CUDA device is visible, device calls raise ``RuntimeError`` loudly.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libtrajseek.so")
+
+TSK_OK, TSK_EINVAL, TSK_ECUDA, TSK_ENOMEM, TSK_ENODEV = 0, 1, 2, 3, 4
+TSK_NOOP = 1 << 0
+TSK_ORDER_REFERENCE = 1 << 1
+TSK_ORDER_QUERY_MAJOR = 1 << 2
+TSK_SPANS_GIVEN = 1 << 3
+TSK_WANT_ORDINALS = 1 << 4
+TSK_QUERIES_RESIDENT = 1 << 5
+TSK_RESULTS_ON_DEVICE = 1 << 6
+TSK_EXTENT_MEMBER, TSK_EXTENT_GRID = 0, 1
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_PI64 = ctypes.POINTER(ctypes.c_int64)
+_PD = ctypes.POINTER(ctypes.c_double)
+
+
+class Columns(ctypes.Structure):
+    """tsk_columns: one sorted store in SoA form."""
+
+    _fields_ = [("n", _I64), ("traj", _P), ("seg", _P)] + [
+        (k, _P) for k in ("xs", "ys", "zs", "ts", "xe", "ye", "ze", "te")
+    ]
+
+
+# Exported symbols and their signatures; tests check the .so exports each one.
+SIGNATURES = {
+    "tsk_abi_version": ([], ctypes.c_int),
+    "tsk_device_count": ([], ctypes.c_int),
+    "tsk_last_error": ([], ctypes.c_char_p),
+    "tsk_db_create": ([ctypes.c_int, ctypes.POINTER(Columns), ctypes.POINTER(_P)], ctypes.c_int),
+    "tsk_db_free": ([_P], None),
+    "tsk_db_size": ([_P], _I64),
+    "tsk_sort_by_start": ([ctypes.c_int, _I64, _PD, _PI64], ctypes.c_int),
+    "tsk_index_build": ([_P, _I64, ctypes.c_int, _PI64, _PD], ctypes.c_int),
+    "tsk_index_copy": ([_P, _PD, _PD, _PI64, _PI64, _PI64], ctypes.c_int),
+    "tsk_candidate_ranges": ([_P, _I64, _PD, _PD, _PI64, _PI64], ctypes.c_int),
+    "tsk_search": ([_P, ctypes.POINTER(Columns), _I64, _PI64, _PI64, _PI64, _PI64,
+                    ctypes.c_double, ctypes.c_uint32, ctypes.POINTER(_P)], ctypes.c_int),
+    "tsk_pair_intervals": ([ctypes.c_int, ctypes.POINTER(Columns), ctypes.POINTER(Columns),
+                            ctypes.c_double, ctypes.POINTER(_P)], ctypes.c_int),
+    "tsk_result_info": ([_P, _PI64, _PI64, _PD], ctypes.c_int),
+    "tsk_result_timing": ([_P, _PD, _PD, _PI64], ctypes.c_int),
+    "tsk_result_per_batch": ([_P, _PI64], ctypes.c_int),
+    "tsk_result_columns": ([_P] + [ctypes.POINTER(_P)] * 8, ctypes.c_int),
+    "tsk_result_free": ([_P], None),
+    "tsk_probe_fp64": ([ctypes.c_int, _PD, _PD, _PD], ctypes.c_int),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load():
+    """Load libtrajseek.so (raises RuntimeError if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(
+                    f"libtrajseek.so not found at {LIB_PATH}; build it with "
+                    "`python -c 'import __graft_entry__ as g; g.build()'`"
+                )
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (args, res) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.argtypes = args
+                fn.restype = res
+            _lib = lib
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc == TSK_OK:
+        return
+    msg = load().tsk_last_error().decode(errors="replace")
+    if rc == TSK_EINVAL:
+        from .core import DomainError
+
+        raise DomainError(msg)
+    if rc == TSK_ENOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(f"libtrajseek error {rc}: {msg}")
+
+
+def device_count() -> int:
+    return int(load().tsk_device_count())
+
+
+_device = int(os.environ.get("TRAJSEEK_DEVICE", "0"))
+
+
+def set_device(ordinal: int) -> None:
+    """Select the CUDA device new device-resident stores are placed on."""
+    global _device
+    _device = int(ordinal)
+
+
+def current_device() -> int:
+    return _device
+
+
+def _ptr(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def columns_of(store) -> tuple[Columns, list]:
+    """tsk_columns view of a SegmentStore (keeps contiguous copies alive)."""
+    keep = []
+
+    def c(a, dt):
+        a = np.ascontiguousarray(a, dtype=dt)
+        keep.append(a)
+        return _ptr(a)
+
+    col = Columns()
+    col.n = len(store)
+    col.traj = c(store.traj, np.int64)
+    col.seg = c(store.seg, np.int64)
+    for k in ("xs", "ys", "zs", "ts", "xe", "ye", "ze", "te"):
+        setattr(col, k, c(getattr(store, k), np.float64))
+    return col, keep
+
+
+class DeviceStore:
+    """Owns a tsk_db handle: a store resident in one GPU's HBM."""
+
+    def __init__(self, store, device: int | None = None):
+        self.device = current_device() if device is None else int(device)
+        lib = load()
+        col, keep = columns_of(store)
+        h = ctypes.c_void_p()
+        check(lib.tsk_db_create(self.device, ctypes.byref(col), ctypes.byref(h)))
+        del keep
+        self.handle = h
+        self.n = len(store)
+        self.index_token = None
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.tsk_db_free(h)
+            self.handle = None
+
+
+class _Owner:
+    """Keeps a tsk_result alive while numpy views of its pinned columns live."""
+
+    def __init__(self, handle):
+        self.handle = handle
+
+    def __del__(self):
+        if self.handle is not None and _lib is not None:
+            _lib.tsk_result_free(self.handle)
+            self.handle = None
+
+
+def _view(owner, ptr, n, dtype):
+    if n == 0 or not ptr:
+        return np.empty(0, dtype=dtype)
+    nbytes = n * np.dtype(dtype).itemsize
+    buf = (ctypes.c_char * nbytes).from_address(ptr)
+    buf._owner = owner  # lifetime: array → buffer → owner → tsk_result
+    arr = np.frombuffer(buf, dtype=dtype)
+    return arr
+
+
+class Result:
+    """Decoded tsk_result: numpy columns (zero-copy over pinned memory)."""
+
+    def __init__(self, handle):
+        lib = load()
+        self._owner = _Owner(handle)
+        n = _I64()
+        nb = _I64()
+        ms = ctypes.c_double()
+        check(lib.tsk_result_info(handle, ctypes.byref(n), ctypes.byref(nb), ctypes.byref(ms)))
+        k1 = ctypes.c_double()
+        nl = _I64()
+        check(lib.tsk_result_timing(handle, ctypes.byref(ms), ctypes.byref(k1), ctypes.byref(nl)))
+        self.n, self.nb = int(n.value), int(nb.value)
+        self.device_ms, self.k1_ms = float(ms.value), float(k1.value)
+        self.launches = int(nl.value)
+        pb = np.empty((self.nb, 4), dtype=np.int64)
+        check(lib.tsk_result_per_batch(handle, pb.ctypes.data_as(_PI64)))
+        self.per_batch = pb  # first, last, overlaps, hits
+        ptrs = [ctypes.c_void_p() for _ in range(8)]
+        check(lib.tsk_result_columns(handle, *[ctypes.byref(p) for p in ptrs]))
+        names = ("query_traj", "query_seg", "entry_traj", "entry_seg", "t_begin", "t_end",
+                 "query_ord", "entry_ord")
+        self.cols = {}
+        for name, p in zip(names, ptrs):
+            dt = np.float64 if name.startswith("t_") else np.int64
+            if not p.value:
+                self.cols[name] = None if self.n else np.empty(0, dtype=dt)
+            else:
+                self.cols[name] = _view(self._owner, p.value, self.n, dt)
+
+
+def search(dev: DeviceStore, queries, lo, hi, first, last, d: float, flags: int) -> Result:
+    lib = load()
+    col, keep = columns_of(queries)
+    lo = np.ascontiguousarray(lo, dtype=np.int64)
+    hi = np.ascontiguousarray(hi, dtype=np.int64)
+    fp = lp = None
+    if first is not None:
+        first = np.ascontiguousarray(first, dtype=np.int64)
+        last = np.ascontiguousarray(last, dtype=np.int64)
+        fp, lp = first.ctypes.data_as(_PI64), last.ctypes.data_as(_PI64)
+    h = ctypes.c_void_p()
+    check(lib.tsk_search(dev.handle, ctypes.byref(col), lo.shape[0], lo.ctypes.data_as(_PI64),
+                         hi.ctypes.data_as(_PI64), fp, lp, float(d), flags, ctypes.byref(h)))
+    del keep
+    return Result(h)
+
+
+def pair_intervals(rows, cols, d: float, device: int | None = None) -> Result:
+    lib = load()
+    rc, rk = columns_of(rows)
+    cc, ck = columns_of(cols)
+    h = ctypes.c_void_p()
+    dev = current_device() if device is None else int(device)
+    check(lib.tsk_pair_intervals(dev, ctypes.byref(rc), ctypes.byref(cc), float(d), ctypes.byref(h)))
+    del rk, ck
+    return Result(h)
+
+
+def sort_by_start(ts: np.ndarray, device: int | None = None) -> np.ndarray:
+    lib = load()
+    ts = np.ascontiguousarray(ts, dtype=np.float64)
+    perm = np.empty(ts.shape[0], dtype=np.int64)
+    dev = current_device() if device is None else int(device)
+    check(lib.tsk_sort_by_start(dev, ts.shape[0], ts.ctypes.data_as(_PD), perm.ctypes.data_as(_PI64)))
+    return perm
+
+
+def index_build(dev: DeviceStore, m: int, rule: int):
+    lib = load()
+    n_ne = _I64()
+    hdr = (ctypes.c_double * 3)()
+    check(lib.tsk_index_build(dev.handle, int(m), int(rule), ctypes.byref(n_ne), hdr))
+    k = int(n_ne.value)
+    ne_start = np.empty(k, np.float64)
+    ne_end = np.empty(k, np.float64)
+    ne_first = np.empty(k, np.int64)
+    ne_last = np.empty(k, np.int64)
+    ne_bin = np.empty(k, np.int64)
+    check(lib.tsk_index_copy(dev.handle, ne_start.ctypes.data_as(_PD), ne_end.ctypes.data_as(_PD),
+                             ne_first.ctypes.data_as(_PI64), ne_last.ctypes.data_as(_PI64),
+                             ne_bin.ctypes.data_as(_PI64)))
+    return (hdr[0], hdr[1], hdr[2]), ne_start, ne_end, ne_first, ne_last, ne_bin
+
+
+def candidate_ranges(dev: DeviceStore, begin: np.ndarray, end: np.ndarray):
+    lib = load()
+    begin = np.ascontiguousarray(begin, np.float64)
+    end = np.ascontiguousarray(end, np.float64)
+    k = begin.shape[0]
+    first = np.empty(k, np.int64)
+    last = np.empty(k, np.int64)
+    check(lib.tsk_candidate_ranges(dev.handle, k, begin.ctypes.data_as(_PD), end.ctypes.data_as(_PD),
+                                   first.ctypes.data_as(_PI64), last.ctypes.data_as(_PI64)))
+    return first, last
+
+
+def probe_fp64(device: int | None = None) -> dict:
+    """Measured FP64 pipe rates (ops/s) of a device (tsk_probe_fp64)."""
+    lib = load()
+    a, m, f = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    dev = current_device() if device is None else int(device)
+    check(lib.tsk_probe_fp64(dev, ctypes.byref(a), ctypes.byref(m), ctypes.byref(f)))
+    return {"dadd_per_s": a.value, "dmul_per_s": m.value, "dfma_per_s": f.value}

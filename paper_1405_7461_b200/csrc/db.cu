@@ -1,0 +1,635 @@
+// db.cu — device-resident segment store, temporal index (K2) and candidate
+// ranges (K3).
+//
+//   SegmentStore residency ........ /root/reference/pkg/src/trajseek/core.py:121-243
+//   stable start-time sort ........ core.py:162-166
+//   build_index ................... index.py:85-146          (K2)
+//   candidate_range ............... index.py:149-173         (K3)
+//   batch extent (range_extent) ... core.py:239-243, engine.py:177-179
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <cstring>
+
+#include "tsk_internal.cuh"
+
+namespace tsk {
+
+void DBuf::reserve(size_t need, cudaStream_t) {
+    if (need <= bytes) return;
+    if (p) TSK_CUDA(cudaFree(p));
+    p = nullptr;
+    bytes = 0;
+    size_t want = need + need / 4 + 256;
+    TSK_CUDA(cudaMalloc(&p, want));
+    bytes = want;
+}
+
+void DBuf::release(cudaStream_t) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+}
+
+// ── SoA storage ────────────────────────────────────────────────────────────
+
+void soa_alloc(Soa &s, int64_t n, bool with_ids, cudaStream_t st) {
+    size_t nn = (size_t)(n > 0 ? n : 1);
+    size_t per = 12 * sizeof(double) + (with_ids ? 2 * sizeof(int64_t) : 0) + 1;
+    s.storage.reserve(nn * per + 64, st);
+    char *base = s.storage.as<char>();
+    double **cols[12] = {&s.ts, &s.te, &s.sx, &s.sy, &s.sz, &s.ex,
+                         &s.ey, &s.ez, &s.dx, &s.dy, &s.dz, &s.rcp};
+    for (int k = 0; k < 12; ++k) {
+        *cols[k] = reinterpret_cast<double *>(base);
+        base += nn * sizeof(double);
+    }
+    if (with_ids) {
+        s.traj = reinterpret_cast<int64_t *>(base);
+        base += nn * sizeof(int64_t);
+        s.seg = reinterpret_cast<int64_t *>(base);
+        base += nn * sizeof(int64_t);
+    } else {
+        s.traj = s.seg = nullptr;
+    }
+    s.unsafe = reinterpret_cast<uint8_t *>(base);
+    s.n = n;
+}
+
+void soa_upload(Soa &s, const tsk_columns *c, cudaStream_t st) {
+    size_t b = (size_t)c->n * sizeof(double);
+    if (c->n == 0) return;
+    const double *src[8] = {c->ts, c->te, c->xs, c->ys, c->zs, c->xe, c->ye, c->ze};
+    double *dst[8] = {s.ts, s.te, s.sx, s.sy, s.sz, s.ex, s.ey, s.ez};
+    for (int k = 0; k < 8; ++k) TSK_CUDA(cudaMemcpyAsync(dst[k], src[k], b, cudaMemcpyHostToDevice, st));
+    if (s.traj) {
+        TSK_CUDA(cudaMemcpyAsync(s.traj, c->traj, (size_t)c->n * 8, cudaMemcpyHostToDevice, st));
+        TSK_CUDA(cudaMemcpyAsync(s.seg, c->seg, (size_t)c->n * 8, cudaMemcpyHostToDevice, st));
+    }
+}
+
+// Exponent window inside which qdiv() is proven exact: all times and
+// extents are 0 or of magnitude in [2^-900, 2^1000], coordinates below
+// 2^1000.  Then every residual of qdiv stays a normal number.
+__device__ __forceinline__ bool mag_bad(double v) {
+    double a = fabs(v);
+    return (a != 0.0 && a < 0x1p-900) || a > 0x1p1000;
+}
+
+__global__ void k_hoist(int64_t n, const double *__restrict__ ts, const double *__restrict__ te,
+                        const double *__restrict__ sx, const double *__restrict__ sy,
+                        const double *__restrict__ sz, const double *__restrict__ ex,
+                        const double *__restrict__ ey, const double *__restrict__ ez,
+                        double *__restrict__ dx, double *__restrict__ dy, double *__restrict__ dz,
+                        double *__restrict__ rcp, uint8_t *__restrict__ unsafe, int *flags) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double t0 = ts[i], t1 = te[i];
+        dx[i] = __dsub_rn(ex[i], sx[i]);
+        dy[i] = __dsub_rn(ey[i], sy[i]);
+        dz[i] = __dsub_rn(ez[i], sz[i]);
+        double ext = __dsub_rn(t1, t0);
+        rcp[i] = ext > 0.0 ? __drcp_rn(ext) : 0.0;
+        bool bad = mag_bad(t0) || mag_bad(t1) || (ext > 0.0 && mag_bad(ext)) ||
+                   fabs(sx[i]) > 0x1p1000 || fabs(sy[i]) > 0x1p1000 || fabs(sz[i]) > 0x1p1000 ||
+                   fabs(ex[i]) > 0x1p1000 || fabs(ey[i]) > 0x1p1000 || fabs(ez[i]) > 0x1p1000;
+        unsafe[i] = bad ? 1 : 0;
+        if (bad) atomicOr(&flags[0], 1);
+        if (i + 1 < n && ts[i + 1] < t0) atomicOr(&flags[1], 1);
+    }
+}
+
+void soa_hoist(Soa &s, cudaStream_t st) {
+    if (s.n == 0) {
+        s.any_unsafe = 0;
+        s.sorted = 1;
+        return;
+    }
+    int *flags;
+    TSK_CUDA(cudaMallocAsync(&flags, 2 * sizeof(int), st));
+    TSK_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), st));
+    int grid = (int)std::min<int64_t>((s.n + 255) / 256, 148 * 16);
+    k_hoist<<<grid, 256, 0, st>>>(s.n, s.ts, s.te, s.sx, s.sy, s.sz, s.ex, s.ey, s.ez, s.dx, s.dy,
+                                  s.dz, s.rcp, s.unsafe, flags);
+    TSK_CUDA(cudaGetLastError());
+    int h[2];
+    TSK_CUDA(cudaMemcpyAsync(h, flags, sizeof(h), cudaMemcpyDeviceToHost, st));
+    TSK_CUDA(cudaFreeAsync(flags, st));
+    TSK_CUDA(cudaStreamSynchronize(st));
+    s.any_unsafe = h[0];
+    s.sorted = h[1] ? 0 : 1;
+}
+
+// ── queries → shared-memory records ────────────────────────────────────────
+
+__global__ void k_qrec(int64_t n, const double *__restrict__ ts, const double *__restrict__ te,
+                       const double *__restrict__ sx, const double *__restrict__ sy,
+                       const double *__restrict__ sz, const double *__restrict__ ex,
+                       const double *__restrict__ ey, const double *__restrict__ ez,
+                       const double *__restrict__ dx, const double *__restrict__ dy,
+                       const double *__restrict__ dz, const double *__restrict__ rcp,
+                       const uint8_t *__restrict__ unsafe, QRec *__restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        QRec r;
+        r.ts = ts[i];
+        r.te = te[i];
+        r.sx = sx[i];
+        r.sy = sy[i];
+        r.sz = sz[i];
+        r.ext = __dsub_rn(r.te, r.ts);
+        r.dx = dx[i];
+        r.dy = dy[i];
+        r.dz = dz[i];
+        r.rcp = rcp[i];
+        r.ex = ex[i];
+        r.ey = ey[i];
+        r.ez = ez[i];
+        r.flag = unsafe[i] ? 1.0 : 0.0;
+        out[i] = r;
+    }
+}
+
+void launch_qrec(const Soa &q, QRec *out, cudaStream_t st) {
+    if (q.n == 0) return;
+    int grid = (int)std::min<int64_t>((q.n + 255) / 256, 148 * 8);
+    k_qrec<<<grid, 256, 0, st>>>(q.n, q.ts, q.te, q.sx, q.sy, q.sz, q.ex, q.ey, q.ez, q.dx, q.dy,
+                                 q.dz, q.rcp, q.unsafe, out);
+    TSK_CUDA(cudaGetLastError());
+}
+
+// ── stable sort by start time ──────────────────────────────────────────────
+
+// Order-preserving map of a double onto uint64 (+0.0 and -0.0 share a key,
+// as they compare equal in numpy's stable argsort).
+__global__ void k_sortkey(int64_t n, const double *__restrict__ ts, uint64_t *__restrict__ key,
+                          int64_t *__restrict__ iota) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double v = ts[i];
+        if (v == 0.0) v = 0.0;
+        uint64_t b = (uint64_t)__double_as_longlong(v);
+        key[i] = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+        iota[i] = i;
+    }
+}
+
+}  // namespace tsk
+
+using namespace tsk;
+
+// ── index build (K2) ───────────────────────────────────────────────────────
+
+namespace tsk {
+
+// bin of ordinal i: min(floor_divide(ts - t0, width), m - 1) (index.py:108-112)
+__device__ __forceinline__ int64_t bin_of(double t, double t0, double width, int64_t m) {
+    if (!(width > 0.0)) return 0;
+    double f = np_floor_divide(__dsub_rn(t, t0), width);
+    double mm = (double)(m - 1);
+    f = f < mm ? f : mm;  // np.minimum(float, m - 1)
+    return (int64_t)f;
+}
+
+// Runs of equal bin id are contiguous because ts is sorted; record the
+// first/last ordinal of each run (the searchsorted pair of index.py:116-118).
+__global__ void k_bin_bounds(int64_t n, const double *__restrict__ ts, double t0, double width,
+                             int64_t m, int64_t *__restrict__ first, int64_t *__restrict__ last) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t b = bin_of(ts[i], t0, width, m);
+        if (i == 0 || bin_of(ts[i - 1], t0, width, m) != b) first[b] = i;
+        if (i == n - 1 || bin_of(ts[i + 1], t0, width, m) != b) last[b] = i;
+    }
+}
+
+__global__ void k_bin_flags(int64_t m, const int64_t *__restrict__ first, int64_t *__restrict__ flag) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m;
+         j += (int64_t)gridDim.x * blockDim.x)
+        flag[j] = first[j] >= 0 ? 1 : 0;
+}
+
+__global__ void k_bin_compact(int64_t m, const int64_t *__restrict__ first,
+                              const int64_t *__restrict__ last, const int64_t *__restrict__ pos,
+                              const double *__restrict__ ts, int rule, double t0, double width,
+                              double *__restrict__ ne_start, int64_t *__restrict__ ne_first,
+                              int64_t *__restrict__ ne_last, int64_t *__restrict__ ne_bin) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        int64_t f = first[j];
+        if (f < 0) continue;
+        int64_t k = pos[j];
+        ne_first[k] = f;
+        ne_last[k] = last[j];
+        ne_bin[k] = j;
+        // member_extents: ts[first]; grid_start: t0 + j * width (index.py:123-126)
+        ne_start[k] = rule == TSK_EXTENT_MEMBER ? ts[f] : __dadd_rn(t0, __dmul_rn((double)j, width));
+    }
+}
+
+// ne_end = max te over the bin's members (maximum.reduceat, index.py:127); one warp per bin.
+__global__ void k_bin_end(int64_t n_ne, const int64_t *__restrict__ ne_first,
+                          const int64_t *__restrict__ ne_last, const double *__restrict__ te,
+                          double *__restrict__ ne_end) {
+    int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t k = warp; k < n_ne; k += nw) {
+        double mx = -INFINITY;
+        for (int64_t i = ne_first[k] + lane; i <= ne_last[k]; i += 32) mx = fmax(mx, te[i]);
+        for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane == 0) ne_end[k] = mx;
+    }
+}
+
+struct MaxOp {
+    __device__ __forceinline__ double operator()(double a, double b) const { return a > b ? a : b; }
+};
+
+// ── candidate ranges (K3) ──────────────────────────────────────────────────
+
+// For [begin, end]: hi = searchsorted(ne_start, end, "right"); the lowest
+// reaching bin is the first k < hi whose running max of ne_end reaches
+// begin; the highest is found by a backward warp scan (index.py:160-173).
+__device__ void range_lookup(double begin, double end, int64_t n_ne, const double *ne_start,
+                             const double *ne_end, const double *ne_endmax, const int64_t *ne_first,
+                             const int64_t *ne_last, int64_t *out_first, int64_t *out_last) {
+    int lane = threadIdx.x & 31;
+    int64_t lo = 0, hi = n_ne;  // upper_bound on ne_start
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (ne_start[mid] <= end) lo = mid + 1;
+        else hi = mid;
+    }
+    int64_t h = lo;
+    int64_t rf = -1, rl = -1;
+    if (h > 0) {
+        int64_t a = 0, b = h;  // lower_bound on the running max
+        while (a < b) {
+            int64_t mid = (a + b) >> 1;
+            if (ne_endmax[mid] >= begin) b = mid;
+            else a = mid + 1;
+        }
+        int64_t klo = a;
+        if (klo < h) {
+            int64_t khi = -1;
+            for (int64_t base = h - 1; base >= klo && khi < 0; base -= 32) {
+                int64_t k = base - lane;
+                bool reach = k >= klo && ne_end[k] >= begin;
+                unsigned m = __ballot_sync(0xffffffffu, reach);
+                if (m) khi = base - (__ffs(m) - 1);
+            }
+            rf = ne_first[klo];
+            rl = ne_last[khi];
+        }
+    }
+    if (lane == 0) {
+        *out_first = rf;
+        *out_last = rl;
+    }
+}
+
+__global__ void k_ranges_given(int64_t k, const double *__restrict__ begin,
+                               const double *__restrict__ end, Index ix, int64_t *first,
+                               int64_t *last) {
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < k; i += nw)
+        range_lookup(begin[i], end[i], ix.n_ne, ix.ne_start, ix.ne_end, ix.ne_endmax, ix.ne_first,
+                     ix.ne_last, first + i, last + i);
+}
+
+// One warp per batch: extent [ts[lo], max te[lo..hi]] then the range lookup.
+__global__ void k_batch_ranges(int64_t nb, const int64_t *__restrict__ lo, const int64_t *__restrict__ hi,
+                               const double *__restrict__ qts, const double *__restrict__ qte,
+                               Index ix, int64_t *first, int64_t *last) {
+    int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t b = warp; b < nb; b += nw) {
+        double mx = -INFINITY;
+        for (int64_t i = lo[b] + lane; i <= hi[b]; i += 32) mx = fmax(mx, qte[i]);
+        for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (ix.n_ne == 0) {
+            if (lane == 0) first[b] = last[b] = -1;
+            continue;
+        }
+        range_lookup(qts[lo[b]], mx, ix.n_ne, ix.ne_start, ix.ne_end, ix.ne_endmax, ix.ne_first,
+                     ix.ne_last, first + b, last + b);
+    }
+}
+
+void launch_ranges(tsk_db *db, const Soa &q, SearchPlanDev &p, bool spans_given, cudaStream_t st) {
+    if (spans_given || p.nb == 0) return;
+    TSK_REQUIRE(db->ix.built, "run_search needs an index: call build_index first");
+    int grid = (int)std::min<int64_t>((p.nb * 32 + 255) / 256, 148 * 8);
+    k_batch_ranges<<<grid, 256, 0, st>>>(p.nb, p.lo, p.hi, q.ts, q.te, db->ix, p.first, p.last);
+    TSK_CUDA(cudaGetLastError());
+}
+
+// ── work items of a plan ───────────────────────────────────────────────────
+
+// Single block: choose the candidate sub-tile count so the grid gets at
+// least ~4 waves of items, then scan items per batch.
+__global__ void k_plan_items(int64_t nb, const int64_t *__restrict__ lo, const int64_t *__restrict__ hi,
+                             const int64_t *__restrict__ first, const int64_t *__restrict__ last,
+                             int64_t *__restrict__ item_off, int64_t *__restrict__ meta,
+                             int64_t slots) {
+    typedef cub::BlockReduce<long long, 1024> BR;
+    typedef cub::BlockScan<long long, 1024> BS;
+    __shared__ union {
+        typename BR::TempStorage r;
+        typename BS::TempStorage s;
+    } tmp;
+    __shared__ long long carry;
+    __shared__ int sub_sh;
+    long long acc = 0;
+    for (int64_t b = threadIdx.x; b < nb; b += blockDim.x) {
+        long long c = first[b] >= 0 ? last[b] - first[b] + 1 : 0;
+        long long tq = (hi[b] - lo[b] + 1 + K1_TQ - 1) / K1_TQ;
+        acc += ((c + K1_THREADS - 1) / K1_THREADS) * tq;
+    }
+    long long tiles = BR(tmp.r).Sum(acc);
+    if (threadIdx.x == 0) {
+        long long want = 4 * slots;
+        int sub = (int)(tiles / (want > 0 ? want : 1));
+        sub_sh = sub < 1 ? 1 : (sub > K1_MAX_SUB ? K1_MAX_SUB : sub);
+        carry = 0;
+    }
+    __syncthreads();
+    const long long ct = (long long)K1_THREADS * sub_sh;
+    for (int64_t base = 0; base < nb; base += blockDim.x) {
+        int64_t b = base + threadIdx.x;
+        long long v = 0;
+        if (b < nb) {
+            long long c = first[b] >= 0 ? last[b] - first[b] + 1 : 0;
+            long long tq = (hi[b] - lo[b] + 1 + K1_TQ - 1) / K1_TQ;
+            v = ((c + ct - 1) / ct) * tq;
+        }
+        long long ex, agg;
+        BS(tmp.s).ExclusiveSum(v, ex, agg);
+        if (b < nb) item_off[b] = carry + ex;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += agg;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        item_off[nb] = carry;
+        meta[0] = carry;
+        meta[1] = sub_sh;
+    }
+}
+
+void launch_plan_items(SearchPlanDev &p, int slots, cudaStream_t st) {
+    k_plan_items<<<1, 1024, 0, st>>>(p.nb, p.lo, p.hi, p.first, p.last, p.item_off, p.meta, slots);
+    TSK_CUDA(cudaGetLastError());
+}
+
+}  // namespace tsk
+
+// ── C-ABI: db / sort / index / ranges ──────────────────────────────────────
+
+extern "C" int tsk_db_create(int device, const tsk_columns *cols, tsk_db **out) {
+    tsk_db *db = nullptr;
+    try {
+        TSK_REQUIRE(cols && out, "null argument");
+        TSK_REQUIRE(cols->n >= 0, "negative store size");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            throw Error{TSK_ENODEV, "no CUDA device visible"};
+        TSK_REQUIRE(device >= 0 && device < ndev, "device ordinal out of range");
+        TSK_CUDA(cudaSetDevice(device));
+        db = new tsk_db();
+        db->device = device;
+        TSK_CUDA(cudaStreamCreateWithFlags(&db->stream, cudaStreamNonBlocking));
+        TSK_CUDA(cudaEventCreate(&db->ev0));
+        TSK_CUDA(cudaEventCreate(&db->ev1));
+        TSK_CUDA(cudaEventCreate(&db->ev_k0));
+        TSK_CUDA(cudaEventCreate(&db->ev_k1));
+        soa_alloc(db->s, cols->n, true, db->stream);
+        soa_upload(db->s, cols, db->stream);
+        soa_hoist(db->s, db->stream);
+        *out = db;
+        return TSK_OK;
+    } catch (const Error &e) {
+        if (db) tsk_db_free(db);
+        return fail(e.code, e.msg);
+    }
+}
+
+extern "C" void tsk_db_free(tsk_db *db) {
+    if (!db) return;
+    cudaSetDevice(db->device);
+    if (db->stream) cudaStreamSynchronize(db->stream);
+    db->s.storage.release(db->stream);
+    db->ix.storage.release(db->stream);
+    db->q.storage.release(db->stream);
+    for (DBuf *b : {&db->q_rec, &db->batches, &db->counters, &db->recs, &db->sorted, &db->cub_tmp,
+                    &db->out_cols})
+        b->release(db->stream);
+    for (cudaEvent_t ev : {db->ev0, db->ev1, db->ev_k0, db->ev_k1})
+        if (ev) cudaEventDestroy(ev);
+    if (db->stream) cudaStreamDestroy(db->stream);
+    delete db;
+}
+
+extern "C" int64_t tsk_db_size(const tsk_db *db) { return db ? db->s.n : -1; }
+
+extern "C" int tsk_sort_by_start(int device, int64_t n, const double *ts, int64_t *perm) {
+    try {
+        TSK_REQUIRE(n >= 0 && (n == 0 || (ts && perm)), "bad arguments");
+        if (n == 0) return TSK_OK;
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            throw Error{TSK_ENODEV, "no CUDA device visible"};
+        TSK_CUDA(cudaSetDevice(device));
+        cudaStream_t st;
+        TSK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        double *dts;
+        uint64_t *k0, *k1;
+        int64_t *v0, *v1;
+        size_t nb = (size_t)n * 8;
+        TSK_CUDA(cudaMallocAsync(&dts, nb, st));
+        TSK_CUDA(cudaMallocAsync(&k0, nb, st));
+        TSK_CUDA(cudaMallocAsync(&k1, nb, st));
+        TSK_CUDA(cudaMallocAsync(&v0, nb, st));
+        TSK_CUDA(cudaMallocAsync(&v1, nb, st));
+        TSK_CUDA(cudaMemcpyAsync(dts, ts, nb, cudaMemcpyHostToDevice, st));
+        int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+        k_sortkey<<<grid, 256, 0, st>>>(n, dts, k0, v0);
+        TSK_CUDA(cudaGetLastError());
+        size_t tb = 0;
+        TSK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, v0, v1, n, 0, 64, st));
+        void *tmp;
+        TSK_CUDA(cudaMallocAsync(&tmp, tb, st));
+        TSK_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k0, k1, v0, v1, n, 0, 64, st));
+        TSK_CUDA(cudaMemcpyAsync(perm, v1, nb, cudaMemcpyDeviceToHost, st));
+        for (void *p : {(void *)dts, (void *)k0, (void *)k1, (void *)v0, (void *)v1, tmp})
+            TSK_CUDA(cudaFreeAsync(p, st));
+        TSK_CUDA(cudaStreamSynchronize(st));
+        TSK_CUDA(cudaStreamDestroy(st));
+        return TSK_OK;
+    } catch (const Error &e) {
+        return fail(e.code, e.msg);
+    }
+}
+
+extern "C" int tsk_index_build(tsk_db *db, int64_t m, int extent_rule, int64_t *n_nonempty,
+                               double *hdr) {
+    try {
+        TSK_REQUIRE(db, "null db");
+        TSK_REQUIRE(m >= 1, "bin count m must be >= 1");
+        TSK_REQUIRE(extent_rule == TSK_EXTENT_MEMBER || extent_rule == TSK_EXTENT_GRID,
+                    "unknown extent rule");
+        TSK_REQUIRE(db->s.n > 0, "cannot index an empty store");
+        TSK_REQUIRE(db->s.sorted, "store is not sorted by start time");
+        TSK_CUDA(cudaSetDevice(db->device));
+        cudaStream_t st = db->stream;
+        Soa &s = db->s;
+        Index &ix = db->ix;
+        const int64_t n = s.n;
+        // t0 = ts[0] (sorted), t_max = max te (core.py:213-225)
+        double t0, tmax;
+        {
+            double *dmax;
+            TSK_CUDA(cudaMallocAsync(&dmax, sizeof(double), st));
+            size_t tb = 0;
+            TSK_CUDA(cub::DeviceReduce::Max(nullptr, tb, s.te, dmax, n, st));
+            void *tmp;
+            TSK_CUDA(cudaMallocAsync(&tmp, tb, st));
+            TSK_CUDA(cub::DeviceReduce::Max(tmp, tb, s.te, dmax, n, st));
+            TSK_CUDA(cudaMemcpyAsync(&tmax, dmax, sizeof(double), cudaMemcpyDeviceToHost, st));
+            TSK_CUDA(cudaMemcpyAsync(&t0, s.ts, sizeof(double), cudaMemcpyDeviceToHost, st));
+            TSK_CUDA(cudaFreeAsync(tmp, st));
+            TSK_CUDA(cudaFreeAsync(dmax, st));
+            TSK_CUDA(cudaStreamSynchronize(st));
+        }
+        volatile double vm = (double)m;
+        double width = (tmax - t0) / vm;  // index.py:107
+        // scratch: first[m], last[m], flag[m], pos[m]
+        size_t mb = (size_t)m * 8;
+        int64_t *first, *last, *flag, *pos, *dn;
+        TSK_CUDA(cudaMallocAsync(&first, mb, st));
+        TSK_CUDA(cudaMallocAsync(&last, mb, st));
+        TSK_CUDA(cudaMallocAsync(&flag, mb, st));
+        TSK_CUDA(cudaMallocAsync(&pos, mb, st));
+        TSK_CUDA(cudaMallocAsync(&dn, 8, st));
+        TSK_CUDA(cudaMemsetAsync(first, 0xff, mb, st));
+        TSK_CUDA(cudaMemsetAsync(last, 0xff, mb, st));
+        int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+        k_bin_bounds<<<grid, 256, 0, st>>>(n, s.ts, t0, width, m, first, last);
+        int gm = (int)std::min<int64_t>((m + 255) / 256, 148 * 8);
+        k_bin_flags<<<gm, 256, 0, st>>>(m, first, flag);
+        TSK_CUDA(cudaGetLastError());
+        size_t tb = 0;
+        TSK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, flag, pos, m, st));
+        void *tmp;
+        TSK_CUDA(cudaMallocAsync(&tmp, tb, st));
+        TSK_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, flag, pos, m, st));
+        TSK_CUDA(cudaFreeAsync(tmp, st));
+        int64_t h_last_pos, h_last_flag;
+        TSK_CUDA(cudaMemcpyAsync(&h_last_pos, pos + (m - 1), 8, cudaMemcpyDeviceToHost, st));
+        TSK_CUDA(cudaMemcpyAsync(&h_last_flag, flag + (m - 1), 8, cudaMemcpyDeviceToHost, st));
+        TSK_CUDA(cudaStreamSynchronize(st));
+        int64_t n_ne = h_last_pos + h_last_flag;
+        size_t nn = (size_t)(n_ne > 0 ? n_ne : 1);
+        ix.storage.reserve(nn * (3 * 8 + 3 * 8) + 64, st);
+        char *base = ix.storage.as<char>();
+        ix.ne_start = (double *)base; base += nn * 8;
+        ix.ne_end = (double *)base; base += nn * 8;
+        ix.ne_endmax = (double *)base; base += nn * 8;
+        ix.ne_first = (int64_t *)base; base += nn * 8;
+        ix.ne_last = (int64_t *)base; base += nn * 8;
+        ix.ne_bin = (int64_t *)base;
+        k_bin_compact<<<gm, 256, 0, st>>>(m, first, last, pos, s.ts, extent_rule, t0, width,
+                                          ix.ne_start, ix.ne_first, ix.ne_last, ix.ne_bin);
+        TSK_CUDA(cudaGetLastError());
+        if (n_ne > 0) {
+            int gw = (int)std::min<int64_t>((n_ne * 32 + 255) / 256, 148 * 16);
+            k_bin_end<<<gw, 256, 0, st>>>(n_ne, ix.ne_first, ix.ne_last, s.te, ix.ne_end);
+            TSK_CUDA(cudaGetLastError());
+            tb = 0;
+            TSK_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tb, ix.ne_end, ix.ne_endmax, MaxOp(),
+                                                    n_ne, st));
+            TSK_CUDA(cudaMallocAsync(&tmp, tb, st));
+            TSK_CUDA(cub::DeviceScan::InclusiveScan(tmp, tb, ix.ne_end, ix.ne_endmax, MaxOp(), n_ne,
+                                                    st));
+            TSK_CUDA(cudaFreeAsync(tmp, st));
+        }
+        for (void *p : {(void *)first, (void *)last, (void *)flag, (void *)pos, (void *)dn})
+            TSK_CUDA(cudaFreeAsync(p, st));
+        TSK_CUDA(cudaStreamSynchronize(st));
+        ix.m = m;
+        ix.n_ne = n_ne;
+        ix.rule = extent_rule;
+        ix.width = width;
+        ix.t0 = t0;
+        ix.t_max = tmax;
+        ix.built = true;
+        if (n_nonempty) *n_nonempty = n_ne;
+        if (hdr) {
+            hdr[0] = width;
+            hdr[1] = t0;
+            hdr[2] = tmax;
+        }
+        return TSK_OK;
+    } catch (const Error &e) {
+        return fail(e.code, e.msg);
+    }
+}
+
+extern "C" int tsk_index_copy(const tsk_db *db, double *ne_start, double *ne_end, int64_t *ne_first,
+                              int64_t *ne_last, int64_t *bin_id) {
+    try {
+        TSK_REQUIRE(db && db->ix.built, "index not built");
+        TSK_CUDA(cudaSetDevice(db->device));
+        const Index &ix = db->ix;
+        size_t b = (size_t)ix.n_ne * 8;
+        if (b) {
+            if (ne_start) TSK_CUDA(cudaMemcpyAsync(ne_start, ix.ne_start, b, cudaMemcpyDeviceToHost, db->stream));
+            if (ne_end) TSK_CUDA(cudaMemcpyAsync(ne_end, ix.ne_end, b, cudaMemcpyDeviceToHost, db->stream));
+            if (ne_first) TSK_CUDA(cudaMemcpyAsync(ne_first, ix.ne_first, b, cudaMemcpyDeviceToHost, db->stream));
+            if (ne_last) TSK_CUDA(cudaMemcpyAsync(ne_last, ix.ne_last, b, cudaMemcpyDeviceToHost, db->stream));
+            if (bin_id) TSK_CUDA(cudaMemcpyAsync(bin_id, ix.ne_bin, b, cudaMemcpyDeviceToHost, db->stream));
+        }
+        TSK_CUDA(cudaStreamSynchronize(db->stream));
+        return TSK_OK;
+    } catch (const Error &e) {
+        return fail(e.code, e.msg);
+    }
+}
+
+extern "C" int tsk_candidate_ranges(tsk_db *db, int64_t k, const double *begin, const double *end,
+                                    int64_t *first, int64_t *last) {
+    try {
+        TSK_REQUIRE(db && db->ix.built, "index not built");
+        TSK_REQUIRE(k >= 0, "negative count");
+        if (k == 0) return TSK_OK;
+        TSK_CUDA(cudaSetDevice(db->device));
+        cudaStream_t st = db->stream;
+        double *d_b, *d_e;
+        int64_t *d_f, *d_l;
+        size_t b = (size_t)k * 8;
+        TSK_CUDA(cudaMallocAsync(&d_b, b, st));
+        TSK_CUDA(cudaMallocAsync(&d_e, b, st));
+        TSK_CUDA(cudaMallocAsync(&d_f, b, st));
+        TSK_CUDA(cudaMallocAsync(&d_l, b, st));
+        TSK_CUDA(cudaMemcpyAsync(d_b, begin, b, cudaMemcpyHostToDevice, st));
+        TSK_CUDA(cudaMemcpyAsync(d_e, end, b, cudaMemcpyHostToDevice, st));
+        if (db->ix.n_ne == 0) {
+            TSK_CUDA(cudaMemsetAsync(d_f, 0xff, b, st));
+            TSK_CUDA(cudaMemsetAsync(d_l, 0xff, b, st));
+        } else {
+            int grid = (int)std::min<int64_t>((k * 32 + 255) / 256, 148 * 8);
+            k_ranges_given<<<grid, 256, 0, st>>>(k, d_b, d_e, db->ix, d_f, d_l);
+            TSK_CUDA(cudaGetLastError());
+        }
+        TSK_CUDA(cudaMemcpyAsync(first, d_f, b, cudaMemcpyDeviceToHost, st));
+        TSK_CUDA(cudaMemcpyAsync(last, d_l, b, cudaMemcpyDeviceToHost, st));
+        for (void *p : {(void *)d_b, (void *)d_e, (void *)d_f, (void *)d_l}) TSK_CUDA(cudaFreeAsync(p, st));
+        TSK_CUDA(cudaStreamSynchronize(st));
+        return TSK_OK;
+    } catch (const Error &e) {
+        return fail(e.code, e.msg);
+    }
+}

@@ -1,0 +1,391 @@
+// k1_pairs.cu — K1, the moving-distance pair kernel (GPUTrajDistSearch).
+//
+// Replaces core.pair_intervals (/root/reference/pkg/src/trajseek/core.py:464-565)
+// driven by engine.execute_batch/_run_chunks (engine.py:78-148) for every
+// batch of a plan at once.
+//
+// Work decomposition.  A work item is (batch b, candidate tile, query tile):
+// up to K1_TQ queries of the batch are staged in shared memory as 112-byte
+// records, the block's 256 threads each hold one candidate entry segment in
+// registers (sub-tiles of 256 candidates are walked in turn), and every
+// warp loops over the window of staged queries that can overlap any of its
+// 32 candidates (entries and queries are both start-time sorted, so the
+// window is two binary searches).  Items are claimed from a global atomic
+// counter by a persistent grid.
+//
+// Arithmetic.  For an overlapping pair the reference clips both segments
+// to [ta, tb] and solves the quadratic (core.py:503-565).  With span > 0,
+// only the earlier-starting segment is interpolated at ta and only the
+// later-ending one at tb; the other endpoint is taken verbatim, which is
+// what the np.where selections of core.py:514 produce.  Interpolation at
+// t == ts is an identity (f == 0), so when a warp disagrees about which
+// segment starts first both are interpolated at ta.  Zero-length shared
+// spans (touching extents, waypoints) take a separate exact path.  The
+// hit test uses disc' = dot^2 - aa*(cc - d^2) (= disc/4, exact scaling) with
+// a tiny negative margin; the few candidates that pass are re-solved with
+// the reference's exact root formula.  All ops are binary64 with explicit
+// rounding; divisions use qdiv() with a per-segment RN(1/ext).
+#include "tsk_internal.cuh"
+
+namespace tsk {
+
+struct Cand {
+    double ts, te, ext, rcp, sx, sy, sz, dx, dy, dz, ex, ey, ez;
+};
+
+template <bool SLOW>
+__device__ __forceinline__ double quot(double a, double b, double y) {
+    return SLOW ? __ddiv_rn(a, b) : qdiv(a, b, y);
+}
+
+// p = s + ((t - ts) / ext) * (e - s), the non-verbatim branch of core.py:508-513
+template <bool SLOW>
+__device__ __forceinline__ void lerp(double t, double ts, double ext, double rcp, double sx, double sy,
+                                     double sz, double dx, double dy, double dz, double &px,
+                                     double &py, double &pz) {
+    double f = quot<SLOW>(__dsub_rn(t, ts), ext, rcp);
+    px = __dadd_rn(sx, __dmul_rn(f, dx));
+    py = __dadd_rn(sy, __dmul_rn(f, dy));
+    pz = __dadd_rn(sz, __dmul_rn(f, dz));
+}
+
+// position_at with every verbatim rule (core.py:309-331 / 503-521); used on
+// the zero-span path only.
+__device__ __forceinline__ void position_exact(double t, double ts, double te, double sx, double sy,
+                                               double sz, double ex, double ey, double ez,
+                                               double dx, double dy, double dz, double &px,
+                                               double &py, double &pz) {
+    double ext = __dsub_rn(te, ts);
+    if (ext == 0.0 || t == ts) {
+        px = sx; py = sy; pz = sz;
+    } else if (t == te) {
+        px = ex; py = ey; pz = ez;
+    } else {
+        double f = __ddiv_rn(__dsub_rn(t, ts), ext);
+        px = __dadd_rn(sx, __dmul_rn(f, dx));
+        py = __dadd_rn(sy, __dmul_rn(f, dy));
+        pz = __dadd_rn(sz, __dmul_rn(f, dz));
+    }
+}
+
+struct Hit {
+    bool hit;
+    double tb, te;
+};
+
+// Exact root solve (core.py:536-558) for one pair with span > 0.
+__device__ __forceinline__ Hit solve_exact(double ta, double tb, double cc, double aa, double dot,
+                                           double e, double d2) {
+    Hit h;
+    double bb = __dmul_rn(2.0, dot);
+    double lo, hi;
+    if (aa == 0.0) {  // constant separation
+        h.hit = cc <= d2;
+        lo = 0.0;
+        hi = 1.0;
+    } else {
+        double disc = __dsub_rn(__dmul_rn(bb, bb), __dmul_rn(__dmul_rn(4.0, aa), e));
+        if (!(disc >= 0.0)) {
+            h.hit = false;
+            h.tb = h.te = 0.0;
+            return h;
+        }
+        double sd = __dsqrt_rn(disc);
+        double qq = bb >= 0.0 ? __dmul_rn(-0.5, __dadd_rn(bb, sd)) : __dmul_rn(-0.5, __dsub_rn(bb, sd));
+        double r1 = __ddiv_rn(qq, aa);
+        double r2 = qq == 0.0 ? r1 : __ddiv_rn(e, qq);
+        lo = r1 < r2 ? r1 : r2;
+        hi = r1 > r2 ? r1 : r2;
+        h.hit = lo <= 1.0 && hi >= 0.0;
+    }
+    double span = __dsub_rn(tb, ta);
+    h.tb = lo <= 0.0 ? ta : __dadd_rn(ta, __dmul_rn(lo, span));
+    h.te = hi >= 1.0 ? tb : __dadd_rn(ta, __dmul_rn(hi, span));
+    return h;
+}
+
+struct ItemCtx {
+    int64_t b, lo_q, first_c, c_hi;  // batch, tile's first query ordinal, tile's candidate range
+    int64_t q0;                      // first query offset within batch (tile)
+    int nt;                          // staged queries
+};
+
+__device__ __forceinline__ void append_hit(const K1Launch &L, bool hit, uint64_t key, double tb,
+                                           double te, int lane) {
+    unsigned hm = __ballot_sync(0xffffffffu, hit);
+    if (!hm) return;
+    int leader = __ffs(hm) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(L.hit_count, (unsigned long long)__popc(hm));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (hit) {
+        unsigned long long idx = base + __popc(hm & ((1u << lane) - 1u));
+        if (idx < L.cap) {
+            L.keys[idx] = key;
+            L.tbeg[idx] = tb;
+            L.tend[idx] = te;
+        }
+    }
+}
+
+__device__ __forceinline__ uint64_t make_key(const K1Launch &L, int64_t b, int64_t e_off,
+                                             int64_t q_off) {
+    uint64_t major = L.query_major ? (uint64_t)q_off : (uint64_t)e_off;
+    uint64_t minor = L.query_major ? (uint64_t)e_off : (uint64_t)q_off;
+    return ((uint64_t)b << (L.major_bits + L.minor_bits)) | (major << L.minor_bits) | minor;
+}
+
+// One warp, one candidate per lane, all staged queries in [jlo, jhi).
+template <bool SLOW>
+__device__ void warp_pairs(const K1Launch &L, const QRec *sq, int jlo, int jhi, const Cand &r,
+                           bool valid, int64_t e_off, const ItemCtx &it, int lane,
+                           unsigned &n_ov, unsigned &n_hit) {
+    const unsigned FULL = 0xffffffffu;
+    const double d2 = L.d2;
+    for (int j = jlo; j < jhi; ++j) {
+        const QRec &Q = sq[j];
+        const double cts = Q.ts, cte = Q.te;
+        const double ta = fmax(r.ts, cts);
+        const double tb = fmin(r.te, cte);
+        const bool ov = valid && ta <= tb;
+        const unsigned mov = __ballot_sync(FULL, ov);
+        if (!mov) continue;
+        n_ov += ov ? 1u : 0u;
+        const bool flat = ov && ta == tb;
+        const unsigned mflat = __ballot_sync(FULL, flat);
+        const unsigned act = mov & ~mflat;
+        bool cand = false;
+        double cc = 0, aa = 0, dot = 0, e = 0;
+        if (act) {
+            const double csx = Q.sx, csy = Q.sy, csz = Q.sz, cext = Q.ext;
+            const double cdx = Q.dx, cdy = Q.dy, cdz = Q.dz, crcp = Q.rcp;
+            double rax, ray, raz, cax, cay, caz, rbx, rby, rbz, cbx, cby, cbz;
+            // ── clip at ta: interpolate the earlier starter ──
+            const unsigned mlr = __ballot_sync(FULL, r.ts < cts) & act;
+            if (mlr == act) {
+                lerp<SLOW>(ta, r.ts, r.ext, r.rcp, r.sx, r.sy, r.sz, r.dx, r.dy, r.dz, rax, ray, raz);
+                cax = csx; cay = csy; caz = csz;
+            } else if (mlr == 0) {
+                rax = r.sx; ray = r.sy; raz = r.sz;
+                lerp<SLOW>(ta, cts, cext, crcp, csx, csy, csz, cdx, cdy, cdz, cax, cay, caz);
+            } else {  // f == 0 for the later starter: both interpolations are exact
+                lerp<SLOW>(ta, r.ts, r.ext, r.rcp, r.sx, r.sy, r.sz, r.dx, r.dy, r.dz, rax, ray, raz);
+                lerp<SLOW>(ta, cts, cext, crcp, csx, csy, csz, cdx, cdy, cdz, cax, cay, caz);
+            }
+            // ── clip at tb: interpolate the later ender ──
+            const bool zr = r.te > cte, zc = cte > r.te;
+            const unsigned mzr = __ballot_sync(FULL, zr) & act;
+            const unsigned mzc = __ballot_sync(FULL, zc) & act;
+            if (mzr == act) {
+                lerp<SLOW>(tb, r.ts, r.ext, r.rcp, r.sx, r.sy, r.sz, r.dx, r.dy, r.dz, rbx, rby, rbz);
+                cbx = Q.ex; cby = Q.ey; cbz = Q.ez;
+            } else if (mzc == act) {
+                rbx = r.ex; rby = r.ey; rbz = r.ez;
+                lerp<SLOW>(tb, cts, cext, crcp, csx, csy, csz, cdx, cdy, cdz, cbx, cby, cbz);
+            } else {
+                double px, py, pz, qx, qy, qz;
+                lerp<SLOW>(tb, r.ts, r.ext, r.rcp, r.sx, r.sy, r.sz, r.dx, r.dy, r.dz, px, py, pz);
+                lerp<SLOW>(tb, cts, cext, crcp, csx, csy, csz, cdx, cdy, cdz, qx, qy, qz);
+                rbx = zr ? px : r.ex; rby = zr ? py : r.ey; rbz = zr ? pz : r.ez;
+                cbx = zc ? qx : Q.ex; cby = zc ? qy : Q.ey; cbz = zc ? qz : Q.ez;
+            }
+            // ── quadratic coefficients (core.py:523-537) ──
+            const double ux = __dsub_rn(rax, cax), uy = __dsub_rn(ray, cay), uz = __dsub_rn(raz, caz);
+            cc = __dadd_rn(__dadd_rn(__dmul_rn(ux, ux), __dmul_rn(uy, uy)), __dmul_rn(uz, uz));
+            const double wx = __dsub_rn(__dsub_rn(rbx, rax), __dsub_rn(cbx, cax));
+            const double wy = __dsub_rn(__dsub_rn(rby, ray), __dsub_rn(cby, cay));
+            const double wz = __dsub_rn(__dsub_rn(rbz, raz), __dsub_rn(cbz, caz));
+            aa = __dadd_rn(__dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy)), __dmul_rn(wz, wz));
+            dot = __dadd_rn(__dadd_rn(__dmul_rn(ux, wx), __dmul_rn(uy, wy)), __dmul_rn(uz, wz));
+            e = __dsub_rn(cc, d2);
+            // disc / 4; a margin keeps the test a superset under underflow
+            const double dq = __dsub_rn(__dmul_rn(dot, dot), __dmul_rn(aa, e));
+            cand = ((act >> lane) & 1u) && dq >= -0x1p-1000;
+        }
+        const unsigned mwork = __ballot_sync(FULL, cand) | mflat;
+        if (!mwork) continue;
+        Hit h;
+        h.hit = false;
+        h.tb = h.te = 0.0;
+        if (cand) {
+            h = solve_exact(ta, tb, cc, aa, dot, e, d2);
+        } else if (flat) {
+            // zero-length shared span: positions at ta with every verbatim
+            // rule, constant separation over the instant (core.py:376-378)
+            double rx, ry, rz, qx, qy, qz;
+            position_exact(ta, r.ts, r.te, r.sx, r.sy, r.sz, r.ex, r.ey, r.ez, r.dx, r.dy, r.dz, rx,
+                           ry, rz);
+            position_exact(ta, cts, cte, Q.sx, Q.sy, Q.sz, Q.ex, Q.ey, Q.ez, Q.dx, Q.dy, Q.dz, qx,
+                           qy, qz);
+            const double ux = __dsub_rn(rx, qx), uy = __dsub_rn(ry, qy), uz = __dsub_rn(rz, qz);
+            const double c2 = __dadd_rn(__dadd_rn(__dmul_rn(ux, ux), __dmul_rn(uy, uy)), __dmul_rn(uz, uz));
+            h.hit = c2 <= d2;
+            h.tb = ta;
+            h.te = tb;
+        }
+        n_hit += h.hit ? 1u : 0u;
+        const int64_t q_off = it.q0 + j;
+        append_hit(L, h.hit, make_key(L, it.b, e_off, q_off), h.tb, h.te, lane);
+    }
+}
+
+__device__ __forceinline__ int lower_bound_pm(const double *pm, int n, double v) {
+    int a = 0, b = n;
+    while (a < b) {
+        int m = (a + b) >> 1;
+        if (pm[m] >= v) b = m;
+        else a = m + 1;
+    }
+    return a;
+}
+
+__device__ __forceinline__ int upper_bound_ts(const QRec *q, int n, double v) {
+    int a = 0, b = n;
+    while (a < b) {
+        int m = (a + b) >> 1;
+        if (q[m].ts <= v) a = m + 1;
+        else b = m;
+    }
+    return a;
+}
+
+__global__ void __launch_bounds__(K1_THREADS, 2) k1_pairs(K1Launch L) {
+    __shared__ QRec sq[K1_TQ];
+    __shared__ double pm[K1_TQ];
+    __shared__ ItemCtx it_sh;
+    __shared__ int64_t item_sh;
+    __shared__ unsigned long long red_ov, red_hit;
+
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int64_t total = L.plan.meta[0];
+    const int sub = (int)L.plan.meta[1];
+    const int64_t ct = (int64_t)K1_THREADS * sub;
+    const int64_t nb = L.plan.nb;
+
+    for (;;) {
+        if (tid == 0) {
+            int64_t item = (int64_t)atomicAdd(L.item_counter, 1ull);
+            item_sh = item;
+            if (item < total) {
+                // batch = last b with item_off[b] <= item
+                int64_t a = 0, z = nb;
+                while (z - a > 1) {
+                    int64_t m = (a + z) >> 1;
+                    if (L.plan.item_off[m] <= item) a = m;
+                    else z = m;
+                }
+                // skip empty batches that share the same offset
+                while (a + 1 < nb && L.plan.item_off[a + 1] <= item) ++a;
+                const int64_t b = a;
+                const int64_t local = item - L.plan.item_off[b];
+                const int64_t s_b = L.plan.hi[b] - L.plan.lo[b] + 1;
+                const int64_t tq_n = (s_b + K1_TQ - 1) / K1_TQ;
+                const int64_t tq = local % tq_n, tc = local / tq_n;
+                ItemCtx c;
+                c.b = b;
+                c.q0 = tq * K1_TQ;
+                c.lo_q = L.plan.lo[b] + c.q0;
+                c.nt = (int)(s_b - c.q0 < K1_TQ ? s_b - c.q0 : K1_TQ);
+                c.first_c = L.plan.first[b] + tc * ct;
+                c.c_hi = c.first_c + ct - 1 < L.plan.last[b] ? c.first_c + ct - 1 : L.plan.last[b];
+                it_sh = c;
+            }
+            red_ov = 0;
+            red_hit = 0;
+        }
+        __syncthreads();
+        if (item_sh >= total) break;
+        const ItemCtx it = it_sh;
+
+        // stage the query tile
+        int unsafe_q = 0;
+        for (int j = tid; j < it.nt; j += K1_THREADS) {
+            QRec rec = L.q[it.lo_q + j];
+            sq[j] = rec;
+            if (rec.flag != 0.0) unsafe_q = 1;
+        }
+        unsafe_q = __syncthreads_or(unsafe_q);
+        // running max of te over the tile (window lower bounds)
+        if (tid < 32) {
+            double carry = -INFINITY;
+            for (int base = 0; base < it.nt; base += 32) {
+                int j = base + lane;
+                double v = j < it.nt ? sq[j].te : -INFINITY;
+                for (int o = 1; o < 32; o <<= 1) {
+                    double t = __shfl_up_sync(0xffffffffu, v, o);
+                    if (lane >= o) v = fmax(v, t);
+                }
+                v = fmax(v, carry);
+                if (j < it.nt) pm[j] = v;
+                carry = __shfl_sync(0xffffffffu, v, 31);
+            }
+        }
+        __syncthreads();
+
+        unsigned n_ov = 0, n_hit = 0;
+        for (int s = 0; s < sub; ++s) {
+            const int64_t e = it.first_c + (int64_t)s * K1_THREADS + tid;
+            if (it.first_c + (int64_t)s * K1_THREADS > it.c_hi) break;  // block-uniform
+            const bool valid = e <= it.c_hi;
+            Cand r;
+            int unsafe_r = 0;
+            if (valid) {
+                r.ts = L.e.ts[e]; r.te = L.e.te[e];
+                r.sx = L.e.sx[e]; r.sy = L.e.sy[e]; r.sz = L.e.sz[e];
+                r.ex = L.e.ex[e]; r.ey = L.e.ey[e]; r.ez = L.e.ez[e];
+                r.dx = L.e.dx[e]; r.dy = L.e.dy[e]; r.dz = L.e.dz[e];
+                r.rcp = L.e.rcp[e];
+                r.ext = __dsub_rn(r.te, r.ts);
+                unsafe_r = L.e.unsafe[e];
+            } else {
+                r.ts = INFINITY; r.te = -INFINITY; r.ext = 1.0; r.rcp = 1.0;
+                r.sx = r.sy = r.sz = r.ex = r.ey = r.ez = r.dx = r.dy = r.dz = 0.0;
+            }
+            if (L.noop) continue;
+            // warp window over the staged queries
+            double wmin = valid ? r.ts : INFINITY, wmax = valid ? r.te : -INFINITY;
+            for (int o = 16; o; o >>= 1) {
+                wmin = fmin(wmin, __shfl_xor_sync(0xffffffffu, wmin, o));
+                wmax = fmax(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+            }
+            if (!__any_sync(0xffffffffu, valid)) continue;
+            int jlo = 0, jhi = it.nt;
+            if (L.window_ok) {
+                jlo = lower_bound_pm(pm, it.nt, wmin);
+                jhi = upper_bound_ts(sq, it.nt, wmax);
+            }
+            const int64_t e_off = e - L.plan.first[it.b];
+            const bool slow = unsafe_q || __any_sync(0xffffffffu, unsafe_r);
+            if (slow) warp_pairs<true>(L, sq, jlo, jhi, r, valid, e_off, it, lane, n_ov, n_hit);
+            else warp_pairs<false>(L, sq, jlo, jhi, r, valid, e_off, it, lane, n_ov, n_hit);
+        }
+        // per-batch counters (64-bit)
+        for (int o = 16; o; o >>= 1) {
+            n_ov += __shfl_xor_sync(0xffffffffu, n_ov, o);
+            n_hit += __shfl_xor_sync(0xffffffffu, n_hit, o);
+        }
+        if (lane == 0 && (n_ov | n_hit)) {
+            atomicAdd(&red_ov, (unsigned long long)n_ov);
+            atomicAdd(&red_hit, (unsigned long long)n_hit);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            if (red_ov) atomicAdd(&L.plan.ovl[it.b], red_ov);
+            if (red_hit) atomicAdd(&L.plan.hits[it.b], red_hit);
+        }
+        __syncthreads();
+    }
+}
+
+int k1_blocks_per_sm() {
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k1_pairs, K1_THREADS, 0);
+    return n > 0 ? n : 1;
+}
+
+void launch_k1(const K1Launch &L, int grid, cudaStream_t st) {
+    k1_pairs<<<grid, K1_THREADS, 0, st>>>(L);
+    TSK_CUDA(cudaGetLastError());
+}
+
+}  // namespace tsk

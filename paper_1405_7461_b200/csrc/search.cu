@@ -1,0 +1,432 @@
+// search.cu — plan execution pipeline, K4 result finalisation and the C-ABI
+// entry points tsk_search / tsk_pair_intervals / tsk_result_*.
+//
+//   run_search ........ /root/reference/pkg/src/trajseek/engine.py:151-204
+//   execute_batch ..... engine.py:97-148
+//   pair_intervals .... core.py:464-565
+//   result assembly ... engine.py:133-146 (id gather), core.py:249-303 (ResultSet)
+//
+// Pipeline on the db's stream (one host sync for the hit count, one at the end):
+//   H2D queries → hoist + 112-B records → K3 batch ranges → item scan →
+//   K1 (persistent, atomic work queue) → [grow + rerun on overflow] →
+//   K4 radix sort of 64-bit (batch, entry, query) keys → id gather → D2H
+//   into a pinned block owned by the tsk_result.
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+
+#include "tsk_internal.cuh"
+
+namespace tsk {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+int fail(int code, const std::string &msg) {
+    set_error(msg);
+    return code;
+}
+
+// ── pinned host pool ───────────────────────────────────────────────────────
+
+static std::mutex g_pin_mu;
+static std::multimap<size_t, void *> g_pin_free;
+static size_t g_pin_cached = 0;
+static const size_t kPinCacheMax = size_t(8) << 30;
+
+static void *pin_alloc(size_t bytes, size_t *got) {
+    if (bytes == 0) bytes = 64;
+    {
+        std::lock_guard<std::mutex> g(g_pin_mu);
+        auto it = g_pin_free.lower_bound(bytes);
+        if (it != g_pin_free.end() && it->first <= 2 * bytes + (size_t(1) << 20)) {
+            void *p = it->second;
+            *got = it->first;
+            g_pin_cached -= it->first;
+            g_pin_free.erase(it);
+            return p;
+        }
+    }
+    void *p = nullptr;
+    TSK_CUDA(cudaHostAlloc(&p, bytes, cudaHostAllocPortable));
+    *got = bytes;
+    return p;
+}
+
+static void pin_free(void *p, size_t bytes) {
+    if (!p) return;
+    std::lock_guard<std::mutex> g(g_pin_mu);
+    if (g_pin_cached + bytes <= kPinCacheMax) {
+        g_pin_free.emplace(bytes, p);
+        g_pin_cached += bytes;
+    } else {
+        cudaFreeHost(p);
+    }
+}
+
+static int bits_for(int64_t count) {  // bits to hold 0..count-1
+    int b = 0;
+    while (b < 63 && (int64_t(1) << b) < count) ++b;
+    return b;
+}
+
+// ── K4: id gather in the requested order ───────────────────────────────────
+
+struct GatherArgs {
+    int64_t n;
+    const uint64_t *keys;
+    const uint32_t *perm;  // nullptr: identity
+    const double *tb_in, *te_in;
+    const int64_t *lo, *first;
+    const int64_t *qtraj, *qseg, *etraj, *eseg;
+    int64_t *o_qtraj, *o_qseg, *o_etraj, *o_eseg, *o_qord, *o_eord;
+    double *o_tb, *o_te;
+    int major_bits, minor_bits, query_major;
+};
+
+__global__ void k_gather(GatherArgs a) {
+    const uint64_t mmask = a.major_bits ? ((~0ull) >> (64 - a.major_bits)) : 0ull;
+    const uint64_t nmask = a.minor_bits ? ((~0ull) >> (64 - a.minor_bits)) : 0ull;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t k = a.keys[i];
+        int64_t b = (int64_t)(a.major_bits + a.minor_bits < 64 ? (k >> (a.major_bits + a.minor_bits)) : 0);
+        int64_t major = (int64_t)((k >> a.minor_bits) & mmask);
+        int64_t minor = (int64_t)(k & nmask);
+        int64_t q_off = a.query_major ? major : minor;
+        int64_t e_off = a.query_major ? minor : major;
+        int64_t q = a.lo[b] + q_off, e = a.first[b] + e_off;
+        int64_t j = a.perm ? (int64_t)a.perm[i] : i;
+        a.o_qtraj[i] = a.qtraj[q];
+        a.o_qseg[i] = a.qseg[q];
+        a.o_etraj[i] = a.etraj[e];
+        a.o_eseg[i] = a.eseg[e];
+        a.o_tb[i] = a.tb_in[j];
+        a.o_te[i] = a.te_in[j];
+        if (a.o_qord) a.o_qord[i] = q;
+        if (a.o_eord) a.o_eord[i] = e;
+    }
+}
+
+__global__ void k_iota(int64_t n, uint32_t *v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        v[i] = (uint32_t)i;
+}
+
+static int sm_count(int device) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+    return n > 0 ? n : 148;
+}
+
+static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int64_t *b_lo,
+                       const int64_t *b_hi, const int64_t *b_first, const int64_t *b_last, double d,
+                       uint32_t flags) {
+    TSK_REQUIRE(std::isfinite(d) && d >= 0.0, "threshold d must be finite and non-negative");
+    TSK_REQUIRE(qc && qc->n > 0, "query set is empty");
+    TSK_REQUIRE(nb >= 1 && b_lo && b_hi, "a plan needs at least one batch");
+    const bool spans_given = flags & TSK_SPANS_GIVEN;
+    const int64_t nq = qc->n, n = db->s.n;
+    int64_t max_s = 1;
+    for (int64_t b = 0; b < nb; ++b) {
+        TSK_REQUIRE(b_lo[b] >= 0 && b_lo[b] <= b_hi[b] && b_hi[b] < nq, "batch outside the query set");
+        max_s = std::max<int64_t>(max_s, b_hi[b] - b_lo[b] + 1);
+        if (spans_given) {
+            TSK_REQUIRE(b_first && b_last, "spans missing");
+            if (b_first[b] >= 0 || b_last[b] >= 0)
+                TSK_REQUIRE(0 <= b_first[b] && b_first[b] <= b_last[b] && b_last[b] < n,
+                            "candidate span outside store");
+        }
+    }
+    TSK_CUDA(cudaSetDevice(db->device));
+    cudaStream_t st = db->stream;
+    const bool query_major = flags & TSK_ORDER_QUERY_MAJOR;
+    const bool ordered = query_major || (flags & TSK_ORDER_REFERENCE);
+    const int bb = bits_for(nb);
+    const int eb = bits_for(std::max<int64_t>(n, 1)), qb = bits_for(max_s);
+    const int major_bits = query_major ? qb : eb, minor_bits = query_major ? eb : qb;
+    TSK_REQUIRE(bb + major_bits + minor_bits <= 64, "result key wider than 64 bits");
+
+    int64_t launches = 0;
+    TSK_CUDA(cudaEventRecord(db->ev0, st));
+    if (flags & TSK_QUERIES_RESIDENT) {
+        TSK_REQUIRE(db->q.n == nq && db->q_rec.p, "no resident query set of this size");
+    } else {
+        // queries → device SoA (+ hoisted invariants) → shared-memory records
+        soa_alloc(db->q, nq, true, st);
+        soa_upload(db->q, qc, st);
+        soa_hoist(db->q, st);
+        db->q_rec.reserve((size_t)nq * sizeof(QRec), st);
+        launch_qrec(db->q, db->q_rec.as<QRec>(), st);
+        launches += 2;
+    }
+
+    // batch table: lo hi first last item_off(nb+1) meta(4) ovl hits
+    size_t nbz = (size_t)nb;
+    db->batches.reserve((nbz * 7 + 8) * 8, st);
+    int64_t *d_lo = db->batches.as<int64_t>();
+    int64_t *d_hi = d_lo + nbz, *d_first = d_hi + nbz, *d_last = d_first + nbz;
+    int64_t *d_off = d_last + nbz, *d_meta = d_off + nbz + 1;
+    unsigned long long *d_ovl = (unsigned long long *)(d_meta + 4);
+    unsigned long long *d_hits = d_ovl + nbz;
+    TSK_CUDA(cudaMemcpyAsync(d_lo, b_lo, nbz * 8, cudaMemcpyHostToDevice, st));
+    TSK_CUDA(cudaMemcpyAsync(d_hi, b_hi, nbz * 8, cudaMemcpyHostToDevice, st));
+    if (spans_given) {
+        TSK_CUDA(cudaMemcpyAsync(d_first, b_first, nbz * 8, cudaMemcpyHostToDevice, st));
+        TSK_CUDA(cudaMemcpyAsync(d_last, b_last, nbz * 8, cudaMemcpyHostToDevice, st));
+    }
+    SearchPlanDev plan{nb, d_lo, d_hi, d_first, d_last, d_off, d_meta, d_ovl, d_hits};
+    launch_ranges(db, db->q, plan, spans_given, st);
+    const int bps = k1_blocks_per_sm();
+    const int slots = sm_count(db->device) * bps;
+    launch_plan_items(plan, slots, st);
+    launches += spans_given ? 1 : 2;
+
+    db->counters.reserve(64, st);
+    unsigned long long *d_ctr = db->counters.as<unsigned long long>();  // [0] items [1] hits
+    uint64_t cap = db->recs.bytes / 24;
+    if (cap < (uint64_t(1) << 20)) {
+        db->recs.reserve((size_t(1) << 20) * 24, st);
+        cap = db->recs.bytes / 24;
+    }
+    K1Launch L;
+    L.e = db->s;
+    L.q = db->q_rec.as<QRec>();
+    L.plan = plan;
+    L.item_counter = d_ctr;
+    L.hit_count = d_ctr + 1;
+    L.d2 = d * d;  // core.py:527
+    L.major_bits = major_bits;
+    L.minor_bits = minor_bits;
+    L.query_major = query_major;
+    L.noop = (flags & TSK_NOOP) ? 1 : 0;
+    L.window_ok = db->q.sorted;
+    unsigned long long h_hits = 0;
+    float k1_ms = 0.f;
+    for (int attempt = 0;; ++attempt) {
+        L.cap = cap;
+        L.keys = db->recs.as<uint64_t>();
+        L.tbeg = reinterpret_cast<double *>(L.keys + cap);
+        L.tend = L.tbeg + cap;
+        TSK_CUDA(cudaMemsetAsync(d_ctr, 0, 16, st));
+        TSK_CUDA(cudaMemsetAsync(d_ovl, 0, nbz * 16, st));
+        TSK_CUDA(cudaEventRecord(db->ev_k0, st));
+        launch_k1(L, slots, st);
+        ++launches;
+        TSK_CUDA(cudaEventRecord(db->ev_k1, st));
+        TSK_CUDA(cudaMemcpyAsync(&h_hits, d_ctr + 1, 8, cudaMemcpyDeviceToHost, st));
+        TSK_CUDA(cudaStreamSynchronize(st));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, db->ev_k0, db->ev_k1);
+        k1_ms += ms;
+        if (h_hits <= cap) break;
+        TSK_REQUIRE(attempt < 3, "result buffer kept overflowing");
+        // overflow-safe sizing: grow to the exact count and rerun K1
+        db->recs.reserve((size_t)h_hits * 24 + 24 * 1024, st);
+        cap = db->recs.bytes / 24;
+    }
+    TSK_REQUIRE(h_hits < (1ull << 32), "more than 2^32 hits in one call");
+    const int64_t nh = (int64_t)h_hits;
+
+    tsk_result *res = new tsk_result();
+    res->n = nh;
+    res->nb = nb;
+    res->k1_ms = k1_ms;
+    res->per_batch.resize(nbz * 4);
+    {
+        std::vector<int64_t> tmp(nbz * 4);
+        TSK_CUDA(cudaMemcpyAsync(tmp.data(), d_first, nbz * 8, cudaMemcpyDeviceToHost, st));
+        TSK_CUDA(cudaMemcpyAsync(tmp.data() + nbz, d_last, nbz * 8, cudaMemcpyDeviceToHost, st));
+        TSK_CUDA(cudaMemcpyAsync(tmp.data() + 2 * nbz, d_ovl, nbz * 8, cudaMemcpyDeviceToHost, st));
+        TSK_CUDA(cudaMemcpyAsync(tmp.data() + 3 * nbz, d_hits, nbz * 8, cudaMemcpyDeviceToHost, st));
+        // host copy happens after the final sync below
+        res->per_batch.swap(tmp);
+    }
+    const bool want_ord = flags & TSK_WANT_ORDINALS;
+    const bool on_device = flags & TSK_RESULTS_ON_DEVICE;
+    const int ncols = want_ord ? 8 : 6;
+    size_t got = 0;
+    res->host = on_device ? nullptr : pin_alloc((size_t)(nh > 0 ? nh : 1) * 8 * ncols, &got);
+    res->host_bytes = got;
+    char *hb = static_cast<char *>(res->host);
+    size_t cb = (size_t)nh * 8;
+    if (hb) {
+        res->qtraj = (int64_t *)(hb + 0 * cb);
+        res->qseg = (int64_t *)(hb + 1 * cb);
+        res->etraj = (int64_t *)(hb + 2 * cb);
+        res->eseg = (int64_t *)(hb + 3 * cb);
+        res->tbeg = (double *)(hb + 4 * cb);
+        res->tend = (double *)(hb + 5 * cb);
+    }
+    if (hb && want_ord) {
+        res->qord = (int64_t *)(hb + 6 * cb);
+        res->eord = (int64_t *)(hb + 7 * cb);
+    }
+    if (nh > 0) {
+        const uint64_t *keys = db->recs.as<uint64_t>();
+        const double *tbin = reinterpret_cast<const double *>(keys + cap);
+        const double *tein = tbin + cap;
+        const uint32_t *perm = nullptr;
+        if (ordered) {
+            // K4: radix sort (batch, major, minor) keys; values = append index
+            db->sorted.reserve((size_t)nh * (8 + 8 + 4 + 4), st);
+            uint64_t *ks = db->sorted.as<uint64_t>();
+            uint64_t *ko = ks + nh;
+            uint32_t *v0 = reinterpret_cast<uint32_t *>(ko + nh);
+            uint32_t *v1 = v0 + nh;
+            int gi = (int)std::min<int64_t>((nh + 255) / 256, 148 * 8);
+            k_iota<<<gi, 256, 0, st>>>(nh, v0);
+            TSK_CUDA(cudaGetLastError());
+            ++launches;
+            TSK_CUDA(cudaMemcpyAsync(ks, keys, cb, cudaMemcpyDeviceToDevice, st));
+            int end_bit = bb + major_bits + minor_bits;
+            if (end_bit == 0) end_bit = 1;
+            size_t tb = 0;
+            TSK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, ks, ko, v0, v1, nh, 0, end_bit, st));
+            db->cub_tmp.reserve(tb, st);
+            TSK_CUDA(cub::DeviceRadixSort::SortPairs(db->cub_tmp.p, tb, ks, ko, v0, v1, nh, 0, end_bit, st));
+            keys = ko;
+            perm = v1;
+        }
+        db->out_cols.reserve(cb * ncols, st);
+        char *ob = db->out_cols.as<char>();
+        GatherArgs g;
+        g.n = nh;
+        g.keys = keys;
+        g.perm = perm;
+        g.tb_in = tbin;
+        g.te_in = tein;
+        g.lo = d_lo;
+        g.first = d_first;
+        g.qtraj = db->q.traj;
+        g.qseg = db->q.seg;
+        g.etraj = db->s.traj;
+        g.eseg = db->s.seg;
+        g.o_qtraj = (int64_t *)(ob + 0 * cb);
+        g.o_qseg = (int64_t *)(ob + 1 * cb);
+        g.o_etraj = (int64_t *)(ob + 2 * cb);
+        g.o_eseg = (int64_t *)(ob + 3 * cb);
+        g.o_tb = (double *)(ob + 4 * cb);
+        g.o_te = (double *)(ob + 5 * cb);
+        g.o_qord = want_ord ? (int64_t *)(ob + 6 * cb) : nullptr;
+        g.o_eord = want_ord ? (int64_t *)(ob + 7 * cb) : nullptr;
+        g.major_bits = major_bits;
+        g.minor_bits = minor_bits;
+        g.query_major = query_major;
+        int gg = (int)std::min<int64_t>((nh + 255) / 256, 148 * 8);
+        k_gather<<<gg, 256, 0, st>>>(g);
+        TSK_CUDA(cudaGetLastError());
+        ++launches;
+        if (!on_device) TSK_CUDA(cudaMemcpyAsync(res->host, ob, cb * ncols, cudaMemcpyDeviceToHost, st));
+    }
+    TSK_CUDA(cudaEventRecord(db->ev1, st));
+    TSK_CUDA(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, db->ev0, db->ev1);
+    res->device_ms = ms;
+    res->launches = launches;
+    return res;
+}
+
+}  // namespace tsk
+
+using namespace tsk;
+
+extern "C" int tsk_abi_version(void) { return TSK_ABI_VERSION; }
+
+extern "C" int tsk_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+extern "C" const char *tsk_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" int tsk_search(tsk_db *db, const tsk_columns *queries, int64_t nb, const int64_t *b_lo,
+                          const int64_t *b_hi, const int64_t *b_first, const int64_t *b_last,
+                          double d, uint32_t flags, tsk_result **out) {
+    try {
+        TSK_REQUIRE(db && out, "null argument");
+        *out = run(db, queries, nb, b_lo, b_hi, b_first, b_last, d, flags);
+        return TSK_OK;
+    } catch (const Error &e) {
+        return fail(e.code, e.msg);
+    }
+}
+
+extern "C" int tsk_pair_intervals(int device, const tsk_columns *rows, const tsk_columns *cols,
+                                  double d, tsk_result **out) {
+    tsk_db *db = nullptr;
+    try {
+        TSK_REQUIRE(rows && cols && out, "null argument");
+        TSK_REQUIRE(std::isfinite(d) && d >= 0.0, "threshold d must be finite and non-negative");
+        TSK_REQUIRE(rows->n > 0 && cols->n > 0, "pair_intervals needs non-empty stores");
+        int rc = tsk_db_create(device, rows, &db);
+        if (rc != TSK_OK) return rc;
+        int64_t lo = 0, hi = cols->n - 1, first = 0, last = rows->n - 1;
+        *out = run(db, cols, 1, &lo, &hi, &first, &last, d,
+                   TSK_SPANS_GIVEN | TSK_ORDER_REFERENCE | TSK_WANT_ORDINALS);
+        tsk_db_free(db);
+        return TSK_OK;
+    } catch (const Error &e) {
+        if (db) tsk_db_free(db);
+        return fail(e.code, e.msg);
+    }
+}
+
+extern "C" int tsk_result_info(const tsk_result *r, int64_t *n_hits, int64_t *nb, double *device_ms) {
+    if (!r) return fail(TSK_EINVAL, "null result");
+    if (n_hits) *n_hits = r->n;
+    if (nb) *nb = r->nb;
+    if (device_ms) *device_ms = r->device_ms;
+    return TSK_OK;
+}
+
+extern "C" int tsk_result_timing(const tsk_result *r, double *device_ms, double *k1_ms,
+                                 int64_t *launches) {
+    if (!r) return fail(TSK_EINVAL, "null result");
+    if (device_ms) *device_ms = r->device_ms;
+    if (k1_ms) *k1_ms = r->k1_ms;
+    if (launches) *launches = r->launches;
+    return TSK_OK;
+}
+
+extern "C" int tsk_result_per_batch(const tsk_result *r, int64_t *per_batch) {
+    if (!r || !per_batch) return fail(TSK_EINVAL, "null argument");
+    // stored column-wise (first[], last[], ovl[], hits[]); returned row-wise
+    const int64_t nb = r->nb;
+    for (int64_t b = 0; b < nb; ++b)
+        for (int k = 0; k < 4; ++k) per_batch[b * 4 + k] = r->per_batch[k * nb + b];
+    return TSK_OK;
+}
+
+extern "C" int tsk_result_columns(const tsk_result *r, const int64_t **query_traj,
+                                  const int64_t **query_seg, const int64_t **entry_traj,
+                                  const int64_t **entry_seg, const double **t_begin,
+                                  const double **t_end, const int64_t **query_ord,
+                                  const int64_t **entry_ord) {
+    if (!r) return fail(TSK_EINVAL, "null result");
+    if (query_traj) *query_traj = r->qtraj;
+    if (query_seg) *query_seg = r->qseg;
+    if (entry_traj) *entry_traj = r->etraj;
+    if (entry_seg) *entry_seg = r->eseg;
+    if (t_begin) *t_begin = r->tbeg;
+    if (t_end) *t_end = r->tend;
+    if (query_ord) *query_ord = r->qord;
+    if (entry_ord) *entry_ord = r->eord;
+    return TSK_OK;
+}
+
+extern "C" void tsk_result_free(tsk_result *r) {
+    if (!r) return;
+    pin_free(r->host, r->host_bytes);
+    delete r;
+}

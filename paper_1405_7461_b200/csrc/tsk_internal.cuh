@@ -1,0 +1,202 @@
+// tsk_internal.cuh — shared device layouts and helpers for libtrajseek.
+//
+// Arithmetic contract: every floating-point step of the pair evaluation is
+// one IEEE-754 binary64 operation, in the reference's order
+// (/root/reference/pkg/src/trajseek/core.py:490-565).  The library is
+// compiled with -fmad=false and the explicit __d*_rn intrinsics below are
+// used on the hot path so that no multiply-add is contracted.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/trajseek.h"
+
+namespace tsk {
+
+// ── error plumbing ──────────────────────────────────────────────────────────
+
+void set_error(const std::string &msg);
+int fail(int code, const std::string &msg);
+
+struct Error {
+    int code;
+    std::string msg;
+};
+
+#define TSK_CUDA(call)                                                                   \
+    do {                                                                                 \
+        cudaError_t _e = (call);                                                         \
+        if (_e != cudaSuccess)                                                           \
+            throw ::tsk::Error{_e == cudaErrorMemoryAllocation ? TSK_ENOMEM : TSK_ECUDA, \
+                               std::string(#call) + ": " + cudaGetErrorString(_e)};      \
+    } while (0)
+
+#define TSK_REQUIRE(cond, msg)                                \
+    do {                                                      \
+        if (!(cond)) throw ::tsk::Error{TSK_EINVAL, (msg)};   \
+    } while (0)
+
+// ── device buffers ──────────────────────────────────────────────────────────
+
+// Grow-only device buffer (stream-ordered allocations on the db's stream).
+struct DBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    template <class T>
+    T *as() const { return static_cast<T *>(p); }
+    void reserve(size_t need, cudaStream_t s);
+    void release(cudaStream_t s);
+};
+
+// Entry (or query) segments in device SoA form.  Hoisted invariants:
+//   dx,dy,dz = xe-xs, ye-ys, ze-zs  (the (e - s) of core.py:512)
+//   rcp      = RN(1/(te-ts)) for te > ts, else 0 (waypoint)
+//   unsafe   = 1 when the Markstein quotient (qdiv below) is not proven
+//              exact for this segment (extreme exponents, see mark_unsafe)
+struct Soa {
+    int64_t n = 0;
+    double *ts = nullptr, *te = nullptr, *sx = nullptr, *sy = nullptr, *sz = nullptr;
+    double *ex = nullptr, *ey = nullptr, *ez = nullptr;
+    double *dx = nullptr, *dy = nullptr, *dz = nullptr, *rcp = nullptr;
+    int64_t *traj = nullptr, *seg = nullptr;
+    uint8_t *unsafe = nullptr;
+    int any_unsafe = 0;
+    int sorted = 1;  // ts non-decreasing
+    DBuf storage;
+};
+
+// Query record staged in shared memory: 7 × 16 B, laid out for LDS.128 pairs.
+struct __align__(16) QRec {
+    double ts, te;
+    double sx, sy;
+    double sz, ext;
+    double dx, dy;
+    double dz, rcp;
+    double ex, ey;
+    double ez, flag;  // flag: 1.0 when the segment is Markstein-unsafe
+};
+static_assert(sizeof(QRec) == 112, "QRec layout");
+
+struct Index {
+    int64_t m = 0, n_ne = 0;
+    int rule = 0;
+    double width = 0, t0 = 0, t_max = 0;
+    double *ne_start = nullptr, *ne_end = nullptr, *ne_endmax = nullptr;
+    int64_t *ne_first = nullptr, *ne_last = nullptr, *ne_bin = nullptr;
+    DBuf storage;
+    bool built = false;
+};
+
+}  // namespace tsk
+
+// The opaque handles of the C-ABI.
+struct tsk_db {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    tsk::Soa s;
+    tsk::Index ix;
+    // search workspace (grow-only)
+    tsk::DBuf q_rec, batches, counters, recs, sorted, cub_tmp, out_cols;
+    tsk::Soa q;  // device copy of the current query set
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_k0 = nullptr, ev_k1 = nullptr;
+};
+
+struct tsk_result {
+    int64_t n = 0, nb = 0;
+    double device_ms = 0, k1_ms = 0;
+    int64_t launches = 0;
+    std::vector<int64_t> per_batch;  // nb × 4
+    void *host = nullptr;            // pinned block holding the columns
+    size_t host_bytes = 0;
+    int64_t *qtraj = nullptr, *qseg = nullptr, *etraj = nullptr, *eseg = nullptr;
+    double *tbeg = nullptr, *tend = nullptr;
+    int64_t *qord = nullptr, *eord = nullptr;
+};
+
+namespace tsk {
+
+// ── exact arithmetic helpers ────────────────────────────────────────────────
+
+// RN(a/b) from y = RN(1/b) with two residual corrections (Markstein).
+// q1 = RN(q0 + r0*y) is within one ulp of a/b; the second correction then
+// returns the correctly rounded quotient (Markstein's theorem, y within
+// half an ulp of 1/b, q1 faithful).  Residuals r = a - b*q are exact in FMA
+// for faithful q as long as nothing underflows; mark_unsafe() routes inputs
+// that could underflow/overflow to IEEE division instead.
+__device__ __forceinline__ double qdiv(double a, double b, double y) {
+    double q = __dmul_rn(a, y);
+    double r = __fma_rn(-b, q, a);
+    q = __fma_rn(r, y, q);
+    r = __fma_rn(-b, q, a);
+    return __fma_rn(r, y, q);
+}
+
+// numpy float64 floor_divide (npy_divmod) — used for bin assignment at
+// index.py:110.  fmod is exact in CUDA; the rest mirrors numpy's steps.
+__device__ __forceinline__ double np_floor_divide(double a, double b) {
+    if (b == 0.0) return __ddiv_rn(a, b);
+    double mod = fmod(a, b);
+    double div = __ddiv_rn(__dsub_rn(a, mod), b);
+    if (mod != 0.0) {
+        if ((b < 0.0) != (mod < 0.0)) {
+            mod = __dadd_rn(mod, b);
+            div = __dsub_rn(div, 1.0);
+        }
+    }
+    double fl;
+    if (div != 0.0) {
+        fl = floor(div);
+        if (__dsub_rn(div, fl) > 0.5) fl = __dadd_rn(fl, 1.0);
+    } else {
+        fl = copysign(0.0, __ddiv_rn(a, b));
+    }
+    return fl;
+}
+
+// ── host-side launchers (defined in the .cu files) ─────────────────────────
+
+void soa_alloc(Soa &s, int64_t n, bool with_ids, cudaStream_t st);
+void soa_upload(Soa &s, const tsk_columns *c, cudaStream_t st);
+void soa_hoist(Soa &s, cudaStream_t st);  // dx/dy/dz, rcp, unsafe, sorted
+
+struct SearchPlanDev {
+    int64_t nb;
+    const int64_t *lo, *hi;        // device
+    int64_t *first, *last;         // device (filled by K3 or given)
+    int64_t *item_off;             // nb + 1
+    int64_t *meta;                 // [0]=total items, [1]=sub tiles, [2..] scratch
+    unsigned long long *ovl, *hits;  // per batch
+};
+
+struct K1Launch {
+    Soa e;  // by value: device pointers
+    const QRec *q;
+    SearchPlanDev plan;
+    unsigned long long *item_counter;
+    unsigned long long *hit_count;
+    uint64_t *keys;
+    double *tbeg, *tend;
+    uint64_t cap;
+    double d2;
+    int major_bits, minor_bits;  // key = b << (major+minor) | major << minor | minor
+    int query_major;             // 0: (b, entry, query); 1: (b, query, entry)
+    int noop;
+    int window_ok;
+};
+
+void launch_ranges(tsk_db *db, const Soa &q, SearchPlanDev &p, bool spans_given, cudaStream_t st);
+void launch_plan_items(SearchPlanDev &p, int sm_count, cudaStream_t st);
+void launch_qrec(const Soa &q, QRec *out, cudaStream_t st);
+void launch_k1(const K1Launch &L, int grid, cudaStream_t st);
+int k1_blocks_per_sm();
+
+constexpr int K1_THREADS = 256;
+constexpr int K1_TQ = 256;        // queries per tile staged in shared memory
+constexpr int K1_MAX_SUB = 8;     // candidate sub-tiles (of K1_THREADS) per item
+
+}  // namespace tsk

@@ -1,0 +1,177 @@
+"""Synthetic trajectory stores for tests and benchmarks (host side).
+
+RandWalk profiles draw the same PCG64 stream, call for call, as the
+reference generator (/root/reference/pkg/src/trajseek/datagen.py:106-267),
+so a (profile, seed) pair yields the reference's dataset byte for byte —
+that is pinned by tests/golden/datagen.npz.  The data generator itself is
+outside the hot path; it exists so the benchmark and the
+parity tests feed identical float64 inputs to the GPU path and the CPU
+baseline.
+
+``galaxy`` adds the Galaxy-shaped star-orbit workload of the paper
+ that the reference does not ship: stars on circular
+orbits in a flat rotation curve with small vertical oscillation, sampled
+once per time unit.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from .core import DomainError, SegmentStore
+
+PROFILE_KINDS = ("uniform", "normal", "normal5", "exp")
+
+
+@dataclass(frozen=True)
+class GenProfile:
+    """Dataset recipe (datagen.py:106-145)."""
+
+    kind: str
+    trajectories: int
+    seed: int
+    timesteps: int = 400
+    start_window: tuple[float, float] = (0.0, 100.0)
+    normal_mean: float = 200.0
+    normal_std: float = 200.0
+    exp_mean: float = 70.0
+    steps_min: int = 2
+    steps_max: int = 1000
+    step_scale: float = 1.0
+    arena: float = 100.0
+
+    def __post_init__(self) -> None:
+        if self.kind not in PROFILE_KINDS:
+            raise DomainError(f"unknown profile kind {self.kind!r}; expected one of {PROFILE_KINDS}")
+        if self.trajectories < 1:
+            raise DomainError(f"trajectories={self.trajectories} must be >= 1")
+        if self.timesteps < 2:
+            raise DomainError(f"timesteps={self.timesteps} must be >= 2 (one segment)")
+        if self.steps_min < 2:
+            raise DomainError(f"steps_min={self.steps_min} must be >= 2")
+        if self.steps_max < self.steps_min:
+            raise DomainError(f"steps_max={self.steps_max} must be >= steps_min")
+        lo, hi = self.start_window
+        if hi < lo:
+            raise DomainError(f"start_window {self.start_window} is inverted")
+        if min(self.exp_mean, self.step_scale, self.arena) <= 0:
+            raise DomainError("exp_mean, step_scale and arena must be positive")
+
+
+_DEFAULT_WINDOWS = {"normal": (0.0, 400.0), "normal5": (0.0, 400.0), "exp": (0.0, 20.0)}
+
+
+def make_profile(kind: str, trajectories: int, seed: int, **overrides) -> GenProfile:
+    """Profile with the per-kind default start window (datagen.py:148-159)."""
+    p = GenProfile(kind=kind, trajectories=trajectories, seed=seed)
+    if kind in _DEFAULT_WINDOWS and "start_window" not in overrides:
+        p = replace(p, start_window=_DEFAULT_WINDOWS[kind])
+    return replace(p, **overrides) if overrides else p
+
+
+def _truncated(rng, sampler, lo: float, hi: float, n: int) -> np.ndarray:
+    """Rejection-sample n values of ``sampler`` into [lo, hi]."""
+    got = []
+    need = n
+    while need > 0:
+        x = sampler(rng, need)
+        x = x[(x >= lo) & (x <= hi)]
+        got.append(x)
+        need -= x.shape[0]
+    return np.concatenate(got) if got else np.empty(0)
+
+
+def _starts(p: GenProfile, rng) -> np.ndarray:
+    lo, hi = p.start_window
+    n = p.trajectories
+    if p.kind in ("uniform", "exp"):
+        return rng.uniform(lo, hi, n)
+    if p.kind == "normal":
+        return _truncated(rng, lambda r, k: r.normal(p.normal_mean, p.normal_std, k), lo, hi, n)
+    width = hi - lo
+    centres = lo + width * (2 * np.arange(5) + 1) / 10.0
+    sd = width / 20.0
+    comp = rng.integers(0, 5, n)
+    out = np.empty(n, dtype=np.float64)
+    for k in range(5):
+        sel = comp == k
+        if sel.any():
+            out[sel] = _truncated(rng, lambda r, m: r.normal(centres[k], sd, m), lo, hi, int(sel.sum()))
+    return out
+
+
+def _lengths(p: GenProfile, rng) -> np.ndarray:
+    if p.kind != "exp":
+        return np.full(p.trajectories, p.timesteps, dtype=np.int64)
+    raw = _truncated(rng, lambda r, k: r.exponential(p.exp_mean, k),
+                     float(p.steps_min), float(p.steps_max), p.trajectories)
+    return np.rint(raw).astype(np.int64)
+
+
+def generate(profile: GenProfile) -> SegmentStore:
+    """Random-walk store for ``profile`` (datagen.py:206-245), sorted by start."""
+    rng = np.random.default_rng(profile.seed)
+    starts = _starts(profile, rng)
+    pts = _lengths(profile, rng)
+    nseg = pts - 1
+    total = int(nseg.sum())
+    cols = {k: np.empty(total, dtype=np.float64) for k in ("xs", "ys", "zs", "ts", "xe", "ye", "ze", "te")}
+    traj = np.repeat(np.arange(profile.trajectories, dtype=np.int64), nseg)
+    offs = np.concatenate([[0], np.cumsum(nseg)])
+    seg = np.arange(total, dtype=np.int64) - np.repeat(offs[:-1], nseg)
+    zero = np.zeros((1, 3))
+    for i in range(profile.trajectories):
+        k = int(nseg[i])
+        a, b = int(offs[i]), int(offs[i + 1])
+        origin = rng.uniform(0.0, profile.arena, 3)
+        walk = origin + np.vstack([zero, np.cumsum(rng.normal(0.0, profile.step_scale, (k, 3)), axis=0)])
+        t = starts[i] + np.arange(k + 1, dtype=np.float64)
+        cols["ts"][a:b] = t[:-1]
+        cols["te"][a:b] = t[1:]
+        for ax, (s, e) in enumerate((("xs", "xe"), ("ys", "ye"), ("zs", "ze"))):
+            cols[s][a:b] = walk[:-1, ax]
+            cols[e][a:b] = walk[1:, ax]
+    return SegmentStore(traj, seg, cols["xs"], cols["ys"], cols["zs"], cols["ts"],
+                        cols["xe"], cols["ye"], cols["ze"], cols["te"], validate=False)
+
+
+def sample_queries(source: SegmentStore, num_traj: int, seed: int) -> SegmentStore:
+    """Whole trajectories drawn without replacement (datagen.py:248-267)."""
+    ids = np.unique(source.traj)
+    if not 1 <= num_traj <= ids.shape[0]:
+        raise DomainError(f"num_traj={num_traj} must be in 1..{ids.shape[0]} (distinct trajectories)")
+    pick = np.random.default_rng(seed).choice(ids, size=num_traj, replace=False)
+    keep = np.isin(source.traj, pick)
+    return SegmentStore(*(getattr(source, k)[keep] for k in
+                          ("traj", "seg", "xs", "ys", "zs", "ts", "xe", "ye", "ze", "te")),
+                        validate=False)
+
+
+def galaxy(stars: int, seed: int, *, points: int = 401, start_window=(0.0, 100.0),
+           r_min: float = 1.0, r_max: float = 50.0, v_circ: float = 0.2,
+           z_amp: float = 0.5) -> SegmentStore:
+    """Galaxy-shaped store: ``stars`` orbits of ``points`` samples each.
+
+    Flat rotation curve (angular speed v_circ / r), uniform disc surface
+    density, small vertical epicycles; start times uniform over the
+    window (PAPER.md:1025-1031 describes the workload).
+    """
+    rng = np.random.default_rng(seed)
+    r = np.sqrt(rng.uniform(r_min * r_min, r_max * r_max, stars))
+    phase = rng.uniform(0.0, 2 * np.pi, stars)
+    zphase = rng.uniform(0.0, 2 * np.pi, stars)
+    t0 = rng.uniform(start_window[0], start_window[1], stars)
+    k = np.arange(points, dtype=np.float64)
+    omega = (v_circ / r)[:, None]
+    ang = phase[:, None] + omega * k[None, :]
+    x = r[:, None] * np.cos(ang)
+    y = r[:, None] * np.sin(ang)
+    z = z_amp * np.sin(zphase[:, None] + 3.0 * omega * k[None, :])
+    t = t0[:, None] + k[None, :]
+    traj = np.repeat(np.arange(stars, dtype=np.int64), points - 1)
+    seg = np.tile(np.arange(points - 1, dtype=np.int64), stars)
+    s, e = (slice(None), slice(None, -1)), (slice(None), slice(1, None))
+    return SegmentStore(traj, seg, x[s].ravel(), y[s].ravel(), z[s].ravel(), t[s].ravel(),
+                        x[e].ravel(), y[e].ravel(), z[e].ravel(), t[e].ravel(), validate=False)

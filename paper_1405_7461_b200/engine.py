@@ -1,0 +1,170 @@
+"""Search execution on the GPU — the drop-in for engine.py.
+
+Same entry points, signatures, statistics and DomainError behaviour as
+/root/reference/pkg/src/trajseek/engine.py:
+
+* :func:`execute_batch` (engine.py:97-148) — one batch against an explicit
+  candidate span.
+* :func:`run_search` (engine.py:151-204) — a whole plan.  All batches go to
+  the device in one call: batch extents and candidate ranges (K3), the pair
+  kernel over every (batch, candidate tile, query tile) work item (K1), the
+  overflow-safe hit buffer, and the radix sort + id gather that returns the
+  hits in the reference's order (batch, entry ordinal, query ordinal) (K4).
+* :func:`launch_overhead_pass` (engine.py:207-224) — the same launch with
+  the pair arithmetic elided.
+
+``workers`` is accepted and validated for API compatibility; parallelism
+is the GPU grid.  Per-batch ``kernel_seconds`` cannot be measured inside
+one fused launch, so the device time is apportioned by interactions.
+"""
+
+from __future__ import annotations
+
+import os
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .core import DomainError, ResultSet, SegmentStore
+from .index import TemporalIndex
+from .planner import BatchPlan
+
+
+@dataclass
+class BatchTrace:
+    """Per-batch accounting (engine.py:32-41)."""
+
+    ordinal: int
+    queries: int
+    candidates: int
+    interactions: int
+    hits: int
+    kernel_seconds: float
+
+
+@dataclass
+class SearchStats:
+    """Counters and timings (engine.py:44-66); interactions_computed ==
+    temporal_misses + spatial_misses + hits."""
+
+    interactions_computed: int = 0
+    temporal_misses: int = 0
+    spatial_misses: int = 0
+    hits: int = 0
+    kernel_seconds: float = 0.0
+    overhead_seconds: float = 0.0
+    assembly_seconds: float = 0.0
+    total_seconds: float = 0.0
+    per_batch: list[BatchTrace] = field(default_factory=list)
+    # device-side timings (CUDA events): whole pipeline and the K1 launches
+    device_seconds: float = 0.0
+    pair_kernel_seconds: float = 0.0
+
+    def wasteful_fraction(self) -> float:
+        if self.interactions_computed == 0:
+            return 0.0
+        return (self.temporal_misses + self.spatial_misses) / self.interactions_computed
+
+
+def resolve_workers(workers: int | None) -> int:
+    """Explicit worker count or machine parallelism (engine.py:69-75)."""
+    if workers is None:
+        return max(1, os.cpu_count() or 1)
+    if workers < 1:
+        raise DomainError(f"workers={workers} must be >= 1")
+    return workers
+
+
+def _result_set(res: _native.Result) -> ResultSet:
+    c = res.cols
+    return ResultSet(c["query_traj"], c["query_seg"], c["entry_traj"], c["entry_seg"],
+                     c["t_begin"], c["t_end"])
+
+
+def execute_batch(store: SegmentStore, batch: SegmentStore, span: tuple[int, int], d: float, *,
+                  workers: int | None = None, _noop: bool = False
+                  ) -> tuple[ResultSet, SearchStats]:
+    """Evaluate one query batch against candidate ordinals span[0]..span[1]."""
+    t_start = time.perf_counter()
+    resolve_workers(workers)
+    first, last = int(span[0]), int(span[1])
+    if not (0 <= first <= last < len(store)):
+        raise DomainError(f"candidate span {span} outside store of {len(store)} segments")
+    if len(batch) == 0:
+        raise DomainError("query batch is empty")
+    flags = _native.TSK_SPANS_GIVEN | _native.TSK_ORDER_REFERENCE
+    if _noop:
+        flags |= _native.TSK_NOOP
+    res = _native.search(store.device(), batch, [0], [len(batch) - 1], [first], [last], d, flags)
+    stats = SearchStats()
+    if not _noop:
+        ints = (last - first + 1) * len(batch)
+        ovl = int(res.per_batch[0, 2])
+        stats.interactions_computed = ints
+        stats.hits = res.n
+        stats.temporal_misses = ints - ovl
+        stats.spatial_misses = ovl - res.n
+    result = _result_set(res) if res.n else ResultSet.empty()
+    stats.device_seconds = res.device_ms / 1e3
+    stats.pair_kernel_seconds = res.k1_ms / 1e3
+    stats.kernel_seconds = stats.total_seconds = time.perf_counter() - t_start
+    return result, stats
+
+
+def run_search(store: SegmentStore, index: TemporalIndex, plan: BatchPlan, d: float, *,
+               workers: int | None = None) -> tuple[ResultSet, SearchStats]:
+    """Execute every batch of ``plan`` against ``store`` on the GPU."""
+    t_start = time.perf_counter()
+    resolve_workers(workers)
+    queries = plan.queries
+    lo, hi = plan.table()
+    dev = index.ensure_device() if index._store is store else _bind_index(store, index)
+    res = _native.search(dev, queries, lo, hi, None, None, d, _native.TSK_ORDER_REFERENCE)
+    t_asm = time.perf_counter()
+    result = _result_set(res) if res.n else ResultSet.empty()
+    stats = SearchStats()
+    pb = res.per_batch
+    sizes = hi - lo + 1
+    cands = np.where(pb[:, 0] >= 0, pb[:, 1] - pb[:, 0] + 1, 0)
+    ints = sizes * cands
+    total_ints = int(ints.sum())
+    dev_s = res.device_ms / 1e3
+    share = ints / total_ints if total_ints else np.zeros_like(ints, dtype=np.float64)
+    stats.per_batch = [
+        BatchTrace(k, int(s), int(c), int(i), int(h), float(f * dev_s))
+        for k, (s, c, i, h, f) in enumerate(zip(sizes.tolist(), cands.tolist(), ints.tolist(),
+                                                pb[:, 3].tolist(), share.tolist()))
+    ]
+    ovl = int(pb[:, 2].sum())
+    stats.interactions_computed = total_ints
+    stats.hits = res.n
+    stats.temporal_misses = total_ints - ovl
+    stats.spatial_misses = ovl - res.n
+    stats.kernel_seconds = dev_s
+    stats.device_seconds = dev_s
+    stats.pair_kernel_seconds = res.k1_ms / 1e3
+    t_end = time.perf_counter()
+    stats.assembly_seconds = t_end - t_asm
+    stats.total_seconds = t_end - t_start
+    stats.overhead_seconds = max(0.0, stats.total_seconds - stats.kernel_seconds - stats.assembly_seconds)
+    return result, stats
+
+
+def _bind_index(store: SegmentStore, index: TemporalIndex):
+    """Device copy of ``store`` carrying an index with ``index``'s parameters."""
+    from .index import _rule_code
+
+    dev = store.device()
+    if dev.index_token is not index:
+        _native.index_build(dev, index.m, _rule_code(index.extent_rule))
+        dev.index_token = index
+    return dev
+
+
+def launch_overhead_pass(store: SegmentStore, batch: SegmentStore, span: tuple[int, int], *,
+                         workers: int | None = None) -> float:
+    """Wall seconds of a batch launch with the pair arithmetic elided."""
+    _, stats = execute_batch(store, batch, span, 0.0, workers=workers, _noop=True)
+    return stats.kernel_seconds
