@@ -331,7 +331,7 @@ void launch_ranges(tsk_db *db, const Soa &q, SearchPlanDev &p, bool spans_given,
 
 // Single block: choose the candidate sub-tile count so the grid gets at
 // least ~4 waves of items, then scan items per batch.
-__global__ void k_plan_items(int64_t nb, const int64_t *__restrict__ lo, const int64_t *__restrict__ hi,
+__global__ void __launch_bounds__(1024, 1) k_plan_items(int64_t nb, const int64_t *__restrict__ lo, const int64_t *__restrict__ hi,
                              const int64_t *__restrict__ first, const int64_t *__restrict__ last,
                              int64_t *__restrict__ item_off, int64_t *__restrict__ meta,
                              int64_t slots) {
