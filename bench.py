@@ -1,0 +1,489 @@
+"""Benchmark: distance-threshold search throughput (segment-pair evals/s) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
+
+A step is one pass of the hot path over the workload's batch plan:
+  * value — device throughput with the queries resident in HBM and hits left
+    in HBM: Σ interactions ÷ CUDA-event time of the search pipeline
+    (K3 ranges → K1 pair kernel → K4 sort/gather), max over ranks.
+  * e2e — the same metric through the public drop-in call
+    ``run_search(store, index, plan, d)`` with pinned host query columns:
+    H2D of the queries and D2H of the ResultSet inside the timed region
+    (the reference's "response time"; DB resident).
+The entry store is replicated on every GPU and the batch plan is sharded
+into contiguous, interaction-balanced slices (no collective on the data
+path; NCCL only carries the timing max).
+
+--impl reference times the reference's CPU algorithm (the numpy port in
+oracle/ — the reference is pure Python + numpy and cannot travel to the
+GPU box) on sampled batches of the same workload on all host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "distance-threshold query response time; segment-pair evals/s @1/2/4/8 B200"
+UNIT = "pair-evals/s"
+
+# Workloads of BASELINE.json "configs".  Entries / query pool:
+# (profile kind, trajectories, seed, timesteps) through the reference datagen stream.
+CONFIGS = {
+    "c1": dict(desc="RandWalk-Uniform 1,000x100 (99,000 entries), 100 query trajectories "
+                    "(9,900 query segments), d=5, Periodic s=120, m=10,000",
+               entries=("uniform", 1000, 1, 100), pool=("uniform", 1000, 2, 100), sample=(100, 3),
+               d=5.0),
+    "c2": dict(desc="Galaxy-shaped star orbits 2,500x401 (1,000,000 entries), 100 orbit "
+                    "trajectories (40,000 query segments), d=0.5, Periodic s=120, m=10,000",
+               galaxy=(2500, 11), galaxy_pool=(400, 12), sample=(100, 13), d=0.5),
+    "c3": dict(desc="RandWalk-Normal 25,000x401 (1e7 entries), 100 query trajectories "
+                    "(40,000 query segments), d=5, Periodic s=120, m=10,000",
+               entries=("normal", 25000, 5, 401), pool=("normal", 1000, 6, 401), sample=(100, 7),
+               d=5.0),
+    "c4": dict(desc="RandWalk-Exp 140,000 trajectories (~1e7 entries), 1,000 query trajectories, "
+                    "d=5, Periodic s=120, m=10,000",
+               entries=("exp", 140000, 8, None), pool=("exp", 14000, 9, None), sample=(1000, 10),
+               d=5.0),
+    "c5": dict(desc="RandWalk-Uniform 250,000x401 (1e8 entries), 1,000 query trajectories "
+                    "(400,000 query segments), d=1, Periodic s=120, m=10,000",
+               entries=("uniform", 250000, 21, 401), pool=("uniform", 1000, 22, 401), sample=None,
+               d=1.0),
+}
+S_BATCH = 120
+M_BINS = 10_000
+W_DECIDE, W_HIT = 50, 9  # FP64 flops per overlapping pair / extra per hit
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ── workload construction ───────────────────────────────────────────────────
+
+
+def workload_columns(cfg):
+    """(entries, queries) as unsorted column dicts — identical on every rank/arm."""
+    from paper_1405_7461_b200 import datagen
+
+    if "galaxy" in cfg:
+        e = datagen.galaxy(*cfg["galaxy"])
+        pool = datagen.galaxy(*cfg["galaxy_pool"])
+        q = datagen.sample_queries(pool, *cfg["sample"])
+        cols = lambda s: {k: getattr(s, k) for k in ("traj", "seg", "xs", "ys", "zs", "ts", "xe", "ye", "ze", "te")}  # noqa: E731
+        return cols(e), cols(q)
+
+    def prof(spec):
+        kind, n, seed, steps = spec
+        kw = {} if steps is None else {"timesteps": steps}
+        return datagen.make_profile(kind, n, seed=seed, **kw)
+
+    e = datagen.generate_columns(prof(cfg["entries"]))
+    p = datagen.generate_columns(prof(cfg["pool"]))
+    if cfg["sample"] is not None:
+        n, seed = cfg["sample"]
+        ids = np.unique(p["traj"])
+        pick = np.random.default_rng(seed).choice(ids, size=n, replace=False)
+        keep = np.isin(p["traj"], pick)
+        p = {k: v[keep] for k, v in p.items()}
+    return e, p
+
+
+FIELDS = ("traj", "seg", "xs", "ys", "zs", "ts", "xe", "ye", "ze", "te")
+
+
+def shard_bounds(ints: np.ndarray, world: int) -> list[tuple[int, int]]:
+    """Contiguous batch shards [b0, b1) with balanced Σ interactions."""
+    nb = ints.shape[0]
+    cum = np.concatenate([[0], np.cumsum(ints, dtype=np.float64)])
+    total = cum[-1]
+    cuts = [0]
+    for r in range(1, world):
+        target = total * r / world
+        cuts.append(int(np.searchsorted(cum, target, side="left")))
+    cuts.append(nb)
+    cuts = [min(max(c, 0), nb) for c in cuts]
+    for i in range(1, len(cuts)):
+        cuts[i] = max(cuts[i], cuts[i - 1])
+    return [(cuts[r], cuts[r + 1]) for r in range(world)]
+
+
+def sub_plan(plan, b0: int, b1: int):
+    """The batches [b0, b1) of ``plan`` over a view of their queries."""
+    import paper_1405_7461_b200 as tsk
+
+    if b1 <= b0:
+        return None
+    bs = plan.batches[b0:b1]
+    lo0, hi1 = bs[0].lo, bs[-1].hi
+    view = plan.queries.view(lo0, hi1)
+    rebased = tuple(tsk.QueryBatch(b.lo - lo0, b.hi - lo0, b.extent, b.first, b.last) for b in bs)
+    return tsk.BatchPlan(view, rebased)
+
+
+# ── clocks ──────────────────────────────────────────────────────────────────
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = os.path.join("/tmp", f"tsk_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        loaded = [s for s in sm if s > 0.5 * (max(sm) if sm else 1)]
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows),
+                "power_w_max": max((float(r[3]) for r in rows if _isnum(r[3])), default=None)}
+
+
+def _isnum(s):
+    try:
+        float(s)
+        return True
+    except ValueError:
+        return False
+
+
+# ── CPU side (reference arm / cpu_baseline): the oracle port ───────────────
+
+
+def cpu_setup(e_cols, q_cols, presorted=False):
+    """Oracle store/index/plan for the reference algorithm (numpy port) plus an
+    evenly spread batch order for sampling."""
+    from oracle import oracle as orc
+
+    t0 = time.perf_counter()
+    e = orc.make_store(*(e_cols[k] for k in FIELDS), presorted=presorted)
+    q = orc.make_store(*(q_cols[k] for k in FIELDS), presorted=presorted)
+    ix = orc.index_build(e, M_BINS)
+    plan = orc.plan_periodic(q, S_BATCH, ix)
+    log(f"[cpu] oracle store/index/plan in {time.perf_counter() - t0:.1f}s, {len(plan)} batches")
+    order = _spread(len(plan))
+    return e, q, ix, plan, order
+
+
+def _spread(n):
+    """Deterministic batch order that samples the plan evenly (0, n/2, n/4, 3n/4, ...)."""
+    seen, out = set(), []
+    step = n
+    while step >= 1 and len(out) < n:
+        for k in range(0, n, step):
+            if k not in seen:
+                seen.add(k)
+                out.append(k)
+        step //= 2
+    return out + [k for k in range(n) if k not in seen]
+
+
+def time_cpu_batches(e, q, ix, plan, d, batch_ids, workers):
+    from oracle import oracle as orc
+
+    t0 = time.perf_counter()
+    _, st = orc.search(e, ix, q, plan, d, workers=workers, batch_ids=batch_ids)
+    return st["interactions"], time.perf_counter() - t0, st["hits"]
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    workers = os.cpu_count() or 1
+    e_cols, q_cols = workload_columns(cfg)
+    e, q, ix, plan, order = cpu_setup(e_cols, q_cols)
+    # one step = a bounded sample of batches (~budget seconds of CPU work)
+    budget = float(os.environ.get("TSK_REF_STEP_S", "8"))
+    cursor = 0
+    step_ints, step_secs, step_batches = [], [], []
+
+    def one_step():
+        nonlocal cursor
+        ints = secs = 0.0
+        ids = []
+        while secs < budget and len(ids) < len(order):
+            k = order[cursor % len(order)]
+            cursor += 1
+            i, s, _ = time_cpu_batches(e, q, ix, plan, cfg["d"], [k], workers)
+            ints += i
+            secs += s
+            ids.append(k)
+        return ints, secs, ids
+
+    for _ in range(args.warmup):
+        one_step()
+    for _ in range(args.steps):
+        i, s, ids = one_step()
+        step_ints.append(i)
+        step_secs.append(s)
+        step_batches.append(len(ids))
+    value = sum(step_ints) / sum(step_secs)
+    sample = (f"{sum(step_batches)} batch evaluations (of {len(plan)} Periodic s={S_BATCH} batches) over {args.steps} steps "
+              f"(evenly spread), {int(sum(step_ints))} interactions")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(step_secs) / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {cfg['desc']}", "parallelism": "host threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ── GPU side (our arm) ──────────────────────────────────────────────────────
+
+
+def run_ours(args, cfg):
+    import paper_1405_7461_b200 as tsk
+    from paper_1405_7461_b200 import _native
+    from paper_1405_7461_b200.engine import search_device
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = tdist
+    tsk.set_device(local)
+    d = cfg["d"] if args.d is None else args.d
+
+    t0 = time.perf_counter()
+    e_cols, q_cols = workload_columns(cfg)
+    store = tsk.SegmentStore(*(e_cols[k] for k in FIELDS), validate=False)
+    queries = tsk.SegmentStore(*(q_cols[k] for k in FIELDS), validate=False)
+    t_gen = time.perf_counter() - t0
+    index = tsk.build_index(store, M_BINS)
+    plan = tsk.periodic(queries, S_BATCH, index)
+    t_setup = time.perf_counter() - t0
+    ints_all = np.array([b.interactions for b in plan.batches], dtype=np.int64)
+    b0, b1 = shard_bounds(ints_all, world)[rank]
+    mine = sub_plan(plan, b0, b1)
+    log(f"[rank {rank}] {len(store)} entries, {len(queries)} queries, {len(plan.batches)} batches; "
+        f"shard [{b0},{b1}); setup {t_setup:.1f}s (gen {t_gen:.1f}s)")
+
+    # pinned host copy of this rank's query columns for the e2e leg
+    if mine is not None:
+        pq = tsk.SegmentStore(*(_native.pinned_copy(np.ascontiguousarray(getattr(mine.queries, k)))
+                                for k in FIELDS), validate=False, presorted=True)
+        e2e_plan = tsk.BatchPlan(pq, mine.batches)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def allmax(x: float) -> float:
+        if dist is None:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(x: float) -> float:
+        if dist is None:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    fp64 = _native.probe_fp64(local)
+    fp64_peak = max(fp64.values())
+
+    # ── value: queries resident in HBM, hits left in HBM ──
+    res = None
+    if mine is not None:
+        res = search_device(store, index, mine, d)  # uploads the queries once
+    for _ in range(args.warmup):
+        if mine is not None:
+            res = search_device(store, index, mine, d, queries_resident=True)
+    barrier()
+    dev_ms, k1_ms, launches, work, hits, ovl = 0.0, 0.0, 0, 0.0, 0, 0
+    with ClockSampler(local) as clk:
+        w0 = time.perf_counter()
+        for _ in range(args.steps):
+            if mine is None:
+                continue
+            r = search_device(store, index, mine, d, queries_resident=True)
+            dev_ms += r.device_ms
+            k1_ms += r.k1_ms
+            launches += r.launches
+            o = int(r.per_batch[:, 2].sum())
+            ovl += o
+            hits += r.n
+            work += W_DECIDE * o + W_HIT * r.n
+        wall_s = time.perf_counter() - w0
+    barrier()
+    my_ints = int(ints_all[b0:b1].sum())
+    t_dev = allmax(dev_ms / 1e3)
+    total_ints = allsum(float(my_ints)) * args.steps
+    value = total_ints / t_dev if t_dev > 0 else 0.0
+
+    # ── e2e: public drop-in call, pinned host inputs, results to host ──
+    for _ in range(max(1, args.warmup // 2)):
+        if mine is not None:
+            tsk.run_search(store, index, e2e_plan, d)
+    barrier()
+    e2e_s, h2d, d2h, e2e_hits = 0.0, 0, 0, 0
+    for _ in range(args.steps):
+        if mine is None:
+            continue
+        t1 = time.perf_counter()
+        rs, st = tsk.run_search(store, index, e2e_plan, d)
+        e2e_s += time.perf_counter() - t1
+        h2d += len(pq) * (2 * 8 + 8 * 8) + len(mine.batches) * 16
+        d2h += len(rs) * 48 + len(mine.batches) * 32
+        e2e_hits += len(rs)
+        assert st.interactions_computed == my_ints
+    t_e2e = allmax(e2e_s)
+    e2e_value = total_ints / t_e2e if t_e2e > 0 else 0.0
+
+    # roofline of the dominant kernel (K1), this rank
+    k1_s = k1_ms / 1e3
+    achieved = work / k1_s / 1e12 if k1_s > 0 else 0.0
+    peak = fp64_peak / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    if os.path.exists(prof):
+        try:
+            tj = json.load(open(prof))
+            if tj.get("config") == args.config:
+                traffic = tj.get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            pass
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        workers = os.cpu_count() or 1
+        sorted_cols = lambda s: {k: getattr(s, k) for k in FIELDS}  # noqa: E731
+        e, q, ix, oplan, order = cpu_setup(sorted_cols(store), sorted_cols(queries), presorted=True)
+        ints = secs = 0.0
+        nbat = 0
+        budget = float(os.environ.get("TSK_CPU_BASELINE_S", "20"))
+        for k in order:
+            i, s, _ = time_cpu_batches(e, q, ix, oplan, d, [k], workers)
+            ints += i
+            secs += s
+            nbat += 1
+            if secs >= budget:
+                break
+        cpu = {"value": ints / secs, "unit": UNIT, "cores": workers, "kind": "port",
+               "sample": f"{nbat} of {len(oplan)} batches (evenly spread), {int(ints)} interactions, "
+                         f"{secs:.1f}s; numpy port of the reference algorithm, workers={workers}"}
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t_dev / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference datagen stream; entry DB resident, replicated per GPU)",
+            "config": {
+                "workload": f"{args.config}: {cfg['desc']}", "entries": len(store),
+                "queries": len(queries), "batches": len(plan.batches), "d": d, "s": S_BATCH,
+                "m": M_BINS, "interactions_per_step": int(total_ints / args.steps),
+                "hits_per_step": int(allsum(float(hits)) / args.steps),
+                "l2": "inputs larger than L2 (entry SoA 112 B/segment resident in HBM)",
+                "parallelism": f"dp{world} (contiguous interaction-balanced batch shards; no collective)",
+            },
+            "response_time_s": t_e2e / args.steps,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d / args.steps),
+                    "d2h_bytes_per_step": int(d2h / args.steps),
+                    "call": "paper_1405_7461_b200.run_search(store, index, plan, d) (pinned host queries)"},
+            "roofline": {
+                "bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak if peak else None, "traffic": traffic,
+                "kernel": "k1_pairs", "work": f"{W_DECIDE}*overlapping pairs + {W_HIT}*hits FP64 flops",
+                "k1_ms_per_step": k1_ms / args.steps,
+                "peak_source": "tsk_probe_fp64 on this GPU in this run (DADD/DMUL/DFMA ops/s); "
+                               "MEASURED_PEAKS.json has no FP64 figure",
+                "hbm_bytes_per_step": None,
+            },
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+            "gpu_launches": launches,
+            "wall_s_value_steps": wall_s,
+            "setup_s": t_setup,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c5")
+    ap.add_argument("--d", type=float, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -115,6 +115,10 @@ int tsk_result_columns(const tsk_result *r, const int64_t **query_traj, const in
                        const int64_t **entry_ord);
 void tsk_result_free(tsk_result *r);
 
+/* Page-locked host memory for query/result staging (cudaHostAlloc). */
+void *tsk_pinned_alloc(int64_t bytes);
+void tsk_pinned_free(void *p);
+
 /* Measured FP64 pipe rate of `device` (DADD/DMUL per second, each counted
  * as one op; DFMA counted as one op too) — the roofline denominator of the
  * FP64-bound pair kernel. */

@@ -61,6 +61,8 @@ SIGNATURES = {
     "tsk_result_columns": ([_P] + [ctypes.POINTER(_P)] * 8, ctypes.c_int),
     "tsk_result_free": ([_P], None),
     "tsk_probe_fp64": ([ctypes.c_int, _PD, _PD, _PD], ctypes.c_int),
+    "tsk_pinned_alloc": ([_I64], _P),
+    "tsk_pinned_free": ([_P], None),
 }
 
 _lib = None
@@ -288,3 +290,32 @@ def probe_fp64(device: int | None = None) -> dict:
     dev = current_device() if device is None else int(device)
     check(lib.tsk_probe_fp64(dev, ctypes.byref(a), ctypes.byref(m), ctypes.byref(f)))
     return {"dadd_per_s": a.value, "dmul_per_s": m.value, "dfma_per_s": f.value}
+
+
+class _Pinned:
+    def __init__(self, ptr):
+        self.ptr = ptr
+
+    def __del__(self):
+        if self.ptr and _lib is not None:
+            _lib.tsk_pinned_free(self.ptr)
+            self.ptr = None
+
+
+def pinned_empty(n: int, dtype) -> np.ndarray:
+    """A numpy array in page-locked host memory (freed with the array)."""
+    dt = np.dtype(dtype)
+    nbytes = max(1, n) * dt.itemsize
+    ptr = load().tsk_pinned_alloc(nbytes)
+    if not ptr:
+        raise MemoryError("tsk_pinned_alloc failed")
+    owner = _Pinned(ptr)
+    buf = (ctypes.c_char * nbytes).from_address(ptr)
+    buf._owner = owner
+    return np.frombuffer(buf, dtype=dt)[:n]
+
+
+def pinned_copy(a: np.ndarray) -> np.ndarray:
+    out = pinned_empty(a.shape[0], a.dtype)
+    out[...] = a
+    return out

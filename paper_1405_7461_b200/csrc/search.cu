@@ -430,3 +430,18 @@ extern "C" void tsk_result_free(tsk_result *r) {
     pin_free(r->host, r->host_bytes);
     delete r;
 }
+
+extern "C" void *tsk_pinned_alloc(int64_t bytes) {
+    void *p = nullptr;
+    if (bytes <= 0) bytes = 64;
+    if (cudaHostAlloc(&p, (size_t)bytes, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("cudaHostAlloc failed");
+        return nullptr;
+    }
+    return p;
+}
+
+extern "C" void tsk_pinned_free(void *p) {
+    if (p) cudaFreeHost(p);
+}

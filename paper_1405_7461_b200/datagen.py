@@ -112,6 +112,13 @@ def _lengths(p: GenProfile, rng) -> np.ndarray:
 
 def generate(profile: GenProfile) -> SegmentStore:
     """Random-walk store for ``profile`` (datagen.py:206-245), sorted by start."""
+    c = generate_columns(profile)
+    return SegmentStore(*(c[k] for k in ("traj", "seg", "xs", "ys", "zs", "ts", "xe", "ye", "ze", "te")),
+                        validate=False)
+
+
+def generate_columns(profile: GenProfile) -> dict:
+    """The unsorted columns of :func:`generate` (trajectory-major order)."""
     rng = np.random.default_rng(profile.seed)
     starts = _starts(profile, rng)
     pts = _lengths(profile, rng)
@@ -133,8 +140,9 @@ def generate(profile: GenProfile) -> SegmentStore:
         for ax, (s, e) in enumerate((("xs", "xe"), ("ys", "ye"), ("zs", "ze"))):
             cols[s][a:b] = walk[:-1, ax]
             cols[e][a:b] = walk[1:, ax]
-    return SegmentStore(traj, seg, cols["xs"], cols["ys"], cols["zs"], cols["ts"],
-                        cols["xe"], cols["ye"], cols["ze"], cols["te"], validate=False)
+    cols["traj"] = traj
+    cols["seg"] = seg
+    return cols
 
 
 def sample_queries(source: SegmentStore, num_traj: int, seed: int) -> SegmentStore:

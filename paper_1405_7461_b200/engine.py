@@ -152,6 +152,23 @@ def run_search(store: SegmentStore, index: TemporalIndex, plan: BatchPlan, d: fl
     return result, stats
 
 
+def search_device(store: SegmentStore, index: TemporalIndex, plan: BatchPlan, d: float, *,
+                  queries_resident: bool = False) -> _native.Result:
+    """Plan execution with hits left in HBM (no D2H of result columns).
+
+    With ``queries_resident`` the query set uploaded by the previous call on
+    this store's device copy is reused (no H2D).  Used to time the device
+    throughput with inputs resident in HBM; returns the raw result (counts,
+    per-batch stats, CUDA-event timings).
+    """
+    lo, hi = plan.table()
+    dev = index.ensure_device() if index._store is store else _bind_index(store, index)
+    flags = _native.TSK_ORDER_REFERENCE | _native.TSK_RESULTS_ON_DEVICE
+    if queries_resident:
+        flags |= _native.TSK_QUERIES_RESIDENT
+    return _native.search(dev, plan.queries, lo, hi, None, None, d, flags)
+
+
 def _bind_index(store: SegmentStore, index: TemporalIndex):
     """Device copy of ``store`` carrying an index with ``index``'s parameters."""
     from .index import _rule_code
