@@ -13,7 +13,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libtrajseek.so")
+LIB_PATH = os.environ.get("TRAJSEEK_LIB") or os.path.join(_HERE, "_lib", "libtrajseek.so")
 
 TSK_OK, TSK_EINVAL, TSK_ECUDA, TSK_ENOMEM, TSK_ENODEV = 0, 1, 2, 3, 4
 TSK_NOOP = 1 << 0

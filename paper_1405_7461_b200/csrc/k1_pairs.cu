@@ -135,97 +135,107 @@ __device__ __forceinline__ uint64_t make_key(const K1Launch &L, int64_t b, int64
     return ((uint64_t)b << (L.major_bits + L.minor_bits)) | (major << L.minor_bits) | minor;
 }
 
-// One warp, one candidate per lane, all staged queries in [jlo, jhi).
-template <bool SLOW>
-__device__ void warp_pairs(const K1Launch &L, const QRec *sq, int jlo, int jhi, const Cand &r,
-                           bool valid, int64_t e_off, const ItemCtx &it, int lane,
-                           unsigned &n_ov, unsigned &n_hit) {
-    const unsigned FULL = 0xffffffffu;
+// Clip-at-ta cases of a query against a warp's 32 candidates.  Queries in a
+// tile are sorted by start time, so each case is a contiguous j range:
+//   TA_C    cts <  every lane's ts: the query started first, interpolate it
+//   TA_R    cts >  every lane's ts: the entry started first, interpolate it
+//   TA_BOTH otherwise: interpolate both (the later starter's f is 0 -> exact)
+enum { TA_C = 0, TA_R = 1, TA_BOTH = 2 };
+
+// Flat (zero-length shared span) pairs and quadratic-root candidates:
+// exact recomputation with every verbatim rule of the reference.
+__device__ __forceinline__ Hit rare_pair(const Cand &r, const QRec &Q, double cc, double aa, double dot,
+                                         double e, double d2) {
+    const double ta = r.ts > Q.ts ? r.ts : Q.ts;
+    const double tb = r.te < Q.te ? r.te : Q.te;
+    if (ta == tb) {
+        // positions at the shared instant, constant separation (core.py:376-378)
+        double rx, ry, rz, qx, qy, qz;
+        position_exact(ta, r.ts, r.te, r.sx, r.sy, r.sz, r.ex, r.ey, r.ez, r.dx, r.dy, r.dz, rx, ry, rz);
+        position_exact(ta, Q.ts, Q.te, Q.sx, Q.sy, Q.sz, Q.ex, Q.ey, Q.ez, Q.dx, Q.dy, Q.dz, qx, qy, qz);
+        const double ux = __dsub_rn(rx, qx), uy = __dsub_rn(ry, qy), uz = __dsub_rn(rz, qz);
+        const double c2 = __dadd_rn(__dadd_rn(__dmul_rn(ux, ux), __dmul_rn(uy, uy)), __dmul_rn(uz, uz));
+        Hit h;
+        h.hit = c2 <= d2;
+        h.tb = ta;
+        h.te = tb;
+        return h;
+    }
+    return solve_exact(ta, tb, cc, aa, dot, e, d2);
+}
+
+// Clip-at-tb cases; TB_R / TB_C are proven for a whole j range from the
+// tile's running max / suffix min of query end times, TB_DYN decides per query.
+enum { TB_R = 0, TB_C = 1, TB_DYN = 2 };
+
+// One warp, one candidate per lane, staged queries j0..j1-1 of one (TA, TB) case.
+template <int TA, int TB, bool SLOW>
+__device__ __forceinline__ void pair_run(const K1Launch &L, const QRec *__restrict__ sq, int j0, int j1,
+                                         const Cand &r, bool valid, double wmin_te, double wmax_te,
+                                         uint64_t key_base, int lane, unsigned &n_ov,
+                                         unsigned &n_hit) {
     const double d2 = L.d2;
-    for (int j = jlo; j < jhi; ++j) {
+    for (int j = j0; j < j1; ++j) {
         const QRec &Q = sq[j];
         const double cts = Q.ts, cte = Q.te;
-        const double ta = fmax(r.ts, cts);
-        const double tb = fmin(r.te, cte);
-        const bool ov = valid && ta <= tb;
-        const unsigned mov = __ballot_sync(FULL, ov);
-        if (!mov) continue;
+        const bool ov = r.ts <= cte && cts <= r.te;  // invalid lanes: ts = +inf
         n_ov += ov ? 1u : 0u;
-        const bool flat = ov && ta == tb;
-        const unsigned mflat = __ballot_sync(FULL, flat);
-        const unsigned act = mov & ~mflat;
-        bool cand = false;
-        double cc = 0, aa = 0, dot = 0, e = 0;
-        if (act) {
-            const double csx = Q.sx, csy = Q.sy, csz = Q.sz, cext = Q.ext;
-            const double cdx = Q.dx, cdy = Q.dy, cdz = Q.dz, crcp = Q.rcp;
-            double rax, ray, raz, cax, cay, caz, rbx, rby, rbz, cbx, cby, cbz;
-            // ── clip at ta: interpolate the earlier starter ──
-            const unsigned mlr = __ballot_sync(FULL, r.ts < cts) & act;
-            if (mlr == act) {
-                lerp<SLOW>(ta, r.ts, r.ext, r.rcp, r.sx, r.sy, r.sz, r.dx, r.dy, r.dz, rax, ray, raz);
-                cax = csx; cay = csy; caz = csz;
-            } else if (mlr == 0) {
-                rax = r.sx; ray = r.sy; raz = r.sz;
-                lerp<SLOW>(ta, cts, cext, crcp, csx, csy, csz, cdx, cdy, cdz, cax, cay, caz);
-            } else {  // f == 0 for the later starter: both interpolations are exact
-                lerp<SLOW>(ta, r.ts, r.ext, r.rcp, r.sx, r.sy, r.sz, r.dx, r.dy, r.dz, rax, ray, raz);
-                lerp<SLOW>(ta, cts, cext, crcp, csx, csy, csz, cdx, cdy, cdz, cax, cay, caz);
-            }
-            // ── clip at tb: interpolate the later ender ──
+        const double csx = Q.sx, csy = Q.sy, csz = Q.sz;
+        // ── clip at ta (core.py:503-516) ──
+        double ta, rax, ray, raz, cax, cay, caz;
+        if (TA == TA_R) {
+            ta = cts;
+            lerp<SLOW>(cts, r.ts, r.ext, r.rcp, r.sx, r.sy, r.sz, r.dx, r.dy, r.dz, rax, ray, raz);
+            cax = csx; cay = csy; caz = csz;
+        } else if (TA == TA_C) {
+            ta = r.ts;
+            rax = r.sx; ray = r.sy; raz = r.sz;
+            lerp<SLOW>(r.ts, cts, Q.ext, Q.rcp, csx, csy, csz, Q.dx, Q.dy, Q.dz, cax, cay, caz);
+        } else {
+            ta = r.ts > cts ? r.ts : cts;
+            lerp<SLOW>(ta, r.ts, r.ext, r.rcp, r.sx, r.sy, r.sz, r.dx, r.dy, r.dz, rax, ray, raz);
+            lerp<SLOW>(ta, cts, Q.ext, Q.rcp, csx, csy, csz, Q.dx, Q.dy, Q.dz, cax, cay, caz);
+        }
+        // ── clip at tb: interpolate the later ender (warp-uniform test) ──
+        double tb, rbx, rby, rbz, cbx, cby, cbz;
+        if (TB == TB_R || (TB == TB_DYN && cte < wmin_te)) {  // every candidate ends after the query
+            tb = cte;
+            lerp<SLOW>(cte, r.ts, r.ext, r.rcp, r.sx, r.sy, r.sz, r.dx, r.dy, r.dz, rbx, rby, rbz);
+            cbx = Q.ex; cby = Q.ey; cbz = Q.ez;
+        } else if (TB == TB_C || (TB == TB_DYN && cte > wmax_te)) {  // the query ends after every candidate
+            tb = r.te;
+            rbx = r.ex; rby = r.ey; rbz = r.ez;
+            lerp<SLOW>(r.te, cts, Q.ext, Q.rcp, csx, csy, csz, Q.dx, Q.dy, Q.dz, cbx, cby, cbz);
+        } else {
+            tb = r.te < cte ? r.te : cte;
+            double px, py, pz, qx, qy, qz;
+            lerp<SLOW>(tb, r.ts, r.ext, r.rcp, r.sx, r.sy, r.sz, r.dx, r.dy, r.dz, px, py, pz);
+            lerp<SLOW>(tb, cts, Q.ext, Q.rcp, csx, csy, csz, Q.dx, Q.dy, Q.dz, qx, qy, qz);
             const bool zr = r.te > cte, zc = cte > r.te;
-            const unsigned mzr = __ballot_sync(FULL, zr) & act;
-            const unsigned mzc = __ballot_sync(FULL, zc) & act;
-            if (mzr == act) {
-                lerp<SLOW>(tb, r.ts, r.ext, r.rcp, r.sx, r.sy, r.sz, r.dx, r.dy, r.dz, rbx, rby, rbz);
-                cbx = Q.ex; cby = Q.ey; cbz = Q.ez;
-            } else if (mzc == act) {
-                rbx = r.ex; rby = r.ey; rbz = r.ez;
-                lerp<SLOW>(tb, cts, cext, crcp, csx, csy, csz, cdx, cdy, cdz, cbx, cby, cbz);
-            } else {
-                double px, py, pz, qx, qy, qz;
-                lerp<SLOW>(tb, r.ts, r.ext, r.rcp, r.sx, r.sy, r.sz, r.dx, r.dy, r.dz, px, py, pz);
-                lerp<SLOW>(tb, cts, cext, crcp, csx, csy, csz, cdx, cdy, cdz, qx, qy, qz);
-                rbx = zr ? px : r.ex; rby = zr ? py : r.ey; rbz = zr ? pz : r.ez;
-                cbx = zc ? qx : Q.ex; cby = zc ? qy : Q.ey; cbz = zc ? qz : Q.ez;
-            }
-            // ── quadratic coefficients (core.py:523-537) ──
-            const double ux = __dsub_rn(rax, cax), uy = __dsub_rn(ray, cay), uz = __dsub_rn(raz, caz);
-            cc = __dadd_rn(__dadd_rn(__dmul_rn(ux, ux), __dmul_rn(uy, uy)), __dmul_rn(uz, uz));
-            const double wx = __dsub_rn(__dsub_rn(rbx, rax), __dsub_rn(cbx, cax));
-            const double wy = __dsub_rn(__dsub_rn(rby, ray), __dsub_rn(cby, cay));
-            const double wz = __dsub_rn(__dsub_rn(rbz, raz), __dsub_rn(cbz, caz));
-            aa = __dadd_rn(__dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy)), __dmul_rn(wz, wz));
-            dot = __dadd_rn(__dadd_rn(__dmul_rn(ux, wx), __dmul_rn(uy, wy)), __dmul_rn(uz, wz));
-            e = __dsub_rn(cc, d2);
-            // disc / 4; a margin keeps the test a superset under underflow
-            const double dq = __dsub_rn(__dmul_rn(dot, dot), __dmul_rn(aa, e));
-            cand = ((act >> lane) & 1u) && dq >= -0x1p-1000;
+            rbx = zr ? px : r.ex; rby = zr ? py : r.ey; rbz = zr ? pz : r.ez;
+            cbx = zc ? qx : Q.ex; cby = zc ? qy : Q.ey; cbz = zc ? qz : Q.ez;
         }
-        const unsigned mwork = __ballot_sync(FULL, cand) | mflat;
-        if (!mwork) continue;
-        Hit h;
-        h.hit = false;
-        h.tb = h.te = 0.0;
-        if (cand) {
-            h = solve_exact(ta, tb, cc, aa, dot, e, d2);
-        } else if (flat) {
-            // zero-length shared span: positions at ta with every verbatim
-            // rule, constant separation over the instant (core.py:376-378)
-            double rx, ry, rz, qx, qy, qz;
-            position_exact(ta, r.ts, r.te, r.sx, r.sy, r.sz, r.ex, r.ey, r.ez, r.dx, r.dy, r.dz, rx,
-                           ry, rz);
-            position_exact(ta, cts, cte, Q.sx, Q.sy, Q.sz, Q.ex, Q.ey, Q.ez, Q.dx, Q.dy, Q.dz, qx,
-                           qy, qz);
-            const double ux = __dsub_rn(rx, qx), uy = __dsub_rn(ry, qy), uz = __dsub_rn(rz, qz);
-            const double c2 = __dadd_rn(__dadd_rn(__dmul_rn(ux, ux), __dmul_rn(uy, uy)), __dmul_rn(uz, uz));
-            h.hit = c2 <= d2;
-            h.tb = ta;
-            h.te = tb;
+        // ── quadratic coefficients (core.py:523-537) ──
+        const double ux = __dsub_rn(rax, cax), uy = __dsub_rn(ray, cay), uz = __dsub_rn(raz, caz);
+        const double cc = __dadd_rn(__dadd_rn(__dmul_rn(ux, ux), __dmul_rn(uy, uy)), __dmul_rn(uz, uz));
+        const double wx = __dsub_rn(__dsub_rn(rbx, rax), __dsub_rn(cbx, cax));
+        const double wy = __dsub_rn(__dsub_rn(rby, ray), __dsub_rn(cby, cay));
+        const double wz = __dsub_rn(__dsub_rn(rbz, raz), __dsub_rn(cbz, caz));
+        const double aa = __dadd_rn(__dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy)), __dmul_rn(wz, wz));
+        const double dot = __dadd_rn(__dadd_rn(__dmul_rn(ux, wx), __dmul_rn(uy, wy)), __dmul_rn(uz, wz));
+        const double e = __dsub_rn(cc, d2);
+        // disc / 4 (exact scaling); the margin keeps the test a superset under underflow
+        const double dq = __dsub_rn(__dmul_rn(dot, dot), __dmul_rn(aa, e));
+        const bool cand = ov && (ta == tb || dq >= -0x1p-1000);
+        if (__ballot_sync(0xffffffffu, cand)) {
+            Hit h;
+            h.hit = false;
+            h.tb = h.te = 0.0;
+            if (cand) h = rare_pair(r, Q, cc, aa, dot, e, d2);
+            n_hit += h.hit ? 1u : 0u;
+            append_hit(L, h.hit, key_base + (L.query_major ? ((uint64_t)j << L.minor_bits) : (uint64_t)j),
+                       h.tb, h.te, lane);
         }
-        n_hit += h.hit ? 1u : 0u;
-        const int64_t q_off = it.q0 + j;
-        append_hit(L, h.hit, make_key(L, it.b, e_off, q_off), h.tb, h.te, lane);
     }
 }
 
@@ -235,6 +245,16 @@ __device__ __forceinline__ int lower_bound_pm(const double *pm, int n, double v)
         int m = (a + b) >> 1;
         if (pm[m] >= v) b = m;
         else a = m + 1;
+    }
+    return a;
+}
+
+__device__ __forceinline__ int lower_bound_ts(const QRec *q, int n, double v) {
+    int a = 0, b = n;
+    while (a < b) {
+        int m = (a + b) >> 1;
+        if (q[m].ts < v) a = m + 1;
+        else b = m;
     }
     return a;
 }
@@ -249,9 +269,13 @@ __device__ __forceinline__ int upper_bound_ts(const QRec *q, int n, double v) {
     return a;
 }
 
-__global__ void __launch_bounds__(K1_THREADS, 2) k1_pairs(K1Launch L) {
+#ifndef K1_MIN_BLOCKS
+#define K1_MIN_BLOCKS 3
+#endif
+__global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L) {
     __shared__ QRec sq[K1_TQ];
-    __shared__ double pm[K1_TQ];
+    __shared__ double pm[K1_TQ];  // running max of te over the tile
+    __shared__ double sm[K1_TQ];  // suffix min of te over the tile
     __shared__ ItemCtx it_sh;
     __shared__ int64_t item_sh;
     __shared__ unsigned long long red_ov, red_hit;
@@ -305,7 +329,22 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_pairs(K1Launch L) {
             if (rec.flag != 0.0) unsafe_q = 1;
         }
         unsafe_q = __syncthreads_or(unsafe_q);
-        // running max of te over the tile (window lower bounds)
+        // running max of te (window lower bounds, TA_C range test) and
+        // suffix min of te (TA_R range test) over the tile
+        if (tid >= 32 && tid < 64) {
+            double carry = INFINITY;
+            for (int base = ((it.nt - 1) & ~31); base >= 0; base -= 32) {
+                int j = base + lane;
+                double v = j < it.nt ? sq[j].te : INFINITY;
+                for (int o = 1; o < 32; o <<= 1) {
+                    double t = __shfl_down_sync(0xffffffffu, v, o);
+                    if (lane + o < 32) v = fmin(v, t);
+                }
+                v = fmin(v, carry);
+                if (j < it.nt) sm[j] = v;
+                carry = __shfl_sync(0xffffffffu, v, 0);
+            }
+        }
         if (tid < 32) {
             double carry = -INFINITY;
             for (int base = 0; base < it.nt; base += 32) {
@@ -355,9 +394,41 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_pairs(K1Launch L) {
                 jhi = upper_bound_ts(sq, it.nt, wmax);
             }
             const int64_t e_off = e - L.plan.first[it.b];
+            // key of (b, e_off, q_off = it.q0 + j) without the j term
+            const uint64_t key_base = make_key(L, it.b, e_off, it.q0);
+            double wmin_te = valid ? r.te : INFINITY;
+            double wmax_ts = valid ? r.ts : -INFINITY;
+            for (int o = 16; o; o >>= 1) {
+                wmin_te = fmin(wmin_te, __shfl_xor_sync(0xffffffffu, wmin_te, o));
+                wmax_ts = fmax(wmax_ts, __shfl_xor_sync(0xffffffffu, wmax_ts, o));
+            }
+            // TA case boundaries within [jlo, jhi)
+            int ja = jhi, jb = jhi;
+            if (L.window_ok) {
+                ja = lower_bound_ts(sq, it.nt, wmin);   // first query with cts >= min lane ts
+                jb = upper_bound_ts(sq, it.nt, wmax_ts); // first query with cts >  max lane ts
+                ja = ja < jlo ? jlo : (ja > jhi ? jhi : ja);
+                jb = jb < ja ? ja : (jb > jhi ? jhi : jb);
+            } else {
+                ja = jlo;
+            }
             const bool slow = unsafe_q || __any_sync(0xffffffffu, unsafe_r);
-            if (slow) warp_pairs<true>(L, sq, jlo, jhi, r, valid, e_off, it, lane, n_ov, n_hit);
-            else warp_pairs<false>(L, sq, jlo, jhi, r, valid, e_off, it, lane, n_ov, n_hit);
+            // tb case of a whole range: every query of [ja0, ja1) ends before
+            // all candidates (running max < min te) or after all of them
+            // (suffix min > max te) — the common case for equal-length steps
+            const bool c_tb_r = jlo < ja && pm[ja - 1] < wmin_te;
+            const bool r_tb_c = jb < jhi && sm[jb] > wmax;
+            if (slow) {
+                pair_run<TA_C, TB_DYN, true>(L, sq, jlo, ja, r, valid, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+                pair_run<TA_BOTH, TB_DYN, true>(L, sq, ja, jb, r, valid, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+                pair_run<TA_R, TB_DYN, true>(L, sq, jb, jhi, r, valid, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+            } else {
+                if (c_tb_r) pair_run<TA_C, TB_R, false>(L, sq, jlo, ja, r, valid, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+                else pair_run<TA_C, TB_DYN, false>(L, sq, jlo, ja, r, valid, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+                pair_run<TA_BOTH, TB_DYN, false>(L, sq, ja, jb, r, valid, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+                if (r_tb_c) pair_run<TA_R, TB_C, false>(L, sq, jb, jhi, r, valid, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+                else pair_run<TA_R, TB_DYN, false>(L, sq, jb, jhi, r, valid, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+            }
         }
         // per-batch counters (64-bit)
         for (int o = 16; o; o >>= 1) {

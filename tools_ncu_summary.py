@@ -1,0 +1,33 @@
+"""Summarise an ncu report: key metrics + SASS op mix of the hot loop (dev helper)."""
+import csv, subprocess, sys
+from collections import Counter
+rep = sys.argv[1]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(raw.splitlines()))
+hdr, units, val = rows[0], rows[1], rows[2]
+keys = ["gpu__time_duration.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+        "smsp__thread_inst_executed_per_inst_executed.ratio", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "smsp__inst_executed.sum", "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_branch_resolving_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio",
+        "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum", "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum",
+        "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum"]
+for k in keys:
+    if k in hdr:
+        i = hdr.index(k)
+        print(f"{k:85s} {val[i]:>16s} {units[i]}")
+src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True, text=True).stdout
+srows = list(csv.reader(src.splitlines()))[2:]
+c = Counter(); tot = 0
+for r in srows:
+    try: n = int(r[5])
+    except (ValueError, IndexError): continue
+    s = r[1].strip()
+    op = (s.split()[1] if s.startswith('@') else s.split()[0]).split('.')[0]
+    c[op] += n; tot += n
+print("warp instructions", tot)
+print("  ".join(f"{op}:{n/tot:.3f}" for op, n in c.most_common(22)))
