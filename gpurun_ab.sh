@@ -8,3 +8,12 @@ for v in $VARIANTS; do
     echo "$out" | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$name', '$cfg', '%.4g'%d['value'], 'frac %.3f'%d['roofline']['frac'], 'e2e %.4g'%d['e2e']['value'], 'ms %.2f'%d['ms_per_step'], 'k1 %.2f'%d['roofline']['k1_ms_per_step'])" || tail -5 /tmp/err_$name_$cfg.log
   done
 done
+if [ -n "$NCU" ]; then
+  export TRAJSEEK_LIB=$(pwd)/${NCU#*:}
+  ncu --set full --clock-control none --import-source on -k regex:k1_pairs -s 3 -c 1 -o gpurun_out/prof_${NCU%%:*} python bench.py --config ${NCUCFG:-c3} --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+  echo ncu done
+fi
+if [ -n "$TEST" ]; then
+  export TRAJSEEK_LIB=$(pwd)/$TEST
+  timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -2
+fi

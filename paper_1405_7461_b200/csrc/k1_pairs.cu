@@ -29,6 +29,29 @@
 
 namespace tsk {
 
+// Shared-memory loads through an explicit 32-bit shared-window address, so
+// the loop carries one address register instead of re-deriving the window
+// base every iteration.
+__device__ __forceinline__ void lds2(uint32_t a, double &x, double &y) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a));
+}
+
+struct QVals {
+    double ts, te, sx, sy, sz, ext, dx, dy, dz, rcp;
+};
+
+__device__ __forceinline__ QVals load_q(uint32_t a) {
+    QVals q;
+    double ex_unused;
+    lds2(a + 0, q.ts, q.te);
+    lds2(a + 16, q.sx, q.sy);
+    lds2(a + 32, q.sz, q.ext);
+    lds2(a + 48, q.dx, q.dy);
+    lds2(a + 64, q.dz, q.rcp);
+    (void)ex_unused;
+    return q;
+}
+
 struct Cand {
     double ts, te, ext, rcp, sx, sy, sz, dx, dy, dz, ex, ey, ez;
 };
@@ -148,6 +171,12 @@ __device__ __forceinline__ Hit rare_pair(const Cand &r, const QRec &Q, double cc
                                          double e, double d2) {
     const double ta = r.ts > Q.ts ? r.ts : Q.ts;
     const double tb = r.te < Q.te ? r.te : Q.te;
+    if (!(ta <= tb)) {  // no temporal overlap (lanes at the edge of a window)
+        Hit h;
+        h.hit = false;
+        h.tb = h.te = 0.0;
+        return h;
+    }
     if (ta == tb) {
         // positions at the shared instant, constant separation (core.py:376-378)
         double rx, ry, rz, qx, qy, qz;
@@ -169,17 +198,24 @@ __device__ __forceinline__ Hit rare_pair(const Cand &r, const QRec &Q, double cc
 enum { TB_R = 0, TB_C = 1, TB_DYN = 2 };
 
 // One warp, one candidate per lane, staged queries j0..j1-1 of one (TA, TB) case.
-template <int TA, int TB, bool SLOW>
+// CNT: count overlaps per iteration; otherwise the caller counts them for
+// the whole range by binary search and lanes that do not overlap a query
+// are rejected on the rare path (they can only occur at window edges).
+template <int TA, int TB, bool SLOW, bool CNT>
 __device__ __forceinline__ void pair_run(const K1Launch &L, const QRec *__restrict__ sq, int j0, int j1,
-                                         const Cand &r, bool valid, double wmin_te, double wmax_te,
+                                         const Cand &r, double wmin_te, double wmax_te,
                                          uint64_t key_base, int lane, unsigned &n_ov,
                                          unsigned &n_hit) {
     const double d2 = L.d2;
-    for (int j = j0; j < j1; ++j) {
-        const QRec &Q = sq[j];
+    uint32_t qa = (uint32_t)__cvta_generic_to_shared(sq) + (uint32_t)j0 * (uint32_t)sizeof(QRec);
+    for (int j = j0; j < j1; ++j, qa += (uint32_t)sizeof(QRec)) {
+        const QVals Q = load_q(qa);
         const double cts = Q.ts, cte = Q.te;
-        const bool ov = r.ts <= cte && cts <= r.te;  // invalid lanes: ts = +inf
-        n_ov += ov ? 1u : 0u;
+        bool ov = true;
+        if (CNT) {
+            ov = r.ts <= cte && cts <= r.te;  // invalid lanes: ts = +inf
+            n_ov += ov ? 1u : 0u;
+        }
         const double csx = Q.sx, csy = Q.sy, csz = Q.sz;
         // ── clip at ta (core.py:503-516) ──
         double ta, rax, ray, raz, cax, cay, caz;
@@ -201,7 +237,9 @@ __device__ __forceinline__ void pair_run(const K1Launch &L, const QRec *__restri
         if (TB == TB_R || (TB == TB_DYN && cte < wmin_te)) {  // every candidate ends after the query
             tb = cte;
             lerp<SLOW>(cte, r.ts, r.ext, r.rcp, r.sx, r.sy, r.sz, r.dx, r.dy, r.dz, rbx, rby, rbz);
-            cbx = Q.ex; cby = Q.ey; cbz = Q.ez;
+            double flag_unused;
+            lds2(qa + 80, cbx, cby);
+            lds2(qa + 96, cbz, flag_unused);
         } else if (TB == TB_C || (TB == TB_DYN && cte > wmax_te)) {  // the query ends after every candidate
             tb = r.te;
             rbx = r.ex; rby = r.ey; rbz = r.ez;
@@ -212,8 +250,11 @@ __device__ __forceinline__ void pair_run(const K1Launch &L, const QRec *__restri
             lerp<SLOW>(tb, r.ts, r.ext, r.rcp, r.sx, r.sy, r.sz, r.dx, r.dy, r.dz, px, py, pz);
             lerp<SLOW>(tb, cts, Q.ext, Q.rcp, csx, csy, csz, Q.dx, Q.dy, Q.dz, qx, qy, qz);
             const bool zr = r.te > cte, zc = cte > r.te;
+            double qex, qey, qez, flag_unused;
+            lds2(qa + 80, qex, qey);
+            lds2(qa + 96, qez, flag_unused);
             rbx = zr ? px : r.ex; rby = zr ? py : r.ey; rbz = zr ? pz : r.ez;
-            cbx = zc ? qx : Q.ex; cby = zc ? qy : Q.ey; cbz = zc ? qz : Q.ez;
+            cbx = zc ? qx : qex; cby = zc ? qy : qey; cbz = zc ? qz : qez;
         }
         // ── quadratic coefficients (core.py:523-537) ──
         const double ux = __dsub_rn(rax, cax), uy = __dsub_rn(ray, cay), uz = __dsub_rn(raz, caz);
@@ -231,7 +272,7 @@ __device__ __forceinline__ void pair_run(const K1Launch &L, const QRec *__restri
             Hit h;
             h.hit = false;
             h.tb = h.te = 0.0;
-            if (cand) h = rare_pair(r, Q, cc, aa, dot, e, d2);
+            if (cand) h = rare_pair(r, sq[j], cc, aa, dot, e, d2);
             n_hit += h.hit ? 1u : 0u;
             append_hit(L, h.hit, key_base + (L.query_major ? ((uint64_t)j << L.minor_bits) : (uint64_t)j),
                        h.tb, h.te, lane);
@@ -254,6 +295,16 @@ __device__ __forceinline__ int lower_bound_ts(const QRec *q, int n, double v) {
     while (a < b) {
         int m = (a + b) >> 1;
         if (q[m].ts < v) a = m + 1;
+        else b = m;
+    }
+    return a;
+}
+
+__device__ __forceinline__ int lower_bound_te(const QRec *q, int n, double v) {
+    int a = 0, b = n;
+    while (a < b) {
+        int m = (a + b) >> 1;
+        if (q[m].te < v) a = m + 1;
         else b = m;
     }
     return a;
@@ -329,6 +380,10 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
             if (rec.flag != 0.0) unsafe_q = 1;
         }
         unsafe_q = __syncthreads_or(unsafe_q);
+        int te_desc = 0;  // any adjacent pair with te decreasing?
+        for (int j = tid; j + 1 < it.nt; j += K1_THREADS)
+            if (sq[j + 1].te < sq[j].te) te_desc = 1;
+        const bool te_sorted = !__syncthreads_or(te_desc);
         // running max of te (window lower bounds, TA_C range test) and
         // suffix min of te (TA_R range test) over the tile
         if (tid >= 32 && tid < 64) {
@@ -419,15 +474,27 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
             const bool c_tb_r = jlo < ja && pm[ja - 1] < wmin_te;
             const bool r_tb_c = jb < jhi && sm[jb] > wmax;
             if (slow) {
-                pair_run<TA_C, TB_DYN, true>(L, sq, jlo, ja, r, valid, wmin_te, wmax, key_base, lane, n_ov, n_hit);
-                pair_run<TA_BOTH, TB_DYN, true>(L, sq, ja, jb, r, valid, wmin_te, wmax, key_base, lane, n_ov, n_hit);
-                pair_run<TA_R, TB_DYN, true>(L, sq, jb, jhi, r, valid, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+                pair_run<TA_C, TB_DYN, true, true>(L, sq, jlo, ja, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+                pair_run<TA_BOTH, TB_DYN, true, true>(L, sq, ja, jb, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+                pair_run<TA_R, TB_DYN, true, true>(L, sq, jb, jhi, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
             } else {
-                if (c_tb_r) pair_run<TA_C, TB_R, false>(L, sq, jlo, ja, r, valid, wmin_te, wmax, key_base, lane, n_ov, n_hit);
-                else pair_run<TA_C, TB_DYN, false>(L, sq, jlo, ja, r, valid, wmin_te, wmax, key_base, lane, n_ov, n_hit);
-                pair_run<TA_BOTH, TB_DYN, false>(L, sq, ja, jb, r, valid, wmin_te, wmax, key_base, lane, n_ov, n_hit);
-                if (r_tb_c) pair_run<TA_R, TB_C, false>(L, sq, jb, jhi, r, valid, wmin_te, wmax, key_base, lane, n_ov, n_hit);
-                else pair_run<TA_R, TB_DYN, false>(L, sq, jb, jhi, r, valid, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+                if (c_tb_r && te_sorted) {
+                    // overlap <=> r.ts <= cte; cte ascending over the tile
+                    const int k = lower_bound_te(sq, it.nt, r.ts);
+                    n_ov += (unsigned)(ja - (k < jlo ? jlo : (k > ja ? ja : k)));
+                    pair_run<TA_C, TB_R, false, false>(L, sq, jlo, ja, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+                } else {
+                    pair_run<TA_C, TB_DYN, false, true>(L, sq, jlo, ja, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+                }
+                pair_run<TA_BOTH, TB_DYN, false, true>(L, sq, ja, jb, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+                if (r_tb_c) {
+                    // overlap <=> cts <= r.te; cts ascending over the tile
+                    const int k = upper_bound_ts(sq, it.nt, r.te);
+                    n_ov += (unsigned)((k < jb ? jb : (k > jhi ? jhi : k)) - jb);
+                    pair_run<TA_R, TB_C, false, false>(L, sq, jb, jhi, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+                } else {
+                    pair_run<TA_R, TB_DYN, false, true>(L, sq, jb, jhi, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+                }
             }
         }
         // per-batch counters (64-bit)
