@@ -103,33 +103,7 @@ def workload_columns(cfg):
 FIELDS = ("traj", "seg", "xs", "ys", "zs", "ts", "xe", "ye", "ze", "te")
 
 
-def shard_bounds(ints: np.ndarray, world: int) -> list[tuple[int, int]]:
-    """Contiguous batch shards [b0, b1) with balanced Σ interactions."""
-    nb = ints.shape[0]
-    cum = np.concatenate([[0], np.cumsum(ints, dtype=np.float64)])
-    total = cum[-1]
-    cuts = [0]
-    for r in range(1, world):
-        target = total * r / world
-        cuts.append(int(np.searchsorted(cum, target, side="left")))
-    cuts.append(nb)
-    cuts = [min(max(c, 0), nb) for c in cuts]
-    for i in range(1, len(cuts)):
-        cuts[i] = max(cuts[i], cuts[i - 1])
-    return [(cuts[r], cuts[r + 1]) for r in range(world)]
-
-
-def sub_plan(plan, b0: int, b1: int):
-    """The batches [b0, b1) of ``plan`` over a view of their queries."""
-    import paper_1405_7461_b200 as tsk
-
-    if b1 <= b0:
-        return None
-    bs = plan.batches[b0:b1]
-    lo0, hi1 = bs[0].lo, bs[-1].hi
-    view = plan.queries.view(lo0, hi1)
-    rebased = tuple(tsk.QueryBatch(b.lo - lo0, b.hi - lo0, b.extent, b.first, b.last) for b in bs)
-    return tsk.BatchPlan(view, rebased)
+from paper_1405_7461_b200.sharding import shard_bounds, sub_plan  # noqa: E402
 
 
 # ── clocks ──────────────────────────────────────────────────────────────────
@@ -305,8 +279,9 @@ def run_ours(args, cfg):
 
     t0 = time.perf_counter()
     e_cols, q_cols = workload_columns(cfg)
-    store = tsk.SegmentStore(*(e_cols[k] for k in FIELDS), validate=False)
-    queries = tsk.SegmentStore(*(q_cols[k] for k in FIELDS), validate=False)
+    store = tsk.SegmentStore.from_columns(e_cols, validate=False)
+    queries = tsk.SegmentStore.from_columns(q_cols, validate=False)
+    del e_cols, q_cols
     t_gen = time.perf_counter() - t0
     index = tsk.build_index(store, M_BINS)
     plan = tsk.periodic(queries, S_BATCH, index)
@@ -411,7 +386,7 @@ def run_ours(args, cfg):
             pass
 
     cpu = None
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and rank == 0:
         workers = os.cpu_count() or 1
         sorted_cols = lambda s: {k: getattr(s, k) for k in FIELDS}  # noqa: E731
         e, q, ix, oplan, order = cpu_setup(sorted_cols(store), sorted_cols(queries), presorted=True)

@@ -114,13 +114,27 @@ def execute_batch(store: SegmentStore, batch: SegmentStore, span: tuple[int, int
 
 
 def run_search(store: SegmentStore, index: TemporalIndex, plan: BatchPlan, d: float, *,
-               workers: int | None = None) -> tuple[ResultSet, SearchStats]:
-    """Execute every batch of ``plan`` against ``store`` on the GPU."""
-    t_start = time.perf_counter()
+               workers: int | None = None, devices: list[int] | None = None
+               ) -> tuple[ResultSet, SearchStats]:
+    """Execute every batch of ``plan`` against ``store`` on the GPU.
+
+    ``devices`` (an addition to the reference signature) shards the plan
+    over several GPUs, each holding a replica of the store: contiguous,
+    interaction-balanced batch shards, one host thread per device, results
+    concatenated in plan order.  No collective is involved.
+    """
     resolve_workers(workers)
+    if devices is not None and len(devices) > 1:
+        return _run_sharded(store, index, plan, d, list(devices))
+    ordinal = None if not devices else devices[0]
+    return _run_one(store, index, plan, d, ordinal, 0)
+
+
+def _run_one(store, index, plan, d, ordinal, replica):
+    t_start = time.perf_counter()
     queries = plan.queries
     lo, hi = plan.table()
-    dev = index.ensure_device() if index._store is store else _bind_index(store, index)
+    dev = index.ensure_device(ordinal, replica, store)
     res = _native.search(dev, queries, lo, hi, None, None, d, _native.TSK_ORDER_REFERENCE)
     t_asm = time.perf_counter()
     result = _result_set(res) if res.n else ResultSet.empty()
@@ -152,6 +166,51 @@ def run_search(store: SegmentStore, index: TemporalIndex, plan: BatchPlan, d: fl
     return result, stats
 
 
+def _run_sharded(store, index, plan, d, devices):
+    from concurrent.futures import ThreadPoolExecutor
+
+    from .sharding import batch_interactions, shard_bounds, sub_plan
+
+    t_start = time.perf_counter()
+    bounds = shard_bounds(batch_interactions(plan, index), len(devices))
+    seen: dict[int, int] = {}
+    jobs = []
+    for (b0, b1), dvc in zip(bounds, devices):
+        replica = seen.get(dvc, 0)
+        seen[dvc] = replica + 1
+        sp = sub_plan(plan, b0, b1)
+        if sp is not None:
+            jobs.append((b0, sp, dvc, replica))
+    # upload replicas (and their indexes) before the parallel section
+    for _, _, dvc, replica in jobs:
+        index.ensure_device(dvc, replica, store)
+    with ThreadPoolExecutor(max_workers=max(1, len(jobs))) as ex:
+        outs = list(ex.map(lambda j: _run_one(store, index, j[1], d, j[2], j[3]), jobs))
+    stats = SearchStats()
+    per_batch: list[BatchTrace] = []
+    for (b0, _, _, _), (_, st) in zip(jobs, outs):
+        for t in st.per_batch:
+            per_batch.append(BatchTrace(t.ordinal + b0, t.queries, t.candidates, t.interactions,
+                                        t.hits, t.kernel_seconds))
+        stats.interactions_computed += st.interactions_computed
+        stats.temporal_misses += st.temporal_misses
+        stats.spatial_misses += st.spatial_misses
+        stats.hits += st.hits
+        stats.kernel_seconds = max(stats.kernel_seconds, st.kernel_seconds)
+        stats.device_seconds = max(stats.device_seconds, st.device_seconds)
+        stats.pair_kernel_seconds = max(stats.pair_kernel_seconds, st.pair_kernel_seconds)
+    # batches of shards that got nothing (more devices than batches) are absent
+    # from `jobs`; every batch belongs to exactly one job otherwise
+    stats.per_batch = sorted(per_batch, key=lambda t: t.ordinal)
+    t_asm = time.perf_counter()
+    result = ResultSet.concatenate([r for r, _ in outs])
+    t_end = time.perf_counter()
+    stats.assembly_seconds = t_end - t_asm
+    stats.total_seconds = t_end - t_start
+    stats.overhead_seconds = max(0.0, stats.total_seconds - stats.kernel_seconds - stats.assembly_seconds)
+    return result, stats
+
+
 def search_device(store: SegmentStore, index: TemporalIndex, plan: BatchPlan, d: float, *,
                   queries_resident: bool = False) -> _native.Result:
     """Plan execution with hits left in HBM (no D2H of result columns).
@@ -162,22 +221,11 @@ def search_device(store: SegmentStore, index: TemporalIndex, plan: BatchPlan, d:
     per-batch stats, CUDA-event timings).
     """
     lo, hi = plan.table()
-    dev = index.ensure_device() if index._store is store else _bind_index(store, index)
+    dev = index.ensure_device(None, 0, store)
     flags = _native.TSK_ORDER_REFERENCE | _native.TSK_RESULTS_ON_DEVICE
     if queries_resident:
         flags |= _native.TSK_QUERIES_RESIDENT
     return _native.search(dev, plan.queries, lo, hi, None, None, d, flags)
-
-
-def _bind_index(store: SegmentStore, index: TemporalIndex):
-    """Device copy of ``store`` carrying an index with ``index``'s parameters."""
-    from .index import _rule_code
-
-    dev = store.device()
-    if dev.index_token is not index:
-        _native.index_build(dev, index.m, _rule_code(index.extent_rule))
-        dev.index_token = index
-    return dev
 
 
 def launch_overhead_pass(store: SegmentStore, batch: SegmentStore, span: tuple[int, int], *,

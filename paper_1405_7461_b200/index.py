@@ -72,11 +72,11 @@ class TemporalIndex:
             return 0
         return min(int((t - self.t0) // self.bin_width), self.m - 1)
 
-    def ensure_device(self):
-        """The store's device copy with this index resident on it."""
+    def ensure_device(self, ordinal: int | None = None, replica: int = 0, store=None):
+        """A device copy of the indexed store (or ``store``) carrying this index."""
         from . import _native
 
-        dev = self._store.device()
+        dev = (self._store if store is None else store).device(ordinal, replica)
         if dev.index_token is not self:
             _native.index_build(dev, self.m, _rule_code(self.extent_rule))
             dev.index_token = self
