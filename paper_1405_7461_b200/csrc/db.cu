@@ -334,7 +334,7 @@ void launch_ranges(tsk_db *db, const Soa &q, SearchPlanDev &p, bool spans_given,
 __global__ void __launch_bounds__(1024, 1) k_plan_items(int64_t nb, const int64_t *__restrict__ lo, const int64_t *__restrict__ hi,
                              const int64_t *__restrict__ first, const int64_t *__restrict__ last,
                              int64_t *__restrict__ item_off, int64_t *__restrict__ meta,
-                             int64_t slots) {
+                             int64_t slots, int stride) {
     typedef cub::BlockReduce<long long, 1024> BR;
     typedef cub::BlockScan<long long, 1024> BS;
     __shared__ union {
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(1024, 1) k_plan_items(int64_t nb, const int64_
     for (int64_t b = threadIdx.x; b < nb; b += blockDim.x) {
         long long c = first[b] >= 0 ? last[b] - first[b] + 1 : 0;
         long long tq = (hi[b] - lo[b] + 1 + K1_TQ - 1) / K1_TQ;
-        acc += ((c + K1_THREADS - 1) / K1_THREADS) * tq;
+        acc += ((c + stride - 1) / stride) * tq;
     }
     long long tiles = BR(tmp.r).Sum(acc);
     if (threadIdx.x == 0) {
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(1024, 1) k_plan_items(int64_t nb, const int64_
         carry = 0;
     }
     __syncthreads();
-    const long long ct = (long long)K1_THREADS * sub_sh;
+    const long long ct = (long long)stride * sub_sh;
     for (int64_t base = 0; base < nb; base += blockDim.x) {
         int64_t b = base + threadIdx.x;
         long long v = 0;
@@ -380,8 +380,9 @@ __global__ void __launch_bounds__(1024, 1) k_plan_items(int64_t nb, const int64_
     }
 }
 
-void launch_plan_items(SearchPlanDev &p, int slots, cudaStream_t st) {
-    k_plan_items<<<1, 1024, 0, st>>>(p.nb, p.lo, p.hi, p.first, p.last, p.item_off, p.meta, slots);
+void launch_plan_items(SearchPlanDev &p, int slots, int stride, cudaStream_t st) {
+    k_plan_items<<<1, 1024, 0, st>>>(p.nb, p.lo, p.hi, p.first, p.last, p.item_off, p.meta, slots,
+                                     stride);
     TSK_CUDA(cudaGetLastError());
 }
 

@@ -6,26 +6,37 @@
 //
 // Work decomposition.  A work item is (batch b, candidate tile, query tile):
 // up to K1_TQ queries of the batch are staged in shared memory as 112-byte
-// records, the block's 256 threads each hold one candidate entry segment in
-// registers (sub-tiles of 256 candidates are walked in turn), and every
-// warp loops over the window of staged queries that can overlap any of its
-// 32 candidates (entries and queries are both start-time sorted, so the
-// window is two binary searches).  Items are claimed from a global atomic
-// counter by a persistent grid.
+// records, each thread holds K1_CPT candidate entry segments in registers
+// (lane l of a warp holds candidates l, l+32, ... of the warp's 32*K1_CPT
+// consecutive ones; sub-tiles of 256*K1_CPT candidates are walked in turn),
+// and every warp loops over the window of staged queries that can overlap
+// any of its candidates (entries and queries are both start-time sorted, so
+// the window is two binary searches).  Items are claimed from a global
+// atomic counter by a persistent grid.
 //
 // Arithmetic.  For an overlapping pair the reference clips both segments
 // to [ta, tb] and solves the quadratic (core.py:503-565).  With span > 0,
 // only the earlier-starting segment is interpolated at ta and only the
 // later-ending one at tb; the other endpoint is taken verbatim, which is
-// what the np.where selections of core.py:514 produce.  Interpolation at
-// t == ts is an identity (f == 0), so when a warp disagrees about which
-// segment starts first both are interpolated at ta.  Zero-length shared
-// spans (touching extents, waypoints) take a separate exact path.  The
-// hit test uses disc' = dot^2 - aa*(cc - d^2) (= disc/4, exact scaling) with
-// a tiny negative margin; the few candidates that pass are re-solved with
-// the reference's exact root formula.  All ops are binary64 with explicit
-// rounding; divisions use qdiv() with a per-segment RN(1/ext).
+// what the np.where selections of core.py:514 produce.  Each warp splits
+// its query window into the three start-time cases (query first / entry
+// first / mixed); in the mixed range both are interpolated at ta, exact
+// because the later starter has f == 0.  The end-time case is proven for a
+// whole range from the tile's running max / suffix min of end times, else
+// decided per query.  Zero-length shared spans (touching extents,
+// waypoints) take the exact rare path.  The hit test uses
+// dq = dot^2 - aa*(cc - d^2) (= disc/4, exact scaling) with a tiny negative
+// margin; the few candidates that pass are re-solved with the reference's
+// exact root formula.  All ops are binary64 with explicit rounding;
+// divisions use qdiv() with a per-segment RN(1/ext).
 #include "tsk_internal.cuh"
+
+#ifndef K1_CPT
+#define K1_CPT 2
+#endif
+#ifndef K1_MIN_BLOCKS
+#define K1_MIN_BLOCKS (K1_CPT == 1 ? 3 : 2)
+#endif
 
 namespace tsk {
 
@@ -42,13 +53,11 @@ struct QVals {
 
 __device__ __forceinline__ QVals load_q(uint32_t a) {
     QVals q;
-    double ex_unused;
     lds2(a + 0, q.ts, q.te);
     lds2(a + 16, q.sx, q.sy);
     lds2(a + 32, q.sz, q.ext);
     lds2(a + 48, q.dx, q.dy);
     lds2(a + 64, q.dz, q.rcp);
-    (void)ex_unused;
     return q;
 }
 
@@ -127,6 +136,31 @@ __device__ __forceinline__ Hit solve_exact(double ta, double tb, double cc, doub
     return h;
 }
 
+// Flat (zero-length shared span) pairs, quadratic-root candidates and lanes
+// at a window edge: exact recomputation with every verbatim rule.
+__device__ __forceinline__ Hit rare_pair(const Cand &r, const QRec &Q, double cc, double aa, double dot,
+                                         double e, double d2) {
+    Hit h;
+    h.hit = false;
+    h.tb = h.te = 0.0;
+    const double ta = r.ts > Q.ts ? r.ts : Q.ts;
+    const double tb = r.te < Q.te ? r.te : Q.te;
+    if (!(ta <= tb)) return h;  // no temporal overlap
+    if (ta == tb) {
+        // positions at the shared instant, constant separation (core.py:376-378)
+        double rx, ry, rz, qx, qy, qz;
+        position_exact(ta, r.ts, r.te, r.sx, r.sy, r.sz, r.ex, r.ey, r.ez, r.dx, r.dy, r.dz, rx, ry, rz);
+        position_exact(ta, Q.ts, Q.te, Q.sx, Q.sy, Q.sz, Q.ex, Q.ey, Q.ez, Q.dx, Q.dy, Q.dz, qx, qy, qz);
+        const double ux = __dsub_rn(rx, qx), uy = __dsub_rn(ry, qy), uz = __dsub_rn(rz, qz);
+        const double c2 = __dadd_rn(__dadd_rn(__dmul_rn(ux, ux), __dmul_rn(uy, uy)), __dmul_rn(uz, uz));
+        h.hit = c2 <= d2;
+        h.tb = ta;
+        h.te = tb;
+        return h;
+    }
+    return solve_exact(ta, tb, cc, aa, dot, e, d2);
+}
+
 struct ItemCtx {
     int64_t b, lo_q, first_c, c_hi;  // batch, tile's first query ordinal, tile's candidate range
     int64_t q0;                      // first query offset within batch (tile)
@@ -158,124 +192,115 @@ __device__ __forceinline__ uint64_t make_key(const K1Launch &L, int64_t b, int64
     return ((uint64_t)b << (L.major_bits + L.minor_bits)) | (major << L.minor_bits) | minor;
 }
 
-// Clip-at-ta cases of a query against a warp's 32 candidates.  Queries in a
+// Clip-at-ta cases of a query against a warp's candidates.  Queries in a
 // tile are sorted by start time, so each case is a contiguous j range:
-//   TA_C    cts <  every lane's ts: the query started first, interpolate it
-//   TA_R    cts >  every lane's ts: the entry started first, interpolate it
+//   TA_C    cts <  every candidate's ts: the query started first, interpolate it
+//   TA_R    cts >  every candidate's ts: the entry started first, interpolate it
 //   TA_BOTH otherwise: interpolate both (the later starter's f is 0 -> exact)
 enum { TA_C = 0, TA_R = 1, TA_BOTH = 2 };
-
-// Flat (zero-length shared span) pairs and quadratic-root candidates:
-// exact recomputation with every verbatim rule of the reference.
-__device__ __forceinline__ Hit rare_pair(const Cand &r, const QRec &Q, double cc, double aa, double dot,
-                                         double e, double d2) {
-    const double ta = r.ts > Q.ts ? r.ts : Q.ts;
-    const double tb = r.te < Q.te ? r.te : Q.te;
-    if (!(ta <= tb)) {  // no temporal overlap (lanes at the edge of a window)
-        Hit h;
-        h.hit = false;
-        h.tb = h.te = 0.0;
-        return h;
-    }
-    if (ta == tb) {
-        // positions at the shared instant, constant separation (core.py:376-378)
-        double rx, ry, rz, qx, qy, qz;
-        position_exact(ta, r.ts, r.te, r.sx, r.sy, r.sz, r.ex, r.ey, r.ez, r.dx, r.dy, r.dz, rx, ry, rz);
-        position_exact(ta, Q.ts, Q.te, Q.sx, Q.sy, Q.sz, Q.ex, Q.ey, Q.ez, Q.dx, Q.dy, Q.dz, qx, qy, qz);
-        const double ux = __dsub_rn(rx, qx), uy = __dsub_rn(ry, qy), uz = __dsub_rn(rz, qz);
-        const double c2 = __dadd_rn(__dadd_rn(__dmul_rn(ux, ux), __dmul_rn(uy, uy)), __dmul_rn(uz, uz));
-        Hit h;
-        h.hit = c2 <= d2;
-        h.tb = ta;
-        h.te = tb;
-        return h;
-    }
-    return solve_exact(ta, tb, cc, aa, dot, e, d2);
-}
-
 // Clip-at-tb cases; TB_R / TB_C are proven for a whole j range from the
 // tile's running max / suffix min of query end times, TB_DYN decides per query.
 enum { TB_R = 0, TB_C = 1, TB_DYN = 2 };
 
-// One warp, one candidate per lane, staged queries j0..j1-1 of one (TA, TB) case.
-// CNT: count overlaps per iteration; otherwise the caller counts them for
-// the whole range by binary search and lanes that do not overlap a query
-// are rejected on the rare path (they can only occur at window edges).
+// The common-path arithmetic of one (candidate, query) pair up to the hit
+// test.  Returns whether the pair needs the exact rare path.
+template <int TA, int TB, bool SLOW>
+__device__ __forceinline__ bool pair_eval(const Cand &r, const QVals &Q, uint32_t qa, double wmin_te,
+                                          double wmax_te, double d2, double &cc, double &aa,
+                                          double &dot, double &e) {
+    const double cts = Q.ts, cte = Q.te;
+    // ── clip at ta (core.py:503-516) ──
+    double ta, rax, ray, raz, cax, cay, caz;
+    if (TA == TA_R) {
+        ta = cts;
+        lerp<SLOW>(cts, r.ts, r.ext, r.rcp, r.sx, r.sy, r.sz, r.dx, r.dy, r.dz, rax, ray, raz);
+        cax = Q.sx; cay = Q.sy; caz = Q.sz;
+    } else if (TA == TA_C) {
+        ta = r.ts;
+        rax = r.sx; ray = r.sy; raz = r.sz;
+        lerp<SLOW>(r.ts, cts, Q.ext, Q.rcp, Q.sx, Q.sy, Q.sz, Q.dx, Q.dy, Q.dz, cax, cay, caz);
+    } else {
+        ta = r.ts > cts ? r.ts : cts;
+        lerp<SLOW>(ta, r.ts, r.ext, r.rcp, r.sx, r.sy, r.sz, r.dx, r.dy, r.dz, rax, ray, raz);
+        lerp<SLOW>(ta, cts, Q.ext, Q.rcp, Q.sx, Q.sy, Q.sz, Q.dx, Q.dy, Q.dz, cax, cay, caz);
+    }
+    // ── clip at tb: interpolate the later ender ──
+    double tb, rbx, rby, rbz, cbx, cby, cbz;
+    if (TB == TB_R || (TB == TB_DYN && cte < wmin_te)) {  // every candidate ends after the query
+        tb = cte;
+        lerp<SLOW>(cte, r.ts, r.ext, r.rcp, r.sx, r.sy, r.sz, r.dx, r.dy, r.dz, rbx, rby, rbz);
+        double flag_unused;
+        lds2(qa + 80, cbx, cby);
+        lds2(qa + 96, cbz, flag_unused);
+    } else if (TB == TB_C || (TB == TB_DYN && cte > wmax_te)) {  // the query ends after every candidate
+        tb = r.te;
+        rbx = r.ex; rby = r.ey; rbz = r.ez;
+        lerp<SLOW>(r.te, cts, Q.ext, Q.rcp, Q.sx, Q.sy, Q.sz, Q.dx, Q.dy, Q.dz, cbx, cby, cbz);
+    } else {
+        tb = r.te < cte ? r.te : cte;
+        double px, py, pz, qx, qy, qz;
+        lerp<SLOW>(tb, r.ts, r.ext, r.rcp, r.sx, r.sy, r.sz, r.dx, r.dy, r.dz, px, py, pz);
+        lerp<SLOW>(tb, cts, Q.ext, Q.rcp, Q.sx, Q.sy, Q.sz, Q.dx, Q.dy, Q.dz, qx, qy, qz);
+        const bool zr = r.te > cte, zc = cte > r.te;
+        double qex, qey, qez, flag_unused;
+        lds2(qa + 80, qex, qey);
+        lds2(qa + 96, qez, flag_unused);
+        rbx = zr ? px : r.ex; rby = zr ? py : r.ey; rbz = zr ? pz : r.ez;
+        cbx = zc ? qx : qex; cby = zc ? qy : qey; cbz = zc ? qz : qez;
+    }
+    // ── quadratic coefficients (core.py:523-537) ──
+    const double ux = __dsub_rn(rax, cax), uy = __dsub_rn(ray, cay), uz = __dsub_rn(raz, caz);
+    cc = __dadd_rn(__dadd_rn(__dmul_rn(ux, ux), __dmul_rn(uy, uy)), __dmul_rn(uz, uz));
+    const double wx = __dsub_rn(__dsub_rn(rbx, rax), __dsub_rn(cbx, cax));
+    const double wy = __dsub_rn(__dsub_rn(rby, ray), __dsub_rn(cby, cay));
+    const double wz = __dsub_rn(__dsub_rn(rbz, raz), __dsub_rn(cbz, caz));
+    aa = __dadd_rn(__dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy)), __dmul_rn(wz, wz));
+    dot = __dadd_rn(__dadd_rn(__dmul_rn(ux, wx), __dmul_rn(uy, wy)), __dmul_rn(uz, wz));
+    e = __dsub_rn(cc, d2);
+    // disc / 4 (exact scaling); the margin keeps the test a superset under underflow
+    const double dq = __dsub_rn(__dmul_rn(dot, dot), __dmul_rn(aa, e));
+    return ta == tb || dq >= -0x1p-1000;
+}
+
+// One warp, K1_CPT candidates per lane, staged queries j0..j1-1 of one
+// (TA, TB) case.  CNT: count overlaps per iteration; otherwise the caller
+// counts them for the whole range by binary search and lanes that do not
+// overlap a query are rejected on the rare path (window edges only).
 template <int TA, int TB, bool SLOW, bool CNT>
 __device__ __forceinline__ void pair_run(const K1Launch &L, const QRec *__restrict__ sq, int j0, int j1,
-                                         const Cand &r, double wmin_te, double wmax_te,
-                                         uint64_t key_base, int lane, unsigned &n_ov,
-                                         unsigned &n_hit) {
+                                         const Cand (&r)[K1_CPT], double wmin_te, double wmax_te,
+                                         const uint64_t (&key_base)[K1_CPT], int lane,
+                                         unsigned &n_ov, unsigned &n_hit) {
     const double d2 = L.d2;
     uint32_t qa = (uint32_t)__cvta_generic_to_shared(sq) + (uint32_t)j0 * (uint32_t)sizeof(QRec);
     for (int j = j0; j < j1; ++j, qa += (uint32_t)sizeof(QRec)) {
         const QVals Q = load_q(qa);
-        const double cts = Q.ts, cte = Q.te;
-        bool ov = true;
-        if (CNT) {
-            ov = r.ts <= cte && cts <= r.te;  // invalid lanes: ts = +inf
-            n_ov += ov ? 1u : 0u;
+        bool cand[K1_CPT];
+        double cc[K1_CPT], aa[K1_CPT], dot[K1_CPT], e[K1_CPT];
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < K1_CPT; ++k) {
+            bool ov = true;
+            if (CNT) {
+                ov = r[k].ts <= Q.te && Q.ts <= r[k].te;  // invalid lanes: ts = +inf
+                n_ov += ov ? 1u : 0u;
+            }
+            cand[k] = pair_eval<TA, TB, SLOW>(r[k], Q, qa, wmin_te, wmax_te, d2, cc[k], aa[k], dot[k],
+                                              e[k]) && ov;
+            any |= cand[k];
         }
-        const double csx = Q.sx, csy = Q.sy, csz = Q.sz;
-        // ── clip at ta (core.py:503-516) ──
-        double ta, rax, ray, raz, cax, cay, caz;
-        if (TA == TA_R) {
-            ta = cts;
-            lerp<SLOW>(cts, r.ts, r.ext, r.rcp, r.sx, r.sy, r.sz, r.dx, r.dy, r.dz, rax, ray, raz);
-            cax = csx; cay = csy; caz = csz;
-        } else if (TA == TA_C) {
-            ta = r.ts;
-            rax = r.sx; ray = r.sy; raz = r.sz;
-            lerp<SLOW>(r.ts, cts, Q.ext, Q.rcp, csx, csy, csz, Q.dx, Q.dy, Q.dz, cax, cay, caz);
-        } else {
-            ta = r.ts > cts ? r.ts : cts;
-            lerp<SLOW>(ta, r.ts, r.ext, r.rcp, r.sx, r.sy, r.sz, r.dx, r.dy, r.dz, rax, ray, raz);
-            lerp<SLOW>(ta, cts, Q.ext, Q.rcp, csx, csy, csz, Q.dx, Q.dy, Q.dz, cax, cay, caz);
-        }
-        // ── clip at tb: interpolate the later ender (warp-uniform test) ──
-        double tb, rbx, rby, rbz, cbx, cby, cbz;
-        if (TB == TB_R || (TB == TB_DYN && cte < wmin_te)) {  // every candidate ends after the query
-            tb = cte;
-            lerp<SLOW>(cte, r.ts, r.ext, r.rcp, r.sx, r.sy, r.sz, r.dx, r.dy, r.dz, rbx, rby, rbz);
-            double flag_unused;
-            lds2(qa + 80, cbx, cby);
-            lds2(qa + 96, cbz, flag_unused);
-        } else if (TB == TB_C || (TB == TB_DYN && cte > wmax_te)) {  // the query ends after every candidate
-            tb = r.te;
-            rbx = r.ex; rby = r.ey; rbz = r.ez;
-            lerp<SLOW>(r.te, cts, Q.ext, Q.rcp, csx, csy, csz, Q.dx, Q.dy, Q.dz, cbx, cby, cbz);
-        } else {
-            tb = r.te < cte ? r.te : cte;
-            double px, py, pz, qx, qy, qz;
-            lerp<SLOW>(tb, r.ts, r.ext, r.rcp, r.sx, r.sy, r.sz, r.dx, r.dy, r.dz, px, py, pz);
-            lerp<SLOW>(tb, cts, Q.ext, Q.rcp, csx, csy, csz, Q.dx, Q.dy, Q.dz, qx, qy, qz);
-            const bool zr = r.te > cte, zc = cte > r.te;
-            double qex, qey, qez, flag_unused;
-            lds2(qa + 80, qex, qey);
-            lds2(qa + 96, qez, flag_unused);
-            rbx = zr ? px : r.ex; rby = zr ? py : r.ey; rbz = zr ? pz : r.ez;
-            cbx = zc ? qx : qex; cby = zc ? qy : qey; cbz = zc ? qz : qez;
-        }
-        // ── quadratic coefficients (core.py:523-537) ──
-        const double ux = __dsub_rn(rax, cax), uy = __dsub_rn(ray, cay), uz = __dsub_rn(raz, caz);
-        const double cc = __dadd_rn(__dadd_rn(__dmul_rn(ux, ux), __dmul_rn(uy, uy)), __dmul_rn(uz, uz));
-        const double wx = __dsub_rn(__dsub_rn(rbx, rax), __dsub_rn(cbx, cax));
-        const double wy = __dsub_rn(__dsub_rn(rby, ray), __dsub_rn(cby, cay));
-        const double wz = __dsub_rn(__dsub_rn(rbz, raz), __dsub_rn(cbz, caz));
-        const double aa = __dadd_rn(__dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy)), __dmul_rn(wz, wz));
-        const double dot = __dadd_rn(__dadd_rn(__dmul_rn(ux, wx), __dmul_rn(uy, wy)), __dmul_rn(uz, wz));
-        const double e = __dsub_rn(cc, d2);
-        // disc / 4 (exact scaling); the margin keeps the test a superset under underflow
-        const double dq = __dsub_rn(__dmul_rn(dot, dot), __dmul_rn(aa, e));
-        const bool cand = ov && (ta == tb || dq >= -0x1p-1000);
-        if (__ballot_sync(0xffffffffu, cand)) {
-            Hit h;
-            h.hit = false;
-            h.tb = h.te = 0.0;
-            if (cand) h = rare_pair(r, sq[j], cc, aa, dot, e, d2);
-            n_hit += h.hit ? 1u : 0u;
-            append_hit(L, h.hit, key_base + (L.query_major ? ((uint64_t)j << L.minor_bits) : (uint64_t)j),
-                       h.tb, h.te, lane);
+        if (__ballot_sync(0xffffffffu, any)) {
+#pragma unroll
+            for (int k = 0; k < K1_CPT; ++k) {
+                Hit h;
+                h.hit = false;
+                h.tb = h.te = 0.0;
+                if (cand[k]) h = rare_pair(r[k], sq[j], cc[k], aa[k], dot[k], e[k], d2);
+                n_hit += h.hit ? 1u : 0u;
+                append_hit(L, h.hit,
+                           key_base[k] + (L.query_major ? ((uint64_t)j << L.minor_bits) : (uint64_t)j),
+                           h.tb, h.te, lane);
+            }
         }
     }
 }
@@ -320,9 +345,18 @@ __device__ __forceinline__ int upper_bound_ts(const QRec *q, int n, double v) {
     return a;
 }
 
-#ifndef K1_MIN_BLOCKS
-#define K1_MIN_BLOCKS 3
-#endif
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+__device__ __forceinline__ double warp_min(double v) {
+    for (int o = 16; o; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
 __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L) {
     __shared__ QRec sq[K1_TQ];
     __shared__ double pm[K1_TQ];  // running max of te over the tile
@@ -331,10 +365,11 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
     __shared__ int64_t item_sh;
     __shared__ unsigned long long red_ov, red_hit;
 
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t total = L.plan.meta[0];
     const int sub = (int)L.plan.meta[1];
-    const int64_t ct = (int64_t)K1_THREADS * sub;
+    constexpr int64_t STRIDE = (int64_t)K1_THREADS * K1_CPT;  // candidates per sub-tile
+    const int64_t ct = STRIDE * sub;
     const int64_t nb = L.plan.nb;
 
     for (;;) {
@@ -342,15 +377,13 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
             int64_t item = (int64_t)atomicAdd(L.item_counter, 1ull);
             item_sh = item;
             if (item < total) {
-                // batch = last b with item_off[b] <= item
+                // batch = last b with item_off[b] <= item (a non-empty batch)
                 int64_t a = 0, z = nb;
                 while (z - a > 1) {
                     int64_t m = (a + z) >> 1;
                     if (L.plan.item_off[m] <= item) a = m;
                     else z = m;
                 }
-                // skip empty batches that share the same offset
-                while (a + 1 < nb && L.plan.item_off[a + 1] <= item) ++a;
                 const int64_t b = a;
                 const int64_t local = item - L.plan.item_off[b];
                 const int64_t s_b = L.plan.hi[b] - L.plan.lo[b] + 1;
@@ -418,83 +451,86 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
 
         unsigned n_ov = 0, n_hit = 0;
         for (int s = 0; s < sub; ++s) {
-            const int64_t e = it.first_c + (int64_t)s * K1_THREADS + tid;
-            if (it.first_c + (int64_t)s * K1_THREADS > it.c_hi) break;  // block-uniform
-            const bool valid = e <= it.c_hi;
-            Cand r;
-            int unsafe_r = 0;
-            if (valid) {
-                r.ts = L.e.ts[e]; r.te = L.e.te[e];
-                r.sx = L.e.sx[e]; r.sy = L.e.sy[e]; r.sz = L.e.sz[e];
-                r.ex = L.e.ex[e]; r.ey = L.e.ey[e]; r.ez = L.e.ez[e];
-                r.dx = L.e.dx[e]; r.dy = L.e.dy[e]; r.dz = L.e.dz[e];
-                r.rcp = L.e.rcp[e];
-                r.ext = __dsub_rn(r.te, r.ts);
-                unsafe_r = L.e.unsafe[e];
-            } else {
-                r.ts = INFINITY; r.te = -INFINITY; r.ext = 1.0; r.rcp = 1.0;
-                r.sx = r.sy = r.sz = r.ex = r.ey = r.ez = r.dx = r.dy = r.dz = 0.0;
+            const int64_t base = it.first_c + (int64_t)s * STRIDE;
+            if (base > it.c_hi) break;  // block-uniform
+            const int64_t wbase = base + (int64_t)warp * 32 * K1_CPT;
+            Cand r[K1_CPT];
+            uint64_t key_base[K1_CPT];
+            bool valid_any = false, unsafe_r = false;
+            double wmin = INFINITY, wmax = -INFINITY, wmin_te = INFINITY, wmax_ts = -INFINITY;
+#pragma unroll
+            for (int k = 0; k < K1_CPT; ++k) {
+                const int64_t e = wbase + (int64_t)k * 32 + lane;
+                const bool valid = e <= it.c_hi;
+                if (valid) {
+                    r[k].ts = L.e.ts[e]; r[k].te = L.e.te[e];
+                    r[k].sx = L.e.sx[e]; r[k].sy = L.e.sy[e]; r[k].sz = L.e.sz[e];
+                    r[k].ex = L.e.ex[e]; r[k].ey = L.e.ey[e]; r[k].ez = L.e.ez[e];
+                    r[k].dx = L.e.dx[e]; r[k].dy = L.e.dy[e]; r[k].dz = L.e.dz[e];
+                    r[k].rcp = L.e.rcp[e];
+                    r[k].ext = __dsub_rn(r[k].te, r[k].ts);
+                    unsafe_r |= L.e.unsafe[e] != 0;
+                    wmin = fmin(wmin, r[k].ts);
+                    wmax = fmax(wmax, r[k].te);
+                    wmin_te = fmin(wmin_te, r[k].te);
+                    wmax_ts = fmax(wmax_ts, r[k].ts);
+                } else {
+                    r[k].ts = INFINITY; r[k].te = -INFINITY; r[k].ext = 1.0; r[k].rcp = 1.0;
+                    r[k].sx = r[k].sy = r[k].sz = r[k].ex = r[k].ey = r[k].ez = 0.0;
+                    r[k].dx = r[k].dy = r[k].dz = 0.0;
+                }
+                valid_any |= valid;
+                // key of (b, e_off, q_off = it.q0 + j) without the j term
+                key_base[k] = make_key(L, it.b, e - L.plan.first[it.b], it.q0);
             }
             if (L.noop) continue;
-            // warp window over the staged queries
-            double wmin = valid ? r.ts : INFINITY, wmax = valid ? r.te : -INFINITY;
-            for (int o = 16; o; o >>= 1) {
-                wmin = fmin(wmin, __shfl_xor_sync(0xffffffffu, wmin, o));
-                wmax = fmax(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
-            }
-            if (!__any_sync(0xffffffffu, valid)) continue;
-            int jlo = 0, jhi = it.nt;
+            if (!__any_sync(0xffffffffu, valid_any)) continue;
+            // warp window over the staged queries and its start-time case ranges
+            wmin = warp_min(wmin);
+            wmax = warp_max(wmax);
+            wmin_te = warp_min(wmin_te);
+            wmax_ts = warp_max(wmax_ts);
+            int jlo = 0, jhi = it.nt, ja = it.nt, jb = it.nt;
             if (L.window_ok) {
-                jlo = lower_bound_pm(pm, it.nt, wmin);
-                jhi = upper_bound_ts(sq, it.nt, wmax);
-            }
-            const int64_t e_off = e - L.plan.first[it.b];
-            // key of (b, e_off, q_off = it.q0 + j) without the j term
-            const uint64_t key_base = make_key(L, it.b, e_off, it.q0);
-            double wmin_te = valid ? r.te : INFINITY;
-            double wmax_ts = valid ? r.ts : -INFINITY;
-            for (int o = 16; o; o >>= 1) {
-                wmin_te = fmin(wmin_te, __shfl_xor_sync(0xffffffffu, wmin_te, o));
-                wmax_ts = fmax(wmax_ts, __shfl_xor_sync(0xffffffffu, wmax_ts, o));
-            }
-            // TA case boundaries within [jlo, jhi)
-            int ja = jhi, jb = jhi;
-            if (L.window_ok) {
-                ja = lower_bound_ts(sq, it.nt, wmin);   // first query with cts >= min lane ts
-                jb = upper_bound_ts(sq, it.nt, wmax_ts); // first query with cts >  max lane ts
-                ja = ja < jlo ? jlo : (ja > jhi ? jhi : ja);
-                jb = jb < ja ? ja : (jb > jhi ? jhi : jb);
+                jlo = lower_bound_pm(pm, it.nt, wmin);   // running max te >= min ts
+                jhi = upper_bound_ts(sq, it.nt, wmax);   // first query starting after max te
+                if (jhi < jlo) jhi = jlo;
+                ja = clampi(lower_bound_ts(sq, it.nt, wmin), jlo, jhi);  // first cts >= min ts
+                jb = clampi(upper_bound_ts(sq, it.nt, wmax_ts), ja, jhi); // first cts >  max ts
             } else {
                 ja = jlo;
+                jb = jhi;  // everything in the generic (mixed) range
             }
             const bool slow = unsafe_q || __any_sync(0xffffffffu, unsafe_r);
-            // tb case of a whole range: every query of [ja0, ja1) ends before
-            // all candidates (running max < min te) or after all of them
-            // (suffix min > max te) — the common case for equal-length steps
+            // tb case of a whole range: every query of the TA_C range ends
+            // before all candidates (running max < min te), or every query of
+            // the TA_R range ends after all of them (suffix min > max te)
             const bool c_tb_r = jlo < ja && pm[ja - 1] < wmin_te;
             const bool r_tb_c = jb < jhi && sm[jb] > wmax;
             if (slow) {
                 pair_run<TA_C, TB_DYN, true, true>(L, sq, jlo, ja, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
                 pair_run<TA_BOTH, TB_DYN, true, true>(L, sq, ja, jb, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
                 pair_run<TA_R, TB_DYN, true, true>(L, sq, jb, jhi, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+                continue;
+            }
+            if (c_tb_r && te_sorted) {
+                // overlap <=> r.ts <= cte; cte ascending over the tile
+#pragma unroll
+                for (int k = 0; k < K1_CPT; ++k)
+                    n_ov += (unsigned)(ja - clampi(lower_bound_te(sq, it.nt, r[k].ts), jlo, ja));
+                pair_run<TA_C, TB_R, false, false>(L, sq, jlo, ja, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
             } else {
-                if (c_tb_r && te_sorted) {
-                    // overlap <=> r.ts <= cte; cte ascending over the tile
-                    const int k = lower_bound_te(sq, it.nt, r.ts);
-                    n_ov += (unsigned)(ja - (k < jlo ? jlo : (k > ja ? ja : k)));
-                    pair_run<TA_C, TB_R, false, false>(L, sq, jlo, ja, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
-                } else {
-                    pair_run<TA_C, TB_DYN, false, true>(L, sq, jlo, ja, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
-                }
-                pair_run<TA_BOTH, TB_DYN, false, true>(L, sq, ja, jb, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
-                if (r_tb_c) {
-                    // overlap <=> cts <= r.te; cts ascending over the tile
-                    const int k = upper_bound_ts(sq, it.nt, r.te);
-                    n_ov += (unsigned)((k < jb ? jb : (k > jhi ? jhi : k)) - jb);
-                    pair_run<TA_R, TB_C, false, false>(L, sq, jb, jhi, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
-                } else {
-                    pair_run<TA_R, TB_DYN, false, true>(L, sq, jb, jhi, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
-                }
+                pair_run<TA_C, TB_DYN, false, true>(L, sq, jlo, ja, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+            }
+            pair_run<TA_BOTH, TB_DYN, false, true>(L, sq, ja, jb, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+            if (r_tb_c) {
+                // overlap <=> cts <= r.te; cts ascending over the tile
+#pragma unroll
+                for (int k = 0; k < K1_CPT; ++k)
+                    n_ov += (unsigned)(clampi(upper_bound_ts(sq, it.nt, r[k].te), jb, jhi) - jb);
+                pair_run<TA_R, TB_C, false, false>(L, sq, jb, jhi, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+            } else {
+                pair_run<TA_R, TB_DYN, false, true>(L, sq, jb, jhi, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
             }
         }
         // per-batch counters (64-bit)
@@ -520,6 +556,8 @@ int k1_blocks_per_sm() {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k1_pairs, K1_THREADS, 0);
     return n > 0 ? n : 1;
 }
+
+int k1_candidates_per_thread() { return K1_CPT; }
 
 void launch_k1(const K1Launch &L, int grid, cudaStream_t st) {
     k1_pairs<<<grid, K1_THREADS, 0, st>>>(L);

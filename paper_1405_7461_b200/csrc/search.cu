@@ -184,7 +184,7 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     launch_ranges(db, db->q, plan, spans_given, st);
     const int bps = k1_blocks_per_sm();
     const int slots = sm_count(db->device) * bps;
-    launch_plan_items(plan, slots, st);
+    launch_plan_items(plan, slots, K1_THREADS * k1_candidates_per_thread(), st);
     launches += spans_given ? 1 : 2;
 
     db->counters.reserve(64, st);

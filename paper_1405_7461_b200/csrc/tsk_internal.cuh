@@ -190,12 +190,16 @@ struct K1Launch {
 };
 
 void launch_ranges(tsk_db *db, const Soa &q, SearchPlanDev &p, bool spans_given, cudaStream_t st);
-void launch_plan_items(SearchPlanDev &p, int sm_count, cudaStream_t st);
+void launch_plan_items(SearchPlanDev &p, int slots, int stride, cudaStream_t st);
 void launch_qrec(const Soa &q, QRec *out, cudaStream_t st);
 void launch_k1(const K1Launch &L, int grid, cudaStream_t st);
 int k1_blocks_per_sm();
+int k1_candidates_per_thread();
 
-constexpr int K1_THREADS = 256;
+#ifndef K1_THREADS_DEF
+#define K1_THREADS_DEF 256
+#endif
+constexpr int K1_THREADS = K1_THREADS_DEF;
 constexpr int K1_TQ = 256;        // queries per tile staged in shared memory
 constexpr int K1_MAX_SUB = 8;     // candidate sub-tiles (of K1_THREADS) per item
 
