@@ -266,13 +266,21 @@ def run_ours(args, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TSK_BENCH_DEVICE pins every rank to one GPU (multi-rank smoke test on a
+    # single-GPU box; the timing collectives then run over gloo)
+    forced = os.environ.get("TSK_BENCH_DEVICE")
+    if forced is not None:
+        local = int(forced)
     dist = None
     if world > 1:
         import torch
         import torch.distributed as tdist
 
         torch.cuda.set_device(local)
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if forced is None:
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            tdist.init_process_group("gloo")
         dist = tdist
     tsk.set_device(local)
     d = cfg["d"] if args.d is None else args.d
@@ -302,23 +310,20 @@ def run_ours(args, cfg):
         if dist is not None:
             dist.barrier()
 
-    def allmax(x: float) -> float:
+    def _reduce(x: float, op) -> float:
         if dist is None:
             return x
         import torch
 
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if forced is not None else "cuda")
+        dist.all_reduce(t, op=op)
         return float(t.item())
+
+    def allmax(x: float) -> float:
+        return _reduce(x, dist.ReduceOp.MAX if dist else None)
 
     def allsum(x: float) -> float:
-        if dist is None:
-            return x
-        import torch
-
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
+        return _reduce(x, dist.ReduceOp.SUM if dist else None)
 
     fp64 = _native.probe_fp64(local)
     fp64_peak = max(fp64.values())
@@ -370,6 +375,7 @@ def run_ours(args, cfg):
         assert st.interactions_computed == my_ints
     t_e2e = allmax(e2e_s)
     e2e_value = total_ints / t_e2e if t_e2e > 0 else 0.0
+    total_hits = allsum(float(hits))  # every rank joins every collective
 
     # roofline of the dominant kernel (K1), this rank
     k1_s = k1_ms / 1e3
@@ -415,7 +421,7 @@ def run_ours(args, cfg):
                 "workload": f"{args.config}: {cfg['desc']}", "entries": len(store),
                 "queries": len(queries), "batches": len(plan.batches), "d": d, "s": S_BATCH,
                 "m": M_BINS, "interactions_per_step": int(total_ints / args.steps),
-                "hits_per_step": int(allsum(float(hits)) / args.steps),
+                "hits_per_step": int(total_hits / args.steps),
                 "l2": "inputs larger than L2 (entry SoA 112 B/segment resident in HBM)",
                 "parallelism": f"dp{world} (contiguous interaction-balanced batch shards; no collective)",
             },
