@@ -150,6 +150,47 @@ __global__ void k_qrec(int64_t n, const double *__restrict__ ts, const double *_
     }
 }
 
+// Queries: hoisted invariants straight into the shared-memory records (one
+// pass, no host sync); flags[0] |= 1 when the start times are not sorted
+// (the pair kernel then disables its windows).
+__global__ void k_qprep(int64_t n, const double *__restrict__ ts, const double *__restrict__ te,
+                        const double *__restrict__ sx, const double *__restrict__ sy,
+                        const double *__restrict__ sz, const double *__restrict__ ex,
+                        const double *__restrict__ ey, const double *__restrict__ ez,
+                        QRec *__restrict__ out, int *flags) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        QRec r;
+        r.ts = ts[i];
+        r.te = te[i];
+        r.sx = sx[i];
+        r.sy = sy[i];
+        r.sz = sz[i];
+        r.ex = ex[i];
+        r.ey = ey[i];
+        r.ez = ez[i];
+        r.dx = __dsub_rn(r.ex, r.sx);
+        r.dy = __dsub_rn(r.ey, r.sy);
+        r.dz = __dsub_rn(r.ez, r.sz);
+        r.ext = __dsub_rn(r.te, r.ts);
+        r.rcp = r.ext > 0.0 ? __drcp_rn(r.ext) : 0.0;
+        bool bad = mag_bad(r.ts) || mag_bad(r.te) || (r.ext > 0.0 && mag_bad(r.ext)) ||
+                   fabs(r.sx) > 0x1p1000 || fabs(r.sy) > 0x1p1000 || fabs(r.sz) > 0x1p1000 ||
+                   fabs(r.ex) > 0x1p1000 || fabs(r.ey) > 0x1p1000 || fabs(r.ez) > 0x1p1000;
+        r.flag = bad ? 1.0 : 0.0;
+        out[i] = r;
+        if (i + 1 < n && ts[i + 1] < r.ts) atomicOr(&flags[0], 1);
+    }
+}
+
+void launch_qprep(const Soa &q, QRec *out, int *flags, cudaStream_t st) {
+    TSK_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), st));
+    if (q.n == 0) return;
+    int grid = (int)std::min<int64_t>((q.n + 255) / 256, 148 * 8);
+    k_qprep<<<grid, 256, 0, st>>>(q.n, q.ts, q.te, q.sx, q.sy, q.sz, q.ex, q.ey, q.ez, out, flags);
+    TSK_CUDA(cudaGetLastError());
+}
+
 void launch_qrec(const Soa &q, QRec *out, cudaStream_t st) {
     if (q.n == 0) return;
     int grid = (int)std::min<int64_t>((q.n + 255) / 256, 148 * 8);

@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
             wmin_te = warp_min(wmin_te);
             wmax_ts = warp_max(wmax_ts);
             int jlo = 0, jhi = it.nt, ja = it.nt, jb = it.nt;
-            if (L.window_ok) {
+            if (!*L.q_unsorted) {
                 jlo = lower_bound_pm(pm, it.nt, wmin);   // running max te >= min ts
                 jhi = upper_bound_ts(sq, it.nt, wmax);   // first query starting after max te
                 if (jhi < jlo) jhi = jlo;

@@ -14,6 +14,8 @@
 #include <cub/cub.cuh>
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -118,6 +120,37 @@ __global__ void k_iota(int64_t n, uint32_t *v) {
         v[i] = (uint32_t)i;
 }
 
+// Opt-in phase trace (TSK_TRACE=1): CUDA events at phase boundaries on the
+// db stream, printed to stderr when the call completes.
+struct Trace {
+    bool on = false;
+    cudaStream_t st = nullptr;
+    std::vector<std::pair<const char *, cudaEvent_t>> marks;
+    explicit Trace(cudaStream_t s) : st(s) {
+        const char *v = getenv("TSK_TRACE");
+        on = v && *v && *v != '0';
+    }
+    void mark(const char *name) {
+        if (!on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        marks.emplace_back(name, e);
+    }
+    ~Trace() {
+        if (!on || marks.empty()) return;
+        cudaEventSynchronize(marks.back().second);
+        fprintf(stderr, "[tsk trace]");
+        for (size_t i = 1; i < marks.size(); ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second);
+            fprintf(stderr, " %s=%.3f", marks[i].first, ms);
+        }
+        fprintf(stderr, " (ms)\n");
+        for (auto &m : marks) cudaEventDestroy(m.second);
+    }
+};
+
 static int sm_count(int device) {
     int n = 0;
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
@@ -153,18 +186,21 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     TSK_REQUIRE(bb + major_bits + minor_bits <= 64, "result key wider than 64 bits");
 
     int64_t launches = 0;
+    Trace tr(st);
+    tr.mark("start");
     TSK_CUDA(cudaEventRecord(db->ev0, st));
     if (flags & TSK_QUERIES_RESIDENT) {
         TSK_REQUIRE(db->q.n == nq && db->q_rec.p, "no resident query set of this size");
     } else {
-        // queries → device SoA (+ hoisted invariants) → shared-memory records
+        // queries → device SoA → shared-memory records with hoisted invariants
         soa_alloc(db->q, nq, true, st);
         soa_upload(db->q, qc, st);
-        soa_hoist(db->q, st);
         db->q_rec.reserve((size_t)nq * sizeof(QRec), st);
-        launch_qrec(db->q, db->q_rec.as<QRec>(), st);
-        launches += 2;
+        db->counters.reserve(64, st);
+        launch_qprep(db->q, db->q_rec.as<QRec>(), db->counters.as<int>() + 8, st);
+        launches += 1;
     }
+    tr.mark("queries");
 
     // batch table: lo hi first last item_off(nb+1) meta(4) ovl hits
     size_t nbz = (size_t)nb;
@@ -186,9 +222,10 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     const int slots = sm_count(db->device) * bps;
     launch_plan_items(plan, slots, K1_THREADS * k1_candidates_per_thread(), st);
     launches += spans_given ? 1 : 2;
+    tr.mark("ranges+items");
 
     db->counters.reserve(64, st);
-    unsigned long long *d_ctr = db->counters.as<unsigned long long>();  // [0] items [1] hits
+    unsigned long long *d_ctr = db->counters.as<unsigned long long>();  // [0] items [1] hits; int[8] = q unsorted
     uint64_t cap = db->recs.bytes / 24;
     if (cap < (uint64_t(1) << 20)) {
         db->recs.reserve((size_t(1) << 20) * 24, st);
@@ -205,7 +242,7 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     L.minor_bits = minor_bits;
     L.query_major = query_major;
     L.noop = (flags & TSK_NOOP) ? 1 : 0;
-    L.window_ok = db->q.sorted;
+    L.q_unsorted = db->counters.as<int>() + 8;
     unsigned long long h_hits = 0;
     float k1_ms = 0.f;
     for (int attempt = 0;; ++attempt) {
@@ -221,6 +258,7 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
         TSK_CUDA(cudaEventRecord(db->ev_k1, st));
         TSK_CUDA(cudaMemcpyAsync(&h_hits, d_ctr + 1, 8, cudaMemcpyDeviceToHost, st));
         TSK_CUDA(cudaStreamSynchronize(st));
+        tr.mark("k1");
         float ms = 0.f;
         cudaEventElapsedTime(&ms, db->ev_k0, db->ev_k1);
         k1_ms += ms;
@@ -237,16 +275,13 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     res->n = nh;
     res->nb = nb;
     res->k1_ms = k1_ms;
-    res->per_batch.resize(nbz * 4);
-    {
-        std::vector<int64_t> tmp(nbz * 4);
-        TSK_CUDA(cudaMemcpyAsync(tmp.data(), d_first, nbz * 8, cudaMemcpyDeviceToHost, st));
-        TSK_CUDA(cudaMemcpyAsync(tmp.data() + nbz, d_last, nbz * 8, cudaMemcpyDeviceToHost, st));
-        TSK_CUDA(cudaMemcpyAsync(tmp.data() + 2 * nbz, d_ovl, nbz * 8, cudaMemcpyDeviceToHost, st));
-        TSK_CUDA(cudaMemcpyAsync(tmp.data() + 3 * nbz, d_hits, nbz * 8, cudaMemcpyDeviceToHost, st));
-        // host copy happens after the final sync below
-        res->per_batch.swap(tmp);
-    }
+    // per-batch first/last/ovl/hits are contiguous on the device (d_first .. d_hits
+    // are laid out first,last,item_off,meta,ovl,hits): copy first/last and ovl/hits
+    size_t pb_got = 0;
+    res->pb_host = static_cast<int64_t *>(pin_alloc(nbz * 4 * 8, &pb_got));
+    res->pb_bytes = pb_got;
+    TSK_CUDA(cudaMemcpyAsync(res->pb_host, d_first, nbz * 16, cudaMemcpyDeviceToHost, st));
+    TSK_CUDA(cudaMemcpyAsync(res->pb_host + 2 * nbz, d_ovl, nbz * 16, cudaMemcpyDeviceToHost, st));
     const bool want_ord = flags & TSK_WANT_ORDINALS;
     const bool on_device = flags & TSK_RESULTS_ON_DEVICE;
     const int ncols = want_ord ? 8 : 6;
@@ -319,10 +354,13 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
         g.minor_bits = minor_bits;
         g.query_major = query_major;
         int gg = (int)std::min<int64_t>((nh + 255) / 256, 148 * 8);
+        tr.mark("sort");
         k_gather<<<gg, 256, 0, st>>>(g);
         TSK_CUDA(cudaGetLastError());
         ++launches;
+        tr.mark("gather");
         if (!on_device) TSK_CUDA(cudaMemcpyAsync(res->host, ob, cb * ncols, cudaMemcpyDeviceToHost, st));
+        tr.mark("d2h");
     }
     TSK_CUDA(cudaEventRecord(db->ev1, st));
     TSK_CUDA(cudaStreamSynchronize(st));
@@ -404,7 +442,7 @@ extern "C" int tsk_result_per_batch(const tsk_result *r, int64_t *per_batch) {
     // stored column-wise (first[], last[], ovl[], hits[]); returned row-wise
     const int64_t nb = r->nb;
     for (int64_t b = 0; b < nb; ++b)
-        for (int k = 0; k < 4; ++k) per_batch[b * 4 + k] = r->per_batch[k * nb + b];
+        for (int k = 0; k < 4; ++k) per_batch[b * 4 + k] = r->pb_host[k * nb + b];
     return TSK_OK;
 }
 
@@ -428,6 +466,7 @@ extern "C" int tsk_result_columns(const tsk_result *r, const int64_t **query_tra
 extern "C" void tsk_result_free(tsk_result *r) {
     if (!r) return;
     pin_free(r->host, r->host_bytes);
+    pin_free(r->pb_host, r->pb_bytes);
     delete r;
 }
 

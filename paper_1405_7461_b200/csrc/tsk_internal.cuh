@@ -110,7 +110,8 @@ struct tsk_result {
     int64_t n = 0, nb = 0;
     double device_ms = 0, k1_ms = 0;
     int64_t launches = 0;
-    std::vector<int64_t> per_batch;  // nb × 4
+    int64_t *pb_host = nullptr;      // pinned nb × 4 (first[], last[], ovl[], hits[])
+    size_t pb_bytes = 0;
     void *host = nullptr;            // pinned block holding the columns
     size_t host_bytes = 0;
     int64_t *qtraj = nullptr, *qseg = nullptr, *etraj = nullptr, *eseg = nullptr;
@@ -186,12 +187,13 @@ struct K1Launch {
     int major_bits, minor_bits;  // key = b << (major+minor) | major << minor | minor
     int query_major;             // 0: (b, entry, query); 1: (b, query, entry)
     int noop;
-    int window_ok;
+    const int *q_unsorted;  // device flag: query start times not sorted -> no windows
 };
 
 void launch_ranges(tsk_db *db, const Soa &q, SearchPlanDev &p, bool spans_given, cudaStream_t st);
 void launch_plan_items(SearchPlanDev &p, int slots, int stride, cudaStream_t st);
 void launch_qrec(const Soa &q, QRec *out, cudaStream_t st);
+void launch_qprep(const Soa &q, QRec *out, int *flags, cudaStream_t st);
 void launch_k1(const K1Launch &L, int grid, cudaStream_t st);
 int k1_blocks_per_sm();
 int k1_candidates_per_thread();
