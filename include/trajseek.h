@@ -115,6 +115,23 @@ int tsk_result_columns(const tsk_result *r, const int64_t **query_traj, const in
                        const int64_t **entry_ord);
 void tsk_result_free(tsk_result *r);
 
+/* Native batch planners over the host copy of the index (host code, no GPU).
+ * Queries are given by their start-sorted ts/te; the index by its non-empty
+ * bin arrays (tsk_index_copy).  Outputs hold up to nq batches: lo/hi query
+ * ordinals, candidate span first/last (-1 when none) and the batch end time.
+ *   tsk_plan_setsplit  mode 0: setsplit_fixed(num_batches)   (planner.py:293-309)
+ *                      mode 1: setsplit_minmax(min, max)     (planner.py:312-358)
+ *   tsk_plan_greedy    variant 0: greedy_min, 1: greedy_max  (planner.py:384-429) */
+int tsk_plan_setsplit(int64_t nq, const double *ts, const double *te, int64_t n_ne,
+                      const double *ne_start, const double *ne_end, const int64_t *ne_first,
+                      const int64_t *ne_last, int mode, int64_t num_batches, int64_t min_size,
+                      int64_t max_size, int64_t *nb_out, int64_t *b_lo, int64_t *b_hi,
+                      int64_t *b_first, int64_t *b_last, double *b_end);
+int tsk_plan_greedy(int64_t nq, const double *ts, const double *te, int64_t n_ne,
+                    const double *ne_start, const double *ne_end, const int64_t *ne_first,
+                    const int64_t *ne_last, int variant, int64_t bound, int64_t *nb_out,
+                    int64_t *b_lo, int64_t *b_hi, int64_t *b_first, int64_t *b_last, double *b_end);
+
 /* Page-locked host memory for query/result staging (cudaHostAlloc). */
 void *tsk_pinned_alloc(int64_t bytes);
 void tsk_pinned_free(void *p);

@@ -61,6 +61,10 @@ SIGNATURES = {
     "tsk_result_columns": ([_P] + [ctypes.POINTER(_P)] * 8, ctypes.c_int),
     "tsk_result_free": ([_P], None),
     "tsk_probe_fp64": ([ctypes.c_int, _PD, _PD, _PD], ctypes.c_int),
+    "tsk_plan_setsplit": ([_I64, _PD, _PD, _I64, _PD, _PD, _PI64, _PI64, ctypes.c_int, _I64, _I64,
+                           _I64, _PI64, _PI64, _PI64, _PI64, _PI64, _PD], ctypes.c_int),
+    "tsk_plan_greedy": ([_I64, _PD, _PD, _I64, _PD, _PD, _PI64, _PI64, ctypes.c_int, _I64, _PI64,
+                         _PI64, _PI64, _PI64, _PI64, _PD], ctypes.c_int),
     "tsk_pinned_alloc": ([_I64], _P),
     "tsk_pinned_free": ([_P], None),
 }
@@ -319,3 +323,29 @@ def pinned_copy(a: np.ndarray) -> np.ndarray:
     out = pinned_empty(a.shape[0], a.dtype)
     out[...] = a
     return out
+
+
+def plan_native(kind: str, ts, te, index, *, num_batches=0, min_size=0, max_size=0, bound=0):
+    """Run a native planner; returns (lo, hi, first, last, end) arrays."""
+    lib = load()
+    ts = np.ascontiguousarray(ts, np.float64)
+    te = np.ascontiguousarray(te, np.float64)
+    nq = ts.shape[0]
+    ne = [np.ascontiguousarray(index._ne_start, np.float64), np.ascontiguousarray(index._ne_end, np.float64),
+          np.ascontiguousarray(index._ne_first, np.int64), np.ascontiguousarray(index._ne_last, np.int64)]
+    out = [np.empty(nq, np.int64) for _ in range(4)] + [np.empty(nq, np.float64)]
+    nb = _I64()
+    common = [nq, ts.ctypes.data_as(_PD), te.ctypes.data_as(_PD), ne[0].shape[0],
+              ne[0].ctypes.data_as(_PD), ne[1].ctypes.data_as(_PD), ne[2].ctypes.data_as(_PI64),
+              ne[3].ctypes.data_as(_PI64)]
+    tail = [ctypes.byref(nb)] + [o.ctypes.data_as(_PI64) for o in out[:4]] + [out[4].ctypes.data_as(_PD)]
+    if kind == "fixed":
+        check(lib.tsk_plan_setsplit(*common, 0, num_batches, 0, 0, *tail))
+    elif kind == "minmax":
+        check(lib.tsk_plan_setsplit(*common, 1, 0, min_size, max_size, *tail))
+    elif kind in ("greedy_min", "greedy_max"):
+        check(lib.tsk_plan_greedy(*common, 0 if kind == "greedy_min" else 1, bound, *tail))
+    else:
+        raise ValueError(kind)
+    k = int(nb.value)
+    return tuple(o[:k] for o in out)

@@ -10,10 +10,13 @@ Same names, arguments, results and DomainError behaviour as
 * ``greedy_min`` / ``greedy_max`` (planner.py:371-429) — free-merge pass,
   then a forward size pass.
 
-The batches are kept in flat arrays linked by prev/next indices; merge
-costs come from the index's candidate ranges (host lookups on the arrays
-the GPU index build copied back; the per-query singleton lookups are done
-vectorised).  The batch table a plan produces feeds the GPU search.
+SetSplit and Greedy run natively by default (C++ in libtrajseek,
+csrc/planner.cu, same heap order and tie-breaking); ``literal=True``
+(SetSplit) and ``native=False`` (Greedy) select the Python implementations
+below, kept as the differential check.  The batches are kept in flat arrays
+linked by prev/next indices; merge costs come from the index's candidate
+ranges (host lookups on the arrays the GPU index build copied back).  The
+batch table a plan produces feeds the GPU search.
 """
 
 from __future__ import annotations
@@ -236,12 +239,37 @@ def _cheapest_rescan(R: _Runs, stop_count: int | None, max_size: int | None) -> 
         live -= 1
 
 
+def _native_plan(queries: SegmentStore, kind: str, index: TemporalIndex, **kw) -> BatchPlan:
+    """The C++ planners of libtrajseek (csrc/planner.cu): same semantics, no Python loop."""
+    from . import _native
+
+    lo, hi, first, last, end = _native.plan_native(kind, queries.ts, queries.te, index, **kw)
+    ts = queries.ts
+    batches = tuple(
+        QueryBatch(a, b, TimeInterval(float(ts[a]), e), None if f < 0 else f, None if f < 0 else l)
+        for a, b, f, l, e in zip(lo.tolist(), hi.tolist(), first.tolist(), last.tolist(), end.tolist())
+    )
+    return BatchPlan(queries, batches)
+
+
+def _native_ok() -> bool:
+    from . import _native
+
+    try:
+        _native.load()
+        return True
+    except (RuntimeError, OSError):
+        return False
+
+
 def setsplit_fixed(queries: SegmentStore, index: TemporalIndex, num_batches: int, *,
                    literal: bool = False) -> BatchPlan:
     """Cheapest-first merging from singletons down to num_batches batches."""
     _check_queries(queries)
     if num_batches < 1:
         raise DomainError(f"num_batches={num_batches} must be >= 1")
+    if not literal and _native_ok():
+        return _native_plan(queries, "fixed", index, num_batches=num_batches)
     R = _Runs(queries, index)
     (_cheapest_rescan if literal else _cheapest_heap)(R, num_batches, None)
     return R.plan()
@@ -257,6 +285,8 @@ def setsplit_minmax(queries: SegmentStore, index: TemporalIndex, min_size: int, 
         raise DomainError(f"min_size={min_size} must be >= 1")
     if max_size < min_size:
         raise DomainError(f"max_size={max_size} must be >= min_size={min_size}")
+    if not literal and _native_ok():
+        return _native_plan(queries, "minmax", index, min_size=min_size, max_size=max_size)
     R = _Runs(queries, index)
     (_cheapest_rescan if literal else _cheapest_heap)(R, None, max_size)
     i = R.head()
@@ -299,10 +329,13 @@ def _free_pass(R: _Runs) -> None:
             i = j
 
 
-def _greedy(queries: SegmentStore, index: TemporalIndex, bound: int, grow) -> BatchPlan:
+def _greedy(queries: SegmentStore, index: TemporalIndex, bound: int, grow, kind=None,
+            native: bool = True) -> BatchPlan:
     _check_queries(queries)
     if bound < 1:
         raise DomainError(f"bound={bound} must be >= 1")
+    if native and kind is not None and _native_ok():
+        return _native_plan(queries, kind, index, bound=bound)
     R = _Runs(queries, index)
     _free_pass(R)
     i = R.head()
@@ -315,11 +348,13 @@ def _greedy(queries: SegmentStore, index: TemporalIndex, bound: int, grow) -> Ba
     return R.plan()
 
 
-def greedy_min(queries: SegmentStore, index: TemporalIndex, bound: int) -> BatchPlan:
+def greedy_min(queries: SegmentStore, index: TemporalIndex, bound: int, *,
+               native: bool = True) -> BatchPlan:
     """Free merges, then grow each batch until it holds at least ``bound``."""
-    return _greedy(queries, index, bound, lambda size, b: size < b)
+    return _greedy(queries, index, bound, lambda size, b: size < b, "greedy_min", native)
 
 
-def greedy_max(queries: SegmentStore, index: TemporalIndex, bound: int) -> BatchPlan:
+def greedy_max(queries: SegmentStore, index: TemporalIndex, bound: int, *,
+               native: bool = True) -> BatchPlan:
     """Free merges, then grow each batch until it exceeds ``bound``."""
-    return _greedy(queries, index, bound, lambda size, b: size <= b)
+    return _greedy(queries, index, bound, lambda size, b: size <= b, "greedy_max", native)

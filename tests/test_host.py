@@ -314,3 +314,39 @@ def test_galaxy_shape():
     assert len(g) == 50 * 40
     assert np.all(np.diff(g.ts) >= 0)
     assert np.allclose(g.te - g.ts, 1.0)
+
+
+# ── native planners (csrc/planner.cu) vs the Python implementations ─────────
+
+
+@pytest.mark.parametrize("seed", [41, 47, 59, 61])
+def test_native_planners_equal_python_planners(seed):
+    from helpers import random_store_arrays
+
+    rng = np.random.default_rng(seed)
+    e = _store(random_store_arrays(rng, 400))
+    q = _store(random_store_arrays(rng, 150, first_traj=10_000))
+    ix = host_index(e, 24)
+    pairs = [
+        (tsk.setsplit_fixed(q, ix, 13), tsk.setsplit_fixed(q, ix, 13, literal=True)),
+        (tsk.setsplit_minmax(q, ix, 4, 17), tsk.setsplit_minmax(q, ix, 4, 17, literal=True)),
+        (tsk.setsplit_max(q, ix, 9), tsk.setsplit_max(q, ix, 9, literal=True)),
+        (tsk.greedy_min(q, ix, 7), tsk.greedy_min(q, ix, 7, native=False)),
+        (tsk.greedy_max(q, ix, 7), tsk.greedy_max(q, ix, 7, native=False)),
+    ]
+    for a, b in pairs:
+        assert a.batches == b.batches
+
+
+def test_native_planners_on_generated_exp_profile():
+    store = tsk.generate(tsk.make_profile("exp", 200, seed=71))
+    pool = tsk.generate(tsk.make_profile("exp", 100, seed=72))
+    q = tsk.sample_queries(pool, 30, seed=73)
+    ix = host_index(store, 1000)
+    from paper_1405_7461_b200 import planner as P
+
+    R = P._Runs(q, ix)
+    P._cheapest_heap(R, None, 120)
+    assert tsk.setsplit_max(q, ix, 120).batches == R.plan().batches
+    assert tsk.greedy_max(q, ix, 120).batches == tsk.greedy_max(q, ix, 120, native=False).batches
+    assert tsk.greedy_min(q, ix, 120).batches == tsk.greedy_min(q, ix, 120, native=False).batches
