@@ -63,6 +63,16 @@ CONFIGS = {
 }
 S_BATCH = 120
 M_BINS = 10_000
+
+# Planner settings of config 4: s = 120 throughout.
+PLANNERS = {
+    "periodic": lambda tsk, q, ix: tsk.periodic(q, S_BATCH, ix),
+    "setsplit_fixed": lambda tsk, q, ix: tsk.setsplit_fixed(q, ix, -(-len(q) // S_BATCH)),
+    "setsplit_max": lambda tsk, q, ix: tsk.setsplit_max(q, ix, S_BATCH),
+    "setsplit_minmax": lambda tsk, q, ix: tsk.setsplit_minmax(q, ix, 16, S_BATCH),
+    "greedy_min": lambda tsk, q, ix: tsk.greedy_min(q, ix, S_BATCH),
+    "greedy_max": lambda tsk, q, ix: tsk.greedy_max(q, ix, S_BATCH),
+}
 W_DECIDE, W_HIT = 50, 9  # FP64 flops per overlapping pair / extra per hit
 
 
@@ -171,16 +181,30 @@ def _isnum(s):
 # ── CPU side (reference arm / cpu_baseline): the oracle port ───────────────
 
 
-def cpu_setup(e_cols, q_cols, presorted=False):
+ORACLE_PLANNERS = {
+    "periodic": lambda orc, q, ix: orc.plan_periodic(q, S_BATCH, ix),
+    "setsplit_fixed": lambda orc, q, ix: orc.plan_setsplit_fixed(q, ix, -(-orc.store_len(q) // S_BATCH)),
+    "setsplit_max": lambda orc, q, ix: orc.plan_setsplit_max(q, ix, S_BATCH),
+    "setsplit_minmax": lambda orc, q, ix: orc.plan_setsplit_minmax(q, ix, 16, S_BATCH),
+    "greedy_min": lambda orc, q, ix: orc.plan_greedy(q, ix, S_BATCH, "min"),
+    "greedy_max": lambda orc, q, ix: orc.plan_greedy(q, ix, S_BATCH, "max"),
+}
+
+
+def cpu_setup(e_cols, q_cols, presorted=False, planner="periodic", table=None):
     """Oracle store/index/plan for the reference algorithm (numpy port) plus an
-    evenly spread batch order for sampling."""
+    evenly spread batch order for sampling.  ``table`` reuses an existing
+    plan's (lo, hi) batches instead of re-planning."""
     from oracle import oracle as orc
 
     t0 = time.perf_counter()
     e = orc.make_store(*(e_cols[k] for k in FIELDS), presorted=presorted)
     q = orc.make_store(*(q_cols[k] for k in FIELDS), presorted=presorted)
     ix = orc.index_build(e, M_BINS)
-    plan = orc.plan_periodic(q, S_BATCH, ix)
+    if table is not None:
+        plan = [(int(a), int(b), None, None, None, None) for a, b in zip(*table)]
+    else:
+        plan = ORACLE_PLANNERS[planner](orc, q, ix)
     log(f"[cpu] oracle store/index/plan in {time.perf_counter() - t0:.1f}s, {len(plan)} batches")
     order = _spread(len(plan))
     return e, q, ix, plan, order
@@ -213,7 +237,7 @@ def run_reference(args, cfg):
         return
     workers = os.cpu_count() or 1
     e_cols, q_cols = workload_columns(cfg)
-    e, q, ix, plan, order = cpu_setup(e_cols, q_cols)
+    e, q, ix, plan, order = cpu_setup(e_cols, q_cols, planner=args.planner)
     # one step = a bounded sample of batches (~budget seconds of CPU work)
     budget = float(os.environ.get("TSK_REF_STEP_S", "8"))
     cursor = 0
@@ -292,7 +316,9 @@ def run_ours(args, cfg):
     del e_cols, q_cols
     t_gen = time.perf_counter() - t0
     index = tsk.build_index(store, M_BINS)
-    plan = tsk.periodic(queries, S_BATCH, index)
+    t_plan0 = time.perf_counter()
+    plan = PLANNERS[args.planner](tsk, queries, index)
+    t_plan = time.perf_counter() - t_plan0
     t_setup = time.perf_counter() - t0
     ints_all = np.array([b.interactions for b in plan.batches], dtype=np.int64)
     b0, b1 = shard_bounds(ints_all, world)[rank]
@@ -358,7 +384,8 @@ def run_ours(args, cfg):
     value = total_ints / t_dev if t_dev > 0 else 0.0
 
     # ── e2e: public drop-in call, pinned host inputs, results to host ──
-    for _ in range(max(1, args.warmup // 2)):
+    # warm-up also fills the pinned result pool (two live results alternate)
+    for _ in range(max(2, args.warmup)):
         if mine is not None:
             tsk.run_search(store, index, e2e_plan, d)
     barrier()
@@ -395,7 +422,8 @@ def run_ours(args, cfg):
     if world == 1 and not args.no_cpu_baseline and rank == 0:
         workers = os.cpu_count() or 1
         sorted_cols = lambda s: {k: getattr(s, k) for k in FIELDS}  # noqa: E731
-        e, q, ix, oplan, order = cpu_setup(sorted_cols(store), sorted_cols(queries), presorted=True)
+        e, q, ix, oplan, order = cpu_setup(sorted_cols(store), sorted_cols(queries), presorted=True,
+                                           table=plan.table())
         ints = secs = 0.0
         nbat = 0
         budget = float(os.environ.get("TSK_CPU_BASELINE_S", "20"))
@@ -420,6 +448,7 @@ def run_ours(args, cfg):
             "config": {
                 "workload": f"{args.config}: {cfg['desc']}", "entries": len(store),
                 "queries": len(queries), "batches": len(plan.batches), "d": d, "s": S_BATCH,
+                "planner": args.planner, "plan_s": t_plan,
                 "m": M_BINS, "interactions_per_step": int(total_ints / args.steps),
                 "hits_per_step": int(total_hits / args.steps),
                 "l2": "inputs larger than L2 (entry SoA 112 B/segment resident in HBM)",
@@ -458,6 +487,8 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c5")
     ap.add_argument("--d", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--planner", choices=sorted(PLANNERS), default="periodic",
+                    help="batch planner (config 4 compares them; PAPER.md Table 3)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
