@@ -329,3 +329,49 @@ def test_batches_without_candidates_and_large_batches():
         _same(res, want)
         assert st.interactions_computed == wst["interactions"]
         assert [t.interactions for t in st.per_batch] == [p[3] for p in wst["per_batch"]]
+
+
+class _RawStore:
+    """Column holder that bypasses SegmentStore's sort (exercises the C-ABI
+    with start times out of order, where K1 must disable its windows)."""
+
+    def __init__(self, arr):
+        for k in ("traj", "seg", "xs", "ys", "zs", "ts", "xe", "ye", "ze", "te"):
+            setattr(self, k, np.ascontiguousarray(arr[k]))
+
+    def __len__(self):
+        return int(self.traj.shape[0])
+
+
+def test_unsorted_queries_through_the_c_abi():
+    from paper_1405_7461_b200 import _native
+
+    rng = np.random.default_rng(17)
+    store = _store(random_store_arrays(rng, 900))
+    qarr = random_store_arrays(rng, 300, first_traj=50_000)  # not sorted by ts
+    assert np.any(np.diff(qarr["ts"]) < 0)
+    raw = _RawStore(qarr)
+    res = _native.search(store.device(), raw, [0], [299], [0], [899], 3.0,
+                         _native.TSK_SPANS_GIVEN | _native.TSK_ORDER_REFERENCE | _native.TSK_WANT_ORDINALS)
+    ri, ci, tb, te, tm, sm = orc.pair_mesh(_cols(store), {k: qarr[k] for k in qarr}, 3.0)
+    assert np.array_equal(res.cols["entry_ord"], ri) and np.array_equal(res.cols["query_ord"], ci)
+    assert np.array_equal(res.cols["t_begin"], tb) and np.array_equal(res.cols["t_end"], te)
+    assert int(res.per_batch[0, 2]) == tm * 0 + (900 * 300 - tm)
+
+
+def test_resident_queries_and_device_only_results():
+    from paper_1405_7461_b200.engine import search_device
+
+    store = tsk.generate(tsk.make_profile("uniform", 200, seed=81, timesteps=90))
+    pool = tsk.generate(tsk.make_profile("uniform", 50, seed=82, timesteps=90))
+    q = tsk.sample_queries(pool, 8, seed=83)
+    ix = tsk.build_index(store, 500)
+    plan = tsk.periodic(q, 50, ix)
+    full, st = tsk.run_search(store, ix, plan, 7.0)
+    r1 = search_device(store, ix, plan, 7.0)
+    r2 = search_device(store, ix, plan, 7.0, queries_resident=True)
+    for r in (r1, r2):
+        assert r.n == len(full)
+        assert r.cols["query_traj"] is None  # hits stayed in HBM
+        assert int(r.per_batch[:, 3].sum()) == st.hits
+        assert int(r.per_batch[:, 2].sum()) == st.hits + st.spatial_misses
