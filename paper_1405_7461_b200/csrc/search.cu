@@ -18,6 +18,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <sys/mman.h>
+#include <unistd.h>
+#include <algorithm>
 #include <mutex>
 
 #include "tsk_internal.cuh"
@@ -35,10 +38,40 @@ int fail(int code, const std::string &msg) {
 
 // ── pinned host pool ───────────────────────────────────────────────────────
 
+// Result columns live in page-locked host blocks kept in a pool: pinning
+// costs ~0.2-0.5 s/GB, so steady-state calls reuse blocks.  Large blocks are
+// anonymous mmaps advised onto transparent huge pages and registered with
+// cudaHostRegister (measured 3x cheaper to pin than cudaHostAlloc on the
+// B200 hosts, same 57 GB/s D2H); small ones come from cudaHostAlloc.
 static std::mutex g_pin_mu;
 static std::multimap<size_t, void *> g_pin_free;
+static std::map<void *, int> g_pin_kind;  // 0: cudaHostAlloc, 1: mmap + register
 static size_t g_pin_cached = 0;
-static const size_t kPinCacheMax = size_t(8) << 30;
+static const size_t kMmapAbove = size_t(32) << 20;
+
+static size_t pin_cache_max() {
+    static size_t cap = [] {
+        long pages = sysconf(_SC_PHYS_PAGES), psize = sysconf(_SC_PAGE_SIZE);
+        size_t ram = (pages > 0 && psize > 0) ? (size_t)pages * (size_t)psize : (size_t(64) << 30);
+        return std::max<size_t>(size_t(8) << 30, ram / 4);
+    }();
+    return cap;
+}
+
+static void pin_release(void *p, size_t bytes) {
+    int kind;
+    {
+        std::lock_guard<std::mutex> g(g_pin_mu);
+        kind = g_pin_kind[p];
+        g_pin_kind.erase(p);
+    }
+    if (kind == 1) {
+        cudaHostUnregister(p);
+        munmap(p, bytes);
+    } else {
+        cudaFreeHost(p);
+    }
+}
 
 static void *pin_alloc(size_t bytes, size_t *got) {
     if (bytes == 0) bytes = 64;
@@ -54,20 +87,41 @@ static void *pin_alloc(size_t bytes, size_t *got) {
         }
     }
     void *p = nullptr;
-    TSK_CUDA(cudaHostAlloc(&p, bytes, cudaHostAllocPortable));
+    int kind = 0;
+    if (bytes >= kMmapAbove) {
+        bytes = (bytes + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1);
+        void *m = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+        if (m != MAP_FAILED) {
+            madvise(m, bytes, MADV_HUGEPAGE);
+            if (cudaHostRegister(m, bytes, cudaHostRegisterPortable) == cudaSuccess) {
+                p = m;
+                kind = 1;
+            } else {
+                cudaGetLastError();
+                munmap(m, bytes);
+            }
+        }
+    }
+    if (!p) TSK_CUDA(cudaHostAlloc(&p, bytes, cudaHostAllocPortable));
+    {
+        std::lock_guard<std::mutex> g(g_pin_mu);
+        g_pin_kind[p] = kind;
+    }
     *got = bytes;
     return p;
 }
 
 static void pin_free(void *p, size_t bytes) {
     if (!p) return;
-    std::lock_guard<std::mutex> g(g_pin_mu);
-    if (g_pin_cached + bytes <= kPinCacheMax) {
-        g_pin_free.emplace(bytes, p);
-        g_pin_cached += bytes;
-    } else {
-        cudaFreeHost(p);
+    {
+        std::lock_guard<std::mutex> g(g_pin_mu);
+        if (g_pin_cached + bytes <= pin_cache_max()) {
+            g_pin_free.emplace(bytes, p);
+            g_pin_cached += bytes;
+            return;
+        }
     }
+    pin_release(p, bytes);
 }
 
 static int bits_for(int64_t count) {  // bits to hold 0..count-1
