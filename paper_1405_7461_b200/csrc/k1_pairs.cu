@@ -290,16 +290,38 @@ __device__ __forceinline__ void pair_run(const K1Launch &L, const QRec *__restri
             any |= cand[k];
         }
         if (__ballot_sync(0xffffffffu, any)) {
+            // Second filter, paid only here: the quadratic q(λ) = aa λ² + 2 dot λ + e
+            // can reach 0 on [0, 1] only if q(0) <= 0, q(1) <= 0 or its vertex
+            // -dot/aa lies in [0, 1].  Outside all three by the relative margin
+            // m = 2^-30 (cc + d² + aa + 2|dot|) — far above the rounding of these
+            // tests — both roots of the computed quadratic lie strictly outside
+            // [0, 1] by more than their own rounding, so the reference's solve
+            // (core.py:536-558) reports a miss.  Flat pairs are always re-solved.
+            bool need[K1_CPT];
+            bool any2 = false;
 #pragma unroll
             for (int k = 0; k < K1_CPT; ++k) {
-                Hit h;
-                h.hit = false;
-                h.tb = h.te = 0.0;
-                if (cand[k]) h = rare_pair(r[k], sq[j], cc[k], aa[k], dot[k], e[k], d2);
-                n_hit += h.hit ? 1u : 0u;
-                append_hit(L, h.hit,
-                           key_base[k] + (L.query_major ? ((uint64_t)j << L.minor_bits) : (uint64_t)j),
-                           h.tb, h.te, lane);
+                const double mag = __dadd_rn(__dadd_rn(cc[k], d2), __dadd_rn(aa[k], 2.0 * fabs(dot[k])));
+                const double m = mag * 0x1p-30;
+                const double q1 = __dadd_rn(__dadd_rn(e[k], dot[k]), __dadd_rn(dot[k], aa[k]));
+                const bool vertex_in = dot[k] <= m && __dadd_rn(dot[k], aa[k]) >= -m;
+                const bool flat = Q.ts == r[k].te || r[k].ts == Q.te || Q.ts == Q.te || r[k].ts == r[k].te;
+                need[k] = cand[k] && (flat || !(e[k] > m) || !(q1 > m) || vertex_in);
+                any2 |= need[k];
+            }
+            if (__ballot_sync(0xffffffffu, any2)) {
+#pragma unroll
+                for (int k = 0; k < K1_CPT; ++k) {
+                    if (!__ballot_sync(0xffffffffu, need[k])) continue;
+                    Hit h;
+                    h.hit = false;
+                    h.tb = h.te = 0.0;
+                    if (need[k]) h = rare_pair(r[k], sq[j], cc[k], aa[k], dot[k], e[k], d2);
+                    n_hit += h.hit ? 1u : 0u;
+                    append_hit(L, h.hit,
+                               key_base[k] + (L.query_major ? ((uint64_t)j << L.minor_bits) : (uint64_t)j),
+                               h.tb, h.te, lane);
+                }
             }
         }
     }
