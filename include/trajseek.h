@@ -47,7 +47,8 @@ enum {
     TSK_SPANS_GIVEN = 1u << 3,   /* b_first/b_last supplied by the caller (execute_batch)        */
     TSK_WANT_ORDINALS = 1u << 4, /* also return query/entry ordinals (pair_intervals)            */
     TSK_QUERIES_RESIDENT = 1u << 5,/* reuse the query set uploaded by the previous call on this db */
-    TSK_RESULTS_ON_DEVICE = 1u << 6 /* leave hit columns in HBM (no D2H): device-throughput runs */
+    TSK_RESULTS_ON_DEVICE = 1u << 6,/* leave hit columns in HBM (no D2H): device-throughput runs */
+    TSK_ORDER_CANONICAL = 1u << 7 /* items in ResultSet.canonical_order (core.py:290-294)        */
 };
 
 /* Index extent rules (index.py:26) */
@@ -131,6 +132,12 @@ int tsk_plan_greedy(int64_t nq, const double *ts, const double *te, int64_t n_ne
                     const double *ne_start, const double *ne_end, const int64_t *ne_first,
                     const int64_t *ne_last, int variant, int64_t bound, int64_t *nb_out,
                     int64_t *b_lo, int64_t *b_hi, int64_t *b_first, int64_t *b_last, double *b_end);
+
+/* Canonical order (core.py:290-294: query ids, entry ids, t_begin, t_end) of
+ * n result rows, computed on `device`; outputs may alias nothing. */
+int tsk_canonical_order(int device, int64_t n, const int64_t *qt, const int64_t *qs, const int64_t *et,
+                        const int64_t *es, const double *tb, const double *te, int64_t *o_qt,
+                        int64_t *o_qs, int64_t *o_et, int64_t *o_es, double *o_tb, double *o_te);
 
 /* Page-locked host memory for query/result staging (cudaHostAlloc). */
 void *tsk_pinned_alloc(int64_t bytes);

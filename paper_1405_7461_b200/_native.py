@@ -23,6 +23,7 @@ TSK_SPANS_GIVEN = 1 << 3
 TSK_WANT_ORDINALS = 1 << 4
 TSK_QUERIES_RESIDENT = 1 << 5
 TSK_RESULTS_ON_DEVICE = 1 << 6
+TSK_ORDER_CANONICAL = 1 << 7
 TSK_EXTENT_MEMBER, TSK_EXTENT_GRID = 0, 1
 
 _P = ctypes.c_void_p
@@ -65,6 +66,8 @@ SIGNATURES = {
                            _I64, _PI64, _PI64, _PI64, _PI64, _PI64, _PD], ctypes.c_int),
     "tsk_plan_greedy": ([_I64, _PD, _PD, _I64, _PD, _PD, _PI64, _PI64, ctypes.c_int, _I64, _PI64,
                          _PI64, _PI64, _PI64, _PI64, _PD], ctypes.c_int),
+    "tsk_canonical_order": ([ctypes.c_int, _I64] + [_PI64] * 4 + [_PD] * 2 + [_PI64] * 4 + [_PD] * 2,
+                            ctypes.c_int),
     "tsk_pinned_alloc": ([_I64], _P),
     "tsk_pinned_free": ([_P], None),
 }
@@ -349,3 +352,16 @@ def plan_native(kind: str, ts, te, index, *, num_batches=0, min_size=0, max_size
         raise ValueError(kind)
     k = int(nb.value)
     return tuple(o[:k] for o in out)
+
+
+def canonical_order(cols: dict, device: int | None = None) -> dict:
+    """Canonically ordered copies of the six result columns, sorted on the GPU."""
+    lib = load()
+    names = ("query_traj", "query_seg", "entry_traj", "entry_seg", "t_begin", "t_end")
+    src = [np.ascontiguousarray(cols[k], np.float64 if k.startswith("t_") else np.int64) for k in names]
+    n = src[0].shape[0]
+    out = [np.empty(n, dtype=a.dtype) for a in src]
+    ptr = lambda a: a.ctypes.data_as(_PD if a.dtype == np.float64 else _PI64)  # noqa: E731
+    dev = current_device() if device is None else int(device)
+    check(lib.tsk_canonical_order(dev, n, *[ptr(a) for a in src], *[ptr(a) for a in out]))
+    return dict(zip(names, out))

@@ -467,7 +467,7 @@ extern "C" void tsk_db_free(tsk_db *db) {
     db->ix.storage.release(db->stream);
     db->q.storage.release(db->stream);
     for (DBuf *b : {&db->q_rec, &db->batches, &db->counters, &db->recs, &db->sorted, &db->cub_tmp,
-                    &db->out_cols})
+                    &db->out_cols, &db->canon_cols, &db->canon_tmp})
         b->release(db->stream);
     for (cudaEvent_t ev : {db->ev0, db->ev1, db->ev_k0, db->ev_k1})
         if (ev) cudaEventDestroy(ev);

@@ -233,6 +233,8 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     TSK_CUDA(cudaSetDevice(db->device));
     cudaStream_t st = db->stream;
     const bool query_major = flags & TSK_ORDER_QUERY_MAJOR;
+    const bool canonical = flags & TSK_ORDER_CANONICAL;
+    TSK_REQUIRE(!(canonical && (flags & TSK_WANT_ORDINALS)), "canonical order does not carry ordinals");
     const bool ordered = query_major || (flags & TSK_ORDER_REFERENCE);
     const int bb = bits_for(nb);
     const int eb = bits_for(std::max<int64_t>(n, 1)), qb = bits_for(max_s);
@@ -413,6 +415,22 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
         TSK_CUDA(cudaGetLastError());
         ++launches;
         tr.mark("gather");
+        if (canonical) {
+            // ResultSet.canonical_order on the device (core.py:290-294)
+            db->canon_cols.reserve(cb * 6 + (size_t)nh * 4 + 64, st);
+            char *cbuf = db->canon_cols.as<char>();
+            uint32_t *perm = reinterpret_cast<uint32_t *>(cbuf + 6 * cb);
+            canonical_perm(nh, g.o_qtraj, g.o_qseg, g.o_etraj, g.o_eseg, g.o_tb, g.o_te, perm,
+                           db->canon_tmp, st);
+            const int64_t *in_i[4] = {g.o_qtraj, g.o_qseg, g.o_etraj, g.o_eseg};
+            const double *in_f[2] = {g.o_tb, g.o_te};
+            int64_t *out_i[4] = {(int64_t *)(cbuf + 0 * cb), (int64_t *)(cbuf + 1 * cb),
+                                 (int64_t *)(cbuf + 2 * cb), (int64_t *)(cbuf + 3 * cb)};
+            double *out_f[2] = {(double *)(cbuf + 4 * cb), (double *)(cbuf + 5 * cb)};
+            permute6(nh, perm, in_i, in_f, out_i, out_f, st);
+            ob = cbuf;
+            tr.mark("canonical");
+        }
         if (!on_device) TSK_CUDA(cudaMemcpyAsync(res->host, ob, cb * ncols, cudaMemcpyDeviceToHost, st));
         tr.mark("d2h");
     }

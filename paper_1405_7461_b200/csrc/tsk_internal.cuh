@@ -101,7 +101,7 @@ struct tsk_db {
     tsk::Soa s;
     tsk::Index ix;
     // search workspace (grow-only)
-    tsk::DBuf q_rec, batches, counters, recs, sorted, cub_tmp, out_cols;
+    tsk::DBuf q_rec, batches, counters, recs, sorted, cub_tmp, out_cols, canon_cols, canon_tmp;
     tsk::Soa q;  // device copy of the current query set
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_k0 = nullptr, ev_k1 = nullptr;
 };
@@ -195,6 +195,11 @@ void launch_plan_items(SearchPlanDev &p, int slots, int stride, cudaStream_t st)
 void launch_qrec(const Soa &q, QRec *out, cudaStream_t st);
 void launch_qprep(const Soa &q, QRec *out, int *flags, cudaStream_t st);
 void launch_k1(const K1Launch &L, int grid, cudaStream_t st);
+void canonical_perm(int64_t n, const int64_t *qt, const int64_t *qs, const int64_t *et,
+                    const int64_t *es, const double *tb, const double *te, uint32_t *perm,
+                    DBuf &scratch, cudaStream_t st);
+void permute6(int64_t n, const uint32_t *perm, const int64_t *const in_i[4], const double *const in_f[2],
+              int64_t *const out_i[4], double *const out_f[2], cudaStream_t st);
 int k1_blocks_per_sm();
 int k1_candidates_per_thread();
 

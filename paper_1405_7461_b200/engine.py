@@ -114,30 +114,41 @@ def execute_batch(store: SegmentStore, batch: SegmentStore, span: tuple[int, int
 
 
 def run_search(store: SegmentStore, index: TemporalIndex, plan: BatchPlan, d: float, *,
-               workers: int | None = None, devices: list[int] | None = None
-               ) -> tuple[ResultSet, SearchStats]:
+               workers: int | None = None, devices: list[int] | None = None,
+               order: str = "reference") -> tuple[ResultSet, SearchStats]:
     """Execute every batch of ``plan`` against ``store`` on the GPU.
 
-    ``devices`` (an addition to the reference signature) shards the plan
-    over several GPUs, each holding a replica of the store: contiguous,
-    interaction-balanced batch shards, one host thread per device, results
-    concatenated in plan order.  No collective is involved.
+    Additions to the reference signature:
+
+    * ``devices`` shards the plan over several GPUs, each holding a replica
+      of the store: contiguous, interaction-balanced batch shards, one host
+      thread per device, results concatenated in plan order.
+      No collective is involved.
+    * ``order="canonical"`` returns the items already in
+      ``ResultSet.canonical_order()`` order, sorted on the GPU (K4); the
+      default ``"reference"`` is the reference engine's item order.
     """
     resolve_workers(workers)
+    if order not in ("reference", "canonical"):
+        raise DomainError(f"unknown order {order!r}")
     if devices is not None and len(devices) > 1:
-        return _run_sharded(store, index, plan, d, list(devices))
+        result, stats = _run_sharded(store, index, plan, d, list(devices))
+        return (result.canonical_order() if order == "canonical" else result), stats
     ordinal = None if not devices else devices[0]
-    return _run_one(store, index, plan, d, ordinal, 0)
+    return _run_one(store, index, plan, d, ordinal, 0, order == "canonical")
 
 
-def _run_one(store, index, plan, d, ordinal, replica):
+def _run_one(store, index, plan, d, ordinal, replica, canonical=False):
     t_start = time.perf_counter()
     queries = plan.queries
     lo, hi = plan.table()
     dev = index.ensure_device(ordinal, replica, store)
-    res = _native.search(dev, queries, lo, hi, None, None, d, _native.TSK_ORDER_REFERENCE)
+    flags = _native.TSK_ORDER_CANONICAL if canonical else _native.TSK_ORDER_REFERENCE
+    res = _native.search(dev, queries, lo, hi, None, None, d, flags)
     t_asm = time.perf_counter()
     result = _result_set(res) if res.n else ResultSet.empty()
+    if canonical:
+        result._canonical = True
     stats = SearchStats()
     pb = res.per_batch
     sizes = hi - lo + 1

@@ -375,3 +375,52 @@ def test_resident_queries_and_device_only_results():
         assert r.cols["query_traj"] is None  # hits stayed in HBM
         assert int(r.per_batch[:, 3].sum()) == st.hits
         assert int(r.per_batch[:, 2].sum()) == st.hits + st.spatial_misses
+
+
+# ── canonical ordering on the device (core.py:290-303) ───────────────────────
+
+
+def _lexsort_cols(c):
+    order = np.lexsort((c["t_end"], c["t_begin"], c["entry_seg"], c["entry_traj"],
+                        c["query_seg"], c["query_traj"]))
+    return {k: v[order] for k, v in c.items()}
+
+
+def test_device_canonical_order_matches_numpy_lexsort():
+    from paper_1405_7461_b200 import _native
+
+    rng = np.random.default_rng(23)
+    n = (1 << 20) + 12345
+    c = {
+        "query_traj": rng.integers(-5, 40, n), "query_seg": rng.integers(0, 7, n),
+        "entry_traj": rng.integers(-(1 << 40), 1 << 40, n), "entry_seg": rng.integers(0, 3, n),
+        "t_begin": np.round(rng.normal(0, 3, n), 2), "t_end": np.round(rng.normal(0, 3, n), 1),
+    }
+    c["t_begin"][::97] = -0.0
+    c["t_end"][::89] = 0.0
+    c["entry_traj"][::5] = 7  # many ties on the ids
+    got = _native.canonical_order(c)
+    want = _lexsort_cols(c)
+    for k in c:
+        assert np.array_equal(got[k], want[k]), k
+    rs = tsk.ResultSet(*(c[k] for k in ("query_traj", "query_seg", "entry_traj", "entry_seg",
+                                        "t_begin", "t_end")))
+    ka = rs.key_array()  # >= 2^20 rows: GPU path
+    assert np.array_equal(ka[:, 0], want["query_traj"].astype(np.float64))
+    assert np.array_equal(ka[:, 5], want["t_end"])
+
+
+def test_run_search_canonical_order():
+    store = tsk.generate(tsk.make_profile("normal", 400, seed=91, timesteps=150))
+    pool = tsk.generate(tsk.make_profile("normal", 80, seed=92, timesteps=150))
+    q = tsk.sample_queries(pool, 10, seed=93)
+    ix = tsk.build_index(store, 3000)
+    plan = tsk.periodic(q, 100, ix)
+    ref, st = tsk.run_search(store, ix, plan, 12.0)
+    can, st2 = tsk.run_search(store, ix, plan, 12.0, order="canonical")
+    assert len(ref) == len(can) > 1000
+    want = ref.canonical_order()
+    for k in ("query_traj", "query_seg", "entry_traj", "entry_seg", "t_begin", "t_end"):
+        assert np.array_equal(getattr(can, k), getattr(want, k)), k
+    assert np.array_equal(can.key_array(), ref.key_array())
+    assert st2.hits == st.hits
