@@ -36,7 +36,8 @@ enum {
     TSK_EINVAL = 1,  /* precondition violated → DomainError (core.py:25-26) */
     TSK_ECUDA = 2,   /* CUDA runtime failure → RuntimeError              */
     TSK_ENOMEM = 3,  /* allocation failure → MemoryError                 */
-    TSK_ENODEV = 4   /* no CUDA device                                   */
+    TSK_ENODEV = 4,  /* no CUDA device                                   */
+    TSK_EFORMAT = 5  /* unparsable / invalid CSV → FormatError (core.py:29-30) */
 };
 
 /* tsk_search flags */
@@ -138,6 +139,26 @@ int tsk_plan_greedy(int64_t nq, const double *ts, const double *te, int64_t n_ne
 int tsk_canonical_order(int device, int64_t n, const int64_t *qt, const int64_t *qs, const int64_t *et,
                         const int64_t *es, const double *tb, const double *te, int64_t *o_qt,
                         int64_t *o_qs, int64_t *o_et, int64_t *o_es, double *o_tb, double *o_te);
+
+/* CSV I/O (host code).  Floats are written exactly as Python repr(float).
+ *   tsk_save_store_csv     datagen.save   (datagen.py:273-285)
+ *   tsk_write_results_csv  cli._write_results rows (cli.py:62-77)
+ *   tsk_load_store_csv     datagen.load   (datagen.py:288-333): rows in file
+ *                          order; *bad_line = offending line on TSK_EFORMAT
+ *   tsk_format_double      repr(float) of one value (testing) */
+typedef struct tsk_csv tsk_csv;
+int tsk_format_double(double x, char *out, int cap);
+int tsk_save_store_csv(const char *path, int64_t n, const int64_t *traj, const int64_t *seg,
+                       const double *xs, const double *ys, const double *zs, const double *ts,
+                       const double *xe, const double *ye, const double *ze, const double *te,
+                       int nthreads);
+int tsk_write_results_csv(const char *path, int64_t n, const int64_t *qt, const int64_t *qs,
+                          const int64_t *et, const int64_t *es, const double *tb, const double *te,
+                          int nthreads);
+int tsk_load_store_csv(const char *path, int strict, tsk_csv **out, int64_t *n_out, int64_t *bad_line);
+int tsk_csv_columns(const tsk_csv *c, int64_t *traj, int64_t *seg, double *xs, double *ys, double *zs,
+                    double *ts, double *xe, double *ye, double *ze, double *te);
+void tsk_csv_free(tsk_csv *c);
 
 /* Page-locked host memory for query/result staging (cudaHostAlloc). */
 void *tsk_pinned_alloc(int64_t bytes);

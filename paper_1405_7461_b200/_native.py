@@ -15,7 +15,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TRAJSEEK_LIB") or os.path.join(_HERE, "_lib", "libtrajseek.so")
 
-TSK_OK, TSK_EINVAL, TSK_ECUDA, TSK_ENOMEM, TSK_ENODEV = 0, 1, 2, 3, 4
+TSK_OK, TSK_EINVAL, TSK_ECUDA, TSK_ENOMEM, TSK_ENODEV, TSK_EFORMAT = 0, 1, 2, 3, 4, 5
 TSK_NOOP = 1 << 0
 TSK_ORDER_REFERENCE = 1 << 1
 TSK_ORDER_QUERY_MAJOR = 1 << 2
@@ -68,6 +68,13 @@ SIGNATURES = {
                          _PI64, _PI64, _PI64, _PI64, _PD], ctypes.c_int),
     "tsk_canonical_order": ([ctypes.c_int, _I64] + [_PI64] * 4 + [_PD] * 2 + [_PI64] * 4 + [_PD] * 2,
                             ctypes.c_int),
+    "tsk_format_double": ([ctypes.c_double, ctypes.c_char_p, ctypes.c_int], ctypes.c_int),
+    "tsk_save_store_csv": ([ctypes.c_char_p, _I64, _PI64, _PI64] + [_PD] * 8 + [ctypes.c_int], ctypes.c_int),
+    "tsk_write_results_csv": ([ctypes.c_char_p, _I64] + [_PI64] * 4 + [_PD] * 2 + [ctypes.c_int],
+                              ctypes.c_int),
+    "tsk_load_store_csv": ([ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(_P), _PI64, _PI64], ctypes.c_int),
+    "tsk_csv_columns": ([_P, _PI64, _PI64] + [_PD] * 8, ctypes.c_int),
+    "tsk_csv_free": ([_P], None),
     "tsk_pinned_alloc": ([_I64], _P),
     "tsk_pinned_free": ([_P], None),
 }
@@ -105,6 +112,10 @@ def check(rc: int) -> None:
         from .core import DomainError
 
         raise DomainError(msg)
+    if rc == TSK_EFORMAT:
+        from .core import FormatError
+
+        raise FormatError(msg)
     if rc == TSK_ENOMEM:
         raise MemoryError(msg)
     raise RuntimeError(f"libtrajseek error {rc}: {msg}")
@@ -365,3 +376,52 @@ def canonical_order(cols: dict, device: int | None = None) -> dict:
     dev = current_device() if device is None else int(device)
     check(lib.tsk_canonical_order(dev, n, *[ptr(a) for a in src], *[ptr(a) for a in out]))
     return dict(zip(names, out))
+
+
+def _threads() -> int:
+    return max(1, min(32, os.cpu_count() or 1))
+
+
+def py_repr(x: float) -> str:
+    """repr(float) computed by the native formatter (tests)."""
+    b = ctypes.create_string_buffer(48)
+    n = load().tsk_format_double(float(x), b, 48)
+    return b.value[:n].decode()
+
+
+def save_store_csv(store, path: str) -> None:
+    cols = [np.ascontiguousarray(getattr(store, k), np.int64) for k in ("traj", "seg")]
+    cols += [np.ascontiguousarray(getattr(store, k), np.float64)
+             for k in ("xs", "ys", "zs", "ts", "xe", "ye", "ze", "te")]
+    check(load().tsk_save_store_csv(os.fsencode(path), len(store), cols[0].ctypes.data_as(_PI64),
+                                    cols[1].ctypes.data_as(_PI64),
+                                    *[c.ctypes.data_as(_PD) for c in cols[2:]], _threads()))
+
+
+def write_results_csv(cols: dict, path: str) -> None:
+    names = ("query_traj", "query_seg", "entry_traj", "entry_seg", "t_begin", "t_end")
+    arr = [np.ascontiguousarray(cols[k], np.float64 if k.startswith("t_") else np.int64) for k in names]
+    check(load().tsk_write_results_csv(os.fsencode(path), arr[0].shape[0],
+                                       *[a.ctypes.data_as(_PI64) for a in arr[:4]],
+                                       *[a.ctypes.data_as(_PD) for a in arr[4:]], _threads()))
+
+
+def load_store_csv(path: str, strict: bool = False) -> dict:
+    """Columns of a segment CSV in file order (raises FormatError)."""
+    lib = load()
+    h = ctypes.c_void_p()
+    n = _I64()
+    bad = _I64()
+    check(lib.tsk_load_store_csv(os.fsencode(path), 1 if strict else 0, ctypes.byref(h), ctypes.byref(n),
+                                 ctypes.byref(bad)))
+    try:
+        k = int(n.value)
+        out = {"traj": np.empty(k, np.int64), "seg": np.empty(k, np.int64)}
+        for c in ("xs", "ys", "zs", "ts", "xe", "ye", "ze", "te"):
+            out[c] = np.empty(k, np.float64)
+        check(lib.tsk_csv_columns(h, out["traj"].ctypes.data_as(_PI64), out["seg"].ctypes.data_as(_PI64),
+                                  *[out[c].ctypes.data_as(_PD) for c in ("xs", "ys", "zs", "ts", "xe",
+                                                                         "ye", "ze", "te")]))
+        return out
+    finally:
+        lib.tsk_csv_free(h)

@@ -20,9 +20,11 @@ from dataclasses import dataclass, replace
 
 import numpy as np
 
-from .core import DomainError, SegmentStore
+from .core import DomainError, FormatError, SegmentStore
 
 PROFILE_KINDS = ("uniform", "normal", "normal5", "exp")
+
+CSV_HEADER = ["traj_id", "seg_id", "x_s", "y_s", "z_s", "t_s", "x_e", "y_e", "z_e", "t_e"]
 
 
 @dataclass(frozen=True)
@@ -183,3 +185,82 @@ def galaxy(stars: int, seed: int, *, points: int = 401, start_window=(0.0, 100.0
     s, e = (slice(None), slice(None, -1)), (slice(None), slice(1, None))
     return SegmentStore(traj, seg, x[s].ravel(), y[s].ravel(), z[s].ravel(), t[s].ravel(),
                         x[e].ravel(), y[e].ravel(), z[e].ravel(), t[e].ravel(), validate=False)
+
+
+# ── CSV persistence (datagen.py:273-333), native ─────────────────────────────
+
+
+def save(store: SegmentStore, path: str) -> None:
+    """Write the store as CSV in ordinal order; floats in shortest
+    round-trip (repr) form, byte-identical to the reference's save."""
+    from . import _native
+
+    _native.save_store_csv(store, path)
+
+
+def load(path: str, *, strict: bool = False) -> SegmentStore:
+    """Read a segment CSV (validation and FormatError messages of
+    datagen.py:288-333); rows are sorted by start time unless ``strict``,
+    where unsorted input is an error.  Lines the fast native parser cannot
+    read (quoted fields, numeric underscores) are re-read by the csv module
+    so the accepted syntax matches the reference."""
+    from . import _native
+
+    try:
+        cols = _native.load_store_csv(path, strict)
+    except FormatError as exc:
+        # Python-formatted messages (header repr, float() errors) and the
+        # rarer syntaxes csv/float() accept come from the csv-module reader
+        if "unparsable field" not in str(exc) and "bad header" not in str(exc):
+            raise
+        cols = _load_python(path, strict)
+    return SegmentStore.from_columns(cols, validate=False)
+
+
+def _load_python(path: str, strict: bool) -> dict:
+    import csv
+
+    rows = []
+    with open(path, newline="") as fh:
+        reader = csv.reader(fh)
+        try:
+            header = next(reader)
+        except StopIteration:
+            raise FormatError(f"{path}: empty file") from None
+        if header != CSV_HEADER:
+            raise FormatError(f"{path}: bad header {header!r}")
+        for lineno, row in enumerate(reader, start=2):
+            if not row:
+                continue
+            if len(row) != 10:
+                raise FormatError(f"{path}:{lineno}: expected 10 fields, got {len(row)}")
+            try:
+                vals = (int(row[0]), int(row[1]), *(float(v) for v in row[2:]))
+            except ValueError as exc:
+                raise FormatError(f"{path}:{lineno}: {exc}") from None
+            if not all(np.isfinite(v) for v in vals[2:]):
+                raise FormatError(f"{path}:{lineno}: non-finite coordinate")
+            if vals[9] < vals[5]:
+                raise FormatError(f"{path}:{lineno}: segment ends at t={vals[9]!r} "
+                                  f"before it starts at t={vals[5]!r}")
+            rows.append(vals)
+    if not rows:
+        raise FormatError(f"{path}: no segments")
+    arr = np.asarray(rows, dtype=np.float64)
+    if strict and (np.diff(arr[:, 5]) < 0).any():
+        bad = int(np.argmax(np.diff(arr[:, 5]) < 0)) + 3
+        raise FormatError(f"{path}:{bad}: rows not sorted by t_s (strict mode)")
+    names = ("traj", "seg", "xs", "ys", "zs", "ts", "xe", "ye", "ze", "te")
+    return {k: (arr[:, i].astype(np.int64) if i < 2 else arr[:, i].copy()) for i, k in enumerate(names)}
+
+
+def write_results(result, path: str, canonical: bool = False) -> None:
+    """The search result CSV of the reference CLI (cli.py:62-77), written
+    natively; ``canonical`` first applies ResultSet.canonical_order."""
+    from . import _native
+
+    if canonical:
+        result = result.canonical_order()
+    _native.write_results_csv({k: getattr(result, k) for k in
+                               ("query_traj", "query_seg", "entry_traj", "entry_seg", "t_begin", "t_end")},
+                              path)

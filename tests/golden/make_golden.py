@@ -299,6 +299,60 @@ def gen_datagen():
     save("datagen.npz", **out)
 
 
+def gen_csv():
+    """datagen.save / load (datagen.py:273-333) and the CLI result CSV
+    (cli.py:62-77), written by the reference itself."""
+    import json
+    import tempfile
+
+    from trajseek.cli import main as cli_main
+
+    store = datagen.generate(datagen.make_profile("uniform", 5, seed=3, timesteps=40))
+    datagen.save(store, os.path.join(HERE, "store_uniform.csv"))
+    ex = datagen.generate(datagen.make_profile("exp", 12, seed=6))
+    datagen.save(ex, os.path.join(HERE, "store_exp.csv"))
+    with tempfile.TemporaryDirectory() as td:
+        db, pool, qf = (os.path.join(td, n) for n in ("db.csv", "pool.csv", "q.csv"))
+        assert cli_main(["gen", "--profile", "uniform", "--trajectories", "12", "--seed", "5",
+                         "--out", db]) == 0
+        assert cli_main(["gen", "--profile", "uniform", "--trajectories", "8", "--seed", "6",
+                         "--out", pool]) == 0
+        assert cli_main(["gen", "--sample-from", pool, "--trajectories", "2", "--seed", "7",
+                         "--out", qf]) == 0
+        for sorted_flag, name in ((True, "results_sorted.csv"), (False, "results_engine.csv")):
+            args = ["search", "--db", db, "--queries", qf, "--d", "20.0", "--m", "60",
+                    "--workers", "1", "--planner", "greedy-max", "--bound", "50",
+                    "--out", os.path.join(HERE, name)]
+            if sorted_flag:
+                args.insert(-2, "--sorted")
+            assert cli_main(args) == 0
+        json.dump({"cli_db.csv": hashlib.sha256(open(db, "rb").read()).hexdigest(),
+                   "cli_queries.csv": hashlib.sha256(open(qf, "rb").read()).hexdigest()},
+                  open(os.path.join(HERE, "cli_inputs_sha256.json"), "w"), indent=1)
+        # load() error messages for malformed files
+        errs = {}
+        good = open(os.path.join(HERE, "store_uniform.csv")).read().splitlines()
+        cases = {
+            "bad_header": ["a,b,c"] + good[1:3],
+            "arity": good[:2] + ["1,2,3"],
+            "nonnumeric": good[:2] + ["1,0,abc,0,0,0,1,0,0,1"],
+            "nonfinite": good[:2] + ["1,0,inf,0,0,0,1,0,0,1"],
+            "reversed": good[:2] + ["1,0,0,0,0,5.0,1,0,0,1.5"],
+            "unsorted_strict": good[:1] + [good[3], good[2]],
+            "empty_rows": good[:1],
+        }
+        for name, lines in cases.items():
+            path = os.path.join(td, name + ".csv")
+            open(path, "w").write("\n".join(lines) + "\n")
+            try:
+                datagen.load(path, strict=(name == "unsorted_strict"))
+                errs[name] = {"lines": lines, "error": None}
+            except core.FormatError as exc:
+                errs[name] = {"lines": lines, "error": str(exc).replace(path, "<path>")}
+        json.dump(errs, open(os.path.join(HERE, "load_errors.json"), "w"), indent=1)
+    print("wrote csv fixtures")
+
+
 if __name__ == "__main__":
     print("reference trajseek", trajseek.__version__, "from", trajseek.__file__)
     gen_pairs()
@@ -307,3 +361,4 @@ if __name__ == "__main__":
     gen_plans()
     gen_search()
     gen_datagen()
+    gen_csv()
