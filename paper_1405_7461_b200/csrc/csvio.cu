@@ -226,13 +226,76 @@ bool parse_i64(const char *b, const char *e, int64_t &v) {
 bool parse_f64(const char *b, const char *e, double &v) {
     while (b < e && (*b == ' ' || *b == '\t')) ++b;
     while (e > b && (e[-1] == ' ' || e[-1] == '\t' || e[-1] == '\r')) --e;
-    if (b == e || e - b > 400) return false;
-    char tmp[416];
-    memcpy(tmp, b, e - b);
-    tmp[e - b] = 0;
-    char *end = nullptr;
-    v = strtod(tmp, &end);  // correctly rounded (glibc), as Python's float()
-    return end == tmp + (e - b);
+    if (b == e) return false;
+    if (*b == '+') ++b;  // float() accepts a leading '+'
+    auto r = std::from_chars(b, e, v);  // correctly rounded, as Python's float()
+    return r.ec == std::errc() && r.ptr == e;
+}
+
+struct Chunk {
+    std::vector<int64_t> traj, seg;
+    std::vector<double> col[8];
+    int64_t lines = 0;       // lines in this chunk
+    int64_t err_line = -1;   // first bad line, relative to the chunk (1-based)
+    int err_kind = 0;        // 1 arity, 2 unparsable, 3 non-finite, 4 reversed
+    int err_count = 0;
+    double err_ts = 0, err_te = 0;
+};
+
+void parse_chunk(const char *p, const char *end, Chunk &c) {
+    const size_t est = (size_t)(end - p) / 120 + 16;
+    c.traj.reserve(est);
+    c.seg.reserve(est);
+    for (auto &v : c.col) v.reserve(est);
+    while (p < end) {
+        const char *b = p;
+        const char *nl = (const char *)memchr(p, '\n', end - p);
+        const char *e = nl ? nl : end;
+        p = nl ? nl + 1 : end;
+        ++c.lines;
+        if (e > b && e[-1] == '\r') --e;
+        if (b == e) continue;  // csv.reader yields [] for an empty line
+        const char *f[11];
+        int count = 1;
+        f[0] = b;
+        for (const char *q = b; q < e; ++q)
+            if (*q == ',') {
+                if (count < 10) f[count] = q + 1;
+                ++count;
+            }
+        if (count != 10) {
+            c.err_line = c.lines;
+            c.err_kind = 1;
+            c.err_count = count;
+            return;
+        }
+        f[10] = e + 1;
+        int64_t iv[2];
+        double dv[8];
+        bool ok = parse_i64(f[0], f[1] - 1, iv[0]) && parse_i64(f[1], f[2] - 1, iv[1]);
+        for (int k = 0; k < 8 && ok; ++k) ok = parse_f64(f[2 + k], f[3 + k] - 1, dv[k]);
+        if (!ok) {
+            c.err_line = c.lines;
+            c.err_kind = 2;
+            return;
+        }
+        for (int k = 0; k < 8; ++k)
+            if (!std::isfinite(dv[k])) {
+                c.err_line = c.lines;
+                c.err_kind = 3;
+                return;
+            }
+        if (dv[7] < dv[3]) {
+            c.err_line = c.lines;
+            c.err_kind = 4;
+            c.err_ts = dv[3];
+            c.err_te = dv[7];
+            return;
+        }
+        c.traj.push_back(iv[0]);
+        c.seg.push_back(iv[1]);
+        for (int k = 0; k < 8; ++k) c.col[k].push_back(dv[k]);
+    }
 }
 
 }  // namespace
@@ -269,53 +332,50 @@ extern "C" int tsk_load_store_csv(const char *path, int strict, tsk_csv **out, i
         if (!next_line(b, e)) throw Error{TSK_EFORMAT, std::string(path) + ": empty file"};
         if (std::string(b, e) != "traj_id,seg_id,x_s,y_s,z_s,t_s,x_e,y_e,z_e,t_e")
             throw Error{TSK_EFORMAT, std::string(path) + ": bad header " + std::string(b, e)};
+        // split the body at line boundaries into one chunk per thread
+        const int nthreads = std::max(1, std::min(32, (int)std::thread::hardware_concurrency()));
+        std::vector<const char *> cut{p};
+        for (int t = 1; t < nthreads; ++t) {
+            const char *c0 = p + (end - p) * t / nthreads;
+            if (c0 < cut.back()) c0 = cut.back();
+            const char *nl = (const char *)memchr(c0, '\n', end - c0);
+            cut.push_back(nl ? nl + 1 : end);
+        }
+        cut.push_back(end);
+        std::vector<Chunk> chunks(nthreads);
+        {
+            std::vector<std::thread> th;
+            for (int t = 0; t < nthreads; ++t)
+                th.emplace_back([&, t] { parse_chunk(cut[t], cut[t + 1], chunks[t]); });
+            for (auto &x : th) x.join();
+        }
+        int64_t lines_before = 1;  // the header
+        for (auto &ch : chunks) {
+            if (ch.err_line >= 0) {
+                const int64_t lineno = lines_before + ch.err_line;
+                *bad_line = lineno;
+                const std::string at = std::string(path) + ":" + std::to_string(lineno) + ": ";
+                if (ch.err_kind == 1)
+                    throw Error{TSK_EFORMAT, at + "expected 10 fields, got " + std::to_string(ch.err_count)};
+                if (ch.err_kind == 2) throw Error{TSK_EFORMAT, at + "unparsable field"};
+                if (ch.err_kind == 3) throw Error{TSK_EFORMAT, at + "non-finite coordinate"};
+                char a1[48], z1[48];
+                a1[py_repr(ch.err_te, a1)] = 0;
+                z1[py_repr(ch.err_ts, z1)] = 0;
+                throw Error{TSK_EFORMAT, at + "segment ends at t=" + a1 + " before it starts at t=" + z1};
+            }
+            lines_before += ch.lines;
+        }
         auto *c = new tsk_csv();
-        int64_t lineno = 1;
-        while (next_line(b, e)) {
-            ++lineno;
-            if (b == e) continue;  // csv.reader yields [] for an empty line
-            const char *f[11];
-            int nf = 0;
-            f[nf++] = b;
-            for (const char *q = b; q < e && nf <= 10; ++q)
-                if (*q == ',') f[nf++] = q + 1;
-            int count = 1;
-            for (const char *q = b; q < e; ++q) count += *q == ',';
-            if (count != 10) {
-                *bad_line = lineno;
-                delete c;
-                throw Error{TSK_EFORMAT, std::string(path) + ":" + std::to_string(lineno) +
-                                             ": expected 10 fields, got " + std::to_string(count)};
-            }
-            f[10] = e + 1;
-            int64_t iv[2];
-            double dv[8];
-            bool ok = parse_i64(f[0], f[1] - 1, iv[0]) && parse_i64(f[1], f[2] - 1, iv[1]);
-            for (int k = 0; k < 8 && ok; ++k) ok = parse_f64(f[2 + k], f[3 + k] - 1, dv[k]);
-            if (!ok) {
-                *bad_line = lineno;
-                delete c;
-                throw Error{TSK_EFORMAT, std::string(path) + ":" + std::to_string(lineno) + ": unparsable field"};
-            }
-            for (int k = 0; k < 8; ++k)
-                if (!std::isfinite(dv[k])) {
-                    *bad_line = lineno;
-                    delete c;
-                    throw Error{TSK_EFORMAT, std::string(path) + ":" + std::to_string(lineno) +
-                                                 ": non-finite coordinate"};
-                }
-            if (dv[7] < dv[3]) {
-                *bad_line = lineno;
-                delete c;
-                char a[48], z[48];
-                a[py_repr(dv[7], a)] = 0;
-                z[py_repr(dv[3], z)] = 0;
-                throw Error{TSK_EFORMAT, std::string(path) + ":" + std::to_string(lineno) +
-                                             ": segment ends at t=" + a + " before it starts at t=" + z};
-            }
-            c->traj.push_back(iv[0]);
-            c->seg.push_back(iv[1]);
-            for (int k = 0; k < 8; ++k) c->col[k].push_back(dv[k]);
+        size_t total = 0;
+        for (auto &ch : chunks) total += ch.traj.size();
+        c->traj.reserve(total);
+        c->seg.reserve(total);
+        for (auto &v : c->col) v.reserve(total);
+        for (auto &ch : chunks) {
+            c->traj.insert(c->traj.end(), ch.traj.begin(), ch.traj.end());
+            c->seg.insert(c->seg.end(), ch.seg.begin(), ch.seg.end());
+            for (int k = 0; k < 8; ++k) c->col[k].insert(c->col[k].end(), ch.col[k].begin(), ch.col[k].end());
         }
         if (c->traj.empty()) {
             delete c;

@@ -122,34 +122,6 @@ void soa_hoist(Soa &s, cudaStream_t st) {
 
 // ── queries → shared-memory records ────────────────────────────────────────
 
-__global__ void k_qrec(int64_t n, const double *__restrict__ ts, const double *__restrict__ te,
-                       const double *__restrict__ sx, const double *__restrict__ sy,
-                       const double *__restrict__ sz, const double *__restrict__ ex,
-                       const double *__restrict__ ey, const double *__restrict__ ez,
-                       const double *__restrict__ dx, const double *__restrict__ dy,
-                       const double *__restrict__ dz, const double *__restrict__ rcp,
-                       const uint8_t *__restrict__ unsafe, QRec *__restrict__ out) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        QRec r;
-        r.ts = ts[i];
-        r.te = te[i];
-        r.sx = sx[i];
-        r.sy = sy[i];
-        r.sz = sz[i];
-        r.ext = __dsub_rn(r.te, r.ts);
-        r.dx = dx[i];
-        r.dy = dy[i];
-        r.dz = dz[i];
-        r.rcp = rcp[i];
-        r.ex = ex[i];
-        r.ey = ey[i];
-        r.ez = ez[i];
-        r.flag = unsafe[i] ? 1.0 : 0.0;
-        out[i] = r;
-    }
-}
-
 // Queries: hoisted invariants straight into the shared-memory records (one
 // pass, no host sync); flags[0] |= 1 when the start times are not sorted
 // (the pair kernel then disables its windows).
@@ -188,14 +160,6 @@ void launch_qprep(const Soa &q, QRec *out, int *flags, cudaStream_t st) {
     if (q.n == 0) return;
     int grid = (int)std::min<int64_t>((q.n + 255) / 256, 148 * 8);
     k_qprep<<<grid, 256, 0, st>>>(q.n, q.ts, q.te, q.sx, q.sy, q.sz, q.ex, q.ey, q.ez, out, flags);
-    TSK_CUDA(cudaGetLastError());
-}
-
-void launch_qrec(const Soa &q, QRec *out, cudaStream_t st) {
-    if (q.n == 0) return;
-    int grid = (int)std::min<int64_t>((q.n + 255) / 256, 148 * 8);
-    k_qrec<<<grid, 256, 0, st>>>(q.n, q.ts, q.te, q.sx, q.sy, q.sz, q.ex, q.ey, q.ez, q.dx, q.dy,
-                                 q.dz, q.rcp, q.unsafe, out);
     TSK_CUDA(cudaGetLastError());
 }
 

@@ -192,7 +192,6 @@ struct K1Launch {
 
 void launch_ranges(tsk_db *db, const Soa &q, SearchPlanDev &p, bool spans_given, cudaStream_t st);
 void launch_plan_items(SearchPlanDev &p, int slots, int stride, cudaStream_t st);
-void launch_qrec(const Soa &q, QRec *out, cudaStream_t st);
 void launch_qprep(const Soa &q, QRec *out, int *flags, cudaStream_t st);
 void launch_k1(const K1Launch &L, int grid, cudaStream_t st);
 void canonical_perm(int64_t n, const int64_t *qt, const int64_t *qs, const int64_t *et,
