@@ -120,6 +120,37 @@ void soa_hoist(Soa &s, cudaStream_t st) {
     s.sorted = h[1] ? 0 : 1;
 }
 
+// max |coordinate| over the six position columns (filter margin of K1)
+__global__ void k_cmax(int64_t n, const double *__restrict__ a, const double *__restrict__ b,
+                       const double *__restrict__ c, const double *__restrict__ d,
+                       const double *__restrict__ e, const double *__restrict__ f,
+                       unsigned long long *out) {
+    double cm = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        cm = fmax(cm, fmax(fmax(fabs(a[i]), fabs(b[i])), fmax(fmax(fabs(c[i]), fabs(d[i])),
+                                                              fmax(fabs(e[i]), fabs(f[i])))));
+    for (int o = 16; o; o >>= 1) cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(cm));
+}
+
+double soa_cmax(const Soa &s, cudaStream_t st) {
+    if (s.n == 0) return 0.0;
+    unsigned long long *d;
+    TSK_CUDA(cudaMallocAsync(&d, 8, st));
+    TSK_CUDA(cudaMemsetAsync(d, 0, 8, st));
+    int grid = (int)std::min<int64_t>((s.n + 255) / 256, 148 * 16);
+    k_cmax<<<grid, 256, 0, st>>>(s.n, s.sx, s.sy, s.sz, s.ex, s.ey, s.ez, d);
+    TSK_CUDA(cudaGetLastError());
+    unsigned long long h = 0;
+    TSK_CUDA(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, st));
+    TSK_CUDA(cudaFreeAsync(d, st));
+    TSK_CUDA(cudaStreamSynchronize(st));
+    double v;
+    memcpy(&v, &h, 8);
+    return v;
+}
+
 // ── queries → shared-memory records ────────────────────────────────────────
 
 // Queries: hoisted invariants straight into the shared-memory records (one
@@ -129,7 +160,8 @@ __global__ void k_qprep(int64_t n, const double *__restrict__ ts, const double *
                         const double *__restrict__ sx, const double *__restrict__ sy,
                         const double *__restrict__ sz, const double *__restrict__ ex,
                         const double *__restrict__ ey, const double *__restrict__ ez,
-                        QRec *__restrict__ out, int *flags) {
+                        QRec *__restrict__ out, int *flags, unsigned long long *cmax_bits) {
+    double cm = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         QRec r;
@@ -152,14 +184,20 @@ __global__ void k_qprep(int64_t n, const double *__restrict__ ts, const double *
         r.flag = bad ? 1.0 : 0.0;
         out[i] = r;
         if (i + 1 < n && ts[i + 1] < r.ts) atomicOr(&flags[0], 1);
+        cm = fmax(cm, fmax(fmax(fabs(r.sx), fabs(r.sy)), fmax(fabs(r.sz), fmax(fabs(r.ex), fmax(fabs(r.ey), fabs(r.ez))))));
     }
+    for (int o = 16; o; o >>= 1) cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+    // non-negative doubles order like their bit patterns
+    if ((threadIdx.x & 31) == 0) atomicMax(cmax_bits, (unsigned long long)__double_as_longlong(cm));
 }
 
-void launch_qprep(const Soa &q, QRec *out, int *flags, cudaStream_t st) {
+void launch_qprep(const Soa &q, QRec *out, int *flags, unsigned long long *cmax_bits, cudaStream_t st) {
     TSK_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), st));
+    TSK_CUDA(cudaMemsetAsync(cmax_bits, 0, sizeof(unsigned long long), st));
     if (q.n == 0) return;
     int grid = (int)std::min<int64_t>((q.n + 255) / 256, 148 * 8);
-    k_qprep<<<grid, 256, 0, st>>>(q.n, q.ts, q.te, q.sx, q.sy, q.sz, q.ex, q.ey, q.ez, out, flags);
+    k_qprep<<<grid, 256, 0, st>>>(q.n, q.ts, q.te, q.sx, q.sy, q.sz, q.ex, q.ey, q.ez, out, flags,
+                                  cmax_bits);
     TSK_CUDA(cudaGetLastError());
 }
 
@@ -415,6 +453,7 @@ extern "C" int tsk_db_create(int device, const tsk_columns *cols, tsk_db **out) 
         soa_alloc(db->s, cols->n, true, db->stream);
         soa_upload(db->s, cols, db->stream);
         soa_hoist(db->s, db->stream);
+        db->cmax = soa_cmax(db->s, db->stream);
         *out = db;
         return TSK_OK;
     } catch (const Error &e) {

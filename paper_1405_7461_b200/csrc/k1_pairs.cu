@@ -262,6 +262,78 @@ __device__ __forceinline__ bool pair_eval(const Cand &r, const QVals &Q, uint32_
     return ta == tb || dq >= -0x1p-1000;
 }
 
+// Fast conservative filter for one pair (span-clip cases as pair_eval).
+// Interpolations use f = (t - ts) * RN(1/ext) and FMAs, so positions are
+// within ~2^-46 C of the reference's (C = max |coordinate| of the launch),
+// u and w within ~2^-45 C, and the coefficients within ~2^-41 C^2 (|dot|, |e|,
+// aa scale).  The test dq_f + 2^-38 (C2 (|dot| + |e| + aa) + dot^2 + aa |e|) >= 0,
+// C2 = 16 C^2 + d^2, therefore holds for every pair whose reference
+// discriminant (core.py:537) is >= 0 — every reference hit, including the
+// constant-separation case — and flagged pairs are re-evaluated exactly
+// (pair_eval) before the reference's solve.  Flat spans are flagged by exact
+// time equality.
+template <int TA, int TB>
+__device__ __forceinline__ bool pair_filter(const Cand &r, const QVals &Q, uint32_t qa, double wmin_te,
+                                            double wmax_te, double d2, double C2) {
+    const double cts = Q.ts, cte = Q.te;
+    double ta, ra[3], ca[3], rb[3], cb[3];
+    const double rs[3] = {r.sx, r.sy, r.sz}, rd[3] = {r.dx, r.dy, r.dz};
+    const double cs[3] = {Q.sx, Q.sy, Q.sz}, cd[3] = {Q.dx, Q.dy, Q.dz};
+    if (TA == TA_R) {
+        ta = cts;
+        const double f = (cts - r.ts) * r.rcp;
+        for (int i = 0; i < 3; ++i) { ra[i] = fma(f, rd[i], rs[i]); ca[i] = cs[i]; }
+    } else if (TA == TA_C) {
+        ta = r.ts;
+        const double f = (r.ts - cts) * Q.rcp;
+        for (int i = 0; i < 3; ++i) { ra[i] = rs[i]; ca[i] = fma(f, cd[i], cs[i]); }
+    } else {
+        ta = r.ts > cts ? r.ts : cts;
+        const double fr = (ta - r.ts) * r.rcp, fc = (ta - cts) * Q.rcp;
+        for (int i = 0; i < 3; ++i) { ra[i] = fma(fr, rd[i], rs[i]); ca[i] = fma(fc, cd[i], cs[i]); }
+    }
+    double tb;
+    if (TB == TB_R || (TB == TB_DYN && cte < wmin_te)) {
+        tb = cte;
+        const double f = (cte - r.ts) * r.rcp;
+        for (int i = 0; i < 3; ++i) rb[i] = fma(f, rd[i], rs[i]);
+        double flag_unused;
+        lds2(qa + 80, cb[0], cb[1]);
+        lds2(qa + 96, cb[2], flag_unused);
+    } else if (TB == TB_C || (TB == TB_DYN && cte > wmax_te)) {
+        tb = r.te;
+        const double f = (r.te - cts) * Q.rcp;
+        rb[0] = r.ex; rb[1] = r.ey; rb[2] = r.ez;
+        for (int i = 0; i < 3; ++i) cb[i] = fma(f, cd[i], cs[i]);
+    } else {
+        tb = r.te < cte ? r.te : cte;
+        const double fr = (tb - r.ts) * r.rcp, fc = (tb - cts) * Q.rcp;
+        double qe[3], flag_unused;
+        lds2(qa + 80, qe[0], qe[1]);
+        lds2(qa + 96, qe[2], flag_unused);
+        const double re[3] = {r.ex, r.ey, r.ez};
+        const bool zr = r.te > cte, zc = cte > r.te;
+        for (int i = 0; i < 3; ++i) {
+            rb[i] = zr ? fma(fr, rd[i], rs[i]) : re[i];
+            cb[i] = zc ? fma(fc, cd[i], cs[i]) : qe[i];
+        }
+    }
+    double u[3], w[3];
+    for (int i = 0; i < 3; ++i) {
+        u[i] = ra[i] - ca[i];
+        w[i] = (rb[i] - ra[i]) - (cb[i] - ca[i]);
+    }
+    const double cc = fma(u[0], u[0], fma(u[1], u[1], u[2] * u[2]));
+    const double aa = fma(w[0], w[0], fma(w[1], w[1], w[2] * w[2]));
+    const double dot = fma(u[0], w[0], fma(u[1], w[1], u[2] * w[2]));
+    const double e = cc - d2;
+    const double ae = fabs(e);
+    const double dot2 = dot * dot;
+    const double dq = fma(-aa, e, dot2);
+    const double m = fma(C2, fabs(dot) + ae + aa, fma(aa, ae, dot2));
+    return ta == tb || fma(m, 0x1p-38, dq) >= 0.0;
+}
+
 // One warp, K1_CPT candidates per lane, staged queries j0..j1-1 of one
 // (TA, TB) case.  CNT: count overlaps per iteration; otherwise the caller
 // counts them for the whole range by binary search and lanes that do not
@@ -270,7 +342,7 @@ template <int TA, int TB, bool SLOW, bool CNT>
 __device__ __forceinline__ void pair_run(const K1Launch &L, const QRec *__restrict__ sq, int j0, int j1,
                                          const Cand (&r)[K1_CPT], double wmin_te, double wmax_te,
                                          const uint64_t (&key_base)[K1_CPT], int lane,
-                                         unsigned &n_ov, unsigned &n_hit) {
+                                         unsigned &n_ov, unsigned &n_hit, double C2) {
     const double d2 = L.d2;
     uint32_t qa = (uint32_t)__cvta_generic_to_shared(sq) + (uint32_t)j0 * (uint32_t)sizeof(QRec);
     for (int j = j0; j < j1; ++j, qa += (uint32_t)sizeof(QRec)) {
@@ -285,9 +357,23 @@ __device__ __forceinline__ void pair_run(const K1Launch &L, const QRec *__restri
                 ov = r[k].ts <= Q.te && Q.ts <= r[k].te;  // invalid lanes: ts = +inf
                 n_ov += ov ? 1u : 0u;
             }
-            cand[k] = pair_eval<TA, TB, SLOW>(r[k], Q, qa, wmin_te, wmax_te, d2, cc[k], aa[k], dot[k],
-                                              e[k]) && ov;
+            if (SLOW)  // extreme exponents: the exact evaluation is the filter
+                cand[k] = pair_eval<TA, TB, true>(r[k], Q, qa, wmin_te, wmax_te, d2, cc[k], aa[k],
+                                                  dot[k], e[k]) && ov;
+            else
+                cand[k] = pair_filter<TA, TB>(r[k], Q, qa, wmin_te, wmax_te, d2, C2) && ov;
             any |= cand[k];
+        }
+        if (!SLOW && __ballot_sync(0xffffffffu, any)) {
+            // flagged pairs: the reference's exact arithmetic (core.py:503-537)
+            any = false;
+#pragma unroll
+            for (int k = 0; k < K1_CPT; ++k) {
+                const bool ex = pair_eval<TA, TB, false>(r[k], Q, qa, wmin_te, wmax_te, d2, cc[k], aa[k],
+                                                         dot[k], e[k]);
+                cand[k] = cand[k] && ex;
+                any |= cand[k];
+            }
         }
         if (__ballot_sync(0xffffffffu, any)) {
             // Second filter, paid only here: the quadratic q(λ) = aa λ² + 2 dot λ + e
@@ -393,6 +479,10 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
     constexpr int64_t STRIDE = (int64_t)K1_THREADS * K1_CPT;  // candidates per sub-tile
     const int64_t ct = STRIDE * sub;
     const int64_t nb = L.plan.nb;
+    // filter margin scale C2 = 16 C^2 + d^2 (see pair_filter)
+    const double cq = __longlong_as_double((long long)*L.q_cmax_bits);
+    const double cmax = L.db_cmax > cq ? L.db_cmax : cq;
+    const double C2 = 16.0 * cmax * cmax + L.d2;
 
     for (;;) {
         if (tid == 0) {
@@ -530,9 +620,9 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
             const bool c_tb_r = jlo < ja && pm[ja - 1] < wmin_te;
             const bool r_tb_c = jb < jhi && sm[jb] > wmax;
             if (slow) {
-                pair_run<TA_C, TB_DYN, true, true>(L, sq, jlo, ja, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
-                pair_run<TA_BOTH, TB_DYN, true, true>(L, sq, ja, jb, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
-                pair_run<TA_R, TB_DYN, true, true>(L, sq, jb, jhi, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+                pair_run<TA_C, TB_DYN, true, true>(L, sq, jlo, ja, r, wmin_te, wmax, key_base, lane, n_ov, n_hit, C2);
+                pair_run<TA_BOTH, TB_DYN, true, true>(L, sq, ja, jb, r, wmin_te, wmax, key_base, lane, n_ov, n_hit, C2);
+                pair_run<TA_R, TB_DYN, true, true>(L, sq, jb, jhi, r, wmin_te, wmax, key_base, lane, n_ov, n_hit, C2);
                 continue;
             }
             if (c_tb_r && te_sorted) {
@@ -540,19 +630,19 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
 #pragma unroll
                 for (int k = 0; k < K1_CPT; ++k)
                     n_ov += (unsigned)(ja - clampi(lower_bound_te(sq, it.nt, r[k].ts), jlo, ja));
-                pair_run<TA_C, TB_R, false, false>(L, sq, jlo, ja, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+                pair_run<TA_C, TB_R, false, false>(L, sq, jlo, ja, r, wmin_te, wmax, key_base, lane, n_ov, n_hit, C2);
             } else {
-                pair_run<TA_C, TB_DYN, false, true>(L, sq, jlo, ja, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+                pair_run<TA_C, TB_DYN, false, true>(L, sq, jlo, ja, r, wmin_te, wmax, key_base, lane, n_ov, n_hit, C2);
             }
-            pair_run<TA_BOTH, TB_DYN, false, true>(L, sq, ja, jb, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+            pair_run<TA_BOTH, TB_DYN, false, true>(L, sq, ja, jb, r, wmin_te, wmax, key_base, lane, n_ov, n_hit, C2);
             if (r_tb_c) {
                 // overlap <=> cts <= r.te; cts ascending over the tile
 #pragma unroll
                 for (int k = 0; k < K1_CPT; ++k)
                     n_ov += (unsigned)(clampi(upper_bound_ts(sq, it.nt, r[k].te), jb, jhi) - jb);
-                pair_run<TA_R, TB_C, false, false>(L, sq, jb, jhi, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+                pair_run<TA_R, TB_C, false, false>(L, sq, jb, jhi, r, wmin_te, wmax, key_base, lane, n_ov, n_hit, C2);
             } else {
-                pair_run<TA_R, TB_DYN, false, true>(L, sq, jb, jhi, r, wmin_te, wmax, key_base, lane, n_ov, n_hit);
+                pair_run<TA_R, TB_DYN, false, true>(L, sq, jb, jhi, r, wmin_te, wmax, key_base, lane, n_ov, n_hit, C2);
             }
         }
         // per-batch counters (64-bit)

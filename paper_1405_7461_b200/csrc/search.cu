@@ -253,7 +253,8 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
         soa_upload(db->q, qc, st);
         db->q_rec.reserve((size_t)nq * sizeof(QRec), st);
         db->counters.reserve(64, st);
-        launch_qprep(db->q, db->q_rec.as<QRec>(), db->counters.as<int>() + 8, st);
+        launch_qprep(db->q, db->q_rec.as<QRec>(), db->counters.as<int>() + 8,
+                     db->counters.as<unsigned long long>() + 5, st);
         launches += 1;
     }
     tr.mark("queries");
@@ -294,6 +295,10 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     L.item_counter = d_ctr;
     L.hit_count = d_ctr + 1;
     L.d2 = d * d;  // core.py:527
+    // filter margin scale: entry max |coordinate| here, the query one is
+    // reduced on the device by qprep and folded in by K1
+    L.db_cmax = db->cmax;
+    L.q_cmax_bits = db->counters.as<unsigned long long>() + 5;
     L.major_bits = major_bits;
     L.minor_bits = minor_bits;
     L.query_major = query_major;

@@ -99,6 +99,7 @@ struct tsk_db {
     int device = 0;
     cudaStream_t stream = nullptr;
     tsk::Soa s;
+    double cmax = 0;  // max |coordinate| of the entry store
     tsk::Index ix;
     // search workspace (grow-only)
     tsk::DBuf q_rec, batches, counters, recs, sorted, cub_tmp, out_cols, canon_cols, canon_tmp;
@@ -184,6 +185,8 @@ struct K1Launch {
     double *tbeg, *tend;
     uint64_t cap;
     double d2;
+    double db_cmax;                          // max |coordinate| of the entries
+    const unsigned long long *q_cmax_bits;   // max |coordinate| of the queries (device, as bits)
     int major_bits, minor_bits;  // key = b << (major+minor) | major << minor | minor
     int query_major;             // 0: (b, entry, query); 1: (b, query, entry)
     int noop;
@@ -192,7 +195,8 @@ struct K1Launch {
 
 void launch_ranges(tsk_db *db, const Soa &q, SearchPlanDev &p, bool spans_given, cudaStream_t st);
 void launch_plan_items(SearchPlanDev &p, int slots, int stride, cudaStream_t st);
-void launch_qprep(const Soa &q, QRec *out, int *flags, cudaStream_t st);
+void launch_qprep(const Soa &q, QRec *out, int *flags, unsigned long long *cmax_bits, cudaStream_t st);
+double soa_cmax(const Soa &s, cudaStream_t st);
 void launch_k1(const K1Launch &L, int grid, cudaStream_t st);
 void canonical_perm(int64_t n, const int64_t *qt, const int64_t *qs, const int64_t *et,
                     const int64_t *es, const double *tb, const double *te, uint32_t *perm,

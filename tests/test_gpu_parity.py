@@ -424,3 +424,85 @@ def test_run_search_canonical_order():
         assert np.array_equal(getattr(can, k), getattr(want, k)), k
     assert np.array_equal(can.key_array(), ref.key_array())
     assert st2.hits == st.hits
+
+
+# ── the K1 filter must flag every reference hit (borderline cases) ───────────
+
+
+def _min_dist_sq(A, B):
+    """Approximate min squared distance of co-moving pairs over their shared span."""
+    ta = np.maximum(A[:, 3], B[:, 3])
+    tb = np.minimum(A[:, 7], B[:, 7])
+    out = np.full(A.shape[0], np.inf)
+    ok = ta < tb
+    lam = np.linspace(0.0, 1.0, 2001)[None, :]
+    for X in (A, B):
+        pass
+    t = ta[ok, None] + lam * (tb - ta)[ok, None]
+
+    def pos(S):
+        f = (t - S[ok, 3:4]) / (S[ok, 7:8] - S[ok, 3:4])
+        return [S[ok, k:k + 1] + f * (S[ok, 4 + k:5 + k] - S[ok, k:k + 1]) for k in range(3)]
+
+    pa, pb = pos(A), pos(B)
+    d2 = sum((pa[k] - pb[k]) ** 2 for k in range(3))
+    out[ok] = d2.min(axis=1)
+    return out
+
+
+@pytest.mark.parametrize("offset,scale,rel", [(0.0, 1.0, 1e-12), (1e5, 1.0, 1e-9), (-3e3, 50.0, 1e-6),
+                                              (0.0, 1e-3, 1e-12)])
+def test_filter_keeps_borderline_pairs(offset, scale, rel):
+    """Thresholds set to each pair's own minimum distance (±rel): every pair sits
+    at the hit/miss boundary.  GPU results must equal the C oracle exactly."""
+    rng = np.random.default_rng(int(abs(offset)) + 7)
+    n = 400
+    t0 = rng.uniform(0, 10, n)
+    A = np.column_stack([rng.uniform(-1, 1, (n, 3)) * scale + offset, t0,
+                         rng.uniform(-1, 1, (n, 3)) * scale + offset, t0 + rng.uniform(0.5, 2, n)])
+    B = np.column_stack([rng.uniform(-1, 1, (n, 3)) * scale + offset, t0 + rng.uniform(-0.3, 0.3, n),
+                         rng.uniform(-1, 1, (n, 3)) * scale + offset, t0 + rng.uniform(0.5, 2, n)])
+    B[:, 7] = np.maximum(B[:, 7], B[:, 3] + 0.1)
+    md = np.sqrt(_min_dist_sq(A, B))
+    for k, sign in ((0, 1.0), (1, -1.0)):
+        sel = np.isfinite(md)
+        for i in np.nonzero(sel)[0][k::2][:60]:
+            d = float(md[i] * (1.0 + sign * rel))
+            rows = tsk.SegmentStore(np.array([0]), np.array([0]), *[A[i:i + 1, c] for c in range(8)])
+            cols = tsk.SegmentStore(np.array([1]), np.array([0]), *[B[i:i + 1, c] for c in range(8)])
+            h = tsk.pair_intervals(rows, cols, d)
+            want = c_oracle.pair(tuple(A[i]), tuple(B[i]), d)
+            got = None if len(h) == 0 else (h.t_begin[0], h.t_end[0])
+            assert got == want, (i, d)
+
+
+def test_filter_exact_meetings_and_parallel_motion():
+    """d = 0 meetings (lines crossing exactly) and near-parallel movers
+    (tiny |w|) against the C oracle over a dense mesh."""
+    rng = np.random.default_rng(11)
+    n = 600
+    t0 = np.round(rng.uniform(0, 20, n), 1)
+    base = np.round(rng.uniform(-50, 50, (n, 3)), 1)
+    vel = np.round(rng.uniform(-2, 2, (n, 3)), 1)
+    arr = {"traj": np.arange(n), "seg": np.zeros(n, np.int64),
+           "xs": base[:, 0], "ys": base[:, 1], "zs": base[:, 2], "ts": t0,
+           "xe": base[:, 0] + vel[:, 0], "ye": base[:, 1] + vel[:, 1], "ze": base[:, 2] + vel[:, 2],
+           "te": t0 + 1.0}
+    par = dict(arr)
+    par["traj"] = np.arange(n) + 10_000
+    jit = rng.integers(0, 2, n) * 1e-13
+    for k, c in (("xs", 0), ("ys", 1), ("zs", 2)):
+        par[k] = arr[k] + 0.5
+    for k, c in (("xe", 0), ("ye", 1), ("ze", 2)):
+        par[k] = arr[k] + 0.5 + jit
+    rows = _store(arr)
+    cols = _store(par)
+    for d in (0.0, 0.8660254037844386, 0.8660254037844387, 3.0):
+        h = tsk.pair_intervals(rows, cols, d)
+        ri, ci, tb, te, tm, sm = orc.pair_mesh(_cols(rows), _cols(cols), d)
+        assert np.array_equal(h.row_idx, ri) and np.array_equal(h.col_idx, ci), d
+        assert np.array_equal(h.t_begin, tb) and np.array_equal(h.t_end, te), d
+    h0 = tsk.pair_intervals(rows, rows, 0.0)  # every segment meets itself
+    ri, ci, tb, te, _, _ = orc.pair_mesh(_cols(rows), _cols(rows), 0.0)
+    assert len(h0) == len(ri) >= n
+    assert np.array_equal(h0.t_begin, tb) and np.array_equal(h0.t_end, te)
