@@ -136,7 +136,7 @@ class ClockSampler:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=self.fh, stderr=subprocess.DEVNULL)
+                 "-lms", "50"], stdout=self.fh, stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
         return self
@@ -358,25 +358,28 @@ def run_ours(args, cfg):
     res = None
     if mine is not None:
         res = search_device(store, index, mine, d)  # uploads the queries once
+    # clocks are sampled from the warm-up through the e2e loop (short timed
+    # regions would otherwise fall between nvidia-smi samples)
+    clk = ClockSampler(local).__enter__()
+    t_clk = time.perf_counter()
     for _ in range(args.warmup):
         if mine is not None:
             res = search_device(store, index, mine, d, queries_resident=True)
     barrier()
     dev_ms, k1_ms, launches, work, hits, ovl = 0.0, 0.0, 0, 0.0, 0, 0
-    with ClockSampler(local) as clk:
-        w0 = time.perf_counter()
-        for _ in range(args.steps):
-            if mine is None:
-                continue
-            r = search_device(store, index, mine, d, queries_resident=True)
-            dev_ms += r.device_ms
-            k1_ms += r.k1_ms
-            launches += r.launches
-            o = int(r.per_batch[:, 2].sum())
-            ovl += o
-            hits += r.n
-            work += W_DECIDE * o + W_HIT * r.n
-        wall_s = time.perf_counter() - w0
+    w0 = time.perf_counter()
+    for _ in range(args.steps):
+        if mine is None:
+            continue
+        r = search_device(store, index, mine, d, queries_resident=True)
+        dev_ms += r.device_ms
+        k1_ms += r.k1_ms
+        launches += r.launches
+        o = int(r.per_batch[:, 2].sum())
+        ovl += o
+        hits += r.n
+        work += W_DECIDE * o + W_HIT * r.n
+    wall_s = time.perf_counter() - w0
     barrier()
     my_ints = int(ints_all[b0:b1].sum())
     t_dev = allmax(dev_ms / 1e3)
@@ -402,6 +405,9 @@ def run_ours(args, cfg):
         d2h += len(rs) * 48 + len(mine.batches) * 32
         e2e_hits += len(rs)
         assert st.interactions_computed == my_ints
+    while time.perf_counter() - t_clk < 0.3:  # at least a few samples
+        time.sleep(0.05)
+    clk.__exit__(None, None, None)
     t_e2e = allmax(e2e_s)
     e2e_value = total_ints / t_e2e if t_e2e > 0 else 0.0
     total_hits = allsum(float(hits))  # every rank joins every collective
