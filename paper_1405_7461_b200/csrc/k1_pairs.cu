@@ -334,22 +334,112 @@ __device__ __forceinline__ bool pair_filter(const Cand &r, const QVals &Q, uint3
     return ta == tb || fma(m, 0x1p-38, dq) >= 0.0;
 }
 
+// Per-warp shared state for the rare path: the warp's 32*K1_CPT candidates
+// staged in shared memory and a queue of flagged (candidate, query) pairs.
+struct CandRec {
+    double ts, te, rcp, sx, sy, sz, dx, dy, dz, ex, ey, ez;
+};
+constexpr int K1_WARPS = K1_THREADS / 32;
+constexpr int K1_QCAP = 64;  // queue entries per warp (>= 32 + 32*K1_CPT - 32)
+static_assert(K1_QCAP >= 32 * K1_CPT, "queue must hold one iteration's flags");
+
+// Output and key layout for the (non-inlined) flush, kept in shared memory
+// so the hot loop does not hold them in registers.
+struct FlushCfg {
+    unsigned long long *hit_count;
+    uint64_t *keys;
+    double *tbeg, *tend;
+    uint64_t cap;
+    double d2;
+    int minor_bits, query_major;
+};
+
+struct WarpRare {
+    CandRec *cs;  // 32*K1_CPT staged candidates of this warp
+    uint32_t *q;  // queue: candidate index << 16 | query index
+    uint64_t key_base0;  // key of (b, e_off of candidate 0, it.q0) without the j term
+    const FlushCfg *cfg;
+};
+
+__device__ __forceinline__ void append_hit_w(const FlushCfg &C, bool hit, uint64_t key, double tb,
+                                             double te, int lane) {
+    unsigned hm = __ballot_sync(0xffffffffu, hit);
+    if (!hm) return;
+    int leader = __ffs(hm) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(C.hit_count, (unsigned long long)__popc(hm));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (hit) {
+        unsigned long long idx = base + __popc(hm & ((1u << lane) - 1u));
+        if (idx < C.cap) {
+            C.keys[idx] = key;
+            C.tbeg[idx] = tb;
+            C.tend[idx] = te;
+        }
+    }
+}
+
+// Exact evaluation of up to 32 queued pairs, one per lane, converged:
+// the reference's arithmetic (pair_eval), the second filter and the exact
+// solve (core.py:503-558), then the warp-aggregated append.
+template <int TA, int TB, bool SLOW>
+__device__ __noinline__ void rare_flush(const QRec *__restrict__ sq, const WarpRare W, int n_items,
+                                        double wmin_te, double wmax_te, int lane, unsigned &n_hit) {
+    const FlushCfg &C = *W.cfg;
+    const double d2 = C.d2;
+    Hit h;
+    h.hit = false;
+    h.tb = h.te = 0.0;
+    uint64_t key = 0;
+    if (lane < n_items) {
+        const uint32_t ent = W.q[lane];
+        const int ci = (int)(ent >> 16), j = (int)(ent & 0xffffu);
+        const CandRec &cr = W.cs[ci];
+        Cand r;
+        r.ts = cr.ts; r.te = cr.te; r.rcp = cr.rcp; r.ext = __dsub_rn(cr.te, cr.ts);
+        r.sx = cr.sx; r.sy = cr.sy; r.sz = cr.sz; r.dx = cr.dx; r.dy = cr.dy; r.dz = cr.dz;
+        r.ex = cr.ex; r.ey = cr.ey; r.ez = cr.ez;
+        const uint32_t qa = (uint32_t)__cvta_generic_to_shared(sq) + (uint32_t)j * (uint32_t)sizeof(QRec);
+        const QVals Q = load_q(qa);
+        double cc, aa, dot, e;
+        const bool ex = pair_eval<TA, TB, SLOW>(r, Q, qa, wmin_te, wmax_te, d2, cc, aa, dot, e);
+        // Second filter: q(λ) = aa λ² + 2 dot λ + e can reach 0 on [0, 1] only if
+        // q(0) <= 0, q(1) <= 0 or the vertex -dot/aa lies in [0, 1].  Outside all
+        // three by m = 2^-30 (cc + d² + aa + 2|dot|) — far above the rounding of
+        // these tests — both roots lie strictly outside [0, 1] beyond their own
+        // rounding and the reference's solve reports a miss.  Flat spans always
+        // go to the exact solve.
+        const double mag = __dadd_rn(__dadd_rn(cc, d2), __dadd_rn(aa, 2.0 * fabs(dot)));
+        const double m = mag * 0x1p-30;
+        const double q1 = __dadd_rn(__dadd_rn(e, dot), __dadd_rn(dot, aa));
+        const bool vertex_in = dot <= m && __dadd_rn(dot, aa) >= -m;
+        const bool flat = Q.ts == r.te || r.ts == Q.te || Q.ts == Q.te || r.ts == r.te;
+        if (ex && (flat || !(e > m) || !(q1 > m) || vertex_in)) h = rare_pair(r, sq[j], cc, aa, dot, e, d2);
+        // candidate ci shifts the entry offset, query j the query offset
+        key = W.key_base0 + (C.query_major ? ((uint64_t)j << C.minor_bits) + (uint64_t)ci
+                                           : ((uint64_t)ci << C.minor_bits) + (uint64_t)j);
+    }
+    n_hit += h.hit ? 1u : 0u;
+    append_hit_w(C, h.hit, key, h.tb, h.te, lane);
+}
+
 // One warp, K1_CPT candidates per lane, staged queries j0..j1-1 of one
 // (TA, TB) case.  CNT: count overlaps per iteration; otherwise the caller
 // counts them for the whole range by binary search and lanes that do not
 // overlap a query are rejected on the rare path (window edges only).
+// Flagged pairs are queued and evaluated exactly 32 at a time (rare_flush),
+// so hit-dense workloads do not serialise the warp on divergent code.
 template <int TA, int TB, bool SLOW, bool CNT>
 __device__ __forceinline__ void pair_run(const K1Launch &L, const QRec *__restrict__ sq, int j0, int j1,
                                          const Cand (&r)[K1_CPT], double wmin_te, double wmax_te,
-                                         const uint64_t (&key_base)[K1_CPT], int lane,
-                                         unsigned &n_ov, unsigned &n_hit, double C2) {
+                                         const WarpRare &W, int lane, unsigned &n_ov, unsigned &n_hit,
+                                         double C2) {
     const double d2 = L.d2;
+    int qn = 0;  // queued entries (warp-uniform)
     uint32_t qa = (uint32_t)__cvta_generic_to_shared(sq) + (uint32_t)j0 * (uint32_t)sizeof(QRec);
     for (int j = j0; j < j1; ++j, qa += (uint32_t)sizeof(QRec)) {
         const QVals Q = load_q(qa);
         bool cand[K1_CPT];
-        double cc[K1_CPT], aa[K1_CPT], dot[K1_CPT], e[K1_CPT];
-        bool any = false;
 #pragma unroll
         for (int k = 0; k < K1_CPT; ++k) {
             bool ov = true;
@@ -357,59 +447,44 @@ __device__ __forceinline__ void pair_run(const K1Launch &L, const QRec *__restri
                 ov = r[k].ts <= Q.te && Q.ts <= r[k].te;  // invalid lanes: ts = +inf
                 n_ov += ov ? 1u : 0u;
             }
-            if (SLOW)  // extreme exponents: the exact evaluation is the filter
-                cand[k] = pair_eval<TA, TB, true>(r[k], Q, qa, wmin_te, wmax_te, d2, cc[k], aa[k],
-                                                  dot[k], e[k]) && ov;
-            else
+            if (SLOW) {  // extreme exponents: the exact evaluation is the filter
+                double cc, aa, dot, e;
+                cand[k] = pair_eval<TA, TB, true>(r[k], Q, qa, wmin_te, wmax_te, d2, cc, aa, dot, e) && ov;
+            } else {
                 cand[k] = pair_filter<TA, TB>(r[k], Q, qa, wmin_te, wmax_te, d2, C2) && ov;
-            any |= cand[k];
-        }
-        if (!SLOW && __ballot_sync(0xffffffffu, any)) {
-            // flagged pairs: the reference's exact arithmetic (core.py:503-537)
-            any = false;
-#pragma unroll
-            for (int k = 0; k < K1_CPT; ++k) {
-                const bool ex = pair_eval<TA, TB, false>(r[k], Q, qa, wmin_te, wmax_te, d2, cc[k], aa[k],
-                                                         dot[k], e[k]);
-                cand[k] = cand[k] && ex;
-                any |= cand[k];
             }
         }
-        if (__ballot_sync(0xffffffffu, any)) {
-            // Second filter, paid only here: the quadratic q(λ) = aa λ² + 2 dot λ + e
-            // can reach 0 on [0, 1] only if q(0) <= 0, q(1) <= 0 or its vertex
-            // -dot/aa lies in [0, 1].  Outside all three by the relative margin
-            // m = 2^-30 (cc + d² + aa + 2|dot|) — far above the rounding of these
-            // tests — both roots of the computed quadratic lie strictly outside
-            // [0, 1] by more than their own rounding, so the reference's solve
-            // (core.py:536-558) reports a miss.  Flat pairs are always re-solved.
-            bool need[K1_CPT];
-            bool any2 = false;
 #pragma unroll
-            for (int k = 0; k < K1_CPT; ++k) {
-                const double mag = __dadd_rn(__dadd_rn(cc[k], d2), __dadd_rn(aa[k], 2.0 * fabs(dot[k])));
-                const double m = mag * 0x1p-30;
-                const double q1 = __dadd_rn(__dadd_rn(e[k], dot[k]), __dadd_rn(dot[k], aa[k]));
-                const bool vertex_in = dot[k] <= m && __dadd_rn(dot[k], aa[k]) >= -m;
-                const bool flat = Q.ts == r[k].te || r[k].ts == Q.te || Q.ts == Q.te || r[k].ts == r[k].te;
-                need[k] = cand[k] && (flat || !(e[k] > m) || !(q1 > m) || vertex_in);
-                any2 |= need[k];
+        for (int k = 0; k < K1_CPT; ++k) {
+            const unsigned m = __ballot_sync(0xffffffffu, cand[k]);
+            if (!m) continue;
+            const int c = __popc(m);
+            if (qn + c > K1_QCAP) {
+                __syncwarp();
+                rare_flush<TA, TB, SLOW>(sq, W, qn < 32 ? qn : 32, wmin_te, wmax_te, lane, n_hit);
+                __syncwarp();
+                const uint32_t moved = lane + 32 < qn ? W.q[lane + 32] : 0u;
+                __syncwarp();
+                if (lane + 32 < qn) W.q[lane] = moved;
+                qn = qn > 32 ? qn - 32 : 0;
             }
-            if (__ballot_sync(0xffffffffu, any2)) {
-#pragma unroll
-                for (int k = 0; k < K1_CPT; ++k) {
-                    if (!__ballot_sync(0xffffffffu, need[k])) continue;
-                    Hit h;
-                    h.hit = false;
-                    h.tb = h.te = 0.0;
-                    if (need[k]) h = rare_pair(r[k], sq[j], cc[k], aa[k], dot[k], e[k], d2);
-                    n_hit += h.hit ? 1u : 0u;
-                    append_hit(L, h.hit,
-                               key_base[k] + (L.query_major ? ((uint64_t)j << L.minor_bits) : (uint64_t)j),
-                               h.tb, h.te, lane);
-                }
-            }
+            if (cand[k]) W.q[qn + __popc(m & ((1u << lane) - 1u))] = ((uint32_t)(k * 32 + lane) << 16) | (uint32_t)j;
+            qn += c;
         }
+        if (qn >= 32) {
+            __syncwarp();
+            rare_flush<TA, TB, SLOW>(sq, W, 32, wmin_te, wmax_te, lane, n_hit);
+            __syncwarp();
+            const uint32_t moved = lane + 32 < qn ? W.q[lane + 32] : 0u;
+            __syncwarp();
+            if (lane + 32 < qn) W.q[lane] = moved;
+            qn -= 32;
+        }
+    }
+    if (qn > 0) {
+        __syncwarp();
+        rare_flush<TA, TB, SLOW>(sq, W, qn, wmin_te, wmax_te, lane, n_hit);
+        __syncwarp();
     }
 }
 
@@ -472,8 +547,25 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
     __shared__ ItemCtx it_sh;
     __shared__ int64_t item_sh;
     __shared__ unsigned long long red_ov, red_hit;
+    extern __shared__ __align__(16) unsigned char k1_dyn[];  // per-warp rare-path state
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ FlushCfg fcfg;
+    if (tid == 0) {
+        fcfg.hit_count = L.hit_count;
+        fcfg.keys = L.keys;
+        fcfg.tbeg = L.tbeg;
+        fcfg.tend = L.tend;
+        fcfg.cap = L.cap;
+        fcfg.d2 = L.d2;
+        fcfg.minor_bits = L.minor_bits;
+        fcfg.query_major = L.query_major;
+    }
+    WarpRare W;
+    W.cfg = &fcfg;
+    W.cs = reinterpret_cast<CandRec *>(k1_dyn) + (size_t)warp * 32 * K1_CPT;
+    W.q = reinterpret_cast<uint32_t *>(k1_dyn + sizeof(CandRec) * 32 * K1_CPT * K1_WARPS) +
+          (size_t)warp * K1_QCAP;
     const int64_t total = L.plan.meta[0];
     const int sub = (int)L.plan.meta[1];
     constexpr int64_t STRIDE = (int64_t)K1_THREADS * K1_CPT;  // candidates per sub-tile
@@ -567,7 +659,6 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
             if (base > it.c_hi) break;  // block-uniform
             const int64_t wbase = base + (int64_t)warp * 32 * K1_CPT;
             Cand r[K1_CPT];
-            uint64_t key_base[K1_CPT];
             bool valid_any = false, unsafe_r = false;
             double wmin = INFINITY, wmax = -INFINITY, wmin_te = INFINITY, wmax_ts = -INFINITY;
 #pragma unroll
@@ -592,9 +683,16 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
                     r[k].dx = r[k].dy = r[k].dz = 0.0;
                 }
                 valid_any |= valid;
-                // key of (b, e_off, q_off = it.q0 + j) without the j term
-                key_base[k] = make_key(L, it.b, e - L.plan.first[it.b], it.q0);
+                // stage for the rare path (queued pairs are evaluated from here)
+                CandRec &cr = W.cs[k * 32 + lane];
+                cr.ts = r[k].ts; cr.te = r[k].te; cr.rcp = r[k].rcp;
+                cr.sx = r[k].sx; cr.sy = r[k].sy; cr.sz = r[k].sz;
+                cr.dx = r[k].dx; cr.dy = r[k].dy; cr.dz = r[k].dz;
+                cr.ex = r[k].ex; cr.ey = r[k].ey; cr.ez = r[k].ez;
             }
+            // key of (b, e_off of the warp's candidate 0, q_off = it.q0) without the j term
+            W.key_base0 = make_key(L, it.b, wbase - L.plan.first[it.b], it.q0);
+            __syncwarp();
             if (L.noop) continue;
             if (!__any_sync(0xffffffffu, valid_any)) continue;
             // warp window over the staged queries and its start-time case ranges
@@ -620,9 +718,9 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
             const bool c_tb_r = jlo < ja && pm[ja - 1] < wmin_te;
             const bool r_tb_c = jb < jhi && sm[jb] > wmax;
             if (slow) {
-                pair_run<TA_C, TB_DYN, true, true>(L, sq, jlo, ja, r, wmin_te, wmax, key_base, lane, n_ov, n_hit, C2);
-                pair_run<TA_BOTH, TB_DYN, true, true>(L, sq, ja, jb, r, wmin_te, wmax, key_base, lane, n_ov, n_hit, C2);
-                pair_run<TA_R, TB_DYN, true, true>(L, sq, jb, jhi, r, wmin_te, wmax, key_base, lane, n_ov, n_hit, C2);
+                pair_run<TA_C, TB_DYN, true, true>(L, sq, jlo, ja, r, wmin_te, wmax, W, lane, n_ov, n_hit, C2);
+                pair_run<TA_BOTH, TB_DYN, true, true>(L, sq, ja, jb, r, wmin_te, wmax, W, lane, n_ov, n_hit, C2);
+                pair_run<TA_R, TB_DYN, true, true>(L, sq, jb, jhi, r, wmin_te, wmax, W, lane, n_ov, n_hit, C2);
                 continue;
             }
             if (c_tb_r && te_sorted) {
@@ -630,19 +728,19 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
 #pragma unroll
                 for (int k = 0; k < K1_CPT; ++k)
                     n_ov += (unsigned)(ja - clampi(lower_bound_te(sq, it.nt, r[k].ts), jlo, ja));
-                pair_run<TA_C, TB_R, false, false>(L, sq, jlo, ja, r, wmin_te, wmax, key_base, lane, n_ov, n_hit, C2);
+                pair_run<TA_C, TB_R, false, false>(L, sq, jlo, ja, r, wmin_te, wmax, W, lane, n_ov, n_hit, C2);
             } else {
-                pair_run<TA_C, TB_DYN, false, true>(L, sq, jlo, ja, r, wmin_te, wmax, key_base, lane, n_ov, n_hit, C2);
+                pair_run<TA_C, TB_DYN, false, true>(L, sq, jlo, ja, r, wmin_te, wmax, W, lane, n_ov, n_hit, C2);
             }
-            pair_run<TA_BOTH, TB_DYN, false, true>(L, sq, ja, jb, r, wmin_te, wmax, key_base, lane, n_ov, n_hit, C2);
+            pair_run<TA_BOTH, TB_DYN, false, true>(L, sq, ja, jb, r, wmin_te, wmax, W, lane, n_ov, n_hit, C2);
             if (r_tb_c) {
                 // overlap <=> cts <= r.te; cts ascending over the tile
 #pragma unroll
                 for (int k = 0; k < K1_CPT; ++k)
                     n_ov += (unsigned)(clampi(upper_bound_ts(sq, it.nt, r[k].te), jb, jhi) - jb);
-                pair_run<TA_R, TB_C, false, false>(L, sq, jb, jhi, r, wmin_te, wmax, key_base, lane, n_ov, n_hit, C2);
+                pair_run<TA_R, TB_C, false, false>(L, sq, jb, jhi, r, wmin_te, wmax, W, lane, n_ov, n_hit, C2);
             } else {
-                pair_run<TA_R, TB_DYN, false, true>(L, sq, jb, jhi, r, wmin_te, wmax, key_base, lane, n_ov, n_hit, C2);
+                pair_run<TA_R, TB_DYN, false, true>(L, sq, jb, jhi, r, wmin_te, wmax, W, lane, n_ov, n_hit, C2);
             }
         }
         // per-batch counters (64-bit)
@@ -663,16 +761,30 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
     }
 }
 
+static size_t k1_dyn_smem() {
+    return (sizeof(CandRec) * 32 * K1_CPT + sizeof(uint32_t) * K1_QCAP) * K1_WARPS;
+}
+
+static void k1_set_attrs() {
+    static bool done = false;
+    if (!done) {
+        cudaFuncSetAttribute(k1_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k1_dyn_smem());
+        done = true;
+    }
+}
+
 int k1_blocks_per_sm() {
+    k1_set_attrs();
     int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k1_pairs, K1_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k1_pairs, K1_THREADS, k1_dyn_smem());
     return n > 0 ? n : 1;
 }
 
 int k1_candidates_per_thread() { return K1_CPT; }
 
 void launch_k1(const K1Launch &L, int grid, cudaStream_t st) {
-    k1_pairs<<<grid, K1_THREADS, 0, st>>>(L);
+    k1_set_attrs();
+    k1_pairs<<<grid, K1_THREADS, k1_dyn_smem(), st>>>(L);
     TSK_CUDA(cudaGetLastError());
 }
 
