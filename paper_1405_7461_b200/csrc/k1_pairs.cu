@@ -29,6 +29,8 @@
 // margin; the few candidates that pass are re-solved with the reference's
 // exact root formula.  All ops are binary64 with explicit rounding;
 // divisions use qdiv() with a per-segment RN(1/ext).
+#include <atomic>
+
 #include "tsk_internal.cuh"
 
 #ifndef K1_CPT
@@ -765,11 +767,16 @@ static size_t k1_dyn_smem() {
     return (sizeof(CandRec) * 32 * K1_CPT + sizeof(uint32_t) * K1_QCAP) * K1_WARPS;
 }
 
+// The dynamic shared-memory limit is a per-device function attribute.
 static void k1_set_attrs() {
-    static bool done = false;
-    if (!done) {
-        cudaFuncSetAttribute(k1_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k1_dyn_smem());
-        done = true;
+    static std::atomic<uint64_t> done_mask{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(done_mask.load() & bit)) {
+        TSK_CUDA(cudaFuncSetAttribute(k1_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)k1_dyn_smem()));
+        done_mask.fetch_or(bit);
     }
 }
 
