@@ -384,18 +384,29 @@ __global__ void __launch_bounds__(1024, 1) k_plan_items(int64_t nb, const int64_
         typename BR::TempStorage r;
         typename BS::TempStorage s;
     } tmp;
-    __shared__ long long carry;
+    __shared__ long long carry, tiles_sh;
     __shared__ int sub_sh;
-    long long acc = 0;
-    for (int64_t b = threadIdx.x; b < nb; b += blockDim.x) {
-        long long c = first[b] >= 0 ? last[b] - first[b] + 1 : 0;
-        long long tq = (hi[b] - lo[b] + 1 + K1_TQ - 1) / K1_TQ;
-        acc += ((c + stride - 1) / stride) * tq;
+    // query tile: K1_TQ, halved (down to 32) while the grid would get fewer
+    // than 4 waves of items — small plans otherwise under-fill 148 SMs
+    const long long want = 4 * slots;
+    int tqs = K1_TQ;
+    for (;;) {
+        long long acc = 0;
+        for (int64_t b = threadIdx.x; b < nb; b += blockDim.x) {
+            long long c = first[b] >= 0 ? last[b] - first[b] + 1 : 0;
+            long long tq = (hi[b] - lo[b] + 1 + tqs - 1) / tqs;
+            acc += ((c + stride - 1) / stride) * tq;
+        }
+        long long tiles = BR(tmp.r).Sum(acc);
+        if (threadIdx.x == 0) tiles_sh = tiles;
+        __syncthreads();
+        tiles = tiles_sh;
+        __syncthreads();
+        if (tiles >= want || tqs <= 32) break;
+        tqs >>= 1;
     }
-    long long tiles = BR(tmp.r).Sum(acc);
     if (threadIdx.x == 0) {
-        long long want = 4 * slots;
-        int sub = (int)(tiles / (want > 0 ? want : 1));
+        int sub = (int)(tiles_sh / (want > 0 ? want : 1));
         sub_sh = sub < 1 ? 1 : (sub > K1_MAX_SUB ? K1_MAX_SUB : sub);
         carry = 0;
     }
@@ -406,7 +417,7 @@ __global__ void __launch_bounds__(1024, 1) k_plan_items(int64_t nb, const int64_
         long long v = 0;
         if (b < nb) {
             long long c = first[b] >= 0 ? last[b] - first[b] + 1 : 0;
-            long long tq = (hi[b] - lo[b] + 1 + K1_TQ - 1) / K1_TQ;
+            long long tq = (hi[b] - lo[b] + 1 + tqs - 1) / tqs;
             v = ((c + ct - 1) / ct) * tq;
         }
         long long ex, agg;
@@ -420,6 +431,7 @@ __global__ void __launch_bounds__(1024, 1) k_plan_items(int64_t nb, const int64_
         item_off[nb] = carry;
         meta[0] = carry;
         meta[1] = sub_sh;
+        meta[2] = tqs;
     }
 }
 

@@ -570,6 +570,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
           (size_t)warp * K1_QCAP;
     const int64_t total = L.plan.meta[0];
     const int sub = (int)L.plan.meta[1];
+    const int64_t tqs = L.plan.meta[2];  // query tile size chosen by k_plan_items (<= K1_TQ)
     constexpr int64_t STRIDE = (int64_t)K1_THREADS * K1_CPT;  // candidates per sub-tile
     const int64_t ct = STRIDE * sub;
     const int64_t nb = L.plan.nb;
@@ -593,13 +594,13 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
                 const int64_t b = a;
                 const int64_t local = item - L.plan.item_off[b];
                 const int64_t s_b = L.plan.hi[b] - L.plan.lo[b] + 1;
-                const int64_t tq_n = (s_b + K1_TQ - 1) / K1_TQ;
+                const int64_t tq_n = (s_b + tqs - 1) / tqs;
                 const int64_t tq = local % tq_n, tc = local / tq_n;
                 ItemCtx c;
                 c.b = b;
-                c.q0 = tq * K1_TQ;
+                c.q0 = tq * tqs;
                 c.lo_q = L.plan.lo[b] + c.q0;
-                c.nt = (int)(s_b - c.q0 < K1_TQ ? s_b - c.q0 : K1_TQ);
+                c.nt = (int)(s_b - c.q0 < tqs ? s_b - c.q0 : tqs);
                 c.first_c = L.plan.first[b] + tc * ct;
                 c.c_hi = c.first_c + ct - 1 < L.plan.last[b] ? c.first_c + ct - 1 : L.plan.last[b];
                 it_sh = c;
