@@ -35,12 +35,12 @@ void DBuf::release(cudaStream_t) {
 
 void soa_alloc(Soa &s, int64_t n, bool with_ids, cudaStream_t st) {
     size_t nn = (size_t)(n > 0 ? n : 1);
-    size_t per = 12 * sizeof(double) + (with_ids ? 2 * sizeof(int64_t) : 0) + 1;
+    size_t per = 15 * sizeof(double) + (with_ids ? 2 * sizeof(int64_t) : 0) + 1;
     s.storage.reserve(nn * per + 64, st);
     char *base = s.storage.as<char>();
-    double **cols[12] = {&s.ts, &s.te, &s.sx, &s.sy, &s.sz, &s.ex,
-                         &s.ey, &s.ez, &s.dx, &s.dy, &s.dz, &s.rcp};
-    for (int k = 0; k < 12; ++k) {
+    double **cols[15] = {&s.ts, &s.te, &s.sx, &s.sy, &s.sz, &s.ex, &s.ey, &s.ez,
+                         &s.dx, &s.dy, &s.dz, &s.rcp, &s.vx, &s.vy, &s.vz};
+    for (int k = 0; k < 15; ++k) {
         *cols[k] = reinterpret_cast<double *>(base);
         base += nn * sizeof(double);
     }
@@ -68,12 +68,38 @@ void soa_upload(Soa &s, const tsk_columns *c, cudaStream_t st) {
     }
 }
 
-// Exponent window inside which qdiv() is proven exact: all times and
-// extents are 0 or of magnitude in [2^-900, 2^1000], coordinates below
-// 2^1000.  Then every residual of qdiv stays a normal number.
-__device__ __forceinline__ bool mag_bad(double v) {
-    double a = fabs(v);
-    return (a != 0.0 && a < 0x1p-900) || a > 0x1p1000;
+// Exponent window inside which qdiv() is proven exact and K1's filter
+// bound holds (filter.cuh): times and extents 0 or of magnitude in
+// [2^-900, 2^1000], coordinates of magnitude <= 2^1000, velocity components
+// 0 or of magnitude in [2^-1000, 2^1000].  NaN fails every test.  Unsafe
+// segments send their K1 tiles to the exact IEEE path.
+__device__ __forceinline__ bool mag_ok(double v) {
+    const double a = fabs(v);
+    return a == 0.0 || (a >= 0x1p-900 && a <= 0x1p1000);
+}
+__device__ __forceinline__ bool coord_ok(double v) { return fabs(v) <= 0x1p1000; }
+__device__ __forceinline__ bool vel_ok(double v) {
+    const double a = fabs(v);
+    return a == 0.0 || (a >= 0x1p-1000 && a <= 0x1p1000);
+}
+
+struct SegHoist {
+    double ext, rcp, d[3], v[3];
+    bool unsafe;
+};
+
+__device__ __forceinline__ SegHoist seg_hoist(double t0, double t1, const double s[3], const double e[3]) {
+    SegHoist h;
+    h.ext = __dsub_rn(t1, t0);
+    h.rcp = h.ext > 0.0 ? __drcp_rn(h.ext) : 0.0;
+    bool ok = mag_ok(t0) && mag_ok(t1) && mag_ok(h.ext);
+    for (int i = 0; i < 3; ++i) {
+        h.d[i] = __dsub_rn(e[i], s[i]);
+        h.v[i] = __dmul_rn(h.d[i], h.rcp);  // seg_velocity (filter.cuh)
+        ok = ok && coord_ok(s[i]) && coord_ok(e[i]) && vel_ok(h.v[i]);
+    }
+    h.unsafe = !ok;
+    return h;
 }
 
 __global__ void k_hoist(int64_t n, const double *__restrict__ ts, const double *__restrict__ te,
@@ -81,20 +107,18 @@ __global__ void k_hoist(int64_t n, const double *__restrict__ ts, const double *
                         const double *__restrict__ sz, const double *__restrict__ ex,
                         const double *__restrict__ ey, const double *__restrict__ ez,
                         double *__restrict__ dx, double *__restrict__ dy, double *__restrict__ dz,
-                        double *__restrict__ rcp, uint8_t *__restrict__ unsafe, int *flags) {
+                        double *__restrict__ rcp, double *__restrict__ vx, double *__restrict__ vy,
+                        double *__restrict__ vz, uint8_t *__restrict__ unsafe, int *flags) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        double t0 = ts[i], t1 = te[i];
-        dx[i] = __dsub_rn(ex[i], sx[i]);
-        dy[i] = __dsub_rn(ey[i], sy[i]);
-        dz[i] = __dsub_rn(ez[i], sz[i]);
-        double ext = __dsub_rn(t1, t0);
-        rcp[i] = ext > 0.0 ? __drcp_rn(ext) : 0.0;
-        bool bad = mag_bad(t0) || mag_bad(t1) || (ext > 0.0 && mag_bad(ext)) ||
-                   fabs(sx[i]) > 0x1p1000 || fabs(sy[i]) > 0x1p1000 || fabs(sz[i]) > 0x1p1000 ||
-                   fabs(ex[i]) > 0x1p1000 || fabs(ey[i]) > 0x1p1000 || fabs(ez[i]) > 0x1p1000;
-        unsafe[i] = bad ? 1 : 0;
-        if (bad) atomicOr(&flags[0], 1);
+        const double t0 = ts[i];
+        const double s[3] = {sx[i], sy[i], sz[i]}, e[3] = {ex[i], ey[i], ez[i]};
+        const SegHoist h = seg_hoist(t0, te[i], s, e);
+        dx[i] = h.d[0]; dy[i] = h.d[1]; dz[i] = h.d[2];
+        vx[i] = h.v[0]; vy[i] = h.v[1]; vz[i] = h.v[2];
+        rcp[i] = h.rcp;
+        unsafe[i] = h.unsafe ? 1 : 0;
+        if (h.unsafe) atomicOr(&flags[0], 1);
         if (i + 1 < n && ts[i + 1] < t0) atomicOr(&flags[1], 1);
     }
 }
@@ -110,7 +134,7 @@ void soa_hoist(Soa &s, cudaStream_t st) {
     TSK_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), st));
     int grid = (int)std::min<int64_t>((s.n + 255) / 256, 148 * 16);
     k_hoist<<<grid, 256, 0, st>>>(s.n, s.ts, s.te, s.sx, s.sy, s.sz, s.ex, s.ey, s.ez, s.dx, s.dy,
-                                  s.dz, s.rcp, s.unsafe, flags);
+                                  s.dz, s.rcp, s.vx, s.vy, s.vz, s.unsafe, flags);
     TSK_CUDA(cudaGetLastError());
     int h[2];
     TSK_CUDA(cudaMemcpyAsync(h, flags, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -173,15 +197,12 @@ __global__ void k_qprep(int64_t n, const double *__restrict__ ts, const double *
         r.ex = ex[i];
         r.ey = ey[i];
         r.ez = ez[i];
-        r.dx = __dsub_rn(r.ex, r.sx);
-        r.dy = __dsub_rn(r.ey, r.sy);
-        r.dz = __dsub_rn(r.ez, r.sz);
-        r.ext = __dsub_rn(r.te, r.ts);
-        r.rcp = r.ext > 0.0 ? __drcp_rn(r.ext) : 0.0;
-        bool bad = mag_bad(r.ts) || mag_bad(r.te) || (r.ext > 0.0 && mag_bad(r.ext)) ||
-                   fabs(r.sx) > 0x1p1000 || fabs(r.sy) > 0x1p1000 || fabs(r.sz) > 0x1p1000 ||
-                   fabs(r.ex) > 0x1p1000 || fabs(r.ey) > 0x1p1000 || fabs(r.ez) > 0x1p1000;
-        r.flag = bad ? 1.0 : 0.0;
+        const double s[3] = {r.sx, r.sy, r.sz}, e[3] = {r.ex, r.ey, r.ez};
+        const SegHoist h = seg_hoist(r.ts, r.te, s, e);
+        r.ext = h.ext;
+        r.dx = h.d[0]; r.dy = h.d[1]; r.dz = h.d[2];
+        r.vx = h.v[0]; r.vy = h.v[1]; r.vz = h.v[2];
+        r.flag = h.unsafe ? 1.0 : 0.0;
         out[i] = r;
         if (i + 1 < n && ts[i + 1] < r.ts) atomicOr(&flags[0], 1);
         cm = fmax(cm, fmax(fmax(fabs(r.sx), fabs(r.sy)), fmax(fabs(r.sz), fmax(fabs(r.ex), fmax(fabs(r.ey), fabs(r.ez))))));

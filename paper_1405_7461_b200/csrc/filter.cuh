@@ -1,0 +1,138 @@
+// filter.cuh — K1's conservative FP64 pair filter (host + device).
+//
+// The common path of K1 only has to decide which (candidate, query) pairs
+// could have a non-negative reference discriminant (core.py:533-537); the
+// flagged ones are recomputed with the reference's exact operation sequence
+// (pair_eval in k1_pairs.cu).  This header holds the filter arithmetic as a
+// pure function so tools/filter_check.cu can test it on the CPU against the
+// exact restatement (oracle/pair_oracle.c) on adversarial pairs.
+//
+// Velocity form.  Each segment carries v = RN(d * RN(1/ext)) (0 for a
+// waypoint).  With delta = cts - r.ts and the shared span [ta, tb]:
+//   u = (r.s - c.s) + delta * v_late      (separation at ta; v_late is the
+//                                          velocity of the earlier starter)
+//   w = (tb - ta) * (r.v - c.v)           (change of separation over the span)
+// and for a query inside every candidate's span (TA_R/TB_R)
+//   w = c.ext * r.v - c.d                 (query endpoints taken verbatim).
+// A zero-length span gives w = 0 exactly, hence aa = dot = 0 and the test
+// below passes: flat pairs are flagged with no separate time comparison,
+// except in TA_R/TB_R, where the query's own ext == 0 is tested.
+//
+// Error bound.  For overlapping pairs of a launch with C = max |coordinate|
+// (C <= 2^250, d <= 2^250, C == 0 or C >= 2^-200; otherwise K1 runs the
+// exact path everywhere) and segments inside the exponent window of
+// seg_unsafe() (db.cu), the filter's u and w are within eu <= 23 ulp(C)
+// ~ 2^-48.5 C and ew <= 64 ulp(C) ~ 2^-47 C per component of the
+// reference's U and W.  Writing D(U,W) = (U.W)^2 - |W|^2 (|U|^2 - d^2)
+// = d^2 |W|^2 - |U x W|^2:
+//   |D(u,w) - D(U,W)| <= 2|U||W|^2 |a| + (|U|^2 + d^2) 2|W||b| + h.o.
+//                     <= 2^-45 C^2 aa + (cc + d^2)(2^-35 aa + 2^-57.4 C^2)
+// (|a| <= sqrt3 eu, |b| <= sqrt3 ew, 2|W||b| <= 2^-35 |W|^2 + 2^35 |b|^2),
+// and both roundings of the discriminant (the reference's and ours) are
+// below 2^-48 aa (cc + d^2).  The test
+//   t = dot^2 - aa e + 2^-35 aa s + KA aa + KC s >= 0,   s = cc + d^2,
+//   KA = 2^-40 C^2,  KC = 2^-54 C^2
+// therefore holds whenever the reference's discriminant is >= 0.  It is
+// evaluated as
+//   x  = fma(e, 2^-35 - 1, 2^-34 d^2 + KA)          (= 2^-35 s - e + KA)
+//   t  = fma(aa, x, dot^2)
+//   t2 = fma(KC, e, t)  >=  -2 KC d^2
+// whose own roundings are below 2^-50 aa s + 2^-52 |t|, inside the slack.
+#pragma once
+
+#include <math.h>
+
+#ifdef __CUDACC__
+#define TSK_HD __host__ __device__ __forceinline__
+#else
+#define TSK_HD inline
+#endif
+
+namespace tsk {
+
+// Clip-at-ta cases of a query against a warp's candidates.  Queries in a
+// tile are sorted by start time, so each case is a contiguous j range:
+//   TA_C    cts <  every candidate's ts: the query started first
+//   TA_R    cts >  every candidate's ts: the entry started first
+//   TA_BOTH otherwise (decided per pair)
+enum { TA_C = 0, TA_R = 1, TA_BOTH = 2 };
+// Clip-at-tb cases; TB_R / TB_C are proven for a whole j range from the
+// tile's running max / suffix min of query end times, TB_DYN decides per
+// query (cte < min te: TB_R, cte > max te: TB_C, else per pair).
+enum { TB_R = 0, TB_C = 1, TB_DYN = 2 };
+
+// Filter view of a candidate (held in registers).
+struct CandF {
+    double ts, te, ext, sx, sy, sz, vx, vy, vz;
+};
+
+// Filter view of a query (read from its shared-memory record).
+struct QF {
+    double ts, te, sx, sy, sz, ext, vx, vy, vz, dx, dy, dz;
+};
+
+struct FilterK {
+    double d2, k5, kc, t0;
+};
+
+TSK_HD FilterK filter_consts(double cmax, double d2) {
+    const double c2 = cmax * cmax;
+    FilterK k;
+    k.d2 = d2;
+    const double ka = 0x1p-40 * c2;
+    k.kc = 0x1p-54 * c2;
+    k.k5 = fma(0x1p-34, d2, ka);
+    k.t0 = -2.0 * k.kc * d2;
+    return k;
+}
+
+// Launch-level validity of the filter's error bound (else: exact path only).
+TSK_HD bool filter_ok(double cmax, double d2) {
+    return cmax <= 0x1p250 && d2 <= 0x1p500 && (cmax == 0.0 || cmax >= 0x1p-200);
+}
+
+// velocity component of a hoisted segment: RN(d * rcp), rcp = RN(1/ext) or 0
+TSK_HD double seg_velocity(double d, double rcp) { return d * rcp; }
+
+template <int TA, int TB>
+TSK_HD bool pair_filter(const CandF &r, const QF &Q, double wmin_te, double wmax_te, const FilterK &K) {
+    const double rv[3] = {r.vx, r.vy, r.vz}, qv[3] = {Q.vx, Q.vy, Q.vz};
+    const double ds[3] = {r.sx - Q.sx, r.sy - Q.sy, r.sz - Q.sz};
+    const double dl = Q.ts - r.ts;
+    double u[3], ta;
+    if (TA == TA_R) {
+        ta = Q.ts;
+        for (int i = 0; i < 3; ++i) u[i] = fma(dl, rv[i], ds[i]);
+    } else if (TA == TA_C) {
+        ta = r.ts;
+        for (int i = 0; i < 3; ++i) u[i] = fma(dl, qv[i], ds[i]);
+    } else {
+        const bool qlate = dl >= 0.0;
+        ta = qlate ? Q.ts : r.ts;
+        for (int i = 0; i < 3; ++i) u[i] = fma(dl, qlate ? rv[i] : qv[i], ds[i]);
+    }
+    const bool tb_r = TB == TB_R || (TB == TB_DYN && Q.te < wmin_te);
+    const bool tb_c = !tb_r && (TB == TB_C || (TB == TB_DYN && Q.te > wmax_te));
+    double w[3];
+    bool flat = false;
+    if (TA == TA_R && tb_r) {
+        const double qd[3] = {Q.dx, Q.dy, Q.dz};
+        for (int i = 0; i < 3; ++i) w[i] = fma(Q.ext, rv[i], -qd[i]);
+        flat = Q.ext == 0.0;
+    } else {
+        double span;
+        if (tb_r) span = Q.te - ta;
+        else if (tb_c) span = TA == TA_C ? r.ext : r.te - ta;
+        else span = (r.te < Q.te ? r.te : Q.te) - ta;
+        for (int i = 0; i < 3; ++i) w[i] = span * (rv[i] - qv[i]);
+    }
+    const double e = fma(u[0], u[0], fma(u[1], u[1], fma(u[2], u[2], -K.d2)));
+    const double aa = fma(w[0], w[0], fma(w[1], w[1], w[2] * w[2]));
+    const double dot = fma(u[0], w[0], fma(u[1], w[1], u[2] * w[2]));
+    const double x = fma(e, 0x1p-35 - 1.0, K.k5);
+    const double t = fma(aa, x, dot * dot);
+    const double t2 = fma(K.kc, e, t);
+    return flat || t2 >= K.t0;
+}
+
+}  // namespace tsk

@@ -31,6 +31,7 @@
 // divisions use qdiv() with a per-segment RN(1/ext).
 #include <atomic>
 
+#include "filter.cuh"
 #include "tsk_internal.cuh"
 
 #ifndef K1_CPT
@@ -49,17 +50,32 @@ __device__ __forceinline__ void lds2(uint32_t a, double &x, double &y) {
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a));
 }
 
+// Exact view of a query record (rare path); RN(1/ext) as the hoist computes it.
 struct QVals {
     double ts, te, sx, sy, sz, ext, dx, dy, dz, rcp;
 };
 
 __device__ __forceinline__ QVals load_q(uint32_t a) {
     QVals q;
+    double vz_unused;
     lds2(a + 0, q.ts, q.te);
     lds2(a + 16, q.sx, q.sy);
     lds2(a + 32, q.sz, q.ext);
-    lds2(a + 48, q.dx, q.dy);
-    lds2(a + 64, q.dz, q.rcp);
+    lds2(a + 64, vz_unused, q.dz);
+    lds2(a + 80, q.dx, q.dy);
+    q.rcp = q.ext > 0.0 ? __drcp_rn(q.ext) : 0.0;
+    return q;
+}
+
+// Filter view of a query record (QRec bytes 0..95).
+__device__ __forceinline__ QF load_qf(uint32_t a) {
+    QF q;
+    lds2(a + 0, q.ts, q.te);
+    lds2(a + 16, q.sx, q.sy);
+    lds2(a + 32, q.sz, q.ext);
+    lds2(a + 48, q.vx, q.vy);
+    lds2(a + 64, q.vz, q.dz);
+    lds2(a + 80, q.dx, q.dy);
     return q;
 }
 
@@ -194,15 +210,11 @@ __device__ __forceinline__ uint64_t make_key(const K1Launch &L, int64_t b, int64
     return ((uint64_t)b << (L.major_bits + L.minor_bits)) | (major << L.minor_bits) | minor;
 }
 
-// Clip-at-ta cases of a query against a warp's candidates.  Queries in a
-// tile are sorted by start time, so each case is a contiguous j range:
-//   TA_C    cts <  every candidate's ts: the query started first, interpolate it
-//   TA_R    cts >  every candidate's ts: the entry started first, interpolate it
-//   TA_BOTH otherwise: interpolate both (the later starter's f is 0 -> exact)
-enum { TA_C = 0, TA_R = 1, TA_BOTH = 2 };
-// Clip-at-tb cases; TB_R / TB_C are proven for a whole j range from the
-// tile's running max / suffix min of query end times, TB_DYN decides per query.
-enum { TB_R = 0, TB_C = 1, TB_DYN = 2 };
+// True when bb^2 = 4 dot^2 and 4 aa e of the reference's discriminant are
+// finite (core.py:537); false for NaN.
+__device__ __forceinline__ bool no_overflow(double aa, double dot, double e) {
+    return fabs(dot) <= 0x1p510 && aa <= 0x1p500 && fabs(e) <= 0x1p500;
+}
 
 // The common-path arithmetic of one (candidate, query) pair up to the hit
 // test.  Returns whether the pair needs the exact rare path.
@@ -232,8 +244,8 @@ __device__ __forceinline__ bool pair_eval(const Cand &r, const QVals &Q, uint32_
         tb = cte;
         lerp<SLOW>(cte, r.ts, r.ext, r.rcp, r.sx, r.sy, r.sz, r.dx, r.dy, r.dz, rbx, rby, rbz);
         double flag_unused;
-        lds2(qa + 80, cbx, cby);
-        lds2(qa + 96, cbz, flag_unused);
+        lds2(qa + 96, cbx, cby);
+        lds2(qa + 112, cbz, flag_unused);
     } else if (TB == TB_C || (TB == TB_DYN && cte > wmax_te)) {  // the query ends after every candidate
         tb = r.te;
         rbx = r.ex; rby = r.ey; rbz = r.ez;
@@ -245,8 +257,8 @@ __device__ __forceinline__ bool pair_eval(const Cand &r, const QVals &Q, uint32_
         lerp<SLOW>(tb, cts, Q.ext, Q.rcp, Q.sx, Q.sy, Q.sz, Q.dx, Q.dy, Q.dz, qx, qy, qz);
         const bool zr = r.te > cte, zc = cte > r.te;
         double qex, qey, qez, flag_unused;
-        lds2(qa + 80, qex, qey);
-        lds2(qa + 96, qez, flag_unused);
+        lds2(qa + 96, qex, qey);
+        lds2(qa + 112, qez, flag_unused);
         rbx = zr ? px : r.ex; rby = zr ? py : r.ey; rbz = zr ? pz : r.ez;
         cbx = zc ? qx : qex; cby = zc ? qy : qey; cbz = zc ? qz : qez;
     }
@@ -259,81 +271,11 @@ __device__ __forceinline__ bool pair_eval(const Cand &r, const QVals &Q, uint32_
     aa = __dadd_rn(__dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy)), __dmul_rn(wz, wz));
     dot = __dadd_rn(__dadd_rn(__dmul_rn(ux, wx), __dmul_rn(uy, wy)), __dmul_rn(uz, wz));
     e = __dsub_rn(cc, d2);
-    // disc / 4 (exact scaling); the margin keeps the test a superset under underflow
+    // disc / 4 (exact scaling); the margin keeps the test a superset under
+    // underflow, and pairs whose reference discriminant could overflow
+    // (bb^2 or 4 aa e beyond 2^1022: disc = +-inf or NaN) go to the exact solve
     const double dq = __dsub_rn(__dmul_rn(dot, dot), __dmul_rn(aa, e));
-    return ta == tb || dq >= -0x1p-1000;
-}
-
-// Fast conservative filter for one pair (span-clip cases as pair_eval).
-// Interpolations use f = (t - ts) * RN(1/ext) and FMAs, so positions are
-// within ~2^-46 C of the reference's (C = max |coordinate| of the launch),
-// u and w within ~2^-45 C, and the coefficients within ~2^-41 C^2 (|dot|, |e|,
-// aa scale).  The test dq_f + 2^-38 (C2 (|dot| + |e| + aa) + dot^2 + aa |e|) >= 0,
-// C2 = 16 C^2 + d^2, therefore holds for every pair whose reference
-// discriminant (core.py:537) is >= 0 — every reference hit, including the
-// constant-separation case — and flagged pairs are re-evaluated exactly
-// (pair_eval) before the reference's solve.  Flat spans are flagged by exact
-// time equality.
-template <int TA, int TB>
-__device__ __forceinline__ bool pair_filter(const Cand &r, const QVals &Q, uint32_t qa, double wmin_te,
-                                            double wmax_te, double d2, double C2) {
-    const double cts = Q.ts, cte = Q.te;
-    double ta, ra[3], ca[3], rb[3], cb[3];
-    const double rs[3] = {r.sx, r.sy, r.sz}, rd[3] = {r.dx, r.dy, r.dz};
-    const double cs[3] = {Q.sx, Q.sy, Q.sz}, cd[3] = {Q.dx, Q.dy, Q.dz};
-    if (TA == TA_R) {
-        ta = cts;
-        const double f = (cts - r.ts) * r.rcp;
-        for (int i = 0; i < 3; ++i) { ra[i] = fma(f, rd[i], rs[i]); ca[i] = cs[i]; }
-    } else if (TA == TA_C) {
-        ta = r.ts;
-        const double f = (r.ts - cts) * Q.rcp;
-        for (int i = 0; i < 3; ++i) { ra[i] = rs[i]; ca[i] = fma(f, cd[i], cs[i]); }
-    } else {
-        ta = r.ts > cts ? r.ts : cts;
-        const double fr = (ta - r.ts) * r.rcp, fc = (ta - cts) * Q.rcp;
-        for (int i = 0; i < 3; ++i) { ra[i] = fma(fr, rd[i], rs[i]); ca[i] = fma(fc, cd[i], cs[i]); }
-    }
-    double tb;
-    if (TB == TB_R || (TB == TB_DYN && cte < wmin_te)) {
-        tb = cte;
-        const double f = (cte - r.ts) * r.rcp;
-        for (int i = 0; i < 3; ++i) rb[i] = fma(f, rd[i], rs[i]);
-        double flag_unused;
-        lds2(qa + 80, cb[0], cb[1]);
-        lds2(qa + 96, cb[2], flag_unused);
-    } else if (TB == TB_C || (TB == TB_DYN && cte > wmax_te)) {
-        tb = r.te;
-        const double f = (r.te - cts) * Q.rcp;
-        rb[0] = r.ex; rb[1] = r.ey; rb[2] = r.ez;
-        for (int i = 0; i < 3; ++i) cb[i] = fma(f, cd[i], cs[i]);
-    } else {
-        tb = r.te < cte ? r.te : cte;
-        const double fr = (tb - r.ts) * r.rcp, fc = (tb - cts) * Q.rcp;
-        double qe[3], flag_unused;
-        lds2(qa + 80, qe[0], qe[1]);
-        lds2(qa + 96, qe[2], flag_unused);
-        const double re[3] = {r.ex, r.ey, r.ez};
-        const bool zr = r.te > cte, zc = cte > r.te;
-        for (int i = 0; i < 3; ++i) {
-            rb[i] = zr ? fma(fr, rd[i], rs[i]) : re[i];
-            cb[i] = zc ? fma(fc, cd[i], cs[i]) : qe[i];
-        }
-    }
-    double u[3], w[3];
-    for (int i = 0; i < 3; ++i) {
-        u[i] = ra[i] - ca[i];
-        w[i] = (rb[i] - ra[i]) - (cb[i] - ca[i]);
-    }
-    const double cc = fma(u[0], u[0], fma(u[1], u[1], u[2] * u[2]));
-    const double aa = fma(w[0], w[0], fma(w[1], w[1], w[2] * w[2]));
-    const double dot = fma(u[0], w[0], fma(u[1], w[1], u[2] * w[2]));
-    const double e = cc - d2;
-    const double ae = fabs(e);
-    const double dot2 = dot * dot;
-    const double dq = fma(-aa, e, dot2);
-    const double m = fma(C2, fabs(dot) + ae + aa, fma(aa, ae, dot2));
-    return ta == tb || fma(m, 0x1p-38, dq) >= 0.0;
+    return ta == tb || dq >= -0x1p-1000 || !no_overflow(aa, dot, e);
 }
 
 // Per-warp shared state for the rare path: the warp's 32*K1_CPT candidates
@@ -342,8 +284,10 @@ struct CandRec {
     double ts, te, rcp, sx, sy, sz, dx, dy, dz, ex, ey, ez;
 };
 constexpr int K1_WARPS = K1_THREADS / 32;
-constexpr int K1_QCAP = 64;  // queue entries per warp (>= 32 + 32*K1_CPT - 32)
-static_assert(K1_QCAP >= 32 * K1_CPT, "queue must hold one iteration's flags");
+// Queue entries per warp.  Before each append of up to 32 flags the queue is
+// flushed down to < 32 entries if it would overflow, and a flush moves at
+// most 32 remaining entries, so 64 suffices for any K1_CPT.
+constexpr int K1_QCAP = 64;
 
 // Output and key layout for the (non-inlined) flush, kept in shared memory
 // so the hot loop does not hold them in registers.
@@ -355,6 +299,14 @@ struct FlushCfg {
     double d2;
     int minor_bits, query_major;
 };
+
+__device__ __forceinline__ Cand cand_exact(const CandRec &cr) {
+    Cand r;
+    r.ts = cr.ts; r.te = cr.te; r.rcp = cr.rcp; r.ext = __dsub_rn(cr.te, cr.ts);
+    r.sx = cr.sx; r.sy = cr.sy; r.sz = cr.sz; r.dx = cr.dx; r.dy = cr.dy; r.dz = cr.dz;
+    r.ex = cr.ex; r.ey = cr.ey; r.ez = cr.ez;
+    return r;
+}
 
 struct WarpRare {
     CandRec *cs;  // 32*K1_CPT staged candidates of this warp
@@ -396,11 +348,7 @@ __device__ __noinline__ void rare_flush(const QRec *__restrict__ sq, const WarpR
     if (lane < n_items) {
         const uint32_t ent = W.q[lane];
         const int ci = (int)(ent >> 16), j = (int)(ent & 0xffffu);
-        const CandRec &cr = W.cs[ci];
-        Cand r;
-        r.ts = cr.ts; r.te = cr.te; r.rcp = cr.rcp; r.ext = __dsub_rn(cr.te, cr.ts);
-        r.sx = cr.sx; r.sy = cr.sy; r.sz = cr.sz; r.dx = cr.dx; r.dy = cr.dy; r.dz = cr.dz;
-        r.ex = cr.ex; r.ey = cr.ey; r.ez = cr.ez;
+        const Cand r = cand_exact(W.cs[ci]);
         const uint32_t qa = (uint32_t)__cvta_generic_to_shared(sq) + (uint32_t)j * (uint32_t)sizeof(QRec);
         const QVals Q = load_q(qa);
         double cc, aa, dot, e;
@@ -411,12 +359,16 @@ __device__ __noinline__ void rare_flush(const QRec *__restrict__ sq, const WarpR
         // these tests — both roots lie strictly outside [0, 1] beyond their own
         // rounding and the reference's solve reports a miss.  Flat spans always
         // go to the exact solve.
+        // (only where the reference's discriminant neither overflows nor has
+        // a subnormal scale: exact-path tiles can hold any finite input)
         const double mag = __dadd_rn(__dadd_rn(cc, d2), __dadd_rn(aa, 2.0 * fabs(dot)));
         const double m = mag * 0x1p-30;
         const double q1 = __dadd_rn(__dadd_rn(e, dot), __dadd_rn(dot, aa));
         const bool vertex_in = dot <= m && __dadd_rn(dot, aa) >= -m;
         const bool flat = Q.ts == r.te || r.ts == Q.te || Q.ts == Q.te || r.ts == r.te;
-        if (ex && (flat || !(e > m) || !(q1 > m) || vertex_in)) h = rare_pair(r, sq[j], cc, aa, dot, e, d2);
+        const bool plain = no_overflow(aa, dot, e) && mag >= 0x1p-900;
+        if (ex && (flat || !plain || !(e > m) || !(q1 > m) || vertex_in))
+            h = rare_pair(r, sq[j], cc, aa, dot, e, d2);
         // candidate ci shifts the entry offset, query j the query offset
         key = W.key_base0 + (C.query_major ? ((uint64_t)j << C.minor_bits) + (uint64_t)ci
                                            : ((uint64_t)ci << C.minor_bits) + (uint64_t)j);
@@ -433,27 +385,41 @@ __device__ __noinline__ void rare_flush(const QRec *__restrict__ sq, const WarpR
 // so hit-dense workloads do not serialise the warp on divergent code.
 template <int TA, int TB, bool SLOW, bool CNT>
 __device__ __forceinline__ void pair_run(const K1Launch &L, const QRec *__restrict__ sq, int j0, int j1,
-                                         const Cand (&r)[K1_CPT], double wmin_te, double wmax_te,
+                                         const CandF (&r)[K1_CPT], double wmin_te, double wmax_te,
                                          const WarpRare &W, int lane, unsigned &n_ov, unsigned &n_hit,
-                                         double C2) {
-    const double d2 = L.d2;
+                                         const FilterK &K) {
     int qn = 0;  // queued entries (warp-uniform)
     uint32_t qa = (uint32_t)__cvta_generic_to_shared(sq) + (uint32_t)j0 * (uint32_t)sizeof(QRec);
     for (int j = j0; j < j1; ++j, qa += (uint32_t)sizeof(QRec)) {
-        const QVals Q = load_q(qa);
         bool cand[K1_CPT];
+        if (SLOW) {  // unsafe tile or launch: the exact evaluation is the filter
+            const QVals Q = load_q(qa);
 #pragma unroll
-        for (int k = 0; k < K1_CPT; ++k) {
-            bool ov = true;
-            if (CNT) {
-                ov = r[k].ts <= Q.te && Q.ts <= r[k].te;  // invalid lanes: ts = +inf
-                n_ov += ov ? 1u : 0u;
-            }
-            if (SLOW) {  // extreme exponents: the exact evaluation is the filter
+            for (int k = 0; k < K1_CPT; ++k) {
+                bool ov = true;
+                if (CNT) {
+                    ov = r[k].ts <= Q.te && Q.ts <= r[k].te;  // invalid lanes: ts = +inf
+                    n_ov += ov ? 1u : 0u;
+                }
+                const Cand x = cand_exact(W.cs[k * 32 + lane]);
                 double cc, aa, dot, e;
-                cand[k] = pair_eval<TA, TB, true>(r[k], Q, qa, wmin_te, wmax_te, d2, cc, aa, dot, e) && ov;
-            } else {
-                cand[k] = pair_filter<TA, TB>(r[k], Q, qa, wmin_te, wmax_te, d2, C2) && ov;
+                cand[k] = pair_eval<TA, TB, true>(x, Q, qa, wmin_te, wmax_te, K.d2, cc, aa, dot, e) && ov;
+            }
+        } else {
+            const QF Q = load_qf(qa);
+#pragma unroll
+            for (int k = 0; k < K1_CPT; ++k) {
+                bool ov = true;
+                if (CNT) {
+                    // TA_C: the query started first, so it overlaps iff it ends
+                    // at or after r.ts; TA_R: iff it starts at or before r.te
+                    // (invalid lanes: ts = +inf, te = -inf)
+                    if (TA == TA_C) ov = r[k].ts <= Q.te;
+                    else if (TA == TA_R) ov = Q.ts <= r[k].te;
+                    else ov = r[k].ts <= Q.te && Q.ts <= r[k].te;
+                    n_ov += ov ? 1u : 0u;
+                }
+                cand[k] = pair_filter<TA, TB>(r[k], Q, wmin_te, wmax_te, K) && ov;
             }
         }
 #pragma unroll
@@ -574,10 +540,11 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
     constexpr int64_t STRIDE = (int64_t)K1_THREADS * K1_CPT;  // candidates per sub-tile
     const int64_t ct = STRIDE * sub;
     const int64_t nb = L.plan.nb;
-    // filter margin scale C2 = 16 C^2 + d^2 (see pair_filter)
+    // filter constants (filter.cuh); C = max |coordinate| of entries and queries
     const double cq = __longlong_as_double((long long)*L.q_cmax_bits);
     const double cmax = L.db_cmax > cq ? L.db_cmax : cq;
-    const double C2 = 16.0 * cmax * cmax + L.d2;
+    const FilterK K = filter_consts(cmax, L.d2);
+    const bool launch_exact = !filter_ok(cmax, L.d2);
 
     for (;;) {
         if (tid == 0) {
@@ -661,37 +628,39 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
             const int64_t base = it.first_c + (int64_t)s * STRIDE;
             if (base > it.c_hi) break;  // block-uniform
             const int64_t wbase = base + (int64_t)warp * 32 * K1_CPT;
-            Cand r[K1_CPT];
+            CandF r[K1_CPT];
             bool valid_any = false, unsafe_r = false;
             double wmin = INFINITY, wmax = -INFINITY, wmin_te = INFINITY, wmax_ts = -INFINITY;
 #pragma unroll
             for (int k = 0; k < K1_CPT; ++k) {
                 const int64_t e = wbase + (int64_t)k * 32 + lane;
                 const bool valid = e <= it.c_hi;
+                // stage the exact record for the rare path (queued pairs are
+                // evaluated from here); the filter view stays in registers
+                CandRec &cr = W.cs[k * 32 + lane];
                 if (valid) {
                     r[k].ts = L.e.ts[e]; r[k].te = L.e.te[e];
                     r[k].sx = L.e.sx[e]; r[k].sy = L.e.sy[e]; r[k].sz = L.e.sz[e];
-                    r[k].ex = L.e.ex[e]; r[k].ey = L.e.ey[e]; r[k].ez = L.e.ez[e];
-                    r[k].dx = L.e.dx[e]; r[k].dy = L.e.dy[e]; r[k].dz = L.e.dz[e];
-                    r[k].rcp = L.e.rcp[e];
+                    r[k].vx = L.e.vx[e]; r[k].vy = L.e.vy[e]; r[k].vz = L.e.vz[e];
                     r[k].ext = __dsub_rn(r[k].te, r[k].ts);
+                    cr.rcp = L.e.rcp[e];
+                    cr.dx = L.e.dx[e]; cr.dy = L.e.dy[e]; cr.dz = L.e.dz[e];
+                    cr.ex = L.e.ex[e]; cr.ey = L.e.ey[e]; cr.ez = L.e.ez[e];
                     unsafe_r |= L.e.unsafe[e] != 0;
                     wmin = fmin(wmin, r[k].ts);
                     wmax = fmax(wmax, r[k].te);
                     wmin_te = fmin(wmin_te, r[k].te);
                     wmax_ts = fmax(wmax_ts, r[k].ts);
                 } else {
-                    r[k].ts = INFINITY; r[k].te = -INFINITY; r[k].ext = 1.0; r[k].rcp = 1.0;
-                    r[k].sx = r[k].sy = r[k].sz = r[k].ex = r[k].ey = r[k].ez = 0.0;
-                    r[k].dx = r[k].dy = r[k].dz = 0.0;
+                    r[k].ts = INFINITY; r[k].te = -INFINITY; r[k].ext = 1.0;
+                    r[k].sx = r[k].sy = r[k].sz = 0.0;
+                    r[k].vx = r[k].vy = r[k].vz = 0.0;
+                    cr.rcp = 1.0;
+                    cr.dx = cr.dy = cr.dz = cr.ex = cr.ey = cr.ez = 0.0;
                 }
                 valid_any |= valid;
-                // stage for the rare path (queued pairs are evaluated from here)
-                CandRec &cr = W.cs[k * 32 + lane];
-                cr.ts = r[k].ts; cr.te = r[k].te; cr.rcp = r[k].rcp;
+                cr.ts = r[k].ts; cr.te = r[k].te;
                 cr.sx = r[k].sx; cr.sy = r[k].sy; cr.sz = r[k].sz;
-                cr.dx = r[k].dx; cr.dy = r[k].dy; cr.dz = r[k].dz;
-                cr.ex = r[k].ex; cr.ey = r[k].ey; cr.ez = r[k].ez;
             }
             // key of (b, e_off of the warp's candidate 0, q_off = it.q0) without the j term
             W.key_base0 = make_key(L, it.b, wbase - L.plan.first[it.b], it.q0);
@@ -714,16 +683,16 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
                 ja = jlo;
                 jb = jhi;  // everything in the generic (mixed) range
             }
-            const bool slow = unsafe_q || __any_sync(0xffffffffu, unsafe_r);
+            const bool slow = launch_exact || unsafe_q || __any_sync(0xffffffffu, unsafe_r);
             // tb case of a whole range: every query of the TA_C range ends
             // before all candidates (running max < min te), or every query of
             // the TA_R range ends after all of them (suffix min > max te)
             const bool c_tb_r = jlo < ja && pm[ja - 1] < wmin_te;
             const bool r_tb_c = jb < jhi && sm[jb] > wmax;
             if (slow) {
-                pair_run<TA_C, TB_DYN, true, true>(L, sq, jlo, ja, r, wmin_te, wmax, W, lane, n_ov, n_hit, C2);
-                pair_run<TA_BOTH, TB_DYN, true, true>(L, sq, ja, jb, r, wmin_te, wmax, W, lane, n_ov, n_hit, C2);
-                pair_run<TA_R, TB_DYN, true, true>(L, sq, jb, jhi, r, wmin_te, wmax, W, lane, n_ov, n_hit, C2);
+                pair_run<TA_C, TB_DYN, true, true>(L, sq, jlo, ja, r, wmin_te, wmax, W, lane, n_ov, n_hit, K);
+                pair_run<TA_BOTH, TB_DYN, true, true>(L, sq, ja, jb, r, wmin_te, wmax, W, lane, n_ov, n_hit, K);
+                pair_run<TA_R, TB_DYN, true, true>(L, sq, jb, jhi, r, wmin_te, wmax, W, lane, n_ov, n_hit, K);
                 continue;
             }
             if (c_tb_r && te_sorted) {
@@ -731,19 +700,19 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
 #pragma unroll
                 for (int k = 0; k < K1_CPT; ++k)
                     n_ov += (unsigned)(ja - clampi(lower_bound_te(sq, it.nt, r[k].ts), jlo, ja));
-                pair_run<TA_C, TB_R, false, false>(L, sq, jlo, ja, r, wmin_te, wmax, W, lane, n_ov, n_hit, C2);
+                pair_run<TA_C, TB_R, false, false>(L, sq, jlo, ja, r, wmin_te, wmax, W, lane, n_ov, n_hit, K);
             } else {
-                pair_run<TA_C, TB_DYN, false, true>(L, sq, jlo, ja, r, wmin_te, wmax, W, lane, n_ov, n_hit, C2);
+                pair_run<TA_C, TB_DYN, false, true>(L, sq, jlo, ja, r, wmin_te, wmax, W, lane, n_ov, n_hit, K);
             }
-            pair_run<TA_BOTH, TB_DYN, false, true>(L, sq, ja, jb, r, wmin_te, wmax, W, lane, n_ov, n_hit, C2);
+            pair_run<TA_BOTH, TB_DYN, false, true>(L, sq, ja, jb, r, wmin_te, wmax, W, lane, n_ov, n_hit, K);
             if (r_tb_c) {
                 // overlap <=> cts <= r.te; cts ascending over the tile
 #pragma unroll
                 for (int k = 0; k < K1_CPT; ++k)
                     n_ov += (unsigned)(clampi(upper_bound_ts(sq, it.nt, r[k].te), jb, jhi) - jb);
-                pair_run<TA_R, TB_C, false, false>(L, sq, jb, jhi, r, wmin_te, wmax, W, lane, n_ov, n_hit, C2);
+                pair_run<TA_R, TB_C, false, false>(L, sq, jb, jhi, r, wmin_te, wmax, W, lane, n_ov, n_hit, K);
             } else {
-                pair_run<TA_R, TB_DYN, false, true>(L, sq, jb, jhi, r, wmin_te, wmax, W, lane, n_ov, n_hit, C2);
+                pair_run<TA_R, TB_DYN, false, true>(L, sq, jb, jhi, r, wmin_te, wmax, W, lane, n_ov, n_hit, K);
             }
         }
         // per-batch counters (64-bit)

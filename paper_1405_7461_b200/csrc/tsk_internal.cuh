@@ -56,13 +56,16 @@ struct DBuf {
 // Entry (or query) segments in device SoA form.  Hoisted invariants:
 //   dx,dy,dz = xe-xs, ye-ys, ze-zs  (the (e - s) of core.py:512)
 //   rcp      = RN(1/(te-ts)) for te > ts, else 0 (waypoint)
-//   unsafe   = 1 when the Markstein quotient (qdiv below) is not proven
-//              exact for this segment (extreme exponents, see mark_unsafe)
+//   vx,vy,vz = RN(d * rcp)  (velocity, K1's filter; filter.cuh)
+//   unsafe   = 1 when the segment is outside the exponent window in which
+//              qdiv below is exact and the filter's error bound holds
+//              (seg_unsafe in db.cu); such tiles are evaluated exactly
 struct Soa {
     int64_t n = 0;
     double *ts = nullptr, *te = nullptr, *sx = nullptr, *sy = nullptr, *sz = nullptr;
     double *ex = nullptr, *ey = nullptr, *ez = nullptr;
     double *dx = nullptr, *dy = nullptr, *dz = nullptr, *rcp = nullptr;
+    double *vx = nullptr, *vy = nullptr, *vz = nullptr;
     int64_t *traj = nullptr, *seg = nullptr;
     uint8_t *unsafe = nullptr;
     int any_unsafe = 0;
@@ -70,17 +73,20 @@ struct Soa {
     DBuf storage;
 };
 
-// Query record staged in shared memory: 7 × 16 B, laid out for LDS.128 pairs.
+// Query record staged in shared memory: 8 × 16 B, laid out for 16-byte
+// shared loads.  The filter reads the first 96 B (ts..dy), the exact path
+// ts..ext, dx..dz and ex..ez; RN(1/ext) is recomputed there.
 struct __align__(16) QRec {
     double ts, te;
     double sx, sy;
     double sz, ext;
+    double vx, vy;
+    double vz, dz;
     double dx, dy;
-    double dz, rcp;
     double ex, ey;
-    double ez, flag;  // flag: 1.0 when the segment is Markstein-unsafe
+    double ez, flag;  // flag: 1.0 when the segment is unsafe (seg_unsafe)
 };
-static_assert(sizeof(QRec) == 112, "QRec layout");
+static_assert(sizeof(QRec) == 128, "QRec layout");
 
 struct Index {
     int64_t m = 0, n_ne = 0;

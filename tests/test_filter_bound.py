@@ -1,0 +1,59 @@
+"""CPU check of K1's conservative filter (paper_1405_7461_b200/csrc/filter.cuh).
+
+tools/filter_check.cpp evaluates the reference's discriminant with the
+vectorised pair arithmetic of core.py:490-537 on adversarial pairs (thresholds
+at each pair's own flip point, near-parallel and constant-offset motion,
+zero-length spans, waypoints, planar data, epoch-scale times) and asserts that
+every pair with a non-negative reference discriminant is flagged by the
+filter in every clip case K1 can route it through.  A mutated margin must
+produce misses, so the generator is known to reach the bound.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import re
+import shutil
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SRC = os.path.join(ROOT, "tools", "filter_check.cpp")
+HDR = os.path.join(ROOT, "paper_1405_7461_b200", "csrc", "filter.cuh")
+
+
+def _build(tmp_path, header=HDR):
+    if shutil.which("g++") is None:
+        pytest.skip("g++ not available")
+    src = open(SRC).read().replace('"../paper_1405_7461_b200/csrc/filter.cuh"', '"%s"' % header)
+    cpp = tmp_path / "fc.cpp"
+    cpp.write_text(src)
+    exe = tmp_path / "fc"
+    # -ffp-contract=off: the library is built with -fmad=false
+    subprocess.run(["g++", "-O2", "-ffp-contract=off", "-std=c++17", "-o", str(exe), str(cpp)], check=True)
+    return exe
+
+
+def _run(exe, iters):
+    p = subprocess.run([str(exe), str(iters)], capture_output=True, text=True)
+    return p.returncode, json.loads(p.stdout.strip().splitlines()[-1]), p.stderr
+
+
+def test_filter_flags_every_nonnegative_reference_discriminant(tmp_path):
+    rc, out, err = _run(_build(tmp_path), 150_000)
+    assert rc == 0, err
+    assert out["edge"]["misses"] == 0 and out["random"]["misses"] == 0
+    assert out["edge"]["disc_pos"] > 100_000 and out["edge"]["skipped"] == 0
+
+
+def test_filter_check_detects_a_too_small_margin(tmp_path):
+    src = open(HDR).read()
+    mutated = re.sub(r"0x1p-40 \* c2", "0.0 * c2", src)
+    mutated = mutated.replace("fma(0x1p-34, d2, ka)", "ka").replace("0x1p-35 - 1.0", "-1.0")
+    assert mutated != src
+    hdr = tmp_path / "filter_mut.cuh"
+    hdr.write_text(mutated)
+    rc, out, _ = _run(_build(tmp_path, str(hdr)), 150_000)
+    assert rc == 1 and out["edge"]["misses"] > 0

@@ -142,6 +142,49 @@ def test_extreme_exponents_take_the_exact_division_path():
     assert np.array_equal(h.t_begin, tb) and np.array_equal(h.t_end, te)
 
 
+def _scaled_mesh(seed, n_rows, n_cols, coord_scale, time_scale=1.0, disp_scale=None):
+    rng = np.random.default_rng(seed)
+    out = []
+    for n, first in ((n_rows, 0), (n_cols, 5000)):
+        a = random_store_arrays(rng, n, first_traj=first)
+        for k in ("ts", "te"):
+            a[k] = a[k] * time_scale
+        for k in ("xs", "ys", "zs"):
+            a[k] = a[k] * coord_scale
+        for k, s in (("xe", "xs"), ("ye", "ys"), ("ze", "zs")):
+            if disp_scale is None:
+                a[k] = a[k] * coord_scale
+            else:  # tiny displacement over the segment
+                a[k] = a[s] + rng.uniform(-1, 1, n) * disp_scale
+        out.append(_store(a))
+    return out
+
+
+@pytest.mark.parametrize("case", ["tiny_velocity", "huge_coords", "tiny_coords", "huge_d"])
+def test_filter_exponent_window_and_launch_exact_mode(case):
+    """Inputs outside the filter's proven window (filter.cuh: subnormal
+    velocities per segment; C > 2^250, 0 < C < 2^-200 or d > 2^250 per launch)
+    are evaluated exactly and still match the oracle bit for bit."""
+    if case == "tiny_velocity":
+        rows, cols = _scaled_mesh(21, 300, 200, 1.0, time_scale=1e10, disp_scale=1e-300)
+        ds = (0.5, 1.5)
+    elif case == "huge_coords":
+        rows, cols = _scaled_mesh(22, 300, 200, 1e80)
+        ds = (1e79, 5e80)
+    elif case == "tiny_coords":
+        rows, cols = _scaled_mesh(23, 300, 200, 1e-70)
+        ds = (1e-71, 5e-70)
+    else:
+        rows, cols = _scaled_mesh(24, 300, 200, 1e77)
+        ds = (3e76, 1e78)
+    for d in ds:
+        h = tsk.pair_intervals(rows, cols, d)
+        ri, ci, tb, te, tm, sm = orc.pair_mesh(_cols(rows), _cols(cols), d)
+        assert np.array_equal(h.row_idx, ri) and np.array_equal(h.col_idx, ci), (case, d)
+        assert np.array_equal(h.t_begin, tb) and np.array_equal(h.t_end, te), (case, d)
+        assert (h.temporal_misses, h.spatial_misses) == (tm, sm)
+
+
 # ── K2 / K3 (index.py:85-173) ───────────────────────────────────────────────
 
 

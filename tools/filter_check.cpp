@@ -1,0 +1,251 @@
+// filter_check.cpp — CPU check of K1's conservative filter (csrc/filter.cuh).
+//
+// TEST INFRASTRUCTURE (run by tests/test_filter_bound.py).  For adversarial
+// (candidate, query) pairs it evaluates the reference's discriminant with the
+// vectorised pair arithmetic of core.py:490-537 (one IEEE op per numpy op,
+// built with -ffp-contract=off) and checks that every pair whose reference
+// discriminant is >= 0 is flagged by pair_filter<TA, TB> in every clip case
+// K1 could route it through.  Prints one JSON line of counts; exit 1 on a
+// miss.
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "../paper_1405_7461_b200/csrc/filter.cuh"
+
+using namespace tsk;
+
+struct Seg {
+    double ts, te, s[3], e[3];
+};
+
+static uint64_t rng_state = 0x9E3779B97F4A7C15ull;
+static uint64_t next_u64() {
+    uint64_t z = (rng_state += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+static double unif() { return (double)(next_u64() >> 11) * 0x1p-53; }
+static double unif(double a, double b) { return a + (b - a) * unif(); }
+
+// clipped() of core.py:503-514 for one segment at time t
+static void clipped(const Seg &g, double t, double p[3]) {
+    const double ext = g.te - g.ts;
+    const double denom = ext == 0.0 ? 1.0 : ext;
+    const double f = (t - g.ts) / denom;
+    for (int i = 0; i < 3; ++i) {
+        double v = g.s[i] + f * (g.e[i] - g.s[i]);
+        if (ext == 0.0 || t == g.ts) v = g.s[i];
+        else if (t == g.te) v = g.e[i];
+        p[i] = v;
+    }
+}
+
+// reference discriminant (core.py:523-537); returns false when no overlap
+static bool ref_disc(const Seg &r, const Seg &c, double d, double &disc, double &cc_out) {
+    const double ta = r.ts > c.ts ? r.ts : c.ts;
+    const double tb = r.te < c.te ? r.te : c.te;
+    if (!(ta <= tb)) return false;
+    double ra[3], rb[3], ca[3], cb[3];
+    clipped(r, ta, ra);
+    clipped(r, tb, rb);
+    clipped(c, ta, ca);
+    clipped(c, tb, cb);
+    const double ux = ra[0] - ca[0], uy = ra[1] - ca[1], uz = ra[2] - ca[2];
+    const double cc = ux * ux + uy * uy + uz * uz;
+    const double d2 = d * d;
+    const double wx = (rb[0] - ra[0]) - (cb[0] - ca[0]);
+    const double wy = (rb[1] - ra[1]) - (cb[1] - ca[1]);
+    const double wz = (rb[2] - ra[2]) - (cb[2] - ca[2]);
+    const double aa = wx * wx + wy * wy + wz * wz;
+    const double bb = 2.0 * (ux * wx + uy * wy + uz * wz);
+    disc = bb * bb - 4.0 * aa * (cc - d2);
+    cc_out = cc;
+    return true;
+}
+
+// hoisting of db.cu (k_hoist / k_qprep) and its exponent window
+static bool mag_ok(double v) {
+    const double a = std::fabs(v);
+    return a == 0.0 || (a >= 0x1p-900 && a <= 0x1p1000);
+}
+static bool vel_ok(double v) {
+    const double a = std::fabs(v);
+    return a == 0.0 || (a >= 0x1p-1000 && a <= 0x1p1000);
+}
+static bool hoist(const Seg &g, double &ext, double v[3], double dd[3]) {
+    ext = g.te - g.ts;
+    const double rcp = ext > 0.0 ? 1.0 / ext : 0.0;
+    bool ok = mag_ok(g.ts) && mag_ok(g.te) && mag_ok(ext);
+    for (int i = 0; i < 3; ++i) {
+        dd[i] = g.e[i] - g.s[i];
+        v[i] = seg_velocity(dd[i], rcp);
+        ok = ok && std::fabs(g.s[i]) <= 0x1p1000 && std::fabs(g.e[i]) <= 0x1p1000 && vel_ok(v[i]);
+    }
+    return ok;
+}
+
+struct Counts {
+    long pairs = 0, overlapping = 0, disc_pos = 0, checks = 0, flagged = 0, misses = 0, skipped = 0;
+};
+
+template <int TA, int TB>
+static void check_case(const CandF &cf, const QF &qf, double wmin, double wmax, const FilterK &K,
+                       bool need, Counts &n, const Seg &r, const Seg &c, double d, const char *tag) {
+    const bool f = pair_filter<TA, TB>(cf, qf, wmin, wmax, K);
+    ++n.checks;
+    n.flagged += f;
+    if (need && !f) {
+        ++n.misses;
+        if (n.misses <= 5)
+            std::fprintf(stderr,
+                         "MISS %s TA=%d TB=%d d=%.17g r=[%.17g %.17g (%.17g %.17g %.17g)->(%.17g %.17g %.17g)] "
+                         "c=[%.17g %.17g (%.17g %.17g %.17g)->(%.17g %.17g %.17g)]\n",
+                         tag, TA, TB, d, r.ts, r.te, r.s[0], r.s[1], r.s[2], r.e[0], r.e[1], r.e[2], c.ts, c.te,
+                         c.s[0], c.s[1], c.s[2], c.e[0], c.e[1], c.e[2]);
+    }
+}
+
+static void check_pair(const Seg &r, const Seg &c, double d, Counts &n, const char *tag) {
+    ++n.pairs;
+    double disc, cc;
+    if (!ref_disc(r, c, d, disc, cc)) return;
+    ++n.overlapping;
+    CandF cf;
+    QF qf;
+    double rv[3], rd[3], qv[3], qd[3];
+    const bool ok = hoist(r, cf.ext, rv, rd) & hoist(c, qf.ext, qv, qd);
+    double cmax = 0.0;
+    for (int i = 0; i < 3; ++i)
+        cmax = std::fmax(cmax, std::fmax(std::fmax(std::fabs(r.s[i]), std::fabs(r.e[i])),
+                                         std::fmax(std::fabs(c.s[i]), std::fabs(c.e[i]))));
+    if (!ok || !filter_ok(cmax, d * d)) {
+        ++n.skipped;  // K1 evaluates these exactly (unsafe tile / launch)
+        return;
+    }
+    const bool need = disc >= 0.0;
+    n.disc_pos += need;
+    cf.ts = r.ts; cf.te = r.te;
+    cf.sx = r.s[0]; cf.sy = r.s[1]; cf.sz = r.s[2];
+    cf.vx = rv[0]; cf.vy = rv[1]; cf.vz = rv[2];
+    qf.ts = c.ts; qf.te = c.te;
+    qf.sx = c.s[0]; qf.sy = c.s[1]; qf.sz = c.s[2];
+    qf.vx = qv[0]; qf.vy = qv[1]; qf.vz = qv[2];
+    qf.dx = qd[0]; qf.dy = qd[1]; qf.dz = qd[2];
+    const FilterK K = filter_consts(cmax, d * d);
+    const double inf = INFINITY;
+    // every route K1 can take for this pair
+    const bool ta_r = c.ts > r.ts, ta_c = c.ts < r.ts;
+    const bool tb_r = c.te < r.te, tb_c = c.te > r.te;
+    // generic per-pair tb, and the dynamic split around this candidate's te
+    check_case<TA_BOTH, TB_DYN>(cf, qf, -inf, inf, K, need, n, r, c, d, tag);
+    check_case<TA_BOTH, TB_DYN>(cf, qf, r.te, r.te, K, need, n, r, c, d, tag);
+    if (ta_r) {
+        check_case<TA_R, TB_DYN>(cf, qf, -inf, inf, K, need, n, r, c, d, tag);
+        check_case<TA_R, TB_DYN>(cf, qf, r.te, r.te, K, need, n, r, c, d, tag);
+        if (tb_c) check_case<TA_R, TB_C>(cf, qf, r.te, r.te, K, need, n, r, c, d, tag);
+    }
+    if (ta_c) {
+        check_case<TA_C, TB_DYN>(cf, qf, -inf, inf, K, need, n, r, c, d, tag);
+        check_case<TA_C, TB_DYN>(cf, qf, r.te, r.te, K, need, n, r, c, d, tag);
+        if (tb_r) check_case<TA_C, TB_R>(cf, qf, r.te, r.te, K, need, n, r, c, d, tag);
+    }
+    (void)tb_r;
+}
+
+// closest approach of the two (linear) motions over the shared span, in
+// long double: the threshold at which the pair flips between hit and miss
+static double min_dist(const Seg &r, const Seg &c) {
+    const long double ta = r.ts > c.ts ? r.ts : c.ts, tb = r.te < c.te ? r.te : c.te;
+    auto pos = [](const Seg &g, long double t, long double p[3]) {
+        const long double ext = (long double)g.te - g.ts;
+        const long double f = ext == 0 ? 0 : (t - g.ts) / ext;
+        for (int i = 0; i < 3; ++i) p[i] = g.s[i] + f * ((long double)g.e[i] - g.s[i]);
+    };
+    long double ra[3], rb[3], ca[3], cb[3];
+    pos(r, ta, ra); pos(r, tb, rb); pos(c, ta, ca); pos(c, tb, cb);
+    long double u[3], w[3], uu = 0, ww = 0, uw = 0;
+    for (int i = 0; i < 3; ++i) {
+        u[i] = ra[i] - ca[i];
+        w[i] = (rb[i] - ra[i]) - (cb[i] - ca[i]);
+        uu += u[i] * u[i]; ww += w[i] * w[i]; uw += u[i] * w[i];
+    }
+    long double lam = ww > 0 ? -uw / ww : 0;
+    // the line distance (the discriminant's root), not clamped to [0, 1]
+    long double m2 = uu + 2 * lam * uw + lam * lam * ww;
+    (void)lam;
+    return (double)std::sqrt(m2 > 0 ? m2 : 0);
+}
+
+static Seg rand_seg(double L, double t0, double t1, double speed) {
+    Seg g;
+    g.ts = t0; g.te = t1;
+    for (int i = 0; i < 3; ++i) {
+        g.s[i] = unif(-L, L);
+        g.e[i] = g.s[i] + speed * unif(-1, 1);
+    }
+    return g;
+}
+
+int main(int argc, char **argv) {
+    long iters = argc > 1 ? std::atol(argv[1]) : 200000;
+    Counts n, nrand;
+    const double scales[] = {1e-3, 1.0, 100.0, 1e4, 1e6};
+    const double tbase[] = {0.0, 1e3, 1.7e9};
+    for (long it = 0; it < iters; ++it) {
+        const double L = scales[next_u64() % 5];
+        const double T = tbase[next_u64() % 3];
+        const double sp = L * (next_u64() % 2 ? 1.0 : 1e-3);
+        // overlapping spans with random alignment
+        const double a0 = T + unif(0, 10), a1 = a0 + unif(0.01, 10);
+        double b0 = T + unif(0, 10), b1 = b0 + unif(0.01, 10);
+        const int mode = (int)(next_u64() % 8);
+        if (mode == 1) b0 = a0;                         // equal starts (TA_BOTH)
+        if (mode == 2) b1 = a1;                         // equal ends
+        if (mode == 3) { b0 = a1; b1 = a1 + 1.0; }      // touching: zero-length span
+        if (mode == 4) b1 = b0;                         // zero-ext query (waypoint)
+        Seg r = rand_seg(L, a0, a1, sp), c = rand_seg(L, b0, b1, sp);
+        if (mode == 5) {  // near-parallel motion
+            const double eps = std::ldexp(1.0, -(int)(next_u64() % 50));
+            for (int i = 0; i < 3; ++i) {
+                c.s[i] = r.s[i] + unif(-1, 1) * L * 1e-3;
+                c.e[i] = c.s[i] + (r.e[i] - r.s[i]) * (1 + eps * unif(-1, 1));
+            }
+            c.ts = r.ts; c.te = r.te;
+        }
+        if (mode == 6) {  // identical motion offset by a constant
+            for (int i = 0; i < 3; ++i) {
+                const double off = unif(-1, 1) * L;
+                c.s[i] = r.s[i] + off;
+                c.e[i] = r.e[i] + off;
+            }
+            c.ts = r.ts; c.te = r.te;
+        }
+        if (next_u64() % 3 == 0) { r.s[2] = r.e[2] = 0.0; c.s[2] = c.e[2] = 0.0; }  // planar data
+        nrand.pairs++;
+        check_pair(r, c, L * 0.01, nrand, "rand");
+        // thresholds straddling the pair's own flip point
+        const double md = min_dist(r, c);
+        if (md > 0 && std::isfinite(md)) {
+            for (int k = 0; k < 6; ++k) {
+                const double rel = std::ldexp(1.0, -(int)(next_u64() % 52)) * (next_u64() % 2 ? 1 : -1);
+                check_pair(r, c, md * (1 + rel), n, "edge");
+            }
+            check_pair(r, c, md, n, "edge0");
+            check_pair(r, c, std::nextafter(md, 0.0), n, "edge-");
+            check_pair(r, c, std::nextafter(md, INFINITY), n, "edge+");
+        } else {
+            check_pair(r, c, 0.0, n, "zero");
+        }
+    }
+    std::printf("{\"edge\": {\"pairs\": %ld, \"overlapping\": %ld, \"disc_pos\": %ld, \"checks\": %ld, "
+                "\"flagged\": %ld, \"skipped\": %ld, \"misses\": %ld}, "
+                "\"random\": {\"pairs\": %ld, \"overlapping\": %ld, \"disc_pos\": %ld, \"checks\": %ld, "
+                "\"flagged\": %ld, \"misses\": %ld}}\n",
+                n.pairs, n.overlapping, n.disc_pos, n.checks, n.flagged, n.skipped, n.misses, nrand.pairs,
+                nrand.overlapping, nrand.disc_pos, nrand.checks, nrand.flagged, nrand.misses);
+    return (n.misses || nrand.misses) ? 1 : 0;
+}
