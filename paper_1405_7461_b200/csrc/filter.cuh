@@ -72,7 +72,7 @@ struct QF {
 };
 
 struct FilterK {
-    double d2, k5, kc, t0;
+    double d2, k5, kc, t0, km;  // km = 2^-35 - 1
 };
 
 TSK_HD FilterK filter_consts(double cmax, double d2) {
@@ -83,10 +83,23 @@ TSK_HD FilterK filter_consts(double cmax, double d2) {
     k.kc = 0x1p-54 * c2;
     k.k5 = fma(0x1p-34, d2, ka);
     k.t0 = -2.0 * k.kc * d2;
+    k.km = 0x1p-35 - 1.0;
     return k;
 }
 
 // Launch-level validity of the filter's error bound (else: exact path only).
+// a >= b as its own compare: keeps the per-candidate tests separate (the
+// compiler otherwise merges `x >= t || y >= t` into a max + compare)
+TSK_HD bool ge_sep(double a, double b) {
+#ifdef __CUDA_ARCH__
+    unsigned r;
+    asm("{.reg .pred p; setp.ge.f64 p, %1, %2; selp.u32 %0, 1, 0, p;}" : "=r"(r) : "d"(a), "d"(b));
+    return r != 0;
+#else
+    return a >= b;
+#endif
+}
+
 TSK_HD bool filter_ok(double cmax, double d2) {
     return cmax <= 0x1p250 && d2 <= 0x1p500 && (cmax == 0.0 || cmax >= 0x1p-200);
 }
@@ -129,10 +142,10 @@ TSK_HD bool pair_filter(const CandF &r, const QF &Q, double wmin_te, double wmax
     const double e = fma(u[0], u[0], fma(u[1], u[1], fma(u[2], u[2], -K.d2)));
     const double aa = fma(w[0], w[0], fma(w[1], w[1], w[2] * w[2]));
     const double dot = fma(u[0], w[0], fma(u[1], w[1], u[2] * w[2]));
-    const double x = fma(e, 0x1p-35 - 1.0, K.k5);
+    const double x = fma(e, K.km, K.k5);
     const double t = fma(aa, x, dot * dot);
     const double t2 = fma(K.kc, e, t);
-    return flat || t2 >= K.t0;
+    return flat || ge_sep(t2, K.t0);
 }
 
 }  // namespace tsk

@@ -389,8 +389,12 @@ __device__ __forceinline__ void pair_run(const K1Launch &L, const QRec *__restri
                                          const WarpRare &W, int lane, unsigned &n_ov, unsigned &n_hit,
                                          const FilterK &K) {
     int qn = 0;  // queued entries (warp-uniform)
-    uint32_t qa = (uint32_t)__cvta_generic_to_shared(sq) + (uint32_t)j0 * (uint32_t)sizeof(QRec);
-    for (int j = j0; j < j1; ++j, qa += (uint32_t)sizeof(QRec)) {
+    const uint32_t qa0 = (uint32_t)__cvta_generic_to_shared(sq) + (uint32_t)j0 * (uint32_t)sizeof(QRec);
+    const uint32_t qa_end = qa0 + (uint32_t)(j1 - j0) * (uint32_t)sizeof(QRec);
+    // The loop is driven by the record address alone; everything the rare
+    // path needs (query index, lane masks) is derived inside its branch, so
+    // the common iteration is loads, FP64 math, one vote and one branch.
+    for (uint32_t qa = qa0; qa < qa_end; qa += (uint32_t)sizeof(QRec)) {
         bool cand[K1_CPT];
         if (SLOW) {  // unsafe tile or launch: the exact evaluation is the filter
             const QVals Q = load_q(qa);
@@ -422,6 +426,14 @@ __device__ __forceinline__ void pair_run(const K1Launch &L, const QRec *__restri
                 cand[k] = pair_filter<TA, TB>(r[k], Q, wmin_te, wmax_te, K) && ov;
             }
         }
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < K1_CPT; ++k) any |= cand[k];
+        if (!__any_sync(0xffffffffu, any)) continue;
+        // rare: queue the flagged pairs of this query, flushing 32 at a time
+        const uint32_t j = (qa - (uint32_t)__cvta_generic_to_shared(sq)) / (uint32_t)sizeof(QRec);
+        unsigned lt;
+        asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
 #pragma unroll
         for (int k = 0; k < K1_CPT; ++k) {
             const unsigned m = __ballot_sync(0xffffffffu, cand[k]);
@@ -436,7 +448,7 @@ __device__ __forceinline__ void pair_run(const K1Launch &L, const QRec *__restri
                 if (lane + 32 < qn) W.q[lane] = moved;
                 qn = qn > 32 ? qn - 32 : 0;
             }
-            if (cand[k]) W.q[qn + __popc(m & ((1u << lane) - 1u))] = ((uint32_t)(k * 32 + lane) << 16) | (uint32_t)j;
+            if (cand[k]) W.q[qn + __popc(m & lt)] = ((uint32_t)(k * 32 + lane) << 16) | j;
             qn += c;
         }
         if (qn >= 32) {
@@ -543,7 +555,8 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
     // filter constants (filter.cuh); C = max |coordinate| of entries and queries
     const double cq = __longlong_as_double((long long)*L.q_cmax_bits);
     const double cmax = L.db_cmax > cq ? L.db_cmax : cq;
-    const FilterK K = filter_consts(cmax, L.d2);
+    FilterK K = filter_consts(cmax, L.d2);
+    K.km = L.filter_km;
     const bool launch_exact = !filter_ok(cmax, L.d2);
 
     for (;;) {

@@ -298,6 +298,7 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     // filter margin scale: entry max |coordinate| here, the query one is
     // reduced on the device by qprep and folded in by K1
     L.db_cmax = db->cmax;
+    L.filter_km = 0x1p-35 - 1.0;
     L.q_cmax_bits = db->counters.as<unsigned long long>() + 5;
     L.major_bits = major_bits;
     L.minor_bits = minor_bits;

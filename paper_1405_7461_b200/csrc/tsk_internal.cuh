@@ -192,6 +192,7 @@ struct K1Launch {
     uint64_t cap;
     double d2;
     double db_cmax;                          // max |coordinate| of the entries
+    double filter_km;                        // 2^-35 - 1 (filter.cuh), a launch value so it stays in a uniform register
     const unsigned long long *q_cmax_bits;   // max |coordinate| of the queries (device, as bits)
     int major_bits, minor_bits;  // key = b << (major+minor) | major << minor | minor
     int query_major;             // 0: (b, entry, query); 1: (b, query, entry)
