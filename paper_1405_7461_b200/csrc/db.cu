@@ -36,7 +36,8 @@ void DBuf::release(cudaStream_t) {
 void soa_alloc(Soa &s, int64_t n, bool with_ids, cudaStream_t st) {
     size_t nn = (size_t)(n > 0 ? n : 1);
     size_t per = 15 * sizeof(double) + (with_ids ? 2 * sizeof(int64_t) : 0) + 1;
-    s.storage.reserve(nn * per + 64, st);
+    const size_t ngb = (nn + GB_SIZE - 1) / GB_SIZE;
+    s.storage.reserve(nn * per + ngb * sizeof(GBound) + 64, st);
     char *base = s.storage.as<char>();
     double **cols[15] = {&s.ts, &s.te, &s.sx, &s.sy, &s.sz, &s.ex, &s.ey, &s.ez,
                          &s.dx, &s.dy, &s.dz, &s.rcp, &s.vx, &s.vy, &s.vz};
@@ -53,6 +54,10 @@ void soa_alloc(Soa &s, int64_t n, bool with_ids, cudaStream_t st) {
         s.traj = s.seg = nullptr;
     }
     s.unsafe = reinterpret_cast<uint8_t *>(base);
+    base += nn;
+    // group bounds after the byte column, 16-byte aligned
+    base = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(base) + 15) & ~uintptr_t(15));
+    s.gb = reinterpret_cast<GBound *>(base);
     s.n = n;
 }
 
@@ -142,6 +147,61 @@ void soa_hoist(Soa &s, cudaStream_t st) {
     TSK_CUDA(cudaStreamSynchronize(st));
     s.any_unsafe = h[0];
     s.sorted = h[1] ? 0 : 1;
+}
+
+// Group bounds (GBound): one warp per group of GB_SIZE segments.
+__global__ void k_group_bounds(int64_t n, const double *__restrict__ ts, const double *__restrict__ sx,
+                               const double *__restrict__ sy, const double *__restrict__ sz,
+                               const double *__restrict__ vx, const double *__restrict__ vy,
+                               const double *__restrict__ vz, GBound *__restrict__ gb) {
+    const int lane = threadIdx.x & 31;
+    const int64_t ngb = (n + GB_SIZE - 1) / GB_SIZE;
+    for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; g < ngb;
+         g += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        double tlo = INFINITY, thi = -INFINITY, vm = 0.0;
+        for (int k = lane; k < GB_SIZE; k += 32) {
+            const int64_t i = g * GB_SIZE + k;
+            if (i >= n) break;
+            const double s3[3] = {sx[i], sy[i], sz[i]};
+            for (int c = 0; c < 3; ++c) {
+                lo[c] = fmin(lo[c], s3[c]);
+                hi[c] = fmax(hi[c], s3[c]);
+            }
+            tlo = fmin(tlo, ts[i]);
+            thi = fmax(thi, ts[i]);
+            vm = fmax(vm, fmax(fabs(vx[i]), fmax(fabs(vy[i]), fabs(vz[i]))));
+        }
+        for (int o = 16; o; o >>= 1) {
+            for (int c = 0; c < 3; ++c) {
+                lo[c] = fmin(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+                hi[c] = fmax(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
+            }
+            tlo = fmin(tlo, __shfl_xor_sync(0xffffffffu, tlo, o));
+            thi = fmax(thi, __shfl_xor_sync(0xffffffffu, thi, o));
+            vm = fmax(vm, __shfl_xor_sync(0xffffffffu, vm, o));
+        }
+        if (lane == 0) {
+            GBound b;
+            for (int c = 0; c < 3; ++c) {
+                b.lo[c] = lo[c];
+                b.hi[c] = hi[c];
+            }
+            b.ts_lo = tlo;
+            b.ts_hi = thi;
+            b.vmax = vm;
+            b.pad = 0.0;
+            gb[g] = b;
+        }
+    }
+}
+
+void soa_group_bounds(Soa &s, cudaStream_t st) {
+    if (s.n == 0) return;
+    const int64_t ngb = (s.n + GB_SIZE - 1) / GB_SIZE;
+    int grid = (int)std::min<int64_t>((ngb + 7) / 8, 148 * 16);
+    k_group_bounds<<<grid, 256, 0, st>>>(s.n, s.ts, s.sx, s.sy, s.sz, s.vx, s.vy, s.vz, s.gb);
+    TSK_CUDA(cudaGetLastError());
 }
 
 // max |coordinate| over the six position columns (filter margin of K1)
@@ -486,6 +546,7 @@ extern "C" int tsk_db_create(int device, const tsk_columns *cols, tsk_db **out) 
         soa_alloc(db->s, cols->n, true, db->stream);
         soa_upload(db->s, cols, db->stream);
         soa_hoist(db->s, db->stream);
+        soa_group_bounds(db->s, db->stream);
         db->cmax = soa_cmax(db->s, db->stream);
         *out = db;
         return TSK_OK;

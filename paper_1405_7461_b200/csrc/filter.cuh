@@ -41,6 +41,7 @@
 #pragma once
 
 #include <math.h>
+#include <cfenv>
 
 #ifdef __CUDACC__
 #define TSK_HD __host__ __device__ __forceinline__
@@ -146,6 +147,137 @@ TSK_HD bool pair_filter(const CandF &r, const QF &Q, double wmin_te, double wmax
     const double t = fma(aa, x, dot * dot);
     const double t2 = fma(K.kc, e, t);
     return flat || ge_sep(t2, K.t0);
+}
+
+
+// ── FP32 pre-filter (K1's common path) ─────────────────────────────────────
+//
+// Per work item, positions and times are taken relative to an origin
+// (O, T0) = the first staged query's start.  A candidate holds
+//   p  = RN32((r.s - O) - (r.ts - T0) v_r)   (its line at time T0)
+//   v  = RN32(v_r),  sr >= |v_r| (rounded up)
+// and a query
+//   ts = RN32(q.ts - T0), s = RN32(q.s - O),
+//   a >= (1 + 2^-8) ext_q,  b >= (1 + 2^-8)(d + |q.e - q.s|) + delta.
+// Then u = (p + ts v) - s approximates u* = r.s + (q.ts - r.ts) V_r - q.s,
+// the separation of the candidate's line from the query's start at q.ts.
+//
+// Why |u| > a sr + b implies a reference miss.  On the shared span
+// [ta, tb] (inside [q.ts, q.te]) both segments are linear, so the true
+// separation s(t) = u* + (t - q.ts)(V_r - V_q) and
+//   |s(t)| >= |u*| - ext_q |V_r| - |q.e - q.s|.
+// A reference hit needs some lambda in [0, 1] with its computed quadratic
+// q(lambda) = |U + lambda W|^2 - d^2 <= mu (d^2 + (|U| + |W|)^2), mu = 2^-20
+// far above the roundings of its coefficients, discriminant and roots (the
+// rare path's second filter rests on the same fact with mu = 2^-30), with
+// U, W the reference's separation at ta and change over the span, within
+// 2^-48 C of the true ones.  That gives
+//   (1 - 2^-10)|U| <= (1 + 2^-20) d + (1 + 2^-10)|W|,
+// so a hit is impossible once |u*| > (1 + 2^-8)(d + ext_q|V_r| + |q.e - q.s|)
+// + 2^-38 C.  FP32 error: every magnitude the FP32 path forms is, per
+// component, at most M = A_r + TV_r + T_q V_r + A_q (A: max |s - O| of the
+// item's candidates / queries, TV_r: max |r.ts - T0| |v_r|, T_q: max
+// |q.ts - T0|, V_r: max |v_r| component) and each of p, ts*v, t, s, u is
+// rounded once, so |u - u*| <= 7 * 2^-24 M < 2^-18 M.  delta adds 2^-18 M
+// + 2^-38 C + 2^-100 (underflow).  The test itself uses |u|^2 rounded down
+// and (a sr + b)^2 rounded up.  Items with M, V_r or ext_q above 2^60 (or
+// d above 2^60) are evaluated exactly instead.
+struct CandF32 {
+    float px, py, pz, vx, vy, vz, sr;
+};
+
+struct F32Item {
+    double ox, oy, oz, t0, delta;
+    bool ok;
+};
+
+#ifndef __CUDA_ARCH__
+inline float tsk_f2f_ru(double x) {
+    float f = (float)x;
+    if ((double)f < x) f = nextafterf(f, INFINITY);
+    return f;
+}
+#endif
+#ifdef __CUDA_ARCH__
+#define TSK_F2F_RN(x) __double2float_rn(x)
+#define TSK_F2F_RU(x) __double2float_ru(x)
+#else
+#define TSK_F2F_RN(x) ((float)(x))
+#define TSK_F2F_RU(x) tsk_f2f_ru(x)
+#endif
+
+// Item bounds (see above): ar = A_r, tvr = TV_r, vr = V_r, aq = A_q,
+// tq = T_q, eq = max ext_q, cmax = max |coordinate| of the launch.
+TSK_HD F32Item f32_item(double ox, double oy, double oz, double t0, double ar, double tvr, double vr,
+                        double aq, double tq, double eq, double cmax) {
+    F32Item it;
+    it.ox = ox; it.oy = oy; it.oz = oz; it.t0 = t0;
+    const double M = ar + tvr + tq * vr + aq;
+    it.ok = M <= 0x1p60 && vr <= 0x1p60 && eq <= 0x1p60;  // false for NaN
+    it.delta = 0x1p-18 * M + 0x1p-38 * cmax + 0x1p-100;
+    return it;
+}
+
+// FP32 view of a query (sx.. its start, ext = RN(te - ts), dx.. = RN(e - s));
+// dthr = d.
+TSK_HD void f32_query(double ts, double sx, double sy, double sz, double ext, double dx, double dy,
+                      double dz, const F32Item &it, double dthr, float out[6]) {
+    const double lq = sqrt(dx * dx + dy * dy + dz * dz) * (1.0 + 0x1p-40);
+    out[0] = TSK_F2F_RN(ts - it.t0);
+    out[1] = TSK_F2F_RN(sx - it.ox);
+    out[2] = TSK_F2F_RN(sy - it.oy);
+    out[3] = TSK_F2F_RN(sz - it.oz);
+    out[4] = TSK_F2F_RU(ext * (1.0 + 0x1p-8));
+    out[5] = TSK_F2F_RU((1.0 + 0x1p-8) * (dthr + lq) + it.delta);
+}
+
+// FP32 view of a candidate (its start, start time and hoisted velocity).
+TSK_HD CandF32 f32_cand(double ts, double sx, double sy, double sz, double vx, double vy, double vz,
+                        const F32Item &it) {
+    CandF32 c;
+    const double dt = ts - it.t0;
+    c.px = TSK_F2F_RN(fma(-dt, vx, sx - it.ox));
+    c.py = TSK_F2F_RN(fma(-dt, vy, sy - it.oy));
+    c.pz = TSK_F2F_RN(fma(-dt, vz, sz - it.oz));
+    c.vx = TSK_F2F_RN(vx);
+    c.vy = TSK_F2F_RN(vy);
+    c.vz = TSK_F2F_RN(vz);
+    c.sr = TSK_F2F_RU(sqrt(vx * vx + vy * vy + vz * vz) * (1.0 + 0x1p-40));
+    return c;
+}
+
+#ifndef __CUDA_ARCH__
+inline float tsk_fma_dir(float a, float b, float c, int mode) {
+    const int m = fegetround();
+    fesetround(mode);
+    volatile float r = fmaf(a, b, c);
+    fesetround(m);
+    return r;
+}
+#endif
+
+// The pre-filter test: true = the pair may hit (NaN flags).
+TSK_HD bool f32_flag(const CandF32 &c, float qts, float qx, float qy, float qz, float qa, float qb) {
+#ifdef __CUDA_ARCH__
+    const float ux = __fsub_rn(__fmaf_rn(qts, c.vx, c.px), qx);
+    const float uy = __fsub_rn(__fmaf_rn(qts, c.vy, c.py), qy);
+    const float uz = __fsub_rn(__fmaf_rn(qts, c.vz, c.pz), qz);
+    const float n = __fmaf_rd(uz, uz, __fmaf_rd(uy, uy, __fmul_rd(ux, ux)));
+    const float R = __fmaf_ru(qa, c.sr, qb);
+    const float R2 = __fmul_ru(R, R);
+    unsigned far;
+    asm("{.reg .pred p; setp.gt.f32 p, %1, %2; selp.u32 %0, 1, 0, p;}" : "=r"(far) : "f"(n), "f"(R2));
+    return far == 0u;
+#else
+    const float ux = fmaf(qts, c.vx, c.px) - qx;
+    const float uy = fmaf(qts, c.vy, c.py) - qy;
+    const float uz = fmaf(qts, c.vz, c.pz) - qz;
+    const float n = tsk_fma_dir(uz, uz, tsk_fma_dir(uy, uy, tsk_fma_dir(ux, ux, 0.f, FE_DOWNWARD), FE_DOWNWARD),
+                                FE_DOWNWARD);
+    const float R = tsk_fma_dir(qa, c.sr, qb, FE_UPWARD);
+    const float R2 = tsk_fma_dir(R, R, 0.f, FE_UPWARD);
+    return !(n > R2);
+#endif
 }
 
 }  // namespace tsk

@@ -40,6 +40,9 @@
 #ifndef K1_MIN_BLOCKS
 #define K1_MIN_BLOCKS (K1_CPT == 1 ? 3 : 2)
 #endif
+#ifndef K1_MIN_BLOCKS_F32
+#define K1_MIN_BLOCKS_F32 2
+#endif
 
 namespace tsk {
 
@@ -284,10 +287,9 @@ struct CandRec {
     double ts, te, rcp, sx, sy, sz, dx, dy, dz, ex, ey, ez;
 };
 constexpr int K1_WARPS = K1_THREADS / 32;
-// Queue entries per warp.  Before each append of up to 32 flags the queue is
-// flushed down to < 32 entries if it would overflow, and a flush moves at
-// most 32 remaining entries, so 64 suffices for any K1_CPT.
-constexpr int K1_QCAP = 64;
+// Queue entries per warp.  A query iteration starts with fewer than 32
+// queued and appends at most 32 * K1_CPT.
+constexpr int K1_QCAP = 32 * (K1_CPT + 1);
 
 // Output and key layout for the (non-inlined) flush, kept in shared memory
 // so the hot loop does not hold them in registers.
@@ -377,94 +379,134 @@ __device__ __noinline__ void rare_flush(const QRec *__restrict__ sq, const WarpR
     append_hit_w(C, h.hit, key, h.tb, h.te, lane);
 }
 
+// Evaluation modes of the common loop (per item / warp sub-tile):
+//   K1_F32  FP32 pre-filter (below); survivors are re-evaluated exactly
+//   K1_F64  the FP64 filter of filter.cuh (items whose magnitudes are
+//           outside the FP32 pre-filter's validity)
+//   K1_ALL  every overlapping pair is queued for the exact IEEE path
+//           (extreme-exponent tiles, launches outside the filter bounds)
+enum { K1_F32 = 0, K1_F64 = 1, K1_ALL = 2 };
+
+// FP32 pre-filter: filter.cuh (f32_item / f32_query / f32_cand / f32_flag).
+
+// Query record of the FP32 pre-filter (48 B): filter view + exact times
+// for per-pair overlap counting.
+struct __align__(16) QF32 {
+    float ts, x, y, z;
+    float a, b, pad0, pad1;
+    double ts64, te64;
+};
+
+__device__ __forceinline__ void lds4f(uint32_t a, float &x, float &y, float &z, float &w) {
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "r"(a));
+}
+
 // One warp, K1_CPT candidates per lane, staged queries j0..j1-1 of one
 // (TA, TB) case.  CNT: count overlaps per iteration; otherwise the caller
 // counts them for the whole range by binary search and lanes that do not
 // overlap a query are rejected on the rare path (window edges only).
 // Flagged pairs are queued and evaluated exactly 32 at a time (rare_flush),
 // so hit-dense workloads do not serialise the warp on divergent code.
-template <int TA, int TB, bool SLOW, bool CNT>
-__device__ __forceinline__ void pair_run(const K1Launch &L, const QRec *__restrict__ sq, int j0, int j1,
-                                         const CandF (&r)[K1_CPT], double wmin_te, double wmax_te,
-                                         const WarpRare &W, int lane, unsigned &n_ov, unsigned &n_hit,
-                                         const FilterK &K) {
+template <int TA, int TB, int MODE, bool CNT>
+__device__ __forceinline__ void pair_run(const K1Launch &L, const QRec *__restrict__ sq,
+                                         const QF32 *__restrict__ sqf, int j0, int j1,
+                                         const CandF (&r)[K1_CPT], const CandF32 (&c32)[K1_CPT],
+                                         double wmin_te, double wmax_te, const WarpRare &W, int lane,
+                                         unsigned &n_ov, unsigned &n_hit, const FilterK &K) {
+    constexpr bool SLOW = MODE == K1_ALL;
+    constexpr uint32_t STRIDE = MODE == K1_F32 ? (uint32_t)sizeof(QF32) : (uint32_t)sizeof(QRec);
+    const uint32_t base = MODE == K1_F32 ? (uint32_t)__cvta_generic_to_shared(sqf)
+                                         : (uint32_t)__cvta_generic_to_shared(sq);
     int qn = 0;  // queued entries (warp-uniform)
-    const uint32_t qa0 = (uint32_t)__cvta_generic_to_shared(sq) + (uint32_t)j0 * (uint32_t)sizeof(QRec);
-    const uint32_t qa_end = qa0 + (uint32_t)(j1 - j0) * (uint32_t)sizeof(QRec);
-    // The loop is driven by the record address alone; everything the rare
-    // path needs (query index, lane masks) is derived inside its branch, so
-    // the common iteration is loads, FP64 math, one vote and one branch.
-    for (uint32_t qa = qa0; qa < qa_end; qa += (uint32_t)sizeof(QRec)) {
-        bool cand[K1_CPT];
-        if (SLOW) {  // unsafe tile or launch: the exact evaluation is the filter
-            const QVals Q = load_q(qa);
+    const uint32_t qa0 = base + (uint32_t)j0 * STRIDE;
+    const uint32_t qa_end = qa0 + (uint32_t)(j1 - j0) * STRIDE;
+    uint32_t qa = qa0;
+    for (;;) {
+        // Inner loop, driven by the record address alone and free of calls
+        // (the flush is called outside it, so nothing it holds needs saving
+        // around a call): loads, math, one vote, one branch per query.  Flags
+        // are queued; it exits when 32 or more are waiting.
+        for (; qa < qa_end; qa += STRIDE) {
+            bool cand[K1_CPT];
+            if (MODE == K1_F32) {
+                float qts, qx, qy, qz, qa4, qb4, p0, p1;
+                lds4f(qa, qts, qx, qy, qz);
+                lds4f(qa + 16, qa4, qb4, p0, p1);
+                double cts = 0.0, cte = 0.0;
+                if (CNT) lds2(qa + 32, cts, cte);
+#pragma unroll
+                for (int k = 0; k < K1_CPT; ++k) {
+                    bool ov = true;
+                    if (CNT) {
+                        if (TA == TA_C) ov = r[k].ts <= cte;
+                        else if (TA == TA_R) ov = cts <= r[k].te;
+                        else ov = r[k].ts <= cte && cts <= r[k].te;
+                        n_ov += ov ? 1u : 0u;
+                    }
+                    cand[k] = f32_flag(c32[k], qts, qx, qy, qz, qa4, qb4) && ov;
+                }
+            } else if (MODE == K1_ALL) {
+                double cts, cte;
+                lds2(qa, cts, cte);
+#pragma unroll
+                for (int k = 0; k < K1_CPT; ++k) {
+                    const bool ov = r[k].ts <= cte && cts <= r[k].te;  // invalid lanes: ts = +inf
+                    if (CNT) n_ov += ov ? 1u : 0u;
+                    cand[k] = ov;
+                }
+            } else {
+                const QF Q = load_qf(qa);
+#pragma unroll
+                for (int k = 0; k < K1_CPT; ++k) {
+                    bool ov = true;
+                    if (CNT) {
+                        // TA_C: the query started first, so it overlaps iff it ends
+                        // at or after r.ts; TA_R: iff it starts at or before r.te
+                        // (invalid lanes: ts = +inf, te = -inf)
+                        if (TA == TA_C) ov = r[k].ts <= Q.te;
+                        else if (TA == TA_R) ov = Q.ts <= r[k].te;
+                        else ov = r[k].ts <= Q.te && Q.ts <= r[k].te;
+                        n_ov += ov ? 1u : 0u;
+                    }
+                    cand[k] = pair_filter<TA, TB>(r[k], Q, wmin_te, wmax_te, K) && ov;
+                }
+            }
+            bool any = false;
+#pragma unroll
+            for (int k = 0; k < K1_CPT; ++k) any |= cand[k];
+            if (!__any_sync(0xffffffffu, any)) continue;
+            // rare: queue the flagged pairs of this query (qn < 32 on entry)
+            const uint32_t j = (qa - base) / STRIDE;
+            unsigned lt;
+            asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
 #pragma unroll
             for (int k = 0; k < K1_CPT; ++k) {
-                bool ov = true;
-                if (CNT) {
-                    ov = r[k].ts <= Q.te && Q.ts <= r[k].te;  // invalid lanes: ts = +inf
-                    n_ov += ov ? 1u : 0u;
-                }
-                const Cand x = cand_exact(W.cs[k * 32 + lane]);
-                double cc, aa, dot, e;
-                cand[k] = pair_eval<TA, TB, true>(x, Q, qa, wmin_te, wmax_te, K.d2, cc, aa, dot, e) && ov;
+                const unsigned m = __ballot_sync(0xffffffffu, cand[k]);
+                if (cand[k]) W.q[qn + __popc(m & lt)] = ((uint32_t)(k * 32 + lane) << 16) | j;
+                qn += __popc(m);
             }
-        } else {
-            const QF Q = load_qf(qa);
-#pragma unroll
-            for (int k = 0; k < K1_CPT; ++k) {
-                bool ov = true;
-                if (CNT) {
-                    // TA_C: the query started first, so it overlaps iff it ends
-                    // at or after r.ts; TA_R: iff it starts at or before r.te
-                    // (invalid lanes: ts = +inf, te = -inf)
-                    if (TA == TA_C) ov = r[k].ts <= Q.te;
-                    else if (TA == TA_R) ov = Q.ts <= r[k].te;
-                    else ov = r[k].ts <= Q.te && Q.ts <= r[k].te;
-                    n_ov += ov ? 1u : 0u;
-                }
-                cand[k] = pair_filter<TA, TB>(r[k], Q, wmin_te, wmax_te, K) && ov;
+            if (qn >= 32) {
+                qa += STRIDE;
+                break;
             }
         }
-        bool any = false;
+        // flush 32 at a time; the last partial batch at the end of the range
+        const bool done = qa >= qa_end;
+        while (qn >= 32 || (done && qn > 0)) {
+            const int nf = qn < 32 ? qn : 32;
+            __syncwarp();
+            rare_flush<TA, TB, SLOW>(sq, W, nf, wmin_te, wmax_te, lane, n_hit);
+            __syncwarp();
+            uint32_t mv[K1_CPT];
 #pragma unroll
-        for (int k = 0; k < K1_CPT; ++k) any |= cand[k];
-        if (!__any_sync(0xffffffffu, any)) continue;
-        // rare: queue the flagged pairs of this query, flushing 32 at a time
-        const uint32_t j = (qa - (uint32_t)__cvta_generic_to_shared(sq)) / (uint32_t)sizeof(QRec);
-        unsigned lt;
-        asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+            for (int k = 0; k < K1_CPT; ++k) mv[k] = lane + 32 * (k + 1) < qn ? W.q[lane + 32 * (k + 1)] : 0u;
+            __syncwarp();
 #pragma unroll
-        for (int k = 0; k < K1_CPT; ++k) {
-            const unsigned m = __ballot_sync(0xffffffffu, cand[k]);
-            if (!m) continue;
-            const int c = __popc(m);
-            if (qn + c > K1_QCAP) {
-                __syncwarp();
-                rare_flush<TA, TB, SLOW>(sq, W, qn < 32 ? qn : 32, wmin_te, wmax_te, lane, n_hit);
-                __syncwarp();
-                const uint32_t moved = lane + 32 < qn ? W.q[lane + 32] : 0u;
-                __syncwarp();
-                if (lane + 32 < qn) W.q[lane] = moved;
-                qn = qn > 32 ? qn - 32 : 0;
-            }
-            if (cand[k]) W.q[qn + __popc(m & lt)] = ((uint32_t)(k * 32 + lane) << 16) | j;
-            qn += c;
+            for (int k = 0; k < K1_CPT; ++k)
+                if (lane + 32 * (k + 1) < qn) W.q[lane + 32 * k] = mv[k];
+            qn -= nf;
         }
-        if (qn >= 32) {
-            __syncwarp();
-            rare_flush<TA, TB, SLOW>(sq, W, 32, wmin_te, wmax_te, lane, n_hit);
-            __syncwarp();
-            const uint32_t moved = lane + 32 < qn ? W.q[lane + 32] : 0u;
-            __syncwarp();
-            if (lane + 32 < qn) W.q[lane] = moved;
-            qn -= 32;
-        }
-    }
-    if (qn > 0) {
-        __syncwarp();
-        rare_flush<TA, TB, SLOW>(sq, W, qn, wmin_te, wmax_te, lane, n_hit);
-        __syncwarp();
+        if (done) break;
     }
 }
 
@@ -520,8 +562,46 @@ __device__ __forceinline__ double warp_max(double v) {
     return v;
 }
 
-__global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L) {
+// The three start-time ranges of a warp's window in one mode.  C_BISECT:
+// every query of the TA_C range ends before all candidates and te is
+// sorted, so overlaps are counted by bisection; R_BISECT likewise for the
+// TA_R range (every query ends after all candidates).
+template <int MODE>
+__device__ __forceinline__ void run_cases(const K1Launch &L, const QRec *__restrict__ sq,
+                                          const QF32 *__restrict__ sqf, int nt, int jlo, int ja, int jb,
+                                          int jhi, bool c_bisect, bool r_bisect,
+                                          const CandF (&r)[K1_CPT], const CandF32 (&c32)[K1_CPT],
+                                          double wmin_te, double wmax, const WarpRare &W, int lane,
+                                          unsigned &n_ov, unsigned &n_hit, const FilterK &K) {
+    if (c_bisect) {
+        // overlap <=> r.ts <= cte; cte ascending over the tile
+#pragma unroll
+        for (int k = 0; k < K1_CPT; ++k)
+            n_ov += (unsigned)(ja - clampi(lower_bound_te(sq, nt, r[k].ts), jlo, ja));
+        pair_run<TA_C, TB_R, MODE, false>(L, sq, sqf, jlo, ja, r, c32, wmin_te, wmax, W, lane, n_ov, n_hit, K);
+    } else {
+        pair_run<TA_C, TB_DYN, MODE, true>(L, sq, sqf, jlo, ja, r, c32, wmin_te, wmax, W, lane, n_ov, n_hit, K);
+    }
+    pair_run<TA_BOTH, TB_DYN, MODE, true>(L, sq, sqf, ja, jb, r, c32, wmin_te, wmax, W, lane, n_ov, n_hit, K);
+    if (r_bisect) {
+        // overlap <=> cts <= r.te; cts ascending over the tile
+#pragma unroll
+        for (int k = 0; k < K1_CPT; ++k)
+            n_ov += (unsigned)(clampi(upper_bound_ts(sq, nt, r[k].te), jb, jhi) - jb);
+        pair_run<TA_R, TB_C, MODE, false>(L, sq, sqf, jb, jhi, r, c32, wmin_te, wmax, W, lane, n_ov, n_hit, K);
+    } else {
+        pair_run<TA_R, TB_DYN, MODE, true>(L, sq, sqf, jb, jhi, r, c32, wmin_te, wmax, W, lane, n_ov, n_hit, K);
+    }
+}
+
+// F32: the FP32 pre-filter kernel (items outside its validity take the
+// exact path); otherwise the FP64-filter kernel.  Two kernels, so that each
+// gets its own register allocation.
+template <bool F32>
+__global__ void __launch_bounds__(K1_THREADS, F32 ? K1_MIN_BLOCKS_F32 : K1_MIN_BLOCKS) k1_pairs(K1Launch L) {
     __shared__ QRec sq[K1_TQ];
+    __shared__ double f32b[8];    // per-item magnitude bounds (FP32 pre-filter)
+    __shared__ F32Item fi_sh;     // the item's FP32 origin and error bound
     __shared__ double pm[K1_TQ];  // running max of te over the tile
     __shared__ double sm[K1_TQ];  // suffix min of te over the tile
     __shared__ ItemCtx it_sh;
@@ -543,8 +623,11 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
     }
     WarpRare W;
     W.cfg = &fcfg;
-    W.cs = reinterpret_cast<CandRec *>(k1_dyn) + (size_t)warp * 32 * K1_CPT;
-    W.q = reinterpret_cast<uint32_t *>(k1_dyn + sizeof(CandRec) * 32 * K1_CPT * K1_WARPS) +
+    // dynamic shared memory: FP32 query records, then per-warp rare-path state
+    QF32 *sqf = reinterpret_cast<QF32 *>(k1_dyn);
+    unsigned char *rare_base = k1_dyn + sizeof(QF32) * K1_TQ;
+    W.cs = reinterpret_cast<CandRec *>(rare_base) + (size_t)warp * 32 * K1_CPT;
+    W.q = reinterpret_cast<uint32_t *>(rare_base + sizeof(CandRec) * 32 * K1_CPT * K1_WARPS) +
           (size_t)warp * K1_QCAP;
     const int64_t total = L.plan.meta[0];
     const int sub = (int)L.plan.meta[1];
@@ -558,6 +641,8 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
     FilterK K = filter_consts(cmax, L.d2);
     K.km = L.filter_km;
     const bool launch_exact = !filter_ok(cmax, L.d2);
+    const double dthr = sqrt(L.d2);  // d (RN(d*d) rounds; sqrt(RN(d^2)) >= d (1 - 2^-52))
+    const bool launch_f32 = F32 && !launch_exact && L.d2 <= 0x1p120 && cmax <= 0x1p60;
 
     for (;;) {
         if (tid == 0) {
@@ -620,6 +705,46 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
                 carry = __shfl_sync(0xffffffffu, v, 0);
             }
         }
+        // FP32 pre-filter bounds of this item relative to (O, T0) = the
+        // first staged query's start: warp 2 over the candidate groups,
+        // warp 3 over the staged queries
+        if (launch_f32 && warp == 2) {
+            const double ox = sq[0].sx, oy = sq[0].sy, oz = sq[0].sz, t0 = sq[0].ts;
+            double ar = 0.0, tvr = 0.0, vr = 0.0;
+            for (int64_t g = it.first_c / GB_SIZE + lane; g <= it.c_hi / GB_SIZE; g += 32) {
+                const GBound gb = L.e.gb[g];
+                ar = fmax(ar, fmax(fmax(fabs(gb.hi[0] - ox), fabs(ox - gb.lo[0])),
+                                   fmax(fmax(fabs(gb.hi[1] - oy), fabs(oy - gb.lo[1])),
+                                        fmax(fabs(gb.hi[2] - oz), fabs(oz - gb.lo[2])))));
+                tvr = fmax(tvr, fmax(fabs(gb.ts_hi - t0), fabs(t0 - gb.ts_lo)) * gb.vmax);
+                vr = fmax(vr, gb.vmax);
+            }
+            ar = warp_max(ar);
+            tvr = warp_max(tvr);
+            vr = warp_max(vr);
+            if (lane == 0) {
+                f32b[0] = ar;
+                f32b[1] = tvr;
+                f32b[2] = vr;
+            }
+        }
+        if (launch_f32 && warp == 3) {
+            const double ox = sq[0].sx, oy = sq[0].sy, oz = sq[0].sz, t0 = sq[0].ts;
+            double aq = 0.0, tq = 0.0, eq = 0.0;
+            for (int j = lane; j < it.nt; j += 32) {
+                aq = fmax(aq, fmax(fabs(sq[j].sx - ox), fmax(fabs(sq[j].sy - oy), fabs(sq[j].sz - oz))));
+                tq = fmax(tq, fabs(sq[j].ts - t0));
+                eq = fmax(eq, sq[j].ext);
+            }
+            aq = warp_max(aq);
+            tq = warp_max(tq);
+            eq = warp_max(eq);
+            if (lane == 0) {
+                f32b[3] = aq;
+                f32b[4] = tq;
+                f32b[5] = eq;
+            }
+        }
         if (tid < 32) {
             double carry = -INFINITY;
             for (int base = 0; base < it.nt; base += 32) {
@@ -635,6 +760,30 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
             }
         }
         __syncthreads();
+        // FP32 pre-filter records; M bounds every magnitude the FP32 path
+        // forms (per component), its error is <= 7 * 2^-24 M
+        bool item_f32 = false;
+        if (launch_f32 && !unsafe_q) {
+            if (tid == 0)
+                fi_sh = f32_item(sq[0].sx, sq[0].sy, sq[0].sz, sq[0].ts, f32b[0], f32b[1], f32b[2], f32b[3],
+                                 f32b[4], f32b[5], cmax);
+            __syncthreads();
+            item_f32 = fi_sh.ok;
+            if (item_f32) {
+                for (int j = tid; j < it.nt; j += K1_THREADS) {
+                    const QRec &q = sq[j];
+                    float v[6];
+                    f32_query(q.ts, q.sx, q.sy, q.sz, q.ext, q.dx, q.dy, q.dz, fi_sh, dthr, v);
+                    QF32 f;
+                    f.ts = v[0]; f.x = v[1]; f.y = v[2]; f.z = v[3]; f.a = v[4]; f.b = v[5];
+                    f.pad0 = f.pad1 = 0.f;
+                    f.ts64 = q.ts;
+                    f.te64 = q.te;
+                    sqf[j] = f;
+                }
+            }
+            __syncthreads();
+        }
 
         unsigned n_ov = 0, n_hit = 0;
         for (int s = 0; s < sub; ++s) {
@@ -675,6 +824,18 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
                 cr.ts = r[k].ts; cr.te = r[k].te;
                 cr.sx = r[k].sx; cr.sy = r[k].sy; cr.sz = r[k].sz;
             }
+            CandF32 c32[K1_CPT];
+            if (item_f32) {
+#pragma unroll
+                for (int k = 0; k < K1_CPT; ++k) {
+                    if (r[k].ts <= r[k].te) {  // valid lane
+                        c32[k] = f32_cand(r[k].ts, r[k].sx, r[k].sy, r[k].sz, r[k].vx, r[k].vy, r[k].vz, fi_sh);
+                    } else {  // far away: never flagged (and rejected exactly if it were)
+                        c32[k].px = c32[k].py = c32[k].pz = 0x1p60f;
+                        c32[k].vx = c32[k].vy = c32[k].vz = c32[k].sr = 0.f;
+                    }
+                }
+            }
             // key of (b, e_off of the warp's candidate 0, q_off = it.q0) without the j term
             W.key_base0 = make_key(L, it.b, wbase - L.plan.first[it.b], it.q0);
             __syncwarp();
@@ -696,37 +857,24 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
                 ja = jlo;
                 jb = jhi;  // everything in the generic (mixed) range
             }
-            const bool slow = launch_exact || unsafe_q || __any_sync(0xffffffffu, unsafe_r);
+            const bool slow = launch_exact || unsafe_q || __any_sync(0xffffffffu, unsafe_r) || (F32 && !item_f32);
             // tb case of a whole range: every query of the TA_C range ends
             // before all candidates (running max < min te), or every query of
             // the TA_R range ends after all of them (suffix min > max te)
             const bool c_tb_r = jlo < ja && pm[ja - 1] < wmin_te;
             const bool r_tb_c = jb < jhi && sm[jb] > wmax;
             if (slow) {
-                pair_run<TA_C, TB_DYN, true, true>(L, sq, jlo, ja, r, wmin_te, wmax, W, lane, n_ov, n_hit, K);
-                pair_run<TA_BOTH, TB_DYN, true, true>(L, sq, ja, jb, r, wmin_te, wmax, W, lane, n_ov, n_hit, K);
-                pair_run<TA_R, TB_DYN, true, true>(L, sq, jb, jhi, r, wmin_te, wmax, W, lane, n_ov, n_hit, K);
+                pair_run<TA_C, TB_DYN, K1_ALL, true>(L, sq, sqf, jlo, ja, r, c32, wmin_te, wmax, W, lane, n_ov, n_hit, K);
+                pair_run<TA_BOTH, TB_DYN, K1_ALL, true>(L, sq, sqf, ja, jb, r, c32, wmin_te, wmax, W, lane, n_ov, n_hit, K);
+                pair_run<TA_R, TB_DYN, K1_ALL, true>(L, sq, sqf, jb, jhi, r, c32, wmin_te, wmax, W, lane, n_ov, n_hit, K);
                 continue;
             }
-            if (c_tb_r && te_sorted) {
-                // overlap <=> r.ts <= cte; cte ascending over the tile
-#pragma unroll
-                for (int k = 0; k < K1_CPT; ++k)
-                    n_ov += (unsigned)(ja - clampi(lower_bound_te(sq, it.nt, r[k].ts), jlo, ja));
-                pair_run<TA_C, TB_R, false, false>(L, sq, jlo, ja, r, wmin_te, wmax, W, lane, n_ov, n_hit, K);
-            } else {
-                pair_run<TA_C, TB_DYN, false, true>(L, sq, jlo, ja, r, wmin_te, wmax, W, lane, n_ov, n_hit, K);
-            }
-            pair_run<TA_BOTH, TB_DYN, false, true>(L, sq, ja, jb, r, wmin_te, wmax, W, lane, n_ov, n_hit, K);
-            if (r_tb_c) {
-                // overlap <=> cts <= r.te; cts ascending over the tile
-#pragma unroll
-                for (int k = 0; k < K1_CPT; ++k)
-                    n_ov += (unsigned)(clampi(upper_bound_ts(sq, it.nt, r[k].te), jb, jhi) - jb);
-                pair_run<TA_R, TB_C, false, false>(L, sq, jb, jhi, r, wmin_te, wmax, W, lane, n_ov, n_hit, K);
-            } else {
-                pair_run<TA_R, TB_DYN, false, true>(L, sq, jb, jhi, r, wmin_te, wmax, W, lane, n_ov, n_hit, K);
-            }
+            if (F32)
+                run_cases<K1_F32>(L, sq, sqf, it.nt, jlo, ja, jb, jhi, c_tb_r && te_sorted, r_tb_c, r, c32,
+                                  wmin_te, wmax, W, lane, n_ov, n_hit, K);
+            else
+                run_cases<K1_F64>(L, sq, sqf, it.nt, jlo, ja, jb, jhi, c_tb_r && te_sorted, r_tb_c, r, c32,
+                                  wmin_te, wmax, W, lane, n_ov, n_hit, K);
         }
         // per-batch counters (64-bit)
         for (int o = 16; o; o >>= 1) {
@@ -747,7 +895,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
 }
 
 static size_t k1_dyn_smem() {
-    return (sizeof(CandRec) * 32 * K1_CPT + sizeof(uint32_t) * K1_QCAP) * K1_WARPS;
+    return sizeof(QF32) * K1_TQ + (sizeof(CandRec) * 32 * K1_CPT + sizeof(uint32_t) * K1_QCAP) * K1_WARPS;
 }
 
 // The dynamic shared-memory limit is a per-device function attribute.
@@ -757,24 +905,30 @@ static void k1_set_attrs() {
     cudaGetDevice(&dev);
     const uint64_t bit = 1ull << (dev & 63);
     if (!(done_mask.load() & bit)) {
-        TSK_CUDA(cudaFuncSetAttribute(k1_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        TSK_CUDA(cudaFuncSetAttribute(k1_pairs<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)k1_dyn_smem()));
+        TSK_CUDA(cudaFuncSetAttribute(k1_pairs<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)k1_dyn_smem()));
         done_mask.fetch_or(bit);
     }
 }
 
-int k1_blocks_per_sm() {
+int k1_blocks_per_sm(bool f32) {
     k1_set_attrs();
     int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k1_pairs, K1_THREADS, k1_dyn_smem());
+    if (f32) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k1_pairs<true>, K1_THREADS, k1_dyn_smem());
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k1_pairs<false>, K1_THREADS, k1_dyn_smem());
     return n > 0 ? n : 1;
 }
 
 int k1_candidates_per_thread() { return K1_CPT; }
 
+bool k1_use_f32(double d2, double db_cmax) { return d2 <= 0x1p120 && db_cmax <= 0x1p60; }
+
 void launch_k1(const K1Launch &L, int grid, cudaStream_t st) {
     k1_set_attrs();
-    k1_pairs<<<grid, K1_THREADS, k1_dyn_smem(), st>>>(L);
+    if (k1_use_f32(L.d2, L.db_cmax)) k1_pairs<true><<<grid, K1_THREADS, k1_dyn_smem(), st>>>(L);
+    else k1_pairs<false><<<grid, K1_THREADS, k1_dyn_smem(), st>>>(L);
     TSK_CUDA(cudaGetLastError());
 }
 

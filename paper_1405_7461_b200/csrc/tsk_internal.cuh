@@ -60,8 +60,20 @@ struct DBuf {
 //   unsafe   = 1 when the segment is outside the exponent window in which
 //              qdiv below is exact and the filter's error bound holds
 //              (seg_unsafe in db.cu); such tiles are evaluated exactly
+// Per-group bounds of GB_SIZE consecutive (start-sorted) segments: the
+// magnitudes K1's FP32 pre-filter needs for its per-item error bound
+// (k1_pairs.cu, "FP32 pre-filter").
+constexpr int GB_SIZE = 256;
+struct GBound {
+    double lo[3], hi[3];  // bounding box of the start positions
+    double ts_lo, ts_hi;  // start-time range
+    double vmax;          // max |velocity component|
+    double pad;
+};
+
 struct Soa {
     int64_t n = 0;
+    GBound *gb = nullptr;  // (n + GB_SIZE - 1) / GB_SIZE groups (entry stores only)
     double *ts = nullptr, *te = nullptr, *sx = nullptr, *sy = nullptr, *sz = nullptr;
     double *ex = nullptr, *ey = nullptr, *ez = nullptr;
     double *dx = nullptr, *dy = nullptr, *dz = nullptr, *rcp = nullptr;
@@ -204,13 +216,15 @@ void launch_ranges(tsk_db *db, const Soa &q, SearchPlanDev &p, bool spans_given,
 void launch_plan_items(SearchPlanDev &p, int slots, int stride, cudaStream_t st);
 void launch_qprep(const Soa &q, QRec *out, int *flags, unsigned long long *cmax_bits, cudaStream_t st);
 double soa_cmax(const Soa &s, cudaStream_t st);
+void soa_group_bounds(Soa &s, cudaStream_t st);  // GBound per GB_SIZE segments
 void launch_k1(const K1Launch &L, int grid, cudaStream_t st);
 void canonical_perm(int64_t n, const int64_t *qt, const int64_t *qs, const int64_t *et,
                     const int64_t *es, const double *tb, const double *te, uint32_t *perm,
                     DBuf &scratch, cudaStream_t st);
 void permute6(int64_t n, const uint32_t *perm, const int64_t *const in_i[4], const double *const in_f[2],
               int64_t *const out_i[4], double *const out_f[2], cudaStream_t st);
-int k1_blocks_per_sm();
+int k1_blocks_per_sm(bool f32);
+bool k1_use_f32(double d2, double db_cmax);
 int k1_candidates_per_thread();
 
 #ifndef K1_THREADS_DEF

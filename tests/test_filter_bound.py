@@ -3,10 +3,13 @@
 tools/filter_check.cpp evaluates the reference's discriminant with the
 vectorised pair arithmetic of core.py:490-537 on adversarial pairs (thresholds
 at each pair's own flip point, near-parallel and constant-offset motion,
-zero-length spans, waypoints, planar data, epoch-scale times) and asserts that
-every pair with a non-negative reference discriminant is flagged by the
-filter in every clip case K1 can route it through.  A mutated margin must
-produce misses, so the generator is known to reach the bound.
+zero-length spans, waypoints, planar data, epoch-scale times, head-on motion
+at the segment-distance flip point) and asserts that every pair with a
+non-negative reference discriminant is flagged by the FP64 filter in every
+clip case K1 can route it through, and that every reference hit is flagged
+by the FP32 pre-filter (with the item origin at the query and at a shifted
+point).  Mutated margins must produce misses, so the generator is known to
+reach both bounds.
 """
 
 from __future__ import annotations
@@ -32,7 +35,9 @@ def _build(tmp_path, header=HDR):
     cpp.write_text(src)
     exe = tmp_path / "fc"
     # -ffp-contract=off: the library is built with -fmad=false
-    subprocess.run(["g++", "-O2", "-ffp-contract=off", "-std=c++17", "-o", str(exe), str(cpp)], check=True)
+    # -frounding-math: the FP32 pre-filter's directed roundings use fesetround
+    subprocess.run(["g++", "-O2", "-ffp-contract=off", "-frounding-math", "-std=c++17", "-o", str(exe), str(cpp)],
+                   check=True)
     return exe
 
 
@@ -46,6 +51,9 @@ def test_filter_flags_every_nonnegative_reference_discriminant(tmp_path):
     assert rc == 0, err
     assert out["edge"]["misses"] == 0 and out["random"]["misses"] == 0
     assert out["edge"]["disc_pos"] > 100_000 and out["edge"]["skipped"] == 0
+    # FP32 pre-filter: every reference hit is flagged
+    assert out["edge"]["f32_misses"] == 0 and out["random"]["f32_misses"] == 0
+    assert out["edge"]["hits"] > 100_000 and out["edge"]["f32_checks"] > 1_000_000
 
 
 def test_filter_check_detects_a_too_small_margin(tmp_path):
@@ -57,3 +65,14 @@ def test_filter_check_detects_a_too_small_margin(tmp_path):
     hdr.write_text(mutated)
     rc, out, _ = _run(_build(tmp_path, str(hdr)), 150_000)
     assert rc == 1 and out["edge"]["misses"] > 0
+
+
+def test_filter_check_detects_a_missing_fp32_margin(tmp_path):
+    src = open(HDR).read()
+    mutated = src.replace("it.delta = 0x1p-18 * M + 0x1p-38 * cmax + 0x1p-100;", "it.delta = 0.0;")
+    mutated = mutated.replace("(1.0 + 0x1p-8) * (dthr + lq)", "(dthr + lq)")
+    assert mutated != src
+    hdr = tmp_path / "filter_mut32.cuh"
+    hdr.write_text(mutated)
+    rc, out, _ = _run(_build(tmp_path, str(hdr)), 150_000)
+    assert rc == 1 and out["edge"]["f32_misses"] > 0

@@ -549,3 +549,38 @@ def test_filter_exact_meetings_and_parallel_motion():
     ri, ci, tb, te, _, _ = orc.pair_mesh(_cols(rows), _cols(rows), 0.0)
     assert len(h0) == len(ri) >= n
     assert np.array_equal(h0.t_begin, tb) and np.array_equal(h0.t_end, te)
+
+
+@pytest.mark.parametrize("t_base,offset", [(0.0, 0.0), (1.7e9, 0.0), (1e3, 1e5)])
+def test_fp32_prefilter_head_on_flip_points(t_base, offset):
+    """The FP32 pre-filter's triangle bound is tight when the candidate moves
+    straight at a query that lies inside its span: thresholds at the segment
+    distance (the hit/miss flip point, reached at the query's end) ±1 ulp and
+    ±1e-12 relative must give the C oracle's result exactly."""
+    rng = np.random.default_rng(int(t_base) % 97 + int(offset) % 89 + 3)
+    checked = 0
+    for i in range(60):
+        ts_r = t_base + rng.uniform(0, 5)
+        te_r = ts_r + 10.0
+        ts_q = ts_r + rng.uniform(0.5, 4.0)
+        te_q = ts_q + rng.uniform(0.01, 4.0)
+        u = rng.normal(size=3)
+        u /= np.linalg.norm(u)
+        dist0 = rng.uniform(0.5, 1.0) * 10 ** rng.uniform(-3, 2)
+        speed = dist0 / rng.uniform(12.0, 40.0)
+        qs = rng.uniform(-1, 1, 3) * 10 + offset
+        qe = qs if i % 2 else qs + u * speed * (te_q - ts_q) * rng.uniform(-1, 1)
+        rs = qs + u * dist0
+        re = rs - u * speed * (te_r - ts_r)
+        A = np.array([*rs, ts_r, *re, te_r])
+        B = np.array([*qs, ts_q, *qe, te_q])
+        md = float(np.sqrt(_min_dist_sq(A[None, :], B[None, :])[0]))
+        for d in (md, np.nextafter(md, 0), np.nextafter(md, np.inf), md * (1 + 1e-12), md * (1 - 1e-12)):
+            rows = tsk.SegmentStore(np.array([0]), np.array([0]), *[A[c:c + 1] for c in range(8)])
+            cols = tsk.SegmentStore(np.array([1]), np.array([0]), *[B[c:c + 1] for c in range(8)])
+            h = tsk.pair_intervals(rows, cols, float(d))
+            want = c_oracle.pair(tuple(A), tuple(B), float(d))
+            got = None if len(h) == 0 else (h.t_begin[0], h.t_end[0])
+            assert got == want, (i, d)
+            checked += want is not None
+    assert checked > 20  # the flip points are straddled

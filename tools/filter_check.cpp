@@ -90,7 +90,79 @@ static bool hoist(const Seg &g, double &ext, double v[3], double dd[3]) {
 
 struct Counts {
     long pairs = 0, overlapping = 0, disc_pos = 0, checks = 0, flagged = 0, misses = 0, skipped = 0;
+    long hits = 0, f32_checks = 0, f32_flagged = 0, f32_misses = 0, f32_skipped = 0;
 };
+
+// the reference's hit decision for an overlapping pair (core.py:523-551)
+static bool ref_hit(const Seg &r, const Seg &c, double d) {
+    const double ta = r.ts > c.ts ? r.ts : c.ts;
+    const double tb = r.te < c.te ? r.te : c.te;
+    if (!(ta <= tb)) return false;
+    double ra[3], rb[3], ca[3], cb[3];
+    clipped(r, ta, ra);
+    clipped(r, tb, rb);
+    clipped(c, ta, ca);
+    clipped(c, tb, cb);
+    const double ux = ra[0] - ca[0], uy = ra[1] - ca[1], uz = ra[2] - ca[2];
+    const double cc = ux * ux + uy * uy + uz * uz;
+    const double d2 = d * d;
+    const double wx = (rb[0] - ra[0]) - (cb[0] - ca[0]);
+    const double wy = (rb[1] - ra[1]) - (cb[1] - ca[1]);
+    const double wz = (rb[2] - ra[2]) - (cb[2] - ca[2]);
+    const double aa = wx * wx + wy * wy + wz * wz;
+    const double bb = 2.0 * (ux * wx + uy * wy + uz * wz);
+    if (aa == 0.0) return cc <= d2;
+    const double disc = bb * bb - 4.0 * aa * (cc - d2);
+    if (!(disc >= 0.0)) return false;
+    const double sd = std::sqrt(disc);
+    const double qq = bb >= 0.0 ? -0.5 * (bb + sd) : -0.5 * (bb - sd);
+    const double r1 = qq / aa;
+    const double r2 = qq == 0.0 ? r1 : (cc - d2) / qq;
+    const double lo = r1 < r2 ? r1 : r2, hi = r1 > r2 ? r1 : r2;
+    return lo <= 1.0 && hi >= 0.0;
+}
+
+// K1's FP32 pre-filter for candidate r and query c, with the item origin at
+// (O, T0) and the item bounds taken from this pair alone (the tightest
+// bounds any item containing the pair can have).
+static void check_f32(const Seg &r, const Seg &c, double d, const double O[3], double T0, double cmax,
+                      Counts &n, const char *tag) {
+    double rext, rv[3], rd[3], cext, cv[3], cd[3];
+    const bool ok = hoist(r, rext, rv, rd) & hoist(c, cext, cv, cd);
+    if (!ok || !filter_ok(cmax, d * d) || !(d * d <= 0x1p120) || !(cmax <= 0x1p60)) {
+        ++n.f32_skipped;
+        return;
+    }
+    double ar = 0, aq = 0, vr = 0;
+    for (int i = 0; i < 3; ++i) {
+        ar = std::fmax(ar, std::fabs(r.s[i] - O[i]));
+        aq = std::fmax(aq, std::fabs(c.s[i] - O[i]));
+        vr = std::fmax(vr, std::fabs(rv[i]));
+    }
+    const double tvr = std::fabs(r.ts - T0) * vr, tq = std::fabs(c.ts - T0);
+    const F32Item it = f32_item(O[0], O[1], O[2], T0, ar, tvr, vr, aq, tq, cext, cmax);
+    if (!it.ok) {
+        ++n.f32_skipped;
+        return;
+    }
+    float q[6];
+    f32_query(c.ts, c.s[0], c.s[1], c.s[2], cext, cd[0], cd[1], cd[2], it, std::sqrt(d * d), q);
+    const CandF32 cf = f32_cand(r.ts, r.s[0], r.s[1], r.s[2], rv[0], rv[1], rv[2], it);
+    const bool f = f32_flag(cf, q[0], q[1], q[2], q[3], q[4], q[5]);
+    const bool need = ref_hit(r, c, d);
+    ++n.f32_checks;
+    n.hits += need;
+    n.f32_flagged += f;
+    if (need && !f) {
+        ++n.f32_misses;
+        if (n.f32_misses <= 5)
+            std::fprintf(stderr,
+                         "F32 MISS %s d=%.17g r=[%.17g %.17g (%.17g %.17g %.17g)->(%.17g %.17g %.17g)] "
+                         "c=[%.17g %.17g (%.17g %.17g %.17g)->(%.17g %.17g %.17g)] O=(%g %g %g) T0=%.17g\n",
+                         tag, d, r.ts, r.te, r.s[0], r.s[1], r.s[2], r.e[0], r.e[1], r.e[2], c.ts, c.te,
+                         c.s[0], c.s[1], c.s[2], c.e[0], c.e[1], c.e[2], O[0], O[1], O[2], T0);
+    }
+}
 
 template <int TA, int TB>
 static void check_case(const CandF &cf, const QF &qf, double wmin, double wmax, const FilterK &K,
@@ -128,6 +200,14 @@ static void check_pair(const Seg &r, const Seg &c, double d, Counts &n, const ch
     }
     const bool need = disc >= 0.0;
     n.disc_pos += need;
+    {
+        // FP32 pre-filter, origin at the query's start and at a shifted point
+        const double O0[3] = {c.s[0], c.s[1], c.s[2]};
+        check_f32(r, c, d, O0, c.ts, cmax, n, tag);
+        double O1[3];
+        for (int i = 0; i < 3; ++i) O1[i] = c.s[i] + unif(-1, 1) * (std::fabs(c.s[i]) + 1.0);
+        check_f32(r, c, d, O1, c.ts - unif(0, 5) * (std::fabs(c.te - c.ts) + 1.0), cmax, n, tag);
+    }
     cf.ts = r.ts; cf.te = r.te;
     cf.sx = r.s[0]; cf.sy = r.s[1]; cf.sz = r.s[2];
     cf.vx = rv[0]; cf.vy = rv[1]; cf.vz = rv[2];
@@ -158,7 +238,7 @@ static void check_pair(const Seg &r, const Seg &c, double d, Counts &n, const ch
 
 // closest approach of the two (linear) motions over the shared span, in
 // long double: the threshold at which the pair flips between hit and miss
-static double min_dist(const Seg &r, const Seg &c) {
+static double min_dist(const Seg &r, const Seg &c, bool clamp = false) {
     const long double ta = r.ts > c.ts ? r.ts : c.ts, tb = r.te < c.te ? r.te : c.te;
     auto pos = [](const Seg &g, long double t, long double p[3]) {
         const long double ext = (long double)g.te - g.ts;
@@ -174,9 +254,10 @@ static double min_dist(const Seg &r, const Seg &c) {
         uu += u[i] * u[i]; ww += w[i] * w[i]; uw += u[i] * w[i];
     }
     long double lam = ww > 0 ? -uw / ww : 0;
-    // the line distance (the discriminant's root), not clamped to [0, 1]
+    // the line distance (the discriminant's root), or with clamp = true the
+    // segment distance (lambda clamped to [0, 1]: where hits flip)
+    if (clamp) lam = lam < 0 ? 0 : (lam > 1 ? 1 : lam);
     long double m2 = uu + 2 * lam * uw + lam * lam * ww;
-    (void)lam;
     return (double)std::sqrt(m2 > 0 ? m2 : 0);
 }
 
@@ -202,7 +283,7 @@ int main(int argc, char **argv) {
         // overlapping spans with random alignment
         const double a0 = T + unif(0, 10), a1 = a0 + unif(0.01, 10);
         double b0 = T + unif(0, 10), b1 = b0 + unif(0.01, 10);
-        const int mode = (int)(next_u64() % 8);
+        const int mode = (int)(next_u64() % 9);
         if (mode == 1) b0 = a0;                         // equal starts (TA_BOTH)
         if (mode == 2) b1 = a1;                         // equal ends
         if (mode == 3) { b0 = a1; b1 = a1 + 1.0; }      // touching: zero-length span
@@ -224,7 +305,24 @@ int main(int argc, char **argv) {
             }
             c.ts = r.ts; c.te = r.te;
         }
-        if (next_u64() % 3 == 0) { r.s[2] = r.e[2] = 0.0; c.s[2] = c.e[2] = 0.0; }  // planar data
+        if (mode == 7) {
+            // head-on: the query sits inside the candidate's span and the
+            // candidate moves straight at the query's start point, so the
+            // FP32 pre-filter's triangle bound is tight at the flip point
+            r.ts = a0; r.te = a0 + 10.0;
+            c.ts = a0 + unif(0.5, 4.0); c.te = c.ts + unif(0.01, 4.0);
+            double dir[3], nrm = 0;
+            for (int i = 0; i < 3; ++i) { dir[i] = unif(-1, 1); nrm += dir[i] * dir[i]; }
+            nrm = std::sqrt(nrm);
+            const double dist0 = L * unif(0.5, 1.0), speed = dist0 / unif(12.0, 40.0);
+            for (int i = 0; i < 3; ++i) {
+                c.s[i] = unif(-L, L);
+                c.e[i] = next_u64() % 2 ? c.s[i] : c.s[i] + dir[i] / nrm * speed * (c.te - c.ts) * unif(-1, 1);
+                r.s[i] = c.s[i] + dir[i] / nrm * dist0;
+                r.e[i] = r.s[i] - dir[i] / nrm * speed * (r.te - r.ts);
+            }
+        }
+        if (mode != 7 && next_u64() % 3 == 0) { r.s[2] = r.e[2] = 0.0; c.s[2] = c.e[2] = 0.0; }  // planar data
         nrand.pairs++;
         check_pair(r, c, L * 0.01, nrand, "rand");
         // thresholds straddling the pair's own flip point
@@ -240,12 +338,26 @@ int main(int argc, char **argv) {
         } else {
             check_pair(r, c, 0.0, n, "zero");
         }
+        // thresholds straddling the segment distance (hit/miss flip point)
+        const double ms = min_dist(r, c, true);
+        if (ms > 0 && std::isfinite(ms)) {
+            for (int k = 0; k < 4; ++k) {
+                const double rel = std::ldexp(1.0, -(int)(next_u64() % 52)) * (next_u64() % 2 ? 1 : -1);
+                check_pair(r, c, ms * (1 + rel), n, "seg");
+            }
+            check_pair(r, c, ms, n, "seg0");
+            check_pair(r, c, std::nextafter(ms, INFINITY), n, "seg+");
+        }
     }
     std::printf("{\"edge\": {\"pairs\": %ld, \"overlapping\": %ld, \"disc_pos\": %ld, \"checks\": %ld, "
-                "\"flagged\": %ld, \"skipped\": %ld, \"misses\": %ld}, "
+                "\"flagged\": %ld, \"skipped\": %ld, \"misses\": %ld, \"hits\": %ld, \"f32_checks\": %ld, "
+                "\"f32_flagged\": %ld, \"f32_skipped\": %ld, \"f32_misses\": %ld}, "
                 "\"random\": {\"pairs\": %ld, \"overlapping\": %ld, \"disc_pos\": %ld, \"checks\": %ld, "
-                "\"flagged\": %ld, \"misses\": %ld}}\n",
-                n.pairs, n.overlapping, n.disc_pos, n.checks, n.flagged, n.skipped, n.misses, nrand.pairs,
-                nrand.overlapping, nrand.disc_pos, nrand.checks, nrand.flagged, nrand.misses);
-    return (n.misses || nrand.misses) ? 1 : 0;
+                "\"flagged\": %ld, \"misses\": %ld, \"hits\": %ld, \"f32_checks\": %ld, \"f32_flagged\": %ld, "
+                "\"f32_misses\": %ld}}\n",
+                n.pairs, n.overlapping, n.disc_pos, n.checks, n.flagged, n.skipped, n.misses, n.hits,
+                n.f32_checks, n.f32_flagged, n.f32_skipped, n.f32_misses, nrand.pairs, nrand.overlapping,
+                nrand.disc_pos, nrand.checks, nrand.flagged, nrand.misses, nrand.hits, nrand.f32_checks,
+                nrand.f32_flagged, nrand.f32_misses);
+    return (n.misses || nrand.misses || n.f32_misses || nrand.f32_misses) ? 1 : 0;
 }
