@@ -310,12 +310,36 @@ __device__ __forceinline__ Cand cand_exact(const CandRec &cr) {
     return r;
 }
 
-struct WarpRare {
-    CandRec *cs;  // 32*K1_CPT staged candidates of this warp
-    uint32_t *q;  // queue: candidate index << 16 | query index
-    uint64_t key_base0;  // key of (b, e_off of candidate 0, it.q0) without the j term
-    const FlushCfg *cfg;
+// Query record of the FP32 pre-filter (48 B): filter view + exact times
+// for per-pair overlap counting.
+struct __align__(16) QF32 {
+    float ts, x, y, z;
+    float a, b, pad0, pad1;
+    double ts64, te64;
 };
+
+// Per-warp context of the current sub-tile, read by the flush.
+struct WarpCtx {
+    uint64_t key_base0;     // key of (b, e_off of candidate 0, it.q0) without the j term
+    double wmin_te, wmax;   // min te / max te of the warp's candidates (tb cases)
+};
+
+// Block-shared state of K1 (both kernels): the flush configuration, the
+// per-warp contexts, and the dynamic region (FP32 query records, then the
+// per-warp staged candidates and queues).  The rare path reaches all of it
+// from the warp index, so the hot loops carry none of it in registers.
+__shared__ FlushCfg k1_fcfg;
+__shared__ WarpCtx k1_wctx[K1_WARPS];
+extern __shared__ __align__(16) unsigned char k1_dyn[];
+
+__device__ __forceinline__ QF32 *k1_sqf() { return reinterpret_cast<QF32 *>(k1_dyn); }
+__device__ __forceinline__ CandRec *warp_cs(int warp) {
+    return reinterpret_cast<CandRec *>(k1_dyn + sizeof(QF32) * K1_TQ) + warp * 32 * K1_CPT;
+}
+__device__ __forceinline__ uint32_t *warp_q(int warp) {
+    return reinterpret_cast<uint32_t *>(k1_dyn + sizeof(QF32) * K1_TQ + sizeof(CandRec) * 32 * K1_CPT * K1_WARPS) +
+           warp * K1_QCAP;
+}
 
 __device__ __forceinline__ void append_hit_w(const FlushCfg &C, bool hit, uint64_t key, double tb,
                                              double te, int lane) {
@@ -339,18 +363,21 @@ __device__ __forceinline__ void append_hit_w(const FlushCfg &C, bool hit, uint64
 // the reference's arithmetic (pair_eval), the second filter and the exact
 // solve (core.py:503-558), then the warp-aggregated append.
 template <int TA, int TB, bool SLOW>
-__device__ __noinline__ void rare_flush(const QRec *__restrict__ sq, const WarpRare W, int n_items,
-                                        double wmin_te, double wmax_te, int lane, unsigned &n_hit) {
-    const FlushCfg &C = *W.cfg;
+__device__ __noinline__ void rare_flush(const QRec *__restrict__ sq, int warp, int n_items, int lane,
+                                        unsigned &n_hit) {
+    const FlushCfg &C = k1_fcfg;
     const double d2 = C.d2;
+    const CandRec *cs = warp_cs(warp);
+    const uint32_t *wq = warp_q(warp);
+    const double wmin_te = k1_wctx[warp].wmin_te, wmax_te = k1_wctx[warp].wmax;
     Hit h;
     h.hit = false;
     h.tb = h.te = 0.0;
     uint64_t key = 0;
     if (lane < n_items) {
-        const uint32_t ent = W.q[lane];
+        const uint32_t ent = wq[lane];
         const int ci = (int)(ent >> 16), j = (int)(ent & 0xffffu);
-        const Cand r = cand_exact(W.cs[ci]);
+        const Cand r = cand_exact(cs[ci]);
         const uint32_t qa = (uint32_t)__cvta_generic_to_shared(sq) + (uint32_t)j * (uint32_t)sizeof(QRec);
         const QVals Q = load_q(qa);
         double cc, aa, dot, e;
@@ -372,7 +399,7 @@ __device__ __noinline__ void rare_flush(const QRec *__restrict__ sq, const WarpR
         if (ex && (flat || !plain || !(e > m) || !(q1 > m) || vertex_in))
             h = rare_pair(r, sq[j], cc, aa, dot, e, d2);
         // candidate ci shifts the entry offset, query j the query offset
-        key = W.key_base0 + (C.query_major ? ((uint64_t)j << C.minor_bits) + (uint64_t)ci
+        key = k1_wctx[warp].key_base0 + (C.query_major ? ((uint64_t)j << C.minor_bits) + (uint64_t)ci
                                            : ((uint64_t)ci << C.minor_bits) + (uint64_t)j);
     }
     n_hit += h.hit ? 1u : 0u;
@@ -389,14 +416,6 @@ enum { K1_F32 = 0, K1_F64 = 1, K1_ALL = 2 };
 
 // FP32 pre-filter: filter.cuh (f32_item / f32_query / f32_cand / f32_flag).
 
-// Query record of the FP32 pre-filter (48 B): filter view + exact times
-// for per-pair overlap counting.
-struct __align__(16) QF32 {
-    float ts, x, y, z;
-    float a, b, pad0, pad1;
-    double ts64, te64;
-};
-
 __device__ __forceinline__ void lds4f(uint32_t a, float &x, float &y, float &z, float &w) {
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "r"(a));
 }
@@ -408,12 +427,13 @@ __device__ __forceinline__ void lds4f(uint32_t a, float &x, float &y, float &z, 
 // Flagged pairs are queued and evaluated exactly 32 at a time (rare_flush),
 // so hit-dense workloads do not serialise the warp on divergent code.
 template <int TA, int TB, int MODE, bool CNT>
-__device__ __forceinline__ void pair_run(const K1Launch &L, const QRec *__restrict__ sq,
+__device__ __forceinline__ void pair_run(const QRec *__restrict__ sq,
                                          const QF32 *__restrict__ sqf, int j0, int j1,
                                          const CandF (&r)[K1_CPT], const CandF32 (&c32)[K1_CPT],
-                                         double wmin_te, double wmax_te, const WarpRare &W, int lane,
+                                         double wmin_te, double wmax_te, int warp, int lane,
                                          unsigned &n_ov, unsigned &n_hit, const FilterK &K) {
     constexpr bool SLOW = MODE == K1_ALL;
+    uint32_t *const wq = warp_q(warp);
     constexpr uint32_t STRIDE = MODE == K1_F32 ? (uint32_t)sizeof(QF32) : (uint32_t)sizeof(QRec);
     const uint32_t base = MODE == K1_F32 ? (uint32_t)__cvta_generic_to_shared(sqf)
                                          : (uint32_t)__cvta_generic_to_shared(sq);
@@ -482,7 +502,7 @@ __device__ __forceinline__ void pair_run(const K1Launch &L, const QRec *__restri
 #pragma unroll
             for (int k = 0; k < K1_CPT; ++k) {
                 const unsigned m = __ballot_sync(0xffffffffu, cand[k]);
-                if (cand[k]) W.q[qn + __popc(m & lt)] = ((uint32_t)(k * 32 + lane) << 16) | j;
+                if (cand[k]) wq[qn + __popc(m & lt)] = ((uint32_t)(k * 32 + lane) << 16) | j;
                 qn += __popc(m);
             }
             if (qn >= 32) {
@@ -495,15 +515,15 @@ __device__ __forceinline__ void pair_run(const K1Launch &L, const QRec *__restri
         while (qn >= 32 || (done && qn > 0)) {
             const int nf = qn < 32 ? qn : 32;
             __syncwarp();
-            rare_flush<TA, TB, SLOW>(sq, W, nf, wmin_te, wmax_te, lane, n_hit);
+            rare_flush<TA, TB, SLOW>(sq, warp, nf, lane, n_hit);
             __syncwarp();
             uint32_t mv[K1_CPT];
 #pragma unroll
-            for (int k = 0; k < K1_CPT; ++k) mv[k] = lane + 32 * (k + 1) < qn ? W.q[lane + 32 * (k + 1)] : 0u;
+            for (int k = 0; k < K1_CPT; ++k) mv[k] = lane + 32 * (k + 1) < qn ? wq[lane + 32 * (k + 1)] : 0u;
             __syncwarp();
 #pragma unroll
             for (int k = 0; k < K1_CPT; ++k)
-                if (lane + 32 * (k + 1) < qn) W.q[lane + 32 * k] = mv[k];
+                if (lane + 32 * (k + 1) < qn) wq[lane + 32 * k] = mv[k];
             qn -= nf;
         }
         if (done) break;
@@ -562,6 +582,42 @@ __device__ __forceinline__ double warp_max(double v) {
     return v;
 }
 
+// FP32 ranges run in their own (non-inlined) function: the caller's item
+// and sub-tile state is saved around the call once per range, and the inner
+// loop gets the register file to itself (inlined, it spilled the FP32
+// candidates to local memory).
+static_assert(K1_CPT == 2, "f32_range passes two candidates by value");
+template <int TA, int TB, bool CNT>
+__device__ __noinline__ uint2 f32_range(const QRec *__restrict__ sq, const QF32 *__restrict__ sqf, int j0,
+                                        int j1, CandF32 c0, CandF32 c1, double ts0, double te0, double ts1,
+                                        double te1, int warp, int lane) {
+    CandF r[K1_CPT];
+    r[0].ts = ts0; r[0].te = te0;
+    r[1].ts = ts1; r[1].te = te1;
+    const CandF32 c32[K1_CPT] = {c0, c1};
+    FilterK K;  // unused in FP32 mode
+    K.d2 = K.k5 = K.kc = K.t0 = K.km = 0.0;
+    unsigned ov = 0, hit = 0;
+    pair_run<TA, TB, K1_F32, CNT>(sq, sqf, j0, j1, r, c32, 0.0, 0.0, warp, lane, ov, hit, K);
+    return make_uint2(ov, hit);
+}
+
+template <int TA, int TB, int MODE, bool CNT>
+__device__ __forceinline__ void range_run(const QRec *__restrict__ sq, const QF32 *__restrict__ sqf, int j0,
+                                          int j1, const CandF (&r)[K1_CPT], const CandF32 (&c32)[K1_CPT],
+                                          double wmin_te, double wmax, int warp, int lane,
+                                          unsigned &n_ov, unsigned &n_hit, const FilterK &K) {
+    if (MODE == K1_F32) {
+        if (j0 >= j1) return;
+        const uint2 o = f32_range<TA, TB, CNT>(sq, sqf, j0, j1, c32[0], c32[1], r[0].ts, r[0].te, r[1].ts,
+                                               r[1].te, warp, lane);
+        n_ov += o.x;
+        n_hit += o.y;
+    } else {
+        pair_run<TA, TB, MODE, CNT>(sq, sqf, j0, j1, r, c32, wmin_te, wmax, warp, lane, n_ov, n_hit, K);
+    }
+}
+
 // The three start-time ranges of a warp's window in one mode.  C_BISECT:
 // every query of the TA_C range ends before all candidates and te is
 // sorted, so overlaps are counted by bisection; R_BISECT likewise for the
@@ -571,26 +627,26 @@ __device__ __forceinline__ void run_cases(const K1Launch &L, const QRec *__restr
                                           const QF32 *__restrict__ sqf, int nt, int jlo, int ja, int jb,
                                           int jhi, bool c_bisect, bool r_bisect,
                                           const CandF (&r)[K1_CPT], const CandF32 (&c32)[K1_CPT],
-                                          double wmin_te, double wmax, const WarpRare &W, int lane,
+                                          double wmin_te, double wmax, int warp, int lane,
                                           unsigned &n_ov, unsigned &n_hit, const FilterK &K) {
     if (c_bisect) {
         // overlap <=> r.ts <= cte; cte ascending over the tile
 #pragma unroll
         for (int k = 0; k < K1_CPT; ++k)
             n_ov += (unsigned)(ja - clampi(lower_bound_te(sq, nt, r[k].ts), jlo, ja));
-        pair_run<TA_C, TB_R, MODE, false>(L, sq, sqf, jlo, ja, r, c32, wmin_te, wmax, W, lane, n_ov, n_hit, K);
+        range_run<TA_C, TB_R, MODE, false>(sq, sqf, jlo, ja, r, c32, wmin_te, wmax, warp, lane, n_ov, n_hit, K);
     } else {
-        pair_run<TA_C, TB_DYN, MODE, true>(L, sq, sqf, jlo, ja, r, c32, wmin_te, wmax, W, lane, n_ov, n_hit, K);
+        range_run<TA_C, TB_DYN, MODE, true>(sq, sqf, jlo, ja, r, c32, wmin_te, wmax, warp, lane, n_ov, n_hit, K);
     }
-    pair_run<TA_BOTH, TB_DYN, MODE, true>(L, sq, sqf, ja, jb, r, c32, wmin_te, wmax, W, lane, n_ov, n_hit, K);
+    range_run<TA_BOTH, TB_DYN, MODE, true>(sq, sqf, ja, jb, r, c32, wmin_te, wmax, warp, lane, n_ov, n_hit, K);
     if (r_bisect) {
         // overlap <=> cts <= r.te; cts ascending over the tile
 #pragma unroll
         for (int k = 0; k < K1_CPT; ++k)
             n_ov += (unsigned)(clampi(upper_bound_ts(sq, nt, r[k].te), jb, jhi) - jb);
-        pair_run<TA_R, TB_C, MODE, false>(L, sq, sqf, jb, jhi, r, c32, wmin_te, wmax, W, lane, n_ov, n_hit, K);
+        range_run<TA_R, TB_C, MODE, false>(sq, sqf, jb, jhi, r, c32, wmin_te, wmax, warp, lane, n_ov, n_hit, K);
     } else {
-        pair_run<TA_R, TB_DYN, MODE, true>(L, sq, sqf, jb, jhi, r, c32, wmin_te, wmax, W, lane, n_ov, n_hit, K);
+        range_run<TA_R, TB_DYN, MODE, true>(sq, sqf, jb, jhi, r, c32, wmin_te, wmax, warp, lane, n_ov, n_hit, K);
     }
 }
 
@@ -607,28 +663,20 @@ __global__ void __launch_bounds__(K1_THREADS, F32 ? K1_MIN_BLOCKS_F32 : K1_MIN_B
     __shared__ ItemCtx it_sh;
     __shared__ int64_t item_sh;
     __shared__ unsigned long long red_ov, red_hit;
-    extern __shared__ __align__(16) unsigned char k1_dyn[];  // per-warp rare-path state
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    __shared__ FlushCfg fcfg;
     if (tid == 0) {
-        fcfg.hit_count = L.hit_count;
-        fcfg.keys = L.keys;
-        fcfg.tbeg = L.tbeg;
-        fcfg.tend = L.tend;
-        fcfg.cap = L.cap;
-        fcfg.d2 = L.d2;
-        fcfg.minor_bits = L.minor_bits;
-        fcfg.query_major = L.query_major;
+        k1_fcfg.hit_count = L.hit_count;
+        k1_fcfg.keys = L.keys;
+        k1_fcfg.tbeg = L.tbeg;
+        k1_fcfg.tend = L.tend;
+        k1_fcfg.cap = L.cap;
+        k1_fcfg.d2 = L.d2;
+        k1_fcfg.minor_bits = L.minor_bits;
+        k1_fcfg.query_major = L.query_major;
     }
-    WarpRare W;
-    W.cfg = &fcfg;
-    // dynamic shared memory: FP32 query records, then per-warp rare-path state
-    QF32 *sqf = reinterpret_cast<QF32 *>(k1_dyn);
-    unsigned char *rare_base = k1_dyn + sizeof(QF32) * K1_TQ;
-    W.cs = reinterpret_cast<CandRec *>(rare_base) + (size_t)warp * 32 * K1_CPT;
-    W.q = reinterpret_cast<uint32_t *>(rare_base + sizeof(CandRec) * 32 * K1_CPT * K1_WARPS) +
-          (size_t)warp * K1_QCAP;
+    QF32 *const sqf = k1_sqf();
+    CandRec *const wcs = warp_cs(warp);
     const int64_t total = L.plan.meta[0];
     const int sub = (int)L.plan.meta[1];
     const int64_t tqs = L.plan.meta[2];  // query tile size chosen by k_plan_items (<= K1_TQ)
@@ -799,7 +847,7 @@ __global__ void __launch_bounds__(K1_THREADS, F32 ? K1_MIN_BLOCKS_F32 : K1_MIN_B
                 const bool valid = e <= it.c_hi;
                 // stage the exact record for the rare path (queued pairs are
                 // evaluated from here); the filter view stays in registers
-                CandRec &cr = W.cs[k * 32 + lane];
+                CandRec &cr = wcs[k * 32 + lane];
                 if (valid) {
                     r[k].ts = L.e.ts[e]; r[k].te = L.e.te[e];
                     r[k].sx = L.e.sx[e]; r[k].sy = L.e.sy[e]; r[k].sz = L.e.sz[e];
@@ -837,7 +885,7 @@ __global__ void __launch_bounds__(K1_THREADS, F32 ? K1_MIN_BLOCKS_F32 : K1_MIN_B
                 }
             }
             // key of (b, e_off of the warp's candidate 0, q_off = it.q0) without the j term
-            W.key_base0 = make_key(L, it.b, wbase - L.plan.first[it.b], it.q0);
+            if (lane == 0) k1_wctx[warp].key_base0 = make_key(L, it.b, wbase - L.plan.first[it.b], it.q0);
             __syncwarp();
             if (L.noop) continue;
             if (!__any_sync(0xffffffffu, valid_any)) continue;
@@ -846,6 +894,10 @@ __global__ void __launch_bounds__(K1_THREADS, F32 ? K1_MIN_BLOCKS_F32 : K1_MIN_B
             wmax = warp_max(wmax);
             wmin_te = warp_min(wmin_te);
             wmax_ts = warp_max(wmax_ts);
+            if (lane == 0) {
+                k1_wctx[warp].wmin_te = wmin_te;
+                k1_wctx[warp].wmax = wmax;
+            }
             int jlo = 0, jhi = it.nt, ja = it.nt, jb = it.nt;
             if (!*L.q_unsorted) {
                 jlo = lower_bound_pm(pm, it.nt, wmin);   // running max te >= min ts
@@ -864,17 +916,17 @@ __global__ void __launch_bounds__(K1_THREADS, F32 ? K1_MIN_BLOCKS_F32 : K1_MIN_B
             const bool c_tb_r = jlo < ja && pm[ja - 1] < wmin_te;
             const bool r_tb_c = jb < jhi && sm[jb] > wmax;
             if (slow) {
-                pair_run<TA_C, TB_DYN, K1_ALL, true>(L, sq, sqf, jlo, ja, r, c32, wmin_te, wmax, W, lane, n_ov, n_hit, K);
-                pair_run<TA_BOTH, TB_DYN, K1_ALL, true>(L, sq, sqf, ja, jb, r, c32, wmin_te, wmax, W, lane, n_ov, n_hit, K);
-                pair_run<TA_R, TB_DYN, K1_ALL, true>(L, sq, sqf, jb, jhi, r, c32, wmin_te, wmax, W, lane, n_ov, n_hit, K);
+                pair_run<TA_C, TB_DYN, K1_ALL, true>(sq, sqf, jlo, ja, r, c32, wmin_te, wmax, warp, lane, n_ov, n_hit, K);
+                pair_run<TA_BOTH, TB_DYN, K1_ALL, true>(sq, sqf, ja, jb, r, c32, wmin_te, wmax, warp, lane, n_ov, n_hit, K);
+                pair_run<TA_R, TB_DYN, K1_ALL, true>(sq, sqf, jb, jhi, r, c32, wmin_te, wmax, warp, lane, n_ov, n_hit, K);
                 continue;
             }
             if (F32)
                 run_cases<K1_F32>(L, sq, sqf, it.nt, jlo, ja, jb, jhi, c_tb_r && te_sorted, r_tb_c, r, c32,
-                                  wmin_te, wmax, W, lane, n_ov, n_hit, K);
+                                  wmin_te, wmax, warp, lane, n_ov, n_hit, K);
             else
                 run_cases<K1_F64>(L, sq, sqf, it.nt, jlo, ja, jb, jhi, c_tb_r && te_sorted, r_tb_c, r, c32,
-                                  wmin_te, wmax, W, lane, n_ov, n_hit, K);
+                                  wmin_te, wmax, warp, lane, n_ov, n_hit, K);
         }
         // per-batch counters (64-bit)
         for (int o = 16; o; o >>= 1) {
