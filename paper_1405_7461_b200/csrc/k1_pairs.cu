@@ -41,7 +41,7 @@
 #define K1_MIN_BLOCKS (K1_CPT == 1 ? 3 : 2)
 #endif
 #ifndef K1_MIN_BLOCKS_F32
-#define K1_MIN_BLOCKS_F32 2
+#define K1_MIN_BLOCKS_F32 3
 #endif
 
 namespace tsk {
@@ -281,11 +281,8 @@ __device__ __forceinline__ bool pair_eval(const Cand &r, const QVals &Q, uint32_
     return ta == tb || dq >= -0x1p-1000 || !no_overflow(aa, dot, e);
 }
 
-// Per-warp shared state for the rare path: the warp's 32*K1_CPT candidates
-// staged in shared memory and a queue of flagged (candidate, query) pairs.
-struct CandRec {
-    double ts, te, rcp, sx, sy, sz, dx, dy, dz, ex, ey, ez;
-};
+// Per-warp shared state for the rare path: a queue of flagged
+// (candidate, query) pairs.
 constexpr int K1_WARPS = K1_THREADS / 32;
 // Queue entries per warp.  A query iteration starts with fewer than 32
 // queued and appends at most 32 * K1_CPT.
@@ -294,6 +291,9 @@ constexpr int K1_QCAP = 32 * (K1_CPT + 1);
 // Output and key layout for the (non-inlined) flush, kept in shared memory
 // so the hot loop does not hold them in registers.
 struct FlushCfg {
+    // entry columns the exact path reads (queued candidates are re-read from
+    // global memory / L2: the rare path is rare)
+    const double *ts, *te, *rcp, *sx, *sy, *sz, *dx, *dy, *dz, *ex, *ey, *ez;
     unsigned long long *hit_count;
     uint64_t *keys;
     double *tbeg, *tend;
@@ -302,11 +302,11 @@ struct FlushCfg {
     int minor_bits, query_major;
 };
 
-__device__ __forceinline__ Cand cand_exact(const CandRec &cr) {
+__device__ __forceinline__ Cand cand_exact(const FlushCfg &C, int64_t e) {
     Cand r;
-    r.ts = cr.ts; r.te = cr.te; r.rcp = cr.rcp; r.ext = __dsub_rn(cr.te, cr.ts);
-    r.sx = cr.sx; r.sy = cr.sy; r.sz = cr.sz; r.dx = cr.dx; r.dy = cr.dy; r.dz = cr.dz;
-    r.ex = cr.ex; r.ey = cr.ey; r.ez = cr.ez;
+    r.ts = C.ts[e]; r.te = C.te[e]; r.rcp = C.rcp[e]; r.ext = __dsub_rn(r.te, r.ts);
+    r.sx = C.sx[e]; r.sy = C.sy[e]; r.sz = C.sz[e]; r.dx = C.dx[e]; r.dy = C.dy[e]; r.dz = C.dz[e];
+    r.ex = C.ex[e]; r.ey = C.ey[e]; r.ez = C.ez[e];
     return r;
 }
 
@@ -322,6 +322,8 @@ struct __align__(16) QF32 {
 struct WarpCtx {
     uint64_t key_base0;     // key of (b, e_off of candidate 0, it.q0) without the j term
     double wmin_te, wmax;   // min te / max te of the warp's candidates (tb cases)
+    int64_t wbase;          // entry ordinal of the warp's candidate 0
+    int nvalid;             // valid candidates of the warp (the rest are past the item)
 };
 
 // Block-shared state of K1 (both kernels): the flush configuration, the
@@ -333,12 +335,8 @@ __shared__ WarpCtx k1_wctx[K1_WARPS];
 extern __shared__ __align__(16) unsigned char k1_dyn[];
 
 __device__ __forceinline__ QF32 *k1_sqf() { return reinterpret_cast<QF32 *>(k1_dyn); }
-__device__ __forceinline__ CandRec *warp_cs(int warp) {
-    return reinterpret_cast<CandRec *>(k1_dyn + sizeof(QF32) * K1_TQ) + warp * 32 * K1_CPT;
-}
 __device__ __forceinline__ uint32_t *warp_q(int warp) {
-    return reinterpret_cast<uint32_t *>(k1_dyn + sizeof(QF32) * K1_TQ + sizeof(CandRec) * 32 * K1_CPT * K1_WARPS) +
-           warp * K1_QCAP;
+    return reinterpret_cast<uint32_t *>(k1_dyn + sizeof(QF32) * K1_TQ) + warp * K1_QCAP;
 }
 
 __device__ __forceinline__ void append_hit_w(const FlushCfg &C, bool hit, uint64_t key, double tb,
@@ -367,17 +365,18 @@ __device__ __noinline__ void rare_flush(const QRec *__restrict__ sq, int warp, i
                                         unsigned &n_hit) {
     const FlushCfg &C = k1_fcfg;
     const double d2 = C.d2;
-    const CandRec *cs = warp_cs(warp);
     const uint32_t *wq = warp_q(warp);
     const double wmin_te = k1_wctx[warp].wmin_te, wmax_te = k1_wctx[warp].wmax;
     Hit h;
     h.hit = false;
     h.tb = h.te = 0.0;
     uint64_t key = 0;
-    if (lane < n_items) {
-        const uint32_t ent = wq[lane];
-        const int ci = (int)(ent >> 16), j = (int)(ent & 0xffffu);
-        const Cand r = cand_exact(cs[ci]);
+    const uint32_t ent = lane < n_items ? wq[lane] : 0u;
+    const int ci = (int)(ent >> 16), j = (int)(ent & 0xffffu);
+    // candidates past the item's range can be queued (flagged with a huge
+    // threshold) but are not pairs of this item
+    if (lane < n_items && ci < k1_wctx[warp].nvalid) {
+        const Cand r = cand_exact(C, k1_wctx[warp].wbase + ci);
         const uint32_t qa = (uint32_t)__cvta_generic_to_shared(sq) + (uint32_t)j * (uint32_t)sizeof(QRec);
         const QVals Q = load_q(qa);
         double cc, aa, dot, e;
@@ -582,24 +581,91 @@ __device__ __forceinline__ double warp_max(double v) {
     return v;
 }
 
-// FP32 ranges run in their own (non-inlined) function: the caller's item
-// and sub-tile state is saved around the call once per range, and the inner
-// loop gets the register file to itself (inlined, it spilled the FP32
-// candidates to local memory).
-static_assert(K1_CPT == 2, "f32_range passes two candidates by value");
-template <int TA, int TB, bool CNT>
-__device__ __noinline__ uint2 f32_range(const QRec *__restrict__ sq, const QF32 *__restrict__ sqf, int j0,
-                                        int j1, CandF32 c0, CandF32 c1, double ts0, double te0, double ts1,
-                                        double te1, int warp, int lane) {
-    CandF r[K1_CPT];
-    r[0].ts = ts0; r[0].te = te0;
-    r[1].ts = ts1; r[1].te = te1;
+// The FP32 inner loop is a leaf function (no calls, so nothing has to be
+// saved around one and it gets clean registers): it scans queries from qa
+// until 32 or more flags are queued or the range ends, and returns
+// (qa, queued, overlaps).  The caller flushes and resumes.
+static_assert(K1_CPT == 2, "f32_scan takes two candidates by value");
+template <int TA, bool CNT>
+__device__ __noinline__ uint4 f32_scan(uint32_t qa, uint32_t qa_end, uint32_t base, int qn, CandF32 c0,
+                                       CandF32 c1, double ts0, double te0, double ts1, double te1, int warp,
+                                       int lane) {
+    uint32_t *const wq = warp_q(warp);
     const CandF32 c32[K1_CPT] = {c0, c1};
-    FilterK K;  // unused in FP32 mode
-    K.d2 = K.k5 = K.kc = K.t0 = K.km = 0.0;
-    unsigned ov = 0, hit = 0;
-    pair_run<TA, TB, K1_F32, CNT>(sq, sqf, j0, j1, r, c32, 0.0, 0.0, warp, lane, ov, hit, K);
-    return make_uint2(ov, hit);
+    const double rts[K1_CPT] = {ts0, ts1}, rte[K1_CPT] = {te0, te1};
+    unsigned n_ov = 0;
+    for (; qa < qa_end; qa += (uint32_t)sizeof(QF32)) {
+        float qts, qx, qy, qz, qa4, qb4, p0, p1;
+        lds4f(qa, qts, qx, qy, qz);
+        lds4f(qa + 16, qa4, qb4, p0, p1);
+        double cts = 0.0, cte = 0.0;
+        if (CNT) lds2(qa + 32, cts, cte);
+        bool cand[K1_CPT];
+#pragma unroll
+        for (int k = 0; k < K1_CPT; ++k) {
+            bool ov = true;
+            if (CNT) {
+                if (TA == TA_C) ov = rts[k] <= cte;
+                else if (TA == TA_R) ov = cts <= rte[k];
+                else ov = rts[k] <= cte && cts <= rte[k];
+                n_ov += ov ? 1u : 0u;
+            }
+            cand[k] = f32_flag(c32[k], qts, qx, qy, qz, qa4, qb4) && ov;
+        }
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < K1_CPT; ++k) any |= cand[k];
+        if (!__any_sync(0xffffffffu, any)) continue;
+        const uint32_t j = (qa - base) / (uint32_t)sizeof(QF32);
+        unsigned lt;
+        asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+#pragma unroll
+        for (int k = 0; k < K1_CPT; ++k) {
+            const unsigned m = __ballot_sync(0xffffffffu, cand[k]);
+            if (cand[k]) wq[qn + __popc(m & lt)] = ((uint32_t)(k * 32 + lane) << 16) | j;
+            qn += __popc(m);
+        }
+        if (qn >= 32) {
+            qa += (uint32_t)sizeof(QF32);
+            break;
+        }
+    }
+    return make_uint4(qa, (unsigned)qn, n_ov, 0u);
+}
+
+// FP32 range: scan, flush 32 at a time, resume.
+template <int TA, int TB, bool CNT>
+__device__ __forceinline__ void f32_range(const QRec *__restrict__ sq, const QF32 *__restrict__ sqf, int j0,
+                                          int j1, const CandF (&r)[K1_CPT], const CandF32 (&c32)[K1_CPT],
+                                          int warp, int lane, unsigned &n_ov, unsigned &n_hit) {
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(sqf);
+    uint32_t qa = base + (uint32_t)j0 * (uint32_t)sizeof(QF32);
+    const uint32_t qa_end = base + (uint32_t)j1 * (uint32_t)sizeof(QF32);
+    uint32_t *const wq = warp_q(warp);
+    int qn = 0;
+    for (;;) {
+        const uint4 o = f32_scan<TA, CNT>(qa, qa_end, base, qn, c32[0], c32[1], r[0].ts, r[0].te, r[1].ts,
+                                          r[1].te, warp, lane);
+        qa = o.x;
+        qn = (int)o.y;
+        n_ov += o.z;
+        const bool done = qa >= qa_end;
+        while (qn >= 32 || (done && qn > 0)) {
+            const int nf = qn < 32 ? qn : 32;
+            __syncwarp();
+            rare_flush<TA, TB, false>(sq, warp, nf, lane, n_hit);
+            __syncwarp();
+            uint32_t mv[K1_CPT];
+#pragma unroll
+            for (int k = 0; k < K1_CPT; ++k) mv[k] = lane + 32 * (k + 1) < qn ? wq[lane + 32 * (k + 1)] : 0u;
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < K1_CPT; ++k)
+                if (lane + 32 * (k + 1) < qn) wq[lane + 32 * k] = mv[k];
+            qn -= nf;
+        }
+        if (done) break;
+    }
 }
 
 template <int TA, int TB, int MODE, bool CNT>
@@ -608,11 +674,7 @@ __device__ __forceinline__ void range_run(const QRec *__restrict__ sq, const QF3
                                           double wmin_te, double wmax, int warp, int lane,
                                           unsigned &n_ov, unsigned &n_hit, const FilterK &K) {
     if (MODE == K1_F32) {
-        if (j0 >= j1) return;
-        const uint2 o = f32_range<TA, TB, CNT>(sq, sqf, j0, j1, c32[0], c32[1], r[0].ts, r[0].te, r[1].ts,
-                                               r[1].te, warp, lane);
-        n_ov += o.x;
-        n_hit += o.y;
+        if (j0 < j1) f32_range<TA, TB, CNT>(sq, sqf, j0, j1, r, c32, warp, lane, n_ov, n_hit);
     } else {
         pair_run<TA, TB, MODE, CNT>(sq, sqf, j0, j1, r, c32, wmin_te, wmax, warp, lane, n_ov, n_hit, K);
     }
@@ -666,6 +728,10 @@ __global__ void __launch_bounds__(K1_THREADS, F32 ? K1_MIN_BLOCKS_F32 : K1_MIN_B
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
+        k1_fcfg.ts = L.e.ts; k1_fcfg.te = L.e.te; k1_fcfg.rcp = L.e.rcp;
+        k1_fcfg.sx = L.e.sx; k1_fcfg.sy = L.e.sy; k1_fcfg.sz = L.e.sz;
+        k1_fcfg.dx = L.e.dx; k1_fcfg.dy = L.e.dy; k1_fcfg.dz = L.e.dz;
+        k1_fcfg.ex = L.e.ex; k1_fcfg.ey = L.e.ey; k1_fcfg.ez = L.e.ez;
         k1_fcfg.hit_count = L.hit_count;
         k1_fcfg.keys = L.keys;
         k1_fcfg.tbeg = L.tbeg;
@@ -676,7 +742,6 @@ __global__ void __launch_bounds__(K1_THREADS, F32 ? K1_MIN_BLOCKS_F32 : K1_MIN_B
         k1_fcfg.query_major = L.query_major;
     }
     QF32 *const sqf = k1_sqf();
-    CandRec *const wcs = warp_cs(warp);
     const int64_t total = L.plan.meta[0];
     const int sub = (int)L.plan.meta[1];
     const int64_t tqs = L.plan.meta[2];  // query tile size chosen by k_plan_items (<= K1_TQ)
@@ -845,17 +910,11 @@ __global__ void __launch_bounds__(K1_THREADS, F32 ? K1_MIN_BLOCKS_F32 : K1_MIN_B
             for (int k = 0; k < K1_CPT; ++k) {
                 const int64_t e = wbase + (int64_t)k * 32 + lane;
                 const bool valid = e <= it.c_hi;
-                // stage the exact record for the rare path (queued pairs are
-                // evaluated from here); the filter view stays in registers
-                CandRec &cr = wcs[k * 32 + lane];
                 if (valid) {
                     r[k].ts = L.e.ts[e]; r[k].te = L.e.te[e];
                     r[k].sx = L.e.sx[e]; r[k].sy = L.e.sy[e]; r[k].sz = L.e.sz[e];
                     r[k].vx = L.e.vx[e]; r[k].vy = L.e.vy[e]; r[k].vz = L.e.vz[e];
                     r[k].ext = __dsub_rn(r[k].te, r[k].ts);
-                    cr.rcp = L.e.rcp[e];
-                    cr.dx = L.e.dx[e]; cr.dy = L.e.dy[e]; cr.dz = L.e.dz[e];
-                    cr.ex = L.e.ex[e]; cr.ey = L.e.ey[e]; cr.ez = L.e.ez[e];
                     unsafe_r |= L.e.unsafe[e] != 0;
                     wmin = fmin(wmin, r[k].ts);
                     wmax = fmax(wmax, r[k].te);
@@ -865,12 +924,8 @@ __global__ void __launch_bounds__(K1_THREADS, F32 ? K1_MIN_BLOCKS_F32 : K1_MIN_B
                     r[k].ts = INFINITY; r[k].te = -INFINITY; r[k].ext = 1.0;
                     r[k].sx = r[k].sy = r[k].sz = 0.0;
                     r[k].vx = r[k].vy = r[k].vz = 0.0;
-                    cr.rcp = 1.0;
-                    cr.dx = cr.dy = cr.dz = cr.ex = cr.ey = cr.ez = 0.0;
                 }
                 valid_any |= valid;
-                cr.ts = r[k].ts; cr.te = r[k].te;
-                cr.sx = r[k].sx; cr.sy = r[k].sy; cr.sz = r[k].sz;
             }
             CandF32 c32[K1_CPT];
             if (item_f32) {
@@ -885,7 +940,12 @@ __global__ void __launch_bounds__(K1_THREADS, F32 ? K1_MIN_BLOCKS_F32 : K1_MIN_B
                 }
             }
             // key of (b, e_off of the warp's candidate 0, q_off = it.q0) without the j term
-            if (lane == 0) k1_wctx[warp].key_base0 = make_key(L, it.b, wbase - L.plan.first[it.b], it.q0);
+            if (lane == 0) {
+                k1_wctx[warp].key_base0 = make_key(L, it.b, wbase - L.plan.first[it.b], it.q0);
+                k1_wctx[warp].wbase = wbase;
+                const int64_t nv = it.c_hi - wbase + 1;
+                k1_wctx[warp].nvalid = nv < 0 ? 0 : (nv > 32 * K1_CPT ? 32 * K1_CPT : (int)nv);
+            }
             __syncwarp();
             if (L.noop) continue;
             if (!__any_sync(0xffffffffu, valid_any)) continue;
@@ -947,7 +1007,7 @@ __global__ void __launch_bounds__(K1_THREADS, F32 ? K1_MIN_BLOCKS_F32 : K1_MIN_B
 }
 
 static size_t k1_dyn_smem() {
-    return sizeof(QF32) * K1_TQ + (sizeof(CandRec) * 32 * K1_CPT + sizeof(uint32_t) * K1_QCAP) * K1_WARPS;
+    return sizeof(QF32) * K1_TQ + sizeof(uint32_t) * K1_QCAP * K1_WARPS;
 }
 
 // The dynamic shared-memory limit is a per-device function attribute.
