@@ -1,0 +1,413 @@
+// k1_f32.cu — K1, the moving-distance pair kernel (GPUTrajDistSearch), with
+// the FP32 pre-filter: the common path of every launch whose coordinates
+// and threshold are below 2^60 (k1_pairs.cu serves the rest).
+//
+// Replaces core.pair_intervals (/root/reference/pkg/src/trajseek/core.py:464-565)
+// driven by engine.execute_batch/_run_chunks (engine.py:78-148) for every
+// batch of a plan at once.
+//
+// Work decomposition.  A work item is (batch b, candidate tile, query tile),
+// claimed from a global counter by a persistent grid.  The query tile is
+// staged in shared memory as 48-byte FP32 pre-filter records (filter.cuh)
+// with the exact start/end times; each lane holds K1F_CPT = 4 candidates
+// (lanes l, l+32, l+64, l+96 of the warp's 128 consecutive entries) in FP32
+// pre-filter form, and each warp loops over the window of staged queries
+// that can overlap any of its candidates (entries and queries are both
+// start-time sorted, so the window is four binary searches, one per lane).
+//
+// Per (candidate, query): 9 FP32 ops and two compares decide "cannot hit"
+// for nearly every pair (f32_flag, with a proven error margin); flagged
+// pairs are queued per warp and re-evaluated 32 at a time with the
+// reference's exact binary64 arithmetic (k1_exact.cuh), which is what makes
+// the result set bit-exact.  Overlaps are counted exactly: by bisection for
+// whole ranges, else with binary64 compares of the exact times.
+#include <atomic>
+
+#include "k1_exact.cuh"
+
+#ifndef K1F_CPT
+#define K1F_CPT 4
+#endif
+#ifndef K1F_MIN_BLOCKS
+#define K1F_MIN_BLOCKS 3
+#endif
+
+namespace tsk {
+
+constexpr int CPT = K1F_CPT;
+constexpr int WCAND = 32 * CPT;         // candidates per warp
+constexpr int QCAP = 32 * (CPT + 1);    // queue entries per warp
+static_assert(WCAND <= 65536, "candidate index must fit the 16-bit queue field");
+
+// Dynamic shared memory: FP32 query records | per-warp queues | per-warp
+// FP32 candidates (structure of arrays, 7 x WCAND floats per warp).
+extern __shared__ __align__(16) unsigned char k1_dyn[];
+__device__ __forceinline__ QF32 *f_sqf() { return reinterpret_cast<QF32 *>(k1_dyn); }
+__device__ __forceinline__ uint32_t *f_queue(int warp) {
+    return reinterpret_cast<uint32_t *>(k1_dyn + sizeof(QF32) * K1_TQ) + warp * QCAP;
+}
+__device__ __forceinline__ float *f_cands(int warp) {
+    return reinterpret_cast<float *>(k1_dyn + sizeof(QF32) * K1_TQ + sizeof(uint32_t) * QCAP * K1_WARPS) +
+           warp * 7 * WCAND;
+}
+
+__device__ __forceinline__ void lds4f(uint32_t a, float &x, float &y, float &z, float &w) {
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "r"(a));
+}
+__device__ __forceinline__ void lds2d(uint32_t a, double &x, double &y) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a));
+}
+
+// The inner loop, a leaf function (no calls inside, so it gets the register
+// file to itself): loads the warp's FP32 candidates, scans queries from qa
+// until 32 or more flags are queued or the range ends, and returns
+// (qa, queued, overlaps).  The caller flushes and resumes.  CNT: count
+// overlaps per pair with the exact times (read from L2 once per call).
+template <int TA, bool CNT>
+__device__ __noinline__ uint4 f32_scan(uint32_t qa, uint32_t qa_end, uint32_t base, int qn, int warp, int lane) {
+    uint32_t *const wq = f_queue(warp);
+    const float *cs = f_cands(warp);
+    CandF32 c[CPT];
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+        const int i = k * 32 + lane;
+        c[k].px = cs[0 * WCAND + i]; c[k].py = cs[1 * WCAND + i]; c[k].pz = cs[2 * WCAND + i];
+        c[k].vx = cs[3 * WCAND + i]; c[k].vy = cs[4 * WCAND + i]; c[k].vz = cs[5 * WCAND + i];
+        c[k].sr = cs[6 * WCAND + i];
+    }
+    double rts[CPT], rte[CPT];
+    if (CNT) {
+        const int64_t wb = k1_wctx[warp].wbase;
+        const int nv = k1_wctx[warp].nvalid;
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            const int i = k * 32 + lane;
+            rts[k] = i < nv ? k1_fcfg.ts[wb + i] : INFINITY;   // invalid lanes never overlap
+            rte[k] = i < nv ? k1_fcfg.te[wb + i] : -INFINITY;
+        }
+    }
+    unsigned n_ov = 0;
+    for (; qa < qa_end; qa += (uint32_t)sizeof(QF32)) {
+        float qts, qx, qy, qz, qa4, qb4, p0, p1;
+        lds4f(qa, qts, qx, qy, qz);
+        lds4f(qa + 16, qa4, qb4, p0, p1);
+        double cts = 0.0, cte = 0.0;
+        if (CNT) lds2d(qa + 32, cts, cte);
+        bool cand[CPT];
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            bool ov = true;
+            if (CNT) {
+                // TA_C: the query started first, so it overlaps iff it ends at
+                // or after r.ts; TA_R: iff it starts at or before r.te
+                if (TA == TA_C) ov = rts[k] <= cte;
+                else if (TA == TA_R) ov = cts <= rte[k];
+                else ov = rts[k] <= cte && cts <= rte[k];
+                n_ov += ov ? 1u : 0u;
+            }
+            cand[k] = f32_flag(c[k], qts, qx, qy, qz, qa4, qb4) && ov;
+            any |= cand[k];
+        }
+        if (!__any_sync(0xffffffffu, any)) continue;
+        // rare: queue the flagged pairs of this query (qn < 32 on entry)
+        const uint32_t j = (qa - base) / (uint32_t)sizeof(QF32);
+        unsigned lt;
+        asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            const unsigned m = __ballot_sync(0xffffffffu, cand[k]);
+            if (cand[k]) wq[qn + __popc(m & lt)] = ((uint32_t)(k * 32 + lane) << 16) | j;
+            qn += __popc(m);
+        }
+        if (qn >= 32) {
+            qa += (uint32_t)sizeof(QF32);
+            break;
+        }
+    }
+    return make_uint4(qa, (unsigned)qn, n_ov, 0u);
+}
+
+// One (TA, TB) range of the window: scan, flush 32 at a time, resume.
+template <int TA, int TB, bool CNT>
+__device__ __forceinline__ void f32_range(const QRec *__restrict__ qt, const QF32 *__restrict__ sqf, int j0,
+                                          int j1, int warp, int lane, unsigned &n_ov, unsigned &n_hit) {
+    if (j0 >= j1) return;
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(sqf);
+    uint32_t qa = base + (uint32_t)j0 * (uint32_t)sizeof(QF32);
+    const uint32_t qa_end = base + (uint32_t)j1 * (uint32_t)sizeof(QF32);
+    uint32_t *const wq = f_queue(warp);
+    int qn = 0;
+    for (;;) {
+        const uint4 o = f32_scan<TA, CNT>(qa, qa_end, base, qn, warp, lane);
+        qa = o.x;
+        qn = (int)o.y;
+        n_ov += o.z;
+        const bool done = qa >= qa_end;
+        flush_queue<TA, TB, false, CPT>(qt, wq, warp, lane, qn, done, n_hit);
+        if (done) break;
+    }
+}
+
+// Exact path for a whole window (extreme-exponent tiles, items outside the
+// pre-filter's validity): every overlapping pair is queued.
+template <int TA>
+__device__ __forceinline__ void all_range(const QRec *__restrict__ qt, const QF32 *__restrict__ sqf, int j0, int j1,
+                                          const double (&rts)[CPT], const double (&rte)[CPT], int warp, int lane,
+                                          unsigned &n_ov, unsigned &n_hit) {
+    uint32_t *const wq = f_queue(warp);
+    int qn = 0;
+    for (int j = j0; j < j1; ++j) {
+        const double cts = sqf[j].ts64, cte = sqf[j].te64;
+        bool cand[CPT];
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            cand[k] = rts[k] <= cte && cts <= rte[k];
+            n_ov += cand[k] ? 1u : 0u;
+            any |= cand[k];
+        }
+        if (__any_sync(0xffffffffu, any)) {
+            unsigned lt;
+            asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) {
+                const unsigned m = __ballot_sync(0xffffffffu, cand[k]);
+                if (cand[k]) wq[qn + __popc(m & lt)] = ((uint32_t)(k * 32 + lane) << 16) | (uint32_t)j;
+                qn += __popc(m);
+            }
+        }
+        flush_queue<TA, TB_DYN, true, CPT>(qt, wq, warp, lane, qn, j + 1 == j1, n_hit);
+    }
+}
+
+__global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Launch L) {
+    __shared__ double pm[K1_TQ];  // running max of te over the tile
+    __shared__ double sm[K1_TQ];  // suffix min of te over the tile
+    __shared__ double f32b[8];    // per-item magnitude bounds
+    __shared__ F32Item fi_sh;     // the item's FP32 origin and error bound
+    __shared__ ItemCtx it_sh;
+    __shared__ int64_t item_sh;
+    __shared__ int flags_sh;      // bit 0: unsafe query, bit 1: te not sorted
+    __shared__ unsigned long long red_ov, red_hit;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) fill_flush_cfg(L);
+    QF32 *const sqf = f_sqf();
+    float *const wcs = f_cands(warp);
+    const int64_t total = L.plan.meta[0];
+    const int sub = (int)L.plan.meta[1];
+    const int64_t tqs = L.plan.meta[2];  // query tile size chosen by k_plan_items (<= K1_TQ)
+    constexpr int64_t STRIDE = (int64_t)K1_THREADS * CPT;  // candidates per sub-tile
+    const int64_t ct = STRIDE * sub;
+    const double cq = __longlong_as_double((long long)*L.q_cmax_bits);
+    const double cmax = L.db_cmax > cq ? L.db_cmax : cq;
+    // launch-level validity: the FP32 pre-filter needs |coordinates| and d
+    // below 2^60 (and the FP64 filter's window for the exact division)
+    const bool launch_ok = filter_ok(cmax, L.d2) && L.d2 <= 0x1p120 && cmax <= 0x1p60;
+    const double dthr = sqrt(L.d2);  // d (sqrt(RN(d^2)) >= d (1 - 2^-52); the margin covers it)
+
+    for (;;) {
+        if (tid == 0) {
+            const int64_t item = (int64_t)atomicAdd(L.item_counter, 1ull);
+            item_sh = item;
+            if (item < total) it_sh = decode_item(L, item, ct, tqs);
+            red_ov = 0;
+            red_hit = 0;
+            flags_sh = 0;
+        }
+        __syncthreads();
+        if (item_sh >= total) break;
+        const ItemCtx it = it_sh;
+        const QRec *const qt = L.q + it.lo_q;  // the tile's exact records (global; rare path)
+
+        // pass 1 over the tile: flags, and the item's magnitude bounds
+        // relative to (O, T0) = the first query's start (warps 2, 3)
+        {
+            int fl = 0;
+            for (int j = tid; j < it.nt; j += K1_THREADS) {
+                if (qt[j].flag != 0.0) fl |= 1;
+                if (j + 1 < it.nt && qt[j + 1].te < qt[j].te) fl |= 2;
+            }
+            if (fl) atomicOr(&flags_sh, fl);
+            const double ox = qt[0].sx, oy = qt[0].sy, oz = qt[0].sz, t0 = qt[0].ts;
+            if (warp == 2) {
+                double ar = 0.0, tvr = 0.0, vr = 0.0;
+                for (int64_t g = it.first_c / GB_SIZE + lane; g <= it.c_hi / GB_SIZE; g += 32) {
+                    const GBound gb = L.e.gb[g];
+                    ar = fmax(ar, fmax(fmax(fabs(gb.hi[0] - ox), fabs(ox - gb.lo[0])),
+                                       fmax(fmax(fabs(gb.hi[1] - oy), fabs(oy - gb.lo[1])),
+                                            fmax(fabs(gb.hi[2] - oz), fabs(oz - gb.lo[2])))));
+                    tvr = fmax(tvr, fmax(fabs(gb.ts_hi - t0), fabs(t0 - gb.ts_lo)) * gb.vmax);
+                    vr = fmax(vr, gb.vmax);
+                }
+                ar = warp_max(ar);
+                tvr = warp_max(tvr);
+                vr = warp_max(vr);
+                if (lane == 0) {
+                    f32b[0] = ar;
+                    f32b[1] = tvr;
+                    f32b[2] = vr;
+                }
+            } else if (warp == 3) {
+                double aq = 0.0, tq = 0.0, eq = 0.0;
+                for (int j = lane; j < it.nt; j += 32) {
+                    const QRec &q = qt[j];
+                    aq = fmax(aq, fmax(fabs(q.sx - ox), fmax(fabs(q.sy - oy), fabs(q.sz - oz))));
+                    tq = fmax(tq, fabs(q.ts - t0));
+                    eq = fmax(eq, q.ext);
+                }
+                aq = warp_max(aq);
+                tq = warp_max(tq);
+                eq = warp_max(eq);
+                if (lane == 0) {
+                    f32b[3] = aq;
+                    f32b[4] = tq;
+                    f32b[5] = eq;
+                }
+            }
+        }
+        __syncthreads();
+        const bool unsafe_q = flags_sh & 1;
+        const bool te_sorted = !(flags_sh & 2);
+        if (tid == 0) {
+            fi_sh = f32_item(qt[0].sx, qt[0].sy, qt[0].sz, qt[0].ts, f32b[0], f32b[1], f32b[2], f32b[3], f32b[4],
+                             f32b[5], cmax);
+            fi_sh.ok = fi_sh.ok && launch_ok && !unsafe_q;
+        }
+        __syncthreads();
+        const bool item_f32 = fi_sh.ok;
+        // pass 2: the FP32 records (exact times always, for windows and counts)
+        for (int j = tid; j < it.nt; j += K1_THREADS) {
+            const QRec &q = qt[j];
+            QF32 f;
+            if (item_f32) {
+                float v[6];
+                f32_query(q.ts, q.sx, q.sy, q.sz, q.ext, q.dx, q.dy, q.dz, fi_sh, dthr, v);
+                f.ts = v[0]; f.x = v[1]; f.y = v[2]; f.z = v[3]; f.a = v[4]; f.b = v[5];
+            } else {
+                f.ts = f.x = f.y = f.z = f.a = f.b = 0.f;
+            }
+            f.pad0 = f.pad1 = 0.f;
+            f.ts64 = q.ts;
+            f.te64 = q.te;
+            sqf[j] = f;
+        }
+        __syncthreads();
+        te_scans(sqf, it.nt, pm, sm, warp, lane);
+        __syncthreads();
+
+        unsigned n_ov = 0, n_hit = 0;
+        for (int s = 0; s < sub; ++s) {
+            const int64_t base = it.first_c + (int64_t)s * STRIDE;
+            if (base > it.c_hi) break;  // block-uniform
+            const int64_t wbase = base + (int64_t)warp * WCAND;
+            double rts[CPT], rte[CPT];
+            bool valid_any = false, unsafe_r = false;
+            double wmin = INFINITY, wmax = -INFINITY, wmin_te = INFINITY, wmax_ts = -INFINITY;
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) {
+                const int i = k * 32 + lane;
+                const int64_t e = wbase + i;
+                const bool valid = e <= it.c_hi;
+                CandF32 c;
+                c.px = c.py = c.pz = 0x1p60f;  // invalid lanes: far away (and rejected exactly if flagged)
+                c.vx = c.vy = c.vz = c.sr = 0.f;
+                rts[k] = INFINITY;
+                rte[k] = -INFINITY;
+                if (valid) {
+                    rts[k] = L.e.ts[e];
+                    rte[k] = L.e.te[e];
+                    unsafe_r |= L.e.unsafe[e] != 0;
+                    if (item_f32)
+                        c = f32_cand(rts[k], L.e.sx[e], L.e.sy[e], L.e.sz[e], L.e.vx[e], L.e.vy[e], L.e.vz[e], fi_sh);
+                    wmin = fmin(wmin, rts[k]);
+                    wmax = fmax(wmax, rte[k]);
+                    wmin_te = fmin(wmin_te, rte[k]);
+                    wmax_ts = fmax(wmax_ts, rts[k]);
+                }
+                valid_any |= valid;
+                wcs[0 * WCAND + i] = c.px; wcs[1 * WCAND + i] = c.py; wcs[2 * WCAND + i] = c.pz;
+                wcs[3 * WCAND + i] = c.vx; wcs[4 * WCAND + i] = c.vy; wcs[5 * WCAND + i] = c.vz;
+                wcs[6 * WCAND + i] = c.sr;
+            }
+            if (L.noop) continue;
+            if (!__any_sync(0xffffffffu, valid_any)) continue;
+            wmin = warp_min(wmin);
+            wmax = warp_max(wmax);
+            wmin_te = warp_min(wmin_te);
+            wmax_ts = warp_max(wmax_ts);
+            if (lane == 0) {
+                k1_wctx[warp].key_base0 = make_key(L, it.b, wbase - L.plan.first[it.b], it.q0);
+                k1_wctx[warp].wbase = wbase;
+                const int64_t nv = it.c_hi - wbase + 1;
+                k1_wctx[warp].nvalid = nv < 0 ? 0 : (nv > WCAND ? WCAND : (int)nv);
+                k1_wctx[warp].wmin_te = wmin_te;
+                k1_wctx[warp].wmax = wmax;
+            }
+            __syncwarp();
+            const int4 w = warp_window(sqf, pm, it.nt, *L.q_unsorted != 0, wmin, wmax, wmax_ts, lane);
+            const int jlo = w.x, ja = w.y, jb = w.z, jhi = w.w;
+            if (!item_f32 || __any_sync(0xffffffffu, unsafe_r)) {
+                all_range<TA_C>(qt, sqf, jlo, ja, rts, rte, warp, lane, n_ov, n_hit);
+                all_range<TA_BOTH>(qt, sqf, ja, jb, rts, rte, warp, lane, n_ov, n_hit);
+                all_range<TA_R>(qt, sqf, jb, jhi, rts, rte, warp, lane, n_ov, n_hit);
+                continue;
+            }
+            // TA_C range: every query ends before all candidates (running max
+            // < min te) and te is sorted → overlaps counted by bisection
+            if (jlo < ja && pm[ja - 1] < wmin_te && te_sorted) {
+#pragma unroll
+                for (int k = 0; k < CPT; ++k)
+                    n_ov += (unsigned)(ja - clampi(lower_bound_te(sqf, it.nt, rts[k]), jlo, ja));
+                f32_range<TA_C, TB_R, false>(qt, sqf, jlo, ja, warp, lane, n_ov, n_hit);
+            } else {
+                f32_range<TA_C, TB_DYN, true>(qt, sqf, jlo, ja, warp, lane, n_ov, n_hit);
+            }
+            f32_range<TA_BOTH, TB_DYN, true>(qt, sqf, ja, jb, warp, lane, n_ov, n_hit);
+            // TA_R range: every query ends after all candidates (suffix min >
+            // max te) → overlap <=> cts <= r.te, counted by bisection
+            if (jb < jhi && sm[jb] > wmax) {
+#pragma unroll
+                for (int k = 0; k < CPT; ++k)
+                    n_ov += (unsigned)(clampi(upper_bound_ts(sqf, it.nt, rte[k]), jb, jhi) - jb);
+                f32_range<TA_R, TB_C, false>(qt, sqf, jb, jhi, warp, lane, n_ov, n_hit);
+            } else {
+                f32_range<TA_R, TB_DYN, true>(qt, sqf, jb, jhi, warp, lane, n_ov, n_hit);
+            }
+        }
+        item_counters(L, it.b, n_ov, n_hit, lane, tid, &red_ov, &red_hit);
+    }
+}
+
+static size_t k1f_dyn_smem() {
+    return sizeof(QF32) * K1_TQ + sizeof(uint32_t) * QCAP * K1_WARPS + sizeof(float) * 7 * WCAND * K1_WARPS;
+}
+
+static void k1f_set_attrs() {
+    static std::atomic<uint64_t> done_mask{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(done_mask.load() & bit)) {
+        TSK_CUDA(cudaFuncSetAttribute(k1_pairs_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k1f_dyn_smem()));
+        done_mask.fetch_or(bit);
+    }
+}
+
+int k1f_blocks_per_sm() {
+    k1f_set_attrs();
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k1_pairs_f32, K1_THREADS, k1f_dyn_smem());
+    return n > 0 ? n : 1;
+}
+
+int k1f_candidates_per_thread() { return CPT; }
+
+void launch_k1f(const K1Launch &L, int grid, cudaStream_t st) {
+    k1f_set_attrs();
+    k1_pairs_f32<<<grid, K1_THREADS, k1f_dyn_smem(), st>>>(L);
+    TSK_CUDA(cudaGetLastError());
+}
+
+}  // namespace tsk

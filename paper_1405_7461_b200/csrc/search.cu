@@ -275,9 +275,10 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     }
     SearchPlanDev plan{nb, d_lo, d_hi, d_first, d_last, d_off, d_meta, d_ovl, d_hits};
     launch_ranges(db, db->q, plan, spans_given, st);
-    const int bps = k1_blocks_per_sm(k1_use_f32(d * d, db->cmax));
+    const bool k1_f32 = k1_use_f32(d * d, db->cmax);
+    const int bps = k1_blocks_per_sm(k1_f32);
     const int slots = sm_count(db->device) * bps;
-    launch_plan_items(plan, slots, K1_THREADS * k1_candidates_per_thread(), st);
+    launch_plan_items(plan, slots, K1_THREADS * k1_candidates_per_thread(k1_f32), st);
     launches += spans_given ? 1 : 2;
     tr.mark("ranges+items");
 

@@ -224,8 +224,11 @@ void canonical_perm(int64_t n, const int64_t *qt, const int64_t *qs, const int64
 void permute6(int64_t n, const uint32_t *perm, const int64_t *const in_i[4], const double *const in_f[2],
               int64_t *const out_i[4], double *const out_f[2], cudaStream_t st);
 int k1_blocks_per_sm(bool f32);
+int k1f_blocks_per_sm();
+int k1f_candidates_per_thread();
+void launch_k1f(const K1Launch &L, int grid, cudaStream_t st);
 bool k1_use_f32(double d2, double db_cmax);
-int k1_candidates_per_thread();
+int k1_candidates_per_thread(bool f32);
 
 #ifndef K1_THREADS_DEF
 #define K1_THREADS_DEF 256
