@@ -74,6 +74,7 @@ PLANNERS = {
     "greedy_max": lambda tsk, q, ix: tsk.greedy_max(q, ix, S_BATCH),
 }
 W_DECIDE, W_HIT = 50, 9  # FP64 flops per overlapping pair / extra per hit
+F32_OPS = 12  # FP32 pre-filter ops per evaluated pair (k1_f32.cu / filter.cuh f32_flag)
 
 
 def log(*a):
@@ -353,6 +354,7 @@ def run_ours(args, cfg):
 
     fp64 = _native.probe_fp64(local)
     fp64_peak = max(fp64.values())
+    fp32_peak = _native.probe_fp32(local)
 
     # ── value: queries resident in HBM, hits left in HBM ──
     res = None
@@ -366,7 +368,7 @@ def run_ours(args, cfg):
         if mine is not None:
             res = search_device(store, index, mine, d, queries_resident=True)
     barrier()
-    dev_ms, k1_ms, launches, work, hits, ovl = 0.0, 0.0, 0, 0.0, 0, 0
+    dev_ms, k1_ms, launches, work, hits, ovl, evals = 0.0, 0.0, 0, 0.0, 0, 0, 0
     w0 = time.perf_counter()
     for _ in range(args.steps):
         if mine is None:
@@ -375,6 +377,7 @@ def run_ours(args, cfg):
         dev_ms += r.device_ms
         k1_ms += r.k1_ms
         launches += r.launches
+        evals += r.k1_evals
         o = int(r.per_batch[:, 2].sum())
         ovl += o
         hits += r.n
@@ -416,6 +419,10 @@ def run_ours(args, cfg):
     k1_s = k1_ms / 1e3
     achieved = work / k1_s / 1e12 if k1_s > 0 else 0.0
     peak = fp64_peak / 1e12
+    # the kernel as implemented: FP32 pre-filter ops per evaluated pair
+    # (3 FFMA + 3 FADD separation, 3 norm, 2 threshold, 1 compare) vs the
+    # measured FFMA rate
+    f32_achieved = F32_OPS * evals / k1_s / 1e12 if k1_s > 0 else 0.0
     traffic = None
     prof = os.path.join(ROOT, "profiles", "k1_traffic.json")
     if os.path.exists(prof):
@@ -459,7 +466,7 @@ def run_ours(args, cfg):
                 "planner": args.planner, "plan_s": t_plan,
                 "m": M_BINS, "interactions_per_step": int(total_ints / args.steps),
                 "hits_per_step": int(total_hits / args.steps),
-                "l2": "inputs larger than L2 (entry SoA 112 B/segment resident in HBM)",
+                "l2": "inputs larger than L2 (entry SoA 137 B/segment resident in HBM)",
                 "parallelism": f"dp{world} (contiguous interaction-balanced batch shards; no collective)",
             },
             "response_time_s": t_e2e / args.steps,
@@ -474,6 +481,14 @@ def run_ours(args, cfg):
                 "peak_source": "tsk_probe_fp64 on this GPU in this run (DADD/DMUL/DFMA ops/s); "
                                "MEASURED_PEAKS.json has no FP64 figure",
                 "hbm_bytes_per_step": None,
+            },
+            "kernel_roofline": {
+                "bound": "fp32 issue (K1's FP32 pre-filter)", "kernel": "k1_pairs_f32",
+                "work": f"{F32_OPS} FP32 ops per evaluated (candidate, query) pair",
+                "evaluated_pairs_per_step": int(evals / args.steps),
+                "achieved": f32_achieved, "peak": fp32_peak / 1e12, "unit": "TOP/s",
+                "frac": f32_achieved * 1e12 / fp32_peak if fp32_peak else None,
+                "peak_source": "tsk_probe_fp32 on this GPU in this run (FFMA ops/s, one op per FFMA)",
             },
             "cpu_baseline": cpu,
             "clocks": clocks,

@@ -5,7 +5,7 @@ for v in $VARIANTS; do
   if [ "$lib" = "default" ]; then unset TRAJSEEK_LIB; else export TRAJSEEK_LIB=$(pwd)/$lib; fi
   for cfg in ${CFGS:-c5}; do
     out=$(timeout 900 python bench.py --config $cfg --steps ${STEPS:-3} --warmup 2 --no-cpu-baseline 2>/tmp/err_$name_$cfg.log)
-    echo "$out" | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$name', '$cfg', '%.4g'%d['value'], 'frac %.3f'%d['roofline']['frac'], 'e2e %.4g'%d['e2e']['value'], 'ms %.2f'%d['ms_per_step'], 'k1 %.2f'%d['roofline']['k1_ms_per_step'])" || tail -5 /tmp/err_$name_$cfg.log
+    echo "$out" | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$name', '$cfg', '%.4g'%d['value'], 'frac %.3f'%d['roofline']['frac'], 'e2e %.4g'%d['e2e']['value'], 'ms %.2f'%d['ms_per_step'], 'k1 %.2f'%d['roofline']['k1_ms_per_step'], 'kfrac %.3f'%(d.get('kernel_roofline') or {}).get('frac',0))" || tail -5 /tmp/err_$name_$cfg.log
   done
 done
 if [ -n "$NCU" ]; then

@@ -111,6 +111,9 @@ int tsk_result_info(const tsk_result *r, int64_t *n_hits, int64_t *nb, double *d
  * the number of kernels this library launched for the call. */
 int tsk_result_timing(const tsk_result *r, double *device_ms, double *k1_ms, int64_t *launches);
 int tsk_result_per_batch(const tsk_result *r, int64_t *per_batch);
+/* (candidate, query) pairs K1's FP32 pre-filter evaluated in the call (its
+ * work count for the kernel roofline; 0 where the FP64 kernel ran). */
+int tsk_result_k1_evals(const tsk_result *r, int64_t *evals);
 int tsk_result_columns(const tsk_result *r, const int64_t **query_traj, const int64_t **query_seg,
                        const int64_t **entry_traj, const int64_t **entry_seg,
                        const double **t_begin, const double **t_end, const int64_t **query_ord,
@@ -168,6 +171,9 @@ void tsk_pinned_free(void *p);
  * as one op; DFMA counted as one op too) — the roofline denominator of the
  * FP64-bound pair kernel. */
 int tsk_probe_fp64(int device, double *dadd_per_s, double *dmul_per_s, double *dfma_per_s);
+/* Measured FP32 FFMA rate of `device` (ops/s, an FFMA counted as one op) —
+ * the issue roofline of K1's FP32 pre-filter. */
+int tsk_probe_fp32(int device, double *ffma_per_s);
 
 #ifdef __cplusplus
 }

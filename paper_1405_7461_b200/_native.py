@@ -62,6 +62,8 @@ SIGNATURES = {
     "tsk_result_columns": ([_P] + [ctypes.POINTER(_P)] * 8, ctypes.c_int),
     "tsk_result_free": ([_P], None),
     "tsk_probe_fp64": ([ctypes.c_int, _PD, _PD, _PD], ctypes.c_int),
+    "tsk_probe_fp32": ([ctypes.c_int, _PD], ctypes.c_int),
+    "tsk_result_k1_evals": ([_P, _PI64], ctypes.c_int),
     "tsk_plan_setsplit": ([_I64, _PD, _PD, _I64, _PD, _PD, _PI64, _PI64, ctypes.c_int, _I64, _I64,
                            _I64, _PI64, _PI64, _PI64, _PI64, _PI64, _PD], ctypes.c_int),
     "tsk_plan_greedy": ([_I64, _PD, _PD, _I64, _PD, _PD, _PI64, _PI64, ctypes.c_int, _I64, _PI64,
@@ -219,6 +221,9 @@ class Result:
         self.n, self.nb = int(n.value), int(nb.value)
         self.device_ms, self.k1_ms = float(ms.value), float(k1.value)
         self.launches = int(nl.value)
+        ev = _I64()
+        check(lib.tsk_result_k1_evals(handle, ctypes.byref(ev)))
+        self.k1_evals = int(ev.value)  # pairs K1's FP32 pre-filter evaluated
         pb = np.empty((self.nb, 4), dtype=np.int64)
         check(lib.tsk_result_per_batch(handle, pb.ctypes.data_as(_PI64)))
         self.per_batch = pb  # first, last, overlaps, hits
@@ -308,6 +313,15 @@ def probe_fp64(device: int | None = None) -> dict:
     dev = current_device() if device is None else int(device)
     check(lib.tsk_probe_fp64(dev, ctypes.byref(a), ctypes.byref(m), ctypes.byref(f)))
     return {"dadd_per_s": a.value, "dmul_per_s": m.value, "dfma_per_s": f.value}
+
+
+def probe_fp32(device: int | None = None) -> float:
+    """Measured FP32 FFMA rate (ops/s) of a device (tsk_probe_fp32)."""
+    lib = load()
+    f = ctypes.c_double()
+    dev = current_device() if device is None else int(device)
+    check(lib.tsk_probe_fp32(dev, ctypes.byref(f)))
+    return f.value
 
 
 class _Pinned:

@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
     __shared__ ItemCtx it_sh;
     __shared__ int64_t item_sh;
     __shared__ int flags_sh;      // bit 0: unsafe query, bit 1: te not sorted
-    __shared__ unsigned long long red_ov, red_hit;
+    __shared__ unsigned long long red_ov, red_hit, red_ev;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) fill_flush_cfg(L);
@@ -214,6 +214,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
             if (item < total) it_sh = decode_item(L, item, ct, tqs);
             red_ov = 0;
             red_hit = 0;
+            red_ev = 0;
             flags_sh = 0;
         }
         __syncthreads();
@@ -298,6 +299,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
         __syncthreads();
 
         unsigned n_ov = 0, n_hit = 0;
+        unsigned long long n_ev = 0;  // pairs evaluated by the pre-filter (warp-uniform)
         for (int s = 0; s < sub; ++s) {
             const int64_t base = it.first_c + (int64_t)s * STRIDE;
             if (base > it.c_hi) break;  // block-uniform
@@ -354,6 +356,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
                 all_range<TA_R>(qt, sqf, jb, jhi, rts, rte, warp, lane, n_ov, n_hit);
                 continue;
             }
+            n_ev += (unsigned long long)(jhi - jlo) * (unsigned long long)k1_wctx[warp].nvalid;
             // TA_C range: every query ends before all candidates (running max
             // < min te) and te is sorted → overlaps counted by bisection
             if (jlo < ja && pm[ja - 1] < wmin_te && te_sorted) {
@@ -376,7 +379,9 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
                 f32_range<TA_R, TB_DYN, true>(qt, sqf, jb, jhi, warp, lane, n_ov, n_hit);
             }
         }
-        item_counters(L, it.b, n_ov, n_hit, lane, tid, &red_ov, &red_hit);
+        if (lane == 0 && n_ev) atomicAdd(&red_ev, n_ev);
+        item_counters(L, it.b, n_ov, n_hit, lane, tid, &red_ov, &red_hit);  // (its barrier publishes red_ev)
+        if (tid == 0 && red_ev) atomicAdd(L.eval_count, red_ev);
     }
 }
 

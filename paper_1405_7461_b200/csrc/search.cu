@@ -295,6 +295,7 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     L.plan = plan;
     L.item_counter = d_ctr;
     L.hit_count = d_ctr + 1;
+    L.eval_count = d_ctr + 2;
     L.d2 = d * d;  // core.py:527
     // filter margin scale: entry max |coordinate| here, the query one is
     // reduced on the device by qprep and folded in by K1
@@ -306,20 +307,21 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     L.query_major = query_major;
     L.noop = (flags & TSK_NOOP) ? 1 : 0;
     L.q_unsorted = db->counters.as<int>() + 8;
-    unsigned long long h_hits = 0;
+    unsigned long long h_ctr[2] = {0, 0};  // hits, evaluated pairs
+    unsigned long long &h_hits = h_ctr[0];
     float k1_ms = 0.f;
     for (int attempt = 0;; ++attempt) {
         L.cap = cap;
         L.keys = db->recs.as<uint64_t>();
         L.tbeg = reinterpret_cast<double *>(L.keys + cap);
         L.tend = L.tbeg + cap;
-        TSK_CUDA(cudaMemsetAsync(d_ctr, 0, 16, st));
+        TSK_CUDA(cudaMemsetAsync(d_ctr, 0, 24, st));
         TSK_CUDA(cudaMemsetAsync(d_ovl, 0, nbz * 16, st));
         TSK_CUDA(cudaEventRecord(db->ev_k0, st));
         launch_k1(L, slots, st);
         ++launches;
         TSK_CUDA(cudaEventRecord(db->ev_k1, st));
-        TSK_CUDA(cudaMemcpyAsync(&h_hits, d_ctr + 1, 8, cudaMemcpyDeviceToHost, st));
+        TSK_CUDA(cudaMemcpyAsync(h_ctr, d_ctr + 1, 16, cudaMemcpyDeviceToHost, st));
         TSK_CUDA(cudaStreamSynchronize(st));
         tr.mark("k1");
         float ms = 0.f;
@@ -338,6 +340,7 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     res->n = nh;
     res->nb = nb;
     res->k1_ms = k1_ms;
+    res->k1_evals = (int64_t)h_ctr[1];
     // per-batch first/last/ovl/hits are contiguous on the device (d_first .. d_hits
     // are laid out first,last,item_off,meta,ovl,hits): copy first/last and ovl/hits
     size_t pb_got = 0;
@@ -504,6 +507,12 @@ extern "C" int tsk_result_info(const tsk_result *r, int64_t *n_hits, int64_t *nb
     if (n_hits) *n_hits = r->n;
     if (nb) *nb = r->nb;
     if (device_ms) *device_ms = r->device_ms;
+    return TSK_OK;
+}
+
+extern "C" int tsk_result_k1_evals(const tsk_result *r, int64_t *evals) {
+    if (!r || !evals) return fail(TSK_EINVAL, "null argument");
+    *evals = r->k1_evals;
     return TSK_OK;
 }
 

@@ -128,6 +128,7 @@ struct tsk_db {
 struct tsk_result {
     int64_t n = 0, nb = 0;
     double device_ms = 0, k1_ms = 0;
+    int64_t k1_evals = 0;  // pairs K1's FP32 pre-filter evaluated (last attempt)
     int64_t launches = 0;
     int64_t *pb_host = nullptr;      // pinned nb × 4 (first[], last[], ovl[], hits[])
     size_t pb_bytes = 0;
@@ -199,6 +200,7 @@ struct K1Launch {
     SearchPlanDev plan;
     unsigned long long *item_counter;
     unsigned long long *hit_count;
+    unsigned long long *eval_count;  // (candidate, query) pairs the FP32 pre-filter evaluated
     uint64_t *keys;
     double *tbeg, *tend;
     uint64_t cap;
