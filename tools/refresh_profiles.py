@@ -26,7 +26,7 @@ with open(f"{P}/r1_launches_c5_final.txt", "w") as f:
 rd = float(re.search(r"dram__bytes_read.sum\s+([\d.]+) Gbyte", summ).group(1)) * 1e9
 wm = re.search(r"dram__bytes_write.sum\s+([\d.]+) (\w+)", summ)
 wr = float(wm.group(1)) * (1e9 if wm.group(2) == "Gbyte" else 1e6)
-json.dump({"config": "c5", "kernel": "k1_pairs", "dram_bytes_per_launch": int(rd + wr),
+json.dump({"config": "c5", "kernel": "k1_pairs_f32", "dram_bytes_per_launch": int(rd + wr),
            "source": "ncu --set full capture, profiles/r1_k1_c5_final_ncu_full.txt"},
           open(f"{P}/k1_traffic.json", "w"), indent=1)
 for c in ("c1", "c2", "c3", "c4", "c5"):
