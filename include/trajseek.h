@@ -49,7 +49,9 @@ enum {
     TSK_WANT_ORDINALS = 1u << 4, /* also return query/entry ordinals (pair_intervals)            */
     TSK_QUERIES_RESIDENT = 1u << 5,/* reuse the query set uploaded by the previous call on this db */
     TSK_RESULTS_ON_DEVICE = 1u << 6,/* leave hit columns in HBM (no D2H): device-throughput runs */
-    TSK_ORDER_CANONICAL = 1u << 7 /* items in ResultSet.canonical_order (core.py:290-294)        */
+    TSK_ORDER_CANONICAL = 1u << 7,/* items in ResultSet.canonical_order (core.py:290-294)        */
+    TSK_COUNT_ONLY = 1u << 8,    /* per-batch overlap/hit counts only; no result rows (perfmodel) */
+    TSK_OVERLAPS_ONLY = 1u << 9  /* per-batch temporal overlaps only (perfmodel.py:327-343)      */
 };
 
 /* Index extent rules (index.py:26) */

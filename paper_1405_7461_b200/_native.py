@@ -24,6 +24,8 @@ TSK_WANT_ORDINALS = 1 << 4
 TSK_QUERIES_RESIDENT = 1 << 5
 TSK_RESULTS_ON_DEVICE = 1 << 6
 TSK_ORDER_CANONICAL = 1 << 7
+TSK_COUNT_ONLY = 1 << 8
+TSK_OVERLAPS_ONLY = 1 << 9
 TSK_EXTENT_MEMBER, TSK_EXTENT_GRID = 0, 1
 
 _P = ctypes.c_void_p

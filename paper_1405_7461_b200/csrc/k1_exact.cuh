@@ -523,4 +523,19 @@ __device__ __forceinline__ void item_counters(const K1Launch &L, int64_t b, unsi
     __syncthreads();
 }
 
+
+// Temporal overlaps of a lane's candidates with staged queries j0..j1-1
+// (TSK_OVERLAPS_ONLY: the perfmodel's temporal-miss fractions).
+template <int CPT, class R>
+__device__ __forceinline__ unsigned count_overlaps(const R *q, int j0, int j1, const double (&ts)[CPT],
+                                                   const double (&te)[CPT]) {
+    unsigned n = 0;
+    for (int j = j0; j < j1; ++j) {
+        const double cts = rec_ts(q[j]), cte = rec_te(q[j]);
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) n += (ts[k] <= cte && cts <= te[k]) ? 1u : 0u;
+    }
+    return n;
+}
+
 }  // namespace tsk

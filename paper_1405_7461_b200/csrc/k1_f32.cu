@@ -350,6 +350,10 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
             __syncwarp();
             const int4 w = warp_window(sqf, pm, it.nt, *L.q_unsorted != 0, wmin, wmax, wmax_ts, lane);
             const int jlo = w.x, ja = w.y, jb = w.z, jhi = w.w;
+            if (L.overlaps_only) {
+                n_ov += count_overlaps<CPT>(sqf, jlo, jhi, rts, rte);
+                continue;
+            }
             if (!item_f32 || __any_sync(0xffffffffu, unsafe_r)) {
                 all_range<TA_C>(qt, sqf, jlo, ja, rts, rte, warp, lane, n_ov, n_hit);
                 all_range<TA_BOTH>(qt, sqf, ja, jb, rts, rte, warp, lane, n_ov, n_hit);

@@ -265,6 +265,16 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
             }
             __syncwarp();
             const int4 w = warp_window(sq, pm, it.nt, *L.q_unsorted != 0, wmin, wmax, wmax_ts, lane);
+            if (L.overlaps_only) {
+                double ts[K1_CPT], te[K1_CPT];
+#pragma unroll
+                for (int k = 0; k < K1_CPT; ++k) {
+                    ts[k] = r[k].ts;
+                    te[k] = r[k].te;
+                }
+                n_ov += count_overlaps<K1_CPT>(sq, w.x, w.w, ts, te);
+                continue;
+            }
             const bool slow = launch_exact || unsafe_q || __any_sync(0xffffffffu, unsafe_r);
             // tb case of a whole range: every query of the TA_C range ends
             // before all candidates (running max < min te), or every query of

@@ -306,12 +306,15 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     L.minor_bits = minor_bits;
     L.query_major = query_major;
     L.noop = (flags & TSK_NOOP) ? 1 : 0;
+    L.overlaps_only = (flags & TSK_OVERLAPS_ONLY) ? 1 : 0;
+    // counts only: no hit rows are written (cap 0), so no regrow and no K4
+    const bool count_only = flags & (TSK_COUNT_ONLY | TSK_OVERLAPS_ONLY);
     L.q_unsorted = db->counters.as<int>() + 8;
     unsigned long long h_ctr[2] = {0, 0};  // hits, evaluated pairs
     unsigned long long &h_hits = h_ctr[0];
     float k1_ms = 0.f;
     for (int attempt = 0;; ++attempt) {
-        L.cap = cap;
+        L.cap = count_only ? 0 : cap;
         L.keys = db->recs.as<uint64_t>();
         L.tbeg = reinterpret_cast<double *>(L.keys + cap);
         L.tend = L.tbeg + cap;
@@ -327,14 +330,14 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
         float ms = 0.f;
         cudaEventElapsedTime(&ms, db->ev_k0, db->ev_k1);
         k1_ms += ms;
-        if (h_hits <= cap) break;
+        if (count_only || h_hits <= cap) break;
         TSK_REQUIRE(attempt < 3, "result buffer kept overflowing");
         // overflow-safe sizing: grow to the exact count and rerun K1
         db->recs.reserve((size_t)h_hits * 24 + 24 * 1024, st);
         cap = db->recs.bytes / 24;
     }
-    TSK_REQUIRE(h_hits < (1ull << 32), "more than 2^32 hits in one call");
-    const int64_t nh = (int64_t)h_hits;
+    TSK_REQUIRE(count_only || h_hits < (1ull << 32), "more than 2^32 hits in one call");
+    const int64_t nh = count_only ? 0 : (int64_t)h_hits;
 
     tsk_result *res = new tsk_result();
     res->n = nh;

@@ -211,6 +211,7 @@ struct K1Launch {
     int major_bits, minor_bits;  // key = b << (major+minor) | major << minor | minor
     int query_major;             // 0: (b, entry, query); 1: (b, query, entry)
     int noop;
+    int overlaps_only;  // count temporal overlaps only (no geometry, no hits)
     const int *q_unsorted;  // device flag: query start times not sorted -> no windows
 };
 

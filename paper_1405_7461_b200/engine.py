@@ -244,3 +244,37 @@ def launch_overhead_pass(store: SegmentStore, batch: SegmentStore, span: tuple[i
     """Wall seconds of a batch launch with the pair arithmetic elided."""
     _, stats = execute_batch(store, batch, span, 0.0, workers=workers, _noop=True)
     return stats.kernel_seconds
+
+
+# ── counting passes (perfmodel on the GPU) ──────────────────────────────────
+
+
+def plan_counts(store: SegmentStore, index: TemporalIndex, plan: BatchPlan, d: float, *,
+                overlaps_only: bool = False) -> np.ndarray:
+    """Per-batch (first, last, overlaps, hits) of ``plan`` without result rows.
+
+    One fused launch (K3 spans, K1 with no hit rows written).  With
+    ``overlaps_only`` K1 skips the geometry and only counts temporally
+    overlapping pairs, so ``interactions - overlaps`` is the reference's
+    temporal-miss count (perfmodel.py:327-343); hits are then 0.
+    """
+    lo, hi = plan.table()
+    dev = index.ensure_device(None, 0, store)
+    flags = _native.TSK_OVERLAPS_ONLY if overlaps_only else _native.TSK_COUNT_ONLY
+    return _native.search(dev, plan.queries, lo, hi, None, None, d, flags).per_batch
+
+
+def span_counts(store: SegmentStore, queries: SegmentStore, lo, hi, first, last, d: float, *,
+                overlaps_only: bool = False) -> np.ndarray:
+    """Per-batch (first, last, overlaps, hits) for explicit batches and spans.
+
+    Batches ``lo[k]..hi[k]`` of ``queries`` (they may overlap each other)
+    against candidate ordinals ``first[k]..last[k]``, all in one launch.
+    """
+    lo = np.ascontiguousarray(lo, dtype=np.int64)
+    if lo.shape[0] == 0:
+        return np.empty((0, 4), dtype=np.int64)
+    flags = _native.TSK_SPANS_GIVEN | (_native.TSK_OVERLAPS_ONLY if overlaps_only else _native.TSK_COUNT_ONLY)
+    return _native.search(store.device(), queries, lo, np.ascontiguousarray(hi, dtype=np.int64),
+                          np.ascontiguousarray(first, dtype=np.int64),
+                          np.ascontiguousarray(last, dtype=np.int64), d, flags).per_batch

@@ -1,0 +1,215 @@
+"""perfmodel drop-in against the reference's own outputs.
+
+Golden vectors: tests/golden/make_golden_perfmodel.py runs the reference
+perfmodel (/root/reference/pkg/src/trajseek/perfmodel.py).  Host arithmetic
+(power-law fit, surface lookup, model documents) is checked on the CPU; the
+GPU-backed parts (hit-rate sampling, temporal-miss fractions, mixes,
+predictions) under ``-m gpu`` — all bit-exact.  Calibration measures this
+GPU, so its tests are structural.
+"""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+import paper_1405_7461_b200 as tsk
+from paper_1405_7461_b200 import datagen, perfmodel as pm
+from paper_1405_7461_b200.core import DomainError, FormatError, TimeInterval
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+Z = np.load(os.path.join(HERE, "golden", "perfmodel.npz"))
+DOC = os.path.join(HERE, "golden", "perfmodel_doc.txt")
+
+# tests/golden/make_golden_perfmodel.py SCENES
+SCENES = {
+    "small": (("uniform", 6, 3, 150), 60, ("uniform", 6, 8, 150), (2, 11), 20.0, 10, 8, 0),
+    "c1": (("uniform", 200, 1, 100), 200, ("uniform", 100, 2, 100), (10, 3), 5.0, 20, 10, 5),
+}
+SURF = ("all_hit", "temporal_miss", "spatial_miss", "launch")
+
+
+def _surfaces():
+    return pm.BenchSurfaces(Z["sf_q"], Z["sf_c"], *(Z[f"sf_{n}"] for n in SURF), 3)
+
+
+def _host():
+    return pm.HostOverheadModel(1000, 1e-3, 5e-3, -0.7, 1e-9)
+
+
+def _profile(name):
+    meta = Z[f"hr_{name}_meta"]
+    epochs = tuple(pm.EpochRate(TimeInterval(float(b[0]), float(b[1])), float(r), bool(s))
+                   for b, r, s in zip(Z[f"hr_{name}_bounds"], Z[f"hr_{name}_rates"], Z[f"hr_{name}_sampled"]))
+    return pm.HitRateProfile(float(meta[0]), float(meta[1]), float(meta[2]), int(meta[3]), epochs,
+                             float(meta[4]), int(meta[5]), bool(meta[6]))
+
+
+# ── host arithmetic (CPU) ───────────────────────────────────────────────────
+
+
+@pytest.mark.parametrize("k", range(6))
+def test_fit_power_law_matches_reference_bit_for_bit(k):
+    f = pm.fit_power_law(Z[f"fit{k}_s"], Z[f"fit{k}_t"])
+    got = np.array([f.offset, f.scale, f.exponent, f.rss, float(f.degenerate)])
+    assert np.array_equal(got, Z[f"fit{k}_out"]), (got, Z[f"fit{k}_out"])
+
+
+@pytest.mark.parametrize("s,t", [([1.0, 2.0], [1.0, 2.0]), ([1.0, 1.0, 1.0, 1.0], [1.0, 2.0, 3.0, 4.0]),
+                                 ([0.0, 1.0, 2.0], [1.0, 2.0, 3.0]), ([-1.0, 1.0, 2.0], [1.0, 2.0, 3.0]),
+                                 ([1.0, 2.0, 3.0], [1.0, 2.0])])
+def test_fit_power_law_rejects_bad_samples(s, t):
+    with pytest.raises(DomainError):
+        pm.fit_power_law(s, t)
+
+
+def test_surface_lookup_matches_reference():
+    sf = _surfaces()
+    for name in SURF:
+        got = np.array([sf.lookup(name, a, b) for a, b in zip(Z["lk_i"], Z["lk_c"])])
+        assert np.array_equal(got, Z[f"lk_{name}"]), name
+    # exact at grid points, clamped outside
+    assert sf.lookup("all_hit", sf.q_axis[3] * sf.c_axis[2], sf.c_axis[2]) == sf.all_hit[3, 2]
+    assert sf.lookup("launch", 1e12, 1e9) == sf.launch[-1, -1]
+
+
+def test_surface_and_grid_validation():
+    with pytest.raises(DomainError):
+        _surfaces().lookup("bogus", 1.0, 1.0)
+    with pytest.raises(DomainError):
+        _surfaces().lookup("all_hit", 1.0, 0.0)
+    with pytest.raises(DomainError):
+        _surfaces().lookup("all_hit", -1.0, 4.0)
+    with pytest.raises(DomainError):
+        pm.SurfaceGrid((1, 1), (2, 3))
+    with pytest.raises(DomainError):
+        pm.default_grid(10, 16)
+    g = pm.default_grid(5000)
+    assert g.q_axis == pm.DEFAULT_QUERY_AXIS and np.array_equal(np.asarray(g.c_axis, float), Z["sf_c"])
+    bad = np.zeros((2, 3))
+    with pytest.raises(DomainError):
+        pm.BenchSurfaces(np.array([1.0, 2.0]), np.array([1.0, 2.0]), bad, bad, bad, bad, 0)
+
+
+def test_host_model_and_profile_rules():
+    h = _host()
+    assert h.evaluate(8, 1000.0) == 1e-3 + 5e-3 * 8.0 ** -0.7 + 1e-9 * 1000.0
+    for kw in ({"scale": 0.0}, {"exponent": 0.1}, {"transfer_per_byte": -1.0}, {"item_bytes": 0}):
+        args = dict(n_queries=10, offset=0.0, scale=1.0, exponent=-0.5, transfer_per_byte=0.0)
+        args.update(kw)
+        with pytest.raises(DomainError):
+            pm.HostOverheadModel(**args)
+    models = (pm.HostOverheadModel(10, 0.0, 1.0, -0.5, 0.0), pm.HostOverheadModel(1000, 0.0, 1.0, -0.5, 0.0))
+    assert pm.nearest_host_model(models, 400).n_queries == 10
+    assert pm.nearest_host_model(models, 700).n_queries == 1000
+    with pytest.raises(DomainError):
+        pm.nearest_host_model((), 5)
+    p = _profile("c1")
+    assert p.rate_at(p.t0 - 100.0) == p.epochs[0].rate and p.rate_at(p.t_max + 100.0) == p.epochs[-1].rate
+    with pytest.raises(DomainError):
+        pm.InteractionMix(0.5, 0.6, -0.1, False)
+
+
+def test_save_model_is_byte_identical_to_the_reference(tmp_path):
+    model = pm.PerfModel(_surfaces(), _profile("c1"),
+                         (_host(), pm.HostOverheadModel(10, 2e-4, 1e-3, -0.5, 2e-9)))
+    path = tmp_path / "m.txt"
+    pm.save_model(model, str(path))
+    assert path.read_bytes() == open(DOC, "rb").read()
+    back = pm.load_model(DOC)
+    assert back.profile == model.profile and back.host_models == model.host_models
+    for n in SURF:
+        assert np.array_equal(getattr(back.surfaces, n), getattr(model.surfaces, n))
+    partial = tmp_path / "p.txt"
+    pm.save_model(pm.PerfModel(profile=model.profile), str(partial))
+    assert pm.load_model(str(partial)) == pm.PerfModel(profile=model.profile)
+
+
+@pytest.mark.parametrize("mutate", ["empty", "version", "tag", "truncated", "junk", "badgrid"])
+def test_load_model_rejects_bad_documents(tmp_path, mutate):
+    text = open(DOC).read()
+    if mutate == "empty":
+        text = ""
+    elif mutate == "version":
+        text = text.replace("trajseek-perfmodel 1", "trajseek-perfmodel 2", 1)
+    elif mutate == "tag":
+        text = text.replace("trajseek-perfmodel 1", "other 1", 1)
+    elif mutate == "truncated":
+        text = "\n".join(text.splitlines()[:20]) + "\n"
+    elif mutate == "junk":
+        text += "what is this\n"
+    else:
+        text = text.replace("grid launch", "grid lunch", 1)
+    p = tmp_path / "bad.txt"
+    p.write_text(text)
+    with pytest.raises(FormatError):
+        pm.load_model(str(p))
+
+
+# ── GPU-backed parts ────────────────────────────────────────────────────────
+
+
+def _scene(name):
+    (k, n, seed, ts), m, (pk, pn, pseed, pts), (nq, qseed), d, s, ne, rseed = SCENES[name]
+    store = datagen.generate(datagen.make_profile(k, n, seed=seed, timesteps=ts))
+    index = tsk.build_index(store, m)
+    pool = datagen.generate(datagen.make_profile(pk, pn, seed=pseed, timesteps=pts))
+    queries = datagen.sample_queries(pool, nq, seed=qseed)
+    return store, index, pool, queries, d, s, ne, rseed
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", list(SCENES))
+def test_hit_rates_mixes_and_predictions_match_reference(name):
+    tsk.set_device(0)
+    store, index, pool, queries, d, s, ne, rseed = _scene(name)
+    prof = pm.estimate_hit_rates(store, index, pool, s, d, num_epochs=ne, seed=rseed)
+    assert prof == _profile(name)
+    plan = tsk.periodic(queries, s, index)
+    tm, mix = [], []
+    for b in plan.batches:
+        if b.first is None:
+            continue
+        batch = queries.view(b.lo, b.hi)
+        tm.append(pm.temporal_miss_fraction(store, (b.first, b.last), batch))
+        m = pm.interaction_mix(store, (b.first, b.last), batch, prof)
+        mix.append([m.hit, m.temporal_miss, m.spatial_miss, float(m.clamped)])
+    assert np.array_equal(np.array(tm), Z[f"tm_{name}"])
+    assert np.array_equal(np.array(mix), Z[f"mix_{name}"])
+    sf, host = _surfaces(), _host()
+    preds = [pm.predict(sv, queries, store, index, sf, prof, host, d) for sv in (3, 5, 10, 20, 40)]
+    got = np.array([[p.s, p.host_seconds, p.kernel_seconds, p.total_seconds, p.result_bytes, p.predicted_hits,
+                     p.clamped_batches] for p in preds])
+    assert np.array_equal(got, Z[f"pred_{name}"])
+    best, all_p = pm.recommend_batch_size([40, 3, 10, 5, 20], queries, store, index, sf, prof, host, d)
+    assert best == int(Z[f"rec_{name}"][0]) and [p.s for p in all_p] == [3, 5, 10, 20, 40]
+
+
+@pytest.mark.gpu
+def test_estimation_is_deterministic_and_validates():
+    tsk.set_device(0)
+    store, index, pool, _, d, s, _, _ = _scene("small")
+    a = pm.estimate_hit_rates(store, index, pool, 8, d, num_epochs=4, seed=9)
+    assert a == pm.estimate_hit_rates(store, index, pool, 8, d, num_epochs=4, seed=9)
+    with pytest.raises(DomainError):
+        pm.estimate_hit_rates(store, index, pool, 0, d)
+    with pytest.raises(DomainError):
+        pm.estimate_hit_rates(store, index, pool, 8, d, num_epochs=0)
+    with pytest.raises(DomainError):
+        pm.temporal_miss_fraction(store, (0, len(store)), pool.view(0, 3))
+
+
+@pytest.mark.gpu
+def test_calibration_on_this_gpu():
+    tsk.set_device(0)
+    grid = pm.SurfaceGrid((1, 20, 120), (16, 1000, 20000))
+    sf = pm.calibrate_surfaces(grid, reps=2)
+    for n in SURF:
+        g = getattr(sf, n)
+        assert g.shape == (3, 3) and (g > 0).all() and np.isfinite(g).all(), n
+    # hits cost at least what spatial misses cost on the biggest batches
+    assert sf.all_hit[-1, -1] >= sf.spatial_miss[-1, -1]
+    host = pm.calibrate_host(2000, [10, 40, 160, 640], reps=2)
+    assert host.exponent < 0 and host.scale > 0 and host.transfer_per_byte >= 0
