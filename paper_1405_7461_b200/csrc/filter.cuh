@@ -256,6 +256,40 @@ inline float tsk_fma_dir(float a, float b, float c, int mode) {
 }
 #endif
 
+// The pre-filter test against a given R2 >= (a sr + b)^2 (rounded up):
+// true = the pair may hit (NaN flags).  K1 passes one R2 per (query, lane),
+// computed with the largest sr of the lane's candidates (R grows with sr,
+// so each pair's own test below is implied).
+TSK_HD bool f32_flag_r2(const CandF32 &c, float qts, float qx, float qy, float qz, float R2) {
+#ifdef __CUDA_ARCH__
+    const float ux = __fsub_rn(__fmaf_rn(qts, c.vx, c.px), qx);
+    const float uy = __fsub_rn(__fmaf_rn(qts, c.vy, c.py), qy);
+    const float uz = __fsub_rn(__fmaf_rn(qts, c.vz, c.pz), qz);
+    const float n = __fmaf_rd(uz, uz, __fmaf_rd(uy, uy, __fmul_rd(ux, ux)));
+    unsigned far;
+    asm("{.reg .pred p; setp.gt.f32 p, %1, %2; selp.u32 %0, 1, 0, p;}" : "=r"(far) : "f"(n), "f"(R2));
+    return far == 0u;
+#else
+    const float ux = fmaf(qts, c.vx, c.px) - qx;
+    const float uy = fmaf(qts, c.vy, c.py) - qy;
+    const float uz = fmaf(qts, c.vz, c.pz) - qz;
+    const float n = tsk_fma_dir(uz, uz, tsk_fma_dir(uy, uy, tsk_fma_dir(ux, ux, 0.f, FE_DOWNWARD), FE_DOWNWARD),
+                                FE_DOWNWARD);
+    return !(n > R2);
+#endif
+}
+
+// (a sr + b)^2 rounded up
+TSK_HD float f32_r2(float qa, float sr, float qb) {
+#ifdef __CUDA_ARCH__
+    const float R = __fmaf_ru(qa, sr, qb);
+    return __fmul_ru(R, R);
+#else
+    const float R = tsk_fma_dir(qa, sr, qb, FE_UPWARD);
+    return tsk_fma_dir(R, R, 0.f, FE_UPWARD);
+#endif
+}
+
 // The pre-filter test: true = the pair may hit (NaN flags).
 TSK_HD bool f32_flag(const CandF32 &c, float qts, float qx, float qy, float qz, float qa, float qb) {
 #ifdef __CUDA_ARCH__

@@ -73,8 +73,12 @@ __device__ __noinline__ uint4 f32_scan(uint32_t qa, uint32_t qa_end, uint32_t ba
         const int i = k * 32 + lane;
         c[k].px = cs[0 * WCAND + i]; c[k].py = cs[1 * WCAND + i]; c[k].pz = cs[2 * WCAND + i];
         c[k].vx = cs[3 * WCAND + i]; c[k].vy = cs[4 * WCAND + i]; c[k].vz = cs[5 * WCAND + i];
-        c[k].sr = cs[6 * WCAND + i];
     }
+    // one threshold per query and lane: the largest speed bound of the lane's
+    // candidates (staged per candidate, reduced here)
+    float srl = 0.f;
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) srl = fmaxf(srl, cs[6 * WCAND + k * 32 + lane]);
     double rts[CPT], rte[CPT];
     if (CNT) {
         const int64_t wb = k1_wctx[warp].wbase;
@@ -95,6 +99,7 @@ __device__ __noinline__ uint4 f32_scan(uint32_t qa, uint32_t qa_end, uint32_t ba
         if (CNT) lds2d(qa + 32, cts, cte);
         bool cand[CPT];
         bool any = false;
+        const float R2 = f32_r2(qa4, srl, qb4);
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
             bool ov = true;
@@ -106,7 +111,7 @@ __device__ __noinline__ uint4 f32_scan(uint32_t qa, uint32_t qa_end, uint32_t ba
                 else ov = rts[k] <= cte && cts <= rte[k];
                 n_ov += ov ? 1u : 0u;
             }
-            cand[k] = f32_flag(c[k], qts, qx, qy, qz, qa4, qb4) && ov;
+            cand[k] = f32_flag_r2(c[k], qts, qx, qy, qz, R2) && ov;
             any |= cand[k];
         }
         if (!__any_sync(0xffffffffu, any)) continue;

@@ -584,3 +584,34 @@ def test_fp32_prefilter_head_on_flip_points(t_base, offset):
             assert got == want, (i, d)
             checked += want is not None
     assert checked > 20  # the flip points are straddled
+
+
+@pytest.mark.parametrize("kind", ["uniform", "exp"])
+def test_counting_modes_match_the_full_search(kind):
+    """TSK_COUNT_ONLY (per-batch hits, no rows) and TSK_OVERLAPS_ONLY
+    (per-batch temporal overlaps) agree with a full run_search and with the
+    oracle's temporal misses, for a plan and for explicit (overlapping) spans."""
+    from paper_1405_7461_b200 import datagen
+    from paper_1405_7461_b200.engine import plan_counts, span_counts
+
+    store = datagen.generate(datagen.make_profile(kind, 300, seed=4, timesteps=80))
+    pool = datagen.generate(datagen.make_profile(kind, 40, seed=5, timesteps=80))
+    queries = datagen.sample_queries(pool, 10, seed=6)
+    index = tsk.build_index(store, 100)
+    plan = tsk.periodic(queries, 25, index)
+    res, st = tsk.run_search(store, index, plan, 3.0)
+    pb = plan_counts(store, index, plan, 3.0)
+    assert int(pb[:, 3].sum()) == len(res) == st.hits
+    ov = plan_counts(store, index, plan, 0.0, overlaps_only=True)
+    assert int(ov[:, 2].sum()) == st.interactions_computed - st.temporal_misses
+    assert np.array_equal(ov[:, 2], pb[:, 2]) and not ov[:, 3].any()
+    # explicit spans, windows overlapping each other
+    lo = np.arange(0, len(queries) - 30, 7)
+    first, last = tsk.candidate_ranges(index, queries.ts[lo], np.maximum.reduceat(queries.te, lo)[: len(lo)])
+    keep = first >= 0
+    lo, first, last = lo[keep], first[keep], last[keep]
+    hi = np.minimum(lo + 29, len(queries) - 1)
+    got = span_counts(store, queries, lo, hi, first, last, 3.0)
+    for k in range(len(lo)):
+        r, s = tsk.execute_batch(store, queries.view(int(lo[k]), int(hi[k])), (int(first[k]), int(last[k])), 3.0)
+        assert int(got[k, 3]) == s.hits and int(got[k, 2]) == s.interactions_computed - s.temporal_misses
