@@ -366,6 +366,20 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
                 continue;
             }
             n_ev += (unsigned long long)(jhi - jlo) * (unsigned long long)k1_wctx[warp].nvalid;
+            if (te_sorted && !*L.q_unsorted) {
+                // start and end times both ascending over the tile: a
+                // candidate overlaps exactly the queries j with
+                // ts_j <= r.te (a prefix) and te_j >= r.ts (a suffix), so its
+                // count is two bisections, and the whole window is one scan
+                // (the exact path decides the clip cases per pair)
+#pragma unroll
+                for (int k = 0; k < CPT; ++k) {
+                    const int c = upper_bound_ts(sqf, it.nt, rte[k]) - lower_bound_te(sqf, it.nt, rts[k]);
+                    n_ov += c > 0 ? (unsigned)c : 0u;
+                }
+                f32_range<TA_BOTH, TB_DYN, false>(qt, sqf, jlo, jhi, warp, lane, n_ov, n_hit);
+                continue;
+            }
             // TA_C range: every query ends before all candidates (running max
             // < min te) and te is sorted → overlaps counted by bisection
             if (jlo < ja && pm[ja - 1] < wmin_te && te_sorted) {
