@@ -174,6 +174,47 @@ __global__ void k_iota(int64_t n, uint32_t *v) {
         v[i] = (uint32_t)i;
 }
 
+// K4 for small hit counts: one CTA sorts up to K4_SMALL (key, append index)
+// pairs in shared memory with a bitonic network — one launch instead of
+// the radix sort's several.  Keys are unique (one hit per pair), so the
+// order equals the stable radix sort's.
+constexpr int K4_SMALL = 4096;
+
+__global__ void __launch_bounds__(1024) k_small_sort(int n, const uint64_t *__restrict__ keys_in,
+                                                     uint64_t *__restrict__ keys_out,
+                                                     uint32_t *__restrict__ perm_out) {
+    __shared__ uint64_t k[K4_SMALL];
+    __shared__ uint32_t v[K4_SMALL];
+    int m = 1;
+    while (m < n) m <<= 1;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        k[i] = i < n ? keys_in[i] : ~0ull;  // padding sorts last
+        v[i] = (uint32_t)i;
+    }
+    __syncthreads();
+    for (int size = 2; size <= m; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = threadIdx.x; t < (m >> 1); t += blockDim.x) {
+                const int i = 2 * t - (t & (stride - 1));  // lower index of the pair
+                const int j = i + stride;
+                const bool up = (i & size) == 0;
+                const uint64_t a = k[i], b = k[j];
+                const uint32_t va = v[i], vb = v[j];
+                // (key, index) order: padding stays behind a real all-ones key
+                if ((a > b || (a == b && va > vb)) == up) {
+                    k[i] = b; k[j] = a;
+                    v[i] = vb; v[j] = va;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        keys_out[i] = k[i];
+        perm_out[i] = v[i];
+    }
+}
+
 // Opt-in phase trace (TSK_TRACE=1): CUDA events at phase boundaries on the
 // db stream, printed to stderr when the call completes.
 struct Trace {
@@ -383,17 +424,23 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
             uint64_t *ko = ks + nh;
             uint32_t *v0 = reinterpret_cast<uint32_t *>(ko + nh);
             uint32_t *v1 = v0 + nh;
-            int gi = (int)std::min<int64_t>((nh + 255) / 256, 148 * 8);
-            k_iota<<<gi, 256, 0, st>>>(nh, v0);
-            TSK_CUDA(cudaGetLastError());
-            ++launches;
-            TSK_CUDA(cudaMemcpyAsync(ks, keys, cb, cudaMemcpyDeviceToDevice, st));
-            int end_bit = bb + major_bits + minor_bits;
-            if (end_bit == 0) end_bit = 1;
-            size_t tb = 0;
-            TSK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, ks, ko, v0, v1, nh, 0, end_bit, st));
-            db->cub_tmp.reserve(tb, st);
-            TSK_CUDA(cub::DeviceRadixSort::SortPairs(db->cub_tmp.p, tb, ks, ko, v0, v1, nh, 0, end_bit, st));
+            if (nh <= K4_SMALL) {
+                k_small_sort<<<1, 1024, 0, st>>>((int)nh, keys, ko, v1);
+                TSK_CUDA(cudaGetLastError());
+                ++launches;
+            } else {
+                int gi = (int)std::min<int64_t>((nh + 255) / 256, 148 * 8);
+                k_iota<<<gi, 256, 0, st>>>(nh, v0);
+                TSK_CUDA(cudaGetLastError());
+                ++launches;
+                TSK_CUDA(cudaMemcpyAsync(ks, keys, cb, cudaMemcpyDeviceToDevice, st));
+                int end_bit = bb + major_bits + minor_bits;
+                if (end_bit == 0) end_bit = 1;
+                size_t tb = 0;
+                TSK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, ks, ko, v0, v1, nh, 0, end_bit, st));
+                db->cub_tmp.reserve(tb, st);
+                TSK_CUDA(cub::DeviceRadixSort::SortPairs(db->cub_tmp.p, tb, ks, ko, v0, v1, nh, 0, end_bit, st));
+            }
             keys = ko;
             perm = v1;
         }
