@@ -505,8 +505,10 @@ __device__ __forceinline__ void flush_queue(const QRec *__restrict__ qt, uint32_
 }
 
 // Per-batch 64-bit counters: warp sums → block sums → one atomic per item.
+// red_ev (optional): the block's evaluated-pair sum, added to L.eval_count.
 __device__ __forceinline__ void item_counters(const K1Launch &L, int64_t b, unsigned n_ov, unsigned n_hit, int lane,
-                                              int tid, unsigned long long *red_ov, unsigned long long *red_hit) {
+                                              int tid, unsigned long long *red_ov, unsigned long long *red_hit,
+                                              const unsigned long long *red_ev = nullptr) {
     for (int o = 16; o; o >>= 1) {
         n_ov += __shfl_xor_sync(0xffffffffu, n_ov, o);
         n_hit += __shfl_xor_sync(0xffffffffu, n_hit, o);
@@ -519,6 +521,7 @@ __device__ __forceinline__ void item_counters(const K1Launch &L, int64_t b, unsi
     if (tid == 0) {
         if (*red_ov) atomicAdd(&L.plan.ovl[b], *red_ov);
         if (*red_hit) atomicAdd(&L.plan.hits[b], *red_hit);
+        if (red_ev && *red_ev) atomicAdd(L.eval_count, *red_ev);
     }
     __syncthreads();
 }

@@ -403,8 +403,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
             }
         }
         if (lane == 0 && n_ev) atomicAdd(&red_ev, n_ev);
-        item_counters(L, it.b, n_ov, n_hit, lane, tid, &red_ov, &red_hit);  // (its barrier publishes red_ev)
-        if (tid == 0 && red_ev) atomicAdd(L.eval_count, red_ev);
+        item_counters(L, it.b, n_ov, n_hit, lane, tid, &red_ov, &red_hit, &red_ev);
     }
 }
 
