@@ -138,7 +138,36 @@ def run_search(store: SegmentStore, index: TemporalIndex, plan: BatchPlan, d: fl
     return _run_one(store, index, plan, d, ordinal, 0, order == "canonical")
 
 
+# Width of K1's hit keys (batch | entry offset | query offset), checked by
+# tsk_search; a plan that needs more is run as consecutive sub-plans.
+_KEY_BITS = 64
+
+
+def _bits_for(count: int) -> int:
+    """Bits to hold 0..count-1 (search.cu bits_for)."""
+    return max(0, int(count - 1).bit_length()) if count > 1 else 0
+
+
+def _split_for_keys(store, plan):
+    """Batch ranges [b0, b1) small enough that each sub-plan's hit keys fit
+    in _KEY_BITS bits, or None when the whole plan fits."""
+    lo, hi = plan.table()
+    eb = _bits_for(max(len(store), 1))
+    qb = _bits_for(int((hi - lo + 1).max()))
+    if _bits_for(len(plan.batches)) + eb + qb <= _KEY_BITS:
+        return None
+    room = _KEY_BITS - eb - qb
+    if room < 0:
+        raise DomainError("a single batch's result keys exceed 64 bits")
+    step = 1 << room
+    nb = len(plan.batches)
+    return [(b0, min(b0 + step, nb)) for b0 in range(0, nb, step)]
+
+
 def _run_one(store, index, plan, d, ordinal, replica, canonical=False):
+    chunks = _split_for_keys(store, plan)
+    if chunks is not None:
+        return _run_chunked(store, index, plan, d, ordinal, replica, canonical, chunks)
     t_start = time.perf_counter()
     queries = plan.queries
     lo, hi = plan.table()
@@ -170,6 +199,33 @@ def _run_one(store, index, plan, d, ordinal, replica, canonical=False):
     stats.kernel_seconds = dev_s
     stats.device_seconds = dev_s
     stats.pair_kernel_seconds = res.k1_ms / 1e3
+    t_end = time.perf_counter()
+    stats.assembly_seconds = t_end - t_asm
+    stats.total_seconds = t_end - t_start
+    stats.overhead_seconds = max(0.0, stats.total_seconds - stats.kernel_seconds - stats.assembly_seconds)
+    return result, stats
+
+
+def _run_chunked(store, index, plan, d, ordinal, replica, canonical, chunks):
+    """Consecutive sub-plans (keys too wide for one call), concatenated in
+    plan order — the reference's item order is per batch, so it is kept."""
+    from .sharding import sub_plan
+
+    t_start = time.perf_counter()
+    parts, stats = [], SearchStats()
+    for b0, b1 in chunks:
+        r, st = _run_one(store, index, sub_plan(plan, b0, b1), d, ordinal, replica, False)
+        parts.append(r)
+        for t in st.per_batch:
+            stats.per_batch.append(BatchTrace(t.ordinal + b0, t.queries, t.candidates, t.interactions, t.hits,
+                                              t.kernel_seconds))
+        for k in ("interactions_computed", "temporal_misses", "spatial_misses", "hits", "kernel_seconds",
+                  "device_seconds", "pair_kernel_seconds"):
+            setattr(stats, k, getattr(stats, k) + getattr(st, k))
+    t_asm = time.perf_counter()
+    result = ResultSet.concatenate(parts)
+    if canonical:
+        result = result.canonical_order()
     t_end = time.perf_counter()
     stats.assembly_seconds = t_end - t_asm
     stats.total_seconds = t_end - t_start

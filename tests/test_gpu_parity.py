@@ -615,3 +615,28 @@ def test_counting_modes_match_the_full_search(kind):
     for k in range(len(lo)):
         r, s = tsk.execute_batch(store, queries.view(int(lo[k]), int(hi[k])), (int(first[k]), int(last[k])), 3.0)
         assert int(got[k, 3]) == s.hits and int(got[k, 2]) == s.interactions_computed - s.temporal_misses
+
+
+def test_plans_with_too_wide_result_keys_run_in_chunks(monkeypatch):
+    """A plan whose (batch, entry, query) keys exceed the key width is run as
+    consecutive sub-plans; items, order and statistics are unchanged."""
+    from paper_1405_7461_b200 import datagen, engine
+
+    store = datagen.generate(datagen.make_profile("uniform", 300, seed=4, timesteps=80))
+    pool = datagen.generate(datagen.make_profile("uniform", 40, seed=5, timesteps=80))
+    queries = datagen.sample_queries(pool, 10, seed=6)
+    index = tsk.build_index(store, 100)
+    plan = tsk.periodic(queries, 16, index)
+    want, ws = tsk.run_search(store, index, plan, 3.0)
+    eb = engine._bits_for(len(store))
+    qb = engine._bits_for(16)
+    monkeypatch.setattr(engine, "_KEY_BITS", eb + qb + 2)  # 4 batches per sub-plan
+    assert len(engine._split_for_keys(store, plan)) > 2
+    got, gs = tsk.run_search(store, index, plan, 3.0)
+    assert np.array_equal(got.key_array(), want.key_array())
+    assert np.array_equal(got.t_begin, want.t_begin) and np.array_equal(got.t_end, want.t_end)
+    assert (gs.interactions_computed, gs.temporal_misses, gs.spatial_misses, gs.hits) == \
+        (ws.interactions_computed, ws.temporal_misses, ws.spatial_misses, ws.hits)
+    assert [(t.ordinal, t.hits) for t in gs.per_batch] == [(t.ordinal, t.hits) for t in ws.per_batch]
+    canon, _ = tsk.run_search(store, index, plan, 3.0, order="canonical")
+    assert np.array_equal(canon.key_array(), want.canonical_order().key_array())
