@@ -586,21 +586,28 @@ def test_fp32_prefilter_head_on_flip_points(t_base, offset):
     assert checked > 20  # the flip points are straddled
 
 
-@pytest.mark.parametrize("kind", ["uniform", "exp"])
-def test_counting_modes_match_the_full_search(kind):
+def _scaled(store, f):
+    return tsk.SegmentStore(store.traj, store.seg, store.xs * f, store.ys * f, store.zs * f, store.ts,
+                            store.xe * f, store.ye * f, store.ze * f, store.te)
+
+
+@pytest.mark.parametrize("kind,scale", [("uniform", 1.0), ("exp", 1.0), ("uniform", 1e70)])
+def test_counting_modes_match_the_full_search(kind, scale):
     """TSK_COUNT_ONLY (per-batch hits, no rows) and TSK_OVERLAPS_ONLY
-    (per-batch temporal overlaps) agree with a full run_search and with the
-    oracle's temporal misses, for a plan and for explicit (overlapping) spans."""
+    (per-batch temporal overlaps) agree with a full run_search, for a plan
+    and for explicit (overlapping) spans; scale 1e70 runs the FP64 kernel."""
     from paper_1405_7461_b200 import datagen
     from paper_1405_7461_b200.engine import plan_counts, span_counts
 
-    store = datagen.generate(datagen.make_profile(kind, 300, seed=4, timesteps=80))
-    pool = datagen.generate(datagen.make_profile(kind, 40, seed=5, timesteps=80))
+    store = _scaled(datagen.generate(datagen.make_profile(kind, 300, seed=4, timesteps=80)), scale)
+    pool = _scaled(datagen.generate(datagen.make_profile(kind, 40, seed=5, timesteps=80)), scale)
     queries = datagen.sample_queries(pool, 10, seed=6)
     index = tsk.build_index(store, 100)
     plan = tsk.periodic(queries, 25, index)
-    res, st = tsk.run_search(store, index, plan, 3.0)
-    pb = plan_counts(store, index, plan, 3.0)
+    d = 3.0 * scale
+    res, st = tsk.run_search(store, index, plan, d)
+    assert st.hits > 0
+    pb = plan_counts(store, index, plan, d)
     assert int(pb[:, 3].sum()) == len(res) == st.hits
     ov = plan_counts(store, index, plan, 0.0, overlaps_only=True)
     assert int(ov[:, 2].sum()) == st.interactions_computed - st.temporal_misses
@@ -611,9 +618,9 @@ def test_counting_modes_match_the_full_search(kind):
     keep = first >= 0
     lo, first, last = lo[keep], first[keep], last[keep]
     hi = np.minimum(lo + 29, len(queries) - 1)
-    got = span_counts(store, queries, lo, hi, first, last, 3.0)
+    got = span_counts(store, queries, lo, hi, first, last, d)
     for k in range(len(lo)):
-        r, s = tsk.execute_batch(store, queries.view(int(lo[k]), int(hi[k])), (int(first[k]), int(last[k])), 3.0)
+        r, s = tsk.execute_batch(store, queries.view(int(lo[k]), int(hi[k])), (int(first[k]), int(last[k])), d)
         assert int(got[k, 3]) == s.hits and int(got[k, 2]) == s.interactions_computed - s.temporal_misses
 
 
