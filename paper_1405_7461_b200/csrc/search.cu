@@ -395,23 +395,28 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     const bool want_ord = flags & TSK_WANT_ORDINALS;
     const bool on_device = flags & TSK_RESULTS_ON_DEVICE;
     const int ncols = want_ord ? 8 : 6;
-    size_t got = 0;
-    res->host = on_device ? nullptr : pin_alloc((size_t)(nh > 0 ? nh : 1) * 8 * ncols, &got);
-    res->host_bytes = got;
-    char *hb = static_cast<char *>(res->host);
     size_t cb = (size_t)nh * 8;
-    if (hb) {
-        res->qtraj = (int64_t *)(hb + 0 * cb);
-        res->qseg = (int64_t *)(hb + 1 * cb);
-        res->etraj = (int64_t *)(hb + 2 * cb);
-        res->eseg = (int64_t *)(hb + 3 * cb);
-        res->tbeg = (double *)(hb + 4 * cb);
-        res->tend = (double *)(hb + 5 * cb);
-    }
-    if (hb && want_ord) {
-        res->qord = (int64_t *)(hb + 6 * cb);
-        res->eord = (int64_t *)(hb + 7 * cb);
-    }
+    // the pinned host block is taken after K4 is enqueued, so a fresh
+    // registration (large results) overlaps the device's sort and gather
+    auto host_block = [&]() {
+        size_t got = 0;
+        res->host = on_device ? nullptr : pin_alloc((size_t)(nh > 0 ? nh : 1) * 8 * ncols, &got);
+        res->host_bytes = got;
+        char *hb = static_cast<char *>(res->host);
+        if (hb) {
+            res->qtraj = (int64_t *)(hb + 0 * cb);
+            res->qseg = (int64_t *)(hb + 1 * cb);
+            res->etraj = (int64_t *)(hb + 2 * cb);
+            res->eseg = (int64_t *)(hb + 3 * cb);
+            res->tbeg = (double *)(hb + 4 * cb);
+            res->tend = (double *)(hb + 5 * cb);
+        }
+        if (hb && want_ord) {
+            res->qord = (int64_t *)(hb + 6 * cb);
+            res->eord = (int64_t *)(hb + 7 * cb);
+        }
+    };
+    if (nh == 0) host_block();
     if (nh > 0) {
         const uint64_t *keys = db->recs.as<uint64_t>();
         const double *tbin = reinterpret_cast<const double *>(keys + cap);
@@ -491,6 +496,7 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
             ob = cbuf;
             tr.mark("canonical");
         }
+        host_block();
         if (!on_device) TSK_CUDA(cudaMemcpyAsync(res->host, ob, cb * ncols, cudaMemcpyDeviceToHost, st));
         tr.mark("d2h");
     }
