@@ -75,6 +75,9 @@ const char *tsk_last_error(void);
 /* Upload a sorted store to `device` and hoist per-segment invariants. */
 int tsk_db_create(int device, const tsk_columns *cols, tsk_db **out);
 void tsk_db_free(tsk_db *db);
+/* Replica of `src` on `device` (device-to-device copy, NVLink peer copy
+ * between GPUs); build its index with tsk_index_build. */
+int tsk_db_replicate(const tsk_db *src, int device, tsk_db **out);
 int64_t tsk_db_size(const tsk_db *db);
 
 /* Stable device sort of n start times: perm[i] = input row of sorted row i

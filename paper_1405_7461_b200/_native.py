@@ -65,6 +65,7 @@ SIGNATURES = {
     "tsk_result_free": ([_P], None),
     "tsk_probe_fp64": ([ctypes.c_int, _PD, _PD, _PD], ctypes.c_int),
     "tsk_probe_fp32": ([ctypes.c_int, _PD], ctypes.c_int),
+    "tsk_db_replicate": ([_P, ctypes.c_int, ctypes.POINTER(_P)], ctypes.c_int),
     "tsk_result_k1_evals": ([_P, _PI64], ctypes.c_int),
     "tsk_plan_setsplit": ([_I64, _PD, _PD, _I64, _PD, _PD, _PI64, _PI64, ctypes.c_int, _I64, _I64,
                            _I64, _PI64, _PI64, _PI64, _PI64, _PI64, _PD], ctypes.c_int),
@@ -167,13 +168,16 @@ def columns_of(store) -> tuple[Columns, list]:
 class DeviceStore:
     """Owns a tsk_db handle: a store resident in one GPU's HBM."""
 
-    def __init__(self, store, device: int | None = None):
+    def __init__(self, store, device: int | None = None, source: "DeviceStore | None" = None):
         self.device = current_device() if device is None else int(device)
         lib = load()
-        col, keep = columns_of(store)
         h = ctypes.c_void_p()
-        check(lib.tsk_db_create(self.device, ctypes.byref(col), ctypes.byref(h)))
-        del keep
+        if source is not None:  # device-to-device replica (NVLink between peers)
+            check(lib.tsk_db_replicate(source.handle, self.device, ctypes.byref(h)))
+        else:
+            col, keep = columns_of(store)
+            check(lib.tsk_db_create(self.device, ctypes.byref(col), ctypes.byref(h)))
+            del keep
         self.handle = h
         self.n = len(store)
         self.index_token = None

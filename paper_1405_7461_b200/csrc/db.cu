@@ -556,6 +556,53 @@ extern "C" int tsk_db_create(int device, const tsk_columns *cols, tsk_db **out) 
     }
 }
 
+// Replica of a device store on another GPU (or another handle on the same
+// one): the SoA block (columns, hoisted invariants, group bounds) is copied
+// device to device — over NVLink when the GPUs are peers — instead of being
+// re-uploaded from the host and re-hoisted.  The index is not copied; it is
+// rebuilt on the replica by tsk_index_build (K2, milliseconds).
+extern "C" int tsk_db_replicate(const tsk_db *src, int device, tsk_db **out) {
+    tsk_db *db = nullptr;
+    try {
+        TSK_REQUIRE(src && out, "null argument");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            throw Error{TSK_ENODEV, "no CUDA device visible"};
+        TSK_REQUIRE(device >= 0 && device < ndev, "device ordinal out of range");
+        TSK_CUDA(cudaSetDevice(src->device));
+        TSK_CUDA(cudaStreamSynchronize(src->stream));  // src fully built
+        TSK_CUDA(cudaSetDevice(device));
+        db = new tsk_db();
+        db->device = device;
+        TSK_CUDA(cudaStreamCreateWithFlags(&db->stream, cudaStreamNonBlocking));
+        TSK_CUDA(cudaEventCreate(&db->ev0));
+        TSK_CUDA(cudaEventCreate(&db->ev1));
+        TSK_CUDA(cudaEventCreate(&db->ev_k0));
+        TSK_CUDA(cudaEventCreate(&db->ev_k1));
+        soa_alloc(db->s, src->s.n, true, db->stream);  // same layout as the source block
+        if (src->s.n > 0) {
+            const char *end = reinterpret_cast<const char *>(src->s.gb + (src->s.n + GB_SIZE - 1) / GB_SIZE);
+            const size_t bytes = (size_t)(end - src->s.storage.as<char>());
+            int can = 0;
+            if (device != src->device && cudaDeviceCanAccessPeer(&can, device, src->device) == cudaSuccess && can) {
+                const cudaError_t e = cudaDeviceEnablePeerAccess(src->device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) TSK_CUDA(e);
+                cudaGetLastError();
+            }
+            TSK_CUDA(cudaMemcpyPeerAsync(db->s.storage.p, device, src->s.storage.p, src->device, bytes, db->stream));
+        }
+        db->s.any_unsafe = src->s.any_unsafe;
+        db->s.sorted = src->s.sorted;
+        db->cmax = src->cmax;
+        TSK_CUDA(cudaStreamSynchronize(db->stream));
+        *out = db;
+        return TSK_OK;
+    } catch (const Error &e) {
+        if (db) tsk_db_free(db);
+        return fail(e.code, e.msg);
+    }
+}
+
 extern "C" void tsk_db_free(tsk_db *db) {
     if (!db) return;
     cudaSetDevice(db->device);

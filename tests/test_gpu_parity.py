@@ -647,3 +647,24 @@ def test_plans_with_too_wide_result_keys_run_in_chunks(monkeypatch):
     assert [(t.ordinal, t.hits) for t in gs.per_batch] == [(t.ordinal, t.hits) for t in ws.per_batch]
     canon, _ = tsk.run_search(store, index, plan, 3.0, order="canonical")
     assert np.array_equal(canon.key_array(), want.canonical_order().key_array())
+
+
+@pytest.mark.parametrize("scale", [1.0, 1e70])
+def test_device_replica_matches_the_uploaded_store(scale):
+    """tsk_db_replicate: a second handle made by a device-to-device copy
+    (columns, hoisted invariants, group bounds, flags) gives the same results
+    as the uploaded store (scale 1e70 runs the FP64 kernel)."""
+    from paper_1405_7461_b200 import datagen
+    from paper_1405_7461_b200.engine import _run_one
+
+    store = _scaled(datagen.generate(datagen.make_profile("normal", 300, seed=7, timesteps=60)), scale)
+    pool = _scaled(datagen.generate(datagen.make_profile("normal", 40, seed=8, timesteps=60)), scale)
+    queries = datagen.sample_queries(pool, 12, seed=9)
+    index = tsk.build_index(store, 64)
+    plan = tsk.periodic(queries, 20, index)
+    want, ws = _run_one(store, index, plan, 4.0 * scale, 0, 0)
+    got, gs = _run_one(store, index, plan, 4.0 * scale, 0, 1)  # replica 1: copied from replica 0
+    assert store._dev[(0, 1)].handle.value != store._dev[(0, 0)].handle.value
+    assert np.array_equal(got.key_array(), want.key_array()) and len(want) > 0
+    assert np.array_equal(got.t_begin, want.t_begin) and np.array_equal(got.t_end, want.t_end)
+    assert (gs.temporal_misses, gs.spatial_misses, gs.hits) == (ws.temporal_misses, ws.spatial_misses, ws.hits)
