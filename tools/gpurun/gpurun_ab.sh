@@ -1,5 +1,5 @@
 # A/B: variants given as "name:libpath" in $VARIANTS (path relative to repo root or "default")
-[ -n "$LAT" ] && ./tools/fp64_latency
+[ -n "$LAT" ] && nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o /tmp/fp64_latency tools/fp64_latency.cu && /tmp/fp64_latency
 for v in $VARIANTS; do
   name=${v%%:*}; lib=${v#*:}
   if [ "$lib" = "default" ]; then unset TRAJSEEK_LIB; else export TRAJSEEK_LIB=$(pwd)/$lib; fi
