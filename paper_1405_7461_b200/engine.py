@@ -68,6 +68,67 @@ class SearchStats:
         return (self.temporal_misses + self.spatial_misses) / self.interactions_computed
 
 
+class _LazyTraces(list):
+    """``SearchStats.per_batch``: a list of BatchTrace built on first use
+    from the per-batch arrays, so a large plan does not pay for thousands of
+    Python objects on every call unless they are read."""
+
+    __slots__ = ("_src",)
+
+    def __init__(self, iterable=(), *, src=None):
+        super().__init__(iterable)
+        self._src = src
+
+    def _fill(self):
+        if self._src is not None:
+            sizes, cands, ints, hits, secs = self._src
+            self._src = None
+            list.extend(self, map(BatchTrace, range(len(sizes)), sizes, cands, ints, hits, secs))
+
+    def __len__(self):
+        self._fill()
+        return list.__len__(self)
+
+    def __iter__(self):
+        self._fill()
+        return list.__iter__(self)
+
+    def __reversed__(self):
+        self._fill()
+        return list.__reversed__(self)
+
+    def __getitem__(self, i):
+        self._fill()
+        return list.__getitem__(self, i)
+
+    def __contains__(self, x):
+        self._fill()
+        return list.__contains__(self, x)
+
+    def __eq__(self, other):
+        self._fill()
+        return list.__eq__(self, other)
+
+    def __ne__(self, other):
+        return not self.__eq__(other)
+
+    def __repr__(self):
+        self._fill()
+        return list.__repr__(self)
+
+    def append(self, x):
+        self._fill()
+        list.append(self, x)
+
+    def extend(self, xs):
+        self._fill()
+        list.extend(self, xs)
+
+    def __reduce__(self):
+        self._fill()
+        return (list, (list(list.__iter__(self)),))
+
+
 def resolve_workers(workers: int | None) -> int:
     """Explicit worker count or machine parallelism (engine.py:69-75)."""
     if workers is None:
@@ -186,11 +247,8 @@ def _run_one(store, index, plan, d, ordinal, replica, canonical=False):
     total_ints = int(ints.sum())
     dev_s = res.device_ms / 1e3
     share = ints / total_ints if total_ints else np.zeros_like(ints, dtype=np.float64)
-    stats.per_batch = [
-        BatchTrace(k, int(s), int(c), int(i), int(h), float(f * dev_s))
-        for k, (s, c, i, h, f) in enumerate(zip(sizes.tolist(), cands.tolist(), ints.tolist(),
-                                                pb[:, 3].tolist(), share.tolist()))
-    ]
+    stats.per_batch = _LazyTraces(src=(sizes.tolist(), cands.tolist(), ints.tolist(), pb[:, 3].tolist(),
+                                       (share * dev_s).tolist()))
     ovl = int(pb[:, 2].sum())
     stats.interactions_computed = total_ints
     stats.hits = res.n
