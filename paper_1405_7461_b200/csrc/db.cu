@@ -272,6 +272,80 @@ __global__ void k_qprep(int64_t n, const double *__restrict__ ts, const double *
     if ((threadIdx.x & 31) == 0) atomicMax(cmax_bits, (unsigned long long)__double_as_longlong(cm));
 }
 
+// Pinned (device-mapped) query columns: read them straight from host memory
+// over PCIe in one kernel — the H2D transfer and the record build fused —
+// writing the device copies of ts/te/traj/seg that K3 and K4 read.
+__global__ void k_qprep_mapped(int64_t n, tsk_columns c, double *__restrict__ ts_out, double *__restrict__ te_out,
+                               int64_t *__restrict__ traj_out, int64_t *__restrict__ seg_out,
+                               QRec *__restrict__ out, int *flags, unsigned long long *cmax_bits) {
+    double cm = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        QRec r;
+        r.ts = c.ts[i];
+        r.te = c.te[i];
+        r.sx = c.xs[i];
+        r.sy = c.ys[i];
+        r.sz = c.zs[i];
+        r.ex = c.xe[i];
+        r.ey = c.ye[i];
+        r.ez = c.ze[i];
+        ts_out[i] = r.ts;
+        te_out[i] = r.te;
+        traj_out[i] = c.traj[i];
+        seg_out[i] = c.seg[i];
+        const double s[3] = {r.sx, r.sy, r.sz}, e[3] = {r.ex, r.ey, r.ez};
+        const SegHoist h = seg_hoist(r.ts, r.te, s, e);
+        r.ext = h.ext;
+        r.dx = h.d[0]; r.dy = h.d[1]; r.dz = h.d[2];
+        r.vx = h.v[0]; r.vy = h.v[1]; r.vz = h.v[2];
+        r.flag = h.unsafe ? 1.0 : 0.0;
+        out[i] = r;
+        if (i + 1 < n && c.ts[i + 1] < r.ts) atomicOr(&flags[0], 1);
+        cm = fmax(cm, fmax(fmax(fabs(r.sx), fabs(r.sy)), fmax(fabs(r.sz), fmax(fabs(r.ex), fmax(fabs(r.ey), fabs(r.ez))))));
+    }
+    for (int o = 16; o; o >>= 1) cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(cmax_bits, (unsigned long long)__double_as_longlong(cm));
+}
+
+// The device pointers of ten query columns when every one is pinned and
+// mapped into the device address space; false otherwise.
+bool mapped_columns(const tsk_columns *c, tsk_columns *dev) {
+    const void *src[10] = {c->traj, c->seg, c->xs, c->ys, c->zs, c->ts, c->xe, c->ye, c->ze, c->te};
+    const void *dst[10];
+    for (int k = 0; k < 10; ++k) {
+        cudaPointerAttributes a;
+        if (!src[k] || cudaPointerGetAttributes(&a, src[k]) != cudaSuccess || a.type != cudaMemoryTypeHost ||
+            !a.devicePointer) {
+            cudaGetLastError();
+            return false;
+        }
+        dst[k] = a.devicePointer;
+    }
+    *dev = *c;
+    dev->traj = (const int64_t *)dst[0];
+    dev->seg = (const int64_t *)dst[1];
+    dev->xs = (const double *)dst[2];
+    dev->ys = (const double *)dst[3];
+    dev->zs = (const double *)dst[4];
+    dev->ts = (const double *)dst[5];
+    dev->xe = (const double *)dst[6];
+    dev->ye = (const double *)dst[7];
+    dev->ze = (const double *)dst[8];
+    dev->te = (const double *)dst[9];
+    return true;
+}
+
+void launch_qprep_mapped(const tsk_columns &dev_cols, Soa &q, QRec *out, int *flags, unsigned long long *cmax_bits,
+                         cudaStream_t st) {
+    TSK_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), st));
+    TSK_CUDA(cudaMemsetAsync(cmax_bits, 0, sizeof(unsigned long long), st));
+    if (q.n == 0) return;
+    int grid = (int)std::min<int64_t>((q.n + 255) / 256, 148 * 8);
+    k_qprep_mapped<<<grid, 256, 0, st>>>(q.n, dev_cols, q.ts, q.te, q.traj, q.seg, out, flags, cmax_bits);
+    TSK_CUDA(cudaGetLastError());
+}
+
 void launch_qprep(const Soa &q, QRec *out, int *flags, unsigned long long *cmax_bits, cudaStream_t st) {
     TSK_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), st));
     TSK_CUDA(cudaMemsetAsync(cmax_bits, 0, sizeof(unsigned long long), st));

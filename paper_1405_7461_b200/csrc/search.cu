@@ -291,11 +291,17 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     } else {
         // queries → device SoA → shared-memory records with hoisted invariants
         soa_alloc(db->q, nq, true, st);
-        soa_upload(db->q, qc, st);
         db->q_rec.reserve((size_t)nq * sizeof(QRec), st);
         db->counters.reserve(64, st);
-        launch_qprep(db->q, db->q_rec.as<QRec>(), db->counters.as<int>() + 8,
-                     db->counters.as<unsigned long long>() + 5, st);
+        tsk_columns mapped;
+        if (mapped_columns(qc, &mapped)) {  // pinned inputs: one kernel reads them over PCIe
+            launch_qprep_mapped(mapped, db->q, db->q_rec.as<QRec>(), db->counters.as<int>() + 8,
+                                db->counters.as<unsigned long long>() + 5, st);
+        } else {
+            soa_upload(db->q, qc, st);
+            launch_qprep(db->q, db->q_rec.as<QRec>(), db->counters.as<int>() + 8,
+                         db->counters.as<unsigned long long>() + 5, st);
+        }
         launches += 1;
     }
     tr.mark("queries");

@@ -218,6 +218,9 @@ struct K1Launch {
 void launch_ranges(tsk_db *db, const Soa &q, SearchPlanDev &p, bool spans_given, cudaStream_t st);
 void launch_plan_items(SearchPlanDev &p, int slots, int stride, cudaStream_t st);
 void launch_qprep(const Soa &q, QRec *out, int *flags, unsigned long long *cmax_bits, cudaStream_t st);
+bool mapped_columns(const tsk_columns *c, tsk_columns *dev);
+void launch_qprep_mapped(const tsk_columns &dev_cols, Soa &q, QRec *out, int *flags, unsigned long long *cmax_bits,
+                         cudaStream_t st);
 double soa_cmax(const Soa &s, cudaStream_t st);
 void soa_group_bounds(Soa &s, cudaStream_t st);  // GBound per GB_SIZE segments
 void launch_k1(const K1Launch &L, int grid, cudaStream_t st);
