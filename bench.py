@@ -467,7 +467,7 @@ def run_ours(args, cfg):
                 "planner": args.planner, "plan_s": t_plan,
                 "m": M_BINS, "interactions_per_step": int(total_ints / args.steps),
                 "hits_per_step": int(total_hits / args.steps),
-                "l2": "inputs larger than L2 (entry SoA 137 B/segment resident in HBM)",
+                "l2": "inputs larger than L2 (entry SoA 141 B/segment resident in HBM)",
                 "parallelism": f"dp{world} (contiguous interaction-balanced batch shards; no collective)",
             },
             "response_time_s": t_e2e / args.steps,

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstring>
 
+#include "filter.cuh"
 #include "tsk_internal.cuh"
 
 namespace tsk {
@@ -35,7 +36,7 @@ void DBuf::release(cudaStream_t) {
 
 void soa_alloc(Soa &s, int64_t n, bool with_ids, cudaStream_t st) {
     size_t nn = (size_t)(n > 0 ? n : 1);
-    size_t per = 15 * sizeof(double) + (with_ids ? 2 * sizeof(int64_t) : 0) + 1;
+    size_t per = 15 * sizeof(double) + (with_ids ? 2 * sizeof(int64_t) : 0) + sizeof(float) + 1;
     const size_t ngb = (nn + GB_SIZE - 1) / GB_SIZE;
     s.storage.reserve(nn * per + ngb * sizeof(GBound) + 64, st);
     char *base = s.storage.as<char>();
@@ -53,6 +54,8 @@ void soa_alloc(Soa &s, int64_t n, bool with_ids, cudaStream_t st) {
     } else {
         s.traj = s.seg = nullptr;
     }
+    s.sr32 = reinterpret_cast<float *>(base);
+    base += nn * sizeof(float);
     s.unsafe = reinterpret_cast<uint8_t *>(base);
     base += nn;
     // group bounds after the byte column, 16-byte aligned
@@ -113,7 +116,8 @@ __global__ void k_hoist(int64_t n, const double *__restrict__ ts, const double *
                         const double *__restrict__ ey, const double *__restrict__ ez,
                         double *__restrict__ dx, double *__restrict__ dy, double *__restrict__ dz,
                         double *__restrict__ rcp, double *__restrict__ vx, double *__restrict__ vy,
-                        double *__restrict__ vz, uint8_t *__restrict__ unsafe, int *flags) {
+                        double *__restrict__ vz, float *__restrict__ sr32, uint8_t *__restrict__ unsafe,
+                        int *flags) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const double t0 = ts[i];
@@ -121,6 +125,7 @@ __global__ void k_hoist(int64_t n, const double *__restrict__ ts, const double *
         const SegHoist h = seg_hoist(t0, te[i], s, e);
         dx[i] = h.d[0]; dy[i] = h.d[1]; dz[i] = h.d[2];
         vx[i] = h.v[0]; vy[i] = h.v[1]; vz[i] = h.v[2];
+        sr32[i] = f32_speed(h.v[0], h.v[1], h.v[2]);
         rcp[i] = h.rcp;
         unsafe[i] = h.unsafe ? 1 : 0;
         if (h.unsafe) atomicOr(&flags[0], 1);
@@ -139,7 +144,7 @@ void soa_hoist(Soa &s, cudaStream_t st) {
     TSK_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), st));
     int grid = (int)std::min<int64_t>((s.n + 255) / 256, 148 * 16);
     k_hoist<<<grid, 256, 0, st>>>(s.n, s.ts, s.te, s.sx, s.sy, s.sz, s.ex, s.ey, s.ez, s.dx, s.dy,
-                                  s.dz, s.rcp, s.vx, s.vy, s.vz, s.unsafe, flags);
+                                  s.dz, s.rcp, s.vx, s.vy, s.vz, s.sr32, s.unsafe, flags);
     TSK_CUDA(cudaGetLastError());
     int h[2];
     TSK_CUDA(cudaMemcpyAsync(h, flags, sizeof(h), cudaMemcpyDeviceToHost, st));

@@ -231,6 +231,27 @@ TSK_HD void f32_query(double ts, double sx, double sy, double sz, double ext, do
     out[5] = TSK_F2F_RU((1.0 + 0x1p-8) * (dthr + lq) + it.delta);
 }
 
+// sr >= |v| in FP32 (rounded up); hoisted per entry at upload.
+TSK_HD float f32_speed(double vx, double vy, double vz) {
+    return TSK_F2F_RU(sqrt(vx * vx + vy * vy + vz * vz) * (1.0 + 0x1p-40));
+}
+
+// FP32 view of a candidate (its start, start time and hoisted velocity;
+// sr = f32_speed of the velocity).
+TSK_HD CandF32 f32_cand_sr(double ts, double sx, double sy, double sz, double vx, double vy, double vz, float sr,
+                           const F32Item &it) {
+    CandF32 c;
+    const double dt = ts - it.t0;
+    c.px = TSK_F2F_RN(fma(-dt, vx, sx - it.ox));
+    c.py = TSK_F2F_RN(fma(-dt, vy, sy - it.oy));
+    c.pz = TSK_F2F_RN(fma(-dt, vz, sz - it.oz));
+    c.vx = TSK_F2F_RN(vx);
+    c.vy = TSK_F2F_RN(vy);
+    c.vz = TSK_F2F_RN(vz);
+    c.sr = sr;
+    return c;
+}
+
 // FP32 view of a candidate (its start, start time and hoisted velocity).
 TSK_HD CandF32 f32_cand(double ts, double sx, double sy, double sz, double vx, double vy, double vz,
                         const F32Item &it) {
@@ -242,7 +263,7 @@ TSK_HD CandF32 f32_cand(double ts, double sx, double sy, double sz, double vx, d
     c.vx = TSK_F2F_RN(vx);
     c.vy = TSK_F2F_RN(vy);
     c.vz = TSK_F2F_RN(vz);
-    c.sr = TSK_F2F_RU(sqrt(vx * vx + vy * vy + vz * vz) * (1.0 + 0x1p-40));
+    c.sr = f32_speed(vx, vy, vz);
     return c;
 }
 

@@ -327,11 +327,13 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
                     rte[k] = L.e.te[e];
                     unsafe_r |= L.e.unsafe[e] != 0;
                     if (item_f32)
-                        c = f32_cand(rts[k], L.e.sx[e], L.e.sy[e], L.e.sz[e], L.e.vx[e], L.e.vy[e], L.e.vz[e], fi_sh);
-                    wmin = fmin(wmin, rts[k]);
-                    wmax = fmax(wmax, rte[k]);
-                    wmin_te = fmin(wmin_te, rte[k]);
-                    wmax_ts = fmax(wmax_ts, rts[k]);
+                        c = f32_cand_sr(rts[k], L.e.sx[e], L.e.sy[e], L.e.sz[e], L.e.vx[e], L.e.vy[e], L.e.vz[e],
+                                        L.e.sr32[e], fi_sh);
+                    // times are finite (validated): plain selects, no NaN handling
+                    wmin = rts[k] < wmin ? rts[k] : wmin;
+                    wmax = rte[k] > wmax ? rte[k] : wmax;
+                    wmin_te = rte[k] < wmin_te ? rte[k] : wmin_te;
+                    wmax_ts = rts[k] > wmax_ts ? rts[k] : wmax_ts;
                 }
                 valid_any |= valid;
                 wcs[0 * WCAND + i] = c.px; wcs[1 * WCAND + i] = c.py; wcs[2 * WCAND + i] = c.pz;

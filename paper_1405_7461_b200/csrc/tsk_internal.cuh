@@ -79,6 +79,7 @@ struct Soa {
     double *dx = nullptr, *dy = nullptr, *dz = nullptr, *rcp = nullptr;
     double *vx = nullptr, *vy = nullptr, *vz = nullptr;
     int64_t *traj = nullptr, *seg = nullptr;
+    float *sr32 = nullptr;  // FP32 pre-filter speed bound (filter.cuh f32_speed)
     uint8_t *unsafe = nullptr;
     int any_unsafe = 0;
     int sorted = 1;  // ts non-decreasing
