@@ -532,12 +532,10 @@ void launch_ranges(tsk_db *db, const Soa &q, SearchPlanDev &p, bool spans_given,
 
 // ── work items of a plan ───────────────────────────────────────────────────
 
-// Single block: choose the candidate sub-tile count so the grid gets at
-// least ~4 waves of items, then scan items per batch.
-__global__ void __launch_bounds__(1024, 1) k_plan_items(int64_t nb, const int64_t *__restrict__ lo, const int64_t *__restrict__ hi,
-                             const int64_t *__restrict__ first, const int64_t *__restrict__ last,
-                             int64_t *__restrict__ item_off, int64_t *__restrict__ meta,
-                             int64_t slots, int stride) {
+// Single block: choose the query tile and the candidate sub-tile count so
+// the grid gets at least ~4 waves of items, then count items per work unit
+// (plan_unit: batch pairs sharing candidates, and the rest) and scan them.
+__global__ void __launch_bounds__(1024, 1) k_plan_items(SearchPlanDev p, int64_t slots, int stride, int pair) {
     typedef cub::BlockReduce<long long, 1024> BR;
     typedef cub::BlockScan<long long, 1024> BS;
     __shared__ union {
@@ -546,15 +544,17 @@ __global__ void __launch_bounds__(1024, 1) k_plan_items(int64_t nb, const int64_
     } tmp;
     __shared__ long long carry, tiles_sh;
     __shared__ int sub_sh;
+    const int64_t nb = p.nb;
     // query tile: K1_TQ, halved (down to 32) while the grid would get fewer
-    // than 4 waves of items — small plans otherwise under-fill 148 SMs
+    // than 4 waves of single-batch items — small plans otherwise under-fill
+    // 148 SMs
     const long long want = 4 * slots;
     int tqs = K1_TQ;
     for (;;) {
         long long acc = 0;
         for (int64_t b = threadIdx.x; b < nb; b += blockDim.x) {
-            long long c = first[b] >= 0 ? last[b] - first[b] + 1 : 0;
-            long long tq = (hi[b] - lo[b] + 1 + tqs - 1) / tqs;
+            long long c = p.first[b] >= 0 ? p.last[b] - p.first[b] + 1 : 0;
+            long long tq = (p.hi[b] - p.lo[b] + 1 + tqs - 1) / tqs;
             acc += ((c + stride - 1) / stride) * tq;
         }
         long long tiles = BR(tmp.r).Sum(acc);
@@ -571,33 +571,39 @@ __global__ void __launch_bounds__(1024, 1) k_plan_items(int64_t nb, const int64_
         carry = 0;
     }
     __syncthreads();
+    // pairing only when the plan is big enough to fill the grid with full tiles
+    const int pr = pair && tqs == K1_TQ;
     const long long ct = (long long)stride * sub_sh;
-    for (int64_t base = 0; base < nb; base += blockDim.x) {
-        int64_t b = base + threadIdx.x;
+    const int64_t nu = plan_units(nb);
+    for (int64_t base = 0; base < nu; base += blockDim.x) {
+        int64_t u = base + threadIdx.x;
         long long v = 0;
-        if (b < nb) {
-            long long c = first[b] >= 0 ? last[b] - first[b] + 1 : 0;
-            long long tq = (hi[b] - lo[b] + 1 + tqs - 1) / tqs;
-            v = ((c + ct - 1) / ct) * tq;
+        if (u < nu) {
+            const Unit U = plan_unit(p, u, tqs, pr);
+            if (U.f <= U.l) {
+                const long long c = U.l - U.f + 1;
+                const long long tq = U.b1 >= 0 ? 1 : (U.s + tqs - 1) / tqs;
+                v = ((c + ct - 1) / ct) * tq;
+            }
         }
         long long ex, agg;
         BS(tmp.s).ExclusiveSum(v, ex, agg);
-        if (b < nb) item_off[b] = carry + ex;
+        if (u < nu) p.item_off[u] = carry + ex;
         __syncthreads();
         if (threadIdx.x == 0) carry += agg;
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        item_off[nb] = carry;
-        meta[0] = carry;
-        meta[1] = sub_sh;
-        meta[2] = tqs;
+        p.item_off[nu] = carry;
+        p.meta[0] = carry;
+        p.meta[1] = sub_sh;
+        p.meta[2] = tqs;
+        p.meta[3] = pr;
     }
 }
 
-void launch_plan_items(SearchPlanDev &p, int slots, int stride, cudaStream_t st) {
-    k_plan_items<<<1, 1024, 0, st>>>(p.nb, p.lo, p.hi, p.first, p.last, p.item_off, p.meta, slots,
-                                     stride);
+void launch_plan_items(SearchPlanDev &p, int slots, int stride, int pair, cudaStream_t st) {
+    k_plan_items<<<1, 1024, 0, st>>>(p, slots, stride, pair);
     TSK_CUDA(cudaGetLastError());
 }
 

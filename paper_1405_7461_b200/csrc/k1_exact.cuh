@@ -137,9 +137,15 @@ __device__ __forceinline__ Hit rare_pair(const Cand &r, const QRec &Q, double cc
 
 struct ItemCtx {
     int64_t b, lo_q, first_c, c_hi;  // batch, tile's first query ordinal, tile's candidate range
-    int64_t q0;                      // first query offset within batch (tile)
-    int nt;                          // staged queries
+    int64_t q0;                      // first query offset within batch b (tile)
+    int64_t b1;                      // shared unit: the second batch (queries js..nt-1), else -1
+    int nt, js;                      // staged queries; queries of batch b (nt when single)
 };
+
+// Per-item counters are kept per batch in one 64-bit word: the low half
+// for batch b, the high half for b1 (a warp's counts in one item are far
+// below 2^32).
+constexpr unsigned long long CNT_B1 = 1ull << 32;
 
 __device__ __forceinline__ uint64_t make_key(const K1Launch &L, int64_t b, int64_t e_off,
                                              int64_t q_off) {
@@ -247,6 +253,8 @@ struct __align__(16) QF32 {
 // Per-warp context of the current sub-tile, read by the flush.
 struct WarpCtx {
     uint64_t key_base0;     // key of (b, e_off of candidate 0, it.q0) without the j term
+    uint64_t key_base1;     // the same for b1 (query offset 0 at tile index js)
+    int js;                 // tile index of b1's first query (nt when single)
     double wmin_te, wmax;   // min te / max te of the warp's candidates (tb cases)
     int64_t wbase;          // entry ordinal of the warp's candidate 0
     int nvalid;             // valid candidates of the warp (the rest are past the item)
@@ -281,7 +289,7 @@ __device__ __forceinline__ void append_hit_w(const FlushCfg &C, bool hit, uint64
 // solve (core.py:503-558), then the warp-aggregated append.
 template <int TA, int TB, bool SLOW>
 __device__ __noinline__ void rare_flush(const QRec *__restrict__ qt, const uint32_t *wq, int warp, int n_items,
-                                        int lane, unsigned &n_hit) {
+                                        int lane, unsigned long long &n_hit) {
     const FlushCfg &C = k1_fcfg;
     const double d2 = C.d2;
     const double wmin_te = k1_wctx[warp].wmin_te, wmax_te = k1_wctx[warp].wmax;
@@ -289,6 +297,7 @@ __device__ __noinline__ void rare_flush(const QRec *__restrict__ qt, const uint3
     h.hit = false;
     h.tb = h.te = 0.0;
     uint64_t key = 0;
+    bool second = false;
     const uint32_t ent = lane < n_items ? wq[lane] : 0u;
     const int ci = (int)(ent >> 16), j = (int)(ent & 0xffffu);
     // candidates past the item's range can be queued (flagged with a huge
@@ -315,11 +324,14 @@ __device__ __noinline__ void rare_flush(const QRec *__restrict__ qt, const uint3
         const bool plain = no_overflow(aa, dot, e) && mag >= 0x1p-900;
         if (ex && (flat || !plain || !(e > m) || !(q1 > m) || vertex_in))
             h = rare_pair(r, *qrec, cc, aa, dot, e, d2);
-        // candidate ci shifts the entry offset, query j the query offset
-        key = k1_wctx[warp].key_base0 + (C.query_major ? ((uint64_t)j << C.minor_bits) + (uint64_t)ci
-                                           : ((uint64_t)ci << C.minor_bits) + (uint64_t)j);
+        // candidate ci shifts the entry offset, query j the query offset,
+        // within the batch the query belongs to
+        second = j >= k1_wctx[warp].js;
+        const uint64_t jj = (uint64_t)(second ? j - k1_wctx[warp].js : j);
+        key = (second ? k1_wctx[warp].key_base1 : k1_wctx[warp].key_base0) +
+              (C.query_major ? (jj << C.minor_bits) + (uint64_t)ci : ((uint64_t)ci << C.minor_bits) + jj);
     }
-    n_hit += h.hit ? 1u : 0u;
+    n_hit += h.hit ? (second ? CNT_B1 : 1ull) : 0ull;
     append_hit_w(C, h.hit, key, h.tb, h.te, lane);
 }
 
@@ -387,28 +399,39 @@ __device__ __forceinline__ double warp_max(double v) {
     return v;
 }
 
-// Decode work item `item` of the plan (k_plan_items: per batch, candidate
-// tiles of ct entries times query tiles of tqs queries).
+// Decode work item `item` of the plan (k_plan_items: per work unit,
+// candidate tiles of ct entries times query tiles of tqs queries; a shared
+// unit has one tile holding both batches' queries).
 __device__ __forceinline__ ItemCtx decode_item(const K1Launch &L, int64_t item, int64_t ct, int64_t tqs) {
-    // batch = last b with item_off[b] <= item (a non-empty batch)
-    int64_t a = 0, z = L.plan.nb;
+    // unit = last u with item_off[u] <= item (a non-empty unit)
+    int64_t a = 0, z = plan_units(L.plan.nb);
     while (z - a > 1) {
         int64_t m = (a + z) >> 1;
         if (L.plan.item_off[m] <= item) a = m;
         else z = m;
     }
-    const int64_t b = a;
-    const int64_t local = item - L.plan.item_off[b];
-    const int64_t s_b = L.plan.hi[b] - L.plan.lo[b] + 1;
-    const int64_t tq_n = (s_b + tqs - 1) / tqs;
-    const int64_t tq = local % tq_n, tc = local / tq_n;
+    const Unit U = plan_unit(L.plan, a, tqs, (int)L.plan.meta[3]);
+    const int64_t local = item - L.plan.item_off[a];
     ItemCtx c;
-    c.b = b;
-    c.q0 = tq * tqs;
-    c.lo_q = L.plan.lo[b] + c.q0;
-    c.nt = (int)(s_b - c.q0 < tqs ? s_b - c.q0 : tqs);
-    c.first_c = L.plan.first[b] + tc * ct;
-    c.c_hi = c.first_c + ct - 1 < L.plan.last[b] ? c.first_c + ct - 1 : L.plan.last[b];
+    c.b = U.b;
+    c.b1 = U.b1;
+    int64_t tc;
+    if (U.b1 >= 0) {  // shared: one tile with both batches' queries
+        tc = local;
+        c.q0 = 0;
+        c.nt = (int)U.s;
+        c.js = (int)U.js;
+    } else {
+        const int64_t tq_n = (U.s + tqs - 1) / tqs;
+        const int64_t tq = local % tq_n;
+        tc = local / tq_n;
+        c.q0 = tq * tqs;
+        c.nt = (int)(U.s - c.q0 < tqs ? U.s - c.q0 : tqs);
+        c.js = c.nt;
+    }
+    c.lo_q = U.lo_q + c.q0;
+    c.first_c = U.f + tc * ct;
+    c.c_hi = c.first_c + ct - 1 < U.l ? c.first_c + ct - 1 : U.l;
     return c;
 }
 
@@ -487,7 +510,7 @@ __device__ __forceinline__ int4 warp_window(const R *q, const double *pm, int nt
 // and the last partial batch when the range is done (qn: warp-uniform).
 template <int TA, int TB, bool SLOW, int CPT>
 __device__ __forceinline__ void flush_queue(const QRec *__restrict__ qt, uint32_t *wq, int warp, int lane, int &qn,
-                                            bool done, unsigned &n_hit) {
+                                            bool done, unsigned long long &n_hit) {
     while (qn >= 32 || (done && qn > 0)) {
         const int nf = qn < 32 ? qn : 32;
         __syncwarp();
@@ -504,41 +527,54 @@ __device__ __forceinline__ void flush_queue(const QRec *__restrict__ qt, uint32_
     }
 }
 
-// Per-batch 64-bit counters: warp sums → block sums → one atomic per item.
+// Per-batch 64-bit counters: warp sums → block sums → atomics per item
+// (low halves to batch b, high halves to b1).
 // red_ev (optional): the block's evaluated-pair sum, added to L.eval_count.
-__device__ __forceinline__ void item_counters(const K1Launch &L, int64_t b, unsigned n_ov, unsigned n_hit, int lane,
-                                              int tid, unsigned long long *red_ov, unsigned long long *red_hit,
-                                              const unsigned long long *red_ev = nullptr) {
+__device__ __forceinline__ void item_counters(const K1Launch &L, const ItemCtx &it, unsigned long long n_ov,
+                                              unsigned long long n_hit, int lane, int tid,
+                                              unsigned long long *red, const unsigned long long *red_ev = nullptr) {
     for (int o = 16; o; o >>= 1) {
         n_ov += __shfl_xor_sync(0xffffffffu, n_ov, o);
         n_hit += __shfl_xor_sync(0xffffffffu, n_hit, o);
     }
     if (lane == 0 && (n_ov | n_hit)) {
-        atomicAdd(red_ov, (unsigned long long)n_ov);
-        atomicAdd(red_hit, (unsigned long long)n_hit);
+        atomicAdd(&red[0], n_ov & 0xffffffffull);
+        atomicAdd(&red[1], n_hit & 0xffffffffull);
+        atomicAdd(&red[2], n_ov >> 32);
+        atomicAdd(&red[3], n_hit >> 32);
     }
     __syncthreads();
     if (tid == 0) {
-        if (*red_ov) atomicAdd(&L.plan.ovl[b], *red_ov);
-        if (*red_hit) atomicAdd(&L.plan.hits[b], *red_hit);
+        if (red[0]) atomicAdd(&L.plan.ovl[it.b], red[0]);
+        if (red[1]) atomicAdd(&L.plan.hits[it.b], red[1]);
+        if (it.b1 >= 0 && red[2]) atomicAdd(&L.plan.ovl[it.b1], red[2]);
+        if (it.b1 >= 0 && red[3]) atomicAdd(&L.plan.hits[it.b1], red[3]);
         if (red_ev && *red_ev) atomicAdd(L.eval_count, *red_ev);
     }
     __syncthreads();
 }
 
-
 // Temporal overlaps of a lane's candidates with staged queries j0..j1-1
 // (TSK_OVERLAPS_ONLY: the perfmodel's temporal-miss fractions).
 template <int CPT, class R>
-__device__ __forceinline__ unsigned count_overlaps(const R *q, int j0, int j1, const double (&ts)[CPT],
-                                                   const double (&te)[CPT]) {
-    unsigned n = 0;
+__device__ __forceinline__ unsigned long long count_overlaps(const R *q, int j0, int j1, int js, const double (&ts)[CPT],
+                                                             const double (&te)[CPT]) {
+    unsigned long long n = 0;
     for (int j = j0; j < j1; ++j) {
         const double cts = rec_ts(q[j]), cte = rec_te(q[j]);
+        const unsigned long long inc = j >= js ? CNT_B1 : 1ull;
 #pragma unroll
-        for (int k = 0; k < CPT; ++k) n += (ts[k] <= cte && cts <= te[k]) ? 1u : 0u;
+        for (int k = 0; k < CPT; ++k) n += (ts[k] <= cte && cts <= te[k]) ? inc : 0ull;
     }
     return n;
+}
+
+// Overlaps of index range [a, b) split at js into the two batch halves.
+__device__ __forceinline__ unsigned long long split_count(int a, int b, int js) {
+    if (b <= a) return 0ull;
+    const int lo = b < js ? b : js;   // [a, min(b, js)) in batch b
+    const int hi = a > js ? a : js;   // [max(a, js), b) in batch b1
+    return (unsigned long long)(lo > a ? lo - a : 0) + (unsigned long long)(b > hi ? b - hi : 0) * CNT_B1;
 }
 
 }  // namespace tsk

@@ -90,7 +90,8 @@ __device__ __noinline__ uint4 f32_scan(uint32_t qa, uint32_t qa_end, uint32_t ba
             rte[k] = i < nv ? k1_fcfg.te[wb + i] : -INFINITY;
         }
     }
-    unsigned n_ov = 0;
+    unsigned long long n_ov = 0;
+    const uint32_t qa_js = base + (uint32_t)k1_wctx[warp].js * (uint32_t)sizeof(QF32);  // b1's first query
     for (; qa < qa_end; qa += (uint32_t)sizeof(QF32)) {
         float qts, qx, qy, qz, qa4, qb4, p0, p1;
         lds4f(qa, qts, qx, qy, qz);
@@ -109,7 +110,7 @@ __device__ __noinline__ uint4 f32_scan(uint32_t qa, uint32_t qa_end, uint32_t ba
                 if (TA == TA_C) ov = rts[k] <= cte;
                 else if (TA == TA_R) ov = cts <= rte[k];
                 else ov = rts[k] <= cte && cts <= rte[k];
-                n_ov += ov ? 1u : 0u;
+                n_ov += ov ? (qa >= qa_js ? CNT_B1 : 1ull) : 0ull;
             }
             cand[k] = f32_flag_r2(c[k], qts, qx, qy, qz, R2) && ov;
             any |= cand[k];
@@ -130,13 +131,14 @@ __device__ __noinline__ uint4 f32_scan(uint32_t qa, uint32_t qa_end, uint32_t ba
             break;
         }
     }
-    return make_uint4(qa, (unsigned)qn, n_ov, 0u);
+    return make_uint4(qa, (unsigned)qn, (unsigned)(n_ov & 0xffffffffull), (unsigned)(n_ov >> 32));
 }
 
 // One (TA, TB) range of the window: scan, flush 32 at a time, resume.
 template <int TA, int TB, bool CNT>
 __device__ __forceinline__ void f32_range(const QRec *__restrict__ qt, const QF32 *__restrict__ sqf, int j0,
-                                          int j1, int warp, int lane, unsigned &n_ov, unsigned &n_hit) {
+                                          int j1, int warp, int lane, unsigned long long &n_ov,
+                                          unsigned long long &n_hit) {
     if (j0 >= j1) return;
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(sqf);
     uint32_t qa = base + (uint32_t)j0 * (uint32_t)sizeof(QF32);
@@ -147,7 +149,7 @@ __device__ __forceinline__ void f32_range(const QRec *__restrict__ qt, const QF3
         const uint4 o = f32_scan<TA, CNT>(qa, qa_end, base, qn, warp, lane);
         qa = o.x;
         qn = (int)o.y;
-        n_ov += o.z;
+        n_ov += (unsigned long long)o.z + (unsigned long long)o.w * CNT_B1;
         const bool done = qa >= qa_end;
         flush_queue<TA, TB, false, CPT>(qt, wq, warp, lane, qn, done, n_hit);
         if (done) break;
@@ -159,17 +161,19 @@ __device__ __forceinline__ void f32_range(const QRec *__restrict__ qt, const QF3
 template <int TA>
 __device__ __forceinline__ void all_range(const QRec *__restrict__ qt, const QF32 *__restrict__ sqf, int j0, int j1,
                                           const double (&rts)[CPT], const double (&rte)[CPT], int warp, int lane,
-                                          unsigned &n_ov, unsigned &n_hit) {
+                                          unsigned long long &n_ov, unsigned long long &n_hit) {
     uint32_t *const wq = f_queue(warp);
     int qn = 0;
+    const int js = k1_wctx[warp].js;
     for (int j = j0; j < j1; ++j) {
         const double cts = sqf[j].ts64, cte = sqf[j].te64;
+        const unsigned long long inc = j >= js ? CNT_B1 : 1ull;
         bool cand[CPT];
         bool any = false;
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
             cand[k] = rts[k] <= cte && cts <= rte[k];
-            n_ov += cand[k] ? 1u : 0u;
+            n_ov += cand[k] ? inc : 0ull;
             any |= cand[k];
         }
         if (__any_sync(0xffffffffu, any)) {
@@ -194,7 +198,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
     __shared__ ItemCtx it_sh;
     __shared__ int64_t item_sh;
     __shared__ int flags_sh;      // bit 0: unsafe query, bit 1: te not sorted
-    __shared__ unsigned long long red_ov, red_hit, red_ev;
+    __shared__ unsigned long long red[4], red_ev;  // per-batch overlap / hit sums, evaluated pairs
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) fill_flush_cfg(L);
@@ -217,8 +221,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
             const int64_t item = (int64_t)atomicAdd(L.item_counter, 1ull);
             item_sh = item;
             if (item < total) it_sh = decode_item(L, item, ct, tqs);
-            red_ov = 0;
-            red_hit = 0;
+            red[0] = red[1] = red[2] = red[3] = 0;
             red_ev = 0;
             flags_sh = 0;
         }
@@ -303,7 +306,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
         te_scans(sqf, it.nt, pm, sm, warp, lane);
         __syncthreads();
 
-        unsigned n_ov = 0, n_hit = 0;
+        unsigned long long n_ov = 0, n_hit = 0;  // batch b in the low half, b1 in the high half
         unsigned long long n_ev = 0;  // pairs evaluated by the pre-filter (warp-uniform)
         for (int s = 0; s < sub; ++s) {
             const int64_t base = it.first_c + (int64_t)s * STRIDE;
@@ -348,6 +351,8 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
             wmax_ts = warp_max(wmax_ts);
             if (lane == 0) {
                 k1_wctx[warp].key_base0 = make_key(L, it.b, wbase - L.plan.first[it.b], it.q0);
+                k1_wctx[warp].key_base1 = it.b1 >= 0 ? make_key(L, it.b1, wbase - L.plan.first[it.b1], 0) : 0;
+                k1_wctx[warp].js = it.js;
                 k1_wctx[warp].wbase = wbase;
                 const int64_t nv = it.c_hi - wbase + 1;
                 k1_wctx[warp].nvalid = nv < 0 ? 0 : (nv > WCAND ? WCAND : (int)nv);
@@ -358,7 +363,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
             const int4 w = warp_window(sqf, pm, it.nt, *L.q_unsorted != 0, wmin, wmax, wmax_ts, lane);
             const int jlo = w.x, ja = w.y, jb = w.z, jhi = w.w;
             if (L.overlaps_only) {
-                n_ov += count_overlaps<CPT>(sqf, jlo, jhi, rts, rte);
+                n_ov += count_overlaps<CPT>(sqf, jlo, jhi, it.js, rts, rte);
                 continue;
             }
             if (!item_f32 || __any_sync(0xffffffffu, unsafe_r)) {
@@ -376,8 +381,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
                 // (the exact path decides the clip cases per pair)
 #pragma unroll
                 for (int k = 0; k < CPT; ++k) {
-                    const int c = upper_bound_ts(sqf, it.nt, rte[k]) - lower_bound_te(sqf, it.nt, rts[k]);
-                    n_ov += c > 0 ? (unsigned)c : 0u;
+                    n_ov += split_count(lower_bound_te(sqf, it.nt, rts[k]), upper_bound_ts(sqf, it.nt, rte[k]), it.js);
                 }
                 f32_range<TA_BOTH, TB_DYN, false>(qt, sqf, jlo, jhi, warp, lane, n_ov, n_hit);
                 continue;
@@ -387,7 +391,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
             if (jlo < ja && pm[ja - 1] < wmin_te && te_sorted) {
 #pragma unroll
                 for (int k = 0; k < CPT; ++k)
-                    n_ov += (unsigned)(ja - clampi(lower_bound_te(sqf, it.nt, rts[k]), jlo, ja));
+                    n_ov += split_count(clampi(lower_bound_te(sqf, it.nt, rts[k]), jlo, ja), ja, it.js);
                 f32_range<TA_C, TB_R, false>(qt, sqf, jlo, ja, warp, lane, n_ov, n_hit);
             } else {
                 f32_range<TA_C, TB_DYN, true>(qt, sqf, jlo, ja, warp, lane, n_ov, n_hit);
@@ -398,14 +402,14 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
             if (jb < jhi && sm[jb] > wmax) {
 #pragma unroll
                 for (int k = 0; k < CPT; ++k)
-                    n_ov += (unsigned)(clampi(upper_bound_ts(sqf, it.nt, rte[k]), jb, jhi) - jb);
+                    n_ov += split_count(jb, clampi(upper_bound_ts(sqf, it.nt, rte[k]), jb, jhi), it.js);
                 f32_range<TA_R, TB_C, false>(qt, sqf, jb, jhi, warp, lane, n_ov, n_hit);
             } else {
                 f32_range<TA_R, TB_DYN, true>(qt, sqf, jb, jhi, warp, lane, n_ov, n_hit);
             }
         }
         if (lane == 0 && n_ev) atomicAdd(&red_ev, n_ev);
-        item_counters(L, it.b, n_ov, n_hit, lane, tid, &red_ov, &red_hit, &red_ev);
+        item_counters(L, it, n_ov, n_hit, lane, tid, red, &red_ev);
     }
 }
 

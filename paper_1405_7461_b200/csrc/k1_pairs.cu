@@ -77,7 +77,7 @@ __device__ __forceinline__ uint32_t *warp_q(int warp) { return reinterpret_cast<
 template <int TA, int TB, bool SLOW, bool CNT>
 __device__ __forceinline__ void pair_run(const QRec *__restrict__ sq, int j0, int j1, const CandF (&r)[K1_CPT],
                                          double wmin_te, double wmax_te, int warp, int lane,
-                                         unsigned &n_ov, unsigned &n_hit, const FilterK &K) {
+                                         unsigned long long &n_ov, unsigned long long &n_hit, const FilterK &K) {
     uint32_t *const wq = warp_q(warp);
     constexpr uint32_t STRIDE = (uint32_t)sizeof(QRec);
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(sq);
@@ -95,7 +95,7 @@ __device__ __forceinline__ void pair_run(const QRec *__restrict__ sq, int j0, in
 #pragma unroll
                 for (int k = 0; k < K1_CPT; ++k) {
                     const bool ov = r[k].ts <= cte && cts <= r[k].te;  // invalid lanes: ts = +inf
-                    if (CNT) n_ov += ov ? 1u : 0u;
+                    if (CNT) n_ov += ov ? 1ull : 0ull;
                     cand[k] = ov;
                 }
             } else {
@@ -110,7 +110,7 @@ __device__ __forceinline__ void pair_run(const QRec *__restrict__ sq, int j0, in
                         if (TA == TA_C) ov = r[k].ts <= Q.te;
                         else if (TA == TA_R) ov = Q.ts <= r[k].te;
                         else ov = r[k].ts <= Q.te && Q.ts <= r[k].te;
-                        n_ov += ov ? 1u : 0u;
+                        n_ov += ov ? 1ull : 0ull;
                     }
                     cand[k] = pair_filter<TA, TB>(r[k], Q, wmin_te, wmax_te, K) && ov;
                 }
@@ -147,14 +147,14 @@ __device__ __forceinline__ void pair_run(const QRec *__restrict__ sq, int j0, in
 template <bool SLOW>
 __device__ __forceinline__ void run_cases(const QRec *__restrict__ sq, int nt, int4 w, bool c_bisect,
                                           bool r_bisect, const CandF (&r)[K1_CPT], double wmin_te,
-                                          double wmax, int warp, int lane, unsigned &n_ov, unsigned &n_hit,
+                                          double wmax, int warp, int lane, unsigned long long &n_ov, unsigned long long &n_hit,
                                           const FilterK &K) {
     const int jlo = w.x, ja = w.y, jb = w.z, jhi = w.w;
     if (c_bisect && !SLOW) {
         // overlap <=> r.ts <= cte; cte ascending over the tile
 #pragma unroll
         for (int k = 0; k < K1_CPT; ++k)
-            n_ov += (unsigned)(ja - clampi(lower_bound_te(sq, nt, r[k].ts), jlo, ja));
+            n_ov += (unsigned long long)(ja - clampi(lower_bound_te(sq, nt, r[k].ts), jlo, ja));
         pair_run<TA_C, TB_R, SLOW, false>(sq, jlo, ja, r, wmin_te, wmax, warp, lane, n_ov, n_hit, K);
     } else {
         pair_run<TA_C, TB_DYN, SLOW, true>(sq, jlo, ja, r, wmin_te, wmax, warp, lane, n_ov, n_hit, K);
@@ -164,7 +164,7 @@ __device__ __forceinline__ void run_cases(const QRec *__restrict__ sq, int nt, i
         // overlap <=> cts <= r.te; cts ascending over the tile
 #pragma unroll
         for (int k = 0; k < K1_CPT; ++k)
-            n_ov += (unsigned)(clampi(upper_bound_ts(sq, nt, r[k].te), jb, jhi) - jb);
+            n_ov += (unsigned long long)(clampi(upper_bound_ts(sq, nt, r[k].te), jb, jhi) - jb);
         pair_run<TA_R, TB_C, SLOW, false>(sq, jb, jhi, r, wmin_te, wmax, warp, lane, n_ov, n_hit, K);
     } else {
         pair_run<TA_R, TB_DYN, SLOW, true>(sq, jb, jhi, r, wmin_te, wmax, warp, lane, n_ov, n_hit, K);
@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
     __shared__ double sm[K1_TQ];  // suffix min of te over the tile
     __shared__ ItemCtx it_sh;
     __shared__ int64_t item_sh;
-    __shared__ unsigned long long red_ov, red_hit;
+    __shared__ unsigned long long red[4];  // per-batch overlap / hit sums
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) fill_flush_cfg(L);
@@ -198,8 +198,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
             const int64_t item = (int64_t)atomicAdd(L.item_counter, 1ull);
             item_sh = item;
             if (item < total) it_sh = decode_item(L, item, ct, tqs);
-            red_ov = 0;
-            red_hit = 0;
+            red[0] = red[1] = red[2] = red[3] = 0;
         }
         __syncthreads();
         if (item_sh >= total) break;
@@ -220,7 +219,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
         te_scans(sq, it.nt, pm, sm, warp, lane);
         __syncthreads();
 
-        unsigned n_ov = 0, n_hit = 0;
+        unsigned long long n_ov = 0, n_hit = 0;
         for (int s = 0; s < sub; ++s) {
             const int64_t base = it.first_c + (int64_t)s * STRIDE;
             if (base > it.c_hi) break;  // block-uniform
@@ -257,6 +256,8 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
             wmax_ts = warp_max(wmax_ts);
             if (lane == 0) {
                 k1_wctx[warp].key_base0 = make_key(L, it.b, wbase - L.plan.first[it.b], it.q0);
+                k1_wctx[warp].key_base1 = 0;  // no shared units in this kernel
+                k1_wctx[warp].js = it.nt;
                 k1_wctx[warp].wbase = wbase;
                 const int64_t nv = it.c_hi - wbase + 1;
                 k1_wctx[warp].nvalid = nv < 0 ? 0 : (nv > 32 * K1_CPT ? 32 * K1_CPT : (int)nv);
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
                     ts[k] = r[k].ts;
                     te[k] = r[k].te;
                 }
-                n_ov += count_overlaps<K1_CPT>(sq, w.x, w.w, ts, te);
+                n_ov += count_overlaps<K1_CPT>(sq, w.x, w.w, it.nt, ts, te);
                 continue;
             }
             const bool slow = launch_exact || unsafe_q || __any_sync(0xffffffffu, unsafe_r);
@@ -287,7 +288,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
                 run_cases<false>(sq, it.nt, w, c_tb_r && te_sorted, r_tb_c, r, wmin_te, wmax, warp, lane, n_ov,
                                  n_hit, K);
         }
-        item_counters(L, it.b, n_ov, n_hit, lane, tid, &red_ov, &red_hit);
+        item_counters(L, it, n_ov, n_hit, lane, tid, red);
     }
 }
 

@@ -306,12 +306,13 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     }
     tr.mark("queries");
 
-    // batch table: lo hi first last item_off(nb+1) meta(4) ovl hits
+    // batch table: lo hi first last item_off(units+1) meta(4) ovl hits
     size_t nbz = (size_t)nb;
-    db->batches.reserve((nbz * 7 + 8) * 8, st);
+    const size_t nuz = (size_t)plan_units(nb);
+    db->batches.reserve((nbz * 6 + nuz + 8) * 8, st);
     int64_t *d_lo = db->batches.as<int64_t>();
     int64_t *d_hi = d_lo + nbz, *d_first = d_hi + nbz, *d_last = d_first + nbz;
-    int64_t *d_off = d_last + nbz, *d_meta = d_off + nbz + 1;
+    int64_t *d_off = d_last + nbz, *d_meta = d_off + nuz + 1;
     unsigned long long *d_ovl = (unsigned long long *)(d_meta + 4);
     unsigned long long *d_hits = d_ovl + nbz;
     TSK_CUDA(cudaMemcpyAsync(d_lo, b_lo, nbz * 8, cudaMemcpyHostToDevice, st));
@@ -325,7 +326,10 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     const bool k1_f32 = k1_use_f32(d * d, db->cmax);
     const int bps = k1_blocks_per_sm(k1_f32);
     const int slots = sm_count(db->device) * bps;
-    launch_plan_items(plan, slots, K1_THREADS * k1_candidates_per_thread(k1_f32), st);
+    // batch pairs share candidate tiles in the FP32 kernel (not in the
+    // FP64 fallback kernel or for brute force's query-major keys)
+    launch_plan_items(plan, slots, K1_THREADS * k1_candidates_per_thread(k1_f32),
+                      (k1_f32 && !query_major) ? 1 : 0, st);
     launches += spans_given ? 1 : 2;
     tr.mark("ranges+items");
 

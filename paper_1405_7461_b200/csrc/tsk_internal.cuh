@@ -195,6 +195,81 @@ struct SearchPlanDev {
     unsigned long long *ovl, *hits;  // per batch
 };
 
+// Work units of a plan (k_plan_items / K1).  Batches are taken in pairs
+// (2k, 2k+1); unit 5k+0 is the candidate range the pair shares, evaluated
+// against both batches' queries in one tile (when they fit), units
+// 5k+1/5k+2 are batch 2k's candidates left/right of it and 5k+3/5k+4 batch
+// 2k+1's.  A pair that cannot share (a batch without candidates, disjoint
+// ranges, queries beyond one tile, batches not adjacent in the query order,
+// or pairing off) leaves unit 5k+0 empty and
+// puts each batch's whole range in its left unit.  Every (candidate, query)
+// pair of the plan is in exactly one unit.
+struct Unit {
+    int64_t b, b1;    // batch, second batch of a shared unit (else -1)
+    int64_t lo_q, s;  // first query ordinal and query count (both batches for a shared unit)
+    int64_t js;       // queries of b (s when single)
+    int64_t f, l;     // candidate segment (empty when f > l)
+};
+
+__device__ __forceinline__ Unit plan_unit(const SearchPlanDev &p, int64_t u, int64_t tqs, int pair) {
+    const int64_t k = u / 5, kind = u % 5;
+    const int64_t b0 = 2 * k, b1 = 2 * k + 1;
+    const bool has1 = b1 < p.nb;
+    const int64_t f0 = p.first[b0], l0 = p.last[b0];
+    const int64_t f1 = has1 ? p.first[b1] : -1, l1 = has1 ? p.last[b1] : -1;
+    const int64_t s0 = p.hi[b0] - p.lo[b0] + 1, s1 = has1 ? p.hi[b1] - p.lo[b1] + 1 : 0;
+    const int64_t ilo = f0 > f1 ? f0 : f1, ihi = l0 < l1 ? l0 : l1;
+    // (batches must be adjacent in the query order: spans-given plans may
+    // hold arbitrary, even overlapping, query ranges)
+    const bool shared = pair && has1 && f0 >= 0 && f1 >= 0 && s0 + s1 <= tqs && ilo <= ihi &&
+                        p.lo[b1] == p.hi[b0] + 1;
+    Unit U;
+    U.b1 = -1;
+    U.f = 1;
+    U.l = 0;  // empty
+    if (kind == 0) {
+        U.b = b0;
+        U.lo_q = p.lo[b0];
+        U.s = s0 + s1;
+        U.js = s0;
+        if (shared) {
+            U.b1 = b1;
+            U.f = ilo;
+            U.l = ihi;
+        }
+        return U;
+    }
+    const bool second = kind >= 3;
+    if (second && !has1) {
+        U.b = b0;
+        U.lo_q = p.lo[b0];
+        U.s = U.js = s0;
+        return U;
+    }
+    const int64_t b = second ? b1 : b0;
+    const int64_t f = second ? f1 : f0, l = second ? l1 : l0;
+    U.b = b;
+    U.lo_q = p.lo[b];
+    U.s = U.js = second ? s1 : s0;
+    if (f < 0) return U;  // no candidates
+    const bool left = kind == 1 || kind == 3;
+    if (!shared) {
+        if (left) {
+            U.f = f;
+            U.l = l;
+        }
+    } else if (left) {
+        U.f = f;
+        U.l = ilo - 1;
+    } else {
+        U.f = ihi + 1;
+        U.l = l;
+    }
+    return U;
+}
+
+__host__ __device__ __forceinline__ int64_t plan_units(int64_t nb) { return 5 * ((nb + 1) / 2); }
+
 struct K1Launch {
     Soa e;  // by value: device pointers
     const QRec *q;
@@ -217,7 +292,7 @@ struct K1Launch {
 };
 
 void launch_ranges(tsk_db *db, const Soa &q, SearchPlanDev &p, bool spans_given, cudaStream_t st);
-void launch_plan_items(SearchPlanDev &p, int slots, int stride, cudaStream_t st);
+void launch_plan_items(SearchPlanDev &p, int slots, int stride, int pair, cudaStream_t st);
 void launch_qprep(const Soa &q, QRec *out, int *flags, unsigned long long *cmax_bits, cudaStream_t st);
 bool mapped_columns(const tsk_columns *c, tsk_columns *dev);
 void launch_qprep_mapped(const tsk_columns &dev_cols, Soa &q, QRec *out, int *flags, unsigned long long *cmax_bits,
