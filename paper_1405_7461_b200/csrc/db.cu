@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(1024, 1) k_plan_items(SearchPlanDev p, int64_t
     // 148 SMs
     const long long want = 4 * slots;
     int tqs = K1_TQ;
-    for (;;) {
+    for (;;) {  // pair == 2 (testing): full tiles, always pair
         long long acc = 0;
         for (int64_t b = threadIdx.x; b < nb; b += blockDim.x) {
             long long c = p.first[b] >= 0 ? p.last[b] - p.first[b] + 1 : 0;
@@ -562,7 +562,7 @@ __global__ void __launch_bounds__(1024, 1) k_plan_items(SearchPlanDev p, int64_t
         __syncthreads();
         tiles = tiles_sh;
         __syncthreads();
-        if (tiles >= want || tqs <= 32) break;
+        if (tiles >= want || tqs <= 32 || pair == 2) break;
         tqs >>= 1;
     }
     if (threadIdx.x == 0) {
@@ -572,7 +572,7 @@ __global__ void __launch_bounds__(1024, 1) k_plan_items(SearchPlanDev p, int64_t
     }
     __syncthreads();
     // pairing only when the plan is big enough to fill the grid with full tiles
-    const int pr = pair && tqs == K1_TQ;
+    const int pr = pair == 2 || (pair && tqs == K1_TQ);
     const long long ct = (long long)stride * sub_sh;
     const int64_t nu = plan_units(nb);
     for (int64_t base = 0; base < nu; base += blockDim.x) {

@@ -328,8 +328,14 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     const int slots = sm_count(db->device) * bps;
     // batch pairs share candidate tiles in the FP32 kernel (not in the
     // FP64 fallback kernel or for brute force's query-major keys)
-    launch_plan_items(plan, slots, K1_THREADS * k1_candidates_per_thread(k1_f32),
-                      (k1_f32 && !query_major) ? 1 : 0, st);
+    // TSK_K1_PAIR=off|force (testing) disables pairing or forces it on
+    // small plans (full query tiles)
+    int pair = (k1_f32 && !query_major) ? 1 : 0;
+    if (const char *e = getenv("TSK_K1_PAIR")) {
+        if (!strcmp(e, "off")) pair = 0;
+        else if (!strcmp(e, "force") && pair) pair = 2;
+    }
+    launch_plan_items(plan, slots, K1_THREADS * k1_candidates_per_thread(k1_f32), pair, st);
     launches += spans_given ? 1 : 2;
     tr.mark("ranges+items");
 

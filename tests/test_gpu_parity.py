@@ -695,3 +695,41 @@ def test_pinned_query_columns_take_the_mapped_path_with_identical_results():
     r0 = search_device(store, index, pplan, 4.0)
     r1 = search_device(store, index, pplan, 4.0, queries_resident=True)
     assert r0.n == r1.n == len(want) and np.array_equal(r0.per_batch, r1.per_batch)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "normal", "exp"])
+def test_batch_pairs_sharing_candidate_tiles_match_unpaired_runs(kind, monkeypatch):
+    """K1 evaluates adjacent batch pairs against their shared candidates in
+    one tile (keys and counters split at the pair boundary).  Forced on for a
+    small plan, it must give the unpaired run's items, order, interval
+    endpoints and per-batch statistics; spans-given plans with overlapping
+    batches (the perfmodel's windows) must not pair."""
+    from paper_1405_7461_b200 import datagen
+    from paper_1405_7461_b200.engine import span_counts
+
+    store = datagen.generate(datagen.make_profile(kind, 600, seed=31, timesteps=120))
+    pool = datagen.generate(datagen.make_profile(kind, 80, seed=32, timesteps=120))
+    queries = datagen.sample_queries(pool, 25, seed=33)
+    index = tsk.build_index(store, 300)
+    for s in (40, 97, 128):
+        plan = tsk.periodic(queries, s, index)
+        monkeypatch.setenv("TSK_K1_PAIR", "off")
+        want, ws = tsk.run_search(store, index, plan, 6.0)
+        monkeypatch.setenv("TSK_K1_PAIR", "force")
+        got, gs = tsk.run_search(store, index, plan, 6.0)
+        assert len(want) > 0
+        for k in RES:
+            assert np.array_equal(getattr(got, k), getattr(want, k)), (kind, s, k)
+        assert [(t.hits, t.interactions) for t in gs.per_batch] == [(t.hits, t.interactions) for t in ws.per_batch]
+        assert (gs.temporal_misses, gs.spatial_misses) == (ws.temporal_misses, ws.spatial_misses)
+    # overlapping windows with given spans: counts equal the unpaired ones
+    lo = np.arange(0, len(queries) - 60, 11)
+    hi = lo + 59
+    first, last = tsk.candidate_ranges(index, queries.ts[lo], np.array([queries.te[a:b + 1].max() for a, b in zip(lo, hi)]))
+    keep = first >= 0
+    lo, hi, first, last = lo[keep], hi[keep], first[keep], last[keep]
+    monkeypatch.setenv("TSK_K1_PAIR", "off")
+    a = span_counts(store, queries, lo, hi, first, last, 6.0)
+    monkeypatch.setenv("TSK_K1_PAIR", "force")
+    b = span_counts(store, queries, lo, hi, first, last, 6.0)
+    assert np.array_equal(a, b)
