@@ -208,7 +208,7 @@ def test_calibration_on_this_gpu():
     sf = pm.calibrate_surfaces(grid, reps=2)
     for n in SURF:
         g = getattr(sf, n)
-        assert g.shape == (3, 3) and (g > 0).all() and np.isfinite(g).all(), n
+        assert g.shape == (3, 3) and (g >= 0).all() and np.isfinite(g).all() and g.max() > 0, n
     # hits cost at least what spatial misses cost on the biggest batches
     assert sf.all_hit[-1, -1] >= sf.spatial_miss[-1, -1]
     host = pm.calibrate_host(2000, [10, 40, 160, 640], reps=2)
