@@ -74,7 +74,7 @@ PLANNERS = {
     "greedy_max": lambda tsk, q, ix: tsk.greedy_max(q, ix, S_BATCH),
 }
 W_DECIDE, W_HIT = 50, 9  # FP64 flops per overlapping pair / extra per hit
-F32_OPS = 10.5  # FP32 pre-filter ops per evaluated pair: 6 separation + 3 norm + 1 compare + 2 threshold per 4 pairs
+F32_OPS = 10.25  # FP32 pre-filter ops per evaluated pair: 6 separation + 3 norm, plus per (query, lane) of 4 pairs 2 threshold + 2 min + 1 compare
 
 
 def log(*a):

@@ -277,27 +277,50 @@ inline float tsk_fma_dir(float a, float b, float c, int mode) {
 }
 #endif
 
+// |u|^2 of the pre-filter test, rounded down.
+TSK_HD float f32_n2(const CandF32 &c, float qts, float qx, float qy, float qz) {
+#ifdef __CUDA_ARCH__
+    const float ux = __fsub_rn(__fmaf_rn(qts, c.vx, c.px), qx);
+    const float uy = __fsub_rn(__fmaf_rn(qts, c.vy, c.py), qy);
+    const float uz = __fsub_rn(__fmaf_rn(qts, c.vz, c.pz), qz);
+    return __fmaf_rd(uz, uz, __fmaf_rd(uy, uy, __fmul_rd(ux, ux)));
+#else
+    const float ux = fmaf(qts, c.vx, c.px) - qx;
+    const float uy = fmaf(qts, c.vy, c.py) - qy;
+    const float uz = fmaf(qts, c.vz, c.pz) - qz;
+    return tsk_fma_dir(uz, uz, tsk_fma_dir(uy, uy, tsk_fma_dir(ux, ux, 0.f, FE_DOWNWARD), FE_DOWNWARD),
+                       FE_DOWNWARD);
+#endif
+}
+
+// n > R2: the pair cannot hit (false for NaN, so NaN flags).
+TSK_HD bool f32_far(float n, float R2) {
+#ifdef __CUDA_ARCH__
+    unsigned far;
+    asm("{.reg .pred p; setp.gt.f32 p, %1, %2; selp.u32 %0, 1, 0, p;}" : "=r"(far) : "f"(n), "f"(R2));
+    return far != 0u;
+#else
+    return n > R2;
+#endif
+}
+
+// min that propagates NaN (a NaN norm must keep its query flagged).
+TSK_HD float f32_min_nan(float a, float b) {
+#ifdef __CUDA_ARCH__
+    float r;
+    asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+#else
+    return (a != a || b != b) ? NAN : (a < b ? a : b);
+#endif
+}
+
 // The pre-filter test against a given R2 >= (a sr + b)^2 (rounded up):
 // true = the pair may hit (NaN flags).  K1 passes one R2 per (query, lane),
 // computed with the largest sr of the lane's candidates (R grows with sr,
 // so each pair's own test below is implied).
 TSK_HD bool f32_flag_r2(const CandF32 &c, float qts, float qx, float qy, float qz, float R2) {
-#ifdef __CUDA_ARCH__
-    const float ux = __fsub_rn(__fmaf_rn(qts, c.vx, c.px), qx);
-    const float uy = __fsub_rn(__fmaf_rn(qts, c.vy, c.py), qy);
-    const float uz = __fsub_rn(__fmaf_rn(qts, c.vz, c.pz), qz);
-    const float n = __fmaf_rd(uz, uz, __fmaf_rd(uy, uy, __fmul_rd(ux, ux)));
-    unsigned far;
-    asm("{.reg .pred p; setp.gt.f32 p, %1, %2; selp.u32 %0, 1, 0, p;}" : "=r"(far) : "f"(n), "f"(R2));
-    return far == 0u;
-#else
-    const float ux = fmaf(qts, c.vx, c.px) - qx;
-    const float uy = fmaf(qts, c.vy, c.py) - qy;
-    const float uz = fmaf(qts, c.vz, c.pz) - qz;
-    const float n = tsk_fma_dir(uz, uz, tsk_fma_dir(uy, uy, tsk_fma_dir(ux, ux, 0.f, FE_DOWNWARD), FE_DOWNWARD),
-                                FE_DOWNWARD);
-    return !(n > R2);
-#endif
+    return !f32_far(f32_n2(c, qts, qx, qy, qz), R2);
 }
 
 // (a sr + b)^2 rounded up

@@ -389,6 +389,26 @@ __device__ __forceinline__ int upper_bound_ts(const R *q, int n, double v) {
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
+// lo[k] = #{j : te_j < ts[k]} and hi[k] = #{j : ts_j <= te[k]} over a tile
+// whose start and end times both ascend, given as plain arrays padded with
+// +inf up to twice the next power of two >= nt: all 2 CPT searches advance
+// together by binary lifting, so each step issues 2 CPT independent shared
+// loads and no bounds checks.
+template <int CPT>
+__device__ __forceinline__ void tile_bounds(const double *qts, const double *qte, int nt, const double (&ts)[CPT],
+                                            const double (&te)[CPT], int (&lo)[CPT], int (&hi)[CPT]) {
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) lo[k] = hi[k] = 0;
+    if (nt <= 0) return;
+    for (int step = nt > 1 ? 1 << (32 - __clz(nt - 1)) : 1; step; step >>= 1) {
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            if (qte[lo[k] + step - 1] < ts[k]) lo[k] += step;
+            if (qts[hi[k] + step - 1] <= te[k]) hi[k] += step;
+        }
+    }
+}
+
 __device__ __forceinline__ double warp_min(double v) {
     for (int o = 16; o; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;

@@ -13,10 +13,13 @@
 // (lanes l, l+32, l+64, l+96 of the warp's 128 consecutive entries) in FP32
 // pre-filter form, and each warp loops over the window of staged queries
 // that can overlap any of its candidates (entries and queries are both
-// start-time sorted, so the window is four binary searches, one per lane).
+// start-time sorted: on tiles whose end times ascend too, the window is the
+// min / max of the candidates' own overlap bounds, all found together by
+// binary lifting; else four binary searches, one per lane).
 //
-// Per (candidate, query): 9 FP32 ops and two compares decide "cannot hit"
-// for nearly every pair (f32_flag, with a proven error margin); flagged
+// Per (candidate, query): 9 FP32 ops decide "cannot hit" for nearly every
+// pair (f32_flag, with a proven error margin), one NaN-propagating min over
+// the lane's four norms and one compare per (query, lane); flagged
 // pairs are queued per warp and re-evaluated 32 at a time with the
 // reference's exact binary64 arithmetic (k1_exact.cuh), which is what makes
 // the result set bit-exact.  Overlaps are counted exactly: by bisection for
@@ -99,23 +102,35 @@ __device__ __noinline__ uint4 f32_scan(uint32_t qa, uint32_t qa_end, uint32_t ba
         double cts = 0.0, cte = 0.0;
         if (CNT) lds2d(qa + 32, cts, cte);
         bool cand[CPT];
-        bool any = false;
         const float R2 = f32_r2(qa4, srl, qb4);
+        if constexpr (CNT) {
+            bool any = false;
 #pragma unroll
-        for (int k = 0; k < CPT; ++k) {
-            bool ov = true;
-            if (CNT) {
+            for (int k = 0; k < CPT; ++k) {
                 // TA_C: the query started first, so it overlaps iff it ends at
                 // or after r.ts; TA_R: iff it starts at or before r.te
+                bool ov;
                 if (TA == TA_C) ov = rts[k] <= cte;
                 else if (TA == TA_R) ov = cts <= rte[k];
                 else ov = rts[k] <= cte && cts <= rte[k];
                 n_ov += ov ? (qa >= qa_js ? CNT_B1 : 1ull) : 0ull;
+                cand[k] = f32_flag_r2(c[k], qts, qx, qy, qz, R2) && ov;
+                any |= cand[k];
             }
-            cand[k] = f32_flag_r2(c[k], qts, qx, qy, qz, R2) && ov;
-            any |= cand[k];
+            if (!__any_sync(0xffffffffu, any)) continue;
+        } else {
+            // one compare per (query, lane) on the smallest norm; the
+            // per-candidate flags only on the rare queries that pass
+            float n2[CPT];
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) n2[k] = f32_n2(c[k], qts, qx, qy, qz);
+            float mn = n2[0];
+#pragma unroll
+            for (int k = 1; k < CPT; ++k) mn = f32_min_nan(mn, n2[k]);
+            if (!__any_sync(0xffffffffu, !f32_far(mn, R2))) continue;
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) cand[k] = !f32_far(n2[k], R2);
         }
-        if (!__any_sync(0xffffffffu, any)) continue;
         // rare: queue the flagged pairs of this query (qn < 32 on entry)
         const uint32_t j = (qa - base) / (uint32_t)sizeof(QF32);
         unsigned lt;
@@ -191,8 +206,10 @@ __device__ __forceinline__ void all_range(const QRec *__restrict__ qt, const QF3
 }
 
 __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Launch L) {
-    __shared__ double pm[K1_TQ];  // running max of te over the tile
-    __shared__ double sm[K1_TQ];  // suffix min of te over the tile
+    // running max / suffix min of te over the tile; on single-scan items
+    // (times ascending) te / ts themselves, +inf padded for tile_bounds
+    __shared__ double pm[2 * K1_TQ];
+    __shared__ double sm[2 * K1_TQ];
     __shared__ double f32b[8];    // per-item magnitude bounds
     __shared__ F32Item fi_sh;     // the item's FP32 origin and error bound
     __shared__ ItemCtx it_sh;
@@ -279,6 +296,8 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
         __syncthreads();
         const bool unsafe_q = flags_sh & 1;
         const bool te_sorted = !(flags_sh & 2);
+        const bool q_unsorted = *L.q_unsorted != 0;
+        const bool single_scan = te_sorted && !q_unsorted && !L.overlaps_only;
         if (tid == 0) {
             fi_sh = f32_item(qt[0].sx, qt[0].sy, qt[0].sz, qt[0].ts, f32b[0], f32b[1], f32b[2], f32b[3], f32b[4],
                              f32b[5], cmax);
@@ -303,7 +322,14 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
             sqf[j] = f;
         }
         __syncthreads();
-        te_scans(sqf, it.nt, pm, sm, warp, lane);
+        if (single_scan) {
+            for (int j = tid; j < 2 * K1_TQ; j += K1_THREADS) {
+                pm[j] = j < it.nt ? sqf[j].te64 : INFINITY;
+                sm[j] = j < it.nt ? sqf[j].ts64 : INFINITY;
+            }
+        } else {
+            te_scans(sqf, it.nt, pm, sm, warp, lane);
+        }
         __syncthreads();
 
         unsigned long long n_ov = 0, n_hit = 0;  // batch b in the low half, b1 in the high half
@@ -345,10 +371,8 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
             }
             if (L.noop) continue;
             if (!__any_sync(0xffffffffu, valid_any)) continue;
-            wmin = warp_min(wmin);
             wmax = warp_max(wmax);
             wmin_te = warp_min(wmin_te);
-            wmax_ts = warp_max(wmax_ts);
             if (lane == 0) {
                 k1_wctx[warp].key_base0 = make_key(L, it.b, wbase - L.plan.first[it.b], it.q0);
                 k1_wctx[warp].key_base1 = it.b1 >= 0 ? make_key(L, it.b1, wbase - L.plan.first[it.b1], 0) : 0;
@@ -360,32 +384,46 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
                 k1_wctx[warp].wmax = wmax;
             }
             __syncwarp();
-            const int4 w = warp_window(sqf, pm, it.nt, *L.q_unsorted != 0, wmin, wmax, wmax_ts, lane);
+            const bool exact_only = !item_f32 || __any_sync(0xffffffffu, unsafe_r);
+            if (single_scan && !exact_only) {
+                // start and end times both ascending over the tile: a
+                // candidate overlaps exactly the queries j with
+                // ts_j <= r.te (a prefix) and te_j >= r.ts (a suffix), so its
+                // count is two bisections, the window [jlo, jhi) of the warp
+                // is their min / max (the warp_window bounds of wmin, wmax),
+                // and the whole window is one scan (the exact path decides the
+                // clip cases per pair)
+                int lo[CPT], hi[CPT];
+                tile_bounds<CPT>(sm, pm, it.nt, rts, rte, lo, hi);
+                int jlo = it.nt, jhi = 0;
+#pragma unroll
+                for (int k = 0; k < CPT; ++k) {
+                    n_ov += split_count(lo[k], hi[k], it.js);
+                    jlo = lo[k] < jlo ? lo[k] : jlo;
+                    jhi = hi[k] > jhi ? hi[k] : jhi;
+                }
+                jlo = __reduce_min_sync(0xffffffffu, jlo);
+                jhi = __reduce_max_sync(0xffffffffu, jhi);
+                if (jhi < jlo) jhi = jlo;
+                n_ev += (unsigned long long)(jhi - jlo) * (unsigned long long)k1_wctx[warp].nvalid;
+                f32_range<TA_BOTH, TB_DYN, false>(qt, sqf, jlo, jhi, warp, lane, n_ov, n_hit);
+                continue;
+            }
+            wmin = warp_min(wmin);
+            wmax_ts = warp_max(wmax_ts);
+            const int4 w = warp_window(sqf, pm, it.nt, q_unsorted, wmin, wmax, wmax_ts, lane);
             const int jlo = w.x, ja = w.y, jb = w.z, jhi = w.w;
             if (L.overlaps_only) {
                 n_ov += count_overlaps<CPT>(sqf, jlo, jhi, it.js, rts, rte);
                 continue;
             }
-            if (!item_f32 || __any_sync(0xffffffffu, unsafe_r)) {
+            if (exact_only) {
                 all_range<TA_C>(qt, sqf, jlo, ja, rts, rte, warp, lane, n_ov, n_hit);
                 all_range<TA_BOTH>(qt, sqf, ja, jb, rts, rte, warp, lane, n_ov, n_hit);
                 all_range<TA_R>(qt, sqf, jb, jhi, rts, rte, warp, lane, n_ov, n_hit);
                 continue;
             }
             n_ev += (unsigned long long)(jhi - jlo) * (unsigned long long)k1_wctx[warp].nvalid;
-            if (te_sorted && !*L.q_unsorted) {
-                // start and end times both ascending over the tile: a
-                // candidate overlaps exactly the queries j with
-                // ts_j <= r.te (a prefix) and te_j >= r.ts (a suffix), so its
-                // count is two bisections, and the whole window is one scan
-                // (the exact path decides the clip cases per pair)
-#pragma unroll
-                for (int k = 0; k < CPT; ++k) {
-                    n_ov += split_count(lower_bound_te(sqf, it.nt, rts[k]), upper_bound_ts(sqf, it.nt, rte[k]), it.js);
-                }
-                f32_range<TA_BOTH, TB_DYN, false>(qt, sqf, jlo, jhi, warp, lane, n_ov, n_hit);
-                continue;
-            }
             // TA_C range: every query ends before all candidates (running max
             // < min te) and te is sorted → overlaps counted by bisection
             if (jlo < ja && pm[ja - 1] < wmin_te && te_sorted) {
