@@ -149,6 +149,76 @@ __device__ __noinline__ uint4 f32_scan(uint32_t qa, uint32_t qa_end, uint32_t ba
     return make_uint4(qa, (unsigned)qn, (unsigned)(n_ov & 0xffffffffull), (unsigned)(n_ov >> 32));
 }
 
+// Flags of one query's pairs (the lane threshold R2), queued with ballots.
+__device__ __forceinline__ void queue_query(uint32_t *wq, const float (&n2)[CPT], float R2, uint32_t j, int lane,
+                                            int &qn) {
+    unsigned lt;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+        const bool cand = !f32_far(n2[k], R2);
+        const unsigned m = __ballot_sync(0xffffffffu, cand);
+        if (cand) wq[qn + __popc(m & lt)] = ((uint32_t)(k * 32 + lane) << 16) | j;
+        qn += __popc(m);
+    }
+}
+
+// f32_scan without per-pair overlap counting, two queries per iteration:
+// one vote for both (the second may lie one record past the range end: it
+// is read but never queued).
+template <int TA>
+__device__ __noinline__ uint4 f32_scan2(uint32_t qa, uint32_t qa_end, uint32_t base, int qn, int warp, int lane) {
+    uint32_t *const wq = f_queue(warp);
+    const float *cs = f_cands(warp);
+    CandF32 c[CPT];
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+        const int i = k * 32 + lane;
+        c[k].px = cs[0 * WCAND + i]; c[k].py = cs[1 * WCAND + i]; c[k].pz = cs[2 * WCAND + i];
+        c[k].vx = cs[3 * WCAND + i]; c[k].vy = cs[4 * WCAND + i]; c[k].vz = cs[5 * WCAND + i];
+    }
+    float srl = 0.f;
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) srl = fmaxf(srl, cs[6 * WCAND + k * 32 + lane]);
+    constexpr uint32_t QB = (uint32_t)sizeof(QF32);
+    for (; qa < qa_end; qa += 2 * QB) {
+        float ts0, x0, y0, z0, a0, b0, ts1, x1, y1, z1, a1, b1, p0, p1;
+        lds4f(qa, ts0, x0, y0, z0);
+        lds4f(qa + 16, a0, b0, p0, p1);
+        lds4f(qa + QB, ts1, x1, y1, z1);
+        lds4f(qa + QB + 16, a1, b1, p0, p1);
+        const float R0 = f32_r2(a0, srl, b0), R1 = f32_r2(a1, srl, b1);
+        float n0[CPT], n1[CPT];
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            n0[k] = f32_n2(c[k], ts0, x0, y0, z0);
+            n1[k] = f32_n2(c[k], ts1, x1, y1, z1);
+        }
+        float m0 = n0[0], m1 = n1[0];
+#pragma unroll
+        for (int k = 1; k < CPT; ++k) {
+            m0 = f32_min_nan(m0, n0[k]);
+            m1 = f32_min_nan(m1, n1[k]);
+        }
+        const bool f0 = !f32_far(m0, R0), f1 = !f32_far(m1, R1);
+        if (!__any_sync(0xffffffffu, f0 || f1)) continue;
+        // rare: queue each query's flags (qn < 32 on entry)
+        const uint32_t j = (qa - base) / QB;
+        if (__any_sync(0xffffffffu, f0)) queue_query(wq, n0, R0, j, lane, qn);
+        if (qn >= 32) {  // the second query is scanned again by the next call
+            qa += QB;
+            break;
+        }
+        if (qa + QB < qa_end && __any_sync(0xffffffffu, f1)) queue_query(wq, n1, R1, j + 1, lane, qn);
+        if (qn >= 32) {
+            qa += 2 * QB;
+            break;
+        }
+    }
+    if (qa > qa_end) qa = qa_end;
+    return make_uint4(qa, (unsigned)qn, 0u, 0u);
+}
+
 // One (TA, TB) range of the window: scan, flush 32 at a time, resume.
 template <int TA, int TB, bool CNT>
 __device__ __forceinline__ void f32_range(const QRec *__restrict__ qt, const QF32 *__restrict__ sqf, int j0,
@@ -161,7 +231,8 @@ __device__ __forceinline__ void f32_range(const QRec *__restrict__ qt, const QF3
     uint32_t *const wq = f_queue(warp);
     int qn = 0;
     for (;;) {
-        const uint4 o = f32_scan<TA, CNT>(qa, qa_end, base, qn, warp, lane);
+        const uint4 o = CNT ? f32_scan<TA, CNT>(qa, qa_end, base, qn, warp, lane)
+                            : f32_scan2<TA>(qa, qa_end, base, qn, warp, lane);
         qa = o.x;
         qn = (int)o.y;
         n_ov += (unsigned long long)o.z + (unsigned long long)o.w * CNT_B1;
