@@ -733,3 +733,22 @@ def test_batch_pairs_sharing_candidate_tiles_match_unpaired_runs(kind, monkeypat
     monkeypatch.setenv("TSK_K1_PAIR", "force")
     b = span_counts(store, queries, lo, hi, first, last, 6.0)
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("nq,seed", [(37, 71), (75, 72), (131, 73), (255, 74)])
+def test_scan_range_ends_with_every_overlap_a_hit(nq, seed):
+    """d so large that every temporally overlapping pair hits: a pair queued
+    twice (a scan reading one record past its range end, where the next
+    start-time range begins) or skipped (an odd window's last query) changes
+    the result set.  Random extents leave the tiles' end times unsorted, so
+    the window splits into its start-time ranges; odd query counts give odd
+    ranges."""
+    rng = np.random.default_rng(seed)
+    store = _store(random_store_arrays(rng, 1500))
+    q = _store(random_store_arrays(rng, nq, first_traj=50_000))
+    res, st = tsk.execute_batch(store, q, (0, 1499), 1e9)
+    (qo, eo, tb, te), tm, sm = orc.run_batch(_cols(store), _cols(q), 0, 1499, 1e9)
+    assert st.hits == len(qo) and sm == 0
+    assert np.array_equal(res.query_traj, q.traj[qo]) and np.array_equal(res.entry_traj, store.traj[eo])
+    assert np.array_equal(res.t_begin, tb) and np.array_equal(res.t_end, te)
+    assert (st.temporal_misses, st.spatial_misses) == (tm, sm)
