@@ -397,15 +397,30 @@ __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? l
 template <int CPT>
 __device__ __forceinline__ void tile_bounds(const double *qts, const double *qte, int nt, const double (&ts)[CPT],
                                             const double (&te)[CPT], int (&lo)[CPT], int (&hi)[CPT]) {
+    // positions kept as shared-window byte addresses of the next unread record
+    const uint32_t bs = (uint32_t)__cvta_generic_to_shared(qts), be = (uint32_t)__cvta_generic_to_shared(qte);
+    uint32_t pl[CPT], ph[CPT];
 #pragma unroll
-    for (int k = 0; k < CPT; ++k) lo[k] = hi[k] = 0;
-    if (nt <= 0) return;
-    for (int step = nt > 1 ? 1 << (32 - __clz(nt - 1)) : 1; step; step >>= 1) {
+    for (int k = 0; k < CPT; ++k) {
+        pl[k] = be;
+        ph[k] = bs;
+    }
+    if (nt > 0) {
+        for (uint32_t sb = 8u * (nt > 1 ? 1u << (32 - __clz(nt - 1)) : 1u); sb >= 8u; sb >>= 1) {
 #pragma unroll
-        for (int k = 0; k < CPT; ++k) {
-            if (qte[lo[k] + step - 1] < ts[k]) lo[k] += step;
-            if (qts[hi[k] + step - 1] <= te[k]) hi[k] += step;
+            for (int k = 0; k < CPT; ++k) {
+                double vl, vh;
+                asm volatile("ld.shared.f64 %0, [%1];" : "=d"(vl) : "r"(pl[k] + sb - 8u));
+                asm volatile("ld.shared.f64 %0, [%1];" : "=d"(vh) : "r"(ph[k] + sb - 8u));
+                pl[k] += vl < ts[k] ? sb : 0u;
+                ph[k] += vh <= te[k] ? sb : 0u;
+            }
         }
+    }
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+        lo[k] = (int)((pl[k] - be) >> 3);
+        hi[k] = (int)((ph[k] - bs) >> 3);
     }
 }
 
