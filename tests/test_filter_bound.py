@@ -8,7 +8,8 @@ at the segment-distance flip point) and asserts that every pair with a
 non-negative reference discriminant is flagged by the FP64 filter in every
 clip case K1 can route it through, and that every reference hit is flagged
 by the FP32 pre-filter (with the item origin at the query and at a shifted
-point).  Mutated margins must produce misses, so the generator is known to
+point), also in K1's lane form (one threshold from the largest of four speed
+bounds, a NaN-propagating min of four norms, then the candidate's own compare).  Mutated margins must produce misses, so the generator is known to
 reach both bounds.
 """
 

@@ -149,6 +149,23 @@ static void check_f32(const Seg &r, const Seg &c, double d, const double O[3], d
     f32_query(c.ts, c.s[0], c.s[1], c.s[2], cext, cd[0], cd[1], cd[2], it, std::sqrt(d * d), q);
     const CandF32 cf = f32_cand(r.ts, r.s[0], r.s[1], r.s[2], rv[0], rv[1], rv[2], it);
     const bool f = f32_flag(cf, q[0], q[1], q[2], q[3], q[4], q[5]);
+    // K1's lane form (f32_scan2): one threshold from the largest speed bound
+    // of the lane's four candidates, the query passes when the NaN-propagating
+    // min of the four norms is not far, then each candidate's own compare
+    // against that threshold.  Companions: random speeds and norms (some NaN).
+    float srl = cf.sr, nmin = f32_n2(cf, q[0], q[1], q[2], q[3]);
+    const float nown = nmin;
+    for (int k = 0; k < 3; ++k) {
+        srl = std::fmax(srl, (float)unif(0.0, 2.0 * cf.sr + 1.0));
+        const float nk = next_u64() % 8 == 0 ? NAN : (float)unif(0.0, 1e6);
+        nmin = f32_min_nan(nmin, nk);
+    }
+    const float R2 = f32_r2(q[4], srl, q[5]);
+    const bool lane_flag = !f32_far(nmin, R2) && !f32_far(nown, R2);
+    if (f && !lane_flag) {
+        ++n.f32_misses;
+        if (n.f32_misses <= 5) std::fprintf(stderr, "F32 LANE MISS %s\n", tag);
+    }
     const bool need = ref_hit(r, c, d);
     ++n.f32_checks;
     n.hits += need;
