@@ -6,7 +6,8 @@
 // driven by engine.execute_batch/_run_chunks (engine.py:78-148) for every
 // batch of a plan at once.
 //
-// Work decomposition.  A work item is (batch b, candidate tile, query tile),
+// Work decomposition.  A work item is (work unit: one batch or an adjacent
+// pair sharing candidates, candidate tile, query tile),
 // claimed from a global counter by a persistent grid.  The query tile is
 // staged in shared memory as 48-byte FP32 pre-filter records (filter.cuh)
 // with the exact start/end times; each lane holds K1F_CPT = 4 candidates
@@ -19,8 +20,9 @@
 //
 // Per (candidate, query): 9 FP32 ops decide "cannot hit" for nearly every
 // pair (f32_flag, with a proven error margin), one NaN-propagating min over
-// the lane's four norms and one compare per (query, lane); flagged
-// pairs are queued per warp and re-evaluated 32 at a time with the
+// the lane's four norms and one compare per (query, lane), two queries per
+// loop iteration with one vote (f32_scan2; f32_scan where overlaps are
+// counted per pair); flagged pairs are queued per warp and re-evaluated 32 at a time with the
 // reference's exact binary64 arithmetic (k1_exact.cuh), which is what makes
 // the result set bit-exact.  Overlaps are counted exactly: by bisection for
 // whole ranges, else with binary64 compares of the exact times.
