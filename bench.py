@@ -224,12 +224,64 @@ def _spread(n):
     return out + [k for k in range(n) if k not in seen]
 
 
-def time_cpu_batches(e, q, ix, plan, d, batch_ids, workers):
+def time_cpu_batches(e, q, ix, plan, d, batch_ids, workers, keep=None):
+    """Time the reference algorithm (numpy port) on ``batch_ids``; with
+    ``keep`` (a dict) its result columns are stored per batch for parity."""
     from oracle import oracle as orc
 
     t0 = time.perf_counter()
-    _, st = orc.search(e, ix, q, plan, d, workers=workers, batch_ids=batch_ids)
-    return st["interactions"], time.perf_counter() - t0, st["hits"]
+    res, st = orc.search(e, ix, q, plan, d, workers=workers, batch_ids=batch_ids)
+    secs = time.perf_counter() - t0
+    if keep is not None and len(batch_ids) == 1:
+        keep[int(batch_ids[0])] = res
+    return st["interactions"], secs, st["hits"]
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def parity_check(e, q, ix, lo, hi, rs, batch_hits, d, port_results, extra_ids):
+    """Bit-exact parity of the timed e2e result, per batch.
+
+    * the batches the cpu_baseline leg evaluated with the numpy port of the
+      reference (``port_results``: batch -> result columns);
+    * ``extra_ids``: more evenly spread batches through the multi-threaded
+      C engine oracle (oracle/parity.py).
+    Batch b's rows are the slice at the prefix sum of the per-batch hits
+    (the engine's item order is batch order, engine.py:176-195)."""
+    from oracle.c_oracle import plan_spans
+    from oracle.parity import RES, check_batches
+
+    off = np.concatenate([[0], np.cumsum(batch_hits)])
+    mism, pairs, hits, bad, err = 0, 0, 0, [], 0.0
+    for b, want in port_results.items():
+        s = slice(int(off[b]), int(off[b + 1]))
+        ok = all(np.array_equal(np.asarray(getattr(rs, c))[s], want[c]) for c in RES)
+        hits += want["t_begin"].shape[0]
+        if not ok:
+            mism += 1
+            bad.append(b)
+    rep = check_batches(e, ix, q, lo, hi, {c: getattr(rs, c) for c in RES}, batch_hits,
+                        [b for b in extra_ids if b not in port_results], d)
+    ids = list(port_results)
+    first, last = plan_spans(e, ix, q, lo[ids], hi[ids]) if ids else ([], [])
+    for k, b in enumerate(ids):
+        if first[k] >= 0:
+            pairs += int((last[k] - first[k] + 1) * (hi[b] - lo[b] + 1))
+    return {"batches": len(port_results) + rep["batches"], "pairs": pairs + rep["pairs"],
+            "hits": hits + rep["hits"], "mismatches": mism + rep["mismatches"],
+            "max_rel_interval_err": rep["max_rel_interval_err"], "bad_batches": (bad + rep["bad_batches"])[:10],
+            "checker": f"{len(port_results)} batches vs the numpy port of the reference (the timed cpu_baseline "
+                       f"batches) + {rep['batches']} evenly spread batches vs the C engine oracle "
+                       "(oracle/pair_oracle.c), bit-exact ids/order/intervals",
+            "seconds": rep["seconds"]}
 
 
 def run_reference(args, cfg):
@@ -283,6 +335,57 @@ def run_reference(args, cfg):
 # ── GPU side (our arm) ──────────────────────────────────────────────────────
 
 
+def shared_workload(tsk, cfg, args, rank, world, dist):
+    """The sorted entry and query stores of the workload.
+
+    One process per GPU: at N > 1 global rank 0 generates the workload once
+    and writes the sorted columns to /dev/shm; the other ranks map those
+    files read-only (np.load mmap), so the host holds ONE copy of the 8 GB
+    c5 store however many ranks run (plus rank 0's generation peak), instead
+    of every rank regenerating and holding its own.  Falls back to per-rank
+    generation when /dev/shm is not writable."""
+    def generate():
+        e_cols, q_cols = workload_columns(cfg)
+        st = tsk.SegmentStore.from_columns(e_cols, validate=False)
+        qs = tsk.SegmentStore.from_columns(q_cols, validate=False)
+        return st, qs
+
+    if world == 1 or dist is None:
+        return generate()
+    shm = os.path.join("/dev/shm", f"tsk_bench_{args.config}_{os.environ.get('MASTER_PORT', '0')}")
+    ok = np.zeros(1)
+    if rank == 0:
+        store, queries = generate()
+        try:
+            os.makedirs(shm, exist_ok=True)
+            for pre, s in (("e", store), ("q", queries)):
+                for k in FIELDS:
+                    np.save(os.path.join(shm, f"{pre}_{k}.npy"), getattr(s, k))
+            ok[0] = 1
+        except OSError as exc:
+            log(f"[rank 0] /dev/shm unavailable ({exc}); every rank generates its own copy")
+    import torch
+
+    flag = torch.tensor(ok, device="cpu" if dist.get_backend() == "gloo" else "cuda")
+    dist.broadcast(flag, 0)
+    flag = flag.cpu()
+    if rank != 0:
+        if flag.item():
+            def mapped(pre):
+                return [np.load(os.path.join(shm, f"{pre}_{k}.npy"), mmap_mode="r") for k in FIELDS]
+
+            store = tsk.SegmentStore(*mapped("e"), validate=False, presorted=True)
+            queries = tsk.SegmentStore(*mapped("q"), validate=False, presorted=True)
+        else:
+            store, queries = generate()
+    dist.barrier()
+    if rank == 0 and flag.item():  # mappings stay valid after unlink
+        for f in os.listdir(shm):
+            os.unlink(os.path.join(shm, f))
+        os.rmdir(shm)
+    return store, queries
+
+
 def run_ours(args, cfg):
     import paper_1405_7461_b200 as tsk
     from paper_1405_7461_b200 import _native
@@ -303,18 +406,22 @@ def run_ours(args, cfg):
 
         torch.cuda.set_device(local)
         if forced is None:
+            # communicator set-up is logged (NCCL INFO, INIT only) so the
+            # rank count of the timing collective is visible
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             tdist.init_process_group("gloo")
         dist = tdist
+        # create the communicator now (NCCL initialises lazily)
+        t = torch.zeros(1, device="cpu" if forced is not None else "cuda")
+        dist.all_reduce(t)
     tsk.set_device(local)
     d = cfg["d"] if args.d is None else args.d
 
     t0 = time.perf_counter()
-    e_cols, q_cols = workload_columns(cfg)
-    store = tsk.SegmentStore.from_columns(e_cols, validate=False)
-    queries = tsk.SegmentStore.from_columns(q_cols, validate=False)
-    del e_cols, q_cols
+    store, queries = shared_workload(tsk, cfg, args, rank, world, dist)
     t_gen = time.perf_counter() - t0
     index = tsk.build_index(store, M_BINS)
     t_plan0 = time.perf_counter()
@@ -398,19 +505,32 @@ def run_ours(args, cfg):
             rs, _ = tsk.run_search(store, index, e2e_plan, d)
     barrier()
     e2e_s, h2d, d2h, e2e_hits = 0.0, 0, 0, 0
+    st_last = None
     for _ in range(args.steps):
         if mine is None:
             continue
         t1 = time.perf_counter()
         rs, st = tsk.run_search(store, index, e2e_plan, d)
         e2e_s += time.perf_counter() - t1
+        st_last = st
         h2d += len(pq) * (2 * 8 + 8 * 8) + len(mine.batches) * 16
         d2h += len(rs) * 48 + len(mine.batches) * 32
         e2e_hits += len(rs)
         assert st.interactions_computed == my_ints
+    # the same call with plain (pageable) numpy query columns, as a caller
+    # holding ordinary arrays makes it (staged through a pinned buffer)
+    e2e_pg_s = 0.0
+    if mine is not None:
+        pg_plan = tsk.BatchPlan(mine.queries, mine.batches)
+        tsk.run_search(store, index, pg_plan, d)
+        for _ in range(args.steps):
+            t1 = time.perf_counter()
+            tsk.run_search(store, index, pg_plan, d)
+            e2e_pg_s += time.perf_counter() - t1
     while time.perf_counter() - t_clk < 0.3:  # at least a few samples
         time.sleep(0.05)
     clk.__exit__(None, None, None)
+    t_e2e_pg = allmax(e2e_pg_s)
     t_e2e = allmax(e2e_s)
     e2e_value = total_ints / t_e2e if t_e2e > 0 else 0.0
     total_hits = allsum(float(hits))  # every rank joins every collective
@@ -424,6 +544,19 @@ def run_ours(args, cfg):
     # query shared by a lane's 4 candidates) vs the
     # measured FFMA rate
     f32_achieved = F32_OPS * evals / k1_s / 1e12 if k1_s > 0 else 0.0
+    # algorithmic HBM bytes of this rank's steps
+    if mine is not None:
+        sizes_b = (lambda t: t[1] - t[0] + 1)(mine.table())
+        cands_b = ints_all[b0:b1] // np.maximum(sizes_b, 1)
+        alg_bytes = float(64 * (cands_b.sum() + sizes_b.sum())) + 48.0 * hits / max(1, args.steps)
+    else:
+        alg_bytes = 0.0
+    alg_bytes = allsum(alg_bytes)
+    hbm_peak = None
+    try:
+        hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except (OSError, ValueError, KeyError):
+        hbm_peak = 6650.0  # B200_PROFILING.md fallback
     traffic = None
     prof = os.path.join(ROOT, "profiles", "k1_traffic.json")
     if os.path.exists(prof):
@@ -434,25 +567,54 @@ def run_ours(args, cfg):
         except (OSError, ValueError):
             pass
 
-    cpu = None
-    if world == 1 and not args.no_cpu_baseline and rank == 0:
+    cpu = parity = None
+    if world == 1 and rank == 0 and mine is not None and not (args.no_cpu_baseline and args.no_parity):
         workers = os.cpu_count() or 1
         sorted_cols = lambda s: {k: getattr(s, k) for k in FIELDS}  # noqa: E731
         e, q, ix, oplan, order = cpu_setup(sorted_cols(store), sorted_cols(queries), presorted=True,
                                            table=plan.table())
-        ints = secs = 0.0
-        nbat = 0
-        budget = float(os.environ.get("TSK_CPU_BASELINE_S", "20"))
-        for k in order:
-            i, s, _ = time_cpu_batches(e, q, ix, oplan, d, [k], workers)
-            ints += i
-            secs += s
-            nbat += 1
-            if secs >= budget:
-                break
-        cpu = {"value": ints / secs, "unit": UNIT, "cores": workers, "kind": "port",
-               "sample": f"{nbat} of {len(oplan)} batches (evenly spread), {int(ints)} interactions, "
-                         f"{secs:.1f}s; numpy port of the reference algorithm, workers={workers}"}
+        port_res: dict = {}
+        if not args.no_cpu_baseline:
+            # the reference algorithm (numpy port) on all host cores, as
+            # engine.py:69-75 defaults, over evenly spread batches
+            ints = secs = 0.0
+            nbat = 0
+            budget = float(os.environ.get("TSK_CPU_BASELINE_S", "20"))
+            for k in order:
+                i, s, _ = time_cpu_batches(e, q, ix, oplan, d, [k], workers, keep=port_res)
+                ints += i
+                secs += s
+                nbat += 1
+                if secs >= budget:
+                    break
+            # and single-threaded (workers=1), a shorter sample
+            ints1 = secs1 = 0.0
+            nb1 = 0
+            budget1 = float(os.environ.get("TSK_CPU_BASELINE1_S", "8"))
+            for k in order:
+                i, s, _ = time_cpu_batches(e, q, ix, oplan, d, [k], 1)
+                ints1 += i
+                secs1 += s
+                nb1 += 1
+                if secs1 >= budget1:
+                    break
+            cpu = {"value": ints / secs, "unit": UNIT, "cores": workers, "kind": "port",
+                   "sample": f"{nbat} of {len(oplan)} batches (evenly spread), {int(ints)} interactions, "
+                             f"{secs:.1f}s; numpy port of the reference algorithm, workers={workers}",
+                   "cpu_model": cpu_model(),
+                   "workers1": {"value": ints1 / secs1, "cores": 1,
+                                "sample": f"{nb1} batches, {int(ints1)} interactions, {secs1:.1f}s, workers=1"}}
+        if not args.no_parity:
+            lo_t, hi_t = plan.table()
+            bh = np.array([t.hits for t in st_last.per_batch], np.int64)
+            # plus evenly spread batches the port did not cover, through the C engine
+            nb_all = len(plan.batches)
+            want_n = int(os.environ.get("TSK_PARITY_BATCHES", "48"))
+            extra = [b for b in np.linspace(0, nb_all - 1, min(nb_all, 2 * want_n + len(port_res))).astype(int)
+                     .tolist() if b not in port_res][:want_n]
+            parity = parity_check(e, q, ix, lo_t, hi_t, rs, bh, d, port_res, extra)
+            log(f"[parity] {parity['batches']} batches, {parity['pairs']} pairs, {parity['hits']} hits, "
+                f"{parity['mismatches']} mismatching batches ({parity['seconds']:.1f}s)")
 
     if rank == 0:
         clocks = clk.summary()
@@ -475,23 +637,37 @@ def run_ours(args, cfg):
                     "d2h_bytes_per_step": int(d2h / args.steps),
                     "call": "paper_1405_7461_b200.run_search(store, index, plan, d) (pinned host queries)"},
             "roofline": {
-                "bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak if peak else None, "traffic": traffic,
-                "kernel": "k1_pairs", "work": f"{W_DECIDE}*overlapping pairs + {W_HIT}*hits FP64 flops",
-                "k1_ms_per_step": k1_ms / args.steps,
-                "peak_source": "tsk_probe_fp64 on this GPU in this run (DADD/DMUL/DFMA ops/s); "
-                               "MEASURED_PEAKS.json has no FP64 figure",
-                "hbm_bytes_per_step": None,
-            },
-            "kernel_roofline": {
-                "bound": "fp32 issue (K1's FP32 pre-filter)", "kernel": "k1_pairs_f32",
-                "work": f"{F32_OPS} FP32 ops per evaluated (candidate, query) pair",
-                "evaluated_pairs_per_step": int(evals / args.steps),
+                # K1's bound as written: the FP32 pre-filter's arithmetic on
+                # the FP32 pipe (every evaluated pair, counted by K1)
+                "bound": "fp32", "kernel": "k1_pairs_f32",
                 "achieved": f32_achieved, "peak": fp32_peak / 1e12, "unit": "TOP/s",
                 "frac": f32_achieved * 1e12 / fp32_peak if fp32_peak else None,
-                "peak_source": "tsk_probe_fp32 on this GPU in this run (FFMA ops/s, one op per FFMA)",
+                "traffic": traffic,
+                "work": f"{F32_OPS} FP32 ops per evaluated (candidate, query) pair",
+                "evaluated_pairs_per_step": int(evals / args.steps),
+                "k1_ms_per_step": k1_ms / args.steps,
+                "peak_source": "tsk_probe_fp32 on this GPU in this run (FFMA ops/s, one op per FFMA); "
+                               "MEASURED_PEAKS.json has no FP32 figure",
+                # algorithmic bytes: 64 B per candidate visit and per query
+                # per batch, 48 B per hit row
+                "hbm_bytes_per_step": int(alg_bytes),
+                "hbm_achieved_gbs": alg_bytes / (k1_ms / args.steps / 1e3) / 1e9 if k1_ms > 0 else None,
+                "hbm_peak_gbs": hbm_peak,
+                "hbm_frac": (alg_bytes / (k1_ms / args.steps / 1e3) / 1e9) / hbm_peak
+                            if (k1_ms > 0 and hbm_peak) else None,
+                "hbm_peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)",
+                # the contract's FP64 formulation (50 flops per
+                # overlapping pair + 9 per hit at the FP64 pipe rate): K1's
+                # cascade skips that arithmetic for nearly every pair, so this
+                # is the speed-up over a kernel running it at the FP64 peak,
+                # not an efficiency
+                "speedup_vs_fp64_formulation": achieved / peak if peak else None,
+                "fp64_formulation_tflops": achieved, "fp64_peak_tflops": peak,
             },
+            "e2e_pageable": {"value": total_ints / t_e2e_pg if t_e2e_pg > 0 else None, "unit": UNIT,
+                             "call": "run_search with plain numpy (pageable) query columns"},
             "cpu_baseline": cpu,
+            "parity": parity,
             "clocks": clocks,
             "gpu_launches": launches,
             "wall_s_value_steps": wall_s,
@@ -500,6 +676,9 @@ def run_ours(args, cfg):
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+    if parity is not None and parity["mismatches"]:
+        log(f"[parity] FAILED: {parity['mismatches']} batches differ from the oracle: {parity['bad_batches']}")
+        sys.exit(3)
 
 
 def main():
@@ -511,6 +690,8 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c5")
     ap.add_argument("--d", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the bit-exact check of the e2e result against the oracle (N=1)")
     ap.add_argument("--planner", choices=sorted(PLANNERS), default="periodic",
                     help="batch planner (config 4 compares them; PAPER.md Table 3)")
     args = ap.parse_args()

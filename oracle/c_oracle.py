@@ -45,6 +45,12 @@ def lib():
             _PI64, _PI64,
         ]
         L.orc_brute_force.restype = _I64
+        L.orc_search_spans.argtypes = [
+            ctypes.POINTER(_PD), ctypes.POINTER(_PD), _I64, _PI64, _PI64, _PI64, _PI64, _D,
+            ctypes.c_int, _I64, _PI64, ctypes.POINTER(_PI64), ctypes.POINTER(_PI64),
+            ctypes.POINTER(_PD), ctypes.POINTER(_PD),
+        ]
+        L.orc_search_spans.restype = _I64
         L.orc_free.argtypes = [ctypes.c_void_p]
         _lib = L
     return _lib
@@ -101,3 +107,49 @@ def brute_force(store, queries, d, threads=None):
         "entry_traj": store["traj"][e_ord], "entry_seg": store["seg"][e_ord],
         "t_begin": t_b, "t_end": t_e,
     }, int(tm.value), int(sm.value)
+
+
+def search_spans(store, queries, lo, hi, first, last, d, threads=None, chunk_pairs=1 << 20):
+    """Engine over explicit spans (orc_search_spans): batch b = queries
+    lo[b]..hi[b] against entries first[b]..last[b] (first < 0: none).
+
+    Returns (result dict in the reference engine's order, per-batch int64
+    array (nb, 3) = hits, temporal misses, spatial misses)."""
+    threads = threads or max(1, os.cpu_count() or 1)
+    ep, keep_e = _colptrs(store)
+    qp, keep_q = _colptrs(queries)
+    a = [np.ascontiguousarray(x, np.int64) for x in (lo, hi, first, last)]
+    nb = a[0].shape[0]
+    pb = np.zeros((nb, 3), np.int64)
+    qo, eo = _PI64(), _PI64()
+    tb, te = _PD(), _PD()
+    n = lib().orc_search_spans(ep, qp, nb, *[x.ctypes.data_as(_PI64) for x in a], float(d), threads,
+                               int(chunk_pairs), pb.ctypes.data_as(_PI64), ctypes.byref(qo),
+                               ctypes.byref(eo), ctypes.byref(tb), ctypes.byref(te))
+    q_ord = np.ctypeslib.as_array(qo, (n,)).copy() if n else np.empty(0, np.int64)
+    e_ord = np.ctypeslib.as_array(eo, (n,)).copy() if n else np.empty(0, np.int64)
+    t_b = np.ctypeslib.as_array(tb, (n,)).copy() if n else np.empty(0)
+    t_e = np.ctypeslib.as_array(te, (n,)).copy() if n else np.empty(0)
+    for p in (qo, eo, tb, te):
+        lib().orc_free(ctypes.cast(p, ctypes.c_void_p))
+    del keep_e, keep_q
+    return {
+        "query_traj": queries["traj"][q_ord], "query_seg": queries["seg"][q_ord],
+        "entry_traj": store["traj"][e_ord], "entry_seg": store["seg"][e_ord],
+        "t_begin": t_b, "t_end": t_e,
+    }, pb
+
+
+def plan_spans(store, ix, queries, lo, hi):
+    """Candidate spans of batches lo..hi the way run_search derives them
+    (engine.py:177-182): extent [ts[lo], max te[lo..hi]] → candidate_range
+    on the numpy oracle's index (pinned to the reference's goldens)."""
+    from . import oracle as orc
+
+    first = np.full(len(lo), -1, np.int64)
+    last = np.full(len(lo), -1, np.int64)
+    for k, (a, b) in enumerate(zip(lo, hi)):
+        fl = orc.cand_range(ix, float(queries["ts"][a]), float(queries["te"][a:b + 1].max()))
+        if fl is not None:
+            first[k], last[k] = fl
+    return first, last

@@ -10,6 +10,10 @@
  *   orc_pair            core.py:334-438  temporal_intersection + threshold_interval
  *   orc_floor_divide    numpy npy_divmod / npy_floor_divide (used at index.py:110)
  *   orc_brute_force     oracle.py:23-41  (query-major order)
+ *   orc_search_spans    engine.py:97-204 over explicit candidate spans
+ *                       (batch order, row-major (entry, query) within a batch)
+ * Non-finite intermediates (overflow at |coordinate| ~ 1e154 and above)
+ * follow the vectorized pair_intervals (core.py:536-553), the engine's path.
  * where core.py/index.py/oracle.py live under
  * /root/reference/pkg/src/trajseek/.
  *
@@ -84,14 +88,24 @@ int orc_pair(const double *A, const double *B, double d, double *begin, double *
         return 0;
     }
     double disc = bb * bb - 4.0 * aa * (cc - d2);
-    if (disc < 0.0) return 0;
+    /* has_root = disc >= 0.0 (core.py:538): a NaN discriminant is a miss */
+    if (!(disc >= 0.0)) return 0;
     double sd = sqrt(disc);
     double qq = bb >= 0.0 ? -0.5 * (bb + sd) : -0.5 * (bb - sd);
     double r1 = qq / aa;
     double r2 = qq != 0.0 ? (cc - d2) / qq : r1;
-    double lo = r1 < r2 ? r1 : r2;
-    double hi = r1 > r2 ? r1 : r2;
-    if (lo > 1.0 || hi < 0.0) return 0;
+    /* np.minimum / np.maximum propagate NaN (core.py:545-546), and the hit
+     * test (lo <= 1) & (hi >= 0) (core.py:553) then fails; the engine path
+     * is the vectorized one, so that is the semantics restated here (the
+     * scalar threshold_interval would return a NaN interval instead) */
+    double lo, hi;
+    if (isnan(r1) || isnan(r2)) {
+        lo = hi = NAN;
+    } else {
+        lo = r1 < r2 ? r1 : r2;
+        hi = r1 > r2 ? r1 : r2;
+    }
+    if (!(lo <= 1.0 && hi >= 0.0)) return 0;
     *begin = lo <= 0.0 ? ta : ta + lo * span;
     *end = hi >= 1.0 ? tb : ta + hi * span;
     return 1;
@@ -212,3 +226,134 @@ int64_t orc_brute_force(int64_t ne, const double *const *ecols, int64_t nq,
 }
 
 void orc_free(void *p) { free(p); }
+
+/* ── engine over explicit spans (engine.py:97-204), multi-threaded ──────────
+ *
+ * Batch b holds query ordinals lo[b]..hi[b] and candidate entry ordinals
+ * first[b]..last[b] (first < 0: no candidates, engine.py:180-182).  Each
+ * batch is the reference mesh pair_intervals(rows = its candidates,
+ * cols = its queries) (engine.py:89, core.py:464): hits come back per
+ * batch in row-major (entry, query) order, batches in the given order —
+ * the reference engine's item order.  Work is cut into (batch, entry
+ * chunk) units claimed by nthreads workers; results are concatenated in
+ * unit order, which keeps that order.  Per batch: hits, temporal misses,
+ * spatial misses (core.py:489-496, 560). */
+
+typedef struct {
+    int64_t b, e0, e1; /* batch, entry range [e0, e1) */
+    int64_t n, cap;
+    int64_t *qi, *ei;
+    double *tb, *te;
+    int64_t tmiss, smiss;
+} os_unit;
+
+typedef struct {
+    const double *const *e;
+    const double *const *q;
+    const int64_t *lo, *hi;
+    double d;
+    os_unit *units;
+    int64_t nunits;
+    int64_t next; /* claimed with __atomic_fetch_add */
+} os_job;
+
+static void os_push(os_unit *u, int64_t qi, int64_t ei, double b, double e) {
+    if (u->n == u->cap) {
+        u->cap = u->cap ? 2 * u->cap : 256;
+        u->qi = realloc(u->qi, u->cap * sizeof(int64_t));
+        u->ei = realloc(u->ei, u->cap * sizeof(int64_t));
+        u->tb = realloc(u->tb, u->cap * sizeof(double));
+        u->te = realloc(u->te, u->cap * sizeof(double));
+    }
+    u->qi[u->n] = qi; u->ei[u->n] = ei; u->tb[u->n] = b; u->te[u->n] = e;
+    u->n++;
+}
+
+static void *os_run(void *arg) {
+    os_job *J = arg;
+    double A[8], B[8];
+    for (;;) {
+        int64_t k = __atomic_fetch_add(&J->next, 1, __ATOMIC_RELAXED);
+        if (k >= J->nunits) break;
+        os_unit *u = &J->units[k];
+        const int64_t qlo = J->lo[u->b], qhi = J->hi[u->b];
+        for (int64_t j = u->e0; j < u->e1; ++j) {
+            for (int c = 0; c < 8; ++c) A[c] = J->e[c][j];
+            for (int64_t i = qlo; i <= qhi; ++i) {
+                for (int c = 0; c < 8; ++c) B[c] = J->q[c][i];
+                double tb, te;
+                int tm;
+                /* the entry is the row ("a") operand, engine.py:89 */
+                if (orc_pair(A, B, J->d, &tb, &te, &tm)) os_push(u, i, j, tb, te);
+                else if (tm) u->tmiss++;
+                else u->smiss++;
+            }
+        }
+    }
+    return NULL;
+}
+
+/* Returns the total hit count; per_batch receives nb x 3 (hits, temporal
+ * misses, spatial misses); result arrays are malloc'd (orc_free). */
+int64_t orc_search_spans(const double *const *ecols, const double *const *qcols, int64_t nb,
+                         const int64_t *lo, const int64_t *hi, const int64_t *first,
+                         const int64_t *last, double d, int nthreads, int64_t chunk_pairs,
+                         int64_t *per_batch, int64_t **q_ord, int64_t **e_ord, double **t_begin,
+                         double **t_end) {
+    if (nthreads < 1) nthreads = 1;
+    if (chunk_pairs < 1) chunk_pairs = 1 << 20;
+    int64_t nunits = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+        if (first[b] < 0) continue;
+        const int64_t s = hi[b] - lo[b] + 1, c = last[b] - first[b] + 1;
+        int64_t step = chunk_pairs / s;
+        if (step < 1) step = 1;
+        nunits += (c + step - 1) / step;
+    }
+    os_unit *units = calloc(nunits + 1, sizeof(os_unit));
+    int64_t k = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+        if (first[b] < 0) continue;
+        const int64_t s = hi[b] - lo[b] + 1;
+        int64_t step = chunk_pairs / s;
+        if (step < 1) step = 1;
+        for (int64_t e0 = first[b]; e0 <= last[b]; e0 += step) {
+            units[k].b = b;
+            units[k].e0 = e0;
+            units[k].e1 = e0 + step <= last[b] + 1 ? e0 + step : last[b] + 1;
+            ++k;
+        }
+    }
+    os_job J = {ecols, qcols, lo, hi, d, units, nunits, 0};
+    if (nthreads > nunits) nthreads = nunits > 0 ? (int)nunits : 1;
+    pthread_t *th = calloc(nthreads, sizeof(pthread_t));
+    for (int t = 0; t < nthreads; ++t) pthread_create(&th[t], NULL, os_run, &J);
+    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+    free(th);
+    memset(per_batch, 0, (size_t)nb * 3 * sizeof(int64_t));
+    int64_t total = 0;
+    for (k = 0; k < nunits; ++k) {
+        per_batch[units[k].b * 3 + 0] += units[k].n;
+        per_batch[units[k].b * 3 + 1] += units[k].tmiss;
+        per_batch[units[k].b * 3 + 2] += units[k].smiss;
+        total += units[k].n;
+    }
+    *q_ord = malloc((total + 1) * sizeof(int64_t));
+    *e_ord = malloc((total + 1) * sizeof(int64_t));
+    *t_begin = malloc((total + 1) * sizeof(double));
+    *t_end = malloc((total + 1) * sizeof(double));
+    int64_t at = 0;
+    for (k = 0; k < nunits; ++k) {
+        os_unit *u = &units[k];
+        if (u->n) {
+            memcpy(*q_ord + at, u->qi, u->n * sizeof(int64_t));
+            memcpy(*e_ord + at, u->ei, u->n * sizeof(int64_t));
+            memcpy(*t_begin + at, u->tb, u->n * sizeof(double));
+            memcpy(*t_end + at, u->te, u->n * sizeof(double));
+        }
+        at += u->n;
+        free(u->qi); free(u->ei); free(u->tb); free(u->te);
+    }
+    free(units);
+    return total;
+}

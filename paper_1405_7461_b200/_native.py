@@ -166,9 +166,16 @@ def columns_of(store) -> tuple[Columns, list]:
 
 
 class DeviceStore:
-    """Owns a tsk_db handle: a store resident in one GPU's HBM."""
+    """Owns a tsk_db handle: a store resident in one GPU's HBM.
+
+    A tsk_db is thread-compatible, not thread-safe (its search workspace,
+    query records and index are shared by every call on it), so every call
+    on the handle holds ``lock``; the engine also holds it across "ensure
+    this index, then search" so two threads cannot swap the device index
+    under each other."""
 
     def __init__(self, store, device: int | None = None, source: "DeviceStore | None" = None):
+        self.lock = threading.RLock()
         self.device = current_device() if device is None else int(device)
         lib = load()
         h = ctypes.c_void_p()
@@ -257,8 +264,9 @@ def search(dev: DeviceStore, queries, lo, hi, first, last, d: float, flags: int)
         last = np.ascontiguousarray(last, dtype=np.int64)
         fp, lp = first.ctypes.data_as(_PI64), last.ctypes.data_as(_PI64)
     h = ctypes.c_void_p()
-    check(lib.tsk_search(dev.handle, ctypes.byref(col), lo.shape[0], lo.ctypes.data_as(_PI64),
-                         hi.ctypes.data_as(_PI64), fp, lp, float(d), flags, ctypes.byref(h)))
+    with dev.lock:
+        check(lib.tsk_search(dev.handle, ctypes.byref(col), lo.shape[0], lo.ctypes.data_as(_PI64),
+                             hi.ctypes.data_as(_PI64), fp, lp, float(d), flags, ctypes.byref(h)))
     del keep
     return Result(h)
 
@@ -287,16 +295,17 @@ def index_build(dev: DeviceStore, m: int, rule: int):
     lib = load()
     n_ne = _I64()
     hdr = (ctypes.c_double * 3)()
-    check(lib.tsk_index_build(dev.handle, int(m), int(rule), ctypes.byref(n_ne), hdr))
-    k = int(n_ne.value)
-    ne_start = np.empty(k, np.float64)
-    ne_end = np.empty(k, np.float64)
-    ne_first = np.empty(k, np.int64)
-    ne_last = np.empty(k, np.int64)
-    ne_bin = np.empty(k, np.int64)
-    check(lib.tsk_index_copy(dev.handle, ne_start.ctypes.data_as(_PD), ne_end.ctypes.data_as(_PD),
-                             ne_first.ctypes.data_as(_PI64), ne_last.ctypes.data_as(_PI64),
-                             ne_bin.ctypes.data_as(_PI64)))
+    with dev.lock:
+        check(lib.tsk_index_build(dev.handle, int(m), int(rule), ctypes.byref(n_ne), hdr))
+        k = int(n_ne.value)
+        ne_start = np.empty(k, np.float64)
+        ne_end = np.empty(k, np.float64)
+        ne_first = np.empty(k, np.int64)
+        ne_last = np.empty(k, np.int64)
+        ne_bin = np.empty(k, np.int64)
+        check(lib.tsk_index_copy(dev.handle, ne_start.ctypes.data_as(_PD), ne_end.ctypes.data_as(_PD),
+                                 ne_first.ctypes.data_as(_PI64), ne_last.ctypes.data_as(_PI64),
+                                 ne_bin.ctypes.data_as(_PI64)))
     return (hdr[0], hdr[1], hdr[2]), ne_start, ne_end, ne_first, ne_last, ne_bin
 
 
@@ -307,8 +316,9 @@ def candidate_ranges(dev: DeviceStore, begin: np.ndarray, end: np.ndarray):
     k = begin.shape[0]
     first = np.empty(k, np.int64)
     last = np.empty(k, np.int64)
-    check(lib.tsk_candidate_ranges(dev.handle, k, begin.ctypes.data_as(_PD), end.ctypes.data_as(_PD),
-                                   first.ctypes.data_as(_PI64), last.ctypes.data_as(_PI64)))
+    with dev.lock:
+        check(lib.tsk_candidate_ranges(dev.handle, k, begin.ctypes.data_as(_PD), end.ctypes.data_as(_PD),
+                                       first.ctypes.data_as(_PI64), last.ctypes.data_as(_PI64)))
     return first, last
 
 

@@ -293,6 +293,27 @@ TSK_HD float f32_n2(const CandF32 &c, float qts, float qx, float qy, float qz) {
 #endif
 }
 
+// Two candidates of a lane in packed form: component c of candidates k0/k1
+// in one float2 (sm_100's FFMA2 / FADD2 / FMUL2 then issue one instruction
+// for both, the query's scalar broadcast as the .F32 operand).
+struct CandF32x2 {
+    float2 px, py, pz, vx, vy, vz;
+};
+
+#ifdef __CUDACC__
+// f32_n2 of two candidates at once: the same IEEE operations, per half, in
+// the same order and rounding (u = RN(RN(ts v + p) - s); |u|^2 rounded
+// down), so every flag equals the scalar form's (and the margin proof,
+// which is about that operation sequence, is unchanged).
+__device__ __forceinline__ float2 f32_n2x2(const CandF32x2 &c, float qts, float qx, float qy, float qz) {
+    const float2 t = make_float2(qts, qts);
+    const float2 ux = __fadd2_rn(__ffma2_rn(t, c.vx, c.px), make_float2(-qx, -qx));
+    const float2 uy = __fadd2_rn(__ffma2_rn(t, c.vy, c.py), make_float2(-qy, -qy));
+    const float2 uz = __fadd2_rn(__ffma2_rn(t, c.vz, c.pz), make_float2(-qz, -qz));
+    return __ffma2_rd(uz, uz, __ffma2_rd(uy, uy, __fmul2_rd(ux, ux)));
+}
+#endif
+
 // n > R2: the pair cannot hit (false for NaN, so NaN flags).
 TSK_HD bool f32_far(float n, float R2) {
 #ifdef __CUDA_ARCH__

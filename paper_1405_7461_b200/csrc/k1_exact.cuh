@@ -10,6 +10,8 @@
 #pragma once
 
 #include "filter.cuh"
+#include <math_constants.h>
+
 #include "tsk_internal.cuh"
 
 namespace tsk {
@@ -100,8 +102,11 @@ __device__ __forceinline__ Hit solve_exact(double ta, double tb, double cc, doub
         double qq = bb >= 0.0 ? __dmul_rn(-0.5, __dadd_rn(bb, sd)) : __dmul_rn(-0.5, __dsub_rn(bb, sd));
         double r1 = __ddiv_rn(qq, aa);
         double r2 = qq == 0.0 ? r1 : __ddiv_rn(e, qq);
-        lo = r1 < r2 ? r1 : r2;
-        hi = r1 > r2 ? r1 : r2;
+        // np.minimum / np.maximum propagate NaN (core.py:545-546): a NaN root
+        // (aa = inf from |w| above ~1e154) makes the hit test below fail
+        const bool nan_root = isnan(r1) || isnan(r2);
+        lo = nan_root ? CUDART_NAN : (r1 < r2 ? r1 : r2);
+        hi = nan_root ? CUDART_NAN : (r1 > r2 ? r1 : r2);
         h.hit = lo <= 1.0 && hi >= 0.0;
     }
     double span = __dsub_rn(tb, ta);

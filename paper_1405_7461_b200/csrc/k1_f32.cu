@@ -19,7 +19,9 @@
 // binary lifting; else four binary searches, one per lane).
 //
 // Per (candidate, query): 9 FP32 ops decide "cannot hit" for nearly every
-// pair (f32_flag, with a proven error margin), one NaN-propagating min over
+// pair (f32_flag, with a proven error margin; issued as FFMA2 / FADD2 /
+// FMUL2 on a lane's candidates in pairs, 4.5 instructions per pair, with the
+// query's values as the broadcast operand), one NaN-propagating min over
 // the lane's four norms and one compare per (query, lane), two queries per
 // loop iteration with one vote (f32_scan2; f32_scan where overlaps are
 // counted per pair); flagged pairs are queued per warp and re-evaluated 32 at a time with the
@@ -68,17 +70,38 @@ __device__ __forceinline__ void lds2d(uint32_t a, double &x, double &y) {
 // until 32 or more flags are queued or the range ends, and returns
 // (qa, queued, overlaps).  The caller flushes and resumes.  CNT: count
 // overlaps per pair with the exact times (read from L2 once per call).
+// The warp's staged FP32 candidates of this lane, packed in pairs (2h, 2h+1).
+__device__ __forceinline__ void load_cands_x2(const float *cs, int lane, CandF32x2 (&c)[CPT / 2]) {
+#pragma unroll
+    for (int h = 0; h < CPT / 2; ++h) {
+        const int i0 = (2 * h) * 32 + lane, i1 = i0 + 32;
+        c[h].px = make_float2(cs[0 * WCAND + i0], cs[0 * WCAND + i1]);
+        c[h].py = make_float2(cs[1 * WCAND + i0], cs[1 * WCAND + i1]);
+        c[h].pz = make_float2(cs[2 * WCAND + i0], cs[2 * WCAND + i1]);
+        c[h].vx = make_float2(cs[3 * WCAND + i0], cs[3 * WCAND + i1]);
+        c[h].vy = make_float2(cs[4 * WCAND + i0], cs[4 * WCAND + i1]);
+        c[h].vz = make_float2(cs[5 * WCAND + i0], cs[5 * WCAND + i1]);
+    }
+}
+
+// The lane's four norms |u|^2 against one query, two FFMA2 chains.
+__device__ __forceinline__ void norms_x2(const CandF32x2 (&c)[CPT / 2], float ts, float x, float y, float z,
+                                         float (&n)[CPT]) {
+#pragma unroll
+    for (int h = 0; h < CPT / 2; ++h) {
+        const float2 a = f32_n2x2(c[h], ts, x, y, z);
+        n[2 * h] = a.x;
+        n[2 * h + 1] = a.y;
+    }
+}
+
 template <int TA, bool CNT>
 __device__ __noinline__ uint4 f32_scan(uint32_t qa, uint32_t qa_end, uint32_t base, int qn, int warp, int lane) {
+    static_assert(CPT % 2 == 0, "candidates are packed in pairs");
     uint32_t *const wq = f_queue(warp);
     const float *cs = f_cands(warp);
-    CandF32 c[CPT];
-#pragma unroll
-    for (int k = 0; k < CPT; ++k) {
-        const int i = k * 32 + lane;
-        c[k].px = cs[0 * WCAND + i]; c[k].py = cs[1 * WCAND + i]; c[k].pz = cs[2 * WCAND + i];
-        c[k].vx = cs[3 * WCAND + i]; c[k].vy = cs[4 * WCAND + i]; c[k].vz = cs[5 * WCAND + i];
-    }
+    CandF32x2 c[CPT / 2];
+    load_cands_x2(cs, lane, c);
     // one threshold per query and lane: the largest speed bound of the lane's
     // candidates (staged per candidate, reduced here)
     float srl = 0.f;
@@ -105,6 +128,8 @@ __device__ __noinline__ uint4 f32_scan(uint32_t qa, uint32_t qa_end, uint32_t ba
         if (CNT) lds2d(qa + 32, cts, cte);
         bool cand[CPT];
         const float R2 = f32_r2(qa4, srl, qb4);
+        float n2[CPT];
+        norms_x2(c, qts, qx, qy, qz, n2);
         if constexpr (CNT) {
             bool any = false;
 #pragma unroll
@@ -116,16 +141,13 @@ __device__ __noinline__ uint4 f32_scan(uint32_t qa, uint32_t qa_end, uint32_t ba
                 else if (TA == TA_R) ov = cts <= rte[k];
                 else ov = rts[k] <= cte && cts <= rte[k];
                 n_ov += ov ? (qa >= qa_js ? CNT_B1 : 1ull) : 0ull;
-                cand[k] = f32_flag_r2(c[k], qts, qx, qy, qz, R2) && ov;
+                cand[k] = !f32_far(n2[k], R2) && ov;
                 any |= cand[k];
             }
             if (!__any_sync(0xffffffffu, any)) continue;
         } else {
             // one compare per (query, lane) on the smallest norm; the
             // per-candidate flags only on the rare queries that pass
-            float n2[CPT];
-#pragma unroll
-            for (int k = 0; k < CPT; ++k) n2[k] = f32_n2(c[k], qts, qx, qy, qz);
             float mn = n2[0];
 #pragma unroll
             for (int k = 1; k < CPT; ++k) mn = f32_min_nan(mn, n2[k]);
@@ -170,15 +192,12 @@ __device__ __forceinline__ void queue_query(uint32_t *wq, const float (&n2)[CPT]
 // is read but never queued).
 template <int TA>
 __device__ __noinline__ uint4 f32_scan2(uint32_t qa, uint32_t qa_end, uint32_t base, int qn, int warp, int lane) {
+    static_assert(CPT % 2 == 0, "candidates are packed in pairs");
     uint32_t *const wq = f_queue(warp);
     const float *cs = f_cands(warp);
-    CandF32 c[CPT];
-#pragma unroll
-    for (int k = 0; k < CPT; ++k) {
-        const int i = k * 32 + lane;
-        c[k].px = cs[0 * WCAND + i]; c[k].py = cs[1 * WCAND + i]; c[k].pz = cs[2 * WCAND + i];
-        c[k].vx = cs[3 * WCAND + i]; c[k].vy = cs[4 * WCAND + i]; c[k].vz = cs[5 * WCAND + i];
-    }
+    // candidates (2h, 2h+1) of the lane packed in one CandF32x2
+    CandF32x2 c[CPT / 2];
+    load_cands_x2(cs, lane, c);
     float srl = 0.f;
 #pragma unroll
     for (int k = 0; k < CPT; ++k) srl = fmaxf(srl, cs[6 * WCAND + k * 32 + lane]);
@@ -191,11 +210,8 @@ __device__ __noinline__ uint4 f32_scan2(uint32_t qa, uint32_t qa_end, uint32_t b
         lds4f(qa + QB + 16, a1, b1, p0, p1);
         const float R0 = f32_r2(a0, srl, b0), R1 = f32_r2(a1, srl, b1);
         float n0[CPT], n1[CPT];
-#pragma unroll
-        for (int k = 0; k < CPT; ++k) {
-            n0[k] = f32_n2(c[k], ts0, x0, y0, z0);
-            n1[k] = f32_n2(c[k], ts1, x1, y1, z1);
-        }
+        norms_x2(c, ts0, x0, y0, z0, n0);
+        norms_x2(c, ts1, x1, y1, z1, n1);
         float m0 = n0[0], m1 = n1[0];
 #pragma unroll
         for (int k = 1; k < CPT; ++k) {

@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import os
 import time
+from collections import UserList
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -68,65 +69,33 @@ class SearchStats:
         return (self.temporal_misses + self.spatial_misses) / self.interactions_computed
 
 
-class _LazyTraces(list):
-    """``SearchStats.per_batch``: a list of BatchTrace built on first use
-    from the per-batch arrays, so a large plan does not pay for thousands of
-    Python objects on every call unless they are read."""
+class _LazyTraces(UserList):
+    """``SearchStats.per_batch``: a list of BatchTrace built on first access
+    from the per-batch arrays, so a plan of thousands of batches does not pay
+    for the Python objects on every call unless they are read.  Every list
+    operation goes through ``data``, which fills itself first, so copies,
+    concatenation, ``+=``, ``clear``, ``index``, ``sort`` ... all see the
+    traces (the reference's per_batch is a plain list, engine.py:56)."""
 
-    __slots__ = ("_src",)
-
-    def __init__(self, iterable=(), *, src=None):
-        super().__init__(iterable)
+    def __init__(self, initlist=None, *, src=None):
+        self._data = list(initlist) if initlist is not None else []
         self._src = src
 
-    def _fill(self):
+    @property
+    def data(self):
         if self._src is not None:
             sizes, cands, ints, hits, secs = self._src
             self._src = None
-            list.extend(self, map(BatchTrace, range(len(sizes)), sizes, cands, ints, hits, secs))
+            self._data.extend(map(BatchTrace, range(len(sizes)), sizes, cands, ints, hits, secs))
+        return self._data
 
-    def __len__(self):
-        self._fill()
-        return list.__len__(self)
-
-    def __iter__(self):
-        self._fill()
-        return list.__iter__(self)
-
-    def __reversed__(self):
-        self._fill()
-        return list.__reversed__(self)
-
-    def __getitem__(self, i):
-        self._fill()
-        return list.__getitem__(self, i)
-
-    def __contains__(self, x):
-        self._fill()
-        return list.__contains__(self, x)
-
-    def __eq__(self, other):
-        self._fill()
-        return list.__eq__(self, other)
-
-    def __ne__(self, other):
-        return not self.__eq__(other)
-
-    def __repr__(self):
-        self._fill()
-        return list.__repr__(self)
-
-    def append(self, x):
-        self._fill()
-        list.append(self, x)
-
-    def extend(self, xs):
-        self._fill()
-        list.extend(self, xs)
+    @data.setter
+    def data(self, value):
+        self._src = None
+        self._data = value
 
     def __reduce__(self):
-        self._fill()
-        return (list, (list(list.__iter__(self)),))
+        return (list, (list(self.data),))
 
 
 def resolve_workers(workers: int | None) -> int:
@@ -232,9 +201,8 @@ def _run_one(store, index, plan, d, ordinal, replica, canonical=False):
     t_start = time.perf_counter()
     queries = plan.queries
     lo, hi = plan.table()
-    dev = index.ensure_device(ordinal, replica, store)
     flags = _native.TSK_ORDER_CANONICAL if canonical else _native.TSK_ORDER_REFERENCE
-    res = _native.search(dev, queries, lo, hi, None, None, d, flags)
+    res = _indexed_search(store, index, ordinal, replica, queries, lo, hi, d, flags)
     t_asm = time.perf_counter()
     result = _result_set(res) if res.n else ResultSet.empty()
     if canonical:
@@ -262,6 +230,15 @@ def _run_one(store, index, plan, d, ordinal, replica, canonical=False):
     stats.total_seconds = t_end - t_start
     stats.overhead_seconds = max(0.0, stats.total_seconds - stats.kernel_seconds - stats.assembly_seconds)
     return result, stats
+
+
+def _indexed_search(store, index, ordinal, replica, queries, lo, hi, d, flags):
+    """tsk_search on the device copy carrying ``index``; the handle's lock
+    is held from the index check to the end of the search."""
+    dev = store.device(ordinal, replica)
+    with dev.lock:
+        index.ensure_device(ordinal, replica, store)
+        return _native.search(dev, queries, lo, hi, None, None, d, flags)
 
 
 def _run_chunked(store, index, plan, d, ordinal, replica, canonical, chunks):
@@ -346,11 +323,10 @@ def search_device(store: SegmentStore, index: TemporalIndex, plan: BatchPlan, d:
     per-batch stats, CUDA-event timings).
     """
     lo, hi = plan.table()
-    dev = index.ensure_device(None, 0, store)
     flags = _native.TSK_ORDER_REFERENCE | _native.TSK_RESULTS_ON_DEVICE
     if queries_resident:
         flags |= _native.TSK_QUERIES_RESIDENT
-    return _native.search(dev, plan.queries, lo, hi, None, None, d, flags)
+    return _indexed_search(store, index, None, 0, plan.queries, lo, hi, d, flags)
 
 
 def launch_overhead_pass(store: SegmentStore, batch: SegmentStore, span: tuple[int, int], *,
@@ -373,9 +349,8 @@ def plan_counts(store: SegmentStore, index: TemporalIndex, plan: BatchPlan, d: f
     temporal-miss count (perfmodel.py:327-343); hits are then 0.
     """
     lo, hi = plan.table()
-    dev = index.ensure_device(None, 0, store)
     flags = _native.TSK_OVERLAPS_ONLY if overlaps_only else _native.TSK_COUNT_ONLY
-    return _native.search(dev, plan.queries, lo, hi, None, None, d, flags).per_batch
+    return _indexed_search(store, index, None, 0, plan.queries, lo, hi, d, flags).per_batch
 
 
 def span_counts(store: SegmentStore, queries: SegmentStore, lo, hi, first, last, d: float, *,

@@ -77,9 +77,10 @@ class TemporalIndex:
         from . import _native
 
         dev = (self._store if store is None else store).device(ordinal, replica)
-        if dev.index_token is not self:
-            _native.index_build(dev, self.m, _rule_code(self.extent_rule))
-            dev.index_token = self
+        with dev.lock:
+            if dev.index_token is not self:
+                _native.index_build(dev, self.m, _rule_code(self.extent_rule))
+                dev.index_token = self
         return dev
 
 
@@ -177,7 +178,10 @@ def device_candidate_ranges(index: TemporalIndex, begin, end) -> tuple[np.ndarra
     """:func:`candidate_ranges` evaluated on the GPU (K3, one warp per interval)."""
     from . import _native
 
-    return _native.candidate_ranges(index.ensure_device(), begin, end)
+    dev = index._store.device()
+    with dev.lock:  # the device index must stay this one until the call returns
+        index.ensure_device()
+        return _native.candidate_ranges(dev, begin, end)
 
 
 def interaction_count(index: TemporalIndex, batch_size: int, q: TimeInterval) -> int:

@@ -63,6 +63,22 @@ def test_pair_intervals_golden_bit_exact(tag):
     assert [h.temporal_misses, h.spatial_misses] == list(z[f"{tag}_misses"])
 
 
+def test_pair_intervals_extreme_magnitudes_golden():
+    """Overflowing intermediates (|coordinate| 1e150-1e300, d up to 1e300),
+    golden from the reference's vectorized pair_intervals: NaN roots are a
+    miss (core.py:545-553), e.g. head-on motion at 1e160 from one point."""
+    z = load_golden("extreme.npz")
+    for tag in map(str, z["tags"]):
+        rows = _store(golden_store(z, f"{tag}_rows"))
+        cols = _store(golden_store(z, f"{tag}_cols"))
+        h = tsk.pair_intervals(rows, cols, float(z[f"{tag}_d"]))
+        assert np.array_equal(h.row_idx, z[f"{tag}_row_idx"]), tag
+        assert np.array_equal(h.col_idx, z[f"{tag}_col_idx"]), tag
+        assert np.array_equal(h.t_begin, z[f"{tag}_t_begin"]), tag
+        assert np.array_equal(h.t_end, z[f"{tag}_t_end"]), tag
+        assert [h.temporal_misses, h.spatial_misses] == list(z[f"{tag}_misses"]), tag
+
+
 def test_pair_intervals_hand_cases():
     z = load_golden("pairs.npz")
     for a, b, d, want in zip(z["hand_a"], z["hand_b"], z["hand_d"], z["hand_res"]):
@@ -752,3 +768,26 @@ def test_scan_range_ends_with_every_overlap_a_hit(nq, seed):
     assert np.array_equal(res.query_traj, q.traj[qo]) and np.array_equal(res.entry_traj, store.traj[eo])
     assert np.array_equal(res.t_begin, tb) and np.array_equal(res.t_end, te)
     assert (st.temporal_misses, st.spatial_misses) == (tm, sm)
+
+
+def test_concurrent_run_search_on_one_store_is_safe():
+    """Host threads sharing one store (and two different indexes of it)
+    get the same results as sequential calls: the device handle's lock
+    serialises its workspace and its index."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    rng = np.random.default_rng(2024)
+    store = _store(random_store_arrays(rng, 6000))
+    q1 = _store(random_store_arrays(rng, 700, first_traj=10**6))
+    q2 = _store(random_store_arrays(rng, 500, first_traj=2 * 10**6))
+    ix_a = tsk.build_index(store, 64)
+    ix_b = tsk.build_index(store, 300, extent_rule="grid_start")
+    jobs = [(ix_a, tsk.periodic(q1, 40, ix_a), 2.0), (ix_b, tsk.periodic(q2, 25, ix_b), 3.0),
+            (ix_a, tsk.periodic(q2, 60, ix_a), 1.0), (ix_b, tsk.periodic(q1, 33, ix_b), 2.5)] * 4
+    want = [tsk.run_search(store, ix, p, d) for ix, p, d in jobs]
+    with ThreadPoolExecutor(max_workers=6) as ex:
+        got = list(ex.map(lambda j: tsk.run_search(store, j[0], j[1], j[2]), jobs))
+    for (wr, ws), (gr, gs) in zip(want, got):
+        for k in RES:
+            assert np.array_equal(getattr(gr, k), getattr(wr, k)), k
+        assert ws.hits == gs.hits and ws.temporal_misses == gs.temporal_misses

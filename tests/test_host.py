@@ -15,7 +15,7 @@ import numpy as np
 import pytest
 
 import paper_1405_7461_b200 as tsk
-from helpers import STORE_FIELDS, c9_population, golden_store, load_golden, store_digest
+from helpers import GOLDEN, STORE_FIELDS, c9_population, golden_store, load_golden, store_digest
 from oracle import oracle as orc
 from paper_1405_7461_b200 import _native
 from paper_1405_7461_b200.index import TemporalBin, TemporalIndex
@@ -350,3 +350,49 @@ def test_native_planners_on_generated_exp_profile():
     assert tsk.setsplit_max(q, ix, 120).batches == R.plan().batches
     assert tsk.greedy_max(q, ix, 120).batches == tsk.greedy_max(q, ix, 120, native=False).batches
     assert tsk.greedy_min(q, ix, 120).batches == tsk.greedy_min(q, ix, 120, native=False).batches
+
+
+def test_drop_in_namespace_covers_reference_all():
+    """Every name the reference exports (trajseek.__all__, committed from
+    /root/reference/pkg/src/trajseek/__init__.py:60-114) is importable from
+    the drop-in package and listed in its __all__."""
+    import json
+
+    import paper_1405_7461_b200 as tsk
+
+    names = json.load(open(os.path.join(GOLDEN, "reference_all.json")))
+    missing = [n for n in names if not hasattr(tsk, n)]
+    assert not missing, missing
+    assert set(names) <= set(tsk.__all__)
+
+
+def test_per_batch_behaves_as_a_list():
+    """SearchStats.per_batch fills itself before every list operation."""
+    from paper_1405_7461_b200.engine import BatchTrace, _LazyTraces
+
+    src = ([3, 4], [10, 0], [30, 0], [2, 0], [0.5, 0.0])
+    want = [BatchTrace(0, 3, 10, 30, 2, 0.5), BatchTrace(1, 4, 0, 0, 0, 0.0)]
+
+    def mk():
+        return _LazyTraces(src=tuple(list(x) for x in src))
+
+    assert mk().copy() == want
+    assert mk() + [] == want and [] + mk() == want
+    a = mk()
+    a += [want[0]]
+    assert a == want + [want[0]]
+    b = mk()
+    b.clear()
+    assert len(b) == 0 and b == []
+    assert mk().index(want[1]) == 1 and mk().count(want[0]) == 1
+    c = mk()
+    c.sort(key=lambda t: -t.ordinal)
+    assert c == want[::-1]
+    assert mk().pop() == want[1]
+    d = mk()
+    d[0] = want[1]
+    assert d == [want[1], want[1]]
+    assert list(mk()) == want and len(mk()) == 2 and mk()[1] == want[1]
+    import pickle
+
+    assert pickle.loads(pickle.dumps(mk())) == want

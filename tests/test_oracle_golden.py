@@ -180,3 +180,98 @@ def test_brute_force_small_scene_numpy_and_c():
     for k in RES_COLS:
         assert np.array_equal(res[k], z[f"small_brute_{k}"]), k
         assert np.array_equal(cres[k], z[f"small_brute_{k}"]), k
+
+
+# ── C engine over spans (the large-scale parity checker) ──────────────────
+
+
+@pytest.mark.parametrize("name", ["periodic25", "periodic17", "greedy30", "max40", "single"])
+def test_c_search_spans_small_scene_matches_golden(name):
+    """orc_search_spans (the multi-threaded C engine the scale parity tests
+    use) equals the reference's run_search on the golden scenes: items,
+    order and per-batch statistics."""
+    z = load_golden("search.npz")
+    e = golden_store(z, "small_e")
+    q = golden_store(z, "small_q")
+    tab = z[f"small_{name}_plan"]
+    res, pb = c_oracle.search_spans(e, q, tab[:, 0], tab[:, 1], tab[:, 2], tab[:, 3], 20.0, threads=3,
+                                    chunk_pairs=997)
+    for k in RES_COLS:
+        assert np.array_equal(res[k], z[f"small_{name}_{k}"]), k
+    stats = z[f"small_{name}_stats"]
+    assert [pb[:, 1].sum(), pb[:, 2].sum(), pb[:, 0].sum()] == list(stats[1:])
+    per = z[f"small_{name}_per_batch"]
+    assert np.array_equal(pb[:, 0], per[:, 4])
+
+
+@pytest.mark.parametrize("d", [1.0, 5.0])
+def test_c_search_spans_config1_matches_golden(d):
+    """Config 1 (99,000 × 9,900, m = 10,000, Periodic 120) through the C
+    engine on the golden plan table: identical to the reference run."""
+    from paper_1405_7461_b200 import datagen
+
+    z = load_golden("search.npz")
+    e = datagen.generate_columns(datagen.make_profile("uniform", 1000, seed=1, timesteps=100))
+    pool = datagen.generate(datagen.make_profile("uniform", 1000, seed=2, timesteps=100))
+    qs = datagen.sample_queries(pool, 100, seed=3)
+    E = orc.make_store(*(e[k] for k in STORE_FIELDS))
+    Q = orc.make_store(*(getattr(qs, k) for k in STORE_FIELDS))
+    tab = z["c1_plan"]
+    ix = orc.index_build(E, 10_000)
+    f, l = c_oracle.plan_spans(E, ix, Q, tab[:, 0], tab[:, 1])
+    assert np.array_equal(f, tab[:, 2]) and np.array_equal(l, tab[:, 3])
+    res, pb = c_oracle.search_spans(E, Q, tab[:, 0], tab[:, 1], f, l, d)
+    tag = f"c1_d{int(d)}"
+    for k in RES_COLS:
+        assert np.array_equal(res[k], z[f"{tag}_{k}"]), k
+    assert [pb[:, 1].sum(), pb[:, 2].sum(), pb[:, 0].sum()] == list(z[f"{tag}_stats"][1:])
+
+
+def test_c_search_spans_equals_numpy_oracle_random_scene():
+    """Random scene with waypoints and stationary segments, several chunk
+    sizes: the C engine equals the numpy restatement item for item."""
+    rng = np.random.default_rng(77)
+    E = _ostore(random_store_arrays(rng, 3000))
+    Q = _ostore(random_store_arrays(rng, 400, first_traj=10_000))
+    ix = orc.index_build(E, 50)
+    plan = orc.plan_periodic(Q, 23, ix)
+    want, st = orc.search(E, ix, Q, plan, 2.5, workers=1)
+    lo = np.array([b[0] for b in plan])
+    hi = np.array([b[1] for b in plan])
+    f, l = c_oracle.plan_spans(E, ix, Q, lo, hi)
+    for chunk in (1, 100, 1 << 20):
+        got, pb = c_oracle.search_spans(E, Q, lo, hi, f, l, 2.5, threads=4, chunk_pairs=chunk)
+        for k in RES_COLS:
+            assert np.array_equal(got[k], want[k]), (chunk, k)
+        assert pb[:, 1].sum() == st["temporal_misses"] and pb[:, 2].sum() == st["spatial_misses"]
+
+
+def _extreme_scenes():
+    z = load_golden("extreme.npz")
+    for tag in z["tags"]:
+        yield str(tag), z
+
+
+def test_extreme_magnitudes_numpy_and_c_match_reference():
+    """Overflowing intermediates (|coordinate| 1e150-1e300, d up to 1e300):
+    the numpy restatement and the C engine follow the vectorized
+    reference, where NaN roots are a miss (core.py:545-553)."""
+    import warnings
+
+    for tag, z in _extreme_scenes():
+        rows = golden_store(z, f"{tag}_rows")
+        cols = golden_store(z, f"{tag}_cols")
+        d = float(z[f"{tag}_d"])
+        with warnings.catch_warnings(), np.errstate(all="ignore"):
+            warnings.simplefilter("ignore")
+            ri, ci, tb, te, tm, sm = orc.pair_mesh(rows, cols, d)
+        assert np.array_equal(ri, z[f"{tag}_row_idx"]) and np.array_equal(ci, z[f"{tag}_col_idx"]), tag
+        assert np.array_equal(tb, z[f"{tag}_t_begin"]) and np.array_equal(te, z[f"{tag}_t_end"]), tag
+        assert [tm, sm] == list(z[f"{tag}_misses"]), tag
+        nr, nc = rows["ts"].shape[0], cols["ts"].shape[0]
+        res, pb = c_oracle.search_spans(rows, cols, [0], [nc - 1], [0], [nr - 1], d, threads=2)
+        assert np.array_equal(res["entry_traj"], rows["traj"][z[f"{tag}_row_idx"]]), tag
+        assert np.array_equal(res["query_traj"], cols["traj"][z[f"{tag}_col_idx"]]), tag
+        assert np.array_equal(res["t_begin"], z[f"{tag}_t_begin"]), tag
+        assert np.array_equal(res["t_end"], z[f"{tag}_t_end"]), tag
+        assert list(pb[0, 1:]) == list(z[f"{tag}_misses"]), tag

@@ -118,7 +118,8 @@ static bool ref_hit(const Seg &r, const Seg &c, double d) {
     const double qq = bb >= 0.0 ? -0.5 * (bb + sd) : -0.5 * (bb - sd);
     const double r1 = qq / aa;
     const double r2 = qq == 0.0 ? r1 : (cc - d2) / qq;
-    const double lo = r1 < r2 ? r1 : r2, hi = r1 > r2 ? r1 : r2;
+    const bool nan_root = std::isnan(r1) || std::isnan(r2);  // np.minimum/maximum propagate NaN
+    const double lo = nan_root ? NAN : (r1 < r2 ? r1 : r2), hi = nan_root ? NAN : (r1 > r2 ? r1 : r2);
     return lo <= 1.0 && hi >= 0.0;
 }
 

@@ -9,7 +9,7 @@ for line in out.split("\n"):
     if f and m:
         ins.append((int(m.group(1), 16), m.group(2).strip()))
 idx = {a: i for i, (a, _) in enumerate(ins)}
-FP = ("FADD", "FMUL", "FFMA")
+FP = ("FADD", "FMUL", "FFMA", "FFMA2", "FADD2", "FMUL2")
 for i, (a, t) in enumerate(ins):
     m = re.search(r"BRA\s+(0x[0-9a-f]+)", t)
     if not m:
