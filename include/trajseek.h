@@ -79,6 +79,13 @@ void tsk_db_free(tsk_db *db);
  * between GPUs); build its index with tsk_index_build. */
 int tsk_db_replicate(const tsk_db *src, int device, tsk_db **out);
 int64_t tsk_db_size(const tsk_db *db);
+/* Register caller-owned host copies of the store's traj/seg id columns
+ * (start-sorted order, n each; NULL, NULL clears).  With them, large
+ * reference-ordered results cross PCIe as 24-byte (ordinals, interval)
+ * rows and the ids are expanded on host threads, pipelined with the copy
+ * (engine.py:136-141's id gather).  The arrays must outlive the handle or
+ * be cleared first. */
+int tsk_db_set_host_ids(tsk_db *db, const int64_t *traj, const int64_t *seg);
 
 /* Stable device sort of n start times: perm[i] = input row of sorted row i
  * (numpy argsort kind="stable", core.py:163). */

@@ -50,6 +50,7 @@ SIGNATURES = {
     "tsk_db_create": ([ctypes.c_int, ctypes.POINTER(Columns), ctypes.POINTER(_P)], ctypes.c_int),
     "tsk_db_free": ([_P], None),
     "tsk_db_size": ([_P], _I64),
+    "tsk_db_set_host_ids": ([_P, _PI64, _PI64], ctypes.c_int),
     "tsk_sort_by_start": ([ctypes.c_int, _I64, _PD, _PI64], ctypes.c_int),
     "tsk_index_build": ([_P, _I64, ctypes.c_int, _PI64, _PD], ctypes.c_int),
     "tsk_index_copy": ([_P, _PD, _PD, _PI64, _PI64, _PI64], ctypes.c_int),
@@ -188,6 +189,10 @@ class DeviceStore:
         self.handle = h
         self.n = len(store)
         self.index_token = None
+        # host id columns for the compact result path (kept alive here)
+        self._host_ids = (np.ascontiguousarray(store.traj, np.int64), np.ascontiguousarray(store.seg, np.int64))
+        check(lib.tsk_db_set_host_ids(h, self._host_ids[0].ctypes.data_as(_PI64),
+                                      self._host_ids[1].ctypes.data_as(_PI64)))
 
     def __del__(self):
         h = getattr(self, "handle", None)

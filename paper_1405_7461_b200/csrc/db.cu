@@ -130,6 +130,7 @@ __global__ void k_hoist(int64_t n, const double *__restrict__ ts, const double *
         unsafe[i] = h.unsafe ? 1 : 0;
         if (h.unsafe) atomicOr(&flags[0], 1);
         if (i + 1 < n && ts[i + 1] < t0) atomicOr(&flags[1], 1);
+        if (i + 1 < n && te[i + 1] < te[i]) atomicOr(&flags[1], 2);
     }
 }
 
@@ -151,7 +152,8 @@ void soa_hoist(Soa &s, cudaStream_t st) {
     TSK_CUDA(cudaFreeAsync(flags, st));
     TSK_CUDA(cudaStreamSynchronize(st));
     s.any_unsafe = h[0];
-    s.sorted = h[1] ? 0 : 1;
+    s.sorted = (h[1] & 1) ? 0 : 1;
+    s.te_sorted = (h[1] & 2) ? 0 : 1;
 }
 
 // Group bounds (GBound): one warp per group of GB_SIZE segments.
@@ -270,6 +272,7 @@ __global__ void k_qprep(int64_t n, const double *__restrict__ ts, const double *
         r.flag = h.unsafe ? 1.0 : 0.0;
         out[i] = r;
         if (i + 1 < n && ts[i + 1] < r.ts) atomicOr(&flags[0], 1);
+        if (i + 1 < n && te[i + 1] < r.te) atomicOr(&flags[0], 2);
         cm = fmax(cm, fmax(fmax(fabs(r.sx), fabs(r.sy)), fmax(fabs(r.sz), fmax(fabs(r.ex), fmax(fabs(r.ey), fabs(r.ez))))));
     }
     for (int o = 16; o; o >>= 1) cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, o));
@@ -307,6 +310,7 @@ __global__ void k_qprep_mapped(int64_t n, tsk_columns c, double *__restrict__ ts
         r.flag = h.unsafe ? 1.0 : 0.0;
         out[i] = r;
         if (i + 1 < n && c.ts[i + 1] < r.ts) atomicOr(&flags[0], 1);
+        if (i + 1 < n && c.te[i + 1] < r.te) atomicOr(&flags[0], 2);
         cm = fmax(cm, fmax(fmax(fabs(r.sx), fabs(r.sy)), fmax(fabs(r.sz), fmax(fabs(r.ex), fmax(fabs(r.ey), fabs(r.ez))))));
     }
     for (int o = 16; o; o >>= 1) cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, o));
@@ -385,14 +389,6 @@ using namespace tsk;
 
 namespace tsk {
 
-// bin of ordinal i: min(floor_divide(ts - t0, width), m - 1) (index.py:108-112)
-__device__ __forceinline__ int64_t bin_of(double t, double t0, double width, int64_t m) {
-    if (!(width > 0.0)) return 0;
-    double f = np_floor_divide(__dsub_rn(t, t0), width);
-    double mm = (double)(m - 1);
-    f = f < mm ? f : mm;  // np.minimum(float, m - 1)
-    return (int64_t)f;
-}
 
 // Runs of equal bin id are contiguous because ts is sorted; record the
 // first/last ordinal of each run (the searchsorted pair of index.py:116-118).
@@ -535,7 +531,8 @@ void launch_ranges(tsk_db *db, const Soa &q, SearchPlanDev &p, bool spans_given,
 // Single block: choose the query tile and the candidate sub-tile count so
 // the grid gets at least ~4 waves of items, then count items per work unit
 // (plan_unit: batch pairs sharing candidates, and the rest) and scan them.
-__global__ void __launch_bounds__(1024, 1) k_plan_items(SearchPlanDev p, int64_t slots, int stride, int pair) {
+__global__ void __launch_bounds__(1024, 1) k_plan_items(SearchPlanDev p, int64_t slots, int stride, int pair,
+                                                         int align) {
     typedef cub::BlockReduce<long long, 1024> BR;
     typedef cub::BlockScan<long long, 1024> BS;
     __shared__ union {
@@ -581,7 +578,9 @@ __global__ void __launch_bounds__(1024, 1) k_plan_items(SearchPlanDev p, int64_t
         if (u < nu) {
             const Unit U = plan_unit(p, u, tqs, pr);
             if (U.f <= U.l) {
-                const long long c = U.l - U.f + 1;
+                // candidate tiles start at a multiple of `align` (K1 layout:
+                // warps then coincide with the box groups; the head is masked)
+                const long long c = U.l - (U.f / align) * align + 1;
                 const long long tq = U.b1 >= 0 ? 1 : (U.s + tqs - 1) / tqs;
                 v = ((c + ct - 1) / ct) * tq;
             }
@@ -602,8 +601,8 @@ __global__ void __launch_bounds__(1024, 1) k_plan_items(SearchPlanDev p, int64_t
     }
 }
 
-void launch_plan_items(SearchPlanDev &p, int slots, int stride, int pair, cudaStream_t st) {
-    k_plan_items<<<1, 1024, 0, st>>>(p, slots, stride, pair);
+void launch_plan_items(SearchPlanDev &p, int slots, int stride, int pair, int align, cudaStream_t st) {
+    k_plan_items<<<1, 1024, 0, st>>>(p, slots, stride, pair, align);
     TSK_CUDA(cudaGetLastError());
 }
 
@@ -678,6 +677,7 @@ extern "C" int tsk_db_replicate(const tsk_db *src, int device, tsk_db **out) {
         }
         db->s.any_unsafe = src->s.any_unsafe;
         db->s.sorted = src->s.sorted;
+        db->s.te_sorted = src->s.te_sorted;
         db->cmax = src->cmax;
         TSK_CUDA(cudaStreamSynchronize(db->stream));
         *out = db;
@@ -694,12 +694,17 @@ extern "C" void tsk_db_free(tsk_db *db) {
     if (db->stream) cudaStreamSynchronize(db->stream);
     db->s.storage.release(db->stream);
     db->ix.storage.release(db->stream);
+    free_k1_layout(db);
     db->q.storage.release(db->stream);
     for (DBuf *b : {&db->q_rec, &db->batches, &db->counters, &db->recs, &db->sorted, &db->cub_tmp,
                     &db->out_cols, &db->canon_cols, &db->canon_tmp})
         b->release(db->stream);
     for (cudaEvent_t ev : {db->ev0, db->ev1, db->ev_k0, db->ev_k1})
         if (ev) cudaEventDestroy(ev);
+    if (db->stream2) {
+        cudaStreamSynchronize(db->stream2);
+        cudaStreamDestroy(db->stream2);
+    }
     if (db->stream) cudaStreamDestroy(db->stream);
     delete db;
 }
@@ -837,6 +842,15 @@ extern "C" int tsk_index_build(tsk_db *db, int64_t m, int extent_rule, int64_t *
         ix.t0 = t0;
         ix.t_max = tmax;
         ix.built = true;
+        // K1's spatially ordered copy for this index's bins (layout.cu); when
+        // it cannot be built (device memory) K1 reads the start-sorted store
+        try {
+            build_k1_layout(db, st);
+        } catch (const Error &) {
+            cudaGetLastError();
+            cudaStreamSynchronize(st);
+            free_k1_layout(db);
+        }
         if (n_nonempty) *n_nonempty = n_ne;
         if (hdr) {
             hdr[0] = width;

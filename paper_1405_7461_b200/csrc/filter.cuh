@@ -105,6 +105,13 @@ TSK_HD bool filter_ok(double cmax, double d2) {
     return cmax <= 0x1p250 && d2 <= 0x1p500 && (cmax == 0.0 || cmax >= 0x1p-200);
 }
 
+// Launch-level validity of K1's FP32 path: |coordinates| and d below 2^60
+// inside the FP64 filter's window.  The box-cull fast path and the external
+// overlap count (layout.cu) run exactly when this holds.
+TSK_HD bool k1f_launch_ok(double cmax, double d2) {
+    return filter_ok(cmax, d2) && d2 <= 0x1p120 && cmax <= 0x1p60;
+}
+
 // velocity component of a hoisted segment: RN(d * rcp), rcp = RN(1/ext) or 0
 TSK_HD double seg_velocity(double d, double rcp) { return d * rcp; }
 
@@ -293,14 +300,62 @@ TSK_HD float f32_n2(const CandF32 &c, float qts, float qx, float qy, float qz) {
 #endif
 }
 
+// ── box cull (K1 layout) ───────────────────────────────────────────────────
+//
+// While both segments of a pair are active each moving point lies on its own
+// segment, so the pair's separation is at least the gap between the two
+// segments' bounding boxes.  A reference hit needs the separation at some
+// instant of the shared span within (1 + 2^-20) d plus the reference's own
+// rounding (2^-38 C, see the FP32 pre-filter below), so a gap above
+//   R = (1 + 2^-8) d + 2^-30 C      (C: max |coordinate| of the launch)
+// proves a miss.  Boxes are rounded outward to FP32 and the gap, its square
+// and sum are rounded down, so the tested value never exceeds the true gap²;
+// R² is rounded up.  tools/filter_check.cpp checks this on the adversarial
+// pairs: no reference hit is ever culled.
+TSK_HD float box_cull_r2(double d, double cmax) {
+    const double r = (1.0 + 0x1p-8) * d + 0x1p-30 * cmax + 0x1p-100;
+    return TSK_F2F_RU(r * r * (1.0 + 0x1p-40));
+}
+
+#ifndef __CUDA_ARCH__
+inline float tsk_f2f_rd(double x) {
+    float f = (float)x;
+    if ((double)f > x) f = nextafterf(f, -INFINITY);
+    return f;
+}
+#endif
+#ifdef __CUDA_ARCH__
+#define TSK_F2F_RD(x) __double2float_rd(x)
+#else
+#define TSK_F2F_RD(x) tsk_f2f_rd(x)
+#endif
+
+// squared gap between boxes [gl, gh] and [ql, qh] (per axis), rounded down
+TSK_HD float box_gap2(float glx, float gly, float glz, float ghx, float ghy, float ghz, float qlx, float qly,
+                      float qlz, float qhx, float qhy, float qhz) {
+#ifdef __CUDA_ARCH__
+    const float gx = fmaxf(fmaxf(__fsub_rd(glx, qhx), __fsub_rd(qlx, ghx)), 0.f);
+    const float gy = fmaxf(fmaxf(__fsub_rd(gly, qhy), __fsub_rd(qly, ghy)), 0.f);
+    const float gz = fmaxf(fmaxf(__fsub_rd(glz, qhz), __fsub_rd(qlz, ghz)), 0.f);
+    return __fmaf_rd(gz, gz, __fmaf_rd(gy, gy, __fmul_rd(gx, gx)));
+#else
+    auto sub = [](float a, float b) { return tsk_fma_dir(1.0f, a, -b, FE_DOWNWARD); };
+    const float gx = std::fmax(std::fmax(sub(glx, qhx), sub(qlx, ghx)), 0.f);
+    const float gy = std::fmax(std::fmax(sub(gly, qhy), sub(qly, ghy)), 0.f);
+    const float gz = std::fmax(std::fmax(sub(glz, qhz), sub(qlz, ghz)), 0.f);
+    return tsk_fma_dir(gz, gz, tsk_fma_dir(gy, gy, tsk_fma_dir(gx, gx, 0.f, FE_DOWNWARD), FE_DOWNWARD),
+                       FE_DOWNWARD);
+#endif
+}
+
 // Two candidates of a lane in packed form: component c of candidates k0/k1
 // in one float2 (sm_100's FFMA2 / FADD2 / FMUL2 then issue one instruction
 // for both, the query's scalar broadcast as the .F32 operand).
+#ifdef __CUDACC__
 struct CandF32x2 {
     float2 px, py, pz, vx, vy, vz;
 };
 
-#ifdef __CUDACC__
 // f32_n2 of two candidates at once: the same IEEE operations, per half, in
 // the same order and rounding (u = RN(RN(ts v + p) - s); |u|^2 rounded
 // down), so every flag equals the scalar form's (and the margin proof,

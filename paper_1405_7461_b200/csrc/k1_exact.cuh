@@ -142,6 +142,7 @@ __device__ __forceinline__ Hit rare_pair(const Cand &r, const QRec &Q, double cc
 
 struct ItemCtx {
     int64_t b, lo_q, first_c, c_hi;  // batch, tile's first query ordinal, tile's candidate range
+    int64_t c_lo;                    // first valid candidate (first_c may be aligned below it)
     int64_t q0;                      // first query offset within batch b (tile)
     int64_t b1;                      // shared unit: the second batch (queries js..nt-1), else -1
     int nt, js;                      // staged queries; queries of batch b (nt when single)
@@ -237,6 +238,7 @@ struct FlushCfg {
     uint64_t cap;
     double d2;
     int minor_bits, query_major;
+    const int64_t *orig;  // K1 layout position -> start-sorted ordinal (nullptr: identity)
 };
 
 __device__ __forceinline__ Cand cand_exact(const FlushCfg &C, int64_t e) {
@@ -259,6 +261,7 @@ struct __align__(16) QF32 {
 struct WarpCtx {
     uint64_t key_base0;     // key of (b, e_off of candidate 0, it.q0) without the j term
     uint64_t key_base1;     // the same for b1 (query offset 0 at tile index js)
+    int64_t f0, f1;         // first candidate ordinal of b / b1 (K1 layout: e_off = orig - f)
     int js;                 // tile index of b1's first query (nt when single)
     double wmin_te, wmax;   // min te / max te of the warp's candidates (tb cases)
     int64_t wbase;          // entry ordinal of the warp's candidate 0
@@ -333,8 +336,13 @@ __device__ __noinline__ void rare_flush(const QRec *__restrict__ qt, const uint3
         // within the batch the query belongs to
         second = j >= k1_wctx[warp].js;
         const uint64_t jj = (uint64_t)(second ? j - k1_wctx[warp].js : j);
+        // the entry term: the candidate's offset in the warp, or in the K1
+        // layout its start-sorted ordinal's offset within the batch's range
+        const uint64_t et = C.orig ? (uint64_t)(C.orig[k1_wctx[warp].wbase + ci] -
+                                                (second ? k1_wctx[warp].f1 : k1_wctx[warp].f0))
+                                   : (uint64_t)ci;
         key = (second ? k1_wctx[warp].key_base1 : k1_wctx[warp].key_base0) +
-              (C.query_major ? (jj << C.minor_bits) + (uint64_t)ci : ((uint64_t)ci << C.minor_bits) + jj);
+              (C.query_major ? (jj << C.minor_bits) + et : (et << C.minor_bits) + jj);
     }
     n_hit += h.hit ? (second ? CNT_B1 : 1ull) : 0ull;
     append_hit_w(C, h.hit, key, h.tb, h.te, lane);
@@ -355,6 +363,17 @@ __device__ __forceinline__ int lower_bound_pm(const double *pm, int n, double v)
         int m = (a + b) >> 1;
         if (pm[m] >= v) b = m;
         else a = m + 1;
+    }
+    return a;
+}
+
+// first index with a[m] > v in a non-decreasing array
+__device__ __forceinline__ int upper_bound_arr(const double *a_, int n, double v) {
+    int a = 0, b = n;
+    while (a < b) {
+        int m = (a + b) >> 1;
+        if (a_[m] <= v) a = m + 1;
+        else b = m;
     }
     return a;
 }
@@ -470,7 +489,11 @@ __device__ __forceinline__ ItemCtx decode_item(const K1Launch &L, int64_t item, 
         c.js = c.nt;
     }
     c.lo_q = U.lo_q + c.q0;
-    c.first_c = U.f + tc * ct;
+    // K1 layout (L.cull): tiles start at a BOX_GROUP multiple (k_plan_items
+    // counts them the same way); candidates before U.f are masked
+    const int64_t f0 = L.cull ? (U.f / BOX_GROUP) * BOX_GROUP : U.f;
+    c.first_c = f0 + tc * ct;
+    c.c_lo = U.f;
     c.c_hi = c.first_c + ct - 1 < U.l ? c.first_c + ct - 1 : U.l;
     return c;
 }
@@ -489,6 +512,23 @@ __device__ __forceinline__ void fill_flush_cfg(const K1Launch &L) {
     f.d2 = L.d2;
     f.minor_bits = L.minor_bits;
     f.query_major = L.query_major;
+    f.orig = L.orig;
+}
+
+// Key bases of a warp's sub-tile (lane 0): without a K1 layout the entry
+// offset of candidate 0 is folded in; with one each hit adds its own
+// (orig - f).
+__device__ __forceinline__ void set_key_bases(const K1Launch &L, const ItemCtx &it, int64_t wbase, int warp) {
+    const int64_t f0 = L.plan.first[it.b], f1 = it.b1 >= 0 ? L.plan.first[it.b1] : 0;
+    if (L.orig) {
+        k1_wctx[warp].key_base0 = make_key(L, it.b, 0, it.q0);
+        k1_wctx[warp].key_base1 = it.b1 >= 0 ? make_key(L, it.b1, 0, 0) : 0;
+    } else {
+        k1_wctx[warp].key_base0 = make_key(L, it.b, wbase - f0, it.q0);
+        k1_wctx[warp].key_base1 = it.b1 >= 0 ? make_key(L, it.b1, wbase - f1, 0) : 0;
+    }
+    k1_wctx[warp].f0 = f0;
+    k1_wctx[warp].f1 = f1;
 }
 
 // Running max (warp 0) / suffix min (warp 1) of the tile's end times.

@@ -57,6 +57,13 @@ __device__ __forceinline__ float *f_cands(int warp) {
     return reinterpret_cast<float *>(k1_dyn + sizeof(QF32) * K1_TQ + sizeof(uint32_t) * QCAP * K1_WARPS) +
            warp * 7 * WCAND;
 }
+// query boxes (2 float4 per staged query: lo, hi of its segment, FP32 outward)
+constexpr size_t QBOX_OFF = sizeof(QF32) * K1_TQ + sizeof(uint32_t) * QCAP * K1_WARPS + sizeof(float) * 7 * WCAND * K1_WARPS;
+__device__ __forceinline__ float4 *f_qbox() { return reinterpret_cast<float4 *>(k1_dyn + QBOX_OFF); }
+// per-warp list of the window's queries that survive the box cull
+__device__ __forceinline__ uint16_t *f_wlist(int warp) {
+    return reinterpret_cast<uint16_t *>(k1_dyn + QBOX_OFF + 2 * sizeof(float4) * K1_TQ) + warp * K1_TQ;
+}
 
 __device__ __forceinline__ void lds4f(uint32_t a, float &x, float &y, float &z, float &w) {
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "r"(a));
@@ -237,6 +244,110 @@ __device__ __noinline__ uint4 f32_scan2(uint32_t qa, uint32_t qa_end, uint32_t b
     return make_uint4(qa, (unsigned)qn, 0u, 0u);
 }
 
+// f32_scan2 over the warp's list of surviving queries (box cull): the same
+// two-query iteration, the tile indices read from the list.  Returns
+// (next list position, queued).
+__device__ __noinline__ uint2 f32_scanl(int k, int ns, uint32_t base, int qn, int warp, int lane) {
+    uint32_t *const wq = f_queue(warp);
+    const uint16_t *const wl = f_wlist(warp);
+    const float *cs = f_cands(warp);
+    CandF32x2 c[CPT / 2];
+    load_cands_x2(cs, lane, c);
+    float srl = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < CPT; ++kk) srl = fmaxf(srl, cs[6 * WCAND + kk * 32 + lane]);
+    constexpr uint32_t QB = (uint32_t)sizeof(QF32);
+    for (; k < ns; k += 2) {
+        const uint32_t j0 = wl[k], j1 = k + 1 < ns ? wl[k + 1] : j0;
+        const uint32_t qa0 = base + j0 * QB, qa1 = base + j1 * QB;
+        float ts0, x0, y0, z0, a0, b0, ts1, x1, y1, z1, a1, b1, p0, p1;
+        lds4f(qa0, ts0, x0, y0, z0);
+        lds4f(qa0 + 16, a0, b0, p0, p1);
+        lds4f(qa1, ts1, x1, y1, z1);
+        lds4f(qa1 + 16, a1, b1, p0, p1);
+        const float R0 = f32_r2(a0, srl, b0), R1 = f32_r2(a1, srl, b1);
+        float n0[CPT], n1[CPT];
+        norms_x2(c, ts0, x0, y0, z0, n0);
+        norms_x2(c, ts1, x1, y1, z1, n1);
+        float m0 = n0[0], m1 = n1[0];
+#pragma unroll
+        for (int kk = 1; kk < CPT; ++kk) {
+            m0 = f32_min_nan(m0, n0[kk]);
+            m1 = f32_min_nan(m1, n1[kk]);
+        }
+        const bool f0 = !f32_far(m0, R0), f1 = !f32_far(m1, R1);
+        if (!__any_sync(0xffffffffu, f0 || f1)) continue;
+        if (__any_sync(0xffffffffu, f0)) queue_query(wq, n0, R0, j0, lane, qn);
+        if (qn >= 32) {  // the second query is scanned again by the next call
+            k += 1;
+            break;
+        }
+        if (k + 1 < ns && __any_sync(0xffffffffu, f1)) queue_query(wq, n1, R1, j1, lane, qn);
+        if (qn >= 32) {
+            k += 2;
+            break;
+        }
+    }
+    if (k > ns) k = ns;
+    return make_uint2((unsigned)k, (unsigned)qn);
+}
+
+// Box cull of a warp's window (K1 layout): lane j tests query jlo + j + 32i
+// against the bounding box of the warp's 128 candidates (the union of the
+// precomputed boxes of the two BOX_GROUPs they span); survivors are listed
+// in f_wlist in window order.  A pair can hit only if its two segments'
+// boxes are within R = (1 + 2^-8) d + 2^-30 C (box_cull_r2): the gap is
+// formed from boxes rounded outward and rounded down itself, so it never
+// exceeds the true gap.  Returns the number of survivors (warp-uniform).
+__device__ __forceinline__ int box_cull(const float4 *__restrict__ gbox, int64_t n, int64_t wbase, int jlo, int jhi,
+                                        float r2, int warp, int lane) {
+    const int64_t g0 = wbase / BOX_GROUP;
+    int64_t g1 = (wbase + WCAND - 1) / BOX_GROUP;
+    const int64_t glast = (n - 1) / BOX_GROUP;
+    g1 = g1 < glast ? g1 : glast;
+    float4 lo = gbox[2 * g0], hi = gbox[2 * g0 + 1];
+    if (g1 != g0) {
+        const float4 l1 = gbox[2 * g1], h1 = gbox[2 * g1 + 1];
+        lo = make_float4(fminf(lo.x, l1.x), fminf(lo.y, l1.y), fminf(lo.z, l1.z), 0.f);
+        hi = make_float4(fmaxf(hi.x, h1.x), fmaxf(hi.y, h1.y), fmaxf(hi.z, h1.z), 0.f);
+    }
+    const float4 *qb = f_qbox();
+    uint16_t *const wl = f_wlist(warp);
+    unsigned lt;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+    int ns = 0;
+    for (int jb = jlo; jb < jhi; jb += 32) {
+        const int j = jb + lane;
+        bool pass = false;
+        if (j < jhi) {
+            const float4 ql = qb[2 * j], qh = qb[2 * j + 1];
+            pass = !(box_gap2(lo.x, lo.y, lo.z, hi.x, hi.y, hi.z, ql.x, ql.y, ql.z, qh.x, qh.y, qh.z) > r2);
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, pass);
+        if (pass) wl[ns + __popc(m & lt)] = (uint16_t)j;
+        ns += __popc(m);
+    }
+    __syncwarp();
+    return ns;
+}
+
+// The scan over the survivors: scan, flush 32 at a time, resume (the
+// single-scan window's cases, TA_BOTH / TB_DYN).
+__device__ __forceinline__ void f32_list_range(const QRec *__restrict__ qt, const QF32 *__restrict__ sqf, int ns,
+                                               int warp, int lane, unsigned long long &n_hit) {
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(sqf);
+    uint32_t *const wq = f_queue(warp);
+    int k = 0, qn = 0;
+    for (;;) {
+        const uint2 o = f32_scanl(k, ns, base, qn, warp, lane);
+        k = (int)o.x;
+        qn = (int)o.y;
+        const bool done = k >= ns;
+        flush_queue<TA_BOTH, TB_DYN, false, CPT>(qt, wq, warp, lane, qn, done, n_hit);
+        if (done) break;
+    }
+}
+
 // One (TA, TB) range of the window: scan, flush 32 at a time, resume.
 template <int TA, int TB, bool CNT>
 __device__ __forceinline__ void f32_range(const QRec *__restrict__ qt, const QF32 *__restrict__ sqf, int j0,
@@ -294,6 +405,105 @@ __device__ __forceinline__ void all_range(const QRec *__restrict__ qt, const QF3
     }
 }
 
+// The warp's candidates in FP32 pre-filter form, staged in shared memory
+// (structure of arrays, lane-interleaved); invalid lanes are far away (and
+// rejected exactly if ever flagged).
+__device__ __forceinline__ void stage_cands(const K1Launch &L, int64_t wbase, int64_t c_lo, int64_t c_hi,
+                                            const double (&rts)[CPT],
+                                            const F32Item &fi, float *wcs, int lane) {
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+        const int i = k * 32 + lane;
+        const int64_t e = wbase + i;
+        CandF32 c;
+        c.px = c.py = c.pz = 0x1p60f;
+        c.vx = c.vy = c.vz = c.sr = 0.f;
+        if (e >= c_lo && e <= c_hi)
+            c = f32_cand_sr(rts[k], L.e.sx[e], L.e.sy[e], L.e.sz[e], L.e.vx[e], L.e.vy[e], L.e.vz[e], L.e.sr32[e], fi);
+        wcs[0 * WCAND + i] = c.px; wcs[1 * WCAND + i] = c.py; wcs[2 * WCAND + i] = c.pz;
+        wcs[3 * WCAND + i] = c.vx; wcs[4 * WCAND + i] = c.vy; wcs[5 * WCAND + i] = c.vz;
+        wcs[6 * WCAND + i] = c.sr;
+    }
+}
+
+// One warp sub-tile on the box-cull fast path (K1 layout, overlaps counted
+// outside K1).  The window is every query whose extent meets the time range
+// of the candidates' groups (two bisections on the tile's sorted ts / te);
+// pairs in it that do not overlap in time are rejected by the exact path if
+// they are ever flagged.  Only warps with a query near their box load their
+// candidates.
+__device__ __noinline__ void fast_subtile(const K1Launch &L, const ItemCtx &it, const QRec *__restrict__ qt,
+                                          const QF32 *__restrict__ sqf, const double *pm, const double *sm,
+                                          int64_t wbase, float cull_r2, const F32Item &fi, bool item_f32, float *wcs,
+                                          int warp, int lane, unsigned long long &n_ev, unsigned long long &n_hit) {
+    const int64_t g0 = wbase / BOX_GROUP;
+    int64_t g1 = (wbase + WCAND - 1 < it.c_hi ? wbase + WCAND - 1 : it.c_hi) / BOX_GROUP;
+    double2 tr = L.gtime[g0];
+    if (g1 != g0) {
+        const double2 t1 = L.gtime[g1];
+        tr.x = tr.x < t1.x ? tr.x : t1.x;
+        tr.y = tr.y > t1.y ? tr.y : t1.y;
+    }
+    // window [jlo, jhi): te_j >= min ts (pm: te ascending) and ts_j <= max te
+    // (sm: ts ascending); both arrays are +inf padded to 2 * K1_TQ
+    int v = 0;
+    if (lane == 0) v = lower_bound_pm(pm, it.nt, tr.x);
+    else if (lane == 1) v = upper_bound_arr(sm, it.nt, tr.y);
+    const int jlo = __shfl_sync(0xffffffffu, v, 0);
+    int jhi = __shfl_sync(0xffffffffu, v, 1);
+    if (jhi < jlo) jhi = jlo;
+    const int ns = box_cull(L.gbox, L.e.n, wbase, jlo, jhi, cull_r2, warp, lane);
+    if (ns == 0) return;
+    // survivors: this warp's candidates
+    double rts[CPT], rte[CPT];
+    bool unsafe_r = false;
+    double wmin = INFINITY, wmax = -INFINITY, wmin_te = INFINITY, wmax_ts = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+        const int64_t e = wbase + k * 32 + lane;
+        rts[k] = INFINITY;
+        rte[k] = -INFINITY;
+        if (e >= it.c_lo && e <= it.c_hi) {
+            rts[k] = L.e.ts[e];
+            rte[k] = L.e.te[e];
+            unsafe_r |= L.e.unsafe[e] != 0;
+            wmin = rts[k] < wmin ? rts[k] : wmin;
+            wmax = rte[k] > wmax ? rte[k] : wmax;
+            wmin_te = rte[k] < wmin_te ? rte[k] : wmin_te;
+            wmax_ts = rts[k] > wmax_ts ? rts[k] : wmax_ts;
+        }
+    }
+    wmax = warp_max(wmax);
+    wmin_te = warp_min(wmin_te);
+    if (lane == 0) {
+        set_key_bases(L, it, wbase, warp);
+        k1_wctx[warp].js = it.js;
+        k1_wctx[warp].wbase = wbase;
+        const int64_t nv = it.c_hi - wbase + 1;
+        k1_wctx[warp].nvalid = nv < 0 ? 0 : (nv > WCAND ? WCAND : (int)nv);
+        k1_wctx[warp].wmin_te = wmin_te;
+        k1_wctx[warp].wmax = wmax;
+    }
+    __syncwarp();
+    if (!item_f32 || __any_sync(0xffffffffu, unsafe_r)) {
+        // extreme-exponent candidates or an item outside the FP32 path's
+        // bounds: the exact path over the whole window
+        // (its per-pair overlap counts are not needed here)
+        unsigned long long ov_unused = 0;
+        wmin = warp_min(wmin);
+        wmax_ts = warp_max(wmax_ts);
+        const int4 w = warp_window(sqf, pm, it.nt, false, wmin, wmax, wmax_ts, lane);
+        all_range<TA_C>(qt, sqf, w.x, w.y, rts, rte, warp, lane, ov_unused, n_hit);
+        all_range<TA_BOTH>(qt, sqf, w.y, w.z, rts, rte, warp, lane, ov_unused, n_hit);
+        all_range<TA_R>(qt, sqf, w.z, w.w, rts, rte, warp, lane, ov_unused, n_hit);
+        return;
+    }
+    n_ev += (unsigned long long)ns * (unsigned long long)k1_wctx[warp].nvalid;
+    stage_cands(L, wbase, it.c_lo, it.c_hi, rts, fi, wcs, lane);
+    __syncwarp();
+    f32_list_range(qt, sqf, ns, warp, lane, n_hit);
+}
+
 __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Launch L) {
     // running max / suffix min of te over the tile; on single-scan items
     // (times ascending) te / ts themselves, +inf padded for tile_bounds
@@ -319,8 +529,10 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
     const double cmax = L.db_cmax > cq ? L.db_cmax : cq;
     // launch-level validity: the FP32 pre-filter needs |coordinates| and d
     // below 2^60 (and the FP64 filter's window for the exact division)
-    const bool launch_ok = filter_ok(cmax, L.d2) && L.d2 <= 0x1p120 && cmax <= 0x1p60;
+    const bool launch_ok = k1f_launch_ok(cmax, L.d2);
     const double dthr = sqrt(L.d2);  // d (sqrt(RN(d^2)) >= d (1 - 2^-52); the margin covers it)
+    const float cull_r2 = box_cull_r2(dthr, cmax);  // filter.cuh
+    const bool cull = L.cull && launch_ok;
 
     for (;;) {
         if (tid == 0) {
@@ -385,8 +597,12 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
         __syncthreads();
         const bool unsafe_q = flags_sh & 1;
         const bool te_sorted = !(flags_sh & 2);
-        const bool q_unsorted = *L.q_unsorted != 0;
+        const bool q_unsorted = (*L.q_unsorted & 1) != 0;  // bit 0: query ts, bit 1: query te not sorted
         const bool single_scan = te_sorted && !q_unsorted && !L.overlaps_only;
+        // box-cull fast path: overlaps are counted outside K1
+        // (count_overlaps_ext), so a warp whose window has no query near its
+        // box costs two bisections and the box tests, nothing per candidate
+        const bool fast = cull && L.ext_count && (*L.q_unsorted & 3) == 0 && single_scan;
         if (tid == 0) {
             fi_sh = f32_item(qt[0].sx, qt[0].sy, qt[0].sz, qt[0].ts, f32b[0], f32b[1], f32b[2], f32b[3], f32b[4],
                              f32b[5], cmax);
@@ -409,6 +625,13 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
             f.ts64 = q.ts;
             f.te64 = q.te;
             sqf[j] = f;
+            if (cull) {  // the query segment's box, rounded outward
+                f_qbox()[2 * j] = make_float4(__double2float_rd(fmin(q.sx, q.ex)), __double2float_rd(fmin(q.sy, q.ey)),
+                                              __double2float_rd(fmin(q.sz, q.ez)), 0.f);
+                f_qbox()[2 * j + 1] = make_float4(__double2float_ru(fmax(q.sx, q.ex)),
+                                                  __double2float_ru(fmax(q.sy, q.ey)),
+                                                  __double2float_ru(fmax(q.sz, q.ez)), 0.f);
+            }
         }
         __syncthreads();
         if (single_scan) {
@@ -427,26 +650,24 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
             const int64_t base = it.first_c + (int64_t)s * STRIDE;
             if (base > it.c_hi) break;  // block-uniform
             const int64_t wbase = base + (int64_t)warp * WCAND;
+            if (fast) {
+                if (wbase > it.c_hi || L.noop) continue;
+                fast_subtile(L, it, qt, sqf, pm, sm, wbase, cull_r2, fi_sh, item_f32, wcs, warp, lane, n_ev, n_hit);
+                continue;
+            }
             double rts[CPT], rte[CPT];
             bool valid_any = false, unsafe_r = false;
             double wmin = INFINITY, wmax = -INFINITY, wmin_te = INFINITY, wmax_ts = -INFINITY;
 #pragma unroll
             for (int k = 0; k < CPT; ++k) {
-                const int i = k * 32 + lane;
-                const int64_t e = wbase + i;
-                const bool valid = e <= it.c_hi;
-                CandF32 c;
-                c.px = c.py = c.pz = 0x1p60f;  // invalid lanes: far away (and rejected exactly if flagged)
-                c.vx = c.vy = c.vz = c.sr = 0.f;
+                const int64_t e = wbase + k * 32 + lane;
+                const bool valid = e >= it.c_lo && e <= it.c_hi;
                 rts[k] = INFINITY;
                 rte[k] = -INFINITY;
                 if (valid) {
                     rts[k] = L.e.ts[e];
                     rte[k] = L.e.te[e];
                     unsafe_r |= L.e.unsafe[e] != 0;
-                    if (item_f32)
-                        c = f32_cand_sr(rts[k], L.e.sx[e], L.e.sy[e], L.e.sz[e], L.e.vx[e], L.e.vy[e], L.e.vz[e],
-                                        L.e.sr32[e], fi_sh);
                     // times are finite (validated): plain selects, no NaN handling
                     wmin = rts[k] < wmin ? rts[k] : wmin;
                     wmax = rte[k] > wmax ? rte[k] : wmax;
@@ -454,17 +675,13 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
                     wmax_ts = rts[k] > wmax_ts ? rts[k] : wmax_ts;
                 }
                 valid_any |= valid;
-                wcs[0 * WCAND + i] = c.px; wcs[1 * WCAND + i] = c.py; wcs[2 * WCAND + i] = c.pz;
-                wcs[3 * WCAND + i] = c.vx; wcs[4 * WCAND + i] = c.vy; wcs[5 * WCAND + i] = c.vz;
-                wcs[6 * WCAND + i] = c.sr;
             }
             if (L.noop) continue;
             if (!__any_sync(0xffffffffu, valid_any)) continue;
             wmax = warp_max(wmax);
             wmin_te = warp_min(wmin_te);
             if (lane == 0) {
-                k1_wctx[warp].key_base0 = make_key(L, it.b, wbase - L.plan.first[it.b], it.q0);
-                k1_wctx[warp].key_base1 = it.b1 >= 0 ? make_key(L, it.b1, wbase - L.plan.first[it.b1], 0) : 0;
+                set_key_bases(L, it, wbase, warp);
                 k1_wctx[warp].js = it.js;
                 k1_wctx[warp].wbase = wbase;
                 const int64_t nv = it.c_hi - wbase + 1;
@@ -494,10 +711,25 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
                 jlo = __reduce_min_sync(0xffffffffu, jlo);
                 jhi = __reduce_max_sync(0xffffffffu, jhi);
                 if (jhi < jlo) jhi = jlo;
+                if (cull) {
+                    // K1 layout: one box test per (query, warp) first; the
+                    // candidates are converted only when a query survives
+                    const int ns = box_cull(L.gbox, L.e.n, wbase, jlo, jhi, cull_r2, warp, lane);
+                    n_ev += (unsigned long long)ns * (unsigned long long)k1_wctx[warp].nvalid;
+                    if (ns == 0) continue;
+                    stage_cands(L, wbase, it.c_lo, it.c_hi, rts, fi_sh, wcs, lane);
+                    __syncwarp();
+                    f32_list_range(qt, sqf, ns, warp, lane, n_hit);
+                    continue;
+                }
+                stage_cands(L, wbase, it.c_lo, it.c_hi, rts, fi_sh, wcs, lane);
+                __syncwarp();
                 n_ev += (unsigned long long)(jhi - jlo) * (unsigned long long)k1_wctx[warp].nvalid;
                 f32_range<TA_BOTH, TB_DYN, false>(qt, sqf, jlo, jhi, warp, lane, n_ov, n_hit);
                 continue;
             }
+            if (item_f32) stage_cands(L, wbase, it.c_lo, it.c_hi, rts, fi_sh, wcs, lane);
+            __syncwarp();
             wmin = warp_min(wmin);
             wmax_ts = warp_max(wmax_ts);
             const int4 w = warp_window(sqf, pm, it.nt, q_unsorted, wmin, wmax, wmax_ts, lane);
@@ -541,7 +773,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
 }
 
 static size_t k1f_dyn_smem() {
-    return sizeof(QF32) * K1_TQ + sizeof(uint32_t) * QCAP * K1_WARPS + sizeof(float) * 7 * WCAND * K1_WARPS;
+    return QBOX_OFF + 2 * sizeof(float4) * K1_TQ + sizeof(uint16_t) * K1_TQ * K1_WARPS;
 }
 
 static void k1f_set_attrs() {

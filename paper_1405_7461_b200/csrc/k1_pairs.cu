@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
 #pragma unroll
             for (int k = 0; k < K1_CPT; ++k) {
                 const int64_t e = wbase + (int64_t)k * 32 + lane;
-                const bool valid = e <= it.c_hi;
+                const bool valid = e >= it.c_lo && e <= it.c_hi;
                 if (valid) {
                     r[k].ts = L.e.ts[e]; r[k].te = L.e.te[e];
                     r[k].sx = L.e.sx[e]; r[k].sy = L.e.sy[e]; r[k].sz = L.e.sz[e];
@@ -255,8 +255,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
             wmin_te = warp_min(wmin_te);
             wmax_ts = warp_max(wmax_ts);
             if (lane == 0) {
-                k1_wctx[warp].key_base0 = make_key(L, it.b, wbase - L.plan.first[it.b], it.q0);
-                k1_wctx[warp].key_base1 = 0;  // no shared units in this kernel
+                set_key_bases(L, it, wbase, warp);  // (no shared units in this kernel: b1 < 0)
                 k1_wctx[warp].js = it.nt;
                 k1_wctx[warp].wbase = wbase;
                 const int64_t nv = it.c_hi - wbase + 1;
@@ -265,7 +264,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
                 k1_wctx[warp].wmax = wmax;
             }
             __syncwarp();
-            const int4 w = warp_window(sq, pm, it.nt, *L.q_unsorted != 0, wmin, wmax, wmax_ts, lane);
+            const int4 w = warp_window(sq, pm, it.nt, (*L.q_unsorted & 1) != 0, wmin, wmax, wmax_ts, lane);
             if (L.overlaps_only) {
                 double ts[K1_CPT], te[K1_CPT];
 #pragma unroll

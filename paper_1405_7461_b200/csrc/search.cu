@@ -22,7 +22,9 @@
 #include <unistd.h>
 #include <algorithm>
 #include <mutex>
+#include <vector>
 
+#include "hostpool.h"
 #include "tsk_internal.cuh"
 
 namespace tsk {
@@ -168,6 +170,30 @@ __global__ void k_gather(GatherArgs a) {
     }
 }
 
+// K4, compact form: per sorted hit row the start-sorted entry ordinal and the
+// query ordinal (u32 each) and the interval, 24 B instead of 48; the host
+// expands the four id columns from the ordinals (search.cu: compact_rows).
+__global__ void k_compact(int64_t r0, int64_t r1, const uint64_t *__restrict__ keys, const uint32_t *__restrict__ perm,
+                          const double *__restrict__ tb_in, const double *__restrict__ te_in,
+                          const int64_t *__restrict__ lo, const int64_t *__restrict__ first, int major_bits,
+                          int minor_bits, double *__restrict__ o_tb, double *__restrict__ o_te,
+                          uint32_t *__restrict__ o_eo, uint32_t *__restrict__ o_qo) {
+    const uint64_t mmask = major_bits ? ((~0ull) >> (64 - major_bits)) : 0ull;
+    const uint64_t nmask = minor_bits ? ((~0ull) >> (64 - minor_bits)) : 0ull;
+    for (int64_t i = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r1;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = keys[i];
+        const int64_t b = (int64_t)(major_bits + minor_bits < 64 ? (k >> (major_bits + minor_bits)) : 0);
+        const int64_t e = first[b] + (int64_t)((k >> minor_bits) & mmask);
+        const int64_t q = lo[b] + (int64_t)(k & nmask);
+        const int64_t j = perm ? (int64_t)perm[i] : i;
+        o_eo[i] = (uint32_t)e;
+        o_qo[i] = (uint32_t)q;
+        o_tb[i] = tb_in[j];
+        o_te[i] = te_in[j];
+    }
+}
+
 __global__ void k_iota(int64_t n, uint32_t *v) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -250,6 +276,91 @@ static int sm_count(int device) {
     int n = 0;
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
     return n > 0 ? n : 148;
+}
+
+// Results of at least this many rows take the compact path (below it the
+// 48-byte device gather and one copy are cheaper than the pipeline).
+static const int64_t kCompactMin = int64_t(1) << 18;
+static const int64_t kCompactChunk = int64_t(1) << 21;  // rows per pipeline chunk
+
+// Compact result assembly, pipelined: for each chunk of sorted rows K4 writes
+// (t_begin, t_end, entry ordinal, query ordinal) on the db stream; a copy
+// stream moves t_begin/t_end straight into the result's pinned columns and
+// the ordinals into a pinned staging block (24 B/row over PCIe instead of
+// 48); host threads expand the four id columns of chunk c from the host id
+// columns while chunk c+1 is in flight.  Result bytes are identical to the
+// device gather's.
+static void compact_rows(tsk_db *db, tsk_result *res, const tsk_columns *qc, int64_t nh, const uint64_t *keys,
+                         const uint32_t *perm, const double *tbin, const double *tein, const int64_t *d_lo,
+                         const int64_t *d_first, int major_bits, int minor_bits, cudaStream_t st,
+                         int64_t &launches) {
+    const size_t cb = (size_t)nh * 8;
+    db->out_cols.reserve((size_t)nh * 24 + 64, st);
+    double *d_tb = db->out_cols.as<double>();
+    double *d_te = d_tb + nh;
+    uint32_t *d_eo = reinterpret_cast<uint32_t *>(d_te + nh);
+    uint32_t *d_qo = d_eo + nh;
+    size_t got = 0;
+    res->host = pin_alloc(cb * 6, &got);
+    res->host_bytes = got;
+    char *hb = static_cast<char *>(res->host);
+    res->qtraj = (int64_t *)(hb + 0 * cb);
+    res->qseg = (int64_t *)(hb + 1 * cb);
+    res->etraj = (int64_t *)(hb + 2 * cb);
+    res->eseg = (int64_t *)(hb + 3 * cb);
+    res->tbeg = (double *)(hb + 4 * cb);
+    res->tend = (double *)(hb + 5 * cb);
+    size_t ogot = 0;
+    uint32_t *h_ord = static_cast<uint32_t *>(pin_alloc((size_t)nh * 8, &ogot));
+    uint32_t *h_eo = h_ord, *h_qo = h_ord + nh;
+    if (!db->stream2) TSK_CUDA(cudaStreamCreateWithFlags(&db->stream2, cudaStreamNonBlocking));
+    cudaStream_t st2 = db->stream2;
+    int64_t chunk = kCompactChunk;
+    if (const char *e = getenv("TSK_COMPACT_CHUNK")) chunk = std::max<int64_t>(1, atoll(e));  // testing
+    const int64_t nc = (nh + chunk - 1) / chunk;
+    std::vector<cudaEvent_t> evg((size_t)nc), evd((size_t)nc);
+    for (int64_t c = 0; c < nc; ++c) {
+        TSK_CUDA(cudaEventCreateWithFlags(&evg[c], cudaEventDisableTiming));
+        TSK_CUDA(cudaEventCreateWithFlags(&evd[c], cudaEventDisableTiming | cudaEventBlockingSync));
+    }
+    for (int64_t c = 0; c < nc; ++c) {
+        const int64_t r0 = c * chunk, r1 = std::min<int64_t>(nh, r0 + chunk), m = r1 - r0;
+        const int grid = (int)std::min<int64_t>((m + 255) / 256, 148 * 8);
+        k_compact<<<grid, 256, 0, st>>>(r0, r1, keys, perm, tbin, tein, d_lo, d_first, major_bits, minor_bits, d_tb,
+                                        d_te, d_eo, d_qo);
+        TSK_CUDA(cudaGetLastError());
+        ++launches;
+        TSK_CUDA(cudaEventRecord(evg[c], st));
+        TSK_CUDA(cudaStreamWaitEvent(st2, evg[c], 0));
+        TSK_CUDA(cudaMemcpyAsync(res->tbeg + r0, d_tb + r0, (size_t)m * 8, cudaMemcpyDeviceToHost, st2));
+        TSK_CUDA(cudaMemcpyAsync(res->tend + r0, d_te + r0, (size_t)m * 8, cudaMemcpyDeviceToHost, st2));
+        TSK_CUDA(cudaMemcpyAsync(h_eo + r0, d_eo + r0, (size_t)m * 4, cudaMemcpyDeviceToHost, st2));
+        TSK_CUDA(cudaMemcpyAsync(h_qo + r0, d_qo + r0, (size_t)m * 4, cudaMemcpyDeviceToHost, st2));
+        TSK_CUDA(cudaEventRecord(evd[c], st2));
+    }
+    // the db stream waits for the copies (the caller's end event covers them)
+    TSK_CUDA(cudaStreamWaitEvent(st, evd[nc - 1], 0));
+    const int64_t *qt = qc->traj, *qs = qc->seg, *et = db->host_etraj, *es = db->host_eseg;
+    HostPool &pool = HostPool::get();
+    for (int64_t c = 0; c < nc; ++c) {
+        const int64_t r0 = c * chunk, r1 = std::min<int64_t>(nh, r0 + chunk);
+        TSK_CUDA(cudaEventSynchronize(evd[c]));
+        pool.run([&](int part, int parts) {
+            const int64_t a = r0 + (r1 - r0) * part / parts, z = r0 + (r1 - r0) * (part + 1) / parts;
+            for (int64_t i = a; i < z; ++i) {
+                const uint32_t q = h_qo[i], e = h_eo[i];
+                res->qtraj[i] = qt[q];
+                res->qseg[i] = qs[q];
+                res->etraj[i] = et[e];
+                res->eseg[i] = es[e];
+            }
+        });
+    }
+    for (int64_t c = 0; c < nc; ++c) {
+        cudaEventDestroy(evg[c]);
+        cudaEventDestroy(evd[c]);
+    }
+    pin_free(h_ord, ogot);
 }
 
 static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int64_t *b_lo,
@@ -335,7 +446,15 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
         if (!strcmp(e, "off")) pair = 0;
         else if (!strcmp(e, "force") && pair) pair = 2;
     }
-    launch_plan_items(plan, slots, K1_THREADS * k1_candidates_per_thread(k1_f32), pair, st);
+    // indexed searches read K1's spatially ordered copy of the store (its
+    // candidate ranges are unions of whole bins, so the same ordinal ranges)
+    // and cull (query, warp) pairs by box; spans given by the caller are
+    // arbitrary and use the start-sorted store.  TSK_SPATIAL=nocull keeps the
+    // layout without the cull (testing).
+    const char *sp_env = getenv("TSK_SPATIAL");
+    const bool use_k = !spans_given && db->k.built;
+    const int cull = (use_k && !(sp_env && !strcmp(sp_env, "nocull"))) ? 1 : 0;
+    launch_plan_items(plan, slots, K1_THREADS * k1_candidates_per_thread(k1_f32), pair, cull ? BOX_GROUP : 1, st);
     launches += spans_given ? 1 : 2;
     tr.mark("ranges+items");
 
@@ -347,7 +466,17 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
         cap = db->recs.bytes / 24;
     }
     K1Launch L;
-    L.e = db->s;
+    L.e = use_k ? db->k.s : db->s;
+    L.orig = use_k ? db->k.orig : nullptr;
+    L.gbox = use_k ? db->k.box : nullptr;
+    L.gtime = use_k ? db->k.gtime : nullptr;
+    L.cull = cull;
+    // overlap counts outside K1 (count_overlaps_ext) when the store's end
+    // times are sorted too; the kernel itself checks the query flags
+    L.ext_count = (L.cull && k1_f32 && db->s.te_sorted && !(flags & (TSK_OVERLAPS_ONLY | TSK_NOOP)) &&
+                   !(sp_env && !strcmp(sp_env, "noext")))
+                      ? 1
+                      : 0;
     L.q = db->q_rec.as<QRec>();
     L.plan = plan;
     L.item_counter = d_ctr;
@@ -377,6 +506,10 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
         L.tend = L.tbeg + cap;
         TSK_CUDA(cudaMemsetAsync(d_ctr, 0, 24, st));
         TSK_CUDA(cudaMemsetAsync(d_ovl, 0, nbz * 16, st));
+        if (L.ext_count) {
+            launch_count_overlaps_ext(plan, db->q, db->s, L.q_unsorted, L.q_cmax_bits, L.db_cmax, L.d2, st);
+            ++launches;
+        }
         TSK_CUDA(cudaEventRecord(db->ev_k0, st));
         launch_k1(L, slots, st);
         ++launches;
@@ -464,6 +597,28 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
             }
             keys = ko;
             perm = v1;
+        }
+        // compact rows + host expansion of the ids, pipelined in chunks over
+        // a second stream (large reference-ordered results of indexed and
+        // span searches; the caller registered the store's host id columns)
+        const char *cpenv = getenv("TSK_COMPACT");
+        const bool compact = !on_device && !canonical && !want_ord && ordered && !query_major &&
+                             db->host_etraj && db->host_eseg && qc->traj && qc->seg && n <= 0xffffffffll &&
+                             nq <= 0xffffffffll &&
+                             (cpenv ? strcmp(cpenv, "off") != 0 : nh >= kCompactMin) &&
+                             !(cpenv && !strcmp(cpenv, "off"));
+        if (compact) {
+            tr.mark("sort");
+            compact_rows(db, res, qc, nh, keys, perm, tbin, tein, d_lo, d_first, major_bits, minor_bits, st,
+                         launches);
+            tr.mark("d2h");
+            TSK_CUDA(cudaEventRecord(db->ev1, st));
+            TSK_CUDA(cudaStreamSynchronize(st));
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, db->ev0, db->ev1);
+            res->device_ms = ms;
+            res->launches = launches;
+            return res;
         }
         db->out_cols.reserve(cb * ncols, st);
         char *ob = db->out_cols.as<char>();
@@ -572,6 +727,14 @@ extern "C" int tsk_pair_intervals(int device, const tsk_columns *rows, const tsk
         if (db) tsk_db_free(db);
         return fail(e.code, e.msg);
     }
+}
+
+extern "C" int tsk_db_set_host_ids(tsk_db *db, const int64_t *traj, const int64_t *seg) {
+    if (!db) return fail(TSK_EINVAL, "null db");
+    if ((traj == nullptr) != (seg == nullptr)) return fail(TSK_EINVAL, "traj and seg go together");
+    db->host_etraj = traj;
+    db->host_eseg = seg;
+    return TSK_OK;
 }
 
 extern "C" int tsk_result_info(const tsk_result *r, int64_t *n_hits, int64_t *nb, double *device_ms) {

@@ -82,7 +82,8 @@ struct Soa {
     float *sr32 = nullptr;  // FP32 pre-filter speed bound (filter.cuh f32_speed)
     uint8_t *unsafe = nullptr;
     int any_unsafe = 0;
-    int sorted = 1;  // ts non-decreasing
+    int sorted = 1;     // ts non-decreasing
+    int te_sorted = 1;  // te non-decreasing too (external overlap counts, count_overlaps_ext)
     DBuf storage;
 };
 
@@ -100,6 +101,27 @@ struct __align__(16) QRec {
     double ez, flag;  // flag: 1.0 when the segment is unsafe (seg_unsafe)
 };
 static_assert(sizeof(QRec) == 128, "QRec layout");
+
+// K1's copy of an indexed store: the same columns, reordered inside each
+// index bin by the Morton code of the segment midpoints (alternating
+// direction bin by bin), so that 128 consecutive entries — one warp's
+// candidates — lie close together in space as well as in time.  A batch's
+// candidate range is a union of whole bins (index.py:160-173), so it is the
+// same contiguous ordinal range in both orders; `orig` maps a K1 position
+// back to its start-sorted ordinal (hit keys, and so the reference's item
+// order, use that).  `box` holds per BOX_GROUP entries the bounding box of
+// their segments, rounded outward to FP32 (lo.xyz, hi.xyz): K1 skips every
+// (query, warp) pair whose boxes are farther apart than the threshold.
+constexpr int BOX_GROUP = 128;
+struct K1Layout {
+    Soa s;
+    int64_t *orig = nullptr;
+    float4 *box = nullptr;  // 2 per group: (lo.x, lo.y, lo.z, 0), (hi.x, hi.y, hi.z, 0)
+    double2 *gtime = nullptr;  // per group: (min ts, max te)
+    int64_t ngroups = 0;
+    DBuf aux;
+    bool built = false;
+};
 
 struct Index {
     int64_t m = 0, n_ne = 0;
@@ -120,10 +142,15 @@ struct tsk_db {
     tsk::Soa s;
     double cmax = 0;  // max |coordinate| of the entry store
     tsk::Index ix;
+    tsk::K1Layout k;  // spatially ordered copy for K1 (built with the index)
     // search workspace (grow-only)
     tsk::DBuf q_rec, batches, counters, recs, sorted, cub_tmp, out_cols, canon_cols, canon_tmp;
     tsk::Soa q;  // device copy of the current query set
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_k0 = nullptr, ev_k1 = nullptr;
+    cudaStream_t stream2 = nullptr;  // result copies of the compact pipeline
+    // caller-owned host copies of the entry id columns (tsk_db_set_host_ids):
+    // the compact result path expands ids from ordinals on the host
+    const int64_t *host_etraj = nullptr, *host_eseg = nullptr;
 };
 
 struct tsk_result {
@@ -178,6 +205,15 @@ __device__ __forceinline__ double np_floor_divide(double a, double b) {
         fl = copysign(0.0, __ddiv_rn(a, b));
     }
     return fl;
+}
+
+// bin of a start time: min(floor_divide(ts - t0, width), m - 1) (index.py:108-112)
+__device__ __forceinline__ int64_t bin_of(double t, double t0, double width, int64_t m) {
+    if (!(width > 0.0)) return 0;
+    double f = np_floor_divide(__dsub_rn(t, t0), width);
+    double mm = (double)(m - 1);
+    f = f < mm ? f : mm;  // np.minimum(float, m - 1)
+    return (int64_t)f;
 }
 
 // ── host-side launchers (defined in the .cu files) ─────────────────────────
@@ -289,10 +325,20 @@ struct K1Launch {
     int noop;
     int overlaps_only;  // count temporal overlaps only (no geometry, no hits)
     const int *q_unsorted;  // device flag: query start times not sorted -> no windows
+    // K1 layout (K1Layout): e is then k.s; orig maps positions to start-sorted
+    // ordinals (nullptr: identity); gbox/cull enable the box cull
+    const int64_t *orig;
+    const float4 *gbox;
+    const double2 *gtime;
+    int cull;
+    // overlap counts come from count_overlaps_ext (store te sorted; used
+    // when the query flags say ts and te are both sorted): K1's box-cull
+    // fast path then skips whole warps and counts no overlaps itself
+    int ext_count;
 };
 
 void launch_ranges(tsk_db *db, const Soa &q, SearchPlanDev &p, bool spans_given, cudaStream_t st);
-void launch_plan_items(SearchPlanDev &p, int slots, int stride, int pair, cudaStream_t st);
+void launch_plan_items(SearchPlanDev &p, int slots, int stride, int pair, int align, cudaStream_t st);
 void launch_qprep(const Soa &q, QRec *out, int *flags, unsigned long long *cmax_bits, cudaStream_t st);
 bool mapped_columns(const tsk_columns *c, tsk_columns *dev);
 void launch_qprep_mapped(const tsk_columns &dev_cols, Soa &q, QRec *out, int *flags, unsigned long long *cmax_bits,
@@ -300,6 +346,10 @@ void launch_qprep_mapped(const tsk_columns &dev_cols, Soa &q, QRec *out, int *fl
 double soa_cmax(const Soa &s, cudaStream_t st);
 void soa_group_bounds(Soa &s, cudaStream_t st);  // GBound per GB_SIZE segments
 void launch_k1(const K1Launch &L, int grid, cudaStream_t st);
+void build_k1_layout(tsk_db *db, cudaStream_t st);  // layout.cu
+void launch_count_overlaps_ext(const SearchPlanDev &p, const Soa &q, const Soa &s, const int *q_flags,
+                               const unsigned long long *q_cmax_bits, double db_cmax, double d2, cudaStream_t st);
+void free_k1_layout(tsk_db *db);
 void canonical_perm(int64_t n, const int64_t *qt, const int64_t *qs, const int64_t *et,
                     const int64_t *es, const double *tb, const double *te, uint32_t *perm,
                     DBuf &scratch, cudaStream_t st);

@@ -9,7 +9,10 @@ non-negative reference discriminant is flagged by the FP64 filter in every
 clip case K1 can route it through, and that every reference hit is flagged
 by the FP32 pre-filter (with the item origin at the query and at a shifted
 point), also in K1's lane form (one threshold from the largest of four speed
-bounds, a NaN-propagating min of four norms, then the candidate's own compare).  Mutated margins must produce misses, so the generator is known to
+bounds, a NaN-propagating min of four norms, then the candidate's own compare), and
+that no reference hit is removed by the box cull of the K1 layout (segment
+boxes rounded outward to FP32, box_gap2 vs box_cull_r2).  Mutated margins of
+the two filters must produce misses, so the generator is known to
 reach both bounds.
 """
 
@@ -54,6 +57,7 @@ def test_filter_flags_every_nonnegative_reference_discriminant(tmp_path):
     assert out["edge"]["disc_pos"] > 100_000 and out["edge"]["skipped"] == 0
     # FP32 pre-filter: every reference hit is flagged
     assert out["edge"]["f32_misses"] == 0 and out["random"]["f32_misses"] == 0
+    assert out["edge"]["box_checks"] > 0  # the box cull's checks count into f32_misses
     assert out["edge"]["hits"] > 100_000 and out["edge"]["f32_checks"] > 1_000_000
 
 

@@ -791,3 +791,57 @@ def test_concurrent_run_search_on_one_store_is_safe():
         for k in RES:
             assert np.array_equal(getattr(gr, k), getattr(wr, k)), k
         assert ws.hits == gs.hits and ws.temporal_misses == gs.temporal_misses
+
+
+@pytest.mark.parametrize("mode", ["fast", "noext", "nocull"])
+def test_k1_layout_paths_equal_oracle(mode, monkeypatch):
+    """The K1 layout's three paths (box-cull fast path with overlaps counted
+    outside K1, box cull with K1's own counts, layout without the cull) give
+    the oracle's items, order and statistics — on a store whose end times
+    are sorted (unit steps) with queries whose end times are not, and with
+    queries whose end times are."""
+    if mode != "fast":
+        monkeypatch.setenv("TSK_SPATIAL", mode)
+    store = tsk.generate(tsk.make_profile("uniform", 400, seed=11, timesteps=60))
+    pool = tsk.generate(tsk.make_profile("uniform", 200, seed=12, timesteps=60))
+    q_sorted = tsk.sample_queries(pool, 30, seed=13)
+    rng = np.random.default_rng(5)
+    qa = random_store_arrays(rng, 900, first_traj=10**6)
+    for k in ("ts", "te"):
+        qa[k] = qa[k] * 8.0  # spread over the store's time range, random durations
+    q_mixed = _store(qa)
+    ix = tsk.build_index(store, 400)
+    oix = orc.index_build(_cols(store), 400)
+    for q in (q_sorted, q_mixed):
+        plan = tsk.periodic(q, 40, ix)
+        res, st = tsk.run_search(store, ix, plan, 3.0)
+        oplan = [(b.lo, b.hi, None, None, None, None) for b in plan.batches]
+        want, wst = orc.search(_cols(store), oix, _cols(q), oplan, 3.0, workers=1)
+        _same(res, want)
+        assert [st.interactions_computed, st.temporal_misses, st.spatial_misses, st.hits] == \
+            [wst["interactions"], wst["temporal_misses"], wst["spatial_misses"], wst["hits"]]
+        assert [t.hits for t in st.per_batch] == [p[4] for p in wst["per_batch"]]
+
+
+@pytest.mark.parametrize("chunk", ["1000", "77777"])
+def test_compact_result_path_equals_device_gather(chunk, monkeypatch):
+    """The compact result path (24-byte rows, ids expanded on host threads,
+    chunks pipelined over a copy stream) returns the device gather's result
+    byte for byte: run_search and execute_batch, several chunk sizes."""
+    rng = np.random.default_rng(31)
+    store = _store(random_store_arrays(rng, 4000))
+    q = _store(random_store_arrays(rng, 600, first_traj=10**6))
+    ix = tsk.build_index(store, 40)
+    plan = tsk.periodic(q, 64, ix)
+    monkeypatch.setenv("TSK_COMPACT", "off")
+    want, wst = tsk.run_search(store, ix, plan, 4.0)
+    wb, _ = tsk.execute_batch(store, q, (200, 3100), 6.0)
+    monkeypatch.setenv("TSK_COMPACT", "force")
+    monkeypatch.setenv("TSK_COMPACT_CHUNK", chunk)
+    got, st = tsk.run_search(store, ix, plan, 4.0)
+    gb, _ = tsk.execute_batch(store, q, (200, 3100), 6.0)
+    assert len(got) == len(want) > 5000 and len(gb) == len(wb) > 5000
+    for k in RES:
+        assert np.array_equal(getattr(got, k), getattr(want, k)), k
+        assert np.array_equal(getattr(gb, k), getattr(wb, k)), k
+    assert st.hits == wst.hits and st.temporal_misses == wst.temporal_misses

@@ -90,7 +90,7 @@ static bool hoist(const Seg &g, double &ext, double v[3], double dd[3]) {
 
 struct Counts {
     long pairs = 0, overlapping = 0, disc_pos = 0, checks = 0, flagged = 0, misses = 0, skipped = 0;
-    long hits = 0, f32_checks = 0, f32_flagged = 0, f32_misses = 0, f32_skipped = 0;
+    long hits = 0, f32_checks = 0, f32_flagged = 0, f32_misses = 0, f32_skipped = 0, box_checks = 0;
 };
 
 // the reference's hit decision for an overlapping pair (core.py:523-551)
@@ -168,6 +168,24 @@ static void check_f32(const Seg &r, const Seg &c, double d, const double O[3], d
         if (n.f32_misses <= 5) std::fprintf(stderr, "F32 LANE MISS %s\n", tag);
     }
     const bool need = ref_hit(r, c, d);
+    // the box cull (K1 layout): segment boxes rounded outward to FP32
+    {
+        float bl[2][3], bh[2][3];
+        const Seg *sg[2] = {&r, &c};
+        for (int k = 0; k < 2; ++k)
+            for (int i = 0; i < 3; ++i) {
+                bl[k][i] = tsk_f2f_rd(std::fmin(sg[k]->s[i], sg[k]->e[i]));
+                bh[k][i] = tsk_f2f_ru(std::fmax(sg[k]->s[i], sg[k]->e[i]));
+            }
+        const float g2 = box_gap2(bl[0][0], bl[0][1], bl[0][2], bh[0][0], bh[0][1], bh[0][2], bl[1][0], bl[1][1],
+                                  bl[1][2], bh[1][0], bh[1][1], bh[1][2]);
+        const bool pass = !(g2 > box_cull_r2(std::sqrt(d * d), cmax));
+        ++n.box_checks;
+        if (need && !pass) {
+            ++n.f32_misses;
+            if (n.f32_misses <= 5) std::fprintf(stderr, "BOX MISS %s d=%.17g\n", tag, d);
+        }
+    }
     ++n.f32_checks;
     n.hits += need;
     n.f32_flagged += f;
@@ -369,12 +387,12 @@ int main(int argc, char **argv) {
     }
     std::printf("{\"edge\": {\"pairs\": %ld, \"overlapping\": %ld, \"disc_pos\": %ld, \"checks\": %ld, "
                 "\"flagged\": %ld, \"skipped\": %ld, \"misses\": %ld, \"hits\": %ld, \"f32_checks\": %ld, "
-                "\"f32_flagged\": %ld, \"f32_skipped\": %ld, \"f32_misses\": %ld}, "
+                "\"f32_flagged\": %ld, \"f32_skipped\": %ld, \"f32_misses\": %ld, \"box_checks\": %ld}, "
                 "\"random\": {\"pairs\": %ld, \"overlapping\": %ld, \"disc_pos\": %ld, \"checks\": %ld, "
                 "\"flagged\": %ld, \"misses\": %ld, \"hits\": %ld, \"f32_checks\": %ld, \"f32_flagged\": %ld, "
                 "\"f32_misses\": %ld}}\n",
                 n.pairs, n.overlapping, n.disc_pos, n.checks, n.flagged, n.skipped, n.misses, n.hits,
-                n.f32_checks, n.f32_flagged, n.f32_skipped, n.f32_misses, nrand.pairs, nrand.overlapping,
+                n.f32_checks, n.f32_flagged, n.f32_skipped, n.f32_misses, n.box_checks, nrand.pairs, nrand.overlapping,
                 nrand.disc_pos, nrand.checks, nrand.flagged, nrand.misses, nrand.hits, nrand.f32_checks,
                 nrand.f32_flagged, nrand.f32_misses);
     return (n.misses || nrand.misses || n.f32_misses || nrand.f32_misses) ? 1 : 0;
