@@ -303,18 +303,58 @@ TSK_HD float f32_n2(const CandF32 &c, float qts, float qx, float qy, float qz) {
 // ── box cull (K1 layout) ───────────────────────────────────────────────────
 //
 // While both segments of a pair are active each moving point lies on its own
-// segment, so the pair's separation is at least the gap between the two
-// segments' bounding boxes.  A reference hit needs the separation at some
-// instant of the shared span within (1 + 2^-20) d plus the reference's own
-// rounding (2^-38 C, see the FP32 pre-filter below), so a gap above
-//   R = (1 + 2^-8) d + 2^-30 C      (C: max |coordinate| of the launch)
-// proves a miss.  Boxes are rounded outward to FP32 and the gap, its square
-// and sum are rounded down, so the tested value never exceeds the true gap²;
-// R² is rounded up.  tools/filter_check.cpp checks this on the adversarial
-// pairs: no reference hit is ever culled.
-TSK_HD float box_cull_r2(double d, double cmax) {
-    const double r = (1.0 + 0x1p-8) * d + 0x1p-30 * cmax + 0x1p-100;
-    return TSK_F2F_RU(r * r * (1.0 + 0x1p-40));
+// segment, so the pair's separation h(t) is at least the gap G between the
+// two segments' bounding boxes.  A reference hit needs some lambda in [0, 1]
+// with |U + lambda W|^2 <= d^2 + mu (d^2 + (|U| + |W|)^2), mu = 2^-24 (U, W:
+// separation at ta and its change over the span; mu is far above the
+// reference's roundings, see the FP32 pre-filter below), so
+//   G <= h <= (1 + 2^-11) d + 2^-12 (|U| + |W|) + 2^-40 C.
+// The error term grows with |U| + |W|, not with d: long motion crossing the
+// query with a perpendicular offset h below the rounding of |U|^2 is a
+// reference hit at any d (cc = |U|^2 absorbs h^2; tools/filter_check.cpp
+// mode 8).  Both ends of U and U + W lie in the boxes, so |U| + |W| <=
+// 3 (G + D), D = the sum of the two boxes' diagonals, and a hit needs
+//   G <= R = (1 + 2^-8) d + 2^-10 D + 2^-29 C      (C: max |coordinate|).
+// Boxes are rounded outward to FP32; the gap, its square and sum are rounded
+// down, so the tested value never exceeds the true G^2; R and R^2 are rounded
+// up.  tools/filter_check.cpp checks this on the adversarial pairs (no
+// reference hit is ever culled) and that dropping the D term misses.
+//
+// The launch-level part of R: (1 + 2^-8) d + 2^-29 C, rounded up.
+TSK_HD float box_cull_rbase(double d, double cmax) {
+    const double r = (1.0 + 0x1p-8) * d + 0x1p-29 * cmax + 0x1p-100;
+    return TSK_F2F_RU(r * (1.0 + 0x1p-40));
+}
+
+#ifndef __CUDA_ARCH__
+inline float tsk_add_dir(float a, float b, int mode) { return tsk_fma_dir(1.0f, a, b, mode); }
+#endif
+
+// A box's share of R: 2^-10 of its diagonal, rounded up.
+TSK_HD float box_cull_dterm(float lx, float ly, float lz, float hx, float hy, float hz) {
+#ifdef __CUDA_ARCH__
+    const float dx = __fsub_ru(hx, lx), dy = __fsub_ru(hy, ly), dz = __fsub_ru(hz, lz);
+    return __fmul_ru(0x1p-10f, __fsqrt_ru(__fmaf_ru(dz, dz, __fmaf_ru(dy, dy, __fmul_ru(dx, dx)))));
+#else
+    const float dx = tsk_add_dir(hx, -lx, FE_UPWARD), dy = tsk_add_dir(hy, -ly, FE_UPWARD),
+                dz = tsk_add_dir(hz, -lz, FE_UPWARD);
+    const float s = tsk_fma_dir(dz, dz, tsk_fma_dir(dy, dy, tsk_fma_dir(dx, dx, 0.f, FE_UPWARD), FE_UPWARD),
+                                FE_UPWARD);
+    float r = std::sqrt(s);
+    if ((double)r * (double)r < (double)s) r = nextafterf(r, INFINITY);
+    return tsk_fma_dir(0x1p-10f, r, 0.f, FE_UPWARD);
+#endif
+}
+
+// R^2 of one (candidate box, query box) test, rounded up.
+TSK_HD float box_cull_r2(float rbase, float dterm_a, float dterm_b) {
+#ifdef __CUDA_ARCH__
+    const float R = __fadd_ru(__fadd_ru(rbase, dterm_a), dterm_b);
+    return __fmul_ru(R, R);
+#else
+    const float R = tsk_add_dir(tsk_add_dir(rbase, dterm_a, FE_UPWARD), dterm_b, FE_UPWARD);
+    return tsk_fma_dir(R, R, 0.f, FE_UPWARD);
+#endif
 }
 
 #ifndef __CUDA_ARCH__

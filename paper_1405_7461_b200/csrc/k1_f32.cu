@@ -296,11 +296,13 @@ __device__ __noinline__ uint2 f32_scanl(int k, int ns, uint32_t base, int qn, in
 // against the bounding box of the warp's 128 candidates (the union of the
 // precomputed boxes of the two BOX_GROUPs they span); survivors are listed
 // in f_wlist in window order.  A pair can hit only if its two segments'
-// boxes are within R = (1 + 2^-8) d + 2^-30 C (box_cull_r2): the gap is
-// formed from boxes rounded outward and rounded down itself, so it never
-// exceeds the true gap.  Returns the number of survivors (warp-uniform).
+// boxes are within R = (1 + 2^-8) d + 2^-10 (D_warp + D_query) + 2^-29 C
+// (filter.cuh, box_cull_*; D: box diagonals, the query's share staged in
+// its box's .w): the gap is formed from boxes rounded outward and rounded
+// down itself, so it never exceeds the true gap.  Returns the number of
+// survivors (warp-uniform).
 __device__ __forceinline__ int box_cull(const float4 *__restrict__ gbox, int64_t n, int64_t wbase, int jlo, int jhi,
-                                        float r2, int warp, int lane) {
+                                        float rbase, int warp, int lane) {
     const int64_t g0 = wbase / BOX_GROUP;
     int64_t g1 = (wbase + WCAND - 1) / BOX_GROUP;
     const int64_t glast = (n - 1) / BOX_GROUP;
@@ -311,6 +313,7 @@ __device__ __forceinline__ int box_cull(const float4 *__restrict__ gbox, int64_t
         lo = make_float4(fminf(lo.x, l1.x), fminf(lo.y, l1.y), fminf(lo.z, l1.z), 0.f);
         hi = make_float4(fmaxf(hi.x, h1.x), fmaxf(hi.y, h1.y), fmaxf(hi.z, h1.z), 0.f);
     }
+    const float rw = __fadd_ru(rbase, box_cull_dterm(lo.x, lo.y, lo.z, hi.x, hi.y, hi.z));
     const float4 *qb = f_qbox();
     uint16_t *const wl = f_wlist(warp);
     unsigned lt;
@@ -321,7 +324,9 @@ __device__ __forceinline__ int box_cull(const float4 *__restrict__ gbox, int64_t
         bool pass = false;
         if (j < jhi) {
             const float4 ql = qb[2 * j], qh = qb[2 * j + 1];
-            pass = !(box_gap2(lo.x, lo.y, lo.z, hi.x, hi.y, hi.z, ql.x, ql.y, ql.z, qh.x, qh.y, qh.z) > r2);
+            const float R = __fadd_ru(rw, ql.w);
+            pass = !(box_gap2(lo.x, lo.y, lo.z, hi.x, hi.y, hi.z, ql.x, ql.y, ql.z, qh.x, qh.y, qh.z) >
+                     __fmul_ru(R, R));
         }
         const unsigned m = __ballot_sync(0xffffffffu, pass);
         if (pass) wl[ns + __popc(m & lt)] = (uint16_t)j;
@@ -434,7 +439,7 @@ __device__ __forceinline__ void stage_cands(const K1Launch &L, int64_t wbase, in
 // candidates.
 __device__ __noinline__ void fast_subtile(const K1Launch &L, const ItemCtx &it, const QRec *__restrict__ qt,
                                           const QF32 *__restrict__ sqf, const double *pm, const double *sm,
-                                          int64_t wbase, float cull_r2, const F32Item &fi, bool item_f32, float *wcs,
+                                          int64_t wbase, float cull_rb, const F32Item &fi, bool item_f32, float *wcs,
                                           int warp, int lane, unsigned long long &n_ev, unsigned long long &n_hit) {
     const int64_t g0 = wbase / BOX_GROUP;
     int64_t g1 = (wbase + WCAND - 1 < it.c_hi ? wbase + WCAND - 1 : it.c_hi) / BOX_GROUP;
@@ -452,7 +457,7 @@ __device__ __noinline__ void fast_subtile(const K1Launch &L, const ItemCtx &it, 
     const int jlo = __shfl_sync(0xffffffffu, v, 0);
     int jhi = __shfl_sync(0xffffffffu, v, 1);
     if (jhi < jlo) jhi = jlo;
-    const int ns = box_cull(L.gbox, L.e.n, wbase, jlo, jhi, cull_r2, warp, lane);
+    const int ns = box_cull(L.gbox, L.e.n, wbase, jlo, jhi, cull_rb, warp, lane);
     if (ns == 0) return;
     // survivors: this warp's candidates
     double rts[CPT], rte[CPT];
@@ -531,7 +536,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
     // below 2^60 (and the FP64 filter's window for the exact division)
     const bool launch_ok = k1f_launch_ok(cmax, L.d2);
     const double dthr = sqrt(L.d2);  // d (sqrt(RN(d^2)) >= d (1 - 2^-52); the margin covers it)
-    const float cull_r2 = box_cull_r2(dthr, cmax);  // filter.cuh
+    const float cull_rb = box_cull_rbase(dthr, cmax);  // filter.cuh
     const bool cull = L.cull && launch_ok;
 
     for (;;) {
@@ -626,11 +631,13 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
             f.te64 = q.te;
             sqf[j] = f;
             if (cull) {  // the query segment's box, rounded outward
-                f_qbox()[2 * j] = make_float4(__double2float_rd(fmin(q.sx, q.ex)), __double2float_rd(fmin(q.sy, q.ey)),
-                                              __double2float_rd(fmin(q.sz, q.ez)), 0.f);
-                f_qbox()[2 * j + 1] = make_float4(__double2float_ru(fmax(q.sx, q.ex)),
-                                                  __double2float_ru(fmax(q.sy, q.ey)),
-                                                  __double2float_ru(fmax(q.sz, q.ez)), 0.f);
+                // .w of the low corner: the box's share of the cull radius
+                const float lx = __double2float_rd(fmin(q.sx, q.ex)), ly = __double2float_rd(fmin(q.sy, q.ey)),
+                            lz = __double2float_rd(fmin(q.sz, q.ez));
+                const float hx = __double2float_ru(fmax(q.sx, q.ex)), hy = __double2float_ru(fmax(q.sy, q.ey)),
+                            hz = __double2float_ru(fmax(q.sz, q.ez));
+                f_qbox()[2 * j] = make_float4(lx, ly, lz, box_cull_dterm(lx, ly, lz, hx, hy, hz));
+                f_qbox()[2 * j + 1] = make_float4(hx, hy, hz, 0.f);
             }
         }
         __syncthreads();
@@ -652,7 +659,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
             const int64_t wbase = base + (int64_t)warp * WCAND;
             if (fast) {
                 if (wbase > it.c_hi || L.noop) continue;
-                fast_subtile(L, it, qt, sqf, pm, sm, wbase, cull_r2, fi_sh, item_f32, wcs, warp, lane, n_ev, n_hit);
+                fast_subtile(L, it, qt, sqf, pm, sm, wbase, cull_rb, fi_sh, item_f32, wcs, warp, lane, n_ev, n_hit);
                 continue;
             }
             double rts[CPT], rte[CPT];
@@ -714,7 +721,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
                 if (cull) {
                     // K1 layout: one box test per (query, warp) first; the
                     // candidates are converted only when a query survives
-                    const int ns = box_cull(L.gbox, L.e.n, wbase, jlo, jhi, cull_r2, warp, lane);
+                    const int ns = box_cull(L.gbox, L.e.n, wbase, jlo, jhi, cull_rb, warp, lane);
                     n_ev += (unsigned long long)ns * (unsigned long long)k1_wctx[warp].nvalid;
                     if (ns == 0) continue;
                     stage_cands(L, wbase, it.c_lo, it.c_hi, rts, fi_sh, wcs, lane);

@@ -8,7 +8,9 @@ Pins core.pair_intervals (/root/reference/pkg/src/trajseek/core.py:464-565)
 on meshes whose arithmetic overflows: |coordinates| from 1e150 to 1e300,
 d up to 1e300.  There aa = |w|^2, cc or the discriminant become inf/NaN,
 and the vectorized np.minimum / np.maximum (core.py:545-546) propagate NaN
-roots into a miss (core.py:549-553).  Writes extreme.npz next to this file.
+roots into a miss (core.py:549-553); and on "absorbed offset" pairs, where
+cc = |U|^2 loses a perpendicular offset (tests/helpers.py
+absorbed_offset_pairs).  Writes extreme.npz next to this file.
 """
 
 from __future__ import annotations
@@ -62,6 +64,15 @@ def scenes():
         R, C = rand(16), rand(16)
         for k, d in enumerate(dvals):
             yield f"{tag}_d{k}", store(R), store(C), d
+    # 3. absorbed offsets: long motion across the query with a perpendicular
+    #    offset h below the rounding of |U|^2: the reference's cc loses h^2
+    #    and it reports hits at thresholds far below h (the box cull's radius
+    #    needs its box-diagonal term, filter.cuh)
+    from helpers import absorbed_offset_pairs
+
+    A, B = absorbed_offset_pairs(24, 777)
+    for k, d in enumerate((1e-9, 1e-12, 0.0, 1e-4)):
+        yield f"absorbed_d{k}", store(A), store(B), d
 
 
 def main():

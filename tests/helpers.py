@@ -69,3 +69,34 @@ def c9_population(n, seed):
     A = np.column_stack([coords[:, 0:3], base, coords[:, 3:6], base + span_a])
     B = np.column_stack([coords[:, 6:9], base + off_b, coords[:, 9:12], base + off_b + span_b])
     return A, B
+
+
+def absorbed_offset_pairs(n, seed, scale=1000.0):
+    """(A, B) as (n, 8) arrays of xs ys zs ts xe ye ze te: pair k moves A_k
+    along one axis straight across the stationary (or co-moving) B_k during
+    [4k, 4k + 1], offset perpendicular by h = scale * 2^-(18..37).  Below
+    h ~ 2^-26 |U| the reference's cc = |U|^2 absorbs h^2, so it reports a
+    hit at any threshold d << h (filter.cuh, box cull; tools/filter_check.cpp
+    mode 8)."""
+    rng = np.random.default_rng(seed)
+    A = np.zeros((n, 8))
+    B = np.zeros((n, 8))
+    for k in range(n):
+        ax = int(rng.integers(3))
+        px = (ax + 1 + int(rng.integers(2))) % 3
+        c = rng.uniform(-scale, scale, 3) * (rng.random() < 0.5)
+        h = scale * np.ldexp(rng.uniform(0.5, 1.0), -int(18 + rng.integers(20)))
+        s, e = c.copy(), c.copy()
+        s[ax] += scale * rng.uniform(0.5, 1.0)
+        e[ax] -= scale * rng.uniform(0.5, 1.0)
+        s[px] += h
+        e[px] += h
+        qe = c.copy()
+        if rng.random() < 0.5:  # the query moves along too (offset kept)
+            m = scale * rng.uniform(-1, 1)
+            qe[ax] += m
+            e[ax] += m
+        t0 = 4.0 * k
+        A[k] = [*s, t0, *e, t0 + 1.0]
+        B[k] = [*c, t0, *qe, t0 + 1.0]
+    return A, B

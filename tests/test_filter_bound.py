@@ -13,7 +13,10 @@ bounds, a NaN-propagating min of four norms, then the candidate's own compare), 
 that no reference hit is removed by the box cull of the K1 layout (segment
 boxes rounded outward to FP32, box_gap2 vs box_cull_r2).  Mutated margins of
 the two filters must produce misses, so the generator is known to
-reach both bounds.
+reach both bounds.  Mode 8 builds the "absorbed offset" pairs: long motion
+crossing the query with a perpendicular offset below the rounding of
+|U|^2, which the reference reports as hits at any threshold; the box cull's
+radius needs its box-diagonal term for them.
 """
 
 from __future__ import annotations
@@ -57,7 +60,10 @@ def test_filter_flags_every_nonnegative_reference_discriminant(tmp_path):
     assert out["edge"]["disc_pos"] > 100_000 and out["edge"]["skipped"] == 0
     # FP32 pre-filter: every reference hit is flagged
     assert out["edge"]["f32_misses"] == 0 and out["random"]["f32_misses"] == 0
-    assert out["edge"]["box_checks"] > 0  # the box cull's checks count into f32_misses
+    # box cull: no reference hit is culled, and the radius's diagonal term is
+    # needed (without it the absorbed-offset pairs of mode 8 are culled)
+    assert out["edge"]["box_checks"] > 1_000_000 and out["edge"]["box_misses"] == 0
+    assert out["edge"]["box_mutation_misses"] > 0
     assert out["edge"]["hits"] > 100_000 and out["edge"]["f32_checks"] > 1_000_000
 
 

@@ -340,6 +340,46 @@ def test_planners_and_profiles_vs_oracle_engine(kind, planner):
         (wst["interactions"], wst["temporal_misses"], wst["spatial_misses"], wst["hits"])
 
 
+@pytest.mark.parametrize("d", [1e-9, 0.0, 1e-4, 2.0])
+def test_absorbed_offsets_survive_the_box_cull(d):
+    """Long motion straight across a query with a perpendicular offset below
+    the rounding of |U|^2: the reference reports hits at thresholds far
+    below the offset (tests/golden/extreme.npz, absorbed_*).  An indexed
+    search runs K1's box cull over the spatially ordered layout; its radius
+    needs the box-diagonal term (filter.cuh), else these hits are culled.
+    The whole plan is compared with the oracle engine, stats included."""
+    from helpers import absorbed_offset_pairs
+
+    A, B = absorbed_offset_pairs(300, 4321)
+    rng = np.random.default_rng(99)
+    filler = random_store_arrays(rng, 5000, first_traj=10_000)
+    for k in ("xs", "ys", "zs", "xe", "ye", "ze"):
+        filler[k] = filler[k] * 100.0
+    span = filler["te"] - filler["ts"]
+    filler["ts"] = filler["ts"] * 150.0  # spread over the pairs' [0, 1200)
+    filler["te"] = filler["ts"] + span
+    cols = ["xs", "ys", "zs", "ts", "xe", "ye", "ze", "te"]
+    ent = {k: np.concatenate([A[:, i], filler[k]]) for i, k in enumerate(cols)}
+    ent["traj"] = np.concatenate([np.arange(len(A)), filler["traj"]])
+    ent["seg"] = np.zeros(len(ent["traj"]), np.int64)
+    qry = {k: B[:, i].copy() for i, k in enumerate(cols)}
+    qry["traj"] = np.arange(len(B), dtype=np.int64) + 50_000
+    qry["seg"] = np.zeros(len(B), np.int64)
+    store, q = _store(ent), _store(qry)
+    ix = tsk.build_index(store, 200)
+    plan = tsk.periodic(q, 7, ix)
+    res, st = tsk.run_search(store, ix, plan, d)
+    oix = orc.index_build(_cols(store), 200)
+    oplan = [(b.lo, b.hi, None, None, None, None) for b in plan.batches]
+    want, wst = orc.search(_cols(store), oix, _cols(q), oplan, d, workers=4)
+    _same(res, want)
+    assert (st.interactions_computed, st.temporal_misses, st.spatial_misses, st.hits) == \
+        (wst["interactions"], wst["temporal_misses"], wst["spatial_misses"], wst["hits"])
+    # absorbed hits are present: entry k hits query k with an offset far above d
+    diag = np.sum((res.entry_traj < len(A)) & (res.query_traj - 50_000 == res.entry_traj))
+    assert diag > 50
+
+
 def test_execute_batch_and_noop_pass():
     rng = np.random.default_rng(5)
     store = _store(random_store_arrays(rng, 800))

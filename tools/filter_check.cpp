@@ -91,6 +91,7 @@ static bool hoist(const Seg &g, double &ext, double v[3], double dd[3]) {
 struct Counts {
     long pairs = 0, overlapping = 0, disc_pos = 0, checks = 0, flagged = 0, misses = 0, skipped = 0;
     long hits = 0, f32_checks = 0, f32_flagged = 0, f32_misses = 0, f32_skipped = 0, box_checks = 0;
+    long box_misses = 0, box_mut_misses = 0;
 };
 
 // the reference's hit decision for an overlapping pair (core.py:523-551)
@@ -179,12 +180,17 @@ static void check_f32(const Seg &r, const Seg &c, double d, const double O[3], d
             }
         const float g2 = box_gap2(bl[0][0], bl[0][1], bl[0][2], bh[0][0], bh[0][1], bh[0][2], bl[1][0], bl[1][1],
                                   bl[1][2], bh[1][0], bh[1][1], bh[1][2]);
-        const bool pass = !(g2 > box_cull_r2(std::sqrt(d * d), cmax));
+        const float rb = box_cull_rbase(std::sqrt(d * d), cmax);
+        const float dr = box_cull_dterm(bl[0][0], bl[0][1], bl[0][2], bh[0][0], bh[0][1], bh[0][2]);
+        const float dq = box_cull_dterm(bl[1][0], bl[1][1], bl[1][2], bh[1][0], bh[1][1], bh[1][2]);
+        const bool pass = !(g2 > box_cull_r2(rb, dr, dq));
         ++n.box_checks;
         if (need && !pass) {
-            ++n.f32_misses;
-            if (n.f32_misses <= 5) std::fprintf(stderr, "BOX MISS %s d=%.17g\n", tag, d);
+            ++n.box_misses;
+            if (n.box_misses <= 5) std::fprintf(stderr, "BOX MISS %s d=%.17g\n", tag, d);
         }
+        // mutation: without the diagonal term the cull must miss (mode 8)
+        if (need && g2 > box_cull_r2(rb, 0.f, 0.f)) ++n.box_mut_misses;
     }
     ++n.f32_checks;
     n.hits += need;
@@ -319,7 +325,7 @@ int main(int argc, char **argv) {
         // overlapping spans with random alignment
         const double a0 = T + unif(0, 10), a1 = a0 + unif(0.01, 10);
         double b0 = T + unif(0, 10), b1 = b0 + unif(0.01, 10);
-        const int mode = (int)(next_u64() % 9);
+        const int mode = (int)(next_u64() % 10);
         if (mode == 1) b0 = a0;                         // equal starts (TA_BOTH)
         if (mode == 2) b1 = a1;                         // equal ends
         if (mode == 3) { b0 = a1; b1 = a1 + 1.0; }      // touching: zero-length span
@@ -358,9 +364,31 @@ int main(int argc, char **argv) {
                 r.e[i] = r.s[i] - dir[i] / nrm * speed * (r.te - r.ts);
             }
         }
-        if (mode != 7 && next_u64() % 3 == 0) { r.s[2] = r.e[2] = 0.0; c.s[2] = c.e[2] = 0.0; }  // planar data
+        if (mode == 8) {
+            // absorbed offset: long motion along one axis crossing the
+            // query, a perpendicular offset h below the rounding of |U|^2
+            // (h ~ 2^-26 |U| and less), so the reference's cc = |U|^2
+            // loses it and reports a hit at a separation far above a tiny d
+            const int ax = (int)(next_u64() % 3), px = (ax + 1 + (int)(next_u64() % 2)) % 3;
+            const double h = L * std::ldexp(unif(0.5, 1.0), -(int)(18 + next_u64() % 20));
+            c.ts = r.ts; c.te = r.te;
+            for (int i = 0; i < 3; ++i) {
+                c.s[i] = c.e[i] = unif(-L, L) * (next_u64() % 2);
+                r.s[i] = r.e[i] = c.s[i];
+            }
+            r.s[ax] = c.s[ax] + L * unif(0.5, 1.0);
+            r.e[ax] = c.s[ax] - L * unif(0.5, 1.0);
+            r.s[px] += h; r.e[px] += h;
+            if (next_u64() % 2) {  // the query moves too (same offset kept)
+                const double m = L * unif(-1, 1);
+                c.e[ax] += m; r.e[ax] += m;
+            }
+        }
+        if (mode != 7 && mode != 8 && next_u64() % 3 == 0) { r.s[2] = r.e[2] = 0.0; c.s[2] = c.e[2] = 0.0; }  // planar data
         nrand.pairs++;
         check_pair(r, c, L * 0.01, nrand, "rand");
+        if (mode == 8)  // thresholds far below the offset
+            for (int k = 0; k < 4; ++k) check_pair(r, c, L * std::ldexp(1.0, -(int)(30 + next_u64() % 40)), n, "absorbed");
         // thresholds straddling the pair's own flip point
         const double md = min_dist(r, c);
         if (md > 0 && std::isfinite(md)) {
@@ -387,13 +415,15 @@ int main(int argc, char **argv) {
     }
     std::printf("{\"edge\": {\"pairs\": %ld, \"overlapping\": %ld, \"disc_pos\": %ld, \"checks\": %ld, "
                 "\"flagged\": %ld, \"skipped\": %ld, \"misses\": %ld, \"hits\": %ld, \"f32_checks\": %ld, "
-                "\"f32_flagged\": %ld, \"f32_skipped\": %ld, \"f32_misses\": %ld, \"box_checks\": %ld}, "
+                "\"f32_flagged\": %ld, \"f32_skipped\": %ld, \"f32_misses\": %ld, \"box_checks\": %ld, "
+                "\"box_misses\": %ld, \"box_mutation_misses\": %ld}, "
                 "\"random\": {\"pairs\": %ld, \"overlapping\": %ld, \"disc_pos\": %ld, \"checks\": %ld, "
                 "\"flagged\": %ld, \"misses\": %ld, \"hits\": %ld, \"f32_checks\": %ld, \"f32_flagged\": %ld, "
                 "\"f32_misses\": %ld}}\n",
                 n.pairs, n.overlapping, n.disc_pos, n.checks, n.flagged, n.skipped, n.misses, n.hits,
-                n.f32_checks, n.f32_flagged, n.f32_skipped, n.f32_misses, n.box_checks, nrand.pairs, nrand.overlapping,
+                n.f32_checks, n.f32_flagged, n.f32_skipped, n.f32_misses, n.box_checks, n.box_misses + nrand.box_misses,
+                n.box_mut_misses + nrand.box_mut_misses, nrand.pairs, nrand.overlapping,
                 nrand.disc_pos, nrand.checks, nrand.flagged, nrand.misses, nrand.hits, nrand.f32_checks,
                 nrand.f32_flagged, nrand.f32_misses);
-    return (n.misses || nrand.misses || n.f32_misses || nrand.f32_misses) ? 1 : 0;
+    return (n.misses || nrand.misses || n.f32_misses || nrand.f32_misses || n.box_misses || nrand.box_misses) ? 1 : 0;
 }
