@@ -186,6 +186,11 @@ int tsk_probe_fp64(int device, double *dadd_per_s, double *dmul_per_s, double *d
 /* Measured FP32 FFMA rate of `device` (ops/s, an FFMA counted as one op) —
  * the issue roofline of K1's FP32 pre-filter. */
 int tsk_probe_fp32(int device, double *ffma_per_s);
+/* K1 development counters of `device` (up to 8: box-cull sub-tiles, box
+ * tests, box survivors, sub-tiles with survivors, pre-filter flags,
+ * separating-axis survivors, exact-path flushes, items); all zero unless
+ * the library was built with -DTSK_K1_STATS.  reset != 0 zeroes them. */
+int tsk_k1_stats(int device, unsigned long long *out, int n, int reset);
 
 #ifdef __cplusplus
 }

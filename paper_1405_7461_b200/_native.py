@@ -66,6 +66,7 @@ SIGNATURES = {
     "tsk_result_free": ([_P], None),
     "tsk_probe_fp64": ([ctypes.c_int, _PD, _PD, _PD], ctypes.c_int),
     "tsk_probe_fp32": ([ctypes.c_int, _PD], ctypes.c_int),
+    "tsk_k1_stats": ([ctypes.c_int, ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int, ctypes.c_int], ctypes.c_int),
     "tsk_db_replicate": ([_P, ctypes.c_int, ctypes.POINTER(_P)], ctypes.c_int),
     "tsk_result_k1_evals": ([_P, _PI64], ctypes.c_int),
     "tsk_plan_setsplit": ([_I64, _PD, _PD, _I64, _PD, _PD, _PI64, _PI64, ctypes.c_int, _I64, _I64,
@@ -343,6 +344,19 @@ def probe_fp32(device: int | None = None) -> float:
     dev = current_device() if device is None else int(device)
     check(lib.tsk_probe_fp32(dev, ctypes.byref(f)))
     return f.value
+
+
+K1_STAT_NAMES = ("subtiles", "box_tests", "box_survivors", "subtiles_with_survivors", "prefilter_flags",
+                 "sep_survivors", "exact_flushes", "items")
+
+
+def k1_stats(device: int | None = None, reset: bool = False) -> dict:
+    """K1's development counters (all zero unless built with -DTSK_K1_STATS)."""
+    lib = load()
+    out = (ctypes.c_ulonglong * 8)()
+    dev = current_device() if device is None else int(device)
+    check(lib.tsk_k1_stats(dev, out, 8, 1 if reset else 0))
+    return dict(zip(K1_STAT_NAMES, (int(v) for v in out)))
 
 
 class _Pinned:

@@ -196,6 +196,7 @@ struct CandF32 {
 struct F32Item {
     double ox, oy, oz, t0, delta;
     bool ok;
+    float sep_rb;  // the separating-axis stage's per-item radius (f32_sep_rbase; set by K1)
 };
 
 #ifndef __CUDA_ARCH__
@@ -222,6 +223,7 @@ TSK_HD F32Item f32_item(double ox, double oy, double oz, double t0, double ar, d
     const double M = ar + tvr + tq * vr + aq;
     it.ok = M <= 0x1p60 && vr <= 0x1p60 && eq <= 0x1p60;  // false for NaN
     it.delta = 0x1p-18 * M + 0x1p-38 * cmax + 0x1p-100;
+    it.sep_rb = INFINITY;  // no separating-axis rejections until K1 sets it
     return it;
 }
 
@@ -447,6 +449,106 @@ TSK_HD float f32_r2(float qa, float sr, float qb) {
 #else
     const float R = tsk_fma_dir(qa, sr, qb, FE_UPWARD);
     return tsk_fma_dir(R, R, 0.f, FE_UPWARD);
+#endif
+}
+
+// ── FP32 separating-axis test (second stage of the pre-filter) ───────────
+//
+// The pre-filter's triangle bound flags every pair whose candidate line
+// passes within ext_q |V_r| + |q.e - q.s| + d of the query's start; with
+// segments much longer than d most flagged pairs are misses.  Before a
+// flagged pair reaches the exact path this test follows both motions over
+// the query's whole span [q.ts, q.te] (a superset of the shared span; the
+// candidate's line is extended): the relative position runs along the
+// segment from D(q.ts) = u to D(q.te) = e, with
+//   u = (p + ts v) - s      (the pre-filter's own u, same operations)
+//   e = (p + te v) - e_q    (te = RN32(q.te - T0), e_q = RN32(q.e - O)).
+// For any direction n, n . D(t) >= min(n . u, n . e) on the segment (it is
+// linear in t), so min(n . u, n . e) > R |n| proves |D(t)| > R throughout.
+// n = u + lambda w (w = e - u, lambda ~ the closest point, any value is
+// valid) makes the test tight.
+//
+// Why R suffices.  A reference hit needs some instant of the shared span
+// with separation h <= (1 + 2^-11) d + 2^-12 (|U| + |W|) + 2^-40 C (the
+// mu = 2^-24 statement of the box cull), and |U| + |W| <= 3 max(|D(q.ts)|,
+// |D(q.te)|) by convexity.  FP32 error: every value formed is, per
+// component, at most M2 = A_r + TV_r + (T_q + E_q) V_r + A_q + D_q
+// (D_q: max |q.e - q.s| component, E_q: max ext_q) and each of p, v, ts,
+// te, s, e_q, the products and sums is rounded once, so u and e are within
+// 2^-19 M2 (Euclidean) of the exact D; the dot products n . u, n . e are
+// within 2^-22 |n| m (m: the larger Euclidean norm of u, e, bounded by
+// 2 max |component|).  Hence with
+//   R = RU((1 + 2^-8) d + 2^-29 C + 2^-14 M2) + 2^-9 max|u_i, e_i|
+// (the first term per item, f32_sep_rbase), nn >= |n| (rounded up) and
+// rhs = RU(R nn), min(n . u, n . e) > rhs proves a reference miss.  NaN
+// anywhere keeps the pair (the compare is false).  Checked by
+// tools/filter_check.cpp on the adversarial pairs (no reference hit is
+// rejected; a mutated, margin-free R does reject hits).
+TSK_HD float f32_sep_rbase(double d, double cmax, double M2) {
+    const double r = (1.0 + 0x1p-8) * d + 0x1p-29 * cmax + 0x1p-14 * M2 + 0x1p-100;
+    return TSK_F2F_RU(r * (1.0 + 0x1p-40));
+}
+
+// FP32 view of a query's end: RN32(q.te - T0), RN32(q.e - O).
+TSK_HD void f32_query_end(double te, double ex, double ey, double ez, const F32Item &it, float out[4]) {
+    out[0] = TSK_F2F_RN(te - it.t0);
+    out[1] = TSK_F2F_RN(ex - it.ox);
+    out[2] = TSK_F2F_RN(ey - it.oy);
+    out[3] = TSK_F2F_RN(ez - it.oz);
+}
+
+#ifndef __CUDA_ARCH__
+inline float tsk_sqrt_ru(float x) {
+    float r = std::sqrt(x);
+    if ((double)r * (double)r < (double)x) r = nextafterf(r, INFINITY);
+    return r;
+}
+#endif
+
+// true = the pair provably cannot hit (false for NaN: the pair is kept).
+TSK_HD bool f32_sep_far(float px, float py, float pz, float vx, float vy, float vz, float qts, float qx,
+                        float qy, float qz, float qte, float qex, float qey, float qez, float rbase,
+                        float mcoef = 0x1p-9f) {
+#ifdef __CUDA_ARCH__
+    const float ux = __fsub_rn(__fmaf_rn(qts, vx, px), qx);
+    const float uy = __fsub_rn(__fmaf_rn(qts, vy, py), qy);
+    const float uz = __fsub_rn(__fmaf_rn(qts, vz, pz), qz);
+    const float ex = __fsub_rn(__fmaf_rn(qte, vx, px), qex);
+    const float ey = __fsub_rn(__fmaf_rn(qte, vy, py), qey);
+    const float ez = __fsub_rn(__fmaf_rn(qte, vz, pz), qez);
+    const float wx = ex - ux, wy = ey - uy, wz = ez - uz;
+    const float ww = __fmaf_rn(wz, wz, __fmaf_rn(wy, wy, wx * wx));
+    const float uw = __fmaf_rn(uz, wz, __fmaf_rn(uy, wy, ux * wx));
+    // any lambda is valid; the closest point's makes the test tight
+    const float lam = ww > 0.f ? fminf(fmaxf(__fdividef(-uw, ww), 0.f), 1.f) : 0.f;
+    const float nx = __fmaf_rn(lam, wx, ux), ny = __fmaf_rn(lam, wy, uy), nz = __fmaf_rn(lam, wz, uz);
+    const float a1 = __fmaf_rn(nz, uz, __fmaf_rn(ny, uy, nx * ux));
+    const float a2 = __fmaf_rn(nz, ez, __fmaf_rn(ny, ey, nx * ex));
+    const float nn = __fsqrt_ru(__fmaf_ru(nz, nz, __fmaf_ru(ny, ny, __fmul_ru(nx, nx))));
+    const float m = fmaxf(fmaxf(fmaxf(fabsf(ux), fabsf(uy)), fmaxf(fabsf(uz), fabsf(ex))),
+                          fmaxf(fabsf(ey), fabsf(ez)));
+    const float rhs = __fmul_ru(__fmaf_ru(m, mcoef, rbase), nn);
+    const float lo = f32_min_nan(a1, a2);
+    unsigned far;
+    asm("{.reg .pred p; setp.gt.f32 p, %1, %2; selp.u32 %0, 1, 0, p;}" : "=r"(far) : "f"(lo), "f"(rhs));
+    return far != 0u;
+#else
+    const float ux = fmaf(qts, vx, px) - qx, uy = fmaf(qts, vy, py) - qy, uz = fmaf(qts, vz, pz) - qz;
+    const float ex = fmaf(qte, vx, px) - qex, ey = fmaf(qte, vy, py) - qey, ez = fmaf(qte, vz, pz) - qez;
+    const float wx = ex - ux, wy = ey - uy, wz = ez - uz;
+    const float ww = fmaf(wz, wz, fmaf(wy, wy, wx * wx));
+    const float uw = fmaf(uz, wz, fmaf(uy, wy, ux * wx));
+    const float lam = ww > 0.f ? std::fmin(std::fmax(-uw / ww, 0.f), 1.f) : 0.f;
+    const float nx = fmaf(lam, wx, ux), ny = fmaf(lam, wy, uy), nz = fmaf(lam, wz, uz);
+    const float a1 = fmaf(nz, uz, fmaf(ny, uy, nx * ux));
+    const float a2 = fmaf(nz, ez, fmaf(ny, ey, nx * ex));
+    const float nn = tsk_sqrt_ru(tsk_fma_dir(nz, nz, tsk_fma_dir(ny, ny, tsk_fma_dir(nx, nx, 0.f, FE_UPWARD),
+                                                               FE_UPWARD), FE_UPWARD));
+    const float m = std::fmax(std::fmax(std::fmax(std::fabs(ux), std::fabs(uy)), std::fmax(std::fabs(uz), std::fabs(ex))),
+                              std::fmax(std::fabs(ey), std::fabs(ez)));
+    const float rhs = tsk_fma_dir(tsk_fma_dir(m, mcoef, rbase, FE_UPWARD), nn, 0.f, FE_UPWARD);
+    const float lo = (a1 != a1 || a2 != a2) ? NAN : std::fmin(a1, a2);
+    return lo > rhs;
 #endif
 }
 

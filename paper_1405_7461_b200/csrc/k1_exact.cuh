@@ -249,11 +249,14 @@ __device__ __forceinline__ Cand cand_exact(const FlushCfg &C, int64_t e) {
     return r;
 }
 
-// Query record of the FP32 pre-filter (48 B): filter view + exact times
-// for per-pair overlap counting.
+// Query record of the FP32 pre-filter (64 B): filter view (start, the
+// triangle bound's a and b), the query's end for the separating-axis stage
+// (filter.cuh f32_sep_far), and the exact times for windows and per-pair
+// overlap counting.
 struct __align__(16) QF32 {
     float ts, x, y, z;
-    float a, b, pad0, pad1;
+    float a, b, te, ex;
+    float ey, ez, pad0, pad1;
     double ts64, te64;
 };
 

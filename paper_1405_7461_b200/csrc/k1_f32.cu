@@ -41,6 +41,18 @@
 
 namespace tsk {
 
+// Development counters (built with -DTSK_K1_STATS only; read by
+// tsk_k1_stats): 0 box-cull sub-tiles, 1 box tests, 2 box survivors,
+// 3 sub-tiles with survivors, 4 pre-filter flags, 5 separating-axis
+// survivors, 6 exact-path flushes, 7 items.
+__device__ unsigned long long k1_stats[8];
+#ifdef TSK_K1_STATS
+#define K1_STAT(i, v) \
+    do { if ((threadIdx.x & 31) == 0) atomicAdd(&k1_stats[i], (unsigned long long)(v)); } while (0)
+#else
+#define K1_STAT(i, v) do { } while (0)
+#endif
+
 constexpr int CPT = K1F_CPT;
 constexpr int WCAND = 32 * CPT;         // candidates per warp
 constexpr int QCAP = 32 * (CPT + 1);    // queue entries per warp
@@ -64,6 +76,13 @@ __device__ __forceinline__ float4 *f_qbox() { return reinterpret_cast<float4 *>(
 __device__ __forceinline__ uint16_t *f_wlist(int warp) {
     return reinterpret_cast<uint16_t *>(k1_dyn + QBOX_OFF + 2 * sizeof(float4) * K1_TQ) + warp * K1_TQ;
 }
+// per-warp queue of the pairs that pass the separating-axis stage (< 64)
+constexpr int Q2CAP = 64;
+constexpr size_t Q2_OFF = QBOX_OFF + 2 * sizeof(float4) * K1_TQ + sizeof(uint16_t) * K1_TQ * K1_WARPS;
+__device__ __forceinline__ uint32_t *f_queue2(int warp) {
+    return reinterpret_cast<uint32_t *>(k1_dyn + Q2_OFF) + warp * Q2CAP;
+}
+__shared__ float k1_sep_rb;  // the item's separating-axis radius term (f32_sep_rbase)
 
 __device__ __forceinline__ void lds4f(uint32_t a, float &x, float &y, float &z, float &w) {
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "r"(a));
@@ -132,7 +151,7 @@ __device__ __noinline__ uint4 f32_scan(uint32_t qa, uint32_t qa_end, uint32_t ba
         lds4f(qa, qts, qx, qy, qz);
         lds4f(qa + 16, qa4, qb4, p0, p1);
         double cts = 0.0, cte = 0.0;
-        if (CNT) lds2d(qa + 32, cts, cte);
+        if (CNT) lds2d(qa + (uint32_t)offsetof(QF32, ts64), cts, cte);
         bool cand[CPT];
         const float R2 = f32_r2(qa4, srl, qb4);
         float n2[CPT];
@@ -244,6 +263,78 @@ __device__ __noinline__ uint4 f32_scan2(uint32_t qa, uint32_t qa_end, uint32_t b
     return make_uint4(qa, (unsigned)qn, 0u, 0u);
 }
 
+// Separating-axis stage (filter.cuh f32_sep_far) over up to 32 queued
+// pairs, one per lane, converged: the pairs it cannot reject move to the
+// warp's stage-2 queue, which feeds the exact path 32 at a time.  Returns
+// the new stage-2 count (< 64).
+__device__ __noinline__ int sep_stage(const QF32 *__restrict__ sqf, const uint32_t *wq, uint32_t *wq2, int nf,
+                                      int qn2, int warp, int lane) {
+    const float *cs = f_cands(warp);
+    bool keep = false;
+    uint32_t ent = 0u;
+    if (lane < nf) {
+        ent = wq[lane];
+        const int ci = (int)(ent >> 16), j = (int)(ent & 0xffffu);
+        const uint32_t qa = (uint32_t)__cvta_generic_to_shared(sqf + j);
+        float qts, qx, qy, qz, qa4, qb4, qte, qex, qey, qez, p0, p1;
+        lds4f(qa, qts, qx, qy, qz);
+        lds4f(qa + 16, qa4, qb4, qte, qex);
+        lds4f(qa + 32, qey, qez, p0, p1);
+        keep = !f32_sep_far(cs[0 * WCAND + ci], cs[1 * WCAND + ci], cs[2 * WCAND + ci], cs[3 * WCAND + ci],
+                            cs[4 * WCAND + ci], cs[5 * WCAND + ci], qts, qx, qy, qz, qte, qex, qey, qez, k1_sep_rb);
+    }
+    unsigned lt;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (keep) wq2[qn2 + __popc(m & lt)] = ent;
+    return qn2 + __popc(m);
+}
+
+// flush_queue with the separating-axis stage in front of the exact path:
+// stage 1 (the pre-filter's flags, qn) is drained 32 at a time through
+// sep_stage; the exact path runs on full batches of 32 survivors (qn2), and
+// on the rest when the range is done.  All counts are warp-uniform.
+template <int TA, int TB>
+__device__ __forceinline__ void flush_tight(const QRec *__restrict__ qt, const QF32 *__restrict__ sqf, uint32_t *wq,
+                                            int warp, int lane, int &qn, int &qn2, bool done,
+                                            unsigned long long &n_hit) {
+    uint32_t *const wq2 = f_queue2(warp);
+    while (qn >= 32 || (done && qn > 0)) {
+        const int nf = qn < 32 ? qn : 32;
+        __syncwarp();
+        K1_STAT(4, nf);
+        const int q2_in = qn2;
+        qn2 = sep_stage(sqf, wq, wq2, nf, qn2, warp, lane);
+        K1_STAT(5, qn2 - q2_in);
+        __syncwarp();
+        uint32_t mv[CPT];
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) mv[k] = lane + 32 * (k + 1) < qn ? wq[lane + 32 * (k + 1)] : 0u;
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < CPT; ++k)
+            if (lane + 32 * (k + 1) < qn) wq[lane + 32 * k] = mv[k];
+        qn -= nf;
+        if (qn2 >= 32) {
+            __syncwarp();
+            K1_STAT(6, 1);
+            rare_flush<TA, TB, false>(qt, wq2, warp, 32, lane, n_hit);
+            __syncwarp();
+            const uint32_t m2 = lane + 32 < qn2 ? wq2[lane + 32] : 0u;
+            __syncwarp();
+            if (lane + 32 < qn2) wq2[lane] = m2;
+            qn2 -= 32;
+        }
+    }
+    if (done && qn2 > 0) {
+        __syncwarp();
+        K1_STAT(6, 1);
+        rare_flush<TA, TB, false>(qt, wq2, warp, qn2, lane, n_hit);
+        __syncwarp();
+        qn2 = 0;
+    }
+}
+
 // f32_scan2 over the warp's list of surviving queries (box cull): the same
 // two-query iteration, the tile indices read from the list.  Returns
 // (next list position, queued).
@@ -342,13 +433,13 @@ __device__ __forceinline__ void f32_list_range(const QRec *__restrict__ qt, cons
                                                int warp, int lane, unsigned long long &n_hit) {
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(sqf);
     uint32_t *const wq = f_queue(warp);
-    int k = 0, qn = 0;
+    int k = 0, qn = 0, qn2 = 0;
     for (;;) {
         const uint2 o = f32_scanl(k, ns, base, qn, warp, lane);
         k = (int)o.x;
         qn = (int)o.y;
         const bool done = k >= ns;
-        flush_queue<TA_BOTH, TB_DYN, false, CPT>(qt, wq, warp, lane, qn, done, n_hit);
+        flush_tight<TA_BOTH, TB_DYN>(qt, sqf, wq, warp, lane, qn, qn2, done, n_hit);
         if (done) break;
     }
 }
@@ -363,7 +454,7 @@ __device__ __forceinline__ void f32_range(const QRec *__restrict__ qt, const QF3
     uint32_t qa = base + (uint32_t)j0 * (uint32_t)sizeof(QF32);
     const uint32_t qa_end = base + (uint32_t)j1 * (uint32_t)sizeof(QF32);
     uint32_t *const wq = f_queue(warp);
-    int qn = 0;
+    int qn = 0, qn2 = 0;
     for (;;) {
         const uint4 o = CNT ? f32_scan<TA, CNT>(qa, qa_end, base, qn, warp, lane)
                             : f32_scan2<TA>(qa, qa_end, base, qn, warp, lane);
@@ -371,7 +462,7 @@ __device__ __forceinline__ void f32_range(const QRec *__restrict__ qt, const QF3
         qn = (int)o.y;
         n_ov += (unsigned long long)o.z + (unsigned long long)o.w * CNT_B1;
         const bool done = qa >= qa_end;
-        flush_queue<TA, TB, false, CPT>(qt, wq, warp, lane, qn, done, n_hit);
+        flush_tight<TA, TB>(qt, sqf, wq, warp, lane, qn, qn2, done, n_hit);
         if (done) break;
     }
 }
@@ -458,6 +549,10 @@ __device__ __noinline__ void fast_subtile(const K1Launch &L, const ItemCtx &it, 
     int jhi = __shfl_sync(0xffffffffu, v, 1);
     if (jhi < jlo) jhi = jlo;
     const int ns = box_cull(L.gbox, L.e.n, wbase, jlo, jhi, cull_rb, warp, lane);
+    K1_STAT(0, 1);
+    K1_STAT(1, jhi - jlo);
+    K1_STAT(2, ns);
+    K1_STAT(3, ns > 0);
     if (ns == 0) return;
     // survivors: this warp's candidates
     double rts[CPT], rte[CPT];
@@ -550,6 +645,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
         }
         __syncthreads();
         if (item_sh >= total) break;
+        if (tid == 0) K1_STAT(7, 1);
         const ItemCtx it = it_sh;
         const QRec *const qt = L.q + it.lo_q;  // the tile's exact records (global; rare path)
 
@@ -582,20 +678,23 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
                     f32b[2] = vr;
                 }
             } else if (warp == 3) {
-                double aq = 0.0, tq = 0.0, eq = 0.0;
+                double aq = 0.0, tq = 0.0, eq = 0.0, dq = 0.0;
                 for (int j = lane; j < it.nt; j += 32) {
                     const QRec &q = qt[j];
                     aq = fmax(aq, fmax(fabs(q.sx - ox), fmax(fabs(q.sy - oy), fabs(q.sz - oz))));
                     tq = fmax(tq, fabs(q.ts - t0));
                     eq = fmax(eq, q.ext);
+                    dq = fmax(dq, fmax(fabs(q.dx), fmax(fabs(q.dy), fabs(q.dz))));
                 }
                 aq = warp_max(aq);
                 tq = warp_max(tq);
                 eq = warp_max(eq);
+                dq = warp_max(dq);
                 if (lane == 0) {
                     f32b[3] = aq;
                     f32b[4] = tq;
                     f32b[5] = eq;
+                    f32b[6] = dq;
                 }
             }
         }
@@ -612,6 +711,9 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
             fi_sh = f32_item(qt[0].sx, qt[0].sy, qt[0].sz, qt[0].ts, f32b[0], f32b[1], f32b[2], f32b[3], f32b[4],
                              f32b[5], cmax);
             fi_sh.ok = fi_sh.ok && launch_ok && !unsafe_q;
+            // separating-axis stage: M2 = A_r + TV_r + (T_q + E_q) V_r + A_q + D_q
+            const double M2 = f32b[0] + f32b[1] + (f32b[4] + f32b[5]) * f32b[2] + f32b[3] + f32b[6];
+            k1_sep_rb = f32_sep_rbase(dthr, cmax, M2);
         }
         __syncthreads();
         const bool item_f32 = fi_sh.ok;
@@ -623,8 +725,12 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
                 float v[6];
                 f32_query(q.ts, q.sx, q.sy, q.sz, q.ext, q.dx, q.dy, q.dz, fi_sh, dthr, v);
                 f.ts = v[0]; f.x = v[1]; f.y = v[2]; f.z = v[3]; f.a = v[4]; f.b = v[5];
+                float w[4];
+                f32_query_end(q.te, q.ex, q.ey, q.ez, fi_sh, w);
+                f.te = w[0]; f.ex = w[1]; f.ey = w[2]; f.ez = w[3];
             } else {
                 f.ts = f.x = f.y = f.z = f.a = f.b = 0.f;
+                f.te = f.ex = f.ey = f.ez = 0.f;
             }
             f.pad0 = f.pad1 = 0.f;
             f.ts64 = q.ts;
@@ -779,9 +885,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
     }
 }
 
-static size_t k1f_dyn_smem() {
-    return QBOX_OFF + 2 * sizeof(float4) * K1_TQ + sizeof(uint16_t) * K1_TQ * K1_WARPS;
-}
+static size_t k1f_dyn_smem() { return Q2_OFF + sizeof(uint32_t) * Q2CAP * K1_WARPS; }
 
 static void k1f_set_attrs() {
     static std::atomic<uint64_t> done_mask{0};
@@ -802,6 +906,23 @@ int k1f_blocks_per_sm() {
 }
 
 int k1f_candidates_per_thread() { return CPT; }
+
+}  // namespace tsk
+
+// Development counters of K1 (zeros unless built with -DTSK_K1_STATS).
+extern "C" int tsk_k1_stats(int device, unsigned long long *out, int n, int reset) {
+    if (cudaSetDevice(device) != cudaSuccess) return 1;
+    unsigned long long v[8] = {0};
+    if (cudaMemcpyFromSymbol(v, tsk::k1_stats, sizeof(v)) != cudaSuccess) return 1;
+    for (int i = 0; i < n && i < 8; ++i) out[i] = v[i];
+    if (reset) {
+        const unsigned long long z[8] = {0};
+        if (cudaMemcpyToSymbol(tsk::k1_stats, z, sizeof(z)) != cudaSuccess) return 1;
+    }
+    return 0;
+}
+
+namespace tsk {
 
 void launch_k1f(const K1Launch &L, int grid, cudaStream_t st) {
     k1f_set_attrs();

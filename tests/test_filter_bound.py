@@ -64,6 +64,10 @@ def test_filter_flags_every_nonnegative_reference_discriminant(tmp_path):
     # needed (without it the absorbed-offset pairs of mode 8 are culled)
     assert out["edge"]["box_checks"] > 1_000_000 and out["edge"]["box_misses"] == 0
     assert out["edge"]["box_mutation_misses"] > 0
+    # separating-axis stage: rejects pairs, never a reference hit; a
+    # margin-free radius does reject hits (the generator reaches the bound)
+    assert out["edge"]["sep_checks"] > 1_000_000 and out["edge"]["sep_rejected"] > 100_000
+    assert out["edge"]["sep_misses"] == 0 and out["edge"]["sep_mutation_misses"] > 0
     assert out["edge"]["hits"] > 100_000 and out["edge"]["f32_checks"] > 1_000_000
 
 

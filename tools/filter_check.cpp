@@ -91,7 +91,8 @@ static bool hoist(const Seg &g, double &ext, double v[3], double dd[3]) {
 struct Counts {
     long pairs = 0, overlapping = 0, disc_pos = 0, checks = 0, flagged = 0, misses = 0, skipped = 0;
     long hits = 0, f32_checks = 0, f32_flagged = 0, f32_misses = 0, f32_skipped = 0, box_checks = 0;
-    long box_misses = 0, box_mut_misses = 0;
+    long box_misses = 0, box_mut_misses = 0, sep_checks = 0, sep_rejected = 0, sep_misses = 0, sep_mut_misses = 0,
+         sep_only = 0;
 };
 
 // the reference's hit decision for an overlapping pair (core.py:523-551)
@@ -169,6 +170,34 @@ static void check_f32(const Seg &r, const Seg &c, double d, const double O[3], d
         if (n.f32_misses <= 5) std::fprintf(stderr, "F32 LANE MISS %s\n", tag);
     }
     const bool need = ref_hit(r, c, d);
+    // the separating-axis second stage over the query's span (f32_sep_far)
+    {
+        double dq = 0;
+        for (int i = 0; i < 3; ++i) dq = std::fmax(dq, std::fabs(c.e[i] - c.s[i]));
+        const double M2 = ar + tvr + (tq + cext) * vr + aq + dq;
+        float qe[4];
+        f32_query_end(c.te, c.e[0], c.e[1], c.e[2], it, qe);
+        const float rb = f32_sep_rbase(std::sqrt(d * d), cmax, M2);
+        const bool far = f32_sep_far(cf.px, cf.py, cf.pz, cf.vx, cf.vy, cf.vz, q[0], q[1], q[2], q[3], qe[0], qe[1],
+                                     qe[2], qe[3], rb);
+        ++n.sep_checks;
+        n.sep_rejected += far;
+        if (need && far) {
+            ++n.sep_misses;
+            if (n.sep_misses <= 5)
+                std::fprintf(stderr, "SEP MISS %s d=%.17g r=[%.17g %.17g (%.17g %.17g %.17g)->(%.17g %.17g %.17g)] "
+                             "c=[%.17g %.17g (%.17g %.17g %.17g)->(%.17g %.17g %.17g)]\n",
+                             tag, d, r.ts, r.te, r.s[0], r.s[1], r.s[2], r.e[0], r.e[1], r.e[2], c.ts, c.te,
+                             c.s[0], c.s[1], c.s[2], c.e[0], c.e[1], c.e[2]);
+        }
+        // mutation: margin-free radius (d itself, no m term) must reject hits
+        const float rb0 = TSK_F2F_RN(std::sqrt(d * d));
+        if (need && f32_sep_far(cf.px, cf.py, cf.pz, cf.vx, cf.vy, cf.vz, q[0], q[1], q[2], q[3], qe[0], qe[1],
+                                qe[2], qe[3], rb0, 0.f))
+            ++n.sep_mut_misses;
+        // every pair the second stage keeps is flagged by the first
+        if (!far && !f) ++n.sep_only;
+    }
     // the box cull (K1 layout): segment boxes rounded outward to FP32
     {
         float bl[2][3], bh[2][3];
@@ -416,14 +445,17 @@ int main(int argc, char **argv) {
     std::printf("{\"edge\": {\"pairs\": %ld, \"overlapping\": %ld, \"disc_pos\": %ld, \"checks\": %ld, "
                 "\"flagged\": %ld, \"skipped\": %ld, \"misses\": %ld, \"hits\": %ld, \"f32_checks\": %ld, "
                 "\"f32_flagged\": %ld, \"f32_skipped\": %ld, \"f32_misses\": %ld, \"box_checks\": %ld, "
-                "\"box_misses\": %ld, \"box_mutation_misses\": %ld}, "
+                "\"box_misses\": %ld, \"box_mutation_misses\": %ld, \"sep_checks\": %ld, \"sep_rejected\": %ld, "
+                "\"sep_misses\": %ld, \"sep_mutation_misses\": %ld}, "
                 "\"random\": {\"pairs\": %ld, \"overlapping\": %ld, \"disc_pos\": %ld, \"checks\": %ld, "
                 "\"flagged\": %ld, \"misses\": %ld, \"hits\": %ld, \"f32_checks\": %ld, \"f32_flagged\": %ld, "
                 "\"f32_misses\": %ld}}\n",
                 n.pairs, n.overlapping, n.disc_pos, n.checks, n.flagged, n.skipped, n.misses, n.hits,
                 n.f32_checks, n.f32_flagged, n.f32_skipped, n.f32_misses, n.box_checks, n.box_misses + nrand.box_misses,
-                n.box_mut_misses + nrand.box_mut_misses, nrand.pairs, nrand.overlapping,
+                n.box_mut_misses + nrand.box_mut_misses, n.sep_checks + nrand.sep_checks, n.sep_rejected + nrand.sep_rejected,
+                n.sep_misses + nrand.sep_misses, n.sep_mut_misses + nrand.sep_mut_misses, nrand.pairs, nrand.overlapping,
                 nrand.disc_pos, nrand.checks, nrand.flagged, nrand.misses, nrand.hits, nrand.f32_checks,
                 nrand.f32_flagged, nrand.f32_misses);
-    return (n.misses || nrand.misses || n.f32_misses || nrand.f32_misses || n.box_misses || nrand.box_misses) ? 1 : 0;
+    return (n.misses || nrand.misses || n.f32_misses || nrand.f32_misses || n.box_misses || nrand.box_misses ||
+            n.sep_misses || nrand.sep_misses) ? 1 : 0;
 }
