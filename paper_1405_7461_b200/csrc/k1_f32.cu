@@ -392,18 +392,7 @@ __device__ __noinline__ uint2 f32_scanl(int k, int ns, uint32_t base, int qn, in
 // its box's .w): the gap is formed from boxes rounded outward and rounded
 // down itself, so it never exceeds the true gap.  Returns the number of
 // survivors (warp-uniform).
-__device__ __forceinline__ int box_cull(const float4 *__restrict__ gbox, int64_t n, int64_t wbase, int jlo, int jhi,
-                                        float rbase, int warp, int lane) {
-    const int64_t g0 = wbase / BOX_GROUP;
-    int64_t g1 = (wbase + WCAND - 1) / BOX_GROUP;
-    const int64_t glast = (n - 1) / BOX_GROUP;
-    g1 = g1 < glast ? g1 : glast;
-    float4 lo = gbox[2 * g0], hi = gbox[2 * g0 + 1];
-    if (g1 != g0) {
-        const float4 l1 = gbox[2 * g1], h1 = gbox[2 * g1 + 1];
-        lo = make_float4(fminf(lo.x, l1.x), fminf(lo.y, l1.y), fminf(lo.z, l1.z), 0.f);
-        hi = make_float4(fmaxf(hi.x, h1.x), fmaxf(hi.y, h1.y), fmaxf(hi.z, h1.z), 0.f);
-    }
+__device__ __forceinline__ int box_cull(float4 lo, float4 hi, int jlo, int jhi, float rbase, int warp, int lane) {
     const float rw = __fadd_ru(rbase, box_cull_dterm(lo.x, lo.y, lo.z, hi.x, hi.y, hi.z));
     const float4 *qb = f_qbox();
     uint16_t *const wl = f_wlist(warp);
@@ -522,19 +511,77 @@ __device__ __forceinline__ void stage_cands(const K1Launch &L, int64_t wbase, in
     }
 }
 
+// The bounding box of a warp's 128 candidates (K1 layout: the union of the
+// boxes of the BOX_GROUPs it spans) and whether a segment in it is unsafe
+// (.w of the low corners).
+__device__ __forceinline__ void warp_box(const K1Launch &L, int64_t wbase, int64_t c_hi, float4 &lo, float4 &hi,
+                                         bool &unsafe) {
+    const int64_t g0 = wbase / BOX_GROUP;
+    const int64_t g1 = (wbase + WCAND - 1 < c_hi ? wbase + WCAND - 1 : c_hi) / BOX_GROUP;
+    lo = L.gbox[2 * g0];
+    hi = L.gbox[2 * g0 + 1];
+    unsafe = lo.w != 0.f;
+    if (g1 != g0) {
+        const float4 l1 = L.gbox[2 * g1], h1 = L.gbox[2 * g1 + 1];
+        unsafe |= l1.w != 0.f;
+        lo = make_float4(fminf(lo.x, l1.x), fminf(lo.y, l1.y), fminf(lo.z, l1.z), 0.f);
+        hi = make_float4(fmaxf(hi.x, h1.x), fmaxf(hi.y, h1.y), fmaxf(hi.z, h1.z), 0.f);
+    }
+}
+
+// Two of a lane's candidates (k0, k0 + 1) in FP32 pre-filter form, staged
+// in shared memory: every global load is issued before any conversion (one
+// round trip); lanes past the item's range stage a far-away point.
+__device__ __forceinline__ void stage_pair(const K1Launch &L, int64_t wbase, int64_t c_lo, int64_t c_hi, int k0,
+                                           const F32Item &fi, float *wcs, int lane) {
+    double ts[2], sx[2], sy[2], sz[2], vx[2], vy[2], vz[2];
+    float sr[2];
+    bool ok[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int64_t e = wbase + (k0 + h) * 32 + lane;
+        ok[h] = e >= c_lo && e <= c_hi;
+        const int64_t ec = ok[h] ? e : c_lo;  // loads stay unconditional
+        ts[h] = L.e.ts[ec];
+        sx[h] = L.e.sx[ec]; sy[h] = L.e.sy[ec]; sz[h] = L.e.sz[ec];
+        vx[h] = L.e.vx[ec]; vy[h] = L.e.vy[ec]; vz[h] = L.e.vz[ec];
+        sr[h] = L.e.sr32[ec];
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int i = (k0 + h) * 32 + lane;
+        CandF32 c;
+        c.px = c.py = c.pz = 0x1p60f;
+        c.vx = c.vy = c.vz = c.sr = 0.f;
+        if (ok[h]) c = f32_cand_sr(ts[h], sx[h], sy[h], sz[h], vx[h], vy[h], vz[h], sr[h], fi);
+        wcs[0 * WCAND + i] = c.px; wcs[1 * WCAND + i] = c.py; wcs[2 * WCAND + i] = c.pz;
+        wcs[3 * WCAND + i] = c.vx; wcs[4 * WCAND + i] = c.vy; wcs[5 * WCAND + i] = c.vz;
+        wcs[6 * WCAND + i] = c.sr;
+    }
+}
+
+// Item-level key bases of the K1 layout (hits add their own orig - f).
+__shared__ uint64_t k1_kb[2];
+__shared__ int64_t k1_kf[2];
+
 // One warp sub-tile on the box-cull fast path (K1 layout, overlaps counted
 // outside K1).  The window is every query whose extent meets the time range
 // of the candidates' groups (two bisections on the tile's sorted ts / te);
 // pairs in it that do not overlap in time are rejected by the exact path if
-// they are ever flagged.  Only warps with a query near their box load their
-// candidates.
+// they are ever flagged (its tb case is chosen per pair: the warp's end-time
+// bounds are left open).  Only warps with a query near their box load their
+// candidates, all columns in one round trip.
 __device__ __noinline__ void fast_subtile(const K1Launch &L, const ItemCtx &it, const QRec *__restrict__ qt,
                                           const QF32 *__restrict__ sqf, const double *pm, const double *sm,
                                           int64_t wbase, float cull_rb, const F32Item &fi, bool item_f32, float *wcs,
                                           int warp, int lane, unsigned long long &n_ev, unsigned long long &n_hit) {
     const int64_t g0 = wbase / BOX_GROUP;
-    int64_t g1 = (wbase + WCAND - 1 < it.c_hi ? wbase + WCAND - 1 : it.c_hi) / BOX_GROUP;
+    const int64_t g1 = (wbase + WCAND - 1 < it.c_hi ? wbase + WCAND - 1 : it.c_hi) / BOX_GROUP;
+    // the groups' time range and box, loaded together
     double2 tr = L.gtime[g0];
+    float4 blo, bhi;
+    bool unsafe_g;
+    warp_box(L, wbase, it.c_hi, blo, bhi, unsafe_g);
     if (g1 != g0) {
         const double2 t1 = L.gtime[g1];
         tr.x = tr.x < t1.x ? tr.x : t1.x;
@@ -548,50 +595,56 @@ __device__ __noinline__ void fast_subtile(const K1Launch &L, const ItemCtx &it, 
     const int jlo = __shfl_sync(0xffffffffu, v, 0);
     int jhi = __shfl_sync(0xffffffffu, v, 1);
     if (jhi < jlo) jhi = jlo;
-    const int ns = box_cull(L.gbox, L.e.n, wbase, jlo, jhi, cull_rb, warp, lane);
+    const int ns = box_cull(blo, bhi, jlo, jhi, cull_rb, warp, lane);
     K1_STAT(0, 1);
     K1_STAT(1, jhi - jlo);
     K1_STAT(2, ns);
     K1_STAT(3, ns > 0);
     if (ns == 0) return;
-    // survivors: this warp's candidates
-    double rts[CPT], rte[CPT];
-    bool unsafe_r = false;
-    double wmin = INFINITY, wmax = -INFINITY, wmin_te = INFINITY, wmax_ts = -INFINITY;
-#pragma unroll
-    for (int k = 0; k < CPT; ++k) {
-        const int64_t e = wbase + k * 32 + lane;
-        rts[k] = INFINITY;
-        rte[k] = -INFINITY;
-        if (e >= it.c_lo && e <= it.c_hi) {
-            rts[k] = L.e.ts[e];
-            rte[k] = L.e.te[e];
-            unsafe_r |= L.e.unsafe[e] != 0;
-            wmin = rts[k] < wmin ? rts[k] : wmin;
-            wmax = rte[k] > wmax ? rte[k] : wmax;
-            wmin_te = rte[k] < wmin_te ? rte[k] : wmin_te;
-            wmax_ts = rts[k] > wmax_ts ? rts[k] : wmax_ts;
-        }
-    }
-    wmax = warp_max(wmax);
-    wmin_te = warp_min(wmin_te);
     if (lane == 0) {
-        set_key_bases(L, it, wbase, warp);
+        k1_wctx[warp].key_base0 = k1_kb[0];
+        k1_wctx[warp].key_base1 = k1_kb[1];
+        k1_wctx[warp].f0 = k1_kf[0];
+        k1_wctx[warp].f1 = k1_kf[1];
         k1_wctx[warp].js = it.js;
         k1_wctx[warp].wbase = wbase;
         const int64_t nv = it.c_hi - wbase + 1;
         k1_wctx[warp].nvalid = nv < 0 ? 0 : (nv > WCAND ? WCAND : (int)nv);
-        k1_wctx[warp].wmin_te = wmin_te;
-        k1_wctx[warp].wmax = wmax;
+        // the exact path picks each pair's tb case itself (TB_DYN, open bounds)
+        k1_wctx[warp].wmin_te = -INFINITY;
+        k1_wctx[warp].wmax = INFINITY;
     }
     __syncwarp();
-    if (!item_f32 || __any_sync(0xffffffffu, unsafe_r)) {
+    if (!item_f32 || unsafe_g) {
         // extreme-exponent candidates or an item outside the FP32 path's
         // bounds: the exact path over the whole window
         // (its per-pair overlap counts are not needed here)
-        unsigned long long ov_unused = 0;
+        double rts[CPT], rte[CPT];
+        double wmin = INFINITY, wmax = -INFINITY, wmin_te = INFINITY, wmax_ts = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            const int64_t e = wbase + k * 32 + lane;
+            rts[k] = INFINITY;
+            rte[k] = -INFINITY;
+            if (e >= it.c_lo && e <= it.c_hi) {
+                rts[k] = L.e.ts[e];
+                rte[k] = L.e.te[e];
+                wmin = rts[k] < wmin ? rts[k] : wmin;
+                wmax = rte[k] > wmax ? rte[k] : wmax;
+                wmin_te = rte[k] < wmin_te ? rte[k] : wmin_te;
+                wmax_ts = rts[k] > wmax_ts ? rts[k] : wmax_ts;
+            }
+        }
+        wmax = warp_max(wmax);
+        wmin_te = warp_min(wmin_te);
         wmin = warp_min(wmin);
         wmax_ts = warp_max(wmax_ts);
+        if (lane == 0) {
+            k1_wctx[warp].wmin_te = wmin_te;
+            k1_wctx[warp].wmax = wmax;
+        }
+        __syncwarp();
+        unsigned long long ov_unused = 0;
         const int4 w = warp_window(sqf, pm, it.nt, false, wmin, wmax, wmax_ts, lane);
         all_range<TA_C>(qt, sqf, w.x, w.y, rts, rte, warp, lane, ov_unused, n_hit);
         all_range<TA_BOTH>(qt, sqf, w.y, w.z, rts, rte, warp, lane, ov_unused, n_hit);
@@ -599,7 +652,8 @@ __device__ __noinline__ void fast_subtile(const K1Launch &L, const ItemCtx &it, 
         return;
     }
     n_ev += (unsigned long long)ns * (unsigned long long)k1_wctx[warp].nvalid;
-    stage_cands(L, wbase, it.c_lo, it.c_hi, rts, fi, wcs, lane);
+#pragma unroll
+    for (int k = 0; k < CPT; k += 2) stage_pair(L, wbase, it.c_lo, it.c_hi, k, fi, wcs, lane);
     __syncwarp();
     f32_list_range(qt, sqf, ns, warp, lane, n_hit);
 }
@@ -714,6 +768,12 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
             // separating-axis stage: M2 = A_r + TV_r + (T_q + E_q) V_r + A_q + D_q
             const double M2 = f32b[0] + f32b[1] + (f32b[4] + f32b[5]) * f32b[2] + f32b[3] + f32b[6];
             k1_sep_rb = f32_sep_rbase(dthr, cmax, M2);
+            if (L.orig) {  // K1 layout: key bases are per item
+                k1_kf[0] = L.plan.first[it.b];
+                k1_kf[1] = it.b1 >= 0 ? L.plan.first[it.b1] : 0;
+                k1_kb[0] = make_key(L, it.b, 0, it.q0);
+                k1_kb[1] = it.b1 >= 0 ? make_key(L, it.b1, 0, 0) : 0;
+            }
         }
         __syncthreads();
         const bool item_f32 = fi_sh.ok;
@@ -827,7 +887,10 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
                 if (cull) {
                     // K1 layout: one box test per (query, warp) first; the
                     // candidates are converted only when a query survives
-                    const int ns = box_cull(L.gbox, L.e.n, wbase, jlo, jhi, cull_rb, warp, lane);
+                    float4 blo, bhi;
+                    bool bunsafe;
+                    warp_box(L, wbase, it.c_hi, blo, bhi, bunsafe);
+                    const int ns = box_cull(blo, bhi, jlo, jhi, cull_rb, warp, lane);
                     n_ev += (unsigned long long)ns * (unsigned long long)k1_wctx[warp].nvalid;
                     if (ns == 0) continue;
                     stage_cands(L, wbase, it.c_lo, it.c_hi, rts, fi_sh, wcs, lane);

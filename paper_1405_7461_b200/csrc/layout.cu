@@ -119,7 +119,7 @@ __global__ void k_layout_gather(int64_t n, const int64_t *__restrict__ perm, Soa
 }
 
 // one warp per BOX_GROUP entries: the segments' bounding box, rounded outward,
-// and the group's time range
+// the group's time range and whether it holds an unsafe segment
 __global__ void k_group_boxes(int64_t n, Soa s, float4 *__restrict__ box, double2 *__restrict__ gtime) {
     const int lane = threadIdx.x & 31;
     const int64_t ng = (n + BOX_GROUP - 1) / BOX_GROUP;
@@ -127,9 +127,11 @@ __global__ void k_group_boxes(int64_t n, Soa s, float4 *__restrict__ box, double
          g += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
         double tlo = INFINITY, thi = -INFINITY;
+        bool unsafe = false;
         for (int k = lane; k < BOX_GROUP; k += 32) {
             const int64_t i = g * BOX_GROUP + k;
             if (i >= n) break;
+            unsafe |= s.unsafe[i] != 0;
             tlo = fmin(tlo, s.ts[i]);
             thi = fmax(thi, s.te[i]);
             const double a[3] = {s.sx[i], s.sy[i], s.sz[i]}, b[3] = {s.ex[i], s.ey[i], s.ez[i]};
@@ -146,10 +148,13 @@ __global__ void k_group_boxes(int64_t n, Soa s, float4 *__restrict__ box, double
             tlo = fmin(tlo, __shfl_xor_sync(0xffffffffu, tlo, o));
             thi = fmax(thi, __shfl_xor_sync(0xffffffffu, thi, o));
         }
+        unsafe = __any_sync(0xffffffffu, unsafe);
         if (lane == 0) {
             gtime[g] = make_double2(tlo, thi);
+            // .w of the low corner: 1 when a segment of the group has extreme
+            // exponents (K1 then evaluates its pairs exactly)
             box[2 * g] = make_float4(__double2float_rd(lo[0]), __double2float_rd(lo[1]),
-                                     __double2float_rd(lo[2]), 0.f);
+                                     __double2float_rd(lo[2]), unsafe ? 1.f : 0.f);
             box[2 * g + 1] = make_float4(__double2float_ru(hi[0]), __double2float_ru(hi[1]),
                                          __double2float_ru(hi[2]), 0.f);
         }
