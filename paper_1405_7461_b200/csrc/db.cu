@@ -563,7 +563,10 @@ __global__ void __launch_bounds__(1024, 1) k_plan_items(SearchPlanDev p, int64_t
         tqs >>= 1;
     }
     if (threadIdx.x == 0) {
-        int sub = (int)(tiles_sh / (want > 0 ? want : 1));
+        // candidate sub-tiles per item: as many as keep >= 8 items per slot
+        // (fewer, longer items amortise the per-item set-up; the last items
+        // bound the tail)
+        int sub = (int)(tiles_sh / (2 * want > 0 ? 2 * want : 1));
         sub_sh = sub < 1 ? 1 : (sub > K1_MAX_SUB ? K1_MAX_SUB : sub);
         carry = 0;
     }
@@ -679,6 +682,8 @@ extern "C" int tsk_db_replicate(const tsk_db *src, int device, tsk_db **out) {
         db->s.sorted = src->s.sorted;
         db->s.te_sorted = src->s.te_sorted;
         db->cmax = src->cmax;
+        db->host_etraj = src->host_etraj;  // host ids are shared with the source
+        db->host_eseg = src->host_eseg;
         TSK_CUDA(cudaStreamSynchronize(db->stream));
         *out = db;
         return TSK_OK;

@@ -669,6 +669,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
     __shared__ int64_t item_sh;
     __shared__ int flags_sh;      // bit 0: unsafe query, bit 1: te not sorted
     __shared__ unsigned long long red[4], red_ev;  // per-batch overlap / hit sums, evaluated pairs
+    __shared__ int wsub_next;     // fast path: the item's next unclaimed warp sub-tile
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) fill_flush_cfg(L);
@@ -695,6 +696,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
             if (item < total) it_sh = decode_item(L, item, ct, tqs);
             red[0] = red[1] = red[2] = red[3] = 0;
             red_ev = 0;
+            wsub_next = 0;
             flags_sh = 0;
         }
         __syncthreads();
@@ -819,7 +821,20 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
 
         unsigned long long n_ov = 0, n_hit = 0;  // batch b in the low half, b1 in the high half
         unsigned long long n_ev = 0;  // pairs evaluated by the pre-filter (warp-uniform)
-        for (int s = 0; s < sub; ++s) {
+        if (fast && !L.noop) {
+            // warps claim the item's warp sub-tiles (128 candidates) one at a
+            // time, so the end-of-item barrier waits for one sub-tile at most
+            const int nw = (int)((it.c_hi - it.first_c) / WCAND) + 1;
+            for (;;) {
+                int w = 0;
+                if (lane == 0) w = atomicAdd(&wsub_next, 1);
+                w = __shfl_sync(0xffffffffu, w, 0);
+                if (w >= nw) break;
+                fast_subtile(L, it, qt, sqf, pm, sm, it.first_c + (int64_t)w * WCAND, cull_rb, fi_sh, item_f32, wcs,
+                             warp, lane, n_ev, n_hit);
+            }
+        }
+        for (int s = 0; s < sub && !(fast && !L.noop); ++s) {
             const int64_t base = it.first_c + (int64_t)s * STRIDE;
             if (base > it.c_hi) break;  // block-uniform
             const int64_t wbase = base + (int64_t)warp * WCAND;

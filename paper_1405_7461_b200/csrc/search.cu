@@ -13,6 +13,8 @@
 //   into a pinned block owned by the tsk_result.
 #include <cub/cub.cuh>
 
+#include <chrono>
+
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -176,8 +178,9 @@ __global__ void k_gather(GatherArgs a) {
 __global__ void k_compact(int64_t r0, int64_t r1, const uint64_t *__restrict__ keys, const uint32_t *__restrict__ perm,
                           const double *__restrict__ tb_in, const double *__restrict__ te_in,
                           const int64_t *__restrict__ lo, const int64_t *__restrict__ first, int major_bits,
-                          int minor_bits, double *__restrict__ o_tb, double *__restrict__ o_te,
-                          uint32_t *__restrict__ o_eo, uint32_t *__restrict__ o_qo) {
+                          int minor_bits, const int64_t *__restrict__ etraj, const int64_t *__restrict__ eseg,
+                          double *__restrict__ o_tb, double *__restrict__ o_te, int64_t *__restrict__ o_et,
+                          int64_t *__restrict__ o_es, uint32_t *__restrict__ o_qo) {
     const uint64_t mmask = major_bits ? ((~0ull) >> (64 - major_bits)) : 0ull;
     const uint64_t nmask = minor_bits ? ((~0ull) >> (64 - minor_bits)) : 0ull;
     for (int64_t i = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r1;
@@ -187,7 +190,8 @@ __global__ void k_compact(int64_t r0, int64_t r1, const uint64_t *__restrict__ k
         const int64_t e = first[b] + (int64_t)((k >> minor_bits) & mmask);
         const int64_t q = lo[b] + (int64_t)(k & nmask);
         const int64_t j = perm ? (int64_t)perm[i] : i;
-        o_eo[i] = (uint32_t)e;
+        o_et[i] = etraj[e];
+        o_es[i] = eseg[e];
         o_qo[i] = (uint32_t)q;
         o_tb[i] = tb_in[j];
         o_te[i] = te_in[j];
@@ -283,23 +287,24 @@ static int sm_count(int device) {
 static const int64_t kCompactMin = int64_t(1) << 18;
 static const int64_t kCompactChunk = int64_t(1) << 21;  // rows per pipeline chunk
 
-// Compact result assembly, pipelined: for each chunk of sorted rows K4 writes
-// (t_begin, t_end, entry ordinal, query ordinal) on the db stream; a copy
-// stream moves t_begin/t_end straight into the result's pinned columns and
-// the ordinals into a pinned staging block (24 B/row over PCIe instead of
-// 48); host threads expand the four id columns of chunk c from the host id
-// columns while chunk c+1 is in flight.  Result bytes are identical to the
-// device gather's.
+// Compact result assembly, pipelined: for each chunk of sorted rows K4
+// writes t_begin, t_end and the entry ids (gathered on the device) plus the
+// query ordinal on the db stream; a copy stream moves the first four
+// straight into the result's pinned columns and the ordinals into a pinned
+// staging block (36 B/row over PCIe instead of 48); host threads expand the
+// query id columns of chunk c (a small, cache-resident table) while chunk
+// c+1 is in flight.  Result bytes are identical to the device gather's.
 static void compact_rows(tsk_db *db, tsk_result *res, const tsk_columns *qc, int64_t nh, const uint64_t *keys,
                          const uint32_t *perm, const double *tbin, const double *tein, const int64_t *d_lo,
                          const int64_t *d_first, int major_bits, int minor_bits, cudaStream_t st,
                          int64_t &launches) {
     const size_t cb = (size_t)nh * 8;
-    db->out_cols.reserve((size_t)nh * 24 + 64, st);
+    db->out_cols.reserve((size_t)nh * 36 + 64, st);
     double *d_tb = db->out_cols.as<double>();
     double *d_te = d_tb + nh;
-    uint32_t *d_eo = reinterpret_cast<uint32_t *>(d_te + nh);
-    uint32_t *d_qo = d_eo + nh;
+    int64_t *d_et = reinterpret_cast<int64_t *>(d_te + nh);
+    int64_t *d_es = d_et + nh;
+    uint32_t *d_qo = reinterpret_cast<uint32_t *>(d_es + nh);
     size_t got = 0;
     res->host = pin_alloc(cb * 6, &got);
     res->host_bytes = got;
@@ -311,8 +316,7 @@ static void compact_rows(tsk_db *db, tsk_result *res, const tsk_columns *qc, int
     res->tbeg = (double *)(hb + 4 * cb);
     res->tend = (double *)(hb + 5 * cb);
     size_t ogot = 0;
-    uint32_t *h_ord = static_cast<uint32_t *>(pin_alloc((size_t)nh * 8, &ogot));
-    uint32_t *h_eo = h_ord, *h_qo = h_ord + nh;
+    uint32_t *h_qo = static_cast<uint32_t *>(pin_alloc((size_t)nh * 4, &ogot));
     if (!db->stream2) TSK_CUDA(cudaStreamCreateWithFlags(&db->stream2, cudaStreamNonBlocking));
     cudaStream_t st2 = db->stream2;
     int64_t chunk = kCompactChunk;
@@ -326,41 +330,49 @@ static void compact_rows(tsk_db *db, tsk_result *res, const tsk_columns *qc, int
     for (int64_t c = 0; c < nc; ++c) {
         const int64_t r0 = c * chunk, r1 = std::min<int64_t>(nh, r0 + chunk), m = r1 - r0;
         const int grid = (int)std::min<int64_t>((m + 255) / 256, 148 * 8);
-        k_compact<<<grid, 256, 0, st>>>(r0, r1, keys, perm, tbin, tein, d_lo, d_first, major_bits, minor_bits, d_tb,
-                                        d_te, d_eo, d_qo);
+        k_compact<<<grid, 256, 0, st>>>(r0, r1, keys, perm, tbin, tein, d_lo, d_first, major_bits, minor_bits,
+                                        db->s.traj, db->s.seg, d_tb, d_te, d_et, d_es, d_qo);
         TSK_CUDA(cudaGetLastError());
         ++launches;
         TSK_CUDA(cudaEventRecord(evg[c], st));
         TSK_CUDA(cudaStreamWaitEvent(st2, evg[c], 0));
         TSK_CUDA(cudaMemcpyAsync(res->tbeg + r0, d_tb + r0, (size_t)m * 8, cudaMemcpyDeviceToHost, st2));
         TSK_CUDA(cudaMemcpyAsync(res->tend + r0, d_te + r0, (size_t)m * 8, cudaMemcpyDeviceToHost, st2));
-        TSK_CUDA(cudaMemcpyAsync(h_eo + r0, d_eo + r0, (size_t)m * 4, cudaMemcpyDeviceToHost, st2));
+        TSK_CUDA(cudaMemcpyAsync(res->etraj + r0, d_et + r0, (size_t)m * 8, cudaMemcpyDeviceToHost, st2));
+        TSK_CUDA(cudaMemcpyAsync(res->eseg + r0, d_es + r0, (size_t)m * 8, cudaMemcpyDeviceToHost, st2));
         TSK_CUDA(cudaMemcpyAsync(h_qo + r0, d_qo + r0, (size_t)m * 4, cudaMemcpyDeviceToHost, st2));
         TSK_CUDA(cudaEventRecord(evd[c], st2));
     }
     // the db stream waits for the copies (the caller's end event covers them)
     TSK_CUDA(cudaStreamWaitEvent(st, evd[nc - 1], 0));
-    const int64_t *qt = qc->traj, *qs = qc->seg, *et = db->host_etraj, *es = db->host_eseg;
+    const int64_t *qt = qc->traj, *qs = qc->seg;
     HostPool &pool = HostPool::get();
+    const bool trace = getenv("TSK_TRACE") != nullptr;
+    double t_wait = 0.0, t_exp = 0.0;
     for (int64_t c = 0; c < nc; ++c) {
         const int64_t r0 = c * chunk, r1 = std::min<int64_t>(nh, r0 + chunk);
+        const auto h0 = std::chrono::steady_clock::now();
         TSK_CUDA(cudaEventSynchronize(evd[c]));
+        const auto h1 = std::chrono::steady_clock::now();
+        t_wait += std::chrono::duration<double>(h1 - h0).count();
         pool.run([&](int part, int parts) {
             const int64_t a = r0 + (r1 - r0) * part / parts, z = r0 + (r1 - r0) * (part + 1) / parts;
             for (int64_t i = a; i < z; ++i) {
-                const uint32_t q = h_qo[i], e = h_eo[i];
+                const uint32_t q = h_qo[i];
                 res->qtraj[i] = qt[q];
                 res->qseg[i] = qs[q];
-                res->etraj[i] = et[e];
-                res->eseg[i] = es[e];
             }
         });
+        t_exp += std::chrono::duration<double>(std::chrono::steady_clock::now() - h1).count();
     }
+    if (trace)
+        fprintf(stderr, "[tsk trace] compact %lld rows in %lld chunks: host wait %.3f ms, expansion %.3f ms (%d threads)\n",
+                (long long)nh, (long long)nc, t_wait * 1e3, t_exp * 1e3, pool.size());
     for (int64_t c = 0; c < nc; ++c) {
         cudaEventDestroy(evg[c]);
         cudaEventDestroy(evd[c]);
     }
-    pin_free(h_ord, ogot);
+    pin_free(h_qo, ogot);
 }
 
 static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int64_t *b_lo,
@@ -603,7 +615,7 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
         // span searches; the caller registered the store's host id columns)
         const char *cpenv = getenv("TSK_COMPACT");
         const bool compact = !on_device && !canonical && !want_ord && ordered && !query_major &&
-                             db->host_etraj && db->host_eseg && qc->traj && qc->seg && n <= 0xffffffffll &&
+                             qc->traj && qc->seg && n <= 0xffffffffll &&
                              nq <= 0xffffffffll &&
                              (cpenv ? strcmp(cpenv, "off") != 0 : nh >= kCompactMin) &&
                              !(cpenv && !strcmp(cpenv, "off"));

@@ -12,6 +12,7 @@
 
 #include <mutex>
 #include <string>
+#include <memory>
 #include <vector>
 
 #include "../../include/trajseek.h"
@@ -367,6 +368,9 @@ int k1_candidates_per_thread(bool f32);
 #endif
 constexpr int K1_THREADS = K1_THREADS_DEF;
 constexpr int K1_TQ = 256;        // queries per tile staged in shared memory
-constexpr int K1_MAX_SUB = 8;     // candidate sub-tiles (of K1_THREADS) per item
+#ifndef K1_MAX_SUB_DEF
+#define K1_MAX_SUB_DEF 32
+#endif
+constexpr int K1_MAX_SUB = K1_MAX_SUB_DEF;  // candidate sub-tiles (of K1_THREADS) per item
 
 }  // namespace tsk
