@@ -242,6 +242,31 @@ double soa_cmax(const Soa &s, cudaStream_t st) {
     return v;
 }
 
+// 1 when every entry id (traj, seg) fits in int32: results then cross PCIe
+// with 4-byte entry ids, widened on the host (search.cu)
+__global__ void k_ids32(int64_t n, const int64_t *__restrict__ traj, const int64_t *__restrict__ seg, int *ok) {
+    bool fit = true;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        fit = fit && traj[i] == (int64_t)(int32_t)traj[i] && seg[i] == (int64_t)(int32_t)seg[i];
+    if (!__all_sync(0xffffffffu, fit) && (threadIdx.x & 31) == 0) atomicAnd(ok, 0);
+}
+
+int soa_ids32(const Soa &s, cudaStream_t st) {
+    if (s.n == 0) return 1;
+    int *d;
+    TSK_CUDA(cudaMallocAsync(&d, 4, st));
+    const int one = 1;
+    TSK_CUDA(cudaMemcpyAsync(d, &one, 4, cudaMemcpyHostToDevice, st));
+    int grid = (int)std::min<int64_t>((s.n + 255) / 256, 148 * 16);
+    k_ids32<<<grid, 256, 0, st>>>(s.n, s.traj, s.seg, d);
+    TSK_CUDA(cudaGetLastError());
+    int h = 0;
+    TSK_CUDA(cudaMemcpyAsync(&h, d, 4, cudaMemcpyDeviceToHost, st));
+    TSK_CUDA(cudaFreeAsync(d, st));
+    TSK_CUDA(cudaStreamSynchronize(st));
+    return h;
+}
+
 // ── queries → shared-memory records ────────────────────────────────────────
 
 // Queries: hoisted invariants straight into the shared-memory records (one
@@ -635,6 +660,7 @@ extern "C" int tsk_db_create(int device, const tsk_columns *cols, tsk_db **out) 
         soa_hoist(db->s, db->stream);
         soa_group_bounds(db->s, db->stream);
         db->cmax = soa_cmax(db->s, db->stream);
+        db->ids32 = soa_ids32(db->s, db->stream);
         *out = db;
         return TSK_OK;
     } catch (const Error &e) {
@@ -682,6 +708,7 @@ extern "C" int tsk_db_replicate(const tsk_db *src, int device, tsk_db **out) {
         db->s.sorted = src->s.sorted;
         db->s.te_sorted = src->s.te_sorted;
         db->cmax = src->cmax;
+        db->ids32 = src->ids32;
         db->host_etraj = src->host_etraj;  // host ids are shared with the source
         db->host_eseg = src->host_eseg;
         TSK_CUDA(cudaStreamSynchronize(db->stream));

@@ -14,6 +14,8 @@
 #include <cub/cub.cuh>
 
 #include <chrono>
+#include <condition_variable>
+#include <thread>
 
 #include <cmath>
 #include <cstdio>
@@ -180,7 +182,7 @@ __global__ void k_compact(int64_t r0, int64_t r1, const uint64_t *__restrict__ k
                           const int64_t *__restrict__ lo, const int64_t *__restrict__ first, int major_bits,
                           int minor_bits, const int64_t *__restrict__ etraj, const int64_t *__restrict__ eseg,
                           double *__restrict__ o_tb, double *__restrict__ o_te, int64_t *__restrict__ o_et,
-                          int64_t *__restrict__ o_es, uint32_t *__restrict__ o_qo) {
+                          int64_t *__restrict__ o_es, uint32_t *__restrict__ o_qo, int ids32) {
     const uint64_t mmask = major_bits ? ((~0ull) >> (64 - major_bits)) : 0ull;
     const uint64_t nmask = minor_bits ? ((~0ull) >> (64 - minor_bits)) : 0ull;
     for (int64_t i = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r1;
@@ -190,8 +192,13 @@ __global__ void k_compact(int64_t r0, int64_t r1, const uint64_t *__restrict__ k
         const int64_t e = first[b] + (int64_t)((k >> minor_bits) & mmask);
         const int64_t q = lo[b] + (int64_t)(k & nmask);
         const int64_t j = perm ? (int64_t)perm[i] : i;
-        o_et[i] = etraj[e];
-        o_es[i] = eseg[e];
+        if (ids32) {  // ids known to fit: 4 bytes each over PCIe
+            reinterpret_cast<int32_t *>(o_et)[i] = (int32_t)etraj[e];
+            reinterpret_cast<int32_t *>(o_es)[i] = (int32_t)eseg[e];
+        } else {
+            o_et[i] = etraj[e];
+            o_es[i] = eseg[e];
+        }
         o_qo[i] = (uint32_t)q;
         o_tb[i] = tb_in[j];
         o_te[i] = te_in[j];
@@ -331,7 +338,7 @@ static void compact_rows(tsk_db *db, tsk_result *res, const tsk_columns *qc, int
         const int64_t r0 = c * chunk, r1 = std::min<int64_t>(nh, r0 + chunk), m = r1 - r0;
         const int grid = (int)std::min<int64_t>((m + 255) / 256, 148 * 8);
         k_compact<<<grid, 256, 0, st>>>(r0, r1, keys, perm, tbin, tein, d_lo, d_first, major_bits, minor_bits,
-                                        db->s.traj, db->s.seg, d_tb, d_te, d_et, d_es, d_qo);
+                                        db->s.traj, db->s.seg, d_tb, d_te, d_et, d_es, d_qo, 0);
         TSK_CUDA(cudaGetLastError());
         ++launches;
         TSK_CUDA(cudaEventRecord(evg[c], st));
@@ -373,6 +380,355 @@ static void compact_rows(tsk_db *db, tsk_result *res, const tsk_columns *qc, int
         cudaEventDestroy(evd[c]);
     }
     pin_free(h_qo, ogot);
+}
+
+// ── pipelined search (north star (d): H2D / compute / D2H overlap) ───────────
+//
+// Reference-ordered results through the compact path (28 B/row over PCIe
+// when entry ids fit in int32, else 36).  The plan is cut into
+// chunks of consecutive batches (even boundaries keep K1's batch pairs);
+// chunk c's K1 appends to the shared result buffer behind chunk c-1's hits,
+// and the host learns each chunk's row range from a counter snapshot.  The
+// db stream runs K1(0) S(0) K1(1) S(1) ... where S(c) sorts chunk c's keys
+// (K4) and gathers its rows (t_begin, t_end, entry ids, query ordinal); the
+// host enqueues S(c) and K1(c+1) as soon as K1(c)'s count arrives (a gap of
+// one host round trip per chunk), the copy stream moves chunk c's rows over
+// PCIe while K1(c+1) computes, and host threads expand the query ids of
+// finished chunks.
+// The rows land in their final place in one pinned block sized by the
+// buffer capacity; the result equals the single-launch path's (batch order
+// is chunk order, engine.py:176-195).  On overflow of the buffer it returns
+// nullptr and the caller falls back to the exact-sizing path.
+static const int64_t kPipeMinRows = int64_t(1) << 20;
+static const int kPipeMinChunks = 4, kPipeMaxChunks = 16;
+
+// Counter snapshot straight into mapped host memory: a copy-engine read
+// would queue behind the chunk copies already crossing PCIe.
+__global__ void k_snap(const unsigned long long *__restrict__ ctr, unsigned long long *host) {
+    host[0] = ctr[1];
+    host[1] = ctr[2];
+    __threadfence_system();
+}
+
+static void sort_rows(tsk_db *db, const uint64_t *keys, uint64_t *ko, uint32_t *v0, uint32_t *v1, int64_t n,
+                      int end_bit, cudaStream_t st, int64_t &launches) {
+    if (n <= K4_SMALL) {
+        k_small_sort<<<1, 1024, 0, st>>>((int)n, keys, ko, v1);
+        TSK_CUDA(cudaGetLastError());
+        ++launches;
+        return;
+    }
+    const int gi = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    k_iota<<<gi, 256, 0, st>>>(n, v0);
+    TSK_CUDA(cudaGetLastError());
+    ++launches;
+    if (end_bit == 0) end_bit = 1;
+    size_t tb = 0;
+    TSK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, ko, v0, v1, n, 0, end_bit, st));
+    db->cub_tmp.reserve(tb, st);
+    TSK_CUDA(cub::DeviceRadixSort::SortPairs(db->cub_tmp.p, tb, keys, ko, v0, v1, n, 0, end_bit, st));
+}
+
+static tsk_result *run_pipelined(tsk_db *db, const tsk_columns *qc, const SearchPlanDev &plan, K1Launch L,
+                                 int slots, int stride, int pair, int align, int major_bits, int minor_bits, int bb,
+                                 uint64_t cap, Trace &tr, int64_t &launches) {
+    const int64_t nb = plan.nb;
+    // chunks: worth it once the rows' PCIe time is noticeable (the previous
+    // call's hit count predicts this one's); ~2^20 rows per chunk, 4..16
+    int C = 0;
+    if (db->last_hits >= kPipeMinRows)
+        C = (int)std::min<int64_t>(kPipeMaxChunks, std::max<int64_t>(kPipeMinChunks, db->last_hits >> 20));
+    if (const char *e = getenv("TSK_PIPE_CHUNKS")) C = std::max(0, atoi(e));  // testing: 0 = off
+    if (C == 0) return nullptr;
+    C = (int)std::max<int64_t>(1, std::min<int64_t>(C, nb / 2));
+    // the host block holds `cap` rows: not when cap is far above recent results
+    if ((double)cap > 8.0 * (double)std::max<int64_t>(db->last_hits, int64_t(1) << 20)) return nullptr;
+    cudaStream_t st = db->stream;
+    if (!db->stream2) TSK_CUDA(cudaStreamCreateWithFlags(&db->stream2, cudaStreamNonBlocking));
+    cudaStream_t st2 = db->stream2;
+
+    // boundaries at even batch ordinals with about equal interactions each,
+    // from the batches' candidate spans (K3 has run: one small read-back)
+    std::vector<int64_t> B((size_t)C + 1);
+    {
+        size_t sg = 0;
+        int64_t *h_fl = static_cast<int64_t *>(pin_alloc((size_t)nb * 16, &sg));
+        TSK_CUDA(cudaMemcpyAsync(h_fl, plan.first, (size_t)nb * 16, cudaMemcpyDeviceToHost, st));  // first[], last[]
+        std::vector<int64_t> blo((size_t)nb), bhi((size_t)nb);
+        TSK_CUDA(cudaMemcpyAsync(blo.data(), plan.lo, (size_t)nb * 8, cudaMemcpyDeviceToHost, st));
+        TSK_CUDA(cudaMemcpyAsync(bhi.data(), plan.hi, (size_t)nb * 8, cudaMemcpyDeviceToHost, st));
+        TSK_CUDA(cudaStreamSynchronize(st));
+        std::vector<double> pre((size_t)nb + 1, 0.0);
+        for (int64_t b = 0; b < nb; ++b) {
+            const int64_t f = h_fl[b], l = h_fl[nb + b];
+            const double w = f >= 0 ? (double)(l - f + 1) * (double)(bhi[b] - blo[b] + 1) : 0.0;
+            pre[b + 1] = pre[b] + w;
+        }
+        pin_free(h_fl, sg);
+        B[0] = 0;
+        for (int c = 1; c < C; ++c) {
+            const double target = pre[nb] * c / C;
+            int64_t b = std::lower_bound(pre.begin(), pre.end(), target) - pre.begin();
+            b &= ~int64_t(1);
+            B[c] = std::max(B[c - 1], std::min(b, nb));
+        }
+        B[C] = nb;
+    }
+    std::vector<SearchPlanDev> pc((size_t)C);
+    size_t words = 0;
+    for (int c = 0; c < C; ++c) words += (size_t)plan_units(B[c + 1] - B[c]) + 5;
+    db->pipe.reserve(words * 8, st);
+    int64_t *pp = db->pipe.as<int64_t>();
+    for (int c = 0; c < C; ++c) {
+        const int64_t b0 = B[c], nbc = B[c + 1] - b0, nu = plan_units(nbc);
+        pc[c] = SearchPlanDev{nbc, plan.lo + b0, plan.hi + b0, plan.first + b0, plan.last + b0, pp, pp + nu + 1,
+                              plan.ovl + b0, plan.hits + b0};
+        pp += nu + 5;
+    }
+    // device buffers sized by the capacity
+    L.cap = cap;
+    L.keys = db->recs.as<uint64_t>();
+    L.tbeg = reinterpret_cast<double *>(L.keys + cap);
+    L.tend = L.tbeg + cap;
+    db->sorted.reserve((size_t)cap * 24 + 64, st);
+    uint64_t *ko = db->sorted.as<uint64_t>();
+    uint32_t *v0 = reinterpret_cast<uint32_t *>(ko + cap), *v1 = v0 + cap;
+    db->out_cols.reserve((size_t)cap * 36 + 64, st);
+    double *d_tb = db->out_cols.as<double>(), *d_te = d_tb + cap;
+    int64_t *d_et = reinterpret_cast<int64_t *>(d_te + cap), *d_es = d_et + cap;
+    uint32_t *d_qo = reinterpret_cast<uint32_t *>(d_es + cap);
+    unsigned long long *d_ctr = L.item_counter;  // [0] items, [1] hits, [2] evaluated pairs
+    TSK_CUDA(cudaMemsetAsync(d_ctr, 0, 24, st));
+    TSK_CUDA(cudaMemsetAsync(plan.ovl, 0, (size_t)nb * 16, st));  // ovl[nb] then hits[nb]
+    // pinned: counter snapshots, the result block (cap rows), query ordinals
+    size_t sgot = 0, hgot = 0, qgot = 0;
+    unsigned long long *snap = static_cast<unsigned long long *>(pin_alloc((size_t)C * 16, &sgot));
+    unsigned long long *snap_dev = nullptr;
+    TSK_CUDA(cudaHostGetDevicePointer((void **)&snap_dev, snap, 0));
+    char *hb = static_cast<char *>(pin_alloc((size_t)cap * 48, &hgot));
+    // query ordinals (and 32-bit entry ids when they fit), widened on the
+    // host.  Beyond ~2^23 rows the host's memory bandwidth, not PCIe, bounds
+    // the call (the widening adds 20 B/row of host traffic to save 8 B/row
+    // of PCIe): c3 d = 30, 8.4e7 rows, 68 ms at 36 B/row vs 73 ms at 28
+    const int ids32 = db->ids32 && db->last_hits < (int64_t(1) << 23);
+    uint32_t *h_qo = static_cast<uint32_t *>(pin_alloc((size_t)cap * (ids32 ? 12 : 4), &qgot));
+    int32_t *h_et32 = reinterpret_cast<int32_t *>(h_qo + cap), *h_es32 = h_et32 + cap;
+    const size_t cs = (size_t)cap * 8;
+    int64_t *o_qt = (int64_t *)(hb + 0 * cs), *o_qs = (int64_t *)(hb + 1 * cs);
+    int64_t *o_et = (int64_t *)(hb + 2 * cs), *o_es = (int64_t *)(hb + 3 * cs);
+    double *o_tb = (double *)(hb + 4 * cs), *o_te = (double *)(hb + 5 * cs);
+
+    std::vector<cudaEvent_t> ek0((size_t)C), ek1((size_t)C), eks((size_t)C), evd((size_t)C);
+    for (int c = 0; c < C; ++c) {
+        TSK_CUDA(cudaEventCreate(&ek0[c]));
+        TSK_CUDA(cudaEventCreate(&ek1[c]));
+        // spin on the count (a blocking wait adds ~0.2 ms of wake-up per chunk)
+        TSK_CUDA(cudaEventCreateWithFlags(&eks[c], cudaEventDisableTiming));
+        TSK_CUDA(cudaEventCreateWithFlags(&evd[c], cudaEventBlockingSync));
+    }
+    const bool trace = getenv("TSK_TRACE") != nullptr;
+    std::vector<cudaEvent_t> esd((size_t)C, nullptr);  // (trace) end of S(c)
+    std::vector<double> h_seen((size_t)C, 0.0);          // (trace) host saw K1(c)'s count, ms after start
+    const auto h_start = std::chrono::steady_clock::now();
+    auto cleanup = [&]() {
+        for (int c = 0; c < C; ++c) {
+            cudaEventDestroy(ek0[c]);
+            cudaEventDestroy(ek1[c]);
+            cudaEventDestroy(eks[c]);
+            cudaEventDestroy(evd[c]);
+            if (esd[c]) cudaEventDestroy(esd[c]);
+        }
+        pin_free(snap, sgot);
+        pin_free(h_qo, qgot);
+    };
+    auto enqueue_k1 = [&](int c) {
+        launch_plan_items(pc[c], slots, stride, pair, align, st);
+        ++launches;
+        TSK_CUDA(cudaMemsetAsync(d_ctr, 0, 8, st));  // the item counter
+        if (L.ext_count) {
+            launch_count_overlaps_ext(pc[c], db->q, db->s, L.q_unsorted, L.q_cmax_bits, L.db_cmax, L.d2, st);
+            ++launches;
+        }
+        K1Launch Lc = L;
+        Lc.plan = pc[c];
+        TSK_CUDA(cudaEventRecord(ek0[c], st));
+        launch_k1(Lc, slots, st);
+        ++launches;
+        TSK_CUDA(cudaEventRecord(ek1[c], st));
+        k_snap<<<1, 1, 0, st>>>(d_ctr, snap_dev + 2 * c);
+        TSK_CUDA(cudaGetLastError());
+        TSK_CUDA(cudaEventRecord(eks[c], st));
+    };
+    tr.mark("ranges");
+    std::vector<int64_t> start((size_t)C + 1, 0);
+    std::vector<char> copied((size_t)C, 0);
+    const int64_t *qt = qc->traj, *qs = qc->seg;
+    HostPool &pool = HostPool::get();
+    // the query-id expansion runs on its own thread (with the host pool) so
+    // the driving thread answers each chunk's count at once
+    std::mutex xmu;
+    std::condition_variable xcv;
+    int x_ready = 0;  // chunks handed to the expander
+    bool x_stop = false;
+    std::thread expander([&] {
+        int c = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(xmu);
+                xcv.wait(lk, [&] { return c < x_ready || x_stop; });
+                if (c >= x_ready) return;
+            }
+            if (copied[c]) {
+                cudaEventSynchronize(evd[c]);
+                const int64_t r0 = start[c], r1 = start[c + 1];
+                pool.run([&](int part, int parts) {
+                    const int64_t a = r0 + (r1 - r0) * part / parts, z = r0 + (r1 - r0) * (part + 1) / parts;
+                    for (int64_t i = a; i < z; ++i) {
+                        const uint32_t q = h_qo[i];
+                        o_qt[i] = qt[q];
+                        o_qs[i] = qs[q];
+                    }
+                    if (ids32)
+                        for (int64_t i = a; i < z; ++i) {
+                            o_et[i] = h_et32[i];
+                            o_es[i] = h_es32[i];
+                        }
+                });
+            }
+            ++c;
+        }
+    });
+    auto hand_over = [&](int upto) {
+        std::lock_guard<std::mutex> g(xmu);
+        x_ready = upto;
+        xcv.notify_one();
+    };
+    auto finish_expander = [&]() {
+        {
+            std::lock_guard<std::mutex> g(xmu);
+            x_stop = true;
+            xcv.notify_one();
+        }
+        expander.join();
+    };
+    const int end_bit = bb + major_bits + minor_bits;
+    enqueue_k1(0);
+    bool overflow = false;
+    for (int c = 0; c < C; ++c) {
+        TSK_CUDA(cudaEventSynchronize(eks[c]));
+        h_seen[c] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h_start).count();
+        const unsigned long long end = snap[2 * c];
+        if (end > cap || end >= (1ull << 32)) {
+            overflow = true;
+            break;
+        }
+        start[c + 1] = (int64_t)end;
+        const int64_t s0 = start[c], n = (int64_t)end - s0;
+        if (n > 0) {
+            sort_rows(db, L.keys + s0, ko + s0, v0 + s0, v1 + s0, n, end_bit, st, launches);
+            const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+            k_compact<<<grid, 256, 0, st>>>(0, n, ko + s0, v1 + s0, L.tbeg + s0, L.tend + s0, plan.lo + B[c],
+                                            plan.first + B[c], major_bits, minor_bits, db->s.traj, db->s.seg,
+                                            d_tb + s0, d_te + s0,
+                                            // 32-bit ids: int32 arrays at the same element offset
+                                            ids32 ? reinterpret_cast<int64_t *>(reinterpret_cast<int32_t *>(d_et) + s0)
+                                                  : d_et + s0,
+                                            ids32 ? reinterpret_cast<int64_t *>(reinterpret_cast<int32_t *>(d_es) + s0)
+                                                  : d_es + s0,
+                                            d_qo + s0, ids32);
+            TSK_CUDA(cudaGetLastError());
+            ++launches;
+            cudaEvent_t eg;
+            TSK_CUDA(cudaEventCreateWithFlags(&eg, cudaEventDisableTiming));
+            TSK_CUDA(cudaEventRecord(eg, st));
+            if (trace) {
+                TSK_CUDA(cudaEventCreate(&esd[c]));
+                TSK_CUDA(cudaEventRecord(esd[c], st));
+            }
+            TSK_CUDA(cudaStreamWaitEvent(st2, eg, 0));
+            TSK_CUDA(cudaEventDestroy(eg));  // destruction is deferred until the event completes
+            TSK_CUDA(cudaMemcpyAsync(o_tb + s0, d_tb + s0, (size_t)n * 8, cudaMemcpyDeviceToHost, st2));
+            TSK_CUDA(cudaMemcpyAsync(o_te + s0, d_te + s0, (size_t)n * 8, cudaMemcpyDeviceToHost, st2));
+            if (ids32) {
+                TSK_CUDA(cudaMemcpyAsync(h_et32 + s0, reinterpret_cast<int32_t *>(d_et) + s0, (size_t)n * 4,
+                                         cudaMemcpyDeviceToHost, st2));
+                TSK_CUDA(cudaMemcpyAsync(h_es32 + s0, reinterpret_cast<int32_t *>(d_es) + s0, (size_t)n * 4,
+                                         cudaMemcpyDeviceToHost, st2));
+            } else {
+                TSK_CUDA(cudaMemcpyAsync(o_et + s0, d_et + s0, (size_t)n * 8, cudaMemcpyDeviceToHost, st2));
+                TSK_CUDA(cudaMemcpyAsync(o_es + s0, d_es + s0, (size_t)n * 8, cudaMemcpyDeviceToHost, st2));
+            }
+            TSK_CUDA(cudaMemcpyAsync(h_qo + s0, d_qo + s0, (size_t)n * 4, cudaMemcpyDeviceToHost, st2));
+            TSK_CUDA(cudaEventRecord(evd[c], st2));
+            copied[c] = 1;
+        }
+        if (c + 1 < C) enqueue_k1(c + 1);
+        hand_over(c + 1);
+    }
+    if (overflow) {
+        hand_over(0);
+        finish_expander();
+        TSK_CUDA(cudaStreamSynchronize(st));
+        TSK_CUDA(cudaStreamSynchronize(st2));
+        cleanup();
+        pin_free(hb, hgot);
+        return nullptr;
+    }
+    tr.mark("pipeline");
+    finish_expander();
+    const int64_t nh = start[C];
+    tsk_result *res = new tsk_result();
+    res->n = nh;
+    res->nb = nb;
+    res->k1_evals = (int64_t)snap[2 * (C - 1) + 1];
+    float k1_ms = 0.f;
+    for (int c = 0; c < C; ++c) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ek0[c], ek1[c]);
+        k1_ms += ms;
+    }
+    res->k1_ms = k1_ms;
+    size_t pb_got = 0;
+    const size_t nbz = (size_t)nb;
+    res->pb_host = static_cast<int64_t *>(pin_alloc(nbz * 4 * 8, &pb_got));
+    res->pb_bytes = pb_got;
+    TSK_CUDA(cudaMemcpyAsync(res->pb_host, plan.first, nbz * 16, cudaMemcpyDeviceToHost, st));
+    TSK_CUDA(cudaMemcpyAsync(res->pb_host + 2 * nbz, plan.ovl, nbz * 16, cudaMemcpyDeviceToHost, st));
+    res->host = hb;
+    res->host_bytes = hgot;
+    res->qtraj = o_qt;
+    res->qseg = o_qs;
+    res->etraj = o_et;
+    res->eseg = o_es;
+    res->tbeg = o_tb;
+    res->tend = o_te;
+    for (int c = C - 1; c >= 0; --c)
+        if (copied[c]) {
+            TSK_CUDA(cudaStreamWaitEvent(st, evd[c], 0));
+            break;
+        }
+    TSK_CUDA(cudaEventRecord(db->ev1, st));
+    TSK_CUDA(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, db->ev0, db->ev1);
+    res->device_ms = ms;
+    res->launches = launches;
+    db->last_hits = nh;
+    if (trace) {
+        auto at = [&](cudaEvent_t e) {
+            float t = -1.f;
+            if (e) cudaEventElapsedTime(&t, db->ev0, e);
+            return t;
+        };
+        fprintf(stderr, "[tsk trace] pipeline %d chunks, %lld rows (ms from start: K1 begin-end / host saw / S end / D2H end):", C,
+                (long long)nh);
+        for (int c = 0; c < C; ++c)
+            fprintf(stderr, " [%.2f-%.2f / %.2f / %.2f / %.2f]", at(ek0[c]), at(ek1[c]), h_seen[c], at(esd[c]),
+                    copied[c] ? at(evd[c]) : -1.f);
+        fprintf(stderr, "\n");
+    }
+    cleanup();
+    return res;
 }
 
 static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int64_t *b_lo,
@@ -466,9 +822,8 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     const char *sp_env = getenv("TSK_SPATIAL");
     const bool use_k = !spans_given && db->k.built;
     const int cull = (use_k && !(sp_env && !strcmp(sp_env, "nocull"))) ? 1 : 0;
-    launch_plan_items(plan, slots, K1_THREADS * k1_candidates_per_thread(k1_f32), pair, cull ? BOX_GROUP : 1, st);
-    launches += spans_given ? 1 : 2;
-    tr.mark("ranges+items");
+    const int k1_stride = K1_THREADS * k1_candidates_per_thread(k1_f32), k1_align = cull ? BOX_GROUP : 1;
+    launches += spans_given ? 0 : 1;
 
     db->counters.reserve(64, st);
     unsigned long long *d_ctr = db->counters.as<unsigned long long>();  // [0] items [1] hits; int[8] = q unsorted
@@ -508,6 +863,20 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     // counts only: no hit rows are written (cap 0), so no regrow and no K4
     const bool count_only = flags & (TSK_COUNT_ONLY | TSK_OVERLAPS_ONLY);
     L.q_unsorted = db->counters.as<int>() + 8;
+    // reference-ordered results through the compact path: K1 chunk by chunk,
+    // each chunk's rows sorted, gathered and copied while later chunks run
+    const bool on_device_early = flags & TSK_RESULTS_ON_DEVICE;
+    if (!count_only && !L.noop && ordered && !query_major && !canonical && !(flags & TSK_WANT_ORDINALS) &&
+        !on_device_early && qc->traj && qc->seg && nq <= 0xffffffffll) {
+        tsk_result *pres = run_pipelined(db, qc, plan, L, slots, k1_stride, pair, k1_align, major_bits, minor_bits,
+                                         bb, cap, tr, launches);
+        if (pres) return pres;
+        // a chunk overflowed the result buffer: the plain path below sizes it
+        // exactly (and the next call's pipeline fits)
+    }
+    launch_plan_items(plan, slots, k1_stride, pair, k1_align, st);
+    ++launches;
+    tr.mark("ranges+items");
     unsigned long long h_ctr[2] = {0, 0};  // hits, evaluated pairs
     unsigned long long &h_hits = h_ctr[0];
     float k1_ms = 0.f;
@@ -540,6 +909,7 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     }
     TSK_REQUIRE(count_only || h_hits < (1ull << 32), "more than 2^32 hits in one call");
     const int64_t nh = count_only ? 0 : (int64_t)h_hits;
+    if (!count_only) db->last_hits = nh;
 
     tsk_result *res = new tsk_result();
     res->n = nh;

@@ -146,6 +146,9 @@ struct tsk_db {
     tsk::K1Layout k;  // spatially ordered copy for K1 (built with the index)
     // search workspace (grow-only)
     tsk::DBuf q_rec, batches, counters, recs, sorted, cub_tmp, out_cols, canon_cols, canon_tmp;
+    tsk::DBuf pipe;         // per-chunk item tables of the pipelined search
+    int64_t last_hits = 0;  // hits of the previous search (sizes the pipeline's host block)
+    int ids32 = 0;          // every entry id fits in int32 (4-byte ids over PCIe)
     tsk::Soa q;  // device copy of the current query set
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_k0 = nullptr, ev_k1 = nullptr;
     cudaStream_t stream2 = nullptr;  // result copies of the compact pipeline
@@ -345,6 +348,7 @@ bool mapped_columns(const tsk_columns *c, tsk_columns *dev);
 void launch_qprep_mapped(const tsk_columns &dev_cols, Soa &q, QRec *out, int *flags, unsigned long long *cmax_bits,
                          cudaStream_t st);
 double soa_cmax(const Soa &s, cudaStream_t st);
+int soa_ids32(const Soa &s, cudaStream_t st);
 void soa_group_bounds(Soa &s, cudaStream_t st);  // GBound per GB_SIZE segments
 void launch_k1(const K1Launch &L, int grid, cudaStream_t st);
 void build_k1_layout(tsk_db *db, cudaStream_t st);  // layout.cu

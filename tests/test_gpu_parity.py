@@ -411,6 +411,57 @@ def test_result_buffer_overflow_regrows():
     _same(res, want)
 
 
+@pytest.mark.parametrize("chunks", ["0", "1", "2", "3", "7"])
+def test_pipelined_search_equals_single_launch(chunks, monkeypatch):
+    """run_search cuts the plan into chunks whose K1 launches overlap the
+    previous chunks' sort, gather and D2H (TSK_PIPE_CHUNKS: 0 = the single
+    launch path).  Rows, order and statistics are identical for any chunk
+    count, including an overflow of the result buffer mid-pipeline (a fresh
+    store's 2^20-row buffer against ~1.7e6 hits) and batches without hits."""
+    rng = np.random.default_rng(17)
+    store = _store(random_store_arrays(rng, 4000))
+    q = _store(random_store_arrays(rng, 1300, first_traj=10**6))
+    ix = tsk.build_index(store, 64)
+    plan = tsk.periodic(q, 50, ix)
+    monkeypatch.setenv("TSK_PIPE_CHUNKS", "0")
+    base, bst = tsk.run_search(store, ix, plan, 4.0)
+    big, gst = tsk.run_search(store, ix, plan, 40.0)
+    monkeypatch.setenv("TSK_PIPE_CHUNKS", chunks)
+    fresh = _store(random_store_arrays(np.random.default_rng(17), 4000))  # new device buffers
+    fix = tsk.build_index(fresh, 64)
+    for st_, ix_, d, want, wst in ((fresh, fix, 40.0, big, gst), (fresh, fix, 4.0, base, bst),
+                                    (store, ix, 4.0, base, bst), (store, ix, 40.0, big, gst)):
+        res, st = tsk.run_search(st_, ix_, plan, d)
+        for k in RES:
+            assert np.array_equal(getattr(res, k), getattr(want, k)), (chunks, d, k)
+        assert (st.interactions_computed, st.temporal_misses, st.spatial_misses, st.hits) == \
+            (wst.interactions_computed, wst.temporal_misses, wst.spatial_misses, wst.hits)
+        assert [t.hits for t in st.per_batch] == [t.hits for t in wst.per_batch]
+    assert gst.hits > (1 << 20)
+
+
+@pytest.mark.parametrize("first_traj", [0, 2**40, -(2**35)])
+def test_pipelined_search_entry_id_widths(first_traj, monkeypatch):
+    """Entry ids that fit in int32 cross PCIe as 4 bytes and are widened on
+    the host; wider (or negative wide) ids go as 8 bytes.  Both through the
+    pipeline (several chunks, > 2^20 rows) equal the single-launch path."""
+    rng = np.random.default_rng(23)
+    arr = random_store_arrays(rng, 3000, first_traj=first_traj)
+    arr["seg"] = np.arange(3000, dtype=np.int64) * (1 if first_traj >= 0 else -7)
+    store = _store(arr)
+    q = _store(random_store_arrays(rng, 1100, first_traj=10**6))
+    ix = tsk.build_index(store, 64)
+    plan = tsk.periodic(q, 60, ix)
+    monkeypatch.setenv("TSK_PIPE_CHUNKS", "0")
+    want, wst = tsk.run_search(store, ix, plan, 40.0)
+    monkeypatch.setenv("TSK_PIPE_CHUNKS", "5")
+    for _ in range(2):  # the second call pipelines inside the grown buffer
+        res, st = tsk.run_search(store, ix, plan, 40.0)
+        for k in RES:
+            assert np.array_equal(getattr(res, k), getattr(want, k)), k
+    assert st.hits == wst.hits > 500_000
+
+
 def test_batches_without_candidates_and_large_batches():
     entries = _store(random_store_arrays(np.random.default_rng(7), 500))
     ix = tsk.build_index(entries, 50)
