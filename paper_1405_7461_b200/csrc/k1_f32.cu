@@ -35,6 +35,9 @@
 #ifndef K1F_CPT
 #define K1F_CPT 4
 #endif
+#ifndef K1_EARLY
+#define K1_EARLY 0  // measured: no gain (more spills)
+#endif
 #ifndef K1F_MIN_BLOCKS
 #define K1F_MIN_BLOCKS 3
 #endif
@@ -529,35 +532,73 @@ __device__ __forceinline__ void warp_box(const K1Launch &L, int64_t wbase, int64
     }
 }
 
-// Two of a lane's candidates (k0, k0 + 1) in FP32 pre-filter form, staged
-// in shared memory: every global load is issued before any conversion (one
-// round trip); lanes past the item's range stage a far-away point.
-__device__ __forceinline__ void stage_pair(const K1Launch &L, int64_t wbase, int64_t c_lo, int64_t c_hi, int k0,
-                                           const F32Item &fi, float *wcs, int lane) {
+// Two of a lane's candidates (k0, k0 + 1): their raw columns in registers
+// (every global load issued before any use), then their FP32 pre-filter
+// form staged in shared memory; lanes past the item's range stage a
+// far-away point.
+struct RawPair {
     double ts[2], sx[2], sy[2], sz[2], vx[2], vy[2], vz[2];
     float sr[2];
     bool ok[2];
+};
+
+__device__ __forceinline__ void load_pair(const K1Launch &L, int64_t wbase, int64_t c_lo, int64_t c_hi, int k0,
+                                          int lane, RawPair &r) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const int64_t e = wbase + (k0 + h) * 32 + lane;
-        ok[h] = e >= c_lo && e <= c_hi;
-        const int64_t ec = ok[h] ? e : c_lo;  // loads stay unconditional
-        ts[h] = L.e.ts[ec];
-        sx[h] = L.e.sx[ec]; sy[h] = L.e.sy[ec]; sz[h] = L.e.sz[ec];
-        vx[h] = L.e.vx[ec]; vy[h] = L.e.vy[ec]; vz[h] = L.e.vz[ec];
-        sr[h] = L.e.sr32[ec];
+        r.ok[h] = e >= c_lo && e <= c_hi;
+        const int64_t ec = r.ok[h] ? e : c_lo;  // loads stay unconditional
+        r.ts[h] = L.e.ts[ec];
+        r.sx[h] = L.e.sx[ec]; r.sy[h] = L.e.sy[ec]; r.sz[h] = L.e.sz[ec];
+        r.vx[h] = L.e.vx[ec]; r.vy[h] = L.e.vy[ec]; r.vz[h] = L.e.vz[ec];
+        r.sr[h] = L.e.sr32[ec];
     }
+}
+
+__device__ __forceinline__ void store_pair(const RawPair &r, int k0, const F32Item &fi, float *wcs, int lane) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const int i = (k0 + h) * 32 + lane;
         CandF32 c;
         c.px = c.py = c.pz = 0x1p60f;
         c.vx = c.vy = c.vz = c.sr = 0.f;
-        if (ok[h]) c = f32_cand_sr(ts[h], sx[h], sy[h], sz[h], vx[h], vy[h], vz[h], sr[h], fi);
+        if (r.ok[h]) c = f32_cand_sr(r.ts[h], r.sx[h], r.sy[h], r.sz[h], r.vx[h], r.vy[h], r.vz[h], r.sr[h], fi);
         wcs[0 * WCAND + i] = c.px; wcs[1 * WCAND + i] = c.py; wcs[2 * WCAND + i] = c.pz;
         wcs[3 * WCAND + i] = c.vx; wcs[4 * WCAND + i] = c.vy; wcs[5 * WCAND + i] = c.vz;
         wcs[6 * WCAND + i] = c.sr;
     }
+}
+
+__device__ __forceinline__ void stage_pair(const K1Launch &L, int64_t wbase, int64_t c_lo, int64_t c_hi, int k0,
+                                           const F32Item &fi, float *wcs, int lane) {
+    RawPair r;
+    load_pair(L, wbase, c_lo, c_hi, k0, lane, r);
+    store_pair(r, k0, fi, wcs, lane);
+}
+
+// jlo = #{j < nt : pm[j] < x} (pm ascending) and jhi = #{j < nt : sm[j] <= y}
+// (sm ascending), both arrays +inf padded to 2 K1_TQ >= 256: two 16-ary
+// rounds, lanes 0-15 on pm and 16-31 on sm (a shared load, a ballot and a
+// popcount each) instead of two serial 9-step bisections.
+static_assert(K1_TQ <= 256, "window_bounds covers 256 queries");
+__device__ __forceinline__ void window_bounds(const double *pm, const double *sm, int nt, double x, double y, int lane,
+                                              int &jlo, int &jhi) {
+    const int l = lane & 15;
+    const bool lo_half = lane < 16;
+    const double *a = lo_half ? pm : sm;
+    // round 1: block l of 16 entries ends at 16 l + 15
+    const double v1 = a[16 * l + 15];
+    const unsigned m1 = __ballot_sync(0xffffffffu, lo_half ? v1 < x : v1 <= y);
+    const int c_lo = __popc(m1 & 0xffffu), c_hi = __popc(m1 >> 16);
+    // round 2: inside the first block not entirely below the bound
+    const int base = 16 * (lo_half ? c_lo : c_hi);
+    const double v2 = base + l < 2 * K1_TQ ? a[base + l] : INFINITY;
+    const unsigned m2 = __ballot_sync(0xffffffffu, lo_half ? v2 < x : v2 <= y);
+    const int r_lo = 16 * c_lo + (c_lo < 16 ? __popc(m2 & 0xffffu) : 0);
+    const int r_hi = 16 * c_hi + (c_hi < 16 ? __popc(m2 >> 16) : 0);
+    jlo = r_lo < nt ? r_lo : nt;
+    jhi = r_hi < nt ? r_hi : nt;
 }
 
 // Item-level key bases of the K1 layout (hits add their own orig - f).
@@ -577,7 +618,13 @@ __device__ __noinline__ void fast_subtile(const K1Launch &L, const ItemCtx &it, 
                                           int warp, int lane, unsigned long long &n_ev, unsigned long long &n_hit) {
     const int64_t g0 = wbase / BOX_GROUP;
     const int64_t g1 = (wbase + WCAND - 1 < it.c_hi ? wbase + WCAND - 1 : it.c_hi) / BOX_GROUP;
-    // the groups' time range and box, loaded together
+    // the groups' time range and box, loaded together, and (speculatively:
+    // nearly every sub-tile has a query near its box) the first candidates'
+    // columns, whose latency then hides behind the window search and cull
+    RawPair r0;
+#if K1_EARLY
+    load_pair(L, wbase, it.c_lo, it.c_hi, 0, lane, r0);
+#endif
     double2 tr = L.gtime[g0];
     float4 blo, bhi;
     bool unsafe_g;
@@ -589,11 +636,8 @@ __device__ __noinline__ void fast_subtile(const K1Launch &L, const ItemCtx &it, 
     }
     // window [jlo, jhi): te_j >= min ts (pm: te ascending) and ts_j <= max te
     // (sm: ts ascending); both arrays are +inf padded to 2 * K1_TQ
-    int v = 0;
-    if (lane == 0) v = lower_bound_pm(pm, it.nt, tr.x);
-    else if (lane == 1) v = upper_bound_arr(sm, it.nt, tr.y);
-    const int jlo = __shfl_sync(0xffffffffu, v, 0);
-    int jhi = __shfl_sync(0xffffffffu, v, 1);
+    int jlo, jhi;
+    window_bounds(pm, sm, it.nt, tr.x, tr.y, lane, jlo, jhi);
     if (jhi < jlo) jhi = jlo;
     const int ns = box_cull(blo, bhi, jlo, jhi, cull_rb, warp, lane);
     K1_STAT(0, 1);
@@ -652,8 +696,15 @@ __device__ __noinline__ void fast_subtile(const K1Launch &L, const ItemCtx &it, 
         return;
     }
     n_ev += (unsigned long long)ns * (unsigned long long)k1_wctx[warp].nvalid;
-#pragma unroll
-    for (int k = 0; k < CPT; k += 2) stage_pair(L, wbase, it.c_lo, it.c_hi, k, fi, wcs, lane);
+    {
+#if !K1_EARLY
+        load_pair(L, wbase, it.c_lo, it.c_hi, 0, lane, r0);
+#endif
+        RawPair r1;
+        load_pair(L, wbase, it.c_lo, it.c_hi, 2, lane, r1);
+        store_pair(r0, 0, fi, wcs, lane);
+        store_pair(r1, 2, fi, wcs, lane);
+    }
     __syncwarp();
     f32_list_range(qt, sqf, ns, warp, lane, n_hit);
 }

@@ -10,7 +10,7 @@ c, rc = sys.argv[1], sys.argv[2]
 try:
     l = json.load(open(f"gpurun_out/{__import__('os').environ.get('TAG','q')}/bench_{c}.json"))
     r = l["roofline"]; p = l.get("parity") or {}
-    print(f"{c} rc={rc} value {l['value']:.3e} e2e {l['e2e']['value']:.3e} resp {l['response_time_s']*1e3:.2f}ms k1 {r['k1_ms_per_step']:.2f}ms evals {r['evaluated_pairs_per_step']:.3e} parity {p.get('mismatches')}/{p.get('batches')}")
+    print(f"{c} rc={rc} value {l['value']:.3e} e2e {l['e2e']['value']:.3e} resp {l['response_time_s']*1e3:.2f}ms k1 {r['k1_ms_per_step']:.2f}ms frac {r['frac']:.3f} evals {r['fp32_prefilter']['evaluated_pairs_per_step']:.3e} parity {p.get('mismatches')}/{p.get('batches')}")
 except Exception as e:
     print(c, "rc", rc, "no line", e)
 PY
