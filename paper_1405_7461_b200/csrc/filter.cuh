@@ -216,11 +216,13 @@ inline float tsk_f2f_ru(double x) {
 
 // Item bounds (see above): ar = A_r, tvr = TV_r, vr = V_r, aq = A_q,
 // tq = T_q, eq = max ext_q, cmax = max |coordinate| of the launch.
+// tr = max |r.ts - T0| of the candidates (the K1 layout's group origins
+// are candidates' starts: their FP32 records are re-based per item).
 TSK_HD F32Item f32_item(double ox, double oy, double oz, double t0, double ar, double tvr, double vr,
-                        double aq, double tq, double eq, double cmax) {
+                        double aq, double tq, double eq, double cmax, double tr = 0.0) {
     F32Item it;
     it.ox = ox; it.oy = oy; it.oz = oz; it.t0 = t0;
-    const double M = ar + tvr + tq * vr + aq;
+    const double M = ar + tvr + tq * vr + aq + tr * vr;
     it.ok = M <= 0x1p60 && vr <= 0x1p60 && eq <= 0x1p60;  // false for NaN
     it.delta = 0x1p-18 * M + 0x1p-38 * cmax + 0x1p-100;
     it.sep_rb = INFINITY;  // no separating-axis rejections until K1 sets it
@@ -257,6 +259,36 @@ TSK_HD CandF32 f32_cand_sr(double ts, double sx, double sy, double sz, double vx
     c.vx = TSK_F2F_RN(vx);
     c.vy = TSK_F2F_RN(vy);
     c.vz = TSK_F2F_RN(vz);
+    c.sr = sr;
+    return c;
+}
+
+// The K1 layout stores every candidate's FP32 view once, relative to its
+// BOX_GROUP's origin (O_g, T_g) = the start of the group's first entry
+// (f32_cand_sr with that origin: pg, v, sr).  An item re-bases it to its own
+// origin (O, T0):
+//   p = RN32(RN32(pg + dO) - dT v),  dO = RN32(O_g - O), dT = RN32(T_g - T0)
+// (one FFMA), for the line (r.s - O) - (r.ts - T0) v_r of the direct form.
+// Error: pg, dO, the sum, dT, v and the FFMA are each rounded once, on
+// magnitudes at most |r.s - O_g| + |r.ts - T_g| V_r, A_r, A_r + |r.ts - T_g|
+// V_r, T_r V_r and A_r + TV_r (O_g is a candidate's start, so |O_g - O| <=
+// A_r and |T_g - T0| <= T_r = max |r.ts - T0|), so |p - p*| <= 16 2^-24 M
+// with M += T_r V_r (f32_item's tr): inside delta = 2^-18 M, which the
+// direct form (7 2^-24 M) left 9x slack for.  tools/filter_check.cpp runs
+// the pre-filter and the separating-axis stage on re-based candidates.
+TSK_HD CandF32 f32_cand_rebase(float pgx, float pgy, float pgz, float vx, float vy, float vz, float sr, float dox,
+                               float doy, float doz, float dt) {
+    CandF32 c;
+#ifdef __CUDA_ARCH__
+    c.px = __fmaf_rn(-dt, vx, __fadd_rn(pgx, dox));
+    c.py = __fmaf_rn(-dt, vy, __fadd_rn(pgy, doy));
+    c.pz = __fmaf_rn(-dt, vz, __fadd_rn(pgz, doz));
+#else
+    c.px = fmaf(-dt, vx, pgx + dox);
+    c.py = fmaf(-dt, vy, pgy + doy);
+    c.pz = fmaf(-dt, vz, pgz + doz);
+#endif
+    c.vx = vx; c.vy = vy; c.vz = vz;
     c.sr = sr;
     return c;
 }
@@ -472,8 +504,9 @@ TSK_HD float f32_r2(float qa, float sr, float qb) {
 // with separation h <= (1 + 2^-11) d + 2^-12 (|U| + |W|) + 2^-40 C (the
 // mu = 2^-24 statement of the box cull), and |U| + |W| <= 3 max(|D(q.ts)|,
 // |D(q.te)|) by convexity.  FP32 error: every value formed is, per
-// component, at most M2 = A_r + TV_r + (T_q + E_q) V_r + A_q + D_q
-// (D_q: max |q.e - q.s| component, E_q: max ext_q) and each of p, v, ts,
+// component, at most M2 = A_r + TV_r + (T_q + E_q + T_r) V_r + A_q + D_q
+// (D_q: max |q.e - q.s| component, E_q: max ext_q; T_r V_r covers the
+// re-based candidate records) and each of p, v, ts,
 // te, s, e_q, the products and sums is rounded once, so u and e are within
 // 2^-19 M2 (Euclidean) of the exact D; the dot products n . u, n . e are
 // within 2^-22 |n| m (m: the larger Euclidean norm of u, e, bounded by

@@ -570,6 +570,37 @@ __device__ __forceinline__ void store_pair(const RawPair &r, int k0, const F32It
     }
 }
 
+// The warp's candidates from the K1 layout's FP32 records (one group: the
+// fast path's sub-tiles are BOX_GROUP-aligned), re-based to the item's
+// origin (filter.cuh f32_cand_rebase): two 16-byte loads per candidate.
+__device__ __forceinline__ void stage_rebased(const K1Launch &L, int64_t wbase, int64_t c_lo, int64_t c_hi,
+                                              const F32Item &fi, float *wcs, int lane) {
+    const double4 go = L.gorig[wbase / BOX_GROUP];
+    float4 a[CPT], b[CPT];
+    bool ok[CPT];
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+        const int64_t e = wbase + k * 32 + lane;
+        ok[k] = e >= c_lo && e <= c_hi;
+        const int64_t ec = ok[k] ? e : c_lo;
+        a[k] = L.frec[2 * ec];
+        b[k] = L.frec[2 * ec + 1];
+    }
+    const float dox = TSK_F2F_RN(go.x - fi.ox), doy = TSK_F2F_RN(go.y - fi.oy), doz = TSK_F2F_RN(go.z - fi.oz);
+    const float dt = TSK_F2F_RN(go.w - fi.t0);
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+        const int i = k * 32 + lane;
+        CandF32 c;
+        c.px = c.py = c.pz = 0x1p60f;
+        c.vx = c.vy = c.vz = c.sr = 0.f;
+        if (ok[k]) c = f32_cand_rebase(a[k].x, a[k].y, a[k].z, b[k].x, b[k].y, b[k].z, a[k].w, dox, doy, doz, dt);
+        wcs[0 * WCAND + i] = c.px; wcs[1 * WCAND + i] = c.py; wcs[2 * WCAND + i] = c.pz;
+        wcs[3 * WCAND + i] = c.vx; wcs[4 * WCAND + i] = c.vy; wcs[5 * WCAND + i] = c.vz;
+        wcs[6 * WCAND + i] = c.sr;
+    }
+}
+
 __device__ __forceinline__ void stage_pair(const K1Launch &L, int64_t wbase, int64_t c_lo, int64_t c_hi, int k0,
                                            const F32Item &fi, float *wcs, int lane) {
     RawPair r;
@@ -696,7 +727,9 @@ __device__ __noinline__ void fast_subtile(const K1Launch &L, const ItemCtx &it, 
         return;
     }
     n_ev += (unsigned long long)ns * (unsigned long long)k1_wctx[warp].nvalid;
-    {
+    if (L.frec && wbase % BOX_GROUP == 0) {
+        stage_rebased(L, wbase, it.c_lo, it.c_hi, fi, wcs, lane);
+    } else {
 #if !K1_EARLY
         load_pair(L, wbase, it.c_lo, it.c_hi, 0, lane, r0);
 #endif
@@ -767,22 +800,26 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
             if (fl) atomicOr(&flags_sh, fl);
             const double ox = qt[0].sx, oy = qt[0].sy, oz = qt[0].sz, t0 = qt[0].ts;
             if (warp == 2) {
-                double ar = 0.0, tvr = 0.0, vr = 0.0;
+                double ar = 0.0, tvr = 0.0, vr = 0.0, trr = 0.0;
                 for (int64_t g = it.first_c / GB_SIZE + lane; g <= it.c_hi / GB_SIZE; g += 32) {
                     const GBound gb = L.e.gb[g];
                     ar = fmax(ar, fmax(fmax(fabs(gb.hi[0] - ox), fabs(ox - gb.lo[0])),
                                        fmax(fmax(fabs(gb.hi[1] - oy), fabs(oy - gb.lo[1])),
                                             fmax(fabs(gb.hi[2] - oz), fabs(oz - gb.lo[2])))));
-                    tvr = fmax(tvr, fmax(fabs(gb.ts_hi - t0), fabs(t0 - gb.ts_lo)) * gb.vmax);
+                    const double tg = fmax(fabs(gb.ts_hi - t0), fabs(t0 - gb.ts_lo));
+                    tvr = fmax(tvr, tg * gb.vmax);
+                    trr = fmax(trr, tg);
                     vr = fmax(vr, gb.vmax);
                 }
                 ar = warp_max(ar);
                 tvr = warp_max(tvr);
                 vr = warp_max(vr);
+                trr = warp_max(trr);
                 if (lane == 0) {
                     f32b[0] = ar;
                     f32b[1] = tvr;
                     f32b[2] = vr;
+                    f32b[7] = trr;
                 }
             } else if (warp == 3) {
                 double aq = 0.0, tq = 0.0, eq = 0.0, dq = 0.0;
@@ -816,10 +853,10 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
         const bool fast = cull && L.ext_count && (*L.q_unsorted & 3) == 0 && single_scan;
         if (tid == 0) {
             fi_sh = f32_item(qt[0].sx, qt[0].sy, qt[0].sz, qt[0].ts, f32b[0], f32b[1], f32b[2], f32b[3], f32b[4],
-                             f32b[5], cmax);
+                             f32b[5], cmax, f32b[7]);
             fi_sh.ok = fi_sh.ok && launch_ok && !unsafe_q;
             // separating-axis stage: M2 = A_r + TV_r + (T_q + E_q) V_r + A_q + D_q
-            const double M2 = f32b[0] + f32b[1] + (f32b[4] + f32b[5]) * f32b[2] + f32b[3] + f32b[6];
+            const double M2 = f32b[0] + f32b[1] + (f32b[4] + f32b[5] + f32b[7]) * f32b[2] + f32b[3] + f32b[6];
             k1_sep_rb = f32_sep_rbase(dthr, cmax, M2);
             if (L.orig) {  // K1 layout: key bases are per item
                 k1_kf[0] = L.plan.first[it.b];

@@ -161,6 +161,20 @@ __global__ void k_group_boxes(int64_t n, Soa s, float4 *__restrict__ box, double
     }
 }
 
+// FP32 pre-filter records relative to each group's origin (the start of its
+// first entry): f32_cand_sr with that origin, stored once per store.
+__global__ void k_f32_records(int64_t n, Soa s, float4 *__restrict__ frec, double4 *__restrict__ gorig) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g0 = (i / BOX_GROUP) * BOX_GROUP;
+        F32Item o;
+        o.ox = s.sx[g0]; o.oy = s.sy[g0]; o.oz = s.sz[g0]; o.t0 = s.ts[g0];
+        const CandF32 c = f32_cand_sr(s.ts[i], s.sx[i], s.sy[i], s.sz[i], s.vx[i], s.vy[i], s.vz[i], s.sr32[i], o);
+        frec[2 * i] = make_float4(c.px, c.py, c.pz, c.sr);
+        frec[2 * i + 1] = make_float4(c.vx, c.vy, c.vz, 0.f);
+        if (i == g0) gorig[i / BOX_GROUP] = make_double4(o.ox, o.oy, o.oz, o.t0);
+    }
+}
+
 // Temporal overlaps per batch without K1 (stores and queries whose start and
 // end times are both non-decreasing): query q overlaps entry e iff
 // e.ts <= q.te and q.ts <= e.te (core.py:490-492), so over a batch's range
@@ -228,6 +242,8 @@ void free_k1_layout(tsk_db *db) {
     k.orig = nullptr;
     k.box = nullptr;
     k.gtime = nullptr;
+    k.frec = nullptr;
+    k.gorig = nullptr;
     k.ngroups = 0;
     k.built = false;
 }
@@ -293,16 +309,22 @@ void build_k1_layout(tsk_db *db, cudaStream_t st) {
     // the reordered columns (no id columns: ids are gathered by start-sorted ordinal)
     soa_alloc(k.s, n, false, st);
     k.ngroups = (n + BOX_GROUP - 1) / BOX_GROUP;
-    k.aux.reserve(nb8 + (size_t)k.ngroups * (2 * sizeof(float4) + sizeof(double2)) + 64, st);
+    k.aux.reserve(nb8 + (size_t)k.ngroups * (2 * sizeof(float4) + sizeof(double2) + sizeof(double4)) +
+                      (size_t)n * 2 * sizeof(float4) + 128,
+                  st);
     k.orig = k.aux.as<int64_t>();
-    k.box = reinterpret_cast<float4 *>(k.aux.as<char>() + ((nb8 + 15) & ~size_t(15)));
+    k.box = reinterpret_cast<float4 *>(k.aux.as<char>() + ((nb8 + 31) & ~size_t(31)));
     k.gtime = reinterpret_cast<double2 *>(k.box + 2 * k.ngroups);
+    k.gorig = reinterpret_cast<double4 *>(k.gtime + k.ngroups + (k.ngroups & 1));  // 32-byte aligned
+    k.frec = reinterpret_cast<float4 *>(k.gorig + k.ngroups);
     k_layout_gather<<<grid, 256, 0, st>>>(n, v1, s, k.s, k.orig);
     TSK_CUDA(cudaGetLastError());
     TSK_CUDA(cudaFreeAsync(v1, st));
     soa_group_bounds(k.s, st);
     const int gg = (int)std::min<int64_t>((k.ngroups * 32 + 255) / 256, 148 * 16);
     k_group_boxes<<<gg, 256, 0, st>>>(n, k.s, k.box, k.gtime);
+    TSK_CUDA(cudaGetLastError());
+    k_f32_records<<<grid, 256, 0, st>>>(n, k.s, k.frec, k.gorig);
     TSK_CUDA(cudaGetLastError());
     k.s.any_unsafe = s.any_unsafe;
     k.s.sorted = 0;

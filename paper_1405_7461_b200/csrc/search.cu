@@ -837,6 +837,8 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     L.orig = use_k ? db->k.orig : nullptr;
     L.gbox = use_k ? db->k.box : nullptr;
     L.gtime = use_k ? db->k.gtime : nullptr;
+    L.frec = use_k && !getenv("TSK_NO_FREC") ? db->k.frec : nullptr;  // TSK_NO_FREC: testing
+    L.gorig = use_k ? db->k.gorig : nullptr;
     L.cull = cull;
     // overlap counts outside K1 (count_overlaps_ext) when the store's end
     // times are sorted too; the kernel itself checks the query flags

@@ -119,6 +119,11 @@ struct K1Layout {
     int64_t *orig = nullptr;
     float4 *box = nullptr;  // 2 per group: (lo.x, lo.y, lo.z, 0), (hi.x, hi.y, hi.z, 0)
     double2 *gtime = nullptr;  // per group: (min ts, max te)
+    // FP32 pre-filter records, 2 float4 per entry: (pgx, pgy, pgz, sr),
+    // (vx, vy, vz, 0), relative to the group origin gorig = (O_g, T_g), the
+    // start of the group's first entry (filter.cuh f32_cand_rebase)
+    float4 *frec = nullptr;
+    double4 *gorig = nullptr;
     int64_t ngroups = 0;
     DBuf aux;
     bool built = false;
@@ -334,6 +339,8 @@ struct K1Launch {
     const int64_t *orig;
     const float4 *gbox;
     const double2 *gtime;
+    const float4 *frec = nullptr;  // K1 layout FP32 records (2 per entry) and group origins
+    const double4 *gorig = nullptr;
     int cull;
     // overlap counts come from count_overlaps_ext (store te sorted; used
     // when the query flags say ts and te are both sorted): K1's box-cull

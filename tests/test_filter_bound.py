@@ -68,6 +68,8 @@ def test_filter_flags_every_nonnegative_reference_discriminant(tmp_path):
     # margin-free radius does reject hits (the generator reaches the bound)
     assert out["edge"]["sep_checks"] > 1_000_000 and out["edge"]["sep_rejected"] > 100_000
     assert out["edge"]["sep_misses"] == 0 and out["edge"]["sep_mutation_misses"] > 0
+    # the K1 layout's re-based FP32 records (group origin -> item origin)
+    assert out["edge"]["rebase_checks"] > 1_000_000 and out["edge"]["rebase_misses"] == 0
     assert out["edge"]["hits"] > 100_000 and out["edge"]["f32_checks"] > 1_000_000
 
 

@@ -92,7 +92,7 @@ struct Counts {
     long pairs = 0, overlapping = 0, disc_pos = 0, checks = 0, flagged = 0, misses = 0, skipped = 0;
     long hits = 0, f32_checks = 0, f32_flagged = 0, f32_misses = 0, f32_skipped = 0, box_checks = 0;
     long box_misses = 0, box_mut_misses = 0, sep_checks = 0, sep_rejected = 0, sep_misses = 0, sep_mut_misses = 0,
-         sep_only = 0;
+         sep_only = 0, rebase_checks = 0, rebase_misses = 0;
 };
 
 // the reference's hit decision for an overlapping pair (core.py:523-551)
@@ -170,6 +170,41 @@ static void check_f32(const Seg &r, const Seg &c, double d, const double O[3], d
         if (n.f32_misses <= 5) std::fprintf(stderr, "F32 LANE MISS %s\n", tag);
     }
     const bool need = ref_hit(r, c, d);
+    // the K1 layout's re-based records: the candidate's FP32 view relative to
+    // a group origin (O_g, T_g) (another candidate's start), re-based to the
+    // item origin (f32_cand_rebase); the item bounds then cover O_g and T_g
+    {
+        double Og[3];
+        for (int i = 0; i < 3; ++i) Og[i] = r.s[i] + unif(-1, 1) * (std::fabs(r.e[i] - r.s[i]) + std::fabs(r.s[i]) * 1e-3 + 1.0);
+        const double Tg = r.ts + unif(-3, 3) * (std::fabs(r.te - r.ts) + 1.0);
+        double ar2 = ar, tr2 = std::fmax(std::fabs(r.ts - T0), std::fabs(Tg - T0));
+        for (int i = 0; i < 3; ++i) ar2 = std::fmax(ar2, std::fabs(Og[i] - O[i]));
+        const double tvr2 = std::fmax(tvr, std::fabs(Tg - T0) * vr);  // the group's own start at T_g
+        const F32Item it2 = f32_item(O[0], O[1], O[2], T0, ar2, tvr2, vr, aq, tq, cext, cmax, tr2);
+        if (it2.ok) {
+            F32Item go;
+            go.ox = Og[0]; go.oy = Og[1]; go.oz = Og[2]; go.t0 = Tg;
+            const CandF32 pg = f32_cand(r.ts, r.s[0], r.s[1], r.s[2], rv[0], rv[1], rv[2], go);
+            const CandF32 rb = f32_cand_rebase(pg.px, pg.py, pg.pz, pg.vx, pg.vy, pg.vz, pg.sr,
+                                               TSK_F2F_RN(Og[0] - O[0]), TSK_F2F_RN(Og[1] - O[1]),
+                                               TSK_F2F_RN(Og[2] - O[2]), TSK_F2F_RN(Tg - T0));
+            float q2[6];
+            f32_query(c.ts, c.s[0], c.s[1], c.s[2], cext, cd[0], cd[1], cd[2], it2, std::sqrt(d * d), q2);
+            const bool f2 = f32_flag(rb, q2[0], q2[1], q2[2], q2[3], q2[4], q2[5]);
+            double dq = 0;
+            for (int i = 0; i < 3; ++i) dq = std::fmax(dq, std::fabs(c.e[i] - c.s[i]));
+            const double M2 = ar2 + tvr2 + (tq + cext + tr2) * vr + aq + dq;
+            float qe[4];
+            f32_query_end(c.te, c.e[0], c.e[1], c.e[2], it2, qe);
+            const bool far2 = f32_sep_far(rb.px, rb.py, rb.pz, rb.vx, rb.vy, rb.vz, q2[0], q2[1], q2[2], q2[3], qe[0],
+                                          qe[1], qe[2], qe[3], f32_sep_rbase(std::sqrt(d * d), cmax, M2));
+            ++n.rebase_checks;
+            if (need && (!f2 || far2)) {
+                ++n.rebase_misses;
+                if (n.rebase_misses <= 5) std::fprintf(stderr, "REBASE MISS %s d=%.17g flag=%d far=%d\n", tag, d, f2, far2);
+            }
+        }
+    }
     // the separating-axis second stage over the query's span (f32_sep_far)
     {
         double dq = 0;
@@ -446,16 +481,17 @@ int main(int argc, char **argv) {
                 "\"flagged\": %ld, \"skipped\": %ld, \"misses\": %ld, \"hits\": %ld, \"f32_checks\": %ld, "
                 "\"f32_flagged\": %ld, \"f32_skipped\": %ld, \"f32_misses\": %ld, \"box_checks\": %ld, "
                 "\"box_misses\": %ld, \"box_mutation_misses\": %ld, \"sep_checks\": %ld, \"sep_rejected\": %ld, "
-                "\"sep_misses\": %ld, \"sep_mutation_misses\": %ld}, "
+                "\"sep_misses\": %ld, \"sep_mutation_misses\": %ld, \"rebase_checks\": %ld, \"rebase_misses\": %ld}, "
                 "\"random\": {\"pairs\": %ld, \"overlapping\": %ld, \"disc_pos\": %ld, \"checks\": %ld, "
                 "\"flagged\": %ld, \"misses\": %ld, \"hits\": %ld, \"f32_checks\": %ld, \"f32_flagged\": %ld, "
                 "\"f32_misses\": %ld}}\n",
                 n.pairs, n.overlapping, n.disc_pos, n.checks, n.flagged, n.skipped, n.misses, n.hits,
                 n.f32_checks, n.f32_flagged, n.f32_skipped, n.f32_misses, n.box_checks, n.box_misses + nrand.box_misses,
                 n.box_mut_misses + nrand.box_mut_misses, n.sep_checks + nrand.sep_checks, n.sep_rejected + nrand.sep_rejected,
-                n.sep_misses + nrand.sep_misses, n.sep_mut_misses + nrand.sep_mut_misses, nrand.pairs, nrand.overlapping,
+                n.sep_misses + nrand.sep_misses, n.sep_mut_misses + nrand.sep_mut_misses,
+                n.rebase_checks + nrand.rebase_checks, n.rebase_misses + nrand.rebase_misses, nrand.pairs, nrand.overlapping,
                 nrand.disc_pos, nrand.checks, nrand.flagged, nrand.misses, nrand.hits, nrand.f32_checks,
                 nrand.f32_flagged, nrand.f32_misses);
     return (n.misses || nrand.misses || n.f32_misses || nrand.f32_misses || n.box_misses || nrand.box_misses ||
-            n.sep_misses || nrand.sep_misses) ? 1 : 0;
+            n.sep_misses || nrand.sep_misses || n.rebase_misses || nrand.rebase_misses) ? 1 : 0;
 }
