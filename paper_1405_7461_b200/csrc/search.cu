@@ -79,8 +79,20 @@ static void pin_release(void *p, size_t bytes) {
     }
 }
 
+// Size classes for large blocks (2^k x {1, 1.25, 1.5, 1.75}): the
+// pipelined and single-launch result paths ask for slightly different sizes
+// of the same result, and both then reuse each other's cached blocks.
+static size_t pin_size_class(size_t bytes) {
+    if (bytes < kMmapAbove) return bytes;
+    size_t p = size_t(1) << (63 - __builtin_clzll((unsigned long long)bytes));
+    for (int q = 4; q <= 8; ++q)
+        if (p / 4 * q >= bytes) return p / 4 * q;
+    return 2 * p;
+}
+
 static void *pin_alloc(size_t bytes, size_t *got) {
     if (bytes == 0) bytes = 64;
+    bytes = pin_size_class(bytes);
     {
         std::lock_guard<std::mutex> g(g_pin_mu);
         auto it = g_pin_free.lower_bound(bytes);

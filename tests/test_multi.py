@@ -120,3 +120,60 @@ def test_library_sharded_run_search_equals_single_device():
         assert (st.interactions_computed, st.temporal_misses, st.spatial_misses, st.hits) == \
             (bst.interactions_computed, bst.temporal_misses, bst.spatial_misses, bst.hits)
         assert [t.interactions for t in st.per_batch] == [t.interactions for t in bst.per_batch]
+
+
+def _gpu_worker(rank, world, port, out):
+    """One rank of the bench's N>1 layout on the GPU library: each rank
+    uploads its own replica of the store (as under torchrun; in one process
+    replicas are device-to-device copies, tsk_db_replicate), the plan is cut
+    into interaction-balanced shards, each rank runs run_search on its shard,
+    and gloo carries the results back."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    tsk.set_device(0)  # both ranks on the one GPU of the box
+    store, _, q, _ = _scene()
+    ix = tsk.build_index(store, 200)
+    plan = tsk.periodic(q, 23, ix)
+    bounds = shard_bounds(batch_interactions(plan, ix), world)
+    b0, b1 = bounds[rank]
+    sp = sub_plan(plan, b0, b1)
+    part = None
+    if sp is not None:
+        res, st = tsk.run_search(store, ix, sp, 9.0)
+        part = ({k: np.asarray(getattr(res, k)).copy() for k in RES},
+                (st.interactions_computed, st.temporal_misses, st.spatial_misses, st.hits))
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (b0, b1, part))
+    if rank == 0:
+        out.put(gathered)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gloo_world2_gpu_ranks_equal_oracle():
+    """The sharded N>1 path with the GPU library in every rank (both ranks on
+    GPU 0 of a one-GPU box): the shard-ordered concatenation equals the CPU
+    oracle's single run bit for bit, statistics included."""
+    if tsk.device_count() < 1:
+        pytest.fail("no CUDA device")
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    gathered = out.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    store, ix, q, plan = _scene()
+    want, wst = _oracle_run(store, ix, plan, 9.0)
+    parts = [g[2] for g in sorted(gathered, key=lambda g: g[0]) if g[2] is not None]
+    assert len(parts) == 2
+    for k in RES:
+        assert np.array_equal(np.concatenate([p[0][k] for p in parts]), want[k]), k
+    tot = np.sum([p[1] for p in parts], axis=0)
+    assert tuple(int(x) for x in tot) == (wst["interactions"], wst["temporal_misses"], wst["spatial_misses"],
+                                           wst["hits"])
