@@ -38,9 +38,6 @@
 #ifndef K1_EARLY
 #define K1_EARLY 0  // measured: no gain (more spills)
 #endif
-#ifndef K1_PREFETCH
-#define K1_PREFETCH 0
-#endif
 #ifndef K1F_MIN_BLOCKS
 #define K1F_MIN_BLOCKS 3
 #endif
@@ -655,14 +652,6 @@ __device__ __noinline__ void fast_subtile(const K1Launch &L, const ItemCtx &it, 
     // the groups' time range and box, loaded together, and (speculatively:
     // nearly every sub-tile has a query near its box) the first candidates'
     // columns, whose latency then hides behind the window search and cull
-#if K1_PREFETCH
-    // the sub-tile's FP32 records (4 KB) into L2 while the window search and
-    // the box cull run: one 128-byte line per lane
-    if (L.frec) {
-        const char *pf = reinterpret_cast<const char *>(L.frec + 2 * wbase) + 128 * lane;
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(pf));
-    }
-#endif
     RawPair r0;
 #if K1_EARLY
     load_pair(L, wbase, it.c_lo, it.c_hi, 0, lane, r0);

@@ -774,6 +774,13 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     TSK_REQUIRE(bb + major_bits + minor_bits <= 64, "result key wider than 64 bits");
 
     int64_t launches = 0;
+    // pinned staging of pageable query columns, returned to the pool when the
+    // call returns (every return path has synchronised the stream)
+    struct Stage {
+        void *p = nullptr;
+        size_t bytes = 0;
+        ~Stage() { pin_free(p, bytes); }
+    } stage;
     Trace tr(st);
     tr.mark("start");
     TSK_CUDA(cudaEventRecord(db->ev0, st));
@@ -789,9 +796,38 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
             launch_qprep_mapped(mapped, db->q, db->q_rec.as<QRec>(), db->counters.as<int>() + 8,
                                 db->counters.as<unsigned long long>() + 5, st);
         } else {
-            soa_upload(db->q, qc, st);
-            launch_qprep(db->q, db->q_rec.as<QRec>(), db->counters.as<int>() + 8,
-                         db->counters.as<unsigned long long>() + 5, st);
+            // pageable inputs (plain numpy): host threads copy the columns
+            // into a pooled pinned block, which the kernel then reads over
+            // PCIe like pinned inputs (a pageable cudaMemcpy runs at a
+            // fraction of the bus rate through the driver's bounce buffer)
+            const size_t cb = (size_t)nq * 8;
+            stage.p = pin_alloc(cb * 10, &stage.bytes);
+            char *sb = static_cast<char *>(stage.p);
+            const void *src[10] = {qc->traj, qc->seg, qc->xs, qc->ys, qc->zs, qc->ts, qc->xe, qc->ye, qc->ze, qc->te};
+            HostPool::get().run([&](int part, int parts) {
+                const size_t a = cb * part / parts & ~size_t(63), z = part + 1 == parts ? cb : cb * (part + 1) / parts & ~size_t(63);
+                for (int k = 0; k < 10; ++k)
+                    if (src[k] && z > a) memcpy(sb + k * cb + a, static_cast<const char *>(src[k]) + a, z - a);
+            });
+            tsk_columns staged = *qc;
+            staged.traj = qc->traj ? (const int64_t *)(sb + 0 * cb) : nullptr;
+            staged.seg = qc->seg ? (const int64_t *)(sb + 1 * cb) : nullptr;
+            staged.xs = (const double *)(sb + 2 * cb);
+            staged.ys = (const double *)(sb + 3 * cb);
+            staged.zs = (const double *)(sb + 4 * cb);
+            staged.ts = (const double *)(sb + 5 * cb);
+            staged.xe = (const double *)(sb + 6 * cb);
+            staged.ye = (const double *)(sb + 7 * cb);
+            staged.ze = (const double *)(sb + 8 * cb);
+            staged.te = (const double *)(sb + 9 * cb);
+            if (qc->traj && mapped_columns(&staged, &mapped)) {
+                launch_qprep_mapped(mapped, db->q, db->q_rec.as<QRec>(), db->counters.as<int>() + 8,
+                                    db->counters.as<unsigned long long>() + 5, st);
+            } else {
+                soa_upload(db->q, &staged, st);
+                launch_qprep(db->q, db->q_rec.as<QRec>(), db->counters.as<int>() + 8,
+                             db->counters.as<unsigned long long>() + 5, st);
+            }
         }
         launches += 1;
     }
