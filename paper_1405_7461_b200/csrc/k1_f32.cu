@@ -643,7 +643,15 @@ __shared__ int64_t k1_kf[2];
 // they are ever flagged (its tb case is chosen per pair: the warp's end-time
 // bounds are left open).  Only warps with a query near their box load their
 // candidates, all columns in one round trip.
-__device__ __noinline__ void fast_subtile(const K1Launch &L, const ItemCtx &it, const QRec *__restrict__ qt,
+#ifndef K1_FAST_INLINE
+#define K1_FAST_INLINE 0
+#endif
+#if K1_FAST_INLINE
+__device__ __forceinline__
+#else
+__device__ __noinline__
+#endif
+void fast_subtile(const K1Launch &L, const ItemCtx &it, const QRec *__restrict__ qt,
                                           const QF32 *__restrict__ sqf, const double *pm, const double *sm,
                                           int64_t wbase, float cull_rb, const F32Item &fi, bool item_f32, float *wcs,
                                           int warp, int lane, unsigned long long &n_ev, unsigned long long &n_hit) {
@@ -742,6 +750,133 @@ __device__ __noinline__ void fast_subtile(const K1Launch &L, const ItemCtx &it, 
     f32_list_range(qt, sqf, ns, warp, lane, n_hit);
 }
 
+// One warp sub-tile outside the box-cull fast path (start-sorted store,
+// spans given by the caller, unsorted queries, counting modes, extreme
+// exponents): per-pair overlap counts, the three start-time ranges, the
+// exact path where the FP32 pre-filter does not apply.  Kept out of the
+// kernel body so the fast path's register allocation is its own.
+__device__ __noinline__ void slow_subtile(const K1Launch &L, const ItemCtx &it, const QRec *__restrict__ qt,
+                                          const QF32 *__restrict__ sqf, const double *pm, const double *sm,
+                                          int64_t wbase, float cull_rb, const F32Item &fi, bool item_f32,
+                                          bool single_scan, bool te_sorted, bool q_unsorted, bool cull, float *wcs,
+                                          int warp, int lane, unsigned long long &n_ov, unsigned long long &n_hit,
+                                          unsigned long long &n_ev) {
+        double rts[CPT], rte[CPT];
+        bool valid_any = false, unsafe_r = false;
+        double wmin = INFINITY, wmax = -INFINITY, wmin_te = INFINITY, wmax_ts = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            const int64_t e = wbase + k * 32 + lane;
+            const bool valid = e >= it.c_lo && e <= it.c_hi;
+            rts[k] = INFINITY;
+            rte[k] = -INFINITY;
+            if (valid) {
+                rts[k] = L.e.ts[e];
+                rte[k] = L.e.te[e];
+                unsafe_r |= L.e.unsafe[e] != 0;
+                // times are finite (validated): plain selects, no NaN handling
+                wmin = rts[k] < wmin ? rts[k] : wmin;
+                wmax = rte[k] > wmax ? rte[k] : wmax;
+                wmin_te = rte[k] < wmin_te ? rte[k] : wmin_te;
+                wmax_ts = rts[k] > wmax_ts ? rts[k] : wmax_ts;
+            }
+            valid_any |= valid;
+        }
+        if (L.noop) return;
+        if (!__any_sync(0xffffffffu, valid_any)) return;
+        wmax = warp_max(wmax);
+        wmin_te = warp_min(wmin_te);
+        if (lane == 0) {
+            set_key_bases(L, it, wbase, warp);
+            k1_wctx[warp].js = it.js;
+            k1_wctx[warp].wbase = wbase;
+            const int64_t nv = it.c_hi - wbase + 1;
+            k1_wctx[warp].nvalid = nv < 0 ? 0 : (nv > WCAND ? WCAND : (int)nv);
+            k1_wctx[warp].wmin_te = wmin_te;
+            k1_wctx[warp].wmax = wmax;
+        }
+        __syncwarp();
+        const bool exact_only = !item_f32 || __any_sync(0xffffffffu, unsafe_r);
+        if (single_scan && !exact_only) {
+            // start and end times both ascending over the tile: a
+            // candidate overlaps exactly the queries j with
+            // ts_j <= r.te (a prefix) and te_j >= r.ts (a suffix), so its
+            // count is two bisections, the window [jlo, jhi) of the warp
+            // is their min / max (the warp_window bounds of wmin, wmax),
+            // and the whole window is one scan (the exact path decides the
+            // clip cases per pair)
+            int lo[CPT], hi[CPT];
+            tile_bounds<CPT>(sm, pm, it.nt, rts, rte, lo, hi);
+            int jlo = it.nt, jhi = 0;
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) {
+                n_ov += split_count(lo[k], hi[k], it.js);
+                jlo = lo[k] < jlo ? lo[k] : jlo;
+                jhi = hi[k] > jhi ? hi[k] : jhi;
+            }
+            jlo = __reduce_min_sync(0xffffffffu, jlo);
+            jhi = __reduce_max_sync(0xffffffffu, jhi);
+            if (jhi < jlo) jhi = jlo;
+            if (cull) {
+                // K1 layout: one box test per (query, warp) first; the
+                // candidates are converted only when a query survives
+                float4 blo, bhi;
+                bool bunsafe;
+                warp_box(L, wbase, it.c_hi, blo, bhi, bunsafe);
+                const int ns = box_cull(blo, bhi, jlo, jhi, cull_rb, warp, lane);
+                n_ev += (unsigned long long)ns * (unsigned long long)k1_wctx[warp].nvalid;
+                if (ns == 0) return;
+                stage_cands(L, wbase, it.c_lo, it.c_hi, rts, fi, wcs, lane);
+                __syncwarp();
+                f32_list_range(qt, sqf, ns, warp, lane, n_hit);
+                return;
+            }
+            stage_cands(L, wbase, it.c_lo, it.c_hi, rts, fi, wcs, lane);
+            __syncwarp();
+            n_ev += (unsigned long long)(jhi - jlo) * (unsigned long long)k1_wctx[warp].nvalid;
+            f32_range<TA_BOTH, TB_DYN, false>(qt, sqf, jlo, jhi, warp, lane, n_ov, n_hit);
+            return;
+        }
+        if (item_f32) stage_cands(L, wbase, it.c_lo, it.c_hi, rts, fi, wcs, lane);
+        __syncwarp();
+        wmin = warp_min(wmin);
+        wmax_ts = warp_max(wmax_ts);
+        const int4 w = warp_window(sqf, pm, it.nt, q_unsorted, wmin, wmax, wmax_ts, lane);
+        const int jlo = w.x, ja = w.y, jb = w.z, jhi = w.w;
+        if (L.overlaps_only) {
+            n_ov += count_overlaps<CPT>(sqf, jlo, jhi, it.js, rts, rte);
+            return;
+        }
+        if (exact_only) {
+            all_range<TA_C>(qt, sqf, jlo, ja, rts, rte, warp, lane, n_ov, n_hit);
+            all_range<TA_BOTH>(qt, sqf, ja, jb, rts, rte, warp, lane, n_ov, n_hit);
+            all_range<TA_R>(qt, sqf, jb, jhi, rts, rte, warp, lane, n_ov, n_hit);
+            return;
+        }
+        n_ev += (unsigned long long)(jhi - jlo) * (unsigned long long)k1_wctx[warp].nvalid;
+        // TA_C range: every query ends before all candidates (running max
+        // < min te) and te is sorted → overlaps counted by bisection
+        if (jlo < ja && pm[ja - 1] < wmin_te && te_sorted) {
+#pragma unroll
+            for (int k = 0; k < CPT; ++k)
+                n_ov += split_count(clampi(lower_bound_te(sqf, it.nt, rts[k]), jlo, ja), ja, it.js);
+            f32_range<TA_C, TB_R, false>(qt, sqf, jlo, ja, warp, lane, n_ov, n_hit);
+        } else {
+            f32_range<TA_C, TB_DYN, true>(qt, sqf, jlo, ja, warp, lane, n_ov, n_hit);
+        }
+        f32_range<TA_BOTH, TB_DYN, true>(qt, sqf, ja, jb, warp, lane, n_ov, n_hit);
+        // TA_R range: every query ends after all candidates (suffix min >
+        // max te) → overlap <=> cts <= r.te, counted by bisection
+        if (jb < jhi && sm[jb] > wmax) {
+#pragma unroll
+            for (int k = 0; k < CPT; ++k)
+                n_ov += split_count(jb, clampi(upper_bound_ts(sqf, it.nt, rte[k]), jb, jhi), it.js);
+            f32_range<TA_R, TB_C, false>(qt, sqf, jb, jhi, warp, lane, n_ov, n_hit);
+        } else {
+            f32_range<TA_R, TB_DYN, true>(qt, sqf, jb, jhi, warp, lane, n_ov, n_hit);
+        }
+}
+
 __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Launch L) {
     // running max / suffix min of te over the tile; on single-scan items
     // (times ascending) te / ts themselves, +inf padded for tile_bounds
@@ -786,7 +921,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
         __syncthreads();
         if (item_sh >= total) break;
         if (tid == 0) K1_STAT(7, 1);
-        const ItemCtx it = it_sh;
+        const ItemCtx &it = it_sh;  // read from shared memory (a register copy spills to the stack)
         const QRec *const qt = L.q + it.lo_q;  // the tile's exact records (global; rare path)
 
         // pass 1 over the tile: flags, and the item's magnitude bounds
@@ -931,120 +1066,8 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
                 fast_subtile(L, it, qt, sqf, pm, sm, wbase, cull_rb, fi_sh, item_f32, wcs, warp, lane, n_ev, n_hit);
                 continue;
             }
-            double rts[CPT], rte[CPT];
-            bool valid_any = false, unsafe_r = false;
-            double wmin = INFINITY, wmax = -INFINITY, wmin_te = INFINITY, wmax_ts = -INFINITY;
-#pragma unroll
-            for (int k = 0; k < CPT; ++k) {
-                const int64_t e = wbase + k * 32 + lane;
-                const bool valid = e >= it.c_lo && e <= it.c_hi;
-                rts[k] = INFINITY;
-                rte[k] = -INFINITY;
-                if (valid) {
-                    rts[k] = L.e.ts[e];
-                    rte[k] = L.e.te[e];
-                    unsafe_r |= L.e.unsafe[e] != 0;
-                    // times are finite (validated): plain selects, no NaN handling
-                    wmin = rts[k] < wmin ? rts[k] : wmin;
-                    wmax = rte[k] > wmax ? rte[k] : wmax;
-                    wmin_te = rte[k] < wmin_te ? rte[k] : wmin_te;
-                    wmax_ts = rts[k] > wmax_ts ? rts[k] : wmax_ts;
-                }
-                valid_any |= valid;
-            }
-            if (L.noop) continue;
-            if (!__any_sync(0xffffffffu, valid_any)) continue;
-            wmax = warp_max(wmax);
-            wmin_te = warp_min(wmin_te);
-            if (lane == 0) {
-                set_key_bases(L, it, wbase, warp);
-                k1_wctx[warp].js = it.js;
-                k1_wctx[warp].wbase = wbase;
-                const int64_t nv = it.c_hi - wbase + 1;
-                k1_wctx[warp].nvalid = nv < 0 ? 0 : (nv > WCAND ? WCAND : (int)nv);
-                k1_wctx[warp].wmin_te = wmin_te;
-                k1_wctx[warp].wmax = wmax;
-            }
-            __syncwarp();
-            const bool exact_only = !item_f32 || __any_sync(0xffffffffu, unsafe_r);
-            if (single_scan && !exact_only) {
-                // start and end times both ascending over the tile: a
-                // candidate overlaps exactly the queries j with
-                // ts_j <= r.te (a prefix) and te_j >= r.ts (a suffix), so its
-                // count is two bisections, the window [jlo, jhi) of the warp
-                // is their min / max (the warp_window bounds of wmin, wmax),
-                // and the whole window is one scan (the exact path decides the
-                // clip cases per pair)
-                int lo[CPT], hi[CPT];
-                tile_bounds<CPT>(sm, pm, it.nt, rts, rte, lo, hi);
-                int jlo = it.nt, jhi = 0;
-#pragma unroll
-                for (int k = 0; k < CPT; ++k) {
-                    n_ov += split_count(lo[k], hi[k], it.js);
-                    jlo = lo[k] < jlo ? lo[k] : jlo;
-                    jhi = hi[k] > jhi ? hi[k] : jhi;
-                }
-                jlo = __reduce_min_sync(0xffffffffu, jlo);
-                jhi = __reduce_max_sync(0xffffffffu, jhi);
-                if (jhi < jlo) jhi = jlo;
-                if (cull) {
-                    // K1 layout: one box test per (query, warp) first; the
-                    // candidates are converted only when a query survives
-                    float4 blo, bhi;
-                    bool bunsafe;
-                    warp_box(L, wbase, it.c_hi, blo, bhi, bunsafe);
-                    const int ns = box_cull(blo, bhi, jlo, jhi, cull_rb, warp, lane);
-                    n_ev += (unsigned long long)ns * (unsigned long long)k1_wctx[warp].nvalid;
-                    if (ns == 0) continue;
-                    stage_cands(L, wbase, it.c_lo, it.c_hi, rts, fi_sh, wcs, lane);
-                    __syncwarp();
-                    f32_list_range(qt, sqf, ns, warp, lane, n_hit);
-                    continue;
-                }
-                stage_cands(L, wbase, it.c_lo, it.c_hi, rts, fi_sh, wcs, lane);
-                __syncwarp();
-                n_ev += (unsigned long long)(jhi - jlo) * (unsigned long long)k1_wctx[warp].nvalid;
-                f32_range<TA_BOTH, TB_DYN, false>(qt, sqf, jlo, jhi, warp, lane, n_ov, n_hit);
-                continue;
-            }
-            if (item_f32) stage_cands(L, wbase, it.c_lo, it.c_hi, rts, fi_sh, wcs, lane);
-            __syncwarp();
-            wmin = warp_min(wmin);
-            wmax_ts = warp_max(wmax_ts);
-            const int4 w = warp_window(sqf, pm, it.nt, q_unsorted, wmin, wmax, wmax_ts, lane);
-            const int jlo = w.x, ja = w.y, jb = w.z, jhi = w.w;
-            if (L.overlaps_only) {
-                n_ov += count_overlaps<CPT>(sqf, jlo, jhi, it.js, rts, rte);
-                continue;
-            }
-            if (exact_only) {
-                all_range<TA_C>(qt, sqf, jlo, ja, rts, rte, warp, lane, n_ov, n_hit);
-                all_range<TA_BOTH>(qt, sqf, ja, jb, rts, rte, warp, lane, n_ov, n_hit);
-                all_range<TA_R>(qt, sqf, jb, jhi, rts, rte, warp, lane, n_ov, n_hit);
-                continue;
-            }
-            n_ev += (unsigned long long)(jhi - jlo) * (unsigned long long)k1_wctx[warp].nvalid;
-            // TA_C range: every query ends before all candidates (running max
-            // < min te) and te is sorted → overlaps counted by bisection
-            if (jlo < ja && pm[ja - 1] < wmin_te && te_sorted) {
-#pragma unroll
-                for (int k = 0; k < CPT; ++k)
-                    n_ov += split_count(clampi(lower_bound_te(sqf, it.nt, rts[k]), jlo, ja), ja, it.js);
-                f32_range<TA_C, TB_R, false>(qt, sqf, jlo, ja, warp, lane, n_ov, n_hit);
-            } else {
-                f32_range<TA_C, TB_DYN, true>(qt, sqf, jlo, ja, warp, lane, n_ov, n_hit);
-            }
-            f32_range<TA_BOTH, TB_DYN, true>(qt, sqf, ja, jb, warp, lane, n_ov, n_hit);
-            // TA_R range: every query ends after all candidates (suffix min >
-            // max te) → overlap <=> cts <= r.te, counted by bisection
-            if (jb < jhi && sm[jb] > wmax) {
-#pragma unroll
-                for (int k = 0; k < CPT; ++k)
-                    n_ov += split_count(jb, clampi(upper_bound_ts(sqf, it.nt, rte[k]), jb, jhi), it.js);
-                f32_range<TA_R, TB_C, false>(qt, sqf, jb, jhi, warp, lane, n_ov, n_hit);
-            } else {
-                f32_range<TA_R, TB_DYN, true>(qt, sqf, jb, jhi, warp, lane, n_ov, n_hit);
-            }
+            slow_subtile(L, it, qt, sqf, pm, sm, wbase, cull_rb, fi_sh, item_f32, single_scan, te_sorted, q_unsorted,
+                         cull, wcs, warp, lane, n_ov, n_hit, n_ev);
         }
         if (lane == 0 && n_ev) atomicAdd(&red_ev, n_ev);
         item_counters(L, it, n_ov, n_hit, lane, tid, red, &red_ev);

@@ -447,9 +447,15 @@ static tsk_result *run_pipelined(tsk_db *db, const tsk_columns *qc, const Search
     const int64_t nb = plan.nb;
     // chunks: worth it once the rows' PCIe time is noticeable (the previous
     // call's hit count predicts this one's); ~2^20 rows per chunk, 4..16
+    // Long kernels with mid-size results (c5: 24 ms, 8.8e5 rows) take 3
+    // chunks: the rows' copy hides behind K1 and the extra launches cost
+    // little against the kernel (measured: -0.8 ms at c5; at c3, 1 ms of K1,
+    // chunking costs more than the 0.35 ms copy it hides).
     int C = 0;
     if (db->last_hits >= kPipeMinRows)
         C = (int)std::min<int64_t>(kPipeMaxChunks, std::max<int64_t>(kPipeMinChunks, db->last_hits >> 20));
+    else if (db->last_hits >= (int64_t(1) << 18) && db->last_k1_ms >= 5.0)
+        C = 3;
     if (const char *e = getenv("TSK_PIPE_CHUNKS")) C = std::max(0, atoi(e));  // testing: 0 = off
     if (C == 0) return nullptr;
     C = (int)std::max<int64_t>(1, std::min<int64_t>(C, nb / 2));
@@ -726,6 +732,7 @@ static tsk_result *run_pipelined(tsk_db *db, const tsk_columns *qc, const Search
     res->device_ms = ms;
     res->launches = launches;
     db->last_hits = nh;
+    db->last_k1_ms = k1_ms;
     if (trace) {
         auto at = [&](cudaEvent_t e) {
             float t = -1.f;
@@ -959,7 +966,10 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     }
     TSK_REQUIRE(count_only || h_hits < (1ull << 32), "more than 2^32 hits in one call");
     const int64_t nh = count_only ? 0 : (int64_t)h_hits;
-    if (!count_only) db->last_hits = nh;
+    if (!count_only) {
+        db->last_hits = nh;
+        db->last_k1_ms = k1_ms;
+    }
 
     tsk_result *res = new tsk_result();
     res->n = nh;

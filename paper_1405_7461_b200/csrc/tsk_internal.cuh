@@ -153,6 +153,7 @@ struct tsk_db {
     tsk::DBuf q_rec, batches, counters, recs, sorted, cub_tmp, out_cols, canon_cols, canon_tmp;
     tsk::DBuf pipe;         // per-chunk item tables of the pipelined search
     int64_t last_hits = 0;  // hits of the previous search (sizes the pipeline's host block)
+    double last_k1_ms = 0;  // and its K1 time (chooses the pipeline's chunk count)
     int ids32 = 0;          // every entry id fits in int32 (4-byte ids over PCIe)
     tsk::Soa q;  // device copy of the current query set
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_k0 = nullptr, ev_k1 = nullptr;
