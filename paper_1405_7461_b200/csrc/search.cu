@@ -303,7 +303,7 @@ static int sm_count(int device) {
 
 // Results of at least this many rows take the compact path (below it the
 // 48-byte device gather and one copy are cheaper than the pipeline).
-static const int64_t kCompactMin = int64_t(1) << 18;
+static const int64_t kCompactMin = int64_t(1) << 21;  // below ~2M rows one 48 B/row copy is faster (c3: 0.44 vs 0.82 ms)
 static const int64_t kCompactChunk = int64_t(1) << 21;  // rows per pipeline chunk
 
 // Compact result assembly, pipelined: for each chunk of sorted rows K4
@@ -344,7 +344,7 @@ static void compact_rows(tsk_db *db, tsk_result *res, const tsk_columns *qc, int
     std::vector<cudaEvent_t> evg((size_t)nc), evd((size_t)nc);
     for (int64_t c = 0; c < nc; ++c) {
         TSK_CUDA(cudaEventCreateWithFlags(&evg[c], cudaEventDisableTiming));
-        TSK_CUDA(cudaEventCreateWithFlags(&evd[c], cudaEventDisableTiming | cudaEventBlockingSync));
+        TSK_CUDA(cudaEventCreateWithFlags(&evd[c], cudaEventDisableTiming));  // spin: a blocking wait wakes ~0.5 ms late
     }
     for (int64_t c = 0; c < nc; ++c) {
         const int64_t r0 = c * chunk, r1 = std::min<int64_t>(nh, r0 + chunk), m = r1 - r0;
@@ -447,15 +447,11 @@ static tsk_result *run_pipelined(tsk_db *db, const tsk_columns *qc, const Search
     const int64_t nb = plan.nb;
     // chunks: worth it once the rows' PCIe time is noticeable (the previous
     // call's hit count predicts this one's); ~2^20 rows per chunk, 4..16
-    // Long kernels with mid-size results (c5: 24 ms, 8.8e5 rows) take 3
-    // chunks: the rows' copy hides behind K1 and the extra launches cost
-    // little against the kernel (measured: -0.8 ms at c5; at c3, 1 ms of K1,
-    // chunking costs more than the 0.35 ms copy it hides).
+    // (Mid-size results go through one 48 B/row copy instead: at c5, 8.8e5
+    // rows behind 24 ms of K1, 3 chunks measured 26.3 ms against 26.0.)
     int C = 0;
     if (db->last_hits >= kPipeMinRows)
         C = (int)std::min<int64_t>(kPipeMaxChunks, std::max<int64_t>(kPipeMinChunks, db->last_hits >> 20));
-    else if (db->last_hits >= (int64_t(1) << 18) && db->last_k1_ms >= 5.0)
-        C = 3;
     if (const char *e = getenv("TSK_PIPE_CHUNKS")) C = std::max(0, atoi(e));  // testing: 0 = off
     if (C == 0) return nullptr;
     C = (int)std::max<int64_t>(1, std::min<int64_t>(C, nb / 2));
@@ -542,7 +538,7 @@ static tsk_result *run_pipelined(tsk_db *db, const tsk_columns *qc, const Search
         TSK_CUDA(cudaEventCreate(&ek1[c]));
         // spin on the count (a blocking wait adds ~0.2 ms of wake-up per chunk)
         TSK_CUDA(cudaEventCreateWithFlags(&eks[c], cudaEventDisableTiming));
-        TSK_CUDA(cudaEventCreateWithFlags(&evd[c], cudaEventBlockingSync));
+        TSK_CUDA(cudaEventCreate(&evd[c]));  // spin wait (see compact_rows)
     }
     const bool trace = getenv("TSK_TRACE") != nullptr;
     std::vector<cudaEvent_t> esd((size_t)C, nullptr);  // (trace) end of S(c)
