@@ -877,7 +877,14 @@ __device__ __noinline__ void slow_subtile(const K1Launch &L, const ItemCtx &it, 
         }
 }
 
-__global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Launch L) {
+__global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Launch Lp) {
+    // the launch parameters in shared memory: the device functions take them
+    // by reference, and a reference to the parameter space would make every
+    // thread keep a copy on its stack (local memory)
+    __shared__ __align__(16) unsigned char l_raw[sizeof(K1Launch)];
+    if (threadIdx.x == 0) *reinterpret_cast<K1Launch *>(l_raw) = Lp;
+    __syncthreads();
+    const K1Launch &L = *reinterpret_cast<const K1Launch *>(l_raw);
     // running max / suffix min of te over the tile; on single-scan items
     // (times ascending) te / ts themselves, +inf padded for tile_bounds
     __shared__ double pm[2 * K1_TQ];
