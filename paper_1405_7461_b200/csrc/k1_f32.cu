@@ -39,7 +39,7 @@
 #define K1_EARLY 0  // measured: no gain (more spills)
 #endif
 #ifndef K1F_MIN_BLOCKS
-#define K1F_MIN_BLOCKS 3
+#define K1F_MIN_BLOCKS 2
 #endif
 
 namespace tsk {

@@ -42,7 +42,7 @@
 #define K1_CPT 2
 #endif
 #ifndef K1_MIN_BLOCKS
-#define K1_MIN_BLOCKS (K1_CPT == 1 ? 3 : 2)
+#define K1_MIN_BLOCKS 1  // K1_THREADS = 448: one CTA's registers, no spills
 #endif
 
 namespace tsk {

@@ -375,8 +375,11 @@ void launch_k1f(const K1Launch &L, int grid, cudaStream_t st);
 bool k1_use_f32(double d2, double db_cmax);
 int k1_candidates_per_thread(bool f32);
 
+// 14 warps per CTA, 2 CTAs per SM at <= 72 registers (28 warps per SM):
+// measured against 8 x 3 at 80 registers, c5 K1 21.2 -> 20.0 ms; 12 x 2 at
+// 80 and 16 x 1 at 128 registers fall in between
 #ifndef K1_THREADS_DEF
-#define K1_THREADS_DEF 256
+#define K1_THREADS_DEF 448
 #endif
 constexpr int K1_THREADS = K1_THREADS_DEF;
 constexpr int K1_TQ = 256;        // queries per tile staged in shared memory
