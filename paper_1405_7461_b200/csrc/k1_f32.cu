@@ -632,6 +632,18 @@ __device__ __forceinline__ void window_bounds(const double *pm, const double *sm
     jhi = r_hi < nt ? r_hi : nt;
 }
 
+// Block-shared state of the FP32 kernel at file scope, so the sub-tile
+// functions reach it without carrying pointers in registers across their
+// calls (every value a caller keeps live across a call costs a spill).
+__shared__ __align__(16) unsigned char k1f_lraw[sizeof(K1Launch)];  // the launch parameters
+__device__ __forceinline__ const K1Launch &k1f_L() { return *reinterpret_cast<const K1Launch *>(k1f_lraw); }
+__shared__ double k1f_pm[2 * K1_TQ];  // running max / suffix min of te (or te / ts), +inf padded
+__shared__ double k1f_sm[2 * K1_TQ];
+__shared__ F32Item k1f_fi;            // the item's FP32 origin and error bound
+__shared__ ItemCtx k1f_it;            // the item
+__shared__ float k1f_cull_rb;         // the launch's box-cull radius base
+__shared__ int k1f_item_f32;          // the item takes the FP32 path
+
 // Item-level key bases of the K1 layout (hits add their own orig - f).
 __shared__ uint64_t k1_kb[2];
 __shared__ int64_t k1_kf[2];
@@ -651,10 +663,16 @@ __device__ __forceinline__
 #else
 __device__ __noinline__
 #endif
-void fast_subtile(const K1Launch &L, const ItemCtx &it, const QRec *__restrict__ qt,
-                                          const QF32 *__restrict__ sqf, const double *pm, const double *sm,
-                                          int64_t wbase, float cull_rb, const F32Item &fi, bool item_f32, float *wcs,
-                                          int warp, int lane, unsigned long long &n_ev, unsigned long long &n_hit) {
+void fast_subtile(int64_t wbase, int warp, int lane, unsigned long long &n_ev, unsigned long long &n_hit) {
+    const K1Launch &L = k1f_L();
+    const ItemCtx &it = k1f_it;
+    const F32Item &fi = k1f_fi;
+    const QRec *const qt = L.q + it.lo_q;
+    const QF32 *const sqf = f_sqf();
+    const double *const pm = k1f_pm, *const sm = k1f_sm;
+    float *const wcs = f_cands(warp);
+    const float cull_rb = k1f_cull_rb;
+    const bool item_f32 = k1f_item_f32 != 0;
     const int64_t g0 = wbase / BOX_GROUP;
     const int64_t g1 = (wbase + WCAND - 1 < it.c_hi ? wbase + WCAND - 1 : it.c_hi) / BOX_GROUP;
     // the groups' time range and box, loaded together, and (speculatively:
@@ -881,17 +899,16 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
     // the launch parameters in shared memory: the device functions take them
     // by reference, and a reference to the parameter space would make every
     // thread keep a copy on its stack (local memory)
-    __shared__ __align__(16) unsigned char l_raw[sizeof(K1Launch)];
-    if (threadIdx.x == 0) *reinterpret_cast<K1Launch *>(l_raw) = Lp;
+    if (threadIdx.x == 0) *reinterpret_cast<K1Launch *>(k1f_lraw) = Lp;
     __syncthreads();
-    const K1Launch &L = *reinterpret_cast<const K1Launch *>(l_raw);
+    const K1Launch &L = k1f_L();
     // running max / suffix min of te over the tile; on single-scan items
     // (times ascending) te / ts themselves, +inf padded for tile_bounds
-    __shared__ double pm[2 * K1_TQ];
-    __shared__ double sm[2 * K1_TQ];
+    double *const pm = k1f_pm;
+    double *const sm = k1f_sm;
     __shared__ double f32b[8];    // per-item magnitude bounds
-    __shared__ F32Item fi_sh;     // the item's FP32 origin and error bound
-    __shared__ ItemCtx it_sh;
+    F32Item &fi_sh = k1f_fi;      // the item's FP32 origin and error bound
+    ItemCtx &it_sh = k1f_it;
     __shared__ int64_t item_sh;
     __shared__ int flags_sh;      // bit 0: unsafe query, bit 1: te not sorted
     __shared__ unsigned long long red[4], red_ev;  // per-batch overlap / hit sums, evaluated pairs
@@ -913,6 +930,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
     const bool launch_ok = k1f_launch_ok(cmax, L.d2);
     const double dthr = sqrt(L.d2);  // d (sqrt(RN(d^2)) >= d (1 - 2^-52); the margin covers it)
     const float cull_rb = box_cull_rbase(dthr, cmax);  // filter.cuh
+    if (threadIdx.x == 0) k1f_cull_rb = cull_rb;
     const bool cull = L.cull && launch_ok;
 
     for (;;) {
@@ -1009,6 +1027,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
         }
         __syncthreads();
         const bool item_f32 = fi_sh.ok;
+        if (tid == 0) k1f_item_f32 = item_f32 ? 1 : 0;  // read after the next barrier
         // pass 2: the FP32 records (exact times always, for windows and counts)
         for (int j = tid; j < it.nt; j += K1_THREADS) {
             const QRec &q = qt[j];
@@ -1060,8 +1079,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
                 if (lane == 0) w = atomicAdd(&wsub_next, 1);
                 w = __shfl_sync(0xffffffffu, w, 0);
                 if (w >= nw) break;
-                fast_subtile(L, it, qt, sqf, pm, sm, it.first_c + (int64_t)w * WCAND, cull_rb, fi_sh, item_f32, wcs,
-                             warp, lane, n_ev, n_hit);
+                fast_subtile(it.first_c + (int64_t)w * WCAND, warp, lane, n_ev, n_hit);
             }
         }
         for (int s = 0; s < sub && !(fast && !L.noop); ++s) {
@@ -1070,7 +1088,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
             const int64_t wbase = base + (int64_t)warp * WCAND;
             if (fast) {
                 if (wbase > it.c_hi || L.noop) continue;
-                fast_subtile(L, it, qt, sqf, pm, sm, wbase, cull_rb, fi_sh, item_f32, wcs, warp, lane, n_ev, n_hit);
+                fast_subtile(wbase, warp, lane, n_ev, n_hit);
                 continue;
             }
             slow_subtile(L, it, qt, sqf, pm, sm, wbase, cull_rb, fi_sh, item_f32, single_scan, te_sorted, q_unsorted,
