@@ -247,7 +247,7 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def parity_check(e, q, ix, lo, hi, rs, batch_hits, d, port_results, extra_ids):
+def parity_check(e, q, ix, lo, hi, rs, batch_hits, d, port_results, extra_ids, batch_ovl=None):
     """Bit-exact parity of the timed e2e result, per batch.
 
     * the batches the cpu_baseline leg evaluated with the numpy port of the
@@ -269,18 +269,20 @@ def parity_check(e, q, ix, lo, hi, rs, batch_hits, d, port_results, extra_ids):
             mism += 1
             bad.append(b)
     rep = check_batches(e, ix, q, lo, hi, {c: getattr(rs, c) for c in RES}, batch_hits,
-                        [b for b in extra_ids if b not in port_results], d)
+                        [b for b in extra_ids if b not in port_results], d, batch_overlaps=batch_ovl)
     ids = list(port_results)
     first, last = plan_spans(e, ix, q, lo[ids], hi[ids]) if ids else ([], [])
     for k, b in enumerate(ids):
         if first[k] >= 0:
             pairs += int((last[k] - first[k] + 1) * (hi[b] - lo[b] + 1))
     return {"batches": len(port_results) + rep["batches"], "pairs": pairs + rep["pairs"],
-            "hits": hits + rep["hits"], "mismatches": mism + rep["mismatches"],
+            "hits": hits + rep["hits"], "mismatches": mism + rep["mismatches"] + rep["overlap_mismatches"],
+            "overlap_mismatches": rep["overlap_mismatches"],
             "max_rel_interval_err": rep["max_rel_interval_err"], "bad_batches": (bad + rep["bad_batches"])[:10],
             "checker": f"{len(port_results)} batches vs the numpy port of the reference (the timed cpu_baseline "
                        f"batches) + {rep['batches']} evenly spread batches vs the C engine oracle "
-                       "(oracle/pair_oracle.c), bit-exact ids/order/intervals",
+                       "(oracle/pair_oracle.c), bit-exact ids/order/intervals, and those batches' temporal "
+                       "overlap counts (the miss statistics)",
             "seconds": rep["seconds"]}
 
 
@@ -476,11 +478,13 @@ def run_ours(args, cfg):
             res = search_device(store, index, mine, d, queries_resident=True)
     barrier()
     dev_ms, k1_ms, launches, work, hits, ovl, evals = 0.0, 0.0, 0, 0.0, 0, 0, 0
+    last_pb = None
     w0 = time.perf_counter()
     for _ in range(args.steps):
         if mine is None:
             continue
         r = search_device(store, index, mine, d, queries_resident=True)
+        last_pb = np.asarray(r.per_batch)
         dev_ms += r.device_ms
         k1_ms += r.k1_ms
         launches += r.launches
@@ -615,7 +619,8 @@ def run_ours(args, cfg):
             want_n = int(os.environ.get("TSK_PARITY_BATCHES", "48"))
             extra = [b for b in np.linspace(0, nb_all - 1, min(nb_all, 2 * want_n + len(port_res))).astype(int)
                      .tolist() if b not in port_res][:want_n]
-            parity = parity_check(e, q, ix, lo_t, hi_t, rs, bh, d, port_res, extra)
+            parity = parity_check(e, q, ix, lo_t, hi_t, rs, bh, d, port_res, extra,
+                                  batch_ovl=None if last_pb is None else last_pb[:, 2])
             log(f"[parity] {parity['batches']} batches, {parity['pairs']} pairs, {parity['hits']} hits, "
                 f"{parity['mismatches']} mismatching batches ({parity['seconds']:.1f}s)")
 
@@ -702,9 +707,14 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true",
                     help="skip the bit-exact check of the e2e result against the oracle (N=1)")
+    ap.add_argument("--s", type=int, default=None,
+                    help="batch size of the planner (default 120; SURVEY.md §8d sweeps c2 over 60/120/240)")
     ap.add_argument("--planner", choices=sorted(PLANNERS), default="periodic",
                     help="batch planner (config 4 compares them; PAPER.md Table 3)")
     args = ap.parse_args()
+    if args.s is not None:
+        global S_BATCH
+        S_BATCH = int(args.s)
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)

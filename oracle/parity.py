@@ -23,7 +23,7 @@ RES = ("query_traj", "query_seg", "entry_traj", "entry_seg", "t_begin", "t_end")
 
 
 def check_batches(store, ix, queries, lo, hi, result_cols, batch_hits, batch_ids, d, *,
-                  first=None, last=None, threads=None):
+                  first=None, last=None, threads=None, batch_overlaps=None):
     """Compare batches ``batch_ids`` of a plan's result with the oracle.
 
     store / queries: dicts of sorted columns (traj seg xs ys zs ts xe ye ze te);
@@ -69,6 +69,16 @@ def check_batches(store, ix, queries, lo, hi, result_cols, batch_hits, batch_ids
                 h = want[c][w][:n]
                 err = np.abs(g - h) / np.maximum(np.abs(h), 1e-300)
                 max_err = max(max_err, float(np.nanmax(err)))
+    # per-batch temporal overlaps (interactions - temporal misses), when the
+    # caller has them (the reference's miss statistics, engine.py:52-55)
+    ovl_bad = []
+    if batch_overlaps is not None:
+        for k, b in enumerate(ids):
+            ints = int((last[k] - first[k] + 1) * (hi[b] - lo[b] + 1)) if first[k] >= 0 else 0
+            if int(batch_overlaps[b]) != ints - int(pb[k, 1]):
+                ovl_bad.append(int(b))
     return {"batches": int(ids.shape[0]), "pairs": pairs, "hits": int(pb[:, 0].sum()),
+            "temporal_misses": int(pb[:, 1].sum()), "spatial_misses": int(pb[:, 2].sum()),
+            "overlap_mismatches": len(ovl_bad), "bad_overlap_batches": ovl_bad[:10],
             "mismatches": mism, "max_rel_interval_err": max_err, "bad_batches": bad[:10],
             "seconds": time.perf_counter() - t0}

@@ -557,7 +557,7 @@ void launch_ranges(tsk_db *db, const Soa &q, SearchPlanDev &p, bool spans_given,
 // the grid gets at least ~4 waves of items, then count items per work unit
 // (plan_unit: batch pairs sharing candidates, and the rest) and scan them.
 __global__ void __launch_bounds__(1024, 1) k_plan_items(SearchPlanDev p, int64_t slots, int stride, int pair,
-                                                         int align) {
+                                                         int align, int tq_max, const int *q_flags) {
     typedef cub::BlockReduce<long long, 1024> BR;
     typedef cub::BlockScan<long long, 1024> BS;
     __shared__ union {
@@ -567,12 +567,12 @@ __global__ void __launch_bounds__(1024, 1) k_plan_items(SearchPlanDev p, int64_t
     __shared__ long long carry, tiles_sh;
     __shared__ int sub_sh;
     const int64_t nb = p.nb;
-    // query tile: K1_TQ, halved (down to 32) while the grid would get fewer
+    // query tile: tq_max (the kernel's), halved (down to 32) while the grid would get fewer
     // than 4 waves of single-batch items — small plans otherwise under-fill
     // 148 SMs
     const long long want = 4 * slots;
-    int tqs = K1_TQ;
-    for (;;) {  // pair == 2 (testing): full tiles, always pair
+    int tqs = tq_max;
+    for (;;) {  // pair == 2 / 5 (testing): full tiles, always pairs / quads
         long long acc = 0;
         for (int64_t b = threadIdx.x; b < nb; b += blockDim.x) {
             long long c = p.first[b] >= 0 ? p.last[b] - p.first[b] + 1 : 0;
@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(1024, 1) k_plan_items(SearchPlanDev p, int64_t
         __syncthreads();
         tiles = tiles_sh;
         __syncthreads();
-        if (tiles >= want || tqs <= 32 || pair == 2) break;
+        if (tiles >= want || tqs <= 32 || pair == 2 || pair == 5) break;
         tqs >>= 1;
     }
     if (threadIdx.x == 0) {
@@ -596,10 +596,18 @@ __global__ void __launch_bounds__(1024, 1) k_plan_items(SearchPlanDev p, int64_t
         carry = 0;
     }
     __syncthreads();
-    // pairing only when the plan is big enough to fill the grid with full tiles
-    const int pr = pair == 2 || (pair && tqs == K1_TQ);
+    // sharing only when the plan is big enough to fill the grid with full
+    // tiles: quads (pair == 4) when the kernel's box-cull fast path takes
+    // every item — query start and end times both sorted (q_flags bits 0, 1
+    // from the query kernel) — else pairs
+    int mode = K1_SHARE_NONE;
+    if (pair == 2) mode = K1_SHARE_PAIRS;  // testing: forced, full tiles
+    else if (pair == 5) mode = (q_flags && (*q_flags & 3) == 0) ? K1_SHARE_QUADS : K1_SHARE_PAIRS;
+    else if (pair && tqs == tq_max)
+        mode = (pair == 4 && q_flags && (*q_flags & 3) == 0) ? K1_SHARE_QUADS : K1_SHARE_PAIRS;
+    const int pr = mode;
     const long long ct = (long long)stride * sub_sh;
-    const int64_t nu = plan_units(nb);
+    const int64_t nu = plan_units_mode(nb, mode);
     for (int64_t base = 0; base < nu; base += blockDim.x) {
         int64_t u = base + threadIdx.x;
         long long v = 0;
@@ -629,8 +637,9 @@ __global__ void __launch_bounds__(1024, 1) k_plan_items(SearchPlanDev p, int64_t
     }
 }
 
-void launch_plan_items(SearchPlanDev &p, int slots, int stride, int pair, int align, cudaStream_t st) {
-    k_plan_items<<<1, 1024, 0, st>>>(p, slots, stride, pair, align);
+void launch_plan_items(SearchPlanDev &p, int slots, int stride, int pair, int align, int tq_max, const int *q_flags,
+                       cudaStream_t st) {
+    k_plan_items<<<1, 1024, 0, st>>>(p, slots, stride, pair, align, tq_max, q_flags);
     TSK_CUDA(cudaGetLastError());
 }
 

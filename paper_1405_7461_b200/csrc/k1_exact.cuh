@@ -144,8 +144,9 @@ struct ItemCtx {
     int64_t b, lo_q, first_c, c_hi;  // batch, tile's first query ordinal, tile's candidate range
     int64_t c_lo;                    // first valid candidate (first_c may be aligned below it)
     int64_t q0;                      // first query offset within batch b (tile)
-    int64_t b1;                      // shared unit: the second batch (queries js..nt-1), else -1
+    int64_t b1;                      // shared unit: the second batch (queries js..), else -1
     int nt, js;                      // staged queries; queries of batch b (nt when single)
+    int js2, js3;                    // quads: tile offsets of batches b + 2, b + 3 (nt when absent)
 };
 
 // Per-item counters are kept per batch in one 64-bit word: the low half
@@ -262,13 +263,15 @@ struct __align__(16) QF32 {
 
 // Per-warp context of the current sub-tile, read by the flush.
 struct WarpCtx {
-    uint64_t key_base0;     // key of (b, e_off of candidate 0, it.q0) without the j term
-    uint64_t key_base1;     // the same for b1 (query offset 0 at tile index js)
-    int64_t f0, f1;         // first candidate ordinal of b / b1 (K1 layout: e_off = orig - f)
-    int js;                 // tile index of b1's first query (nt when single)
+    uint64_t key_base[4];   // key of (b + g, e_off of candidate 0, query offset 0) without the j term
+                            // (g = 0: it.q0; g >= 1: the batch's first query at tile index js_g)
+    int64_t f[4];           // first candidate ordinal of batch b + g (K1 layout: e_off = orig - f)
+    int js;                 // tile index of batch b + 1's first query (nt when single)
+    int js2, js3;           // ... of b + 2, b + 3 (quads; nt when absent)
     double wmin_te, wmax;   // min te / max te of the warp's candidates (tb cases)
     int64_t wbase;          // entry ordinal of the warp's candidate 0
     int nvalid;             // valid candidates of the warp (the rest are past the item)
+    int nlo;                // ... from this index on (the masked head of a tile aligned below c_lo)
 };
 
 // Block-shared state of K1 (both kernels): the flush configuration and the
@@ -276,6 +279,7 @@ struct WarpCtx {
 // hot loops carry none of it in registers.
 __shared__ FlushCfg k1_fcfg;
 __shared__ WarpCtx k1_wctx[K1_WARPS];
+__shared__ unsigned long long k1_hits23[2];  // per item: hits of batches b + 2, b + 3 (quads)
 
 __device__ __forceinline__ void append_hit_w(const FlushCfg &C, bool hit, uint64_t key, double tb,
                                              double te, int lane) {
@@ -308,7 +312,7 @@ __device__ __noinline__ void rare_flush(const QRec *__restrict__ qt, const uint3
     h.hit = false;
     h.tb = h.te = 0.0;
     uint64_t key = 0;
-    bool second = false;
+    int g = 0;
     const uint32_t ent = lane < n_items ? wq[lane] : 0u;
     const int ci = (int)(ent >> 16), j = (int)(ent & 0xffffu);
     // candidates past the item's range can be queued (flagged with a huge
@@ -336,18 +340,21 @@ __device__ __noinline__ void rare_flush(const QRec *__restrict__ qt, const uint3
         if (ex && (flat || !plain || !(e > m) || !(q1 > m) || vertex_in))
             h = rare_pair(r, *qrec, cc, aa, dot, e, d2);
         // candidate ci shifts the entry offset, query j the query offset,
-        // within the batch the query belongs to
-        second = j >= k1_wctx[warp].js;
-        const uint64_t jj = (uint64_t)(second ? j - k1_wctx[warp].js : j);
+        // within the batch the query belongs to (g: which of the tile's
+        // batches, from the tile offsets where they start)
+        const int js = k1_wctx[warp].js, js2 = k1_wctx[warp].js2, js3 = k1_wctx[warp].js3;
+        g = (j >= js) + (j >= js2) + (j >= js3);
+        const int jb = g == 0 ? 0 : (g == 1 ? js : (g == 2 ? js2 : js3));
+        const uint64_t jj = (uint64_t)(j - jb);
         // the entry term: the candidate's offset in the warp, or in the K1
         // layout its start-sorted ordinal's offset within the batch's range
-        const uint64_t et = C.orig ? (uint64_t)(C.orig[k1_wctx[warp].wbase + ci] -
-                                                (second ? k1_wctx[warp].f1 : k1_wctx[warp].f0))
-                                   : (uint64_t)ci;
-        key = (second ? k1_wctx[warp].key_base1 : k1_wctx[warp].key_base0) +
-              (C.query_major ? (jj << C.minor_bits) + et : (et << C.minor_bits) + jj);
+        const uint64_t et = C.orig ? (uint64_t)(C.orig[k1_wctx[warp].wbase + ci] - k1_wctx[warp].f[g]) : (uint64_t)ci;
+        key = k1_wctx[warp].key_base[g] + (C.query_major ? (jj << C.minor_bits) + et : (et << C.minor_bits) + jj);
     }
-    n_hit += h.hit ? (second ? CNT_B1 : 1ull) : 0ull;
+    // batches b and b + 1 count in the halves of the lane's counter; b + 2
+    // and b + 3 (quads) in block counters (hits are rare)
+    n_hit += h.hit && g < 2 ? (g ? CNT_B1 : 1ull) : 0ull;
+    if (h.hit && g >= 2) atomicAdd(&k1_hits23[g - 2], 1ull);
     append_hit_w(C, h.hit, key, h.tb, h.te, lane);
 }
 
@@ -466,30 +473,33 @@ __device__ __forceinline__ double warp_max(double v) {
 // unit has one tile holding both batches' queries).
 __device__ __forceinline__ ItemCtx decode_item(const K1Launch &L, int64_t item, int64_t ct, int64_t tqs) {
     // unit = last u with item_off[u] <= item (a non-empty unit)
-    int64_t a = 0, z = plan_units(L.plan.nb);
+    const int mode = (int)L.plan.meta[3];
+    int64_t a = 0, z = plan_units_mode(L.plan.nb, mode);
     while (z - a > 1) {
         int64_t m = (a + z) >> 1;
         if (L.plan.item_off[m] <= item) a = m;
         else z = m;
     }
-    const Unit U = plan_unit(L.plan, a, tqs, (int)L.plan.meta[3]);
+    const Unit U = plan_unit(L.plan, a, tqs, mode);
     const int64_t local = item - L.plan.item_off[a];
     ItemCtx c;
     c.b = U.b;
     c.b1 = U.b1;
     int64_t tc;
-    if (U.b1 >= 0) {  // shared: one tile with both batches' queries
+    if (U.b1 >= 0) {  // shared: one tile with all the group's queries
         tc = local;
         c.q0 = 0;
         c.nt = (int)U.s;
         c.js = (int)U.js;
+        c.js2 = (int)U.js2;
+        c.js3 = (int)U.js3;
     } else {
         const int64_t tq_n = (U.s + tqs - 1) / tqs;
         const int64_t tq = local % tq_n;
         tc = local / tq_n;
         c.q0 = tq * tqs;
         c.nt = (int)(U.s - c.q0 < tqs ? U.s - c.q0 : tqs);
-        c.js = c.nt;
+        c.js = c.js2 = c.js3 = c.nt;
     }
     c.lo_q = U.lo_q + c.q0;
     // K1 layout (L.cull): tiles start at a BOX_GROUP multiple (k_plan_items
@@ -522,16 +532,17 @@ __device__ __forceinline__ void fill_flush_cfg(const K1Launch &L) {
 // offset of candidate 0 is folded in; with one each hit adds its own
 // (orig - f).
 __device__ __forceinline__ void set_key_bases(const K1Launch &L, const ItemCtx &it, int64_t wbase, int warp) {
-    const int64_t f0 = L.plan.first[it.b], f1 = it.b1 >= 0 ? L.plan.first[it.b1] : 0;
-    if (L.orig) {
-        k1_wctx[warp].key_base0 = make_key(L, it.b, 0, it.q0);
-        k1_wctx[warp].key_base1 = it.b1 >= 0 ? make_key(L, it.b1, 0, 0) : 0;
-    } else {
-        k1_wctx[warp].key_base0 = make_key(L, it.b, wbase - f0, it.q0);
-        k1_wctx[warp].key_base1 = it.b1 >= 0 ? make_key(L, it.b1, wbase - f1, 0) : 0;
+    const int nb = it.b1 < 0 ? 1 : (it.js2 >= it.nt ? 2 : (it.js3 >= it.nt ? 3 : 4));
+    for (int g = 0; g < 4; ++g) {
+        const int64_t b = it.b + g;
+        const int64_t f = g < nb ? L.plan.first[b] : 0;
+        const int64_t q0 = g == 0 ? it.q0 : 0;
+        k1_wctx[warp].f[g] = f;
+        k1_wctx[warp].key_base[g] = g >= nb ? 0 : (L.orig ? make_key(L, b, 0, q0) : make_key(L, b, wbase - f, q0));
     }
-    k1_wctx[warp].f0 = f0;
-    k1_wctx[warp].f1 = f1;
+    k1_wctx[warp].js = it.js;
+    k1_wctx[warp].js2 = it.js2;
+    k1_wctx[warp].js3 = it.js3;
 }
 
 // Running max (warp 0) / suffix min (warp 1) of the tile's end times.
@@ -632,6 +643,11 @@ __device__ __forceinline__ void item_counters(const K1Launch &L, const ItemCtx &
         if (red[1]) atomicAdd(&L.plan.hits[it.b], red[1]);
         if (it.b1 >= 0 && red[2]) atomicAdd(&L.plan.ovl[it.b1], red[2]);
         if (it.b1 >= 0 && red[3]) atomicAdd(&L.plan.hits[it.b1], red[3]);
+        if (it.b1 >= 0 && it.js2 < it.nt) {  // quads: batches b + 2, b + 3 (rare_flush counted them)
+            if (k1_hits23[0]) atomicAdd(&L.plan.hits[it.b + 2], k1_hits23[0]);
+            if (it.js3 < it.nt && k1_hits23[1]) atomicAdd(&L.plan.hits[it.b + 3], k1_hits23[1]);
+        }
+        k1_hits23[0] = k1_hits23[1] = 0;  // for the next item (the barrier below orders it)
         if (red_ev && *red_ev) atomicAdd(L.eval_count, *red_ev);
     }
     __syncthreads();

@@ -139,12 +139,13 @@ __device__ __noinline__ uint4 f32_scan(uint32_t qa, uint32_t qa_end, uint32_t ba
     double rts[CPT], rte[CPT];
     if (CNT) {
         const int64_t wb = k1_wctx[warp].wbase;
-        const int nv = k1_wctx[warp].nvalid;
+        const int nv = k1_wctx[warp].nvalid, nlo = k1_wctx[warp].nlo;
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
             const int i = k * 32 + lane;
-            rts[k] = i < nv ? k1_fcfg.ts[wb + i] : INFINITY;   // invalid lanes never overlap
-            rte[k] = i < nv ? k1_fcfg.te[wb + i] : -INFINITY;
+            const bool valid = i >= nlo && i < nv;  // (a K1-layout tile's head below c_lo is another unit's)
+            rts[k] = valid ? k1_fcfg.ts[wb + i] : INFINITY;   // invalid lanes never overlap
+            rte[k] = valid ? k1_fcfg.te[wb + i] : -INFINITY;
         }
     }
     unsigned long long n_ov = 0;
@@ -609,25 +610,28 @@ __device__ __forceinline__ void stage_pair(const K1Launch &L, int64_t wbase, int
 }
 
 // jlo = #{j < nt : pm[j] < x} (pm ascending) and jhi = #{j < nt : sm[j] <= y}
-// (sm ascending), both arrays +inf padded to 2 K1_TQ >= 256: two 16-ary
-// rounds, lanes 0-15 on pm and 16-31 on sm (a shared load, a ballot and a
-// popcount each) instead of two serial 9-step bisections.
-static_assert(K1_TQ <= 256, "window_bounds covers 256 queries");
+// (sm ascending), both arrays +inf padded to 2 K1_TQ: 16-ary rounds, lanes
+// 0-15 on pm and 16-31 on sm (a shared load, a ballot and a popcount each:
+// two rounds for 256 queries, three for 512) instead of two serial
+// bisections.
+static_assert(K1_TQ == 256 || K1_TQ == 512, "window_bounds covers 256 or 512 queries");
 __device__ __forceinline__ void window_bounds(const double *pm, const double *sm, int nt, double x, double y, int lane,
                                               int &jlo, int &jhi) {
     const int l = lane & 15;
     const bool lo_half = lane < 16;
     const double *a = lo_half ? pm : sm;
-    // round 1: block l of 16 entries ends at 16 l + 15
-    const double v1 = a[16 * l + 15];
-    const unsigned m1 = __ballot_sync(0xffffffffu, lo_half ? v1 < x : v1 <= y);
-    const int c_lo = __popc(m1 & 0xffffu), c_hi = __popc(m1 >> 16);
-    // round 2: inside the first block not entirely below the bound
-    const int base = 16 * (lo_half ? c_lo : c_hi);
-    const double v2 = base + l < 2 * K1_TQ ? a[base + l] : INFINITY;
-    const unsigned m2 = __ballot_sync(0xffffffffu, lo_half ? v2 < x : v2 <= y);
-    const int r_lo = 16 * c_lo + (c_lo < 16 ? __popc(m2 & 0xffffu) : 0);
-    const int r_hi = 16 * c_hi + (c_hi < 16 ? __popc(m2 >> 16) : 0);
+    int r_lo = 0, r_hi = 0;
+#pragma unroll
+    for (int step = K1_TQ / 16; step >= 1; step = step >= 16 ? step / 16 : (step > 1 ? 1 : 0)) {
+        // block l of `step` entries past the current bound ends at r + step (l + 1) - 1
+        const int r = lo_half ? r_lo : r_hi;
+        const int idx = r + step * (l + 1) - 1;
+        const double v = idx < 2 * K1_TQ ? a[idx] : INFINITY;
+        const unsigned m = __ballot_sync(0xffffffffu, lo_half ? v < x : v <= y);
+        r_lo += step * __popc(m & 0xffffu);
+        r_hi += step * __popc(m >> 16);
+        if (step == 1) break;
+    }
     jlo = r_lo < nt ? r_lo : nt;
     jhi = r_hi < nt ? r_hi : nt;
 }
@@ -645,8 +649,8 @@ __shared__ float k1f_cull_rb;         // the launch's box-cull radius base
 __shared__ int k1f_item_f32;          // the item takes the FP32 path
 
 // Item-level key bases of the K1 layout (hits add their own orig - f).
-__shared__ uint64_t k1_kb[2];
-__shared__ int64_t k1_kf[2];
+__shared__ uint64_t k1_kb[4];  // per batch of the tile (pairs: 2, quads: 4)
+__shared__ int64_t k1_kf[4];
 
 // One warp sub-tile on the box-cull fast path (K1 layout, overlaps counted
 // outside K1).  The window is every query whose extent meets the time range
@@ -703,14 +707,18 @@ void fast_subtile(int64_t wbase, int warp, int lane, unsigned long long &n_ev, u
     K1_STAT(3, ns > 0);
     if (ns == 0) return;
     if (lane == 0) {
-        k1_wctx[warp].key_base0 = k1_kb[0];
-        k1_wctx[warp].key_base1 = k1_kb[1];
-        k1_wctx[warp].f0 = k1_kf[0];
-        k1_wctx[warp].f1 = k1_kf[1];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            k1_wctx[warp].key_base[g] = k1_kb[g];
+            k1_wctx[warp].f[g] = k1_kf[g];
+        }
         k1_wctx[warp].js = it.js;
+        k1_wctx[warp].js2 = it.js2;
+        k1_wctx[warp].js3 = it.js3;
         k1_wctx[warp].wbase = wbase;
         const int64_t nv = it.c_hi - wbase + 1;
         k1_wctx[warp].nvalid = nv < 0 ? 0 : (nv > WCAND ? WCAND : (int)nv);
+        k1_wctx[warp].nlo = it.c_lo > wbase ? (int)(it.c_lo - wbase < WCAND ? it.c_lo - wbase : WCAND) : 0;
         // the exact path picks each pair's tb case itself (TB_DYN, open bounds)
         k1_wctx[warp].wmin_te = -INFINITY;
         k1_wctx[warp].wmax = INFINITY;
@@ -810,6 +818,7 @@ __device__ __noinline__ void slow_subtile(const K1Launch &L, const ItemCtx &it, 
             k1_wctx[warp].wbase = wbase;
             const int64_t nv = it.c_hi - wbase + 1;
             k1_wctx[warp].nvalid = nv < 0 ? 0 : (nv > WCAND ? WCAND : (int)nv);
+            k1_wctx[warp].nlo = it.c_lo > wbase ? (int)(it.c_lo - wbase < WCAND ? it.c_lo - wbase : WCAND) : 0;
             k1_wctx[warp].wmin_te = wmin_te;
             k1_wctx[warp].wmax = wmax;
         }
@@ -915,7 +924,10 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
     __shared__ int wsub_next;     // fast path: the item's next unclaimed warp sub-tile
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) fill_flush_cfg(L);
+    if (tid == 0) {
+        fill_flush_cfg(L);
+        k1_hits23[0] = k1_hits23[1] = 0;
+    }
     QF32 *const sqf = f_sqf();
     float *const wcs = f_cands(warp);
     const int64_t total = L.plan.meta[0];
@@ -1018,11 +1030,12 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
             // separating-axis stage: M2 = A_r + TV_r + (T_q + E_q) V_r + A_q + D_q
             const double M2 = f32b[0] + f32b[1] + (f32b[4] + f32b[5] + f32b[7]) * f32b[2] + f32b[3] + f32b[6];
             k1_sep_rb = f32_sep_rbase(dthr, cmax, M2);
-            if (L.orig) {  // K1 layout: key bases are per item
-                k1_kf[0] = L.plan.first[it.b];
-                k1_kf[1] = it.b1 >= 0 ? L.plan.first[it.b1] : 0;
-                k1_kb[0] = make_key(L, it.b, 0, it.q0);
-                k1_kb[1] = it.b1 >= 0 ? make_key(L, it.b1, 0, 0) : 0;
+            if (L.orig) {  // K1 layout: key bases are per item and batch
+                const int nbat = it.b1 < 0 ? 1 : (it.js2 >= it.nt ? 2 : (it.js3 >= it.nt ? 3 : 4));
+                for (int g = 0; g < 4; ++g) {
+                    k1_kf[g] = g < nbat ? L.plan.first[it.b + g] : 0;
+                    k1_kb[g] = g < nbat ? make_key(L, it.b + g, 0, g == 0 ? it.q0 : 0) : 0;
+                }
             }
         }
         __syncthreads();

@@ -172,18 +172,21 @@ __device__ __forceinline__ void run_cases(const QRec *__restrict__ sq, int nt, i
 }
 
 __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L) {
-    __shared__ QRec sq[K1_TQ];
-    __shared__ double pm[K1_TQ];  // running max of te over the tile
-    __shared__ double sm[K1_TQ];  // suffix min of te over the tile
+    __shared__ QRec sq[K1P_TQ];
+    __shared__ double pm[K1P_TQ];  // running max of te over the tile
+    __shared__ double sm[K1P_TQ];  // suffix min of te over the tile
     __shared__ ItemCtx it_sh;
     __shared__ int64_t item_sh;
     __shared__ unsigned long long red[4];  // per-batch overlap / hit sums
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) fill_flush_cfg(L);
+    if (tid == 0) {
+        fill_flush_cfg(L);
+        k1_hits23[0] = k1_hits23[1] = 0;
+    }
     const int64_t total = L.plan.meta[0];
     const int sub = (int)L.plan.meta[1];
-    const int64_t tqs = L.plan.meta[2];  // query tile size chosen by k_plan_items (<= K1_TQ)
+    const int64_t tqs = L.plan.meta[2];  // query tile size chosen by k_plan_items (<= K1P_TQ)
     constexpr int64_t STRIDE = (int64_t)K1_THREADS * K1_CPT;  // candidates per sub-tile
     const int64_t ct = STRIDE * sub;
     // filter constants (filter.cuh); C = max |coordinate| of entries and queries
@@ -260,6 +263,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
                 k1_wctx[warp].wbase = wbase;
                 const int64_t nv = it.c_hi - wbase + 1;
                 k1_wctx[warp].nvalid = nv < 0 ? 0 : (nv > 32 * K1_CPT ? 32 * K1_CPT : (int)nv);
+                k1_wctx[warp].nlo = it.c_lo > wbase ? (int)(it.c_lo - wbase < 32 * K1_CPT ? it.c_lo - wbase : 32 * K1_CPT) : 0;
                 k1_wctx[warp].wmin_te = wmin_te;
                 k1_wctx[warp].wmax = wmax;
             }

@@ -442,7 +442,7 @@ static void sort_rows(tsk_db *db, const uint64_t *keys, uint64_t *ko, uint32_t *
 }
 
 static tsk_result *run_pipelined(tsk_db *db, const tsk_columns *qc, const SearchPlanDev &plan, K1Launch L,
-                                 int slots, int stride, int pair, int align, int major_bits, int minor_bits, int bb,
+                                 int slots, int stride, int pair, int align, int tq_max, int major_bits, int minor_bits, int bb,
                                  uint64_t cap, Trace &tr, int64_t &launches) {
     const int64_t nb = plan.nb;
     // chunks: worth it once the rows' PCIe time is noticeable (the previous
@@ -556,7 +556,7 @@ static tsk_result *run_pipelined(tsk_db *db, const tsk_columns *qc, const Search
         pin_free(h_qo, qgot);
     };
     auto enqueue_k1 = [&](int c) {
-        launch_plan_items(pc[c], slots, stride, pair, align, st);
+        launch_plan_items(pc[c], slots, stride, pair, align, tq_max, L.q_unsorted, st);
         ++launches;
         TSK_CUDA(cudaMemsetAsync(d_ctr, 0, 8, st));  // the item counter
         if (L.ext_count) {
@@ -874,6 +874,7 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     const bool use_k = !spans_given && db->k.built;
     const int cull = (use_k && !(sp_env && !strcmp(sp_env, "nocull"))) ? 1 : 0;
     const int k1_stride = K1_THREADS * k1_candidates_per_thread(k1_f32), k1_align = cull ? BOX_GROUP : 1;
+    const int k1_tq_max = k1_f32 ? K1_TQ : K1P_TQ;
     launches += spans_given ? 0 : 1;
 
     db->counters.reserve(64, st);
@@ -916,18 +917,26 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     // counts only: no hit rows are written (cap 0), so no regrow and no K4
     const bool count_only = flags & (TSK_COUNT_ONLY | TSK_OVERLAPS_ONLY);
     L.q_unsorted = db->counters.as<int>() + 8;
+    // quads of batches per tile when every item takes the box-cull fast path
+    // (k_plan_items confirms the query order on the device); TSK_K1_QUADS=off
+    // (testing) keeps pairs
+    {
+        const char *qe = getenv("TSK_K1_QUADS");
+        if (pair == 1 && L.cull && L.ext_count && k1_tq_max >= 512 && !(qe && !strcmp(qe, "off")))
+            pair = (qe && !strcmp(qe, "force")) ? 5 : 4;  // force: quads on small plans too (testing)
+    }
     // reference-ordered results through the compact path: K1 chunk by chunk,
     // each chunk's rows sorted, gathered and copied while later chunks run
     const bool on_device_early = flags & TSK_RESULTS_ON_DEVICE;
     if (!count_only && !L.noop && ordered && !query_major && !canonical && !(flags & TSK_WANT_ORDINALS) &&
         !on_device_early && qc->traj && qc->seg && nq <= 0xffffffffll) {
-        tsk_result *pres = run_pipelined(db, qc, plan, L, slots, k1_stride, pair, k1_align, major_bits, minor_bits,
+        tsk_result *pres = run_pipelined(db, qc, plan, L, slots, k1_stride, pair, k1_align, k1_tq_max, major_bits, minor_bits,
                                          bb, cap, tr, launches);
         if (pres) return pres;
         // a chunk overflowed the result buffer: the plain path below sizes it
         // exactly (and the next call's pipeline fits)
     }
-    launch_plan_items(plan, slots, k1_stride, pair, k1_align, st);
+    launch_plan_items(plan, slots, k1_stride, pair, k1_align, k1_tq_max, L.q_unsorted, st);
     ++launches;
     tr.mark("ranges+items");
     unsigned long long h_ctr[2] = {0, 0};  // hits, evaluated pairs

@@ -241,23 +241,122 @@ struct SearchPlanDev {
     unsigned long long *ovl, *hits;  // per batch
 };
 
-// Work units of a plan (k_plan_items / K1).  Batches are taken in pairs
-// (2k, 2k+1); unit 5k+0 is the candidate range the pair shares, evaluated
-// against both batches' queries in one tile (when they fit), units
-// 5k+1/5k+2 are batch 2k's candidates left/right of it and 5k+3/5k+4 batch
-// 2k+1's.  A pair that cannot share (a batch without candidates, disjoint
-// ranges, queries beyond one tile, batches not adjacent in the query order,
-// or pairing off) leaves unit 5k+0 empty and
-// puts each batch's whole range in its left unit.  Every (candidate, query)
-// pair of the plan is in exactly one unit.
+// Work units of a plan (k_plan_items / K1), in the plan's sharing mode
+// (meta[3]).
+//  * Pairs (and no sharing): batches are taken in pairs (2k, 2k+1); unit
+//    5k+0 is the candidate range the pair shares, evaluated against both
+//    batches' queries in one tile (when they fit), units 5k+1/5k+2 are batch
+//    2k's candidates left/right of it and 5k+3/5k+4 batch 2k+1's.  A pair
+//    that cannot share (a batch without candidates, disjoint ranges, queries
+//    beyond one tile, batches not adjacent in the query order, or sharing
+//    off) leaves unit 5k+0 empty and puts each batch's whole range in its
+//    left unit.
+//  * Quads: batches are taken in groups of four, whose candidate ranges
+//    [f_g, l_g] usually advance together (time-sorted queries): with f and
+//    l both non-decreasing, the batches holding a candidate c are the
+//    contiguous run [ga, gb] (gb: last g with f_g <= c, ga: first g with
+//    l_g >= c), so the group's range splits at the sorted boundaries
+//    {f_g, l_g + 1} into at most 7 segments, each evaluated once against its
+//    run's queries (one tile of up to 4 batches): a "staircase" that visits
+//    each candidate once per group.  A group that is not monotone, not
+//    adjacent in the query order or too large for a tile takes one unit per
+//    batch (its whole range).
+// Every (candidate, query) pair of the plan is in exactly one unit.
+constexpr int K1_SHARE_NONE = 0, K1_SHARE_PAIRS = 1, K1_SHARE_QUADS = 4;
+
 struct Unit {
-    int64_t b, b1;    // batch, second batch of a shared unit (else -1)
-    int64_t lo_q, s;  // first query ordinal and query count (both batches for a shared unit)
-    int64_t js;       // queries of b (s when single)
+    int64_t b, b1;    // first batch, second batch of a multi-batch unit (else -1)
+    int64_t lo_q, s;  // first query ordinal and query count (all the unit's batches)
+    int64_t js;       // tile offset of the second batch's queries (s when single)
+    int64_t js2, js3; // ... of the third and fourth (s when absent)
     int64_t f, l;     // candidate segment (empty when f > l)
 };
 
-__device__ __forceinline__ Unit plan_unit(const SearchPlanDev &p, int64_t u, int64_t tqs, int pair) {
+__host__ __device__ __forceinline__ int64_t plan_units_mode(int64_t nb, int mode) {
+    return mode == K1_SHARE_QUADS ? 7 * ((nb + 3) / 4) : 5 * ((nb + 1) / 2);
+}
+// the most any mode needs (buffer sizing)
+__host__ __device__ __forceinline__ int64_t plan_units(int64_t nb) {
+    const int64_t a = plan_units_mode(nb, K1_SHARE_PAIRS), b = plan_units_mode(nb, K1_SHARE_QUADS);
+    return a > b ? a : b;
+}
+
+__device__ __forceinline__ Unit plan_unit_quads(const SearchPlanDev &p, int64_t u, int64_t tqs) {
+    const int64_t k = u / 7, kind = u % 7;
+    const int64_t b0 = 4 * k;
+    const int gc = (int)(p.nb - b0 < 4 ? p.nb - b0 : 4);
+    int64_t f[4], l[4], sg[4];
+    bool mono = true;
+    int64_t stot = 0;
+    for (int g = 0; g < gc; ++g) {
+        const int64_t b = b0 + g;
+        f[g] = p.first[b];
+        l[g] = p.last[b];
+        sg[g] = p.hi[b] - p.lo[b] + 1;
+        stot += sg[g];
+        mono = mono && f[g] >= 0 &&
+               (g == 0 || (f[g] >= f[g - 1] && l[g] >= l[g - 1] && p.lo[b] == p.hi[b - 1] + 1));
+    }
+    mono = mono && stot <= tqs;
+    Unit U;
+    U.b1 = -1;
+    U.f = 1;
+    U.l = 0;  // empty
+    if (!mono) {  // one unit per batch
+        const int g = kind < gc ? (int)kind : 0;
+        U.b = b0 + g;
+        U.lo_q = p.lo[U.b];
+        U.s = U.js = U.js2 = U.js3 = sg[g];
+        if (kind < gc && f[g] >= 0) {
+            U.f = f[g];
+            U.l = l[g];
+        }
+        return U;
+    }
+    // sorted segment boundaries {f_g, l_g + 1}
+    int64_t bd[8];
+    int nbd = 0;
+    for (int g = 0; g < gc; ++g) {
+        bd[nbd++] = f[g];
+        bd[nbd++] = l[g] + 1;
+    }
+    for (int i = 1; i < nbd; ++i)
+        for (int j = i; j > 0 && bd[j - 1] > bd[j]; --j) {
+            const int64_t t = bd[j];
+            bd[j] = bd[j - 1];
+            bd[j - 1] = t;
+        }
+    U.b = b0;
+    U.lo_q = p.lo[b0];
+    U.s = U.js = U.js2 = U.js3 = sg[0];
+    if (kind + 1 >= nbd) return U;
+    const int64_t c0 = bd[kind], c1 = bd[kind + 1] - 1;
+    if (c0 > c1) return U;
+    int ga = gc, gb = -1;  // the run of batches holding the segment
+    for (int g = 0; g < gc; ++g) {
+        if (f[g] <= c0) gb = g;
+        if (ga == gc && l[g] >= c0) ga = g;
+    }
+    if (ga > gb) return U;  // a gap no batch covers
+    U.b = b0 + ga;
+    U.lo_q = p.lo[U.b];
+    U.s = 0;
+    for (int g = ga; g <= gb; ++g) U.s += sg[g];
+    U.js = U.js2 = U.js3 = U.s;
+    if (gb > ga) {
+        U.b1 = U.b + 1;
+        U.js = sg[ga];
+        if (gb > ga + 1) U.js2 = sg[ga] + sg[ga + 1];
+        if (gb > ga + 2) U.js3 = sg[ga] + sg[ga + 1] + sg[ga + 2];
+    }
+    U.f = c0;
+    U.l = c1;
+    return U;
+}
+
+__device__ __forceinline__ Unit plan_unit(const SearchPlanDev &p, int64_t u, int64_t tqs, int mode) {
+    if (mode == K1_SHARE_QUADS) return plan_unit_quads(p, u, tqs);
+    const int pair = mode != K1_SHARE_NONE;
     const int64_t k = u / 5, kind = u % 5;
     const int64_t b0 = 2 * k, b1 = 2 * k + 1;
     const bool has1 = b1 < p.nb;
@@ -278,6 +377,7 @@ __device__ __forceinline__ Unit plan_unit(const SearchPlanDev &p, int64_t u, int
         U.lo_q = p.lo[b0];
         U.s = s0 + s1;
         U.js = s0;
+        U.js2 = U.js3 = U.s;
         if (shared) {
             U.b1 = b1;
             U.f = ilo;
@@ -289,14 +389,14 @@ __device__ __forceinline__ Unit plan_unit(const SearchPlanDev &p, int64_t u, int
     if (second && !has1) {
         U.b = b0;
         U.lo_q = p.lo[b0];
-        U.s = U.js = s0;
+        U.s = U.js = U.js2 = U.js3 = s0;
         return U;
     }
     const int64_t b = second ? b1 : b0;
     const int64_t f = second ? f1 : f0, l = second ? l1 : l0;
     U.b = b;
     U.lo_q = p.lo[b];
-    U.s = U.js = second ? s1 : s0;
+    U.s = U.js = U.js2 = U.js3 = second ? s1 : s0;
     if (f < 0) return U;  // no candidates
     const bool left = kind == 1 || kind == 3;
     if (!shared) {
@@ -313,8 +413,6 @@ __device__ __forceinline__ Unit plan_unit(const SearchPlanDev &p, int64_t u, int
     }
     return U;
 }
-
-__host__ __device__ __forceinline__ int64_t plan_units(int64_t nb) { return 5 * ((nb + 1) / 2); }
 
 struct K1Launch {
     Soa e;  // by value: device pointers
@@ -350,7 +448,8 @@ struct K1Launch {
 };
 
 void launch_ranges(tsk_db *db, const Soa &q, SearchPlanDev &p, bool spans_given, cudaStream_t st);
-void launch_plan_items(SearchPlanDev &p, int slots, int stride, int pair, int align, cudaStream_t st);
+void launch_plan_items(SearchPlanDev &p, int slots, int stride, int pair, int align, int tq_max, const int *q_flags,
+                       cudaStream_t st);
 void launch_qprep(const Soa &q, QRec *out, int *flags, unsigned long long *cmax_bits, cudaStream_t st);
 bool mapped_columns(const tsk_columns *c, tsk_columns *dev);
 void launch_qprep_mapped(const tsk_columns &dev_cols, Soa &q, QRec *out, int *flags, unsigned long long *cmax_bits,
@@ -375,14 +474,18 @@ void launch_k1f(const K1Launch &L, int grid, cudaStream_t st);
 bool k1_use_f32(double d2, double db_cmax);
 int k1_candidates_per_thread(bool f32);
 
-// 14 warps per CTA, 2 CTAs per SM at <= 72 registers (28 warps per SM):
-// measured against 8 x 3 at 80 registers, c5 K1 21.2 -> 20.0 ms; 12 x 2 at
-// 80 and 16 x 1 at 128 registers fall in between
+// 8 warps per CTA, 2 CTAs per SM at up to 128 registers, with 512-query
+// tiles (quads of Periodic batches share candidate tiles): the shared
+// memory of a 512-query tile fits twice per SM at this width
 #ifndef K1_THREADS_DEF
-#define K1_THREADS_DEF 448
+#define K1_THREADS_DEF 256
 #endif
 constexpr int K1_THREADS = K1_THREADS_DEF;
-constexpr int K1_TQ = 256;        // queries per tile staged in shared memory
+#ifndef K1_TQ_DEF
+#define K1_TQ_DEF 512
+#endif
+constexpr int K1_TQ = K1_TQ_DEF;   // queries per tile of the FP32 kernel, staged in shared memory
+constexpr int K1P_TQ = 256;        // queries per tile of the FP64-filter kernel (k1_pairs.cu)
 #ifndef K1_MAX_SUB_DEF
 #define K1_MAX_SUB_DEF 32
 #endif

@@ -49,13 +49,19 @@ class Scene:
         self.oix = orc.index_build(self.E, M)
 
     def check(self, plan, d, batch_ids=None):
+        from paper_1405_7461_b200.engine import search_device
+
         res, st = tsk.run_search(self.store, self.index, plan, d)
         lo, hi = plan.table()
         hits = np.array([t.hits for t in st.per_batch], np.int64)
         ids = range(len(lo)) if batch_ids is None else batch_ids
         cols = {k: getattr(res, k) for k in orc_res()}
-        rep = check_batches(self.E, self.oix, self.Q, lo, hi, cols, hits, ids, d)
+        # per-batch temporal overlaps from the device pipeline (the miss
+        # statistics' source) against the oracle's
+        ovl = np.asarray(search_device(self.store, self.index, plan, d).per_batch)[:, 2]
+        rep = check_batches(self.E, self.oix, self.Q, lo, hi, cols, hits, ids, d, batch_overlaps=ovl)
         assert rep["mismatches"] == 0, rep
+        assert rep["overlap_mismatches"] == 0, rep
         # per-batch interactions (engine.py:145) against the oracle's spans
         ints = np.array([t.interactions for t in st.per_batch], np.int64)
         assert rep["pairs"] == int(ints[np.asarray(sorted(set(ids)))].sum())
@@ -92,6 +98,7 @@ def test_c2_galaxy_full_plan(d, s):
     res, st, rep = sc.check(plan, d)
     assert rep["batches"] == len(plan.batches)
     assert st.hits == rep["hits"] == len(res)
+    assert (st.temporal_misses, st.spatial_misses) == (rep["temporal_misses"], rep["spatial_misses"])
     assert st.hits > 0
     frac = st.hits / st.interactions_computed
     assert (1e-7 < frac < 1e-5) if d < 0.5 else (5e-5 < frac < 1e-3)
