@@ -8,3 +8,5 @@ timeout 1500 python bench.py --steps 10 --warmup 3 > gpurun_out/$TAG/bench_c5.js
 for c in c1 c2 c3 c4; do timeout 900 python bench.py --config $c --steps 10 --warmup 3 > gpurun_out/$TAG/bench_$c.json 2> gpurun_out/$TAG/bench_$c.err; echo "$c rc=$?"; done
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/$TAG/bench_ref_c5.json 2> gpurun_out/$TAG/bench_ref_c5.err; echo "ref rc=$?"
 TAG=$TAG bash tools/gpurun/r2_prof2.sh
+# 2 ranks on the one GPU (TSK_BENCH_DEVICE pins both; timing collectives over gloo): the N>1 path end to end
+TSK_BENCH_DEVICE=0 timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --config c3 --steps 5 --warmup 3 > gpurun_out/$TAG/bench_c3_2rank_samegpu.json 2> gpurun_out/$TAG/bench_c3_2rank.err; echo "2rank rc=$?"
