@@ -81,10 +81,17 @@ class BatchPlan:
         return [b.size for b in self.batches]
 
     def table(self) -> tuple[np.ndarray, np.ndarray]:
-        """(lo, hi) int64 arrays — the batch table handed to the GPU."""
-        lo = np.fromiter((b.lo for b in self.batches), np.int64, len(self.batches))
-        hi = np.fromiter((b.hi for b in self.batches), np.int64, len(self.batches))
-        return lo, hi
+        """(lo, hi) int64 arrays — the batch table handed to the GPU (built
+        once per plan: the plan and its batches are immutable; read-only)."""
+        t = self.__dict__.get("_table")
+        if t is None:
+            lo = np.fromiter((b.lo for b in self.batches), np.int64, len(self.batches))
+            hi = np.fromiter((b.hi for b in self.batches), np.int64, len(self.batches))
+            lo.flags.writeable = False
+            hi.flags.writeable = False
+            t = (lo, hi)
+            object.__setattr__(self, "_table", t)
+        return t
 
 
 def num_interactions(batch: QueryBatch, index: TemporalIndex) -> int:
