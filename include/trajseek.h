@@ -37,7 +37,8 @@ enum {
     TSK_ECUDA = 2,   /* CUDA runtime failure → RuntimeError              */
     TSK_ENOMEM = 3,  /* allocation failure → MemoryError                 */
     TSK_ENODEV = 4,  /* no CUDA device                                   */
-    TSK_EFORMAT = 5  /* unparsable / invalid CSV → FormatError (core.py:29-30) */
+    TSK_EFORMAT = 5, /* unparsable / invalid CSV → FormatError (core.py:29-30) */
+    TSK_ETOOMANY = 6 /* more hits than one call returns (2^32): split the plan and call again */
 };
 
 /* tsk_search flags */

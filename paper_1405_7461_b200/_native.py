@@ -15,7 +15,13 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TRAJSEEK_LIB") or os.path.join(_HERE, "_lib", "libtrajseek.so")
 
-TSK_OK, TSK_EINVAL, TSK_ECUDA, TSK_ENOMEM, TSK_ENODEV, TSK_EFORMAT = 0, 1, 2, 3, 4, 5
+TSK_OK, TSK_EINVAL, TSK_ECUDA, TSK_ENOMEM, TSK_ENODEV, TSK_EFORMAT, TSK_ETOOMANY = 0, 1, 2, 3, 4, 5, 6
+
+
+class TooManyHits(RuntimeError):
+    """One call's result exceeds what a call returns (2^32 rows); the engine
+    splits the plan and calls again (the reference grows its accumulator on
+    demand, SPEC.md:222)."""
 TSK_NOOP = 1 << 0
 TSK_ORDER_REFERENCE = 1 << 1
 TSK_ORDER_QUERY_MAJOR = 1 << 2
@@ -125,6 +131,8 @@ def check(rc: int) -> None:
         raise FormatError(msg)
     if rc == TSK_ENOMEM:
         raise MemoryError(msg)
+    if rc == TSK_ETOOMANY:
+        raise TooManyHits(msg)
     raise RuntimeError(f"libtrajseek error {rc}: {msg}")
 
 

@@ -422,6 +422,13 @@ __global__ void k_snap(const unsigned long long *__restrict__ ctr, unsigned long
     __threadfence_system();
 }
 
+// Rows one call returns: 2^32 (TSK_MAX_HITS lowers it for testing).
+static unsigned long long max_hits_per_call() {
+    unsigned long long m = 1ull << 32;
+    if (const char *e = getenv("TSK_MAX_HITS")) m = std::min<unsigned long long>(m, strtoull(e, nullptr, 10));
+    return m;
+}
+
 static void sort_rows(tsk_db *db, const uint64_t *keys, uint64_t *ko, uint32_t *v0, uint32_t *v1, int64_t n,
                       int end_bit, cudaStream_t st, int64_t &launches) {
     if (n <= K4_SMALL) {
@@ -632,7 +639,7 @@ static tsk_result *run_pipelined(tsk_db *db, const tsk_columns *qc, const Search
         TSK_CUDA(cudaEventSynchronize(eks[c]));
         h_seen[c] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h_start).count();
         const unsigned long long end = snap[2 * c];
-        if (end > cap || end >= (1ull << 32)) {
+        if (end > cap || end >= max_hits_per_call()) {
             overflow = true;
             break;
         }
@@ -969,7 +976,9 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
         db->recs.reserve((size_t)h_hits * 24 + 24 * 1024, st);
         cap = db->recs.bytes / 24;
     }
-    TSK_REQUIRE(count_only || h_hits < (1ull << 32), "more than 2^32 hits in one call");
+    if (!count_only && h_hits >= max_hits_per_call())
+        throw Error{TSK_ETOOMANY, "more than " + std::to_string(max_hits_per_call()) +
+                                      " hits in one call (the row permutation is 32-bit): split the plan"};
     const int64_t nh = count_only ? 0 : (int64_t)h_hits;
     if (!count_only) {
         db->last_hits = nh;

@@ -198,6 +198,18 @@ def _run_one(store, index, plan, d, ordinal, replica, canonical=False):
     chunks = _split_for_keys(store, plan)
     if chunks is not None:
         return _run_chunked(store, index, plan, d, ordinal, replica, canonical, chunks)
+    try:
+        return _run_one_call(store, index, plan, d, ordinal, replica, canonical)
+    except _native.TooManyHits:
+        # more rows than one call returns: halves of the plan, concatenated in
+        # plan order (results decompose per batch, engine.py:176-195)
+        nb = len(plan.batches)
+        if nb < 2:
+            raise
+        return _run_chunked(store, index, plan, d, ordinal, replica, canonical, [(0, nb // 2), (nb // 2, nb)])
+
+
+def _run_one_call(store, index, plan, d, ordinal, replica, canonical=False):
     t_start = time.perf_counter()
     queries = plan.queries
     lo, hi = plan.table()

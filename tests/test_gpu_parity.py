@@ -462,6 +462,33 @@ def test_pipelined_search_entry_id_widths(first_traj, monkeypatch):
     assert st.hits == wst.hits > 500_000
 
 
+@pytest.mark.parametrize("chunks", ["0", "3"])
+def test_results_beyond_one_call_split_the_plan(chunks, monkeypatch):
+    """A call returns at most 2^32 rows (TSK_MAX_HITS lowers the limit): the
+    engine splits the plan into halves until each call fits and concatenates
+    them in plan order, like the reference's growing accumulator.
+    The result and the statistics equal one call's."""
+    rng = np.random.default_rng(29)
+    store = _store(random_store_arrays(rng, 2500))
+    q = _store(random_store_arrays(rng, 700, first_traj=10**6))
+    ix = tsk.build_index(store, 50)
+    plan = tsk.periodic(q, 30, ix)
+    monkeypatch.setenv("TSK_PIPE_CHUNKS", chunks)
+    want, ws = tsk.run_search(store, ix, plan, 5.0)
+    per_batch_max = max(t.hits for t in ws.per_batch)
+    monkeypatch.setenv("TSK_MAX_HITS", str(per_batch_max * 3))
+    got, gs = tsk.run_search(store, ix, plan, 5.0)
+    assert len(want) > per_batch_max * 3
+    for k in RES:
+        assert np.array_equal(getattr(got, k), getattr(want, k)), k
+    assert (gs.interactions_computed, gs.temporal_misses, gs.spatial_misses, gs.hits) == \
+        (ws.interactions_computed, ws.temporal_misses, ws.spatial_misses, ws.hits)
+    assert [t.hits for t in gs.per_batch] == [t.hits for t in ws.per_batch]
+    monkeypatch.setenv("TSK_MAX_HITS", str(per_batch_max - 1))
+    with pytest.raises(RuntimeError):  # one batch alone exceeds the limit
+        tsk.run_search(store, ix, plan, 5.0)
+
+
 def test_batches_without_candidates_and_large_batches():
     entries = _store(random_store_arrays(np.random.default_rng(7), 500))
     ix = tsk.build_index(entries, 50)
