@@ -422,6 +422,25 @@ TSK_HD float box_gap2(float glx, float gly, float glz, float ghx, float ghy, flo
 #endif
 }
 
+#ifdef __CUDACC__
+// box_gap2 of one box [g] against two query boxes at once (FADD2 / FFMA2 /
+// FMUL2 with the same directed roundings per element: each half equals the
+// scalar form bit for bit, so the cull's proof is unchanged).
+__device__ __forceinline__ float2 box_gap2_x2(float glx, float gly, float glz, float ghx, float ghy, float ghz,
+                                              float2 qlx, float2 qly, float2 qlz, float2 qhx, float2 qhy, float2 qhz) {
+    const float2 a0 = __fadd2_rd(make_float2(glx, glx), make_float2(-qhx.x, -qhx.y));
+    const float2 a1 = __fadd2_rd(qlx, make_float2(-ghx, -ghx));
+    const float2 b0 = __fadd2_rd(make_float2(gly, gly), make_float2(-qhy.x, -qhy.y));
+    const float2 b1 = __fadd2_rd(qly, make_float2(-ghy, -ghy));
+    const float2 c0 = __fadd2_rd(make_float2(glz, glz), make_float2(-qhz.x, -qhz.y));
+    const float2 c1 = __fadd2_rd(qlz, make_float2(-ghz, -ghz));
+    const float2 gx = make_float2(fmaxf(fmaxf(a0.x, a1.x), 0.f), fmaxf(fmaxf(a0.y, a1.y), 0.f));
+    const float2 gy = make_float2(fmaxf(fmaxf(b0.x, b1.x), 0.f), fmaxf(fmaxf(b0.y, b1.y), 0.f));
+    const float2 gz = make_float2(fmaxf(fmaxf(c0.x, c1.x), 0.f), fmaxf(fmaxf(c0.y, c1.y), 0.f));
+    return __ffma2_rd(gz, gz, __ffma2_rd(gy, gy, __fmul2_rd(gx, gx)));
+}
+#endif
+
 // Two candidates of a lane in packed form: component c of candidates k0/k1
 // in one float2 (sm_100's FFMA2 / FADD2 / FMUL2 then issue one instruction
 // for both, the query's scalar broadcast as the .F32 operand).

@@ -403,18 +403,24 @@ __device__ __forceinline__ int box_cull(float4 lo, float4 hi, int jlo, int jhi, 
     unsigned lt;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
     int ns = 0;
-    for (int jb = jlo; jb < jhi; jb += 32) {
-        const int j = jb + lane;
-        bool pass = false;
-        if (j < jhi) {
-            const float4 ql = qb[2 * j], qh = qb[2 * j + 1];
-            const float R = __fadd_ru(rw, ql.w);
-            pass = !(box_gap2(lo.x, lo.y, lo.z, hi.x, hi.y, hi.z, ql.x, ql.y, ql.z, qh.x, qh.y, qh.z) >
-                     __fmul_ru(R, R));
-        }
-        const unsigned m = __ballot_sync(0xffffffffu, pass);
-        if (pass) wl[ns + __popc(m & lt)] = (uint16_t)j;
-        ns += __popc(m);
+    // two queries per lane per iteration (j and j + 32), packed; survivors
+    // keep window order (the first 32's ballot, then the second's)
+    for (int jb = jlo; jb < jhi; jb += 64) {
+        const int j0 = jb + lane, j1 = j0 + 32;
+        const int c0 = j0 < jhi ? j0 : jhi - 1, c1 = j1 < jhi ? j1 : jhi - 1;  // clamped reads
+        const float4 l0 = qb[2 * c0], h0 = qb[2 * c0 + 1], l1 = qb[2 * c1], h1 = qb[2 * c1 + 1];
+        const float2 g2 = box_gap2_x2(lo.x, lo.y, lo.z, hi.x, hi.y, hi.z, make_float2(l0.x, l1.x),
+                                      make_float2(l0.y, l1.y), make_float2(l0.z, l1.z), make_float2(h0.x, h1.x),
+                                      make_float2(h0.y, h1.y), make_float2(h0.z, h1.z));
+        const float2 R = __fadd2_ru(make_float2(rw, rw), make_float2(l0.w, l1.w));
+        const float2 R2 = __fmul2_ru(R, R);
+        const bool p0 = j0 < jhi && !(g2.x > R2.x), p1 = j1 < jhi && !(g2.y > R2.y);
+        const unsigned m0 = __ballot_sync(0xffffffffu, p0);
+        if (p0) wl[ns + __popc(m0 & lt)] = (uint16_t)j0;
+        ns += __popc(m0);
+        const unsigned m1 = __ballot_sync(0xffffffffu, p1);
+        if (p1) wl[ns + __popc(m1 & lt)] = (uint16_t)j1;
+        ns += __popc(m1);
     }
     __syncwarp();
     return ns;
