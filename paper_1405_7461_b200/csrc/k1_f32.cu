@@ -35,9 +35,6 @@
 #ifndef K1F_CPT
 #define K1F_CPT 4
 #endif
-#ifndef K1_EARLY
-#define K1_EARLY 0  // measured: no gain (more spills)
-#endif
 #ifndef K1F_MIN_BLOCKS
 #define K1F_MIN_BLOCKS 2
 #endif
@@ -665,15 +662,7 @@ __shared__ int64_t k1_kf[4];
 // they are ever flagged (its tb case is chosen per pair: the warp's end-time
 // bounds are left open).  Only warps with a query near their box load their
 // candidates, all columns in one round trip.
-#ifndef K1_FAST_INLINE
-#define K1_FAST_INLINE 0
-#endif
-#if K1_FAST_INLINE
-__device__ __forceinline__
-#else
-__device__ __noinline__
-#endif
-void fast_subtile(int64_t wbase, int warp, int lane, unsigned long long &n_ev, unsigned long long &n_hit) {
+__device__ __noinline__ void fast_subtile(int64_t wbase, int warp, int lane, unsigned long long &n_ev, unsigned long long &n_hit) {
     const K1Launch &L = k1f_L();
     const ItemCtx &it = k1f_it;
     const F32Item &fi = k1f_fi;
@@ -685,13 +674,7 @@ void fast_subtile(int64_t wbase, int warp, int lane, unsigned long long &n_ev, u
     const bool item_f32 = k1f_item_f32 != 0;
     const int64_t g0 = wbase / BOX_GROUP;
     const int64_t g1 = (wbase + WCAND - 1 < it.c_hi ? wbase + WCAND - 1 : it.c_hi) / BOX_GROUP;
-    // the groups' time range and box, loaded together, and (speculatively:
-    // nearly every sub-tile has a query near its box) the first candidates'
-    // columns, whose latency then hides behind the window search and cull
-    RawPair r0;
-#if K1_EARLY
-    load_pair(L, wbase, it.c_lo, it.c_hi, 0, lane, r0);
-#endif
+    // the groups' time range and box, loaded together
     double2 tr = L.gtime[g0];
     float4 blo, bhi;
     bool unsafe_g;
@@ -770,10 +753,8 @@ void fast_subtile(int64_t wbase, int warp, int lane, unsigned long long &n_ev, u
     if (L.frec && wbase % BOX_GROUP == 0) {
         stage_rebased(L, wbase, it.c_lo, it.c_hi, fi, wcs, lane);
     } else {
-#if !K1_EARLY
+        RawPair r0, r1;
         load_pair(L, wbase, it.c_lo, it.c_hi, 0, lane, r0);
-#endif
-        RawPair r1;
         load_pair(L, wbase, it.c_lo, it.c_hi, 2, lane, r1);
         store_pair(r0, 0, fi, wcs, lane);
         store_pair(r1, 2, fi, wcs, lane);
