@@ -15,6 +15,7 @@
 
 #include <chrono>
 #include <condition_variable>
+#include <functional>
 #include <thread>
 
 #include <cmath>
@@ -630,8 +631,23 @@ static tsk_result *run_pipelined(tsk_db *db, const tsk_columns *qc, const Search
             x_stop = true;
             xcv.notify_one();
         }
-        expander.join();
+        if (expander.joinable()) expander.join();
     };
+    // a CUDA error thrown below must not leave the thread joinable
+    // (std::thread's destructor would terminate the process)
+    struct JoinGuard {
+        const std::function<void()> fn;
+        ~JoinGuard() { fn(); }
+    } join_guard{[&] {
+        if (!expander.joinable()) return;
+        {
+            std::lock_guard<std::mutex> g(xmu);
+            x_ready = 0;  // skip chunks not expanded yet: the call is failing
+            x_stop = true;
+            xcv.notify_one();
+        }
+        expander.join();
+    }};
     const int end_bit = bb + major_bits + minor_bits;
     enqueue_k1(0);
     bool overflow = false;
