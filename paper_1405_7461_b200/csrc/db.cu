@@ -334,8 +334,18 @@ __global__ void k_qprep_mapped(int64_t n, tsk_columns c, double *__restrict__ ts
         r.vx = h.v[0]; r.vy = h.v[1]; r.vz = h.v[2];
         r.flag = h.unsafe ? 1.0 : 0.0;
         out[i] = r;
-        if (i + 1 < n && c.ts[i + 1] < r.ts) atomicOr(&flags[0], 1);
-        if (i + 1 < n && c.te[i + 1] < r.te) atomicOr(&flags[0], 2);
+        // the next query's times from the neighbouring lane (only the last
+        // lane re-reads host memory: every column crosses PCIe once)
+        const unsigned act = __activemask();
+        const int lane = threadIdx.x & 31;
+        double nts = __shfl_down_sync(act, r.ts, 1), nte = __shfl_down_sync(act, r.te, 1);
+        const bool last = lane == 31 || !((act >> (lane + 1)) & 1u);
+        if (last && i + 1 < n) {
+            nts = c.ts[i + 1];
+            nte = c.te[i + 1];
+        }
+        if (i + 1 < n && nts < r.ts) atomicOr(&flags[0], 1);
+        if (i + 1 < n && nte < r.te) atomicOr(&flags[0], 2);
         cm = fmax(cm, fmax(fmax(fabs(r.sx), fabs(r.sy)), fmax(fabs(r.sz), fmax(fabs(r.ex), fmax(fabs(r.ey), fabs(r.ez))))));
     }
     for (int o = 16; o; o >>= 1) cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, o));
