@@ -540,13 +540,14 @@ static tsk_result *run_pipelined(tsk_db *db, const tsk_columns *qc, const Search
     int64_t *o_et = (int64_t *)(hb + 2 * cs), *o_es = (int64_t *)(hb + 3 * cs);
     double *o_tb = (double *)(hb + 4 * cs), *o_te = (double *)(hb + 5 * cs);
 
-    std::vector<cudaEvent_t> ek0((size_t)C), ek1((size_t)C), eks((size_t)C), evd((size_t)C);
+    std::vector<cudaEvent_t> ek0((size_t)C), ek1((size_t)C), eks((size_t)C), evd((size_t)C), evq((size_t)C);
     for (int c = 0; c < C; ++c) {
         TSK_CUDA(cudaEventCreate(&ek0[c]));
         TSK_CUDA(cudaEventCreate(&ek1[c]));
         // spin on the count (a blocking wait adds ~0.2 ms of wake-up per chunk)
         TSK_CUDA(cudaEventCreateWithFlags(&eks[c], cudaEventDisableTiming));
         TSK_CUDA(cudaEventCreate(&evd[c]));  // spin wait (see compact_rows)
+        TSK_CUDA(cudaEventCreateWithFlags(&evq[c], cudaEventDisableTiming));
     }
     const bool trace = getenv("TSK_TRACE") != nullptr;
     std::vector<cudaEvent_t> esd((size_t)C, nullptr);  // (trace) end of S(c)
@@ -558,6 +559,7 @@ static tsk_result *run_pipelined(tsk_db *db, const tsk_columns *qc, const Search
             cudaEventDestroy(ek1[c]);
             cudaEventDestroy(eks[c]);
             cudaEventDestroy(evd[c]);
+            cudaEventDestroy(evq[c]);
             if (esd[c]) cudaEventDestroy(esd[c]);
         }
         pin_free(snap, sgot);
@@ -567,10 +569,6 @@ static tsk_result *run_pipelined(tsk_db *db, const tsk_columns *qc, const Search
         launch_plan_items(pc[c], slots, stride, pair, align, tq_max, L.q_unsorted, st);
         ++launches;
         TSK_CUDA(cudaMemsetAsync(d_ctr, 0, 8, st));  // the item counter
-        if (L.ext_count) {
-            launch_count_overlaps_ext(pc[c], db->q, db->s, L.q_unsorted, L.q_cmax_bits, L.db_cmax, L.d2, st);
-            ++launches;
-        }
         K1Launch Lc = L;
         Lc.plan = pc[c];
         TSK_CUDA(cudaEventRecord(ek0[c], st));
@@ -601,7 +599,7 @@ static tsk_result *run_pipelined(tsk_db *db, const tsk_columns *qc, const Search
                 if (c >= x_ready) return;
             }
             if (copied[c]) {
-                cudaEventSynchronize(evd[c]);
+                cudaEventSynchronize(evq[c]);
                 const int64_t r0 = start[c], r1 = start[c + 1];
                 pool.run([&](int part, int parts) {
                     const int64_t a = r0 + (r1 - r0) * part / parts, z = r0 + (r1 - r0) * (part + 1) / parts;
@@ -610,12 +608,17 @@ static tsk_result *run_pipelined(tsk_db *db, const tsk_columns *qc, const Search
                         o_qt[i] = qt[q];
                         o_qs[i] = qs[q];
                     }
-                    if (ids32)
+                });
+                if (ids32) {
+                    cudaEventSynchronize(evd[c]);
+                    pool.run([&](int part, int parts) {
+                        const int64_t a = r0 + (r1 - r0) * part / parts, z = r0 + (r1 - r0) * (part + 1) / parts;
                         for (int64_t i = a; i < z; ++i) {
                             o_et[i] = h_et32[i];
                             o_es[i] = h_es32[i];
                         }
-                });
+                    });
+                }
             }
             ++c;
         }
@@ -684,6 +687,10 @@ static tsk_result *run_pipelined(tsk_db *db, const tsk_columns *qc, const Search
             }
             TSK_CUDA(cudaStreamWaitEvent(st2, eg, 0));
             TSK_CUDA(cudaEventDestroy(eg));  // destruction is deferred until the event completes
+            // the query ordinals first: the expander gathers the query ids
+            // while the chunk's other columns cross PCIe
+            TSK_CUDA(cudaMemcpyAsync(h_qo + s0, d_qo + s0, (size_t)n * 4, cudaMemcpyDeviceToHost, st2));
+            TSK_CUDA(cudaEventRecord(evq[c], st2));
             TSK_CUDA(cudaMemcpyAsync(o_tb + s0, d_tb + s0, (size_t)n * 8, cudaMemcpyDeviceToHost, st2));
             TSK_CUDA(cudaMemcpyAsync(o_te + s0, d_te + s0, (size_t)n * 8, cudaMemcpyDeviceToHost, st2));
             if (ids32) {
@@ -695,7 +702,6 @@ static tsk_result *run_pipelined(tsk_db *db, const tsk_columns *qc, const Search
                 TSK_CUDA(cudaMemcpyAsync(o_et + s0, d_et + s0, (size_t)n * 8, cudaMemcpyDeviceToHost, st2));
                 TSK_CUDA(cudaMemcpyAsync(o_es + s0, d_es + s0, (size_t)n * 8, cudaMemcpyDeviceToHost, st2));
             }
-            TSK_CUDA(cudaMemcpyAsync(h_qo + s0, d_qo + s0, (size_t)n * 4, cudaMemcpyDeviceToHost, st2));
             TSK_CUDA(cudaEventRecord(evd[c], st2));
             copied[c] = 1;
         }
@@ -710,6 +716,12 @@ static tsk_result *run_pipelined(tsk_db *db, const tsk_columns *qc, const Search
         cleanup();
         pin_free(hb, hgot);
         return nullptr;
+    }
+    // the overlap counts (statistics only) once for the whole plan, behind
+    // the last chunk's copy instead of on the K1 chain of every chunk
+    if (L.ext_count) {
+        launch_count_overlaps_ext(plan, db->q, db->s, L.q_unsorted, L.q_cmax_bits, L.db_cmax, L.d2, st);
+        ++launches;
     }
     tr.mark("pipeline");
     finish_expander();
