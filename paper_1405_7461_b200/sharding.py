@@ -26,14 +26,33 @@ def batch_interactions(plan: BatchPlan, index: TemporalIndex) -> np.ndarray:
     return np.where(f >= 0, (l - f + 1) * (hi - lo + 1), 0).astype(np.int64)
 
 
-def shard_bounds(ints: np.ndarray, world: int) -> list[tuple[int, int]]:
-    """Contiguous batch shards [b0, b1) with balanced Σ interactions."""
+# K1's fixed cost per non-empty batch (its work items' set-up, window and
+# cull visits) in units of the plan's mean interactions per batch: 1.35 us
+# per batch at c5 (Periodic s = 30 vs 120: +10,000 batches, +13.5 ms at equal
+# interactions) against ~6e7 interactions per batch at 6.4e-11 ms each.
+# Without it the plan's two end shards, whose batches hold fewer candidates,
+# ran 9% longer than the middle ones at N = 8 (tools/shard_cost.py).
+BATCH_COST_FRAC = 0.35
+
+
+def shard_bounds(ints: np.ndarray, world: int, batch_cost: float | None = None) -> list[tuple[int, int]]:
+    """Contiguous batch shards [b0, b1) with balanced estimated K1 time:
+    Σ interactions plus ``batch_cost`` per non-empty batch (default
+    ``BATCH_COST_FRAC`` × the mean interactions of a non-empty batch)."""
     nb = int(ints.shape[0])
-    cum = np.concatenate([[0.0], np.cumsum(ints, dtype=np.float64)])
+    ints = np.asarray(ints, dtype=np.float64)
+    live = ints > 0
+    if batch_cost is None:
+        batch_cost = BATCH_COST_FRAC * float(ints[live].mean()) if live.any() else 0.0
+    cum = np.concatenate([[0.0], np.cumsum(ints + batch_cost * live, dtype=np.float64)])
     total = cum[-1]
     cuts = [0]
-    for r in range(1, world):
-        cuts.append(int(np.searchsorted(cum, total * r / world, side="left")))
+    for r in range(1, world):  # the batch boundary nearest the target
+        t = total * r / world
+        i = int(np.searchsorted(cum, t, side="left"))
+        if 0 < i <= nb and t - cum[i - 1] <= cum[i] - t:
+            i -= 1
+        cuts.append(i)
     cuts.append(nb)
     for i in range(1, len(cuts)):
         cuts[i] = min(max(cuts[i], cuts[i - 1]), nb)
