@@ -582,7 +582,7 @@ __global__ void __launch_bounds__(1024, 1) k_plan_items(SearchPlanDev p, int64_t
     // 148 SMs
     const long long want = 4 * slots;
     int tqs = tq_max;
-    for (;;) {  // pair == 2 / 5 (testing): full tiles, always pairs / quads
+    for (;;) {  // pair == 2 / 5 / 9 (testing): full tiles, always pairs / quads / octets
         long long acc = 0;
         for (int64_t b = threadIdx.x; b < nb; b += blockDim.x) {
             long long c = p.first[b] >= 0 ? p.last[b] - p.first[b] + 1 : 0;
@@ -594,7 +594,7 @@ __global__ void __launch_bounds__(1024, 1) k_plan_items(SearchPlanDev p, int64_t
         __syncthreads();
         tiles = tiles_sh;
         __syncthreads();
-        if (tiles >= want || tqs <= 32 || pair == 2 || pair == 5) break;
+        if (tiles >= want || tqs <= 32 || pair == 2 || pair == 5 || pair == 9) break;
         tqs >>= 1;
     }
     if (threadIdx.x == 0) {
@@ -610,11 +610,14 @@ __global__ void __launch_bounds__(1024, 1) k_plan_items(SearchPlanDev p, int64_t
     // tiles: quads (pair == 4) when the kernel's box-cull fast path takes
     // every item — query start and end times both sorted (q_flags bits 0, 1
     // from the query kernel) — else pairs
+    // (pair == 8 / 9: octets, the 1,024-query kernel; 9 forces them)
+    const bool sorted_q = q_flags && (*q_flags & 3) == 0;
+    const int group = pair >= 8 ? K1_SHARE_OCTETS : K1_SHARE_QUADS;
     int mode = K1_SHARE_NONE;
     if (pair == 2) mode = K1_SHARE_PAIRS;  // testing: forced, full tiles
-    else if (pair == 5) mode = (q_flags && (*q_flags & 3) == 0) ? K1_SHARE_QUADS : K1_SHARE_PAIRS;
+    else if (pair == 5 || pair == 9) mode = sorted_q ? group : K1_SHARE_PAIRS;
     else if (pair && tqs == tq_max)
-        mode = (pair == 4 && q_flags && (*q_flags & 3) == 0) ? K1_SHARE_QUADS : K1_SHARE_PAIRS;
+        mode = ((pair == 4 || pair == 8) && sorted_q) ? group : K1_SHARE_PAIRS;
     const int pr = mode;
     const long long ct = (long long)stride * sub_sh;
     const int64_t nu = plan_units_mode(nb, mode);
@@ -622,7 +625,7 @@ __global__ void __launch_bounds__(1024, 1) k_plan_items(SearchPlanDev p, int64_t
         int64_t u = base + threadIdx.x;
         long long v = 0;
         if (u < nu) {
-            const Unit U = plan_unit(p, u, tqs, pr);
+            const UnitT<K1_UNIT_GMAX> U = plan_unit<K1_UNIT_GMAX, false>(p, u, tqs, pr);
             if (U.f <= U.l) {
                 // candidate tiles start at a multiple of `align` (K1 layout:
                 // warps then coincide with the box groups; the head is masked)

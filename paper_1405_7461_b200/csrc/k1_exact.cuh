@@ -146,8 +146,17 @@ struct ItemCtx {
     int64_t q0;                      // first query offset within batch b (tile)
     int64_t b1;                      // shared unit: the second batch (queries js..), else -1
     int nt, js;                      // staged queries; queries of batch b (nt when single)
-    int js2, js3;                    // quads: tile offsets of batches b + 2, b + 3 (nt when absent)
+    int jx[K1_GMAX - 2];             // groups: tile offsets of batches b + 2 .. (nt when absent)
 };
+
+// Batches in an item's tile (1 .. K1_GMAX).
+__device__ __forceinline__ int item_batches(const ItemCtx &it) {
+    if (it.b1 < 0) return 1;
+    int n = 2;
+#pragma unroll
+    for (int i = 0; i < K1_GMAX - 2; ++i) n += it.jx[i] < it.nt;
+    return n;
+}
 
 // Per-item counters are kept per batch in one 64-bit word: the low half
 // for batch b, the high half for b1 (a warp's counts in one item are far
@@ -263,11 +272,11 @@ struct __align__(16) QF32 {
 
 // Per-warp context of the current sub-tile, read by the flush.
 struct WarpCtx {
-    uint64_t key_base[4];   // key of (b + g, e_off of candidate 0, query offset 0) without the j term
+    uint64_t key_base[K1_GMAX];  // key of (b + g, e_off of candidate 0, query offset 0) without the j term
                             // (g = 0: it.q0; g >= 1: the batch's first query at tile index js_g)
-    int64_t f[4];           // first candidate ordinal of batch b + g (K1 layout: e_off = orig - f)
+    int64_t f[K1_GMAX];     // first candidate ordinal of batch b + g (K1 layout: e_off = orig - f)
     int js;                 // tile index of batch b + 1's first query (nt when single)
-    int js2, js3;           // ... of b + 2, b + 3 (quads; nt when absent)
+    int jx[K1_GMAX - 2];    // ... of b + 2 .. (groups; nt when absent)
     double wmin_te, wmax;   // min te / max te of the warp's candidates (tb cases)
     int64_t wbase;          // entry ordinal of the warp's candidate 0
     int nvalid;             // valid candidates of the warp (the rest are past the item)
@@ -279,7 +288,7 @@ struct WarpCtx {
 // hot loops carry none of it in registers.
 __shared__ FlushCfg k1_fcfg;
 __shared__ WarpCtx k1_wctx[K1_WARPS];
-__shared__ unsigned long long k1_hits23[2];  // per item: hits of batches b + 2, b + 3 (quads)
+__shared__ unsigned long long k1_hitsx[K1_GMAX - 2];  // per item: hits of batches b + 2 .. (groups)
 
 __device__ __forceinline__ void append_hit_w(const FlushCfg &C, bool hit, uint64_t key, double tb,
                                              double te, int lane) {
@@ -342,9 +351,17 @@ __device__ __noinline__ void rare_flush(const QRec *__restrict__ qt, const uint3
         // candidate ci shifts the entry offset, query j the query offset,
         // within the batch the query belongs to (g: which of the tile's
         // batches, from the tile offsets where they start)
-        const int js = k1_wctx[warp].js, js2 = k1_wctx[warp].js2, js3 = k1_wctx[warp].js3;
-        g = (j >= js) + (j >= js2) + (j >= js3);
-        const int jb = g == 0 ? 0 : (g == 1 ? js : (g == 2 ? js2 : js3));
+        const int js = k1_wctx[warp].js;
+        g = j >= js;
+        int jb = g ? js : 0;
+#pragma unroll
+        for (int i = 0; i < K1_GMAX - 2; ++i) {
+            const int ji = k1_wctx[warp].jx[i];
+            if (j >= ji) {
+                g = i + 2;
+                jb = ji;
+            }
+        }
         const uint64_t jj = (uint64_t)(j - jb);
         // the entry term: the candidate's offset in the warp, or in the K1
         // layout its start-sorted ordinal's offset within the batch's range
@@ -352,9 +369,9 @@ __device__ __noinline__ void rare_flush(const QRec *__restrict__ qt, const uint3
         key = k1_wctx[warp].key_base[g] + (C.query_major ? (jj << C.minor_bits) + et : (et << C.minor_bits) + jj);
     }
     // batches b and b + 1 count in the halves of the lane's counter; b + 2
-    // and b + 3 (quads) in block counters (hits are rare)
+    // on (groups) in block counters (hits are rare)
     n_hit += h.hit && g < 2 ? (g ? CNT_B1 : 1ull) : 0ull;
-    if (h.hit && g >= 2) atomicAdd(&k1_hits23[g - 2], 1ull);
+    if (h.hit && g >= 2) atomicAdd(&k1_hitsx[g - 2], 1ull);
     append_hit_w(C, h.hit, key, h.tb, h.te, lane);
 }
 
@@ -428,6 +445,18 @@ __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? l
 // +inf up to twice the next power of two >= nt: all 2 CPT searches advance
 // together by binary lifting, so each step issues 2 CPT independent shared
 // loads and no bounds checks.
+// Entries of the FP32 kernel's window arrays (running max / suffix min of
+// the tile's end / start times, +inf padded).  Binary lifting over nt
+// entries (tile_bounds) reads below 2 pow2(nt), window_bounds below
+// K1_TQ + 64; the wide build (1,024-query tiles, where 2 K1_TQ would not
+// fit beside 16 warps' shared memory) pads to K1_TQ + 64 and clamps
+// tile_bounds' reads.
+#ifdef K1_WIDE
+constexpr int K1_PMN = K1_TQ + 64;
+#else
+constexpr int K1_PMN = 2 * K1_TQ;
+#endif
+
 template <int CPT>
 __device__ __forceinline__ void tile_bounds(const double *qts, const double *qte, int nt, const double (&ts)[CPT],
                                             const double (&te)[CPT], int (&lo)[CPT], int (&hi)[CPT]) {
@@ -446,6 +475,10 @@ __device__ __forceinline__ void tile_bounds(const double *qts, const double *qte
                 double vl, vh;
                 asm volatile("ld.shared.f64 %0, [%1];" : "=d"(vl) : "r"(pl[k] + sb - 8u));
                 asm volatile("ld.shared.f64 %0, [%1];" : "=d"(vh) : "r"(ph[k] + sb - 8u));
+                if (K1_PMN < 2 * K1_TQ) {  // wide build: past the padding reads +inf
+                    if (pl[k] + sb - 8u >= be + 8u * K1_PMN) vl = INFINITY;
+                    if (ph[k] + sb - 8u >= bs + 8u * K1_PMN) vh = INFINITY;
+                }
                 pl[k] += vl < ts[k] ? sb : 0u;
                 ph[k] += vh <= te[k] ? sb : 0u;
             }
@@ -480,7 +513,7 @@ __device__ __forceinline__ ItemCtx decode_item(const K1Launch &L, int64_t item, 
         if (L.plan.item_off[m] <= item) a = m;
         else z = m;
     }
-    const Unit U = plan_unit(L.plan, a, tqs, mode);
+    const UnitT<K1_GMAX> U = plan_unit<K1_GMAX>(L.plan, a, tqs, mode);  // (the host launches octets in the wide build only)
     const int64_t local = item - L.plan.item_off[a];
     ItemCtx c;
     c.b = U.b;
@@ -491,15 +524,17 @@ __device__ __forceinline__ ItemCtx decode_item(const K1Launch &L, int64_t item, 
         c.q0 = 0;
         c.nt = (int)U.s;
         c.js = (int)U.js;
-        c.js2 = (int)U.js2;
-        c.js3 = (int)U.js3;
+#pragma unroll
+        for (int i = 0; i < K1_GMAX - 2; ++i) c.jx[i] = (int)U.jx[i];
     } else {
         const int64_t tq_n = (U.s + tqs - 1) / tqs;
         const int64_t tq = local % tq_n;
         tc = local / tq_n;
         c.q0 = tq * tqs;
         c.nt = (int)(U.s - c.q0 < tqs ? U.s - c.q0 : tqs);
-        c.js = c.js2 = c.js3 = c.nt;
+        c.js = c.nt;
+#pragma unroll
+        for (int i = 0; i < K1_GMAX - 2; ++i) c.jx[i] = c.nt;
     }
     c.lo_q = U.lo_q + c.q0;
     // K1 layout (L.cull): tiles start at a BOX_GROUP multiple (k_plan_items
@@ -532,8 +567,8 @@ __device__ __forceinline__ void fill_flush_cfg(const K1Launch &L) {
 // offset of candidate 0 is folded in; with one each hit adds its own
 // (orig - f).
 __device__ __forceinline__ void set_key_bases(const K1Launch &L, const ItemCtx &it, int64_t wbase, int warp) {
-    const int nb = it.b1 < 0 ? 1 : (it.js2 >= it.nt ? 2 : (it.js3 >= it.nt ? 3 : 4));
-    for (int g = 0; g < 4; ++g) {
+    const int nb = item_batches(it);
+    for (int g = 0; g < K1_GMAX; ++g) {
         const int64_t b = it.b + g;
         const int64_t f = g < nb ? L.plan.first[b] : 0;
         const int64_t q0 = g == 0 ? it.q0 : 0;
@@ -541,8 +576,8 @@ __device__ __forceinline__ void set_key_bases(const K1Launch &L, const ItemCtx &
         k1_wctx[warp].key_base[g] = g >= nb ? 0 : (L.orig ? make_key(L, b, 0, q0) : make_key(L, b, wbase - f, q0));
     }
     k1_wctx[warp].js = it.js;
-    k1_wctx[warp].js2 = it.js2;
-    k1_wctx[warp].js3 = it.js3;
+#pragma unroll
+    for (int i = 0; i < K1_GMAX - 2; ++i) k1_wctx[warp].jx[i] = it.jx[i];
 }
 
 // Running max (warp 0) / suffix min (warp 1) of the tile's end times.
@@ -643,11 +678,11 @@ __device__ __forceinline__ void item_counters(const K1Launch &L, const ItemCtx &
         if (red[1]) atomicAdd(&L.plan.hits[it.b], red[1]);
         if (it.b1 >= 0 && red[2]) atomicAdd(&L.plan.ovl[it.b1], red[2]);
         if (it.b1 >= 0 && red[3]) atomicAdd(&L.plan.hits[it.b1], red[3]);
-        if (it.b1 >= 0 && it.js2 < it.nt) {  // quads: batches b + 2, b + 3 (rare_flush counted them)
-            if (k1_hits23[0]) atomicAdd(&L.plan.hits[it.b + 2], k1_hits23[0]);
-            if (it.js3 < it.nt && k1_hits23[1]) atomicAdd(&L.plan.hits[it.b + 3], k1_hits23[1]);
+        if (it.b1 >= 0) {  // groups: batches b + 2 .. (rare_flush counted them)
+            for (int i = 0; i < K1_GMAX - 2; ++i)
+                if (it.jx[i] < it.nt && k1_hitsx[i]) atomicAdd(&L.plan.hits[it.b + 2 + i], k1_hitsx[i]);
         }
-        k1_hits23[0] = k1_hits23[1] = 0;  // for the next item (the barrier below orders it)
+        for (int i = 0; i < K1_GMAX - 2; ++i) k1_hitsx[i] = 0;  // for the next item (the barrier below orders it)
         if (red_ev && *red_ev) atomicAdd(L.eval_count, *red_ev);
     }
     __syncthreads();

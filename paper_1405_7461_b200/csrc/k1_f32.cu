@@ -32,6 +32,20 @@
 
 #include "k1_exact.cuh"
 
+// The library builds this file twice: as is (512-query tiles, 8-warp CTAs,
+// two per SM) and from k1_f32_wide.cu (K1_WIDE: 1,024-query tiles, 14-warp
+// CTAs, one per SM, octets of batches); the wide build's host-visible names
+// carry a suffix.
+#ifdef K1_WIDE
+#define K1F_NAME(x) x##_wide
+#define K1F_NS_OPEN inline namespace wide {
+#define K1F_NS_CLOSE }
+#else
+#define K1F_NAME(x) x
+#define K1F_NS_OPEN
+#define K1F_NS_CLOSE
+#endif
+
 #ifndef K1F_CPT
 #define K1F_CPT 4
 #endif
@@ -40,15 +54,16 @@
 #endif
 
 namespace tsk {
+K1F_NS_OPEN
 
 // Development counters (built with -DTSK_K1_STATS only; read by
 // tsk_k1_stats): 0 box-cull sub-tiles, 1 box tests, 2 box survivors,
 // 3 sub-tiles with survivors, 4 pre-filter flags, 5 separating-axis
 // survivors, 6 exact-path flushes, 7 items.
-__device__ unsigned long long k1_stats[8];
+__device__ unsigned long long K1F_NAME(k1_stats)[8];
 #ifdef TSK_K1_STATS
 #define K1_STAT(i, v) \
-    do { if ((threadIdx.x & 31) == 0) atomicAdd(&k1_stats[i], (unsigned long long)(v)); } while (0)
+    do { if ((threadIdx.x & 31) == 0) atomicAdd(&K1F_NAME(k1_stats)[i], (unsigned long long)(v)); } while (0)
 #else
 #define K1_STAT(i, v) do { } while (0)
 #endif
@@ -613,11 +628,11 @@ __device__ __forceinline__ void stage_pair(const K1Launch &L, int64_t wbase, int
 }
 
 // jlo = #{j < nt : pm[j] < x} (pm ascending) and jhi = #{j < nt : sm[j] <= y}
-// (sm ascending), both arrays +inf padded to 2 K1_TQ: 16-ary rounds, lanes
+// (sm ascending), both arrays +inf padded to K1_PMN (k1_exact.cuh): 16-ary rounds, lanes
 // 0-15 on pm and 16-31 on sm (a shared load, a ballot and a popcount each:
-// two rounds for 256 queries, three for 512) instead of two serial
+// two rounds for 256 queries, three for 512 or 1,024) instead of two serial
 // bisections.
-static_assert(K1_TQ == 256 || K1_TQ == 512, "window_bounds covers 256 or 512 queries");
+static_assert(K1_TQ == 256 || K1_TQ == 512 || K1_TQ == 1024, "window_bounds covers 256, 512 or 1024 queries");
 __device__ __forceinline__ void window_bounds(const double *pm, const double *sm, int nt, double x, double y, int lane,
                                               int &jlo, int &jhi) {
     const int l = lane & 15;
@@ -629,7 +644,7 @@ __device__ __forceinline__ void window_bounds(const double *pm, const double *sm
         // block l of `step` entries past the current bound ends at r + step (l + 1) - 1
         const int r = lo_half ? r_lo : r_hi;
         const int idx = r + step * (l + 1) - 1;
-        const double v = idx < 2 * K1_TQ ? a[idx] : INFINITY;
+        const double v = idx < K1_PMN ? a[idx] : INFINITY;
         const unsigned m = __ballot_sync(0xffffffffu, lo_half ? v < x : v <= y);
         r_lo += step * __popc(m & 0xffffu);
         r_hi += step * __popc(m >> 16);
@@ -644,16 +659,17 @@ __device__ __forceinline__ void window_bounds(const double *pm, const double *sm
 // calls (every value a caller keeps live across a call costs a spill).
 __shared__ __align__(16) unsigned char k1f_lraw[sizeof(K1Launch)];  // the launch parameters
 __device__ __forceinline__ const K1Launch &k1f_L() { return *reinterpret_cast<const K1Launch *>(k1f_lraw); }
-__shared__ double k1f_pm[2 * K1_TQ];  // running max / suffix min of te (or te / ts), +inf padded
-__shared__ double k1f_sm[2 * K1_TQ];
+__shared__ double k1f_pm[K1_PMN];  // running max / suffix min of te (or te / ts), +inf padded
+__shared__ double k1f_sm[K1_PMN];
 __shared__ F32Item k1f_fi;            // the item's FP32 origin and error bound
 __shared__ ItemCtx k1f_it;            // the item
 __shared__ float k1f_cull_rb;         // the launch's box-cull radius base
 __shared__ int k1f_item_f32;          // the item takes the FP32 path
 
 // Item-level key bases of the K1 layout (hits add their own orig - f).
-__shared__ uint64_t k1_kb[4];  // per batch of the tile (pairs: 2, quads: 4)
-__shared__ int64_t k1_kf[4];
+__shared__ uint64_t k1_kb[K1_GMAX];  // per batch of the tile (pairs: 2, quads: 4, octets: 8)
+__shared__ int64_t k1_kf[K1_GMAX];
+__shared__ int k1_nbat;               // batches in the item's tile
 
 // One warp sub-tile on the box-cull fast path (K1 layout, overlaps counted
 // outside K1).  The window is every query whose extent meets the time range
@@ -685,7 +701,7 @@ __device__ __noinline__ void fast_subtile(int64_t wbase, int warp, int lane, uns
         tr.y = tr.y > t1.y ? tr.y : t1.y;
     }
     // window [jlo, jhi): te_j >= min ts (pm: te ascending) and ts_j <= max te
-    // (sm: ts ascending); both arrays are +inf padded to 2 * K1_TQ
+    // (sm: ts ascending); both arrays are +inf padded to K1_PMN
     int jlo, jhi;
     window_bounds(pm, sm, it.nt, tr.x, tr.y, lane, jlo, jhi);
     if (jhi < jlo) jhi = jlo;
@@ -696,14 +712,16 @@ __device__ __noinline__ void fast_subtile(int64_t wbase, int warp, int lane, uns
     K1_STAT(3, ns > 0);
     if (ns == 0) return;
     if (lane == 0) {
+        const int nbat = k1_nbat;
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-            k1_wctx[warp].key_base[g] = k1_kb[g];
-            k1_wctx[warp].f[g] = k1_kf[g];
-        }
+        for (int g = 0; g < K1_GMAX; ++g)
+            if (g < nbat) {
+                k1_wctx[warp].key_base[g] = k1_kb[g];
+                k1_wctx[warp].f[g] = k1_kf[g];
+            }
         k1_wctx[warp].js = it.js;
-        k1_wctx[warp].js2 = it.js2;
-        k1_wctx[warp].js3 = it.js3;
+#pragma unroll
+        for (int i = 0; i < K1_GMAX - 2; ++i) k1_wctx[warp].jx[i] = it.jx[i];
         k1_wctx[warp].wbase = wbase;
         const int64_t nv = it.c_hi - wbase + 1;
         k1_wctx[warp].nvalid = nv < 0 ? 0 : (nv > WCAND ? WCAND : (int)nv);
@@ -891,7 +909,7 @@ __device__ __noinline__ void slow_subtile(const K1Launch &L, const ItemCtx &it, 
         }
 }
 
-__global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Launch Lp) {
+__global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) K1F_NAME(k1_pairs_f32)(K1Launch Lp) {
     // the launch parameters in shared memory: the device functions take them
     // by reference, and a reference to the parameter space would make every
     // thread keep a copy on its stack (local memory)
@@ -913,7 +931,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
         fill_flush_cfg(L);
-        k1_hits23[0] = k1_hits23[1] = 0;
+        for (int i = 0; i < K1_GMAX - 2; ++i) k1_hitsx[i] = 0;
     }
     QF32 *const sqf = f_sqf();
     float *const wcs = f_cands(warp);
@@ -1018,10 +1036,11 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
             const double M2 = f32b[0] + f32b[1] + (f32b[4] + f32b[5] + f32b[7]) * f32b[2] + f32b[3] + f32b[6];
             k1_sep_rb = f32_sep_rbase(dthr, cmax, M2);
             if (L.orig) {  // K1 layout: key bases are per item and batch
-                const int nbat = it.b1 < 0 ? 1 : (it.js2 >= it.nt ? 2 : (it.js3 >= it.nt ? 3 : 4));
-                for (int g = 0; g < 4; ++g) {
-                    k1_kf[g] = g < nbat ? L.plan.first[it.b + g] : 0;
-                    k1_kb[g] = g < nbat ? make_key(L, it.b + g, 0, g == 0 ? it.q0 : 0) : 0;
+                const int nbat = item_batches(it);
+                k1_nbat = nbat;
+                for (int g = 0; g < nbat; ++g) {
+                    k1_kf[g] = L.plan.first[it.b + g];
+                    k1_kb[g] = make_key(L, it.b + g, 0, g == 0 ? it.q0 : 0);
                 }
             }
         }
@@ -1059,7 +1078,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) k1_pairs_f32(K1Lau
         }
         __syncthreads();
         if (single_scan) {
-            for (int j = tid; j < 2 * K1_TQ; j += K1_THREADS) {
+            for (int j = tid; j < K1_PMN; j += K1_THREADS) {
                 pm[j] = j < it.nt ? sqf[j].te64 : INFINITY;
                 sm[j] = j < it.nt ? sqf[j].ts64 : INFINITY;
             }
@@ -1107,22 +1126,24 @@ static void k1f_set_attrs() {
     cudaGetDevice(&dev);
     const uint64_t bit = 1ull << (dev & 63);
     if (!(done_mask.load() & bit)) {
-        TSK_CUDA(cudaFuncSetAttribute(k1_pairs_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k1f_dyn_smem()));
+        TSK_CUDA(cudaFuncSetAttribute(K1F_NAME(k1_pairs_f32), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k1f_dyn_smem()));
         done_mask.fetch_or(bit);
     }
 }
 
-int k1f_blocks_per_sm() {
+int K1F_NAME(k1f_blocks_per_sm)() {
     k1f_set_attrs();
     int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k1_pairs_f32, K1_THREADS, k1f_dyn_smem());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, K1F_NAME(k1_pairs_f32), K1_THREADS, k1f_dyn_smem());
     return n > 0 ? n : 1;
 }
 
-int k1f_candidates_per_thread() { return CPT; }
+int K1F_NAME(k1f_candidates_per_thread)() { return CPT; }
 
+K1F_NS_CLOSE
 }  // namespace tsk
 
+#ifndef K1_WIDE
 // Development counters of K1 (zeros unless built with -DTSK_K1_STATS).
 extern "C" int tsk_k1_stats(int device, unsigned long long *out, int n, int reset) {
     if (cudaSetDevice(device) != cudaSuccess) return 1;
@@ -1135,13 +1156,16 @@ extern "C" int tsk_k1_stats(int device, unsigned long long *out, int n, int rese
     }
     return 0;
 }
+#endif
 
 namespace tsk {
+K1F_NS_OPEN
 
-void launch_k1f(const K1Launch &L, int grid, cudaStream_t st) {
+void K1F_NAME(launch_k1f)(const K1Launch &L, int grid, cudaStream_t st) {
     k1f_set_attrs();
-    k1_pairs_f32<<<grid, K1_THREADS, k1f_dyn_smem(), st>>>(L);
+    K1F_NAME(k1_pairs_f32)<<<grid, K1_THREADS, k1f_dyn_smem(), st>>>(L);
     TSK_CUDA(cudaGetLastError());
 }
 
+K1F_NS_CLOSE
 }  // namespace tsk

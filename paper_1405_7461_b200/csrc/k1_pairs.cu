@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_MIN_BLOCKS) k1_pairs(K1Launch L
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
         fill_flush_cfg(L);
-        k1_hits23[0] = k1_hits23[1] = 0;
+        for (int i = 0; i < K1_GMAX - 2; ++i) k1_hitsx[i] = 0;
     }
     const int64_t total = L.plan.meta[0];
     const int sub = (int)L.plan.meta[1];
@@ -323,7 +323,8 @@ int k1_candidates_per_thread(bool f32) { return f32 ? k1f_candidates_per_thread(
 
 void launch_k1(const K1Launch &L, int grid, cudaStream_t st) {
     if (k1_use_f32(L.d2, L.db_cmax)) {
-        launch_k1f(L, grid, st);
+        if (L.wide) launch_k1f_wide(L, grid, st);
+        else launch_k1f(L, grid, st);
         return;
     }
     k1_set_attrs();

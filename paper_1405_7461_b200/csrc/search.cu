@@ -413,6 +413,11 @@ static void compact_rows(tsk_db *db, tsk_result *res, const tsk_columns *qc, int
 // is chunk order, engine.py:176-195).  On overflow of the buffer it returns
 // nullptr and the caller falls back to the exact-sizing path.
 static const int64_t kPipeMinRows = int64_t(1) << 20;
+// Plans of at least this many batches run K1 in its wide build (octets).
+// Measured K1 time, wide against 512-query tiles: c5 (3,334 batches) -6.5%,
+// its N = 2 / 4 shards (1,667 / 834) -4% / -1%, c4 (575) -6%; N = 8 shards
+// (417) +3%, c3 (334) +3%, c2 (334) +26%.
+static const int64_t kWideMinBatches = 512;
 static const int kPipeMinChunks = 4, kPipeMaxChunks = 16;
 
 // Counter snapshot straight into mapped host memory: a copy-engine read
@@ -890,7 +895,7 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     launch_ranges(db, db->q, plan, spans_given, st);
     const bool k1_f32 = k1_use_f32(d * d, db->cmax);
     const int bps = k1_blocks_per_sm(k1_f32);
-    const int slots = sm_count(db->device) * bps;
+    int slots = sm_count(db->device) * bps;
     // batch pairs share candidate tiles in the FP32 kernel (not in the
     // FP64 fallback kernel or for brute force's query-major keys)
     // TSK_K1_PAIR=off|force (testing) disables pairing or forces it on
@@ -908,8 +913,9 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
     const char *sp_env = getenv("TSK_SPATIAL");
     const bool use_k = !spans_given && db->k.built;
     const int cull = (use_k && !(sp_env && !strcmp(sp_env, "nocull"))) ? 1 : 0;
-    const int k1_stride = K1_THREADS * k1_candidates_per_thread(k1_f32), k1_align = cull ? BOX_GROUP : 1;
-    const int k1_tq_max = k1_f32 ? K1_TQ : K1P_TQ;
+    int k1_stride = K1_THREADS * k1_candidates_per_thread(k1_f32);
+    const int k1_align = cull ? BOX_GROUP : 1;
+    int k1_tq_max = k1_f32 ? K1_TQ : K1P_TQ;
     launches += spans_given ? 0 : 1;
 
     db->counters.reserve(64, st);
@@ -959,6 +965,20 @@ static tsk_result *run(tsk_db *db, const tsk_columns *qc, int64_t nb, const int6
         const char *qe = getenv("TSK_K1_QUADS");
         if (pair == 1 && L.cull && L.ext_count && k1_tq_max >= 512 && !(qe && !strcmp(qe, "off")))
             pair = (qe && !strcmp(qe, "force")) ? 5 : 4;  // force: quads on small plans too (testing)
+        // octets in the wide kernel (1,024-query tiles, one CTA per SM) for
+        // plans with enough groups of 8 to fill the grid; TSK_K1_WIDE=off|force
+        // (testing: force takes it on any plan quads would take)
+        const char *we = getenv("TSK_K1_WIDE");
+        bool wide = (pair == 4 || pair == 5) && nb >= kWideMinBatches;
+        if (we && !strcmp(we, "off")) wide = false;
+        if (we && !strcmp(we, "force") && (pair == 4 || pair == 5)) wide = true;
+        if (wide) {
+            L.wide = 1;
+            pair = pair == 5 ? 9 : 8;
+            slots = sm_count(db->device) * k1f_blocks_per_sm_wide();
+            k1_stride = K1W_THREADS * k1_candidates_per_thread(true);
+            k1_tq_max = K1W_TQ;
+        }
     }
     // reference-ordered results through the compact path: K1 chunk by chunk,
     // each chunk's rows sorted, gathered and copied while later chunks run

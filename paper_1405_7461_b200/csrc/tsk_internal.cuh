@@ -251,41 +251,60 @@ struct SearchPlanDev {
 //    beyond one tile, batches not adjacent in the query order, or sharing
 //    off) leaves unit 5k+0 empty and puts each batch's whole range in its
 //    left unit.
-//  * Quads: batches are taken in groups of four, whose candidate ranges
-//    [f_g, l_g] usually advance together (time-sorted queries): with f and
-//    l both non-decreasing, the batches holding a candidate c are the
-//    contiguous run [ga, gb] (gb: last g with f_g <= c, ga: first g with
-//    l_g >= c), so the group's range splits at the sorted boundaries
-//    {f_g, l_g + 1} into at most 7 segments, each evaluated once against its
-//    run's queries (one tile of up to 4 batches): a "staircase" that visits
-//    each candidate once per group.  A group that is not monotone, not
-//    adjacent in the query order or too large for a tile takes one unit per
-//    batch (its whole range).
-// Every (candidate, query) pair of the plan is in exactly one unit.
-constexpr int K1_SHARE_NONE = 0, K1_SHARE_PAIRS = 1, K1_SHARE_QUADS = 4;
+//  * Groups (quads, or octets in the 1,024-query kernel): batches are taken
+//    in groups of G = 4 or 8, whose candidate ranges [f_g, l_g] usually
+//    advance together (time-sorted queries): with f and l both
+//    non-decreasing, the batches holding a candidate c are the contiguous
+//    run [ga, gb] (gb: last g with f_g <= c, ga: first g with l_g >= c), so
+//    the group's range splits at the sorted boundaries {f_g, l_g + 1} into
+//    at most 2G - 1 segments, each evaluated once against its run's queries
+//    (one tile of up to G batches): a "staircase" that visits each
+//    candidate once per group.  A group that is not monotone, not adjacent
+//    in the query order or too large for a tile takes one unit per batch
+//    (its whole range).
+// Every (candidate, query) pair of the plan is in exactly one unit.  The
+// sharing mode is the group size: 0 none, 1 pairs, 4 quads, 8 octets.
+constexpr int K1_SHARE_NONE = 0, K1_SHARE_PAIRS = 1, K1_SHARE_QUADS = 4, K1_SHARE_OCTETS = 8;
+// most batches in one tile of this build's FP32 kernel (4; the wide build 8)
+#ifndef K1_GMAX_DEF
+#define K1_GMAX_DEF 4
+#endif
+constexpr int K1_GMAX = K1_GMAX_DEF;
+constexpr int K1_UNIT_GMAX = 8;  // the item planner handles every group size
 
-struct Unit {
+template <int GM>
+struct UnitT {
     int64_t b, b1;    // first batch, second batch of a multi-batch unit (else -1)
     int64_t lo_q, s;  // first query ordinal and query count (all the unit's batches)
     int64_t js;       // tile offset of the second batch's queries (s when single)
-    int64_t js2, js3; // ... of the third and fourth (s when absent)
+    int64_t jx[GM - 2];  // ... of the third to the last (s when absent)
     int64_t f, l;     // candidate segment (empty when f > l)
 };
 
+template <int GM>
+__host__ __device__ __forceinline__ void unit_offsets(UnitT<GM> &U, int64_t v) {
+    U.js = v;
+#pragma unroll
+    for (int i = 0; i < GM - 2; ++i) U.jx[i] = v;
+}
+
 __host__ __device__ __forceinline__ int64_t plan_units_mode(int64_t nb, int mode) {
-    return mode == K1_SHARE_QUADS ? 7 * ((nb + 3) / 4) : 5 * ((nb + 1) / 2);
+    return mode >= K1_SHARE_QUADS ? (2 * mode - 1) * ((nb + mode - 1) / mode) : 5 * ((nb + 1) / 2);
 }
 // the most any mode needs (buffer sizing)
 __host__ __device__ __forceinline__ int64_t plan_units(int64_t nb) {
-    const int64_t a = plan_units_mode(nb, K1_SHARE_PAIRS), b = plan_units_mode(nb, K1_SHARE_QUADS);
-    return a > b ? a : b;
+    const int64_t a = plan_units_mode(nb, K1_SHARE_PAIRS), b = plan_units_mode(nb, K1_SHARE_QUADS),
+                  c = plan_units_mode(nb, K1_SHARE_OCTETS);
+    return a > b ? (a > c ? a : c) : (b > c ? b : c);
 }
 
-__device__ __forceinline__ Unit plan_unit_quads(const SearchPlanDev &p, int64_t u, int64_t tqs) {
-    const int64_t k = u / 7, kind = u % 7;
-    const int64_t b0 = 4 * k;
-    const int gc = (int)(p.nb - b0 < 4 ? p.nb - b0 : 4);
-    int64_t f[4], l[4], sg[4];
+// (GM: the array bound, >= the group size G)
+template <int GM>
+__device__ __forceinline__ UnitT<GM> plan_unit_group(const SearchPlanDev &p, int64_t u, int64_t tqs, int G) {
+    const int64_t k = u / (2 * G - 1), kind = u % (2 * G - 1);
+    const int64_t b0 = G * k;
+    const int gc = (int)(p.nb - b0 < G ? p.nb - b0 : G);
+    int64_t f[GM], l[GM], sg[GM];
     bool mono = true;
     int64_t stot = 0;
     for (int g = 0; g < gc; ++g) {
@@ -298,7 +317,7 @@ __device__ __forceinline__ Unit plan_unit_quads(const SearchPlanDev &p, int64_t 
                (g == 0 || (f[g] >= f[g - 1] && l[g] >= l[g - 1] && p.lo[b] == p.hi[b - 1] + 1));
     }
     mono = mono && stot <= tqs;
-    Unit U;
+    UnitT<GM> U;
     U.b1 = -1;
     U.f = 1;
     U.l = 0;  // empty
@@ -306,7 +325,8 @@ __device__ __forceinline__ Unit plan_unit_quads(const SearchPlanDev &p, int64_t 
         const int g = kind < gc ? (int)kind : 0;
         U.b = b0 + g;
         U.lo_q = p.lo[U.b];
-        U.s = U.js = U.js2 = U.js3 = sg[g];
+        U.s = sg[g];
+        unit_offsets(U, sg[g]);
         if (kind < gc && f[g] >= 0) {
             U.f = f[g];
             U.l = l[g];
@@ -314,7 +334,7 @@ __device__ __forceinline__ Unit plan_unit_quads(const SearchPlanDev &p, int64_t 
         return U;
     }
     // sorted segment boundaries {f_g, l_g + 1}
-    int64_t bd[8];
+    int64_t bd[2 * GM];
     int nbd = 0;
     for (int g = 0; g < gc; ++g) {
         bd[nbd++] = f[g];
@@ -328,7 +348,8 @@ __device__ __forceinline__ Unit plan_unit_quads(const SearchPlanDev &p, int64_t 
         }
     U.b = b0;
     U.lo_q = p.lo[b0];
-    U.s = U.js = U.js2 = U.js3 = sg[0];
+    U.s = sg[0];
+    unit_offsets(U, sg[0]);
     if (kind + 1 >= nbd) return U;
     const int64_t c0 = bd[kind], c1 = bd[kind + 1] - 1;
     if (c0 > c1) return U;
@@ -342,20 +363,28 @@ __device__ __forceinline__ Unit plan_unit_quads(const SearchPlanDev &p, int64_t 
     U.lo_q = p.lo[U.b];
     U.s = 0;
     for (int g = ga; g <= gb; ++g) U.s += sg[g];
-    U.js = U.js2 = U.js3 = U.s;
+    unit_offsets(U, U.s);
     if (gb > ga) {
         U.b1 = U.b + 1;
-        U.js = sg[ga];
-        if (gb > ga + 1) U.js2 = sg[ga] + sg[ga + 1];
-        if (gb > ga + 2) U.js3 = sg[ga] + sg[ga + 1] + sg[ga + 2];
+        int64_t acc = sg[ga];
+        U.js = acc;
+#pragma unroll
+        for (int i = 0; i < GM - 2; ++i)  // (constant indices keep U in registers)
+            if (ga + 2 + i <= gb) {
+                acc += sg[ga + 1 + i];
+                U.jx[i] = acc;
+            }
     }
     U.f = c0;
     U.l = c1;
     return U;
 }
 
-__device__ __forceinline__ Unit plan_unit(const SearchPlanDev &p, int64_t u, int64_t tqs, int mode) {
-    if (mode == K1_SHARE_QUADS) return plan_unit_quads(p, u, tqs);
+// (FIXED: the group size is GM — a kernel build decodes only its own
+// groups; the item planner passes the mode's)
+template <int GM, bool FIXED = true>
+__device__ __forceinline__ UnitT<GM> plan_unit(const SearchPlanDev &p, int64_t u, int64_t tqs, int mode) {
+    if (mode >= K1_SHARE_QUADS) return plan_unit_group<GM>(p, u, tqs, FIXED ? GM : (mode < GM ? mode : GM));
     const int pair = mode != K1_SHARE_NONE;
     const int64_t k = u / 5, kind = u % 5;
     const int64_t b0 = 2 * k, b1 = 2 * k + 1;
@@ -368,7 +397,7 @@ __device__ __forceinline__ Unit plan_unit(const SearchPlanDev &p, int64_t u, int
     // hold arbitrary, even overlapping, query ranges)
     const bool shared = pair && has1 && f0 >= 0 && f1 >= 0 && s0 + s1 <= tqs && ilo <= ihi &&
                         p.lo[b1] == p.hi[b0] + 1;
-    Unit U;
+    UnitT<GM> U;
     U.b1 = -1;
     U.f = 1;
     U.l = 0;  // empty
@@ -376,8 +405,8 @@ __device__ __forceinline__ Unit plan_unit(const SearchPlanDev &p, int64_t u, int
         U.b = b0;
         U.lo_q = p.lo[b0];
         U.s = s0 + s1;
+        unit_offsets(U, U.s);
         U.js = s0;
-        U.js2 = U.js3 = U.s;
         if (shared) {
             U.b1 = b1;
             U.f = ilo;
@@ -389,14 +418,16 @@ __device__ __forceinline__ Unit plan_unit(const SearchPlanDev &p, int64_t u, int
     if (second && !has1) {
         U.b = b0;
         U.lo_q = p.lo[b0];
-        U.s = U.js = U.js2 = U.js3 = s0;
+        U.s = s0;
+        unit_offsets(U, s0);
         return U;
     }
     const int64_t b = second ? b1 : b0;
     const int64_t f = second ? f1 : f0, l = second ? l1 : l0;
     U.b = b;
     U.lo_q = p.lo[b];
-    U.s = U.js = U.js2 = U.js3 = second ? s1 : s0;
+    U.s = second ? s1 : s0;
+    unit_offsets(U, U.s);
     if (f < 0) return U;  // no candidates
     const bool left = kind == 1 || kind == 3;
     if (!shared) {
@@ -445,6 +476,7 @@ struct K1Launch {
     // when the query flags say ts and te are both sorted): K1's box-cull
     // fast path then skips whole warps and counts no overlaps itself
     int ext_count;
+    int wide = 0;  // launch the wide FP32 kernel (k1_f32_wide.cu: 1,024-query tiles, octets)
 };
 
 void launch_ranges(tsk_db *db, const Soa &q, SearchPlanDev &p, bool spans_given, cudaStream_t st);
@@ -471,6 +503,15 @@ int k1_blocks_per_sm(bool f32);
 int k1f_blocks_per_sm();
 int k1f_candidates_per_thread();
 void launch_k1f(const K1Launch &L, int grid, cudaStream_t st);
+// the wide build of the FP32 kernel (k1_f32_wide.cu)
+inline namespace wide {
+int k1f_blocks_per_sm_wide();
+void launch_k1f_wide(const K1Launch &L, int grid, cudaStream_t st);
+}
+#ifndef K1W_THREADS_DEF
+#define K1W_THREADS_DEF 512
+#endif
+constexpr int K1W_THREADS = K1W_THREADS_DEF, K1W_TQ = 1024;
 bool k1_use_f32(double d2, double db_cmax);
 int k1_candidates_per_thread(bool f32);
 

@@ -903,6 +903,49 @@ def test_batch_quads_staircase_match_the_oracle(kind, monkeypatch):
         assert gs.hits == rst["hits"]
 
 
+@pytest.mark.parametrize("kind", ["uniform", "normal", "exp"])
+def test_batch_octets_wide_kernel_match_the_oracle(kind, monkeypatch):
+    """Octets: the wide build of the FP32 kernel (k1_f32_wide.cu, 1,024-query
+    tiles) takes groups of eight batches, split into up to 15 staircase
+    segments, each evaluated against the run of batches holding it (keys,
+    hit counters and tile offsets for batches b .. b + 7).  Forced on small
+    plans (TSK_K1_WIDE=force with TSK_K1_QUADS=force), including batch sizes
+    whose groups exceed one tile (s = 140: 1,120 queries) and plans whose last
+    group is short, the result equals the unshared run and the oracle engine
+    bit for bit, per-batch counters included; the default (auto) choice on a
+    plan of this size keeps the 512-query kernel and gives the same result."""
+    from paper_1405_7461_b200 import datagen
+
+    store = datagen.generate(datagen.make_profile(kind, 700, seed=51, timesteps=120))
+    pool = datagen.generate(datagen.make_profile(kind, 90, seed=52, timesteps=120))
+    queries = datagen.sample_queries(pool, 27, seed=53)
+    index = tsk.build_index(store, 300)
+    oix = orc.index_build(_cols(store), 300)
+    for s in (13, 20, 61, 97, 128, 140):
+        plan = tsk.periodic(queries, s, index)
+        monkeypatch.setenv("TSK_K1_QUADS", "off")
+        monkeypatch.setenv("TSK_K1_PAIR", "off")
+        monkeypatch.setenv("TSK_K1_WIDE", "off")
+        want, ws = tsk.run_search(store, index, plan, 6.0)
+        monkeypatch.delenv("TSK_K1_PAIR")
+        monkeypatch.setenv("TSK_K1_QUADS", "force")
+        monkeypatch.setenv("TSK_K1_WIDE", "force")
+        got, gs = tsk.run_search(store, index, plan, 6.0)
+        monkeypatch.delenv("TSK_K1_QUADS")
+        monkeypatch.delenv("TSK_K1_WIDE")
+        auto, _ = tsk.run_search(store, index, plan, 6.0)
+        assert len(want) > 0
+        for k in RES:
+            assert np.array_equal(getattr(got, k), getattr(want, k)), (kind, s, k)
+            assert np.array_equal(getattr(auto, k), getattr(want, k)), (kind, s, k)
+        assert [(t.hits, t.interactions) for t in gs.per_batch] == [(t.hits, t.interactions) for t in ws.per_batch]
+        assert (gs.temporal_misses, gs.spatial_misses) == (ws.temporal_misses, ws.spatial_misses)
+        oplan = [(b.lo, b.hi, None, None, None, None) for b in plan.batches]
+        ref, rst = orc.search(_cols(store), oix, _cols(queries), oplan, 6.0, workers=4)
+        _same(got, ref)
+        assert gs.hits == rst["hits"]
+
+
 @pytest.mark.parametrize("nq,seed", [(37, 71), (75, 72), (131, 73), (255, 74)])
 def test_scan_range_ends_with_every_overlap_a_hit(nq, seed):
     """d so large that every temporally overlapping pair hits: a pair queued

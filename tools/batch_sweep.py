@@ -13,7 +13,7 @@ store = tsk.SegmentStore.from_columns(e, validate=False)
 queries = tsk.SegmentStore.from_columns(q, validate=False)
 del e, q
 ix = tsk.build_index(store, 10_000)
-for s in (30, 60, 120, 240, 480, 960):
+for s in [int(v) for v in (sys.argv[2].split(",") if len(sys.argv) > 2 else "30,60,120,240,480,960".split(","))]:
     plan = tsk.periodic(queries, s, ix)
     ints = sum(b.interactions for b in plan.batches)
     r = search_device(store, ix, plan, cfg["d"])
