@@ -570,14 +570,26 @@ static tsk_result *run_pipelined(tsk_db *db, const tsk_columns *qc, const Search
         pin_free(snap, sgot);
         pin_free(h_qo, qgot);
     };
+    // a chunk below the wide kernel's plan size runs the 512-query kernel
+    // (quads) even when the whole plan chose the wide one
+    const char *we = getenv("TSK_K1_WIDE");
+    const bool force_wide = we && !strcmp(we, "force");
     auto enqueue_k1 = [&](int c) {
-        launch_plan_items(pc[c], slots, stride, pair, align, tq_max, L.q_unsorted, st);
-        ++launches;
-        TSK_CUDA(cudaMemsetAsync(d_ctr, 0, 8, st));  // the item counter
         K1Launch Lc = L;
         Lc.plan = pc[c];
+        int c_slots = slots, c_stride = stride, c_pair = pair, c_tq = tq_max;
+        if (L.wide && !force_wide && pc[c].nb < kWideMinBatches) {
+            Lc.wide = 0;
+            c_slots = sm_count(db->device) * k1_blocks_per_sm(true);
+            c_stride = K1_THREADS * k1_candidates_per_thread(true);
+            c_pair = pair == 9 ? 5 : 4;
+            c_tq = K1_TQ;
+        }
+        launch_plan_items(pc[c], c_slots, c_stride, c_pair, align, c_tq, L.q_unsorted, st);
+        ++launches;
+        TSK_CUDA(cudaMemsetAsync(d_ctr, 0, 8, st));  // the item counter
         TSK_CUDA(cudaEventRecord(ek0[c], st));
-        launch_k1(Lc, slots, st);
+        launch_k1(Lc, c_slots, st);
         ++launches;
         TSK_CUDA(cudaEventRecord(ek1[c], st));
         k_snap<<<1, 1, 0, st>>>(d_ctr, snap_dev + 2 * c);
