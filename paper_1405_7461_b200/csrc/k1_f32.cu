@@ -6,8 +6,9 @@
 // driven by engine.execute_batch/_run_chunks (engine.py:78-148) for every
 // batch of a plan at once.
 //
-// Work decomposition.  A work item is (work unit: one batch or an adjacent
-// pair sharing candidates, candidate tile, query tile),
+// Work decomposition.  A work item is (work unit: one batch, an adjacent
+// pair sharing candidates, or a staircase segment of a group of 4 or 8
+// batches (tsk_internal.cuh), candidate tile, query tile),
 // claimed from a global counter by a persistent grid.  The query tile is
 // staged in shared memory as 48-byte FP32 pre-filter records (filter.cuh)
 // with the exact start/end times; each lane holds K1F_CPT = 4 candidates
@@ -33,9 +34,9 @@
 #include "k1_exact.cuh"
 
 // The library builds this file twice: as is (512-query tiles, 8-warp CTAs,
-// two per SM) and from k1_f32_wide.cu (K1_WIDE: 1,024-query tiles, 14-warp
+// two per SM) and from k1_f32_wide.cu (K1_WIDE: 1,024-query tiles, 16-warp
 // CTAs, one per SM, octets of batches); the wide build's host-visible names
-// carry a suffix.
+// carry a suffix and its device code lives in tsk::wide.
 #ifdef K1_WIDE
 #define K1F_NAME(x) x##_wide
 #define K1F_NS_OPEN inline namespace wide {
