@@ -52,6 +52,10 @@ CONFIGS = {
                     "(40,000 query segments), d=5, Periodic s=120, m=10,000",
                entries=("normal", 25000, 5, 401), pool=("normal", 1000, 6, 401), sample=(100, 7),
                d=5.0),
+    "c3n5": dict(desc="RandWalk-Normal5 25,000x401 (1e7 entries), 100 query trajectories "
+                      "(40,000 query segments), d=5, Periodic s=120, m=10,000 (config 3's Normal5 variant)",
+                 entries=("normal5", 25000, 5, 401), pool=("normal5", 1000, 6, 401), sample=(100, 7),
+                 d=5.0),
     "c4": dict(desc="RandWalk-Exp 140,000 trajectories (~1e7 entries), 1,000 query trajectories, "
                     "d=5, Periodic s=120, m=10,000",
                entries=("exp", 140000, 8, None), pool=("exp", 14000, 9, None), sample=(1000, 10),

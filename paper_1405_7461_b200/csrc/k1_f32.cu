@@ -1145,18 +1145,34 @@ K1F_NS_CLOSE
 }  // namespace tsk
 
 #ifndef K1_WIDE
-// Development counters of K1 (zeros unless built with -DTSK_K1_STATS).
+// Development counters of K1 (zeros unless built with -DTSK_K1_STATS):
+// both builds' counters, summed.
 extern "C" int tsk_k1_stats(int device, unsigned long long *out, int n, int reset) {
     if (cudaSetDevice(device) != cudaSuccess) return 1;
-    unsigned long long v[8] = {0};
+    unsigned long long v[8] = {0}, w[8] = {0};
     if (cudaMemcpyFromSymbol(v, tsk::k1_stats, sizeof(v)) != cudaSuccess) return 1;
-    for (int i = 0; i < n && i < 8; ++i) out[i] = v[i];
+    if (tsk::k1f_stats_wide(w, reset) != 0) return 1;
+    for (int i = 0; i < n && i < 8; ++i) out[i] = v[i] + w[i];
     if (reset) {
         const unsigned long long z[8] = {0};
         if (cudaMemcpyToSymbol(tsk::k1_stats, z, sizeof(z)) != cudaSuccess) return 1;
     }
     return 0;
 }
+#else
+namespace tsk {
+inline namespace wide {
+// the wide build's development counters (read, optionally reset)
+int k1f_stats_wide(unsigned long long *v, int reset) {
+    if (cudaMemcpyFromSymbol(v, k1_stats_wide, 8 * sizeof(unsigned long long)) != cudaSuccess) return 1;
+    if (reset) {
+        const unsigned long long z[8] = {0};
+        if (cudaMemcpyToSymbol(k1_stats_wide, z, sizeof(z)) != cudaSuccess) return 1;
+    }
+    return 0;
+}
+}  // namespace wide
+}  // namespace tsk
 #endif
 
 namespace tsk {

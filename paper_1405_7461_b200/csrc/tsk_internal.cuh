@@ -505,6 +505,7 @@ int k1f_candidates_per_thread();
 void launch_k1f(const K1Launch &L, int grid, cudaStream_t st);
 // the wide build of the FP32 kernel (k1_f32_wide.cu)
 inline namespace wide {
+int k1f_stats_wide(unsigned long long *v, int reset);
 int k1f_blocks_per_sm_wide();
 void launch_k1f_wide(const K1Launch &L, int grid, cudaStream_t st);
 }
