@@ -922,6 +922,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) K1F_NAME(k1_pairs_
     double *const pm = k1f_pm;
     double *const sm = k1f_sm;
     __shared__ double f32b[8];    // per-item magnitude bounds
+    __shared__ double f32p[K1_WARPS][4];  // per-warp partial maxima of the bounds pass
     F32Item &fi_sh = k1f_fi;      // the item's FP32 origin and error bound
     ItemCtx &it_sh = k1f_it;
     __shared__ int64_t item_sh;
@@ -977,9 +978,13 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) K1F_NAME(k1_pairs_
             }
             if (fl) atomicOr(&flags_sh, fl);
             const double ox = qt[0].sx, oy = qt[0].sy, oz = qt[0].sz, t0 = qt[0].ts;
-            if (warp == 2) {
+            // warps 2 .. 2 + KW - 1 bound the candidate groups, the warps above
+            // them the queries; thread 0 folds the per-warp maxima (fmax is
+            // exact and order-free) after the barrier
+            constexpr int KW = (K1_WARPS - 2) / 2;
+            if (warp >= 2 && warp < 2 + KW) {
                 double ar = 0.0, tvr = 0.0, vr = 0.0, trr = 0.0;
-                for (int64_t g = it.first_c / GB_SIZE + lane; g <= it.c_hi / GB_SIZE; g += 32) {
+                for (int64_t g = it.first_c / GB_SIZE + (warp - 2) * 32 + lane; g <= it.c_hi / GB_SIZE; g += 32 * KW) {
                     const GBound gb = L.e.gb[g];
                     ar = fmax(ar, fmax(fmax(fabs(gb.hi[0] - ox), fabs(ox - gb.lo[0])),
                                        fmax(fmax(fabs(gb.hi[1] - oy), fabs(oy - gb.lo[1])),
@@ -994,14 +999,15 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) K1F_NAME(k1_pairs_
                 vr = warp_max(vr);
                 trr = warp_max(trr);
                 if (lane == 0) {
-                    f32b[0] = ar;
-                    f32b[1] = tvr;
-                    f32b[2] = vr;
-                    f32b[7] = trr;
+                    f32p[warp][0] = ar;
+                    f32p[warp][1] = tvr;
+                    f32p[warp][2] = vr;
+                    f32p[warp][3] = trr;
                 }
-            } else if (warp == 3) {
+            } else if (warp >= 2 + KW) {
+                constexpr int QW = K1_WARPS - 2 - KW;
                 double aq = 0.0, tq = 0.0, eq = 0.0, dq = 0.0;
-                for (int j = lane; j < it.nt; j += 32) {
+                for (int j = (warp - 2 - KW) * 32 + lane; j < it.nt; j += 32 * QW) {
                     const QRec &q = qt[j];
                     aq = fmax(aq, fmax(fabs(q.sx - ox), fmax(fabs(q.sy - oy), fabs(q.sz - oz))));
                     tq = fmax(tq, fabs(q.ts - t0));
@@ -1013,10 +1019,10 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) K1F_NAME(k1_pairs_
                 eq = warp_max(eq);
                 dq = warp_max(dq);
                 if (lane == 0) {
-                    f32b[3] = aq;
-                    f32b[4] = tq;
-                    f32b[5] = eq;
-                    f32b[6] = dq;
+                    f32p[warp][0] = aq;
+                    f32p[warp][1] = tq;
+                    f32p[warp][2] = eq;
+                    f32p[warp][3] = dq;
                 }
             }
         }
@@ -1030,6 +1036,23 @@ __global__ void __launch_bounds__(K1_THREADS, K1F_MIN_BLOCKS) K1F_NAME(k1_pairs_
         // box costs two bisections and the box tests, nothing per candidate
         const bool fast = cull && L.ext_count && (*L.q_unsorted & 3) == 0 && single_scan;
         if (tid == 0) {
+            {  // fold the bounds pass's per-warp maxima
+                constexpr int KW = (K1_WARPS - 2) / 2;
+                double m[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+                for (int w = 2; w < K1_WARPS; ++w)
+                    for (int k = 0; k < 4; ++k) {
+                        const int o = w < 2 + KW ? k : 4 + k;
+                        m[o] = fmax(m[o], f32p[w][k]);
+                    }
+                f32b[0] = m[0];  // ar
+                f32b[1] = m[1];  // tvr
+                f32b[2] = m[2];  // vr
+                f32b[7] = m[3];  // trr
+                f32b[3] = m[4];  // aq
+                f32b[4] = m[5];  // tq
+                f32b[5] = m[6];  // eq
+                f32b[6] = m[7];  // dq
+            }
             fi_sh = f32_item(qt[0].sx, qt[0].sy, qt[0].sz, qt[0].ts, f32b[0], f32b[1], f32b[2], f32b[3], f32b[4],
                              f32b[5], cmax, f32b[7]);
             fi_sh.ok = fi_sh.ok && launch_ok && !unsafe_q;
