@@ -150,6 +150,14 @@ int tsk_plan_greedy(int64_t nq, const double *ts, const double *te, int64_t n_ne
                     const int64_t *ne_last, int variant, int64_t bound, int64_t *nb_out,
                     int64_t *b_lo, int64_t *b_hi, int64_t *b_first, int64_t *b_last, double *b_end);
 
+/* Work units of a plan (host code; the decomposition K1 runs, tsk_internal.cuh):
+ * mode 0 none, 1 pairs, 4 quads, 8 octets (staircase groups), tqs the query
+ * tile.  Writes 13 int64 per unit (b, b1, lo_q, s, js, jx[6], f, l) and
+ * returns the unit count (-1 if it exceeds cap).  No reference counterpart:
+ * a test hook for the partition property of the sharing layouts. */
+int64_t tsk_plan_units(int64_t nb, const int64_t *lo, const int64_t *hi, const int64_t *first,
+                       const int64_t *last, int mode, int64_t tqs, int64_t *out, int64_t cap);
+
 /* Canonical order (core.py:290-294: query ids, entry ids, t_begin, t_end) of
  * n result rows, computed on `device`; outputs may alias nothing. */
 int tsk_canonical_order(int device, int64_t n, const int64_t *qt, const int64_t *qs, const int64_t *et,

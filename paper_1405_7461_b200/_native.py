@@ -79,6 +79,7 @@ SIGNATURES = {
                            _I64, _PI64, _PI64, _PI64, _PI64, _PI64, _PD], ctypes.c_int),
     "tsk_plan_greedy": ([_I64, _PD, _PD, _I64, _PD, _PD, _PI64, _PI64, ctypes.c_int, _I64, _PI64,
                          _PI64, _PI64, _PI64, _PI64, _PD], ctypes.c_int),
+    "tsk_plan_units": ([_I64, _PI64, _PI64, _PI64, _PI64, ctypes.c_int, _I64, _PI64, _I64], _I64),
     "tsk_canonical_order": ([ctypes.c_int, _I64] + [_PI64] * 4 + [_PD] * 2 + [_PI64] * 4 + [_PD] * 2,
                             ctypes.c_int),
     "tsk_format_double": ([ctypes.c_double, ctypes.c_char_p, ctypes.c_int], ctypes.c_int),

@@ -660,6 +660,37 @@ void launch_plan_items(SearchPlanDev &p, int slots, int stride, int pair, int al
 
 // ── C-ABI: db / sort / index / ranges ──────────────────────────────────────
 
+// The work units of a plan in a sharing mode (host code: the same
+// plan_unit the item planner and K1 decode run on the device; tests check
+// that every (batch, candidate) pair lies in exactly one unit).  Per unit 13
+// int64: b, b1, lo_q, s, js, jx[0..5], f, l.  Returns the unit count, or -1
+// when `cap` units do not fit.
+extern "C" int64_t tsk_plan_units(int64_t nb, const int64_t *lo, const int64_t *hi, const int64_t *first,
+                                  const int64_t *last, int mode, int64_t tqs, int64_t *out, int64_t cap) {
+    using namespace tsk;
+    const int64_t nu = plan_units_mode(nb, mode);
+    if (nb < 1 || !out || nu > cap) return -1;
+    SearchPlanDev p{};
+    p.nb = nb;
+    p.lo = lo;
+    p.hi = hi;
+    p.first = const_cast<int64_t *>(first);
+    p.last = const_cast<int64_t *>(last);
+    for (int64_t u = 0; u < nu; ++u) {
+        const UnitT<K1_UNIT_GMAX> U = plan_unit<K1_UNIT_GMAX, false>(p, u, tqs, mode);
+        int64_t *o = out + 13 * u;
+        o[0] = U.b;
+        o[1] = U.b1;
+        o[2] = U.lo_q;
+        o[3] = U.s;
+        o[4] = U.js;
+        for (int i = 0; i < K1_UNIT_GMAX - 2; ++i) o[5 + i] = U.jx[i];
+        o[11] = U.f;
+        o[12] = U.l;
+    }
+    return nu;
+}
+
 extern "C" int tsk_db_create(int device, const tsk_columns *cols, tsk_db **out) {
     tsk_db *db = nullptr;
     try {

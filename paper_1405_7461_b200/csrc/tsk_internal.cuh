@@ -300,7 +300,7 @@ __host__ __device__ __forceinline__ int64_t plan_units(int64_t nb) {
 
 // (GM: the array bound, >= the group size G)
 template <int GM>
-__device__ __forceinline__ UnitT<GM> plan_unit_group(const SearchPlanDev &p, int64_t u, int64_t tqs, int G) {
+__host__ __device__ __forceinline__ UnitT<GM> plan_unit_group(const SearchPlanDev &p, int64_t u, int64_t tqs, int G) {
     const int64_t k = u / (2 * G - 1), kind = u % (2 * G - 1);
     const int64_t b0 = G * k;
     const int gc = (int)(p.nb - b0 < G ? p.nb - b0 : G);
@@ -383,7 +383,7 @@ __device__ __forceinline__ UnitT<GM> plan_unit_group(const SearchPlanDev &p, int
 // (FIXED: the group size is GM — a kernel build decodes only its own
 // groups; the item planner passes the mode's)
 template <int GM, bool FIXED = true>
-__device__ __forceinline__ UnitT<GM> plan_unit(const SearchPlanDev &p, int64_t u, int64_t tqs, int mode) {
+__host__ __device__ __forceinline__ UnitT<GM> plan_unit(const SearchPlanDev &p, int64_t u, int64_t tqs, int mode) {
     if (mode >= K1_SHARE_QUADS) return plan_unit_group<GM>(p, u, tqs, FIXED ? GM : (mode < GM ? mode : GM));
     const int pair = mode != K1_SHARE_NONE;
     const int64_t k = u / 5, kind = u % 5;

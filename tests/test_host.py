@@ -396,3 +396,62 @@ def test_per_batch_behaves_as_a_list():
     import pickle
 
     assert pickle.loads(pickle.dumps(mk())) == want
+
+
+@pytest.mark.parametrize("mode", [0, 1, 4, 8])
+def test_plan_units_partition_every_batch_candidate_pair(mode):
+    """The work units K1 runs (pairs, staircase quads and octets,
+    tsk_internal.cuh) partition the plan: every (batch, candidate) pair of
+    every batch's span lies in exactly one unit, a unit's batches are
+    consecutive and adjacent in the query order, and its tile offsets are
+    the running sums of their sizes.  Random plans with monotone and
+    non-monotone spans, empty spans and groups larger than a tile."""
+    rng = np.random.default_rng(100 + mode)
+    lib = _native.load()
+    widest = 0  # most batches in one unit (the staircase must be exercised)
+    for trial in range(60):
+        nb = int(rng.integers(1, 70))
+        sizes = rng.integers(1, 200, nb)
+        hi = np.cumsum(sizes) - 1
+        lo = hi - sizes + 1
+        f = np.cumsum(rng.integers(0, 50, nb))
+        if trial % 3 == 0:  # break monotonicity
+            f = rng.permutation(f)
+        last = f + rng.integers(0, 400, nb)
+        if trial % 3 != 0:  # both ends non-decreasing: groups form staircases
+            last = np.maximum.accumulate(last)
+        empty = rng.random(nb) < (0.1 if trial % 2 else 0.0)
+        first = np.where(empty, -1, f).astype(np.int64)
+        last = np.where(empty, -1, last).astype(np.int64)
+        tqs = int(rng.choice([256, 512, 1024]))
+        cap = 16 * nb + 16
+        out = np.zeros(13 * cap, np.int64)
+        arr = [np.ascontiguousarray(a, dtype=np.int64) for a in (lo, hi, first, last)]
+        nu = lib.tsk_plan_units(nb, *[a.ctypes.data_as(_native._PI64) for a in arr], mode, tqs,
+                                out.ctypes.data_as(_native._PI64), cap)
+        assert nu > 0
+        cover = [[] for _ in range(nb)]
+        for u in out[:13 * nu].reshape(nu, 13):
+            b, b1, lo_q, s, js, jx, uf, ul = u[0], u[1], u[2], u[3], u[4], u[5:11], u[11], u[12]
+            if uf > ul:
+                continue  # an empty unit holds no work items
+            k = 1 if b1 < 0 else 2 + int((jx < s).sum())
+            widest = max(widest, k)
+            assert b1 < 0 or b1 == b + 1
+            assert lo_q == lo[b] and s == sizes[b:b + k].sum()
+            offs = np.concatenate([[0], np.cumsum(sizes[b:b + k])[:-1]])
+            if k > 1:
+                assert js == offs[1] and list(jx[:k - 2]) == list(offs[2:k])
+                assert all(lo[g + 1] == hi[g] + 1 for g in range(b, b + k - 1))
+            for g in range(b, b + k):
+                cover[g].append((int(uf), int(ul)))
+        for g in range(nb):
+            iv = sorted(cover[g])
+            if first[g] < 0:
+                assert iv == [], (g, iv)
+                continue
+            assert iv, g
+            assert iv[0][0] == first[g] and iv[-1][1] == last[g], (g, iv, first[g], last[g])
+            for (a0, a1), (b0, b1_) in zip(iv, iv[1:]):
+                assert b0 == a1 + 1, (g, iv)  # contiguous, no overlap
+    assert widest == {0: 1, 1: 2, 4: 4, 8: 8}[mode], widest
